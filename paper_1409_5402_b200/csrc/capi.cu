@@ -1,0 +1,986 @@
+// capi.cu -- libsamelda_cuda.so: device context and the C ABI of include/samelda_cu.h.
+//
+// Host-side logic here mirrors the reference's host code exactly where it
+// feeds the hot path (MinibatchStream corpus.cpp:252-285, anneal_m /
+// rho_schedule sampler.cpp:231-267, the train() period loop and its trace
+// bookkeeping sampler.cpp:269-353); every arithmetic step of the hot path
+// itself runs in the kernels of kernels.cu.  There is no CPU fallback: a
+// missing device is an error.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <chrono>
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "../../include/samelda_cu.h"
+#include "kernels.cuh"
+#include "philox.cuh"
+
+namespace {
+
+constexpr int kVersion = 1;
+
+struct DevBuf {
+  void* p = nullptr;
+  size_t bytes = 0;
+  ~DevBuf() {
+    if (p) cudaFree(p);
+  }
+  template <class T>
+  T* as() const {
+    return static_cast<T*>(p);
+  }
+};
+
+struct Fail {
+  int code;
+  std::string msg;
+};
+
+[[noreturn]] void fail(int code, const char* fmt, ...) {
+  char buf[512];
+  va_list ap;
+  va_start(ap, fmt);
+  std::vsnprintf(buf, sizeof(buf), fmt, ap);
+  va_end(ap);
+  throw Fail{code, buf};
+}
+
+void ck(cudaError_t e, const char* what) {
+  if (e != cudaSuccess) fail(SAMELDA_CU_CUDA, "%s: %s", what, cudaGetErrorString(e));
+}
+
+template <class T>
+T* ensure(DevBuf& b, int64_t n) {
+  const size_t need = static_cast<size_t>(std::max<int64_t>(n, 1)) * sizeof(T);
+  if (b.bytes < need) {
+    if (b.p) ck(cudaFree(b.p), "cudaFree");
+    b.p = nullptr;
+    b.bytes = 0;
+    ck(cudaMalloc(&b.p, need), "cudaMalloc");
+    b.bytes = need;
+  }
+  return static_cast<T*>(b.p);
+}
+
+// Resident CSR corpus with a cheap identity check: the per-call API receives
+// an arbitrary corpus every call (sampler.hpp:74-91), so the slot re-uploads
+// only when pointers, sizes or a content fingerprint change.
+struct CorpusSlot {
+  bool valid = false;
+  uint64_t fp = 0;
+  int64_t n_docs = 0, n_words = 0, nnz = 0, n_tokens = 0;
+  std::vector<int64_t> offsets;     // host copy (batch prefixes)
+  std::vector<int64_t> doc_tokens;  // Corpus::doc_tokens (corpus.cpp:16-23)
+  DevBuf offs, words, counts;
+};
+
+uint64_t fnv(uint64_t h, const void* data, size_t bytes) {
+  const unsigned char* p = static_cast<const unsigned char*>(data);
+  for (size_t i = 0; i < bytes; ++i) {
+    h ^= p[i];
+    h *= 1099511628211ull;
+  }
+  return h;
+}
+
+uint64_t fingerprint(const samelda_cu_corpus* c) {
+  uint64_t h = 1469598103934665603ull;
+  const int64_t nnz = c->doc_offsets[c->n_docs];
+  const uintptr_t ptrs[3] = {reinterpret_cast<uintptr_t>(c->doc_offsets),
+                             reinterpret_cast<uintptr_t>(c->word_ids),
+                             reinterpret_cast<uintptr_t>(c->counts)};
+  h = fnv(h, ptrs, sizeof(ptrs));
+  const int64_t dims[3] = {c->n_docs, c->n_words, nnz};
+  h = fnv(h, dims, sizeof(dims));
+  if (nnz <= (int64_t{1} << 20)) {
+    h = fnv(h, c->doc_offsets, sizeof(int64_t) * (c->n_docs + 1));
+    h = fnv(h, c->word_ids, sizeof(int32_t) * nnz);
+    h = fnv(h, c->counts, sizeof(int32_t) * nnz);
+  } else {
+    const int64_t step = nnz / 65536;
+    for (int64_t i = 0; i < nnz; i += step) {
+      h = fnv(h, c->word_ids + i, 4);
+      h = fnv(h, c->counts + i, 4);
+    }
+    const int64_t dstep = std::max<int64_t>(1, c->n_docs / 65536);
+    for (int64_t d = 0; d <= c->n_docs; d += dstep) h = fnv(h, c->doc_offsets + d, 8);
+  }
+  return h;
+}
+
+void validate_corpus(const samelda_cu_corpus* c) {
+  if (c == nullptr || c->doc_offsets == nullptr) fail(SAMELDA_CU_CONFIG, "corpus is null");
+  if (c->n_docs < 0 || c->n_words < 0) fail(SAMELDA_CU_CONFIG, "corpus dimensions negative");
+  if (c->doc_offsets[0] != 0) fail(SAMELDA_CU_CONFIG, "corpus doc_offsets[0] != 0");
+}
+
+void upload_corpus(CorpusSlot& s, const samelda_cu_corpus* c, cudaStream_t st) {
+  validate_corpus(c);
+  const uint64_t fp = fingerprint(c);
+  const int64_t nnz = c->doc_offsets[c->n_docs];
+  if (s.valid && s.fp == fp && s.n_docs == c->n_docs && s.nnz == nnz &&
+      s.n_words == c->n_words)
+    return;
+  s.valid = false;
+  s.n_docs = c->n_docs;
+  s.n_words = c->n_words;
+  s.nnz = nnz;
+  s.offsets.assign(c->doc_offsets, c->doc_offsets + c->n_docs + 1);
+  s.doc_tokens.assign(static_cast<size_t>(c->n_docs), 0);
+  s.n_tokens = 0;
+  for (int64_t d = 0; d < c->n_docs; ++d) {
+    int64_t tok = 0;
+    for (int64_t i = c->doc_offsets[d]; i < c->doc_offsets[d + 1]; ++i) tok += c->counts[i];
+    s.doc_tokens[static_cast<size_t>(d)] = tok;
+    s.n_tokens += tok;
+  }
+  ck(cudaMemcpyAsync(ensure<int64_t>(s.offs, c->n_docs + 1), c->doc_offsets,
+                     sizeof(int64_t) * (c->n_docs + 1), cudaMemcpyHostToDevice, st),
+     "upload offsets");
+  if (nnz > 0) {
+    ck(cudaMemcpyAsync(ensure<int32_t>(s.words, nnz), c->word_ids, sizeof(int32_t) * nnz,
+                       cudaMemcpyHostToDevice, st),
+       "upload word ids");
+    ck(cudaMemcpyAsync(ensure<int32_t>(s.counts, nnz), c->counts, sizeof(int32_t) * nnz,
+                       cudaMemcpyHostToDevice, st),
+       "upload counts");
+  } else {
+    ensure<int32_t>(s.words, 1);
+    ensure<int32_t>(s.counts, 1);
+  }
+  ck(cudaStreamSynchronize(st), "corpus upload");
+  s.fp = fp;
+  s.valid = true;
+}
+
+// Host MinibatchStream (corpus.cpp:252-285) on the same Philox streams.
+struct Batches {
+  int64_t n_docs = 0;
+  uint64_t seed = 0;
+  int64_t batch_size = 1;
+  uint32_t pass = 0;
+  int64_t cursor = 0;
+  std::vector<int32_t> order;
+
+  void start_pass() {
+    scu::Stream s;
+    s.init(seed, pass, 0, 0, scu::make_tag(scu::kBatchShuffle, 0, 0));
+    order.resize(static_cast<size_t>(n_docs));
+    for (int64_t i = 0; i < n_docs; ++i) order[static_cast<size_t>(i)] = static_cast<int32_t>(i);
+    for (int64_t i = n_docs - 1; i > 0; --i) {
+      const int64_t j = static_cast<int64_t>(s.uniform_below(static_cast<uint64_t>(i) + 1));
+      std::swap(order[static_cast<size_t>(i)], order[static_cast<size_t>(j)]);
+    }
+    cursor = 0;
+  }
+  int64_t next(int32_t* out) {
+    if (cursor >= n_docs) {
+      ++pass;
+      start_pass();
+    }
+    const int64_t take = std::min<int64_t>(batch_size, n_docs - cursor);
+    std::memcpy(out, order.data() + cursor, sizeof(int32_t) * static_cast<size_t>(take));
+    cursor += take;
+    return take;
+  }
+  int64_t per_pass() const { return (n_docs + batch_size - 1) / batch_size; }
+};
+
+void validate_config(const samelda_cu_config* c) {
+  // sampler.cpp:47-78
+  if (c == nullptr) fail(SAMELDA_CU_CONFIG, "config is null");
+  if (c->n_topics < 1 || c->n_topics >= (1 << 20)) fail(SAMELDA_CU_CONFIG, "n_topics must be in [1, 2^20)");
+  if (!(c->m > 0.0) || !std::isfinite(c->m)) fail(SAMELDA_CU_CONFIG, "m must be positive and finite");
+  if (!(c->tau0 >= 1.0)) fail(SAMELDA_CU_CONFIG, "tau0 must be >= 1");
+  if (!(c->gamma >= 0.5 && c->gamma <= 1.0)) fail(SAMELDA_CU_CONFIG, "gamma must be in [0.5, 1]");
+  if (!(c->batch_fraction > 0.0 && c->batch_fraction <= 1.0))
+    fail(SAMELDA_CU_CONFIG, "batch_fraction must be in (0, 1]");
+  if (c->t_max < 0) fail(SAMELDA_CU_CONFIG, "t_max must be >= 0");
+  if (c->inner_sweeps < 1 || c->inner_sweeps > 255) fail(SAMELDA_CU_CONFIG, "inner_sweeps must be in [1, 255]");
+  if (!(c->alpha > 0.0) || !(c->beta > 0.0)) fail(SAMELDA_CU_CONFIG, "alpha and beta must be positive");
+  if (!(c->init_noise >= 0.0) || !std::isfinite(c->init_noise))
+    fail(SAMELDA_CU_CONFIG, "init_noise must be finite and >= 0");
+  if (c->mode != SAMELDA_CU_MODE_PARITY && c->mode != SAMELDA_CU_MODE_EXPECTED)
+    fail(SAMELDA_CU_CONFIG, "unknown sampling mode %d", c->mode);
+  if (c->schedule < 0 || c->schedule > 3) fail(SAMELDA_CU_CONFIG, "unknown schedule %d", c->schedule);
+}
+
+double rho_schedule_host(int64_t t, double tau0, double gamma) {
+  // sampler.cpp:231-242
+  if (t < 0) fail(SAMELDA_CU_CONFIG, "rho_schedule: t must be >= 0");
+  if (!(tau0 >= 1.0)) fail(SAMELDA_CU_CONFIG, "rho_schedule: tau0 must be >= 1");
+  if (!(gamma >= 0.5 && gamma <= 1.0)) fail(SAMELDA_CU_CONFIG, "rho_schedule: gamma must be in [0.5, 1]");
+  return std::pow(tau0 + static_cast<double>(t), -gamma);
+}
+
+double anneal_m_host(int schedule, int64_t t, int64_t t_max, double m) {
+  // sampler.cpp:244-267
+  if (t < 1 || t > t_max) fail(SAMELDA_CU_CONFIG, "anneal_m: t must be in [1, t_max]");
+  const double td = static_cast<double>(t);
+  const double nd = static_cast<double>(t_max);
+  switch (schedule) {
+    case SAMELDA_CU_SCHEDULE_CONSTANT: return m;
+    case SAMELDA_CU_SCHEDULE_LINEAR: return 2.0 * m * td / (nd + 1.0);
+    case SAMELDA_CU_SCHEDULE_INVLINEAR: return 2.0 * m * (nd + 1.0 - td) / (nd + 1.0);
+    case SAMELDA_CU_SCHEDULE_LOG: {
+      if (t_max == 1) return m;
+      const double value = m * nd * std::log(td) / std::lgamma(nd + 1.0);
+      return std::max(value, 0.01);
+    }
+    default: fail(SAMELDA_CU_CONFIG, "anneal_m: unknown schedule");
+  }
+}
+
+}  // namespace
+
+struct samelda_cu_ctx {
+  int device = 0;
+  cudaStream_t own_stream = nullptr;
+  cudaStream_t stream = nullptr;
+  std::string error;
+  int64_t launches = 0;
+
+  CorpusSlot train;    // corpus of the per-call API and of the resident trainer
+  CorpusSlot heldout;  // test corpus of perword_loglik / evaluate
+  uint64_t split_seed = 0;
+  bool split_ready = false;
+  DevBuf tok_offsets, slots, fold_counts, score_counts, doc_logp, doc_scored;
+
+  // resident model (train_begin)
+  bool model_ready = false;
+  samelda_cu_config cfg{};
+  int K = 0;
+  int64_t W = 0, D = 0;
+  DevBuf theta, phi;  // D x K, W x K
+
+  // per-period state
+  int64_t B = 0, nnzB = 0;
+  double m_t = 1.0;
+  bool counts_ready = false;
+  bool counts_float = false;
+
+  // scratch
+  DevBuf batch, prefix, theta_batch, mu, tc, pc, tf, pf, cand, totals, err, ll, phi_call,
+      phi_call_wk, theta_call, eval_scratch, theta_rows;
+  int32_t* h_batch = nullptr;
+  int64_t* h_prefix = nullptr;
+  int64_t h_cap = 0;
+
+  ~samelda_cu_ctx() {
+    if (h_batch) cudaFreeHost(h_batch);
+    if (h_prefix) cudaFreeHost(h_prefix);
+    if (own_stream) cudaStreamDestroy(own_stream);
+  }
+
+  int* d_err() { return ensure<int>(err, 1); }
+
+  void reset_err() { ck(cudaMemsetAsync(d_err(), 0, sizeof(int), stream), "reset error flag"); }
+
+  void check_err(const char* what) {
+    int h = 0;
+    ck(cudaMemcpyAsync(&h, err.p, sizeof(int), cudaMemcpyDeviceToHost, stream), "read error flag");
+    ck(cudaStreamSynchronize(stream), what);
+    ck(cudaGetLastError(), what);
+    if (h & scu::kErrNumerical) fail(SAMELDA_CU_NUMERICAL, "%s: nonfinite or negative value", what);
+  }
+
+  void stage(int64_t B_) {
+    if (h_cap < B_ + 1) {
+      if (h_batch) cudaFreeHost(h_batch);
+      if (h_prefix) cudaFreeHost(h_prefix);
+      h_cap = std::max<int64_t>(B_ + 1, 1024);
+      ck(cudaHostAlloc(&h_batch, sizeof(int32_t) * h_cap, cudaHostAllocDefault), "pinned batch");
+      ck(cudaHostAlloc(&h_prefix, sizeof(int64_t) * h_cap, cudaHostAllocDefault), "pinned prefix");
+    }
+  }
+
+  // Upload a batch of doc ids of `slot` and its nonzero prefix (sampler.cpp:18-24).
+  scu::BatchView upload_batch(const CorpusSlot& slot, const int32_t* doc_ids, int64_t B_) {
+    // the previous period's async copies out of the pinned staging buffers
+    // must have landed before they are overwritten
+    ck(cudaStreamSynchronize(stream), "batch staging");
+    stage(B_);
+    h_prefix[0] = 0;
+    for (int64_t b = 0; b < B_; ++b) {
+      const int32_t d = doc_ids[b];
+      if (d < 0 || d >= slot.n_docs) fail(SAMELDA_CU_CONFIG, "batch doc id %d out of range", d);
+      h_batch[b] = d;
+      h_prefix[b + 1] = h_prefix[b] + (slot.offsets[static_cast<size_t>(d) + 1] -
+                                       slot.offsets[static_cast<size_t>(d)]);
+    }
+    int32_t* db = ensure<int32_t>(batch, B_);
+    int64_t* dp = ensure<int64_t>(prefix, B_ + 1);
+    if (B_ > 0)
+      ck(cudaMemcpyAsync(db, h_batch, sizeof(int32_t) * B_, cudaMemcpyHostToDevice, stream),
+         "upload batch");
+    ck(cudaMemcpyAsync(dp, h_prefix, sizeof(int64_t) * (B_ + 1), cudaMemcpyHostToDevice, stream),
+       "upload prefix");
+    scu::BatchView bv;
+    bv.doc_offsets = slot.offs.as<int64_t>();
+    bv.word_ids = slot.words.as<int32_t>();
+    bv.counts = slot.counts.as<int32_t>();
+    bv.batch_docs = db;
+    bv.batch_prefix = dp;
+    bv.B = B_;
+    bv.nnz = h_prefix[B_];
+    return bv;
+  }
+
+  // phi K x W host -> W x K device (per-call boundary)
+  double* upload_phi(const double* phi_kw, int64_t K_, int64_t W_) {
+    double* tmp = ensure<double>(phi_call, K_ * W_);
+    double* out = ensure<double>(phi_call_wk, K_ * W_);
+    if (K_ * W_ > 0) {
+      ck(cudaMemcpyAsync(tmp, phi_kw, sizeof(double) * K_ * W_, cudaMemcpyHostToDevice, stream),
+         "upload phi");
+      launches += scu::launch_transpose(tmp, K_, W_, out, stream);
+    }
+    return out;
+  }
+
+  // one sweep's sampling into tc/pc (or tf/pf): zeroes the count buffers first
+  void sample_sweep(const scu::BatchView& bv, const double* theta_b, const double* phi_wk,
+                    const double* mu_d, int K_, int64_t W_, double m_t_, uint64_t seed,
+                    int64_t t, int sweep, int mode) {
+    if (mode == SAMELDA_CU_MODE_EXPECTED) {
+      double* tf_ = ensure<double>(tf, bv.B * K_);
+      double* pf_ = ensure<double>(pf, W_ * K_);
+      ck(cudaMemsetAsync(tf_, 0, sizeof(double) * std::max<int64_t>(bv.B * K_, 1), stream), "zero tf");
+      ck(cudaMemsetAsync(pf_, 0, sizeof(double) * std::max<int64_t>(W_ * K_, 1), stream), "zero pf");
+      launches += scu::launch_sample(bv, theta_b, phi_wk, mu_d, K_, m_t_, seed,
+                                     static_cast<uint32_t>(t), static_cast<uint32_t>(sweep), mode,
+                                     nullptr, nullptr, tf_, pf_, d_err(), stream);
+    } else {
+      auto* tc_ = ensure<unsigned long long>(tc, bv.B * K_);
+      auto* pc_ = ensure<unsigned long long>(pc, W_ * K_);
+      ck(cudaMemsetAsync(tc_, 0, sizeof(unsigned long long) * std::max<int64_t>(bv.B * K_, 1), stream), "zero tc");
+      ck(cudaMemsetAsync(pc_, 0, sizeof(unsigned long long) * std::max<int64_t>(W_ * K_, 1), stream), "zero pc");
+      launches += scu::launch_sample(bv, theta_b, phi_wk, mu_d, K_, m_t_, seed,
+                                     static_cast<uint32_t>(t), static_cast<uint32_t>(sweep), mode,
+                                     tc_, pc_, nullptr, nullptr, d_err(), stream);
+    }
+  }
+
+  // eval split for the heldout slot (eval.cpp:99-121), cached per (corpus, seed)
+  void prepare_split(uint64_t seed) {
+    if (split_ready && split_seed == seed) return;
+    const int64_t nd = heldout.n_docs;
+    std::vector<int64_t> tok(static_cast<size_t>(nd) + 1, 0);
+    for (int64_t d = 0; d < nd; ++d) tok[d + 1] = tok[d] + heldout.doc_tokens[static_cast<size_t>(d)];
+    int64_t* dtok = ensure<int64_t>(tok_offsets, nd + 1);
+    ck(cudaMemcpyAsync(dtok, tok.data(), sizeof(int64_t) * (nd + 1), cudaMemcpyHostToDevice, stream),
+       "upload token offsets");
+    launches += scu::launch_eval_split(heldout.offs.as<int64_t>(), heldout.counts.as<int32_t>(), dtok,
+                                       nd, seed, ensure<int32_t>(slots, tok[nd]),
+                                       ensure<int32_t>(fold_counts, heldout.nnz),
+                                       ensure<int32_t>(score_counts, heldout.nnz), stream);
+    ck(cudaStreamSynchronize(stream), "eval split");
+    split_seed = seed;
+    split_ready = true;
+  }
+
+  double eval_ll(const double* phi_wk, int K_, double alpha) {
+    const int64_t nd = heldout.n_docs;
+    double* lp = ensure<double>(doc_logp, nd);
+    int64_t* sc = ensure<int64_t>(doc_scored, nd);
+    const int64_t need = scu::eval_scratch_doubles(K_);
+    double* scratch = need > 0 ? ensure<double>(eval_scratch, need) : nullptr;
+    reset_err();
+    launches += scu::launch_eval_docs(heldout.offs.as<int64_t>(), heldout.words.as<int32_t>(),
+                                      fold_counts.as<int32_t>(), score_counts.as<int32_t>(), nd,
+                                      phi_wk, K_, alpha, 50, lp, sc, nullptr, scratch, need,
+                                      d_err(), stream);
+    double* dll = ensure<double>(ll, 1);
+    launches += scu::launch_ordered_ll(lp, sc, nd, dll, d_err(), stream);
+    double out = 0.0;
+    ck(cudaMemcpyAsync(&out, dll, sizeof(double), cudaMemcpyDeviceToHost, stream), "read ll");
+    check_err("perword_loglik");
+    return out;
+  }
+};
+
+namespace {
+
+template <class F>
+int guarded(samelda_cu_ctx* ctx, F&& fn) {
+  if (ctx == nullptr) return SAMELDA_CU_CONFIG;
+  try {
+    ck(cudaSetDevice(ctx->device), "cudaSetDevice");
+    fn();
+    ctx->error.clear();
+    return SAMELDA_CU_OK;
+  } catch (const Fail& f) {
+    ctx->error = f.msg;
+    if (f.code == SAMELDA_CU_CUDA) cudaGetLastError();
+    return f.code;
+  } catch (const std::exception& e) {
+    ctx->error = e.what();
+    return SAMELDA_CU_CUDA;
+  }
+}
+
+int64_t batch_nnz_host(const CorpusSlot& s, const int32_t* doc_ids, int64_t B) {
+  int64_t n = 0;
+  for (int64_t b = 0; b < B; ++b) {
+    const int32_t d = doc_ids[b];
+    if (d < 0 || d >= s.n_docs) fail(SAMELDA_CU_CONFIG, "batch doc id %d out of range", d);
+    n += s.offsets[static_cast<size_t>(d) + 1] - s.offsets[static_cast<size_t>(d)];
+  }
+  return n;
+}
+
+}  // namespace
+
+extern "C" {
+
+int samelda_cu_version(void) { return kVersion; }
+
+int samelda_cu_create(int device, samelda_cu_ctx** out) {
+  if (out == nullptr) return SAMELDA_CU_CONFIG;
+  *out = nullptr;
+  int n = 0;
+  if (cudaGetDeviceCount(&n) != cudaSuccess || n <= device || device < 0) {
+    cudaGetLastError();
+    return SAMELDA_CU_CUDA;
+  }
+  auto* ctx = new samelda_cu_ctx();
+  ctx->device = device;
+  if (cudaSetDevice(device) != cudaSuccess ||
+      cudaStreamCreateWithFlags(&ctx->own_stream, cudaStreamNonBlocking) != cudaSuccess) {
+    delete ctx;
+    return SAMELDA_CU_CUDA;
+  }
+  ctx->stream = ctx->own_stream;
+  *out = ctx;
+  return SAMELDA_CU_OK;
+}
+
+void samelda_cu_destroy(samelda_cu_ctx* ctx) {
+  if (ctx) {
+    cudaSetDevice(ctx->device);
+    cudaStreamSynchronize(ctx->stream);
+    delete ctx;
+  }
+}
+
+const char* samelda_cu_last_error(const samelda_cu_ctx* ctx) {
+  return ctx ? ctx->error.c_str() : "null context";
+}
+
+int samelda_cu_set_stream(samelda_cu_ctx* ctx, void* cuda_stream) {
+  return guarded(ctx, [&] {
+    ck(cudaStreamSynchronize(ctx->stream), "sync old stream");
+    ctx->stream = cuda_stream ? static_cast<cudaStream_t>(cuda_stream) : ctx->own_stream;
+  });
+}
+
+int samelda_cu_synchronize(samelda_cu_ctx* ctx) {
+  return guarded(ctx, [&] { ck(cudaStreamSynchronize(ctx->stream), "synchronize"); });
+}
+
+int64_t samelda_cu_launch_count(const samelda_cu_ctx* ctx) { return ctx ? ctx->launches : 0; }
+
+// ------------------------------------------------------------ per-call API
+
+int samelda_cu_sddmm(samelda_cu_ctx* ctx, const samelda_cu_corpus* corpus,
+                     const double* theta_batch, int64_t B, int64_t K_theta, const double* phi,
+                     int64_t K, int64_t W, const int32_t* doc_ids, double* mu_out,
+                     int64_t mu_cap, int64_t* mu_len) {
+  return guarded(ctx, [&] {
+    // sampler.cpp:90-98
+    if (K_theta != K) fail(SAMELDA_CU_CONFIG, "sddmm: theta columns must match phi rows");
+    validate_corpus(corpus);
+    if (W != corpus->n_words) fail(SAMELDA_CU_CONFIG, "sddmm: phi columns must match the vocabulary size");
+    if (K < 1 || K >= (1 << 20)) fail(SAMELDA_CU_CONFIG, "sddmm: K out of range");
+    *mu_len = 0;
+    if (B == 0) return;
+    upload_corpus(ctx->train, corpus, ctx->stream);
+    const scu::BatchView bv = ctx->upload_batch(ctx->train, doc_ids, B);
+    if (bv.nnz > mu_cap) fail(SAMELDA_CU_CONFIG, "sddmm: mu buffer too small");
+    double* th = ensure<double>(ctx->theta_call, B * K);
+    ck(cudaMemcpyAsync(th, theta_batch, sizeof(double) * B * K, cudaMemcpyHostToDevice, ctx->stream), "upload theta");
+    const double* phi_wk = ctx->upload_phi(phi, K, W);
+    double* mu = ensure<double>(ctx->mu, bv.nnz);
+    ctx->launches += scu::launch_sddmm(bv, th, phi_wk, static_cast<int>(K), mu, ctx->stream);
+    if (bv.nnz > 0)
+      ck(cudaMemcpyAsync(mu_out, mu, sizeof(double) * bv.nnz, cudaMemcpyDeviceToHost, ctx->stream), "download mu");
+    ck(cudaStreamSynchronize(ctx->stream), "sddmm");
+    ck(cudaGetLastError(), "sddmm");
+    *mu_len = bv.nnz;
+  });
+}
+
+static void sample_call(samelda_cu_ctx* ctx, const samelda_cu_corpus* corpus,
+                        const double* theta_batch, int64_t B, int64_t K_theta,
+                        const double* phi, int64_t K, int64_t W, const double* mu,
+                        int64_t mu_len, const int32_t* doc_ids, double m_t, uint64_t seed,
+                        int64_t t, int32_t sweep, int mode, void* theta_out, void* phi_out) {
+  // sampler.cpp:130-140
+  if (!(m_t > 0.0) || !std::isfinite(m_t)) fail(SAMELDA_CU_CONFIG, "sample_counts: m_t must be positive and finite");
+  if (K_theta != K) fail(SAMELDA_CU_CONFIG, "sample_counts: theta columns must match phi rows");
+  if (K < 1 || K >= (1 << 20)) fail(SAMELDA_CU_CONFIG, "sample_counts: K out of range");
+  validate_corpus(corpus);
+  if (W != corpus->n_words) fail(SAMELDA_CU_CONFIG, "sample_counts: phi columns must match the vocabulary size");
+  if (sweep < 0 || sweep > 255) fail(SAMELDA_CU_CONFIG, "sample_counts: sweep out of range");
+  upload_corpus(ctx->train, corpus, ctx->stream);
+  const int64_t nnz = batch_nnz_host(ctx->train, doc_ids, B);
+  if (mu_len != nnz) fail(SAMELDA_CU_CONFIG, "sample_counts: mu is not aligned with the batch nonzeros");
+  const size_t elem = 8;
+  if (B == 0) {
+    std::memset(phi_out, 0, elem * W * K);
+    return;
+  }
+  const scu::BatchView bv = ctx->upload_batch(ctx->train, doc_ids, B);
+  double* th = ensure<double>(ctx->theta_call, B * K);
+  ck(cudaMemcpyAsync(th, theta_batch, sizeof(double) * B * K, cudaMemcpyHostToDevice, ctx->stream), "upload theta");
+  const double* phi_wk = ctx->upload_phi(phi, K, W);
+  double* mu_d = ensure<double>(ctx->mu, nnz);
+  if (nnz > 0)
+    ck(cudaMemcpyAsync(mu_d, mu, sizeof(double) * nnz, cudaMemcpyHostToDevice, ctx->stream), "upload mu");
+  ctx->reset_err();
+  ctx->sample_sweep(bv, th, phi_wk, mu_d, static_cast<int>(K), W, m_t, seed, t, sweep, mode);
+  ctx->check_err("sample_counts");
+  const void* tsrc = mode == SAMELDA_CU_MODE_EXPECTED ? ctx->tf.p : ctx->tc.p;
+  const void* psrc = mode == SAMELDA_CU_MODE_EXPECTED ? ctx->pf.p : ctx->pc.p;
+  ck(cudaMemcpyAsync(theta_out, tsrc, elem * B * K, cudaMemcpyDeviceToHost, ctx->stream), "download theta counts");
+  ck(cudaMemcpyAsync(phi_out, psrc, elem * W * K, cudaMemcpyDeviceToHost, ctx->stream), "download phi counts");
+  ck(cudaStreamSynchronize(ctx->stream), "sample_counts");
+}
+
+int samelda_cu_sample_counts(samelda_cu_ctx* ctx, const samelda_cu_corpus* corpus,
+                             const double* theta_batch, int64_t B, int64_t K_theta,
+                             const double* phi, int64_t K, int64_t W, const double* mu,
+                             int64_t mu_len, const int32_t* doc_ids, double m_t, uint64_t seed,
+                             int64_t t, int32_t sweep, int64_t* theta_counts,
+                             int64_t* phi_counts) {
+  return guarded(ctx, [&] {
+    sample_call(ctx, corpus, theta_batch, B, K_theta, phi, K, W, mu, mu_len, doc_ids, m_t, seed,
+                t, sweep, SAMELDA_CU_MODE_PARITY, theta_counts, phi_counts);
+  });
+}
+
+int samelda_cu_expected_counts(samelda_cu_ctx* ctx, const samelda_cu_corpus* corpus,
+                               const double* theta_batch, int64_t B, int64_t K_theta,
+                               const double* phi, int64_t K, int64_t W, const double* mu,
+                               int64_t mu_len, const int32_t* doc_ids, double m_t,
+                               double* theta_expected, double* phi_expected) {
+  return guarded(ctx, [&] {
+    sample_call(ctx, corpus, theta_batch, B, K_theta, phi, K, W, mu, mu_len, doc_ids, m_t, 0, 0,
+                0, SAMELDA_CU_MODE_EXPECTED, theta_expected, phi_expected);
+  });
+}
+
+static void update_call(samelda_cu_ctx* ctx, double* theta, int64_t D, double* phi, int64_t K,
+                        int64_t W, double alpha, double beta, const int32_t* doc_ids, int64_t B,
+                        const void* tcounts, const void* pcounts, bool expected, double m_t,
+                        double rho_t) {
+  // sampler.cpp:197-229
+  if (!(rho_t > 0.0 && rho_t <= 1.0)) fail(SAMELDA_CU_CONFIG, "update_model: rho_t must be in (0, 1]");
+  if (K < 1 || W < 0 || D < 0) fail(SAMELDA_CU_CONFIG, "update_model: counts are not shaped for this model");
+  for (int64_t b = 0; b < B; ++b)
+    if (doc_ids[b] < 0 || doc_ids[b] >= D) fail(SAMELDA_CU_CONFIG, "update_model: doc id out of range");
+  cudaStream_t st = ctx->stream;
+  const int Ki = static_cast<int>(K);
+  ctx->reset_err();
+  // theta rows: computed on the device for the batch, placed into the host rows
+  if (B > 0) {
+    int32_t* db = ensure<int32_t>(ctx->batch, B);
+    ck(cudaMemcpyAsync(db, doc_ids, sizeof(int32_t) * B, cudaMemcpyHostToDevice, st), "upload ids");
+    double* rows = ensure<double>(ctx->theta_rows, B * K);
+    if (expected) {
+      double* tf = ensure<double>(ctx->tf, B * K);
+      ck(cudaMemcpyAsync(tf, tcounts, sizeof(double) * B * K, cudaMemcpyHostToDevice, st), "upload tf");
+      ctx->launches += scu::launch_theta_from_counts(nullptr, tf, B * K, m_t, alpha, rows, st);
+    } else {
+      auto* tc = ensure<unsigned long long>(ctx->tc, B * K);
+      ck(cudaMemcpyAsync(tc, tcounts, sizeof(int64_t) * B * K, cudaMemcpyHostToDevice, st), "upload tc");
+      ctx->launches += scu::launch_theta_from_counts(tc, nullptr, B * K, m_t, alpha, rows, st);
+    }
+    std::vector<double> h(static_cast<size_t>(B * K));
+    ck(cudaMemcpyAsync(h.data(), rows, sizeof(double) * B * K, cudaMemcpyDeviceToHost, st), "download rows");
+    ck(cudaStreamSynchronize(st), "theta rows");
+    for (int64_t b = 0; b < B; ++b)
+      std::memcpy(theta + static_cast<int64_t>(doc_ids[b]) * K, h.data() + b * K, sizeof(double) * K);
+  }
+  if (W * K == 0) return;
+  double* phi_wk = ctx->upload_phi(phi, K, W);
+  double* cand = ensure<double>(ctx->cand, W * K);
+  double* totals = ensure<double>(ctx->totals, K);
+  if (expected) {
+    double* pf = ensure<double>(ctx->pf, W * K);
+    ck(cudaMemcpyAsync(pf, pcounts, sizeof(double) * W * K, cudaMemcpyHostToDevice, st), "upload pf");
+    ctx->launches += scu::launch_phi_mstep(nullptr, pf, W, Ki, m_t, beta, rho_t, phi_wk, cand, totals, ctx->d_err(), st);
+  } else {
+    auto* pc = ensure<unsigned long long>(ctx->pc, W * K);
+    ck(cudaMemcpyAsync(pc, pcounts, sizeof(int64_t) * W * K, cudaMemcpyHostToDevice, st), "upload pc");
+    ctx->launches += scu::launch_phi_mstep(pc, nullptr, W, Ki, m_t, beta, rho_t, phi_wk, cand, totals, ctx->d_err(), st);
+  }
+  double* back = ensure<double>(ctx->phi_call, K * W);
+  ctx->launches += scu::launch_transpose(phi_wk, W, K, back, st);
+  ctx->check_err("update_model: phi row mass is not positive and finite");
+  ck(cudaMemcpyAsync(phi, back, sizeof(double) * K * W, cudaMemcpyDeviceToHost, st), "download phi");
+  ck(cudaStreamSynchronize(st), "update_model");
+}
+
+int samelda_cu_update_model(samelda_cu_ctx* ctx, double* theta, int64_t D, double* phi,
+                            int64_t K, int64_t W, double alpha, double beta,
+                            const int32_t* doc_ids, int64_t B, const int64_t* theta_counts,
+                            const int64_t* phi_counts, double m_t, double rho_t) {
+  return guarded(ctx, [&] {
+    update_call(ctx, theta, D, phi, K, W, alpha, beta, doc_ids, B, theta_counts, phi_counts,
+                false, m_t, rho_t);
+  });
+}
+
+int samelda_cu_update_model_expected(samelda_cu_ctx* ctx, double* theta, int64_t D,
+                                     double* phi, int64_t K, int64_t W, double alpha,
+                                     double beta, const int32_t* doc_ids, int64_t B,
+                                     const double* theta_expected, const double* phi_expected,
+                                     double m_t, double rho_t) {
+  return guarded(ctx, [&] {
+    update_call(ctx, theta, D, phi, K, W, alpha, beta, doc_ids, B, theta_expected, phi_expected,
+                true, m_t, rho_t);
+  });
+}
+
+int samelda_cu_rho_schedule(int64_t t, double tau0, double gamma, double* out) {
+  try {
+    *out = rho_schedule_host(t, tau0, gamma);
+    return SAMELDA_CU_OK;
+  } catch (const Fail& f) {
+    return f.code;
+  }
+}
+
+int samelda_cu_anneal_m(int32_t schedule, int64_t t, int64_t t_max, double m, double* out) {
+  try {
+    *out = anneal_m_host(schedule, t, t_max, m);
+    return SAMELDA_CU_OK;
+  } catch (const Fail& f) {
+    return f.code;
+  }
+}
+
+int samelda_cu_fold_in_theta(samelda_cu_ctx* ctx, const double* phi, int64_t K, int64_t W,
+                             const int32_t* words, const int32_t* counts, int64_t n,
+                             double alpha, int32_t sweeps, double* theta_out) {
+  return guarded(ctx, [&] {
+    if (K < 1) fail(SAMELDA_CU_CONFIG, "fold_in_theta: K must be >= 1");
+    for (int64_t i = 0; i < n; ++i)
+      if (words[i] < 0 || words[i] >= W) fail(SAMELDA_CU_CONFIG, "fold_in_theta: word id out of range");
+    // one-document corpus: the fold counts are the given counts
+    const int64_t offs[2] = {0, n};
+    std::vector<int32_t> zeros(static_cast<size_t>(std::max<int64_t>(n, 1)), 0);
+    samelda_cu_corpus c{offs, n ? words : zeros.data(), n ? counts : zeros.data(), 1, W};
+    CorpusSlot one;
+    upload_corpus(one, &c, ctx->stream);
+    const double* phi_wk = ctx->upload_phi(phi, K, W);
+    int32_t* fc = ensure<int32_t>(ctx->fold_counts, std::max<int64_t>(n, 1));
+    int32_t* sc = ensure<int32_t>(ctx->score_counts, std::max<int64_t>(n, 1));
+    if (n > 0) {
+      ck(cudaMemcpyAsync(fc, counts, sizeof(int32_t) * n, cudaMemcpyHostToDevice, ctx->stream), "upload counts");
+      ck(cudaMemsetAsync(sc, 0, sizeof(int32_t) * n, ctx->stream), "zero score");
+    }
+    ctx->split_ready = false;  // fold/score buffers now hold this call's counts
+    double* lp = ensure<double>(ctx->doc_logp, 1);
+    int64_t* scd = ensure<int64_t>(ctx->doc_scored, 1);
+    double* th = ensure<double>(ctx->theta_rows, K);
+    const int64_t need = scu::eval_scratch_doubles(static_cast<int>(K));
+    double* scratch = need > 0 ? ensure<double>(ctx->eval_scratch, need) : nullptr;
+    ctx->reset_err();
+    ctx->launches += scu::launch_eval_docs(one.offs.as<int64_t>(), one.words.as<int32_t>(), fc, sc, 1, phi_wk,
+                                           static_cast<int>(K), alpha, sweeps, lp, scd, th, scratch, need,
+                                           ctx->d_err(), ctx->stream);
+    ck(cudaMemcpyAsync(theta_out, th, sizeof(double) * K, cudaMemcpyDeviceToHost, ctx->stream), "download theta");
+    ck(cudaStreamSynchronize(ctx->stream), "fold_in_theta");
+    ck(cudaGetLastError(), "fold_in_theta");
+  });
+}
+
+int samelda_cu_perword_loglik(samelda_cu_ctx* ctx, const double* phi, int64_t K, int64_t W,
+                              const samelda_cu_corpus* test, double alpha, uint64_t seed,
+                              double* ll_out) {
+  return guarded(ctx, [&] {
+    validate_corpus(test);
+    if (test->n_docs < 1) fail(SAMELDA_CU_CONFIG, "perword_loglik: test corpus is empty");
+    if (W != test->n_words) fail(SAMELDA_CU_CONFIG, "perword_loglik: phi width disagrees with corpus vocabulary");
+    if (K < 1) fail(SAMELDA_CU_CONFIG, "perword_loglik: K must be >= 1");
+    const uint64_t before = ctx->heldout.fp;
+    const bool was_valid = ctx->heldout.valid;
+    upload_corpus(ctx->heldout, test, ctx->stream);
+    if (!was_valid || before != ctx->heldout.fp) ctx->split_ready = false;
+    ctx->prepare_split(seed);
+    const double* phi_wk = ctx->upload_phi(phi, K, W);
+    *ll_out = ctx->eval_ll(phi_wk, static_cast<int>(K), alpha);
+  });
+}
+
+// ------------------------------------------------------------ trainer
+
+int samelda_cu_batches_create(int64_t n_docs, double batch_fraction, uint64_t seed,
+                              samelda_cu_batches** out) {
+  if (!(batch_fraction > 0.0 && batch_fraction <= 1.0)) return SAMELDA_CU_CONFIG;
+  if (n_docs < 0 || out == nullptr) return SAMELDA_CU_CONFIG;
+  auto* b = new Batches();
+  b->n_docs = n_docs;
+  b->seed = seed;
+  b->batch_size = std::max<int64_t>(
+      1, static_cast<int64_t>(std::llround(batch_fraction * static_cast<double>(n_docs))));
+  b->start_pass();
+  *out = reinterpret_cast<samelda_cu_batches*>(b);
+  return SAMELDA_CU_OK;
+}
+
+int64_t samelda_cu_batches_size(const samelda_cu_batches* s) {
+  return reinterpret_cast<const Batches*>(s)->batch_size;
+}
+
+int64_t samelda_cu_batches_per_pass(const samelda_cu_batches* s) {
+  return reinterpret_cast<const Batches*>(s)->per_pass();
+}
+
+int64_t samelda_cu_batches_next(samelda_cu_batches* s, int32_t* out) {
+  return reinterpret_cast<Batches*>(s)->next(out);
+}
+
+void samelda_cu_batches_destroy(samelda_cu_batches* s) { delete reinterpret_cast<Batches*>(s); }
+
+int samelda_cu_train_begin(samelda_cu_ctx* ctx, const samelda_cu_corpus* corpus,
+                           const samelda_cu_config* config) {
+  return guarded(ctx, [&] {
+    validate_config(config);
+    validate_corpus(corpus);
+    if (corpus->n_docs < 1) fail(SAMELDA_CU_CONFIG, "train: corpus is empty");
+    upload_corpus(ctx->train, corpus, ctx->stream);
+    ctx->cfg = *config;
+    ctx->K = static_cast<int>(config->n_topics);
+    ctx->W = corpus->n_words;
+    ctx->D = corpus->n_docs;
+    const int64_t K = ctx->K;
+    double* th = ensure<double>(ctx->theta, ctx->D * K);
+    double* ph = ensure<double>(ctx->phi, ctx->W * K);
+    // init_model (model.cpp:41-52) then the seeded perturbation
+    // (sampler.cpp:285-298), which only applies when t_max > 0
+    ctx->launches += scu::launch_fill(th, ctx->D * K, config->alpha + 1.0 / static_cast<double>(K), ctx->stream);
+    ctx->launches += scu::launch_phi_init(ph, ctx->W, ctx->K, config->t_max > 0 ? config->init_noise : 0.0,
+                                          config->seed, ensure<double>(ctx->totals, K), ctx->stream);
+    ck(cudaStreamSynchronize(ctx->stream), "train_begin");
+    ck(cudaGetLastError(), "train_begin");
+    ctx->model_ready = true;
+    ctx->counts_ready = false;
+  });
+}
+
+int samelda_cu_heldout(samelda_cu_ctx* ctx, const samelda_cu_corpus* test, uint64_t seed) {
+  return guarded(ctx, [&] {
+    validate_corpus(test);
+    if (test->n_docs < 1) fail(SAMELDA_CU_CONFIG, "perword_loglik: test corpus is empty");
+    const uint64_t before = ctx->heldout.fp;
+    const bool was_valid = ctx->heldout.valid;
+    upload_corpus(ctx->heldout, test, ctx->stream);
+    if (!was_valid || before != ctx->heldout.fp) ctx->split_ready = false;
+    ctx->prepare_split(seed);
+  });
+}
+
+int samelda_cu_period_sample(samelda_cu_ctx* ctx, const int32_t* doc_ids, int64_t B, int64_t t,
+                             double m_t) {
+  return guarded(ctx, [&] {
+    if (!ctx->model_ready) fail(SAMELDA_CU_CONFIG, "period: call samelda_cu_train_begin first");
+    if (!(m_t > 0.0) || !std::isfinite(m_t)) fail(SAMELDA_CU_CONFIG, "sample_counts: m_t must be positive and finite");
+    const samelda_cu_config& c = ctx->cfg;
+    const int K = ctx->K;
+    cudaStream_t st = ctx->stream;
+    const scu::BatchView bv = ctx->upload_batch(ctx->train, doc_ids, B);
+    ctx->B = B;
+    ctx->nnzB = bv.nnz;
+    ctx->m_t = m_t;
+    double* thb = ensure<double>(ctx->theta_batch, B * K);
+    double* mu = ensure<double>(ctx->mu, bv.nnz);
+    ctx->reset_err();
+    ctx->launches += scu::launch_gather_theta(ctx->theta.as<double>(), bv.batch_docs, B, K, thb, st);
+    for (int64_t sweep = 0; sweep < c.inner_sweeps; ++sweep) {
+      ctx->launches += scu::launch_sddmm(bv, thb, ctx->phi.as<double>(), K, mu, st);
+      ctx->sample_sweep(bv, thb, ctx->phi.as<double>(), mu, K, ctx->W, m_t, c.seed, t,
+                        static_cast<int>(sweep), c.mode);
+      if (sweep + 1 < c.inner_sweeps) {
+        if (c.mode == SAMELDA_CU_MODE_EXPECTED)
+          ctx->launches += scu::launch_theta_from_counts(nullptr, ctx->tf.as<double>(), B * K, m_t, c.alpha, thb, st);
+        else
+          ctx->launches += scu::launch_theta_from_counts(ctx->tc.as<unsigned long long>(), nullptr, B * K, m_t,
+                                                         c.alpha, thb, st);
+      }
+    }
+    ck(cudaGetLastError(), "period sample launch");
+    ctx->counts_ready = true;
+    ctx->counts_float = c.mode == SAMELDA_CU_MODE_EXPECTED;
+  });
+}
+
+int samelda_cu_period_update(samelda_cu_ctx* ctx, double rho_t) {
+  return guarded(ctx, [&] {
+    if (!ctx->counts_ready) fail(SAMELDA_CU_CONFIG, "period_update without period_sample");
+    if (!(rho_t > 0.0 && rho_t <= 1.0)) fail(SAMELDA_CU_CONFIG, "update_model: rho_t must be in (0, 1]");
+    const samelda_cu_config& c = ctx->cfg;
+    const int K = ctx->K;
+    cudaStream_t st = ctx->stream;
+    const bool f = ctx->counts_float;
+    const auto* tcu = f ? nullptr : ctx->tc.as<unsigned long long>();
+    const auto* pcu = f ? nullptr : ctx->pc.as<unsigned long long>();
+    const double* tcf = f ? ctx->tf.as<double>() : nullptr;
+    const double* pcf = f ? ctx->pf.as<double>() : nullptr;
+    ctx->launches += scu::launch_theta_persist(tcu, tcf, ctx->batch.as<int32_t>(), ctx->B, K, ctx->m_t, c.alpha,
+                                               ctx->theta.as<double>(), st);
+    ctx->launches += scu::launch_phi_mstep(pcu, pcf, ctx->W, K, ctx->m_t, c.beta, rho_t, ctx->phi.as<double>(),
+                                           ensure<double>(ctx->cand, ctx->W * K), ensure<double>(ctx->totals, K),
+                                           ctx->d_err(), st);
+    ctx->check_err("period");
+  });
+}
+
+int samelda_cu_period(samelda_cu_ctx* ctx, const int32_t* doc_ids, int64_t B, int64_t t,
+                      double m_t, double rho_t) {
+  int rc = samelda_cu_period_sample(ctx, doc_ids, B, t, m_t);
+  if (rc) return rc;
+  return samelda_cu_period_update(ctx, rho_t);
+}
+
+int samelda_cu_phi_counts_device(samelda_cu_ctx* ctx, void** ptr, int64_t* n_elems,
+                                 int32_t* elem_bytes, int32_t* is_float) {
+  return guarded(ctx, [&] {
+    if (!ctx->counts_ready) fail(SAMELDA_CU_CONFIG, "no sampled counts yet");
+    *ptr = ctx->counts_float ? ctx->pf.p : ctx->pc.p;
+    *n_elems = ctx->W * ctx->K;
+    *elem_bytes = 8;
+    *is_float = ctx->counts_float ? 1 : 0;
+  });
+}
+
+int samelda_cu_batch_theta(samelda_cu_ctx* ctx, double* out, int64_t cap) {
+  return guarded(ctx, [&] {
+    if (!ctx->model_ready) fail(SAMELDA_CU_CONFIG, "no model");
+    const int64_t n = ctx->B * ctx->K;
+    if (cap < n) fail(SAMELDA_CU_CONFIG, "batch_theta: buffer too small");
+    double* rows = ensure<double>(ctx->theta_rows, n);
+    ctx->launches += scu::launch_gather_theta(ctx->theta.as<double>(), ctx->batch.as<int32_t>(), ctx->B, ctx->K,
+                                              rows, ctx->stream);
+    if (n > 0)
+      ck(cudaMemcpyAsync(out, rows, sizeof(double) * n, cudaMemcpyDeviceToHost, ctx->stream), "download rows");
+    ck(cudaStreamSynchronize(ctx->stream), "batch_theta");
+  });
+}
+
+int samelda_cu_count_totals(samelda_cu_ctx* ctx, int64_t* theta_total, int64_t* phi_total) {
+  return guarded(ctx, [&] {
+    if (!ctx->counts_ready || ctx->counts_float) fail(SAMELDA_CU_CONFIG, "no integer counts");
+    std::vector<int64_t> a(static_cast<size_t>(std::max<int64_t>(ctx->B * ctx->K, 1)));
+    std::vector<int64_t> b(static_cast<size_t>(std::max<int64_t>(ctx->W * ctx->K, 1)));
+    ck(cudaMemcpyAsync(a.data(), ctx->tc.p, sizeof(int64_t) * ctx->B * ctx->K, cudaMemcpyDeviceToHost, ctx->stream), "tc");
+    ck(cudaMemcpyAsync(b.data(), ctx->pc.p, sizeof(int64_t) * ctx->W * ctx->K, cudaMemcpyDeviceToHost, ctx->stream), "pc");
+    ck(cudaStreamSynchronize(ctx->stream), "count totals");
+    int64_t s0 = 0, s1 = 0;
+    for (int64_t i = 0; i < ctx->B * ctx->K; ++i) s0 += a[static_cast<size_t>(i)];
+    for (int64_t i = 0; i < ctx->W * ctx->K; ++i) s1 += b[static_cast<size_t>(i)];
+    *theta_total = s0;
+    *phi_total = s1;
+  });
+}
+
+int samelda_cu_evaluate(samelda_cu_ctx* ctx, double* ll_out) {
+  return guarded(ctx, [&] {
+    if (!ctx->model_ready) fail(SAMELDA_CU_CONFIG, "evaluate: no model");
+    if (!ctx->heldout.valid || !ctx->split_ready) fail(SAMELDA_CU_CONFIG, "evaluate: call samelda_cu_heldout first");
+    if (ctx->heldout.n_words != ctx->W) fail(SAMELDA_CU_CONFIG, "perword_loglik: phi width disagrees with corpus vocabulary");
+    *ll_out = ctx->eval_ll(ctx->phi.as<double>(), ctx->K, ctx->cfg.alpha);
+  });
+}
+
+int samelda_cu_model_download(samelda_cu_ctx* ctx, double* phi, double* theta) {
+  return guarded(ctx, [&] {
+    if (!ctx->model_ready) fail(SAMELDA_CU_CONFIG, "no model");
+    const int64_t K = ctx->K;
+    if (phi) {
+      double* tmp = ensure<double>(ctx->phi_call, K * ctx->W);
+      ctx->launches += scu::launch_transpose(ctx->phi.as<double>(), ctx->W, K, tmp, ctx->stream);
+      ck(cudaMemcpyAsync(phi, tmp, sizeof(double) * K * ctx->W, cudaMemcpyDeviceToHost, ctx->stream), "download phi");
+    }
+    if (theta)
+      ck(cudaMemcpyAsync(theta, ctx->theta.p, sizeof(double) * ctx->D * K, cudaMemcpyDeviceToHost, ctx->stream),
+         "download theta");
+    ck(cudaStreamSynchronize(ctx->stream), "model_download");
+  });
+}
+
+int samelda_cu_model_upload(samelda_cu_ctx* ctx, const double* phi, const double* theta) {
+  return guarded(ctx, [&] {
+    if (!ctx->model_ready) fail(SAMELDA_CU_CONFIG, "no model");
+    const int64_t K = ctx->K;
+    if (phi) {
+      const double* wk = ctx->upload_phi(phi, K, ctx->W);
+      ck(cudaMemcpyAsync(ctx->phi.p, wk, sizeof(double) * K * ctx->W, cudaMemcpyDeviceToDevice, ctx->stream), "phi");
+    }
+    if (theta)
+      ck(cudaMemcpyAsync(ctx->theta.p, theta, sizeof(double) * ctx->D * K, cudaMemcpyHostToDevice, ctx->stream), "theta");
+    ck(cudaStreamSynchronize(ctx->stream), "model_upload");
+  });
+}
+
+int samelda_cu_train(samelda_cu_ctx* ctx, const samelda_cu_corpus* corpus,
+                     const samelda_cu_config* config, const samelda_cu_corpus* heldout,
+                     int64_t eval_every, double* phi_out, double* theta_out,
+                     samelda_cu_trace_row* trace, int64_t trace_cap, int64_t* n_trace) {
+  // sampler.cpp:269-353
+  int rc = samelda_cu_train_begin(ctx, corpus, config);
+  if (rc) return rc;
+  *n_trace = 0;
+  const bool do_eval = heldout != nullptr && eval_every > 0;
+  if (do_eval && config->t_max > 0) {
+    rc = samelda_cu_heldout(ctx, heldout, config->seed);
+    if (rc) return rc;
+  }
+  return guarded(ctx, [&] {
+    if (config->t_max > 0) {
+      Batches batches;
+      batches.n_docs = corpus->n_docs;
+      batches.seed = config->seed;
+      batches.batch_size = std::max<int64_t>(
+          1, static_cast<int64_t>(std::llround(config->batch_fraction * static_cast<double>(corpus->n_docs))));
+      batches.start_pass();
+      const auto t_start = std::chrono::steady_clock::now();
+      double tokens_seen = 0.0;
+      double samples_per_word = 0.0;
+      const double corpus_tokens = static_cast<double>(ctx->train.n_tokens);
+      std::vector<int32_t> batch(static_cast<size_t>(batches.batch_size));
+      for (int64_t t = 0; t < config->t_max; ++t) {
+        const int64_t B = batches.next(batch.data());
+        const double m_t = anneal_m_host(config->schedule, t + 1, config->t_max, config->m);
+        const double rho_t = rho_schedule_host(t, config->tau0, config->gamma);
+        int r = samelda_cu_period(ctx, batch.data(), B, t, m_t, rho_t);
+        if (r) throw Fail{r, ctx->error};
+        double batch_tokens = 0.0;
+        for (int64_t b = 0; b < B; ++b)
+          batch_tokens += static_cast<double>(ctx->train.doc_tokens[static_cast<size_t>(batch[b])]);
+        tokens_seen += batch_tokens;
+        samples_per_word += m_t * batch_tokens / corpus_tokens;
+        if (do_eval && ((t + 1) % eval_every == 0 || t + 1 == config->t_max)) {
+          double ll = 0.0;
+          r = samelda_cu_evaluate(ctx, &ll);
+          if (r) throw Fail{r, ctx->error};
+          const std::chrono::duration<double> el = std::chrono::steady_clock::now() - t_start;
+          if (*n_trace >= trace_cap) fail(SAMELDA_CU_CONFIG, "trace buffer too small");
+          trace[(*n_trace)++] = {t, tokens_seen / corpus_tokens, samples_per_word, ll, el.count(), m_t};
+        }
+      }
+    }
+    int r = samelda_cu_model_download(ctx, phi_out, theta_out);
+    if (r) throw Fail{r, ctx->error};
+  });
+}
+
+}  // extern "C"

@@ -1,0 +1,100 @@
+// kernels.cuh -- launchers for the sm_100a SAME/LDA kernels (internal API).
+//
+// Device data model:
+//   corpus   CSR, doc-major: doc_offsets i64[D+1], word_ids i32[nnz], counts i32[nnz]
+//            (corpus.hpp:15-32), uploaded once and kept resident
+//   theta    D x K f64, row-major (model.hpp:40-47)
+//   phi      W x K f64, WORD-major (the reference stores K x W and transposes
+//            twice per sweep, sampler.cpp:100,140; we never transpose on the
+//            hot path)
+//   counts   theta B x K and phi W x K, u64 (SampledCounts, sampler.hpp:50-68)
+//   batch    doc ids i32[B] in MinibatchStream order + nnz prefix i64[B+1]
+//            (batch_nnz_prefix, sampler.cpp:18-24)
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+namespace scu {
+
+enum Mode : int { kModeParity = 0, kModeExpected = 1, kModeFast = 2 };
+
+enum ErrBits : int { kErrNumerical = 1 };
+
+struct BatchView {
+  const int64_t* doc_offsets;
+  const int32_t* word_ids;
+  const int32_t* counts;
+  const int32_t* batch_docs;
+  const int64_t* batch_prefix;
+  int64_t B;
+  int64_t nnz;  // batch_prefix[B]
+};
+
+// theta_batch[b,:] = theta[batch_docs[b],:]            (sampler.cpp:313-317)
+int launch_gather_theta(const double* theta, const int32_t* batch_docs, int64_t B, int K,
+                         double* theta_batch, cudaStream_t st);
+
+// mu[p] = sum_k theta_batch[b,k] * phi[w,k], sequential k  (sampler.cpp:88-123)
+int launch_sddmm(const BatchView& bv, const double* theta_batch, const double* phi_wk, int K,
+                  double* mu, cudaStream_t st);
+
+// Poisson replica sampling + count scatter                (sampler.cpp:125-195)
+// mode kModeParity: reference-identical draws into u64 counts;
+// mode kModeExpected: z := rate into f64 counts (deterministic factored path).
+int launch_sample(const BatchView& bv, const double* theta_batch, const double* phi_wk,
+                   const double* mu, int K, double m_t, uint64_t seed, uint32_t t,
+                   uint32_t sweep, int mode, unsigned long long* theta_counts,
+                   unsigned long long* phi_counts, double* theta_exp, double* phi_exp,
+                   int* err, cudaStream_t st);
+
+// out[i] = counts[i] / m_t + alpha over n entries       (sampler.cpp:324-330)
+int launch_theta_from_counts(const unsigned long long* counts_u, const double* counts_f,
+                              int64_t n, double m_t, double alpha, double* out,
+                              cudaStream_t st);
+
+// theta[batch_docs[b],k] = counts[b,k] / m_t + alpha     (sampler.cpp:204-210)
+int launch_theta_persist(const unsigned long long* counts_u, const double* counts_f,
+                          const int32_t* batch_docs, int64_t B, int K, double m_t,
+                          double alpha, double* theta, cudaStream_t st);
+
+// M-step for phi (sampler.cpp:211-228):
+//   cand[w,k] = counts[w,k]/m_t + beta; total[k] = sum_w cand (sequential w);
+//   phi = (1-rho) phi + rho cand / total
+int launch_phi_mstep(const unsigned long long* counts_u, const double* counts_f, int64_t W,
+                      int K, double m_t, double beta, double rho, double* phi_wk,
+                      double* cand_scratch, double* totals, int* err, cudaStream_t st);
+
+// phi init with seeded perturbation (model.cpp:41-52, sampler.cpp:285-298)
+int launch_phi_init(double* phi_wk, int64_t W, int K, double init_noise, uint64_t seed,
+                     double* totals, cudaStream_t st);
+
+// theta init alpha + 1/K (model.cpp:41-52)
+int launch_fill(double* p, int64_t n, double v, cudaStream_t st);
+
+// K x W <-> W x K transposes for the per-call boundary (model.cpp:31-39)
+int launch_transpose(const double* in, int64_t rows, int64_t cols, double* out,
+                      cudaStream_t st);
+
+// eval.cpp:99-121: per-doc seeded token split -> fold / score counts per cell
+int launch_eval_split(const int64_t* doc_offsets, const int32_t* counts,
+                       const int64_t* token_offsets, int64_t n_docs, uint64_t seed,
+                       int32_t* slots, int32_t* fold_counts, int32_t* score_counts,
+                       cudaStream_t st);
+
+// eval.cpp:19-64 + 125-145: per-doc fold-in then scoring.  theta_out (optional) n_docs x K.
+int launch_eval_docs(const int64_t* doc_offsets, const int32_t* word_ids,
+                      const int32_t* fold_counts, const int32_t* score_counts, int64_t n_docs,
+                      const double* phi_wk, int K, double alpha, int sweeps, double* doc_logp,
+                      int64_t* doc_scored, double* theta_out, double* scratch,
+                      int64_t scratch_doubles, int* err, cudaStream_t st);
+
+// eval.cpp:148-158: doc-order reduction -> ll
+int launch_ordered_ll(const double* doc_logp, const int64_t* doc_scored, int64_t n_docs,
+                       double* ll_out, int* err, cudaStream_t st);
+
+// scratch doubles launch_eval_docs needs when K is too large for shared memory
+int64_t eval_scratch_doubles(int K);
+
+}  // namespace scu

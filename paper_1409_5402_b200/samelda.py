@@ -1,0 +1,574 @@
+"""Python mirror of the reference `samelda` sampler/eval interface over the C ABI.
+
+Same names, argument meaning and error behaviour as the reference's
+``sampler.hpp`` / ``eval.hpp`` (proj/include/samelda/), so the parity tests
+read like the reference's own tests:
+
+    sddmm(theta_batch, phi, corpus, doc_ids)                    sampler.hpp:74-81
+    sample_counts(theta_batch, phi, mu, corpus, doc_ids, m_t,
+                  seed, t, sweep)                               sampler.hpp:83-91
+    update_model(model, counts, rho_t)                          sampler.hpp:93-97
+    rho_schedule(t, tau0, gamma), anneal_m(schedule, t, t_max, m)
+    train(corpus, config, heldout, eval_every)                  sampler.hpp:105-110
+    fold_in_theta(phi, words, counts, alpha, sweeps)            eval.hpp:32-36
+    perword_loglik(phi, test, alpha, seed)                      eval.hpp:38-43
+
+Every call goes through ``libsamelda_cuda.so`` (include/samelda_cu.h).  There
+is no CPU fallback: importing this module without the built library, or
+calling it without a CUDA device, raises.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+from dataclasses import dataclass, field
+
+import numpy as np
+
+_LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "libsamelda_cuda.so")
+
+MODE_PARITY = 0
+MODE_EXPECTED = 1
+SCHEDULES = {"constant": 0, "linear": 1, "log": 2, "invlinear": 3}
+
+
+class SameldaError(RuntimeError):
+    """Base of the reference's error classes (errors.hpp:7-20)."""
+
+
+class ConfigError(SameldaError):
+    pass
+
+
+class IoError(SameldaError):
+    pass
+
+
+class NumericalError(SameldaError):
+    pass
+
+
+class CudaError(SameldaError):
+    pass
+
+
+_CODES = {1: ConfigError, 2: IoError, 3: NumericalError, 4: CudaError}
+
+
+class _Corpus(C.Structure):
+    _fields_ = [("doc_offsets", C.c_void_p), ("word_ids", C.c_void_p), ("counts", C.c_void_p),
+                ("n_docs", C.c_int64), ("n_words", C.c_int64)]
+
+
+class _Config(C.Structure):
+    _fields_ = [("n_topics", C.c_int64), ("m", C.c_double), ("schedule", C.c_int32),
+                ("tau0", C.c_double), ("gamma", C.c_double), ("batch_fraction", C.c_double),
+                ("t_max", C.c_int64), ("inner_sweeps", C.c_int64), ("seed", C.c_uint64),
+                ("alpha", C.c_double), ("beta", C.c_double), ("init_noise", C.c_double),
+                ("mode", C.c_int32)]
+
+
+class _TraceRow(C.Structure):
+    _fields_ = [("t", C.c_int64), ("passes", C.c_double), ("samples_per_word", C.c_double),
+                ("ll", C.c_double), ("wall_seconds", C.c_double), ("m_t", C.c_double)]
+
+
+# (name, restype, argtypes) of every entry point in include/samelda_cu.h
+_P, _I64, _I32, _D, _U64 = C.c_void_p, C.c_int64, C.c_int32, C.c_double, C.c_uint64
+_CP = C.POINTER(_Corpus)
+SIGNATURES = [
+    ("samelda_cu_version", C.c_int, []),
+    ("samelda_cu_create", C.c_int, [C.c_int, C.POINTER(C.c_void_p)]),
+    ("samelda_cu_destroy", None, [_P]),
+    ("samelda_cu_last_error", C.c_char_p, [_P]),
+    ("samelda_cu_set_stream", C.c_int, [_P, _P]),
+    ("samelda_cu_synchronize", C.c_int, [_P]),
+    ("samelda_cu_launch_count", _I64, [_P]),
+    ("samelda_cu_sddmm", C.c_int, [_P, _CP, _P, _I64, _I64, _P, _I64, _I64, _P, _P, _I64,
+                                   C.POINTER(_I64)]),
+    ("samelda_cu_sample_counts", C.c_int, [_P, _CP, _P, _I64, _I64, _P, _I64, _I64, _P, _I64,
+                                           _P, _D, _U64, _I64, _I32, _P, _P]),
+    ("samelda_cu_expected_counts", C.c_int, [_P, _CP, _P, _I64, _I64, _P, _I64, _I64, _P, _I64,
+                                             _P, _D, _P, _P]),
+    ("samelda_cu_update_model", C.c_int, [_P, _P, _I64, _P, _I64, _I64, _D, _D, _P, _I64, _P,
+                                          _P, _D, _D]),
+    ("samelda_cu_update_model_expected", C.c_int, [_P, _P, _I64, _P, _I64, _I64, _D, _D, _P,
+                                                   _I64, _P, _P, _D, _D]),
+    ("samelda_cu_rho_schedule", C.c_int, [_I64, _D, _D, C.POINTER(_D)]),
+    ("samelda_cu_anneal_m", C.c_int, [_I32, _I64, _I64, _D, C.POINTER(_D)]),
+    ("samelda_cu_fold_in_theta", C.c_int, [_P, _P, _I64, _I64, _P, _P, _I64, _D, _I32, _P]),
+    ("samelda_cu_perword_loglik", C.c_int, [_P, _P, _I64, _I64, _CP, _D, _U64, C.POINTER(_D)]),
+    ("samelda_cu_batches_create", C.c_int, [_I64, _D, _U64, C.POINTER(C.c_void_p)]),
+    ("samelda_cu_batches_size", _I64, [_P]),
+    ("samelda_cu_batches_per_pass", _I64, [_P]),
+    ("samelda_cu_batches_next", _I64, [_P, _P]),
+    ("samelda_cu_batches_destroy", None, [_P]),
+    ("samelda_cu_train_begin", C.c_int, [_P, _CP, C.POINTER(_Config)]),
+    ("samelda_cu_heldout", C.c_int, [_P, _CP, _U64]),
+    ("samelda_cu_period", C.c_int, [_P, _P, _I64, _I64, _D, _D]),
+    ("samelda_cu_period_sample", C.c_int, [_P, _P, _I64, _I64, _D]),
+    ("samelda_cu_period_update", C.c_int, [_P, _D]),
+    ("samelda_cu_phi_counts_device", C.c_int, [_P, C.POINTER(C.c_void_p), C.POINTER(_I64),
+                                               C.POINTER(_I32), C.POINTER(_I32)]),
+    ("samelda_cu_batch_theta", C.c_int, [_P, _P, _I64]),
+    ("samelda_cu_count_totals", C.c_int, [_P, C.POINTER(_I64), C.POINTER(_I64)]),
+    ("samelda_cu_evaluate", C.c_int, [_P, C.POINTER(_D)]),
+    ("samelda_cu_model_download", C.c_int, [_P, _P, _P]),
+    ("samelda_cu_model_upload", C.c_int, [_P, _P, _P]),
+    ("samelda_cu_train", C.c_int, [_P, _CP, C.POINTER(_Config), _CP, _I64, _P, _P,
+                                   C.POINTER(_TraceRow), _I64, C.POINTER(_I64)]),
+]
+
+_lib = None
+
+
+def load_library(path: str = _LIB_PATH) -> C.CDLL:
+    """Load libsamelda_cuda.so (raises if it was not built -- no fallback)."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(path):
+            raise ImportError(f"{path} is missing: run `python -m paper_1409_5402_b200.build` "
+                              "(there is no CPU fallback)")
+        lib = C.CDLL(path)
+        for name, res, args in SIGNATURES:
+            fn = getattr(lib, name)
+            fn.restype = res
+            fn.argtypes = args
+        _lib = lib
+    return _lib
+
+
+def _ptr(a: np.ndarray | None):
+    return None if a is None else a.ctypes.data_as(C.c_void_p)
+
+
+@dataclass
+class Corpus:
+    """CSR corpus (corpus.hpp:15-32)."""
+
+    doc_offsets: np.ndarray
+    word_ids: np.ndarray
+    counts: np.ndarray
+    n_words: int
+
+    def __post_init__(self):
+        self.doc_offsets = np.ascontiguousarray(self.doc_offsets, np.int64)
+        self.word_ids = np.ascontiguousarray(self.word_ids, np.int32)
+        self.counts = np.ascontiguousarray(self.counts, np.int32)
+        if len(self.word_ids) == 0:  # keep valid pointers for empty corpora
+            self._w_keep = np.zeros(1, np.int32)
+            self._c_keep = np.zeros(1, np.int32)
+
+    @classmethod
+    def of(cls, c) -> "Corpus":
+        return c if isinstance(c, Corpus) else cls(c.doc_offsets, c.word_ids, c.counts,
+                                                   int(c.n_words))
+
+    @property
+    def n_docs(self) -> int:
+        return len(self.doc_offsets) - 1
+
+    @property
+    def nnz(self) -> int:
+        return int(self.doc_offsets[-1])
+
+    @property
+    def n_tokens(self) -> int:
+        return int(self.counts.astype(np.int64).sum())
+
+    def doc_tokens(self) -> np.ndarray:
+        return np.add.reduceat(self.counts.astype(np.int64), self.doc_offsets[:-1]) * (
+            np.diff(self.doc_offsets) > 0) if self.nnz else np.zeros(self.n_docs, np.int64)
+
+    def _struct(self) -> _Corpus:
+        w = self.word_ids if len(self.word_ids) else self._w_keep
+        c = self.counts if len(self.counts) else self._c_keep
+        return _Corpus(self.doc_offsets.ctypes.data, w.ctypes.data, c.ctypes.data, self.n_docs,
+                       int(self.n_words))
+
+
+@dataclass
+class SamplerConfig:
+    """sampler.hpp:23-42 (same defaults); `mode` selects parity / expected counts."""
+
+    n_topics: int = 16
+    m: float = 100.0
+    schedule: str = "constant"
+    tau0: float = 1.0
+    gamma: float = 0.5
+    batch_fraction: float = 0.05
+    t_max: int = 0
+    inner_sweeps: int = 2
+    seed: int = 0
+    alpha: float = 0.1
+    beta: float = 0.01
+    n_threads: int = 1
+    init_noise: float = 0.1
+    mode: int = MODE_PARITY
+
+    def _struct(self) -> _Config:
+        if self.schedule not in SCHEDULES:
+            raise ConfigError(f"unknown schedule '{self.schedule}' "
+                              "(expected constant|linear|log|invlinear)")
+        return _Config(int(self.n_topics), float(self.m), SCHEDULES[self.schedule],
+                       float(self.tau0), float(self.gamma), float(self.batch_fraction),
+                       int(self.t_max), int(self.inner_sweeps), int(self.seed), float(self.alpha),
+                       float(self.beta), float(self.init_noise), int(self.mode))
+
+
+@dataclass
+class SampledCounts:
+    """sampler.hpp:50-68: theta B x K and phi W x K integer counts."""
+
+    doc_ids: np.ndarray
+    n_topics: int
+    n_words: int
+    m_t: float
+    theta_counts: np.ndarray
+    phi_counts: np.ndarray
+
+    def theta_hat(self, b, k):
+        return float(self.theta_counts[b, k]) / self.m_t
+
+    def phi_hat(self, k, w):
+        return float(self.phi_counts[w, k]) / self.m_t
+
+    def theta_total(self) -> int:
+        return int(self.theta_counts.sum())
+
+    def phi_total(self) -> int:
+        return int(self.phi_counts.sum())
+
+
+@dataclass
+class Model:
+    """model.hpp:40-47: phi K x W, theta D x K."""
+
+    n_topics: int
+    n_words: int
+    alpha: float
+    beta: float
+    phi: np.ndarray
+    theta: np.ndarray
+
+
+def init_model(n_topics, n_words, n_docs, alpha, beta) -> Model:
+    """model.cpp:41-52 (host fill; not on the hot path)."""
+    return Model(n_topics, n_words, alpha, beta,
+                 np.full((n_topics, n_words), 1.0 / n_words),
+                 np.full((n_docs, n_topics), alpha + 1.0 / n_topics))
+
+
+class Context:
+    """Owns one device context (streams, resident corpus/model, scratch)."""
+
+    def __init__(self, device: int = 0):
+        self.lib = load_library()
+        h = C.c_void_p()
+        rc = self.lib.samelda_cu_create(device, C.byref(h))
+        if rc:
+            raise CudaError(f"samelda_cu_create(device={device}) failed with code {rc}: "
+                            "no usable CUDA device (there is no CPU fallback)")
+        self.h = h
+        self.device = device
+
+    def close(self):
+        if getattr(self, "h", None):
+            self.lib.samelda_cu_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def check(self, rc: int):
+        if rc:
+            msg = self.lib.samelda_cu_last_error(self.h).decode(errors="replace")
+            raise _CODES.get(rc, SameldaError)(msg)
+
+    def set_stream(self, stream_handle: int | None):
+        self.check(self.lib.samelda_cu_set_stream(self.h, stream_handle))
+
+    def synchronize(self):
+        self.check(self.lib.samelda_cu_synchronize(self.h))
+
+    @property
+    def launches(self) -> int:
+        return int(self.lib.samelda_cu_launch_count(self.h))
+
+
+_default_ctx: Context | None = None
+
+
+def default_context() -> Context:
+    global _default_ctx
+    if _default_ctx is None:
+        _default_ctx = Context(0)
+    return _default_ctx
+
+
+def _f64(a):
+    return np.ascontiguousarray(a, np.float64)
+
+
+def _ids(doc_ids):
+    ids = np.ascontiguousarray(doc_ids, np.int32)
+    return ids if len(ids) else np.zeros(1, np.int32), len(ids)
+
+
+# --------------------------------------------------------------- per-call API
+
+def sddmm(theta_batch, phi, corpus, doc_ids, n_threads: int = 1, ctx: Context | None = None):
+    """sampler.cpp:88-123 on the device; returns mu aligned with the batch nonzeros."""
+    ctx = ctx or default_context()
+    corpus = Corpus.of(corpus)
+    theta_batch = _f64(theta_batch)
+    phi = _f64(phi)
+    ids, B = _ids(doc_ids)
+    K, W = phi.shape
+    Kt = theta_batch.shape[1] if theta_batch.ndim == 2 else K
+    if theta_batch.shape[0] != B if theta_batch.ndim == 2 else B != 0:
+        raise ConfigError("sddmm: theta rows must match the batch size")
+    nnz = int((corpus.doc_offsets[ids[:B].astype(np.int64) + 1] -
+               corpus.doc_offsets[ids[:B].astype(np.int64)]).sum()) if B else 0
+    mu = np.zeros(max(nnz, 1))
+    n = C.c_int64()
+    cs = corpus._struct()
+    tb = theta_batch if theta_batch.size else np.zeros(1)
+    ctx.check(ctx.lib.samelda_cu_sddmm(ctx.h, C.byref(cs), _ptr(tb), B, Kt, _ptr(phi), K, W,
+                                       _ptr(ids), _ptr(mu), len(mu), C.byref(n)))
+    return mu[:n.value]
+
+
+def sample_counts(theta_batch, phi, mu, corpus, doc_ids, m_t, seed, t, sweep=0, n_threads=1,
+                  ctx: Context | None = None) -> SampledCounts:
+    """sampler.cpp:125-195 on the device (reference-identical Poisson replicas)."""
+    ctx = ctx or default_context()
+    corpus = Corpus.of(corpus)
+    theta_batch = _f64(theta_batch)
+    phi = _f64(phi)
+    mu = _f64(mu)
+    ids, B = _ids(doc_ids)
+    K, W = phi.shape
+    Kt = theta_batch.shape[1] if theta_batch.ndim == 2 and theta_batch.size else K
+    tc = np.zeros(max(B * K, 1), np.int64)
+    pc = np.zeros(max(W * K, 1), np.int64)
+    cs = corpus._struct()
+    ctx.check(ctx.lib.samelda_cu_sample_counts(
+        ctx.h, C.byref(cs), _ptr(theta_batch if theta_batch.size else np.zeros(1)), B, Kt,
+        _ptr(phi), K, W, _ptr(mu if len(mu) else np.zeros(1)), len(mu), _ptr(ids), float(m_t),
+        int(seed) & (2**64 - 1), int(t), int(sweep), _ptr(tc), _ptr(pc)))
+    return SampledCounts(ids[:B].copy(), K, W, float(m_t), tc[:B * K].reshape(B, K),
+                         pc[:W * K].reshape(W, K))
+
+
+def expected_counts(theta_batch, phi, mu, corpus, doc_ids, m_t, ctx: Context | None = None):
+    """Deterministic factored path: (theta_expected B x K, phi_expected W x K), f64."""
+    ctx = ctx or default_context()
+    corpus = Corpus.of(corpus)
+    theta_batch = _f64(theta_batch)
+    phi = _f64(phi)
+    mu = _f64(mu)
+    ids, B = _ids(doc_ids)
+    K, W = phi.shape
+    tf = np.zeros(max(B * K, 1))
+    pf = np.zeros(max(W * K, 1))
+    cs = corpus._struct()
+    ctx.check(ctx.lib.samelda_cu_expected_counts(
+        ctx.h, C.byref(cs), _ptr(theta_batch if theta_batch.size else np.zeros(1)), B,
+        theta_batch.shape[1] if theta_batch.size else K, _ptr(phi), K, W,
+        _ptr(mu if len(mu) else np.zeros(1)), len(mu), _ptr(ids), float(m_t), _ptr(tf),
+        _ptr(pf)))
+    return tf[:B * K].reshape(B, K), pf[:W * K].reshape(W, K)
+
+
+def update_model(model: Model, counts, rho_t: float, ctx: Context | None = None,
+                 expected: bool = False) -> None:
+    """sampler.cpp:197-229 on the device; updates model.theta / model.phi in place."""
+    ctx = ctx or default_context()
+    if counts.n_topics != model.n_topics or counts.n_words != model.n_words:
+        raise ConfigError("update_model: counts are not shaped for this model")
+    model.theta = _f64(model.theta)
+    model.phi = _f64(model.phi)
+    ids, B = _ids(counts.doc_ids)
+    fn = ctx.lib.samelda_cu_update_model_expected if expected else ctx.lib.samelda_cu_update_model
+    dt = np.float64 if expected else np.int64
+    tc = np.ascontiguousarray(counts.theta_counts, dt).reshape(-1)
+    pc = np.ascontiguousarray(counts.phi_counts, dt).reshape(-1)
+    ctx.check(fn(ctx.h, _ptr(model.theta), model.theta.shape[0], _ptr(model.phi),
+                 model.n_topics, model.n_words, float(model.alpha), float(model.beta), _ptr(ids),
+                 B, _ptr(tc if len(tc) else np.zeros(1, dt)), _ptr(pc if len(pc) else
+                                                                    np.zeros(1, dt)),
+                 float(counts.m_t), float(rho_t)))
+
+
+def rho_schedule(t: int, tau0: float, gamma: float) -> float:
+    out = C.c_double()
+    rc = load_library().samelda_cu_rho_schedule(int(t), float(tau0), float(gamma), C.byref(out))
+    if rc:
+        raise _CODES[rc]("rho_schedule: argument out of range")
+    return out.value
+
+
+def anneal_m(schedule, t: int, t_max: int, m: float) -> float:
+    s = SCHEDULES[schedule] if isinstance(schedule, str) else int(schedule)
+    out = C.c_double()
+    rc = load_library().samelda_cu_anneal_m(s, int(t), int(t_max), float(m), C.byref(out))
+    if rc:
+        raise _CODES[rc]("anneal_m: t must be in [1, t_max]")
+    return out.value
+
+
+def parse_schedule(name: str) -> str:
+    if name not in SCHEDULES:
+        raise ConfigError(f"unknown schedule '{name}' (expected constant|linear|log|invlinear)")
+    return name
+
+
+def fold_in_theta(phi, words, counts, alpha, sweeps=50, ctx: Context | None = None):
+    """eval.cpp:19-73 on the device."""
+    ctx = ctx or default_context()
+    phi = _f64(phi)
+    K, W = phi.shape
+    w = np.ascontiguousarray(words, np.int32)
+    c = np.ascontiguousarray(counts, np.int32)
+    out = np.zeros(K)
+    ctx.check(ctx.lib.samelda_cu_fold_in_theta(
+        ctx.h, _ptr(phi), K, W, _ptr(w if len(w) else np.zeros(1, np.int32)),
+        _ptr(c if len(c) else np.zeros(1, np.int32)), len(w), float(alpha), int(sweeps),
+        _ptr(out)))
+    return out
+
+
+def perword_loglik(phi, test_corpus, alpha, seed, n_threads=1, ctx: Context | None = None):
+    """eval.cpp:75-159 on the device: held-out per-word log-likelihood (nats)."""
+    ctx = ctx or default_context()
+    phi = _f64(phi)
+    K, W = phi.shape
+    test = Corpus.of(test_corpus)
+    out = C.c_double()
+    cs = test._struct()
+    ctx.check(ctx.lib.samelda_cu_perword_loglik(ctx.h, _ptr(phi), K, W, C.byref(cs),
+                                                float(alpha), int(seed) & (2**64 - 1),
+                                                C.byref(out)))
+    return out.value
+
+
+# ----------------------------------------------------------------- trainer
+
+class MinibatchStream:
+    """corpus.cpp:252-285 (host, same Philox streams as the reference)."""
+
+    def __init__(self, n_docs: int, batch_fraction: float, seed: int):
+        self.lib = load_library()
+        h = C.c_void_p()
+        rc = self.lib.samelda_cu_batches_create(int(n_docs), float(batch_fraction),
+                                                int(seed) & (2**64 - 1), C.byref(h))
+        if rc:
+            raise ConfigError("minibatch_stream: batch_fraction must be in (0,1]")
+        self.h = h
+        self.batch_size = int(self.lib.samelda_cu_batches_size(h))
+        self._buf = np.zeros(max(self.batch_size, 1), np.int32)
+
+    def batches_per_pass(self) -> int:
+        return int(self.lib.samelda_cu_batches_per_pass(self.h))
+
+    def next(self) -> np.ndarray:
+        n = self.lib.samelda_cu_batches_next(self.h, _ptr(self._buf))
+        return self._buf[:n].copy()
+
+    def __del__(self):
+        try:
+            self.lib.samelda_cu_batches_destroy(self.h)
+        except Exception:
+            pass
+
+
+class Trainer:
+    """Device-resident train() split at the period (sampler.cpp:269-353)."""
+
+    def __init__(self, corpus, config: SamplerConfig, ctx: Context | None = None):
+        self.ctx = ctx or default_context()
+        self.corpus = Corpus.of(corpus)
+        self.config = config
+        self._cs = self.corpus._struct()
+        self._cfg = config._struct()
+        self.ctx.check(self.ctx.lib.samelda_cu_train_begin(self.ctx.h, C.byref(self._cs),
+                                                           C.byref(self._cfg)))
+
+    def set_heldout(self, heldout, seed: int | None = None):
+        self.heldout = Corpus.of(heldout)
+        self._hs = self.heldout._struct()
+        self.ctx.check(self.ctx.lib.samelda_cu_heldout(
+            self.ctx.h, C.byref(self._hs),
+            int(self.config.seed if seed is None else seed) & (2**64 - 1)))
+
+    def period(self, doc_ids, t, m_t, rho_t):
+        ids, B = _ids(doc_ids)
+        self.ctx.check(self.ctx.lib.samelda_cu_period(self.ctx.h, _ptr(ids), B, int(t),
+                                                      float(m_t), float(rho_t)))
+
+    def period_sample(self, doc_ids, t, m_t):
+        ids, B = _ids(doc_ids)
+        self.ctx.check(self.ctx.lib.samelda_cu_period_sample(self.ctx.h, _ptr(ids), B, int(t),
+                                                             float(m_t)))
+
+    def period_update(self, rho_t):
+        self.ctx.check(self.ctx.lib.samelda_cu_period_update(self.ctx.h, float(rho_t)))
+
+    def phi_counts_device(self):
+        """(device pointer, n elements, element bytes, is_float) of the phi count buffer."""
+        p, n, eb, fl = C.c_void_p(), C.c_int64(), C.c_int32(), C.c_int32()
+        self.ctx.check(self.ctx.lib.samelda_cu_phi_counts_device(
+            self.ctx.h, C.byref(p), C.byref(n), C.byref(eb), C.byref(fl)))
+        return p.value, n.value, eb.value, bool(fl.value)
+
+    def count_totals(self):
+        a, b = C.c_int64(), C.c_int64()
+        self.ctx.check(self.ctx.lib.samelda_cu_count_totals(self.ctx.h, C.byref(a), C.byref(b)))
+        return a.value, b.value
+
+    def batch_theta(self, B: int) -> np.ndarray:
+        out = np.zeros(max(B * self.config.n_topics, 1))
+        self.ctx.check(self.ctx.lib.samelda_cu_batch_theta(self.ctx.h, _ptr(out), len(out)))
+        return out[:B * self.config.n_topics].reshape(B, self.config.n_topics)
+
+    def evaluate(self) -> float:
+        out = C.c_double()
+        self.ctx.check(self.ctx.lib.samelda_cu_evaluate(self.ctx.h, C.byref(out)))
+        return out.value
+
+    def model(self, with_theta: bool = True) -> Model:
+        K, W, D = self.config.n_topics, self.corpus.n_words, self.corpus.n_docs
+        phi = np.zeros(K * W)
+        theta = np.zeros(D * K) if with_theta else None
+        self.ctx.check(self.ctx.lib.samelda_cu_model_download(self.ctx.h, _ptr(phi),
+                                                              _ptr(theta)))
+        return Model(K, W, self.config.alpha, self.config.beta, phi.reshape(K, W),
+                     theta.reshape(D, K) if theta is not None else None)
+
+
+def train(corpus, config: SamplerConfig, heldout=None, eval_every: int = 0,
+          ctx: Context | None = None):
+    """sampler.cpp:269-353 end to end on the device -> (Model, trace rows)."""
+    ctx = ctx or default_context()
+    corpus = Corpus.of(corpus)
+    cs = corpus._struct()
+    cfg = config._struct()
+    hs = Corpus.of(heldout)._struct() if heldout is not None else None
+    K, W, D = config.n_topics, corpus.n_words, corpus.n_docs
+    phi = np.zeros(max(K * W, 1))
+    theta = np.zeros(max(D * K, 1))
+    cap = max(int(config.t_max), 1)
+    rows = (_TraceRow * cap)()
+    n = C.c_int64()
+    ctx.check(ctx.lib.samelda_cu_train(ctx.h, C.byref(cs), C.byref(cfg),
+                                       C.byref(hs) if hs is not None else None, int(eval_every),
+                                       _ptr(phi), _ptr(theta), rows, cap, C.byref(n)))
+    trace = [dict(t=rows[i].t, passes=rows[i].passes, samples_per_word=rows[i].samples_per_word,
+                  ll=rows[i].ll, wall_seconds=rows[i].wall_seconds, m_t=rows[i].m_t)
+             for i in range(n.value)]
+    return Model(K, W, config.alpha, config.beta, phi[:K * W].reshape(K, W),
+                 theta[:D * K].reshape(D, K)), trace

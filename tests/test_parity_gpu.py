@@ -1,0 +1,371 @@
+"""CUDA path (through the C ABI) against the reference's golden fixtures and the
+oracle on seeded inputs.  Bar: bit-exact for counts, ids and the parity-mode
+model (f64, reference rounding); 1e-12 relative for ll; 1e-5 relative for the
+expected-count path (north_star).  Also the reference's own statistical and
+error-convention tests (test_sampler.cpp, test_eval.cpp) ported verbatim."""
+from __future__ import annotations
+
+import hashlib
+import json
+import math
+import os
+
+import numpy as np
+import pytest
+
+from oracle import CorpusArrays, TrainConfig
+
+pytestmark = pytest.mark.gpu
+
+S = None
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _samelda(cuda_ctx):
+    global S
+    from paper_1409_5402_b200 import samelda
+    S = samelda
+    yield
+
+
+def tiny(n_docs, n_words, cells):
+    """test_sampler.cpp:18-42 make_corpus from (doc, word, count) triplets."""
+    offs = np.zeros(n_docs + 1, np.int64)
+    words, counts = [], []
+    for d, w, c in cells:
+        offs[d + 1:] += 1
+        words.append(w)
+        counts.append(c)
+    return CorpusArrays(offs, np.array(words, np.int32), np.array(counts, np.int32), n_words)
+
+
+def all_docs(c):
+    return np.arange(c.n_docs, dtype=np.int32)
+
+
+# ------------------------------------------------------------ golden parity
+
+def test_sddmm_bit_exact(golden, small):
+    tb = golden["small_theta"][golden["small_batch"]]
+    mu = S.sddmm(tb, golden["small_phi"], small, golden["small_batch"])
+    np.testing.assert_array_equal(mu, golden["small_mu"])
+
+
+def test_sample_counts_bit_exact(golden, small):
+    batch, phi = golden["small_batch"], golden["small_phi"]
+    tb = golden["small_theta"][batch]
+    for i, (m_t, seed, (t, sweep)) in enumerate(zip(golden["sample_m_t"], golden["sample_seed"],
+                                                    golden["sample_t_sweep"])):
+        sc = S.sample_counts(tb, phi, golden["small_mu"], small, batch, m_t, int(seed), int(t),
+                             int(sweep))
+        np.testing.assert_array_equal(sc.theta_counts, golden[f"small_tc{i}"])
+        np.testing.assert_array_equal(sc.phi_counts, golden[f"small_pc{i}"])
+        assert sc.theta_total() == sc.phi_total()
+
+
+def test_sample_counts_ptrs_bit_exact(golden, small):
+    batch, phi = golden["small_batch"], golden["small_phi"]
+    big = golden["small_theta"][batch] * 50.0
+    mu = S.sddmm(big, phi, small, batch)
+    sc = S.sample_counts(big, phi, mu, small, batch, 2000.0, 5, 1, 0)
+    np.testing.assert_array_equal(sc.theta_counts, golden["small_big_tc"])
+    np.testing.assert_array_equal(sc.phi_counts, golden["small_big_pc"])
+
+
+def test_update_model_bit_exact(golden):
+    batch, theta, phi = golden["small_batch"], golden["small_theta"], golden["small_phi"]
+    K, W = phi.shape
+    for i, m_t in enumerate(golden["sample_m_t"]):
+        model = S.Model(K, W, 0.1, 0.01, phi.copy(), theta.copy())
+        counts = S.SampledCounts(batch, K, W, float(m_t), golden[f"small_tc{i}"],
+                                 golden[f"small_pc{i}"])
+        S.update_model(model, counts, 0.37 + 0.2 * i)
+        np.testing.assert_array_equal(model.theta, golden[f"small_upd_theta{i}"])
+        np.testing.assert_array_equal(model.phi, golden[f"small_upd_phi{i}"])
+
+
+def test_eval_matches_reference(golden, small):
+    ll = S.perword_loglik(small.phi_true, small, 0.1, 3)
+    assert ll == pytest.approx(golden["small_ll_true"][0], rel=1e-12, abs=0)
+    ll2 = S.perword_loglik(golden["small_phi"], small, 0.1, 12345)
+    assert ll2 == pytest.approx(golden["small_ll_rand"][0], rel=1e-12, abs=0)
+    w0 = small.word_ids[small.doc_offsets[0]:small.doc_offsets[1]]
+    c0 = small.counts[small.doc_offsets[0]:small.doc_offsets[1]]
+    np.testing.assert_allclose(S.fold_in_theta(small.phi_true, w0, c0, 0.1, 50),
+                               golden["small_fold_in"], rtol=1e-12, atol=0)
+    np.testing.assert_allclose(S.fold_in_theta(golden["small_phi"], w0, c0, 0.3, 5),
+                               golden["small_fold_in_5"], rtol=1e-12, atol=0)
+
+
+def _cfg_from(arr, cls):
+    n_topics, m, sched, t_max, bf, inner, seed, noise = arr
+    return cls(n_topics=int(n_topics), m=float(m),
+               schedule=["constant", "linear", "log", "invlinear"][int(sched)], t_max=int(t_max),
+               batch_fraction=float(bf), inner_sweeps=int(inner), seed=int(seed),
+               init_noise=float(noise))
+
+
+@pytest.mark.parametrize("name", ["train_a", "train_b", "train_c"])
+def test_train_bit_exact(golden, small_split, name):
+    tr, te = small_split
+    model, trace = S.train(tr, _cfg_from(golden[f"{name}_cfg"], S.SamplerConfig), te, 2)
+    np.testing.assert_array_equal(model.phi, golden[f"{name}_phi"])
+    np.testing.assert_array_equal(model.theta, golden[f"{name}_theta"])
+    np.testing.assert_allclose([r["ll"] for r in trace], golden[f"{name}_ll"], rtol=1e-12, atol=0)
+    np.testing.assert_array_equal([r["samples_per_word"] for r in trace], golden[f"{name}_spw"])
+    np.testing.assert_array_equal([r["passes"] for r in trace], golden[f"{name}_passes"])
+
+
+def test_c1_train_matches_reference(port):
+    """BASELINE config 0 end to end: 20 full-batch periods, K=32, m=10."""
+    rec = json.load(open(os.path.join(os.path.dirname(__file__), "golden", "c1_train.json")))
+    c = rec["corpus"]
+    g = port.make_corpus(c["n_docs"], c["n_words"], c["n_topics"], c["len_mean"], c["seed"])
+    tr, te = port.split_holdout(g, 0.1, 1)
+    cfg = S.SamplerConfig(**rec["config"])
+    model, trace = S.train(tr, cfg, te, 5)
+    got = [r["ll"] for r in trace]
+    want = [float.fromhex(r["ll"]) for r in rec["trace"]]
+    np.testing.assert_allclose(got, want, rtol=1e-12, atol=0)
+    assert [r["samples_per_word"].hex() for r in trace] == [r["samples_per_word"]
+                                                           for r in rec["trace"]]
+    digest = hashlib.sha256(np.ascontiguousarray(model.phi).tobytes()).hexdigest()
+    assert digest == rec["phi_digest"]
+
+
+def test_trainer_periods_equal_composed_calls(port, small_split):
+    """samelda_cu_period == sddmm -> sample_counts -> update_model composed by hand."""
+    tr, _ = small_split
+    cfg = S.SamplerConfig(n_topics=4, m=7.0, t_max=3, batch_fraction=0.3, seed=9)
+    trainer = S.Trainer(tr, cfg)
+    model = trainer.model()
+    stream = S.MinibatchStream(tr.n_docs, cfg.batch_fraction, cfg.seed)
+    for t in range(3):
+        batch = stream.next()
+        m_t, rho = S.anneal_m("constant", t + 1, 3, cfg.m), S.rho_schedule(t, 1.0, 0.5)
+        trainer.period(batch, t, m_t, rho)
+        tb = model.theta[batch]
+        for sweep in range(cfg.inner_sweeps):
+            mu = S.sddmm(tb, model.phi, tr, batch)
+            counts = S.sample_counts(tb, model.phi, mu, tr, batch, m_t, cfg.seed, t, sweep)
+            tb = counts.theta_counts / m_t + cfg.alpha
+        S.update_model(model, counts, rho)
+        assert trainer.count_totals() == (counts.theta_total(), counts.phi_total())
+        dev = trainer.model()
+        np.testing.assert_array_equal(dev.phi, model.phi)
+        np.testing.assert_array_equal(dev.theta, model.theta)
+
+
+def test_expected_counts_match_oracle(port, golden, small):
+    batch, phi = golden["small_batch"], golden["small_phi"]
+    tb = golden["small_theta"][batch]
+    mu = golden["small_mu"]
+    tf, pf = S.expected_counts(tb, phi, mu, small, batch, 3.0)
+    otf, opf = port.expected_counts(tb, phi, mu, small, batch, 3.0)
+    np.testing.assert_allclose(tf, otf, rtol=1e-12, atol=1e-300)
+    np.testing.assert_allclose(pf, opf, rtol=1e-12, atol=1e-300)
+
+
+def test_expected_train_within_1e5(port, small_split):
+    tr, te = small_split
+    cfg = S.SamplerConfig(n_topics=4, m=10.0, t_max=6, batch_fraction=0.5, seed=3,
+                          mode=S.MODE_EXPECTED)
+    model, trace = S.train(tr, cfg, te, 3)
+    ocfg = TrainConfig(n_topics=4, m=10.0, t_max=6, batch_fraction=0.5, seed=3)
+    ophi, otheta, otrace = port.train(tr, ocfg, te, 3, expected=True)
+    np.testing.assert_allclose(model.phi, ophi, rtol=1e-5, atol=1e-12)
+    np.testing.assert_allclose(model.theta, otheta, rtol=1e-5, atol=1e-12)
+    np.testing.assert_allclose([r["ll"] for r in trace], [r["ll"] for r in otrace], rtol=1e-9)
+
+
+def test_random_larger_case_bit_exact(port):
+    """K=256 (8 topics per lane), multi-chunk docs, random theta/phi: counts bit-exact."""
+    g = port.make_corpus(300, 700, 8, 120.0, 21)
+    rng = np.random.default_rng(5)
+    K = 256
+    theta = rng.gamma(0.3, 1.0, size=(g.n_docs, K)) + 1e-3
+    phi = rng.gamma(0.2, 1.0, size=(K, g.n_words)) + 1e-9
+    phi /= phi.sum(1, keepdims=True)
+    batch = rng.permutation(g.n_docs)[:211].astype(np.int32)
+    tb = theta[batch]
+    mu = S.sddmm(tb, phi, g, batch)
+    np.testing.assert_array_equal(mu, port.sddmm(tb, phi, g, batch))
+    sc = S.sample_counts(tb, phi, mu, g, batch, 100.0, 77, 4, 1)
+    otc, opc = port.sample_counts(tb, phi, mu, g, batch, 100.0, 77, 4, 1)
+    np.testing.assert_array_equal(sc.theta_counts, otc)
+    np.testing.assert_array_equal(sc.phi_counts, opc)
+    # per-doc and per-word integer totals
+    np.testing.assert_array_equal(sc.theta_counts.sum(1), otc.sum(1))
+    np.testing.assert_array_equal(sc.phi_counts.sum(1), opc.sum(1))
+
+
+@pytest.mark.parametrize("K", [1, 3, 33, 100, 300, 1024])
+def test_odd_topic_counts_bit_exact(port, K):
+    g = port.make_corpus(40, 90, 5, 30.0, 3 + K)
+    rng = np.random.default_rng(K)
+    theta = rng.uniform(0.01, 1.0, size=(g.n_docs, K))
+    phi = rng.uniform(0.0, 1.0, size=(K, g.n_words))
+    phi /= phi.sum(1, keepdims=True)
+    batch = all_docs(g)
+    mu = S.sddmm(theta, phi, g, batch)
+    np.testing.assert_array_equal(mu, port.sddmm(theta, phi, g, batch))
+    sc = S.sample_counts(theta, phi, mu, g, batch, 12.5, 3, 2, 0)
+    otc, opc = port.sample_counts(theta, phi, mu, g, batch, 12.5, 3, 2, 0)
+    np.testing.assert_array_equal(sc.theta_counts, otc)
+    np.testing.assert_array_equal(sc.phi_counts, opc)
+    ll = S.perword_loglik(phi, g, 0.1, 4)
+    assert ll == pytest.approx(port.perword_loglik(phi, g, 0.1, 4), rel=1e-12, abs=0)
+
+
+# -------------------------------------- reference unit tests (test_sampler.cpp)
+
+def test_sddmm_unit_theta_row():
+    c = tiny(1, 2, [(0, 1, 1)])
+    mu = S.sddmm(np.array([[1.0, 0.0]]), np.array([[0.3, 0.7], [0.5, 0.5]]), c, [0])
+    assert len(mu) == 1 and mu[0] == pytest.approx(0.7, rel=1e-15)
+
+
+def test_sddmm_empty_and_shape_errors():
+    c = tiny(2, 3, [(0, 1, 4)])
+    assert len(S.sddmm(np.zeros((0, 2)), np.full((2, 3), 0.5), c, [])) == 0
+    c1 = tiny(1, 3, [(0, 0, 1)])
+    with pytest.raises(S.ConfigError):
+        S.sddmm(np.zeros((1, 2)), np.full((3, 3), 0.5), c1, [0])
+
+
+def test_single_topic_scaled_poisson():
+    # test_sampler.cpp:160-179
+    c = tiny(1, 2, [(0, 0, 2), (0, 1, 1)])
+    theta, phi, m_t = np.ones((1, 1)), np.full((1, 2), 0.5), 4.0
+    mu = S.sddmm(theta, phi, c, [0])
+    vals = [S.sample_counts(theta, phi, mu, c, [0], m_t, r, 0, 0).theta_hat(0, 0)
+            for r in range(2000)]
+    assert abs(np.mean(vals) - 3.0) < 3.0 * math.sqrt(3.0 / m_t / len(vals))
+
+
+def test_large_m_recovers_responsibilities():
+    c = tiny(1, 1, [(0, 0, 1)])
+    theta, phi = np.ones((1, 2)), np.array([[0.2], [0.8]])
+    mu = S.sddmm(theta, phi, c, [0])
+    sc = S.sample_counts(theta, phi, mu, c, [0], 1e4, 9, 0, 0)
+    assert sc.theta_hat(0, 0) == pytest.approx(0.2, rel=0.02)
+    assert sc.theta_hat(0, 1) == pytest.approx(0.8, rel=0.02)
+
+
+def test_poisson_splitting():
+    # test_sampler.cpp:262-282 (fewer runs)
+    c = tiny(1, 1, [(0, 0, 2)])
+    theta, phi, m_t = np.ones((1, 4)), np.full((4, 1), 0.25), 5.0
+    mu = S.sddmm(theta, phi, c, [0])
+    tot = np.array([S.sample_counts(theta, phi, mu, c, [0], m_t, r, 0, 0).theta_total()
+                    for r in range(3000)], dtype=float)
+    rate = m_t * 2.0
+    assert abs(tot.mean() - rate) < 3.0 * math.sqrt(rate / len(tot))
+
+
+def test_vanishing_mu_uniform_fallback():
+    c = tiny(1, 1, [(0, 0, 4)])
+    theta, phi = np.zeros((1, 2)), np.full((2, 1), 0.5)
+    mu = S.sddmm(theta, phi, c, [0])
+    assert mu[0] == 0.0
+    sums = np.zeros(2)
+    for r in range(1000):
+        sc = S.sample_counts(theta, phi, mu, c, [0], 50.0, r, 0, 0)
+        sums += [sc.theta_hat(0, 0), sc.theta_hat(0, 1)]
+    assert np.all(np.abs(sums / 1000 - 2.0) < 3.0 * math.sqrt(2.0 / 50.0 / 1000) + 1e-9)
+
+
+def test_nonfinite_rate_raises_numerical_error():
+    c = tiny(1, 1, [(0, 0, 1)])
+    theta = np.array([[np.inf, 1.0]])
+    with pytest.raises(S.NumericalError):
+        S.sample_counts(theta, np.full((2, 1), 0.5), [1.0], c, [0], 1.0, 1, 0, 0)
+
+
+def test_sample_counts_config_errors():
+    c = tiny(1, 1, [(0, 0, 1)])
+    with pytest.raises(S.ConfigError):
+        S.sample_counts(np.ones((1, 2)), np.full((2, 1), 0.5), [1.0], c, [0], 0.0, 1, 0, 0)
+    with pytest.raises(S.ConfigError):
+        S.sample_counts(np.ones((1, 2)), np.full((2, 1), 0.5), [1.0, 2.0], c, [0], 1.0, 1, 0, 0)
+
+
+def test_update_model_known_answers():
+    # test_sampler.cpp:319-380
+    model = S.init_model(2, 3, 1, 0.1, 0.01)
+    pc = np.zeros((3, 2), np.int64)
+    pc[0, 0], pc[1, 0] = 2, 6
+    S.update_model(model, S.SampledCounts(np.array([0], np.int32), 2, 3, 2.0,
+                                          np.array([[3, 5]]), pc), 1.0)
+    assert model.theta[0, 0] == pytest.approx(1.6, rel=1e-12)
+    assert model.theta[0, 1] == pytest.approx(2.6, rel=1e-12)
+    total = 4.0 + 3 * 0.01
+    assert model.phi[0, 0] == pytest.approx(1.01 / total, rel=1e-12)
+    assert model.phi[0, 2] == pytest.approx(0.01 / total, rel=1e-12)
+    assert np.allclose(model.phi[1], 1.0 / 3, rtol=1e-12)
+    m2 = S.init_model(1, 2, 1, 0.1, 0.01)
+    m2.phi[0] = [0.6, 0.4]
+    cnt = S.SampledCounts(np.array([0], np.int32), 1, 2, 1.0, np.array([[0]]),
+                          np.array([[1000000000000], [4000000000000]]))
+    S.update_model(m2, cnt, 0.5)
+    assert m2.phi[0, 0] == pytest.approx(0.4, rel=1e-12)
+    for bad in (0.0, 1.5):
+        with pytest.raises(S.ConfigError):
+            S.update_model(m2, cnt, bad)
+
+
+def test_phi_rows_stochastic_after_training(port):
+    g = port.make_corpus(30, 8, 3, 6.0, 77)
+    model, _ = S.train(g, S.SamplerConfig(n_topics=3, m=7.5, t_max=25, batch_fraction=0.2,
+                                          seed=5))
+    assert np.all(model.phi >= 0)
+    np.testing.assert_allclose(model.phi.sum(1), 1.0, atol=1e-6)
+
+
+def test_zero_periods_returns_init(port):
+    g = port.make_corpus(10, 6, 2, 5.0, 12)
+    model, trace = S.train(g, S.SamplerConfig(n_topics=2, t_max=0))
+    assert trace == []
+    np.testing.assert_allclose(model.phi, 1.0 / 6, rtol=1e-12)
+
+
+def test_training_deterministic(port):
+    g = port.make_corpus(60, 20, 3, 10.0, 44)
+    tr, te = port.split_holdout(g, 0.2, 9)
+    cfg = S.SamplerConfig(n_topics=3, m=20.0, t_max=12, batch_fraction=0.25, seed=31)
+    a, ta = S.train(tr, cfg, te, 4)
+    b, tb = S.train(tr, cfg, te, 4)
+    assert [r["ll"] for r in ta] == [r["ll"] for r in tb]
+    np.testing.assert_array_equal(a.phi, b.phi)
+
+
+def test_config_validation():
+    g = tiny(2, 2, [(0, 0, 1), (1, 1, 1)])
+    for kw in [dict(n_topics=0), dict(m=-1.0), dict(tau0=0.5), dict(gamma=0.3),
+               dict(batch_fraction=0.0), dict(t_max=-1), dict(inner_sweeps=0),
+               dict(inner_sweeps=256), dict(alpha=0.0), dict(init_noise=-1.0)]:
+        with pytest.raises(S.ConfigError):
+            S.train(g, S.SamplerConfig(**{"n_topics": 2, "t_max": 1, **kw}))
+
+
+# ------------------------------------------------ reference eval tests
+
+def test_fold_in_known_answers():
+    assert S.fold_in_theta(np.full((1, 4), 0.25), [0, 2], [3, 1], 0.1)[0] == pytest.approx(1.0)
+    th = S.fold_in_theta(np.array([[1.0, 0.0], [0.0, 1.0]]), [0], [5], 1e-9)
+    assert th[0] == pytest.approx(1.0, rel=1e-6) and abs(th[1]) < 1e-6
+    np.testing.assert_allclose(S.fold_in_theta(np.full((4, 3), 1 / 3), [], [], 0.1), 0.25)
+
+
+def test_uniform_model_scores_minus_log_w(port):
+    g = port.make_corpus(15, 8, 2, 12.0, 71)
+    assert S.perword_loglik(np.full((1, 8), 0.125), g, 0.1, 3) == pytest.approx(-math.log(8.0),
+                                                                                  rel=1e-12)
+
+
+def test_eval_errors(port):
+    g = port.make_corpus(5, 8, 2, 12.0, 71)
+    with pytest.raises(S.ConfigError):
+        S.perword_loglik(np.full((1, 9), 1 / 9), g, 0.1, 3)
+    with pytest.raises(S.NumericalError):
+        S.perword_loglik(np.zeros((1, 8)), g, 0.1, 3)
