@@ -177,6 +177,16 @@ int samelda_cu_period_update(samelda_cu_ctx* ctx, double rho_t);
  * elem_bytes is 8 (u64 parity counts or f64 expected counts); is_float 1 for f64. */
 int samelda_cu_phi_counts_device(samelda_cu_ctx* ctx, void** ptr, int64_t* n_elems,
                                  int32_t* elem_bytes, int32_t* is_float);
+/* Doc-sharded runs: this context holds documents [doc_base, doc_base + D)
+ * of the global corpus under local ids 0..D-1; Philox stream keys use the
+ * global id, so every shard draws exactly what a single GPU would. */
+int samelda_cu_set_doc_base(samelda_cu_ctx* ctx, int64_t doc_base);
+/* CUDA-event timing of the period kernels (0 sample, 1 sddmm, 2 M-step). */
+int samelda_cu_profile(samelda_cu_ctx* ctx, int32_t enable);
+/* ms_out[3] summed event time, launches_out[3] launches timed; batch nonzeros
+ * and docs seen by the timed sample launches.  Resets the accumulators. */
+int samelda_cu_profile_read(samelda_cu_ctx* ctx, double* ms_out, int64_t* launches_out,
+                            int64_t* nnz_sampled, int64_t* docs_sampled);
 /* copy the batch theta rows (B x K, f64, batch order) of the last period */
 int samelda_cu_batch_theta(samelda_cu_ctx* ctx, double* out, int64_t cap);
 /* sums of the last sweep's integer theta and phi counts (mass balance) */

@@ -24,7 +24,9 @@ UNITS = {
     "kernels.cu": ["-fmad=false"],
     "fast_kernels.cu": [],
     "capi.cu": [],
+    "synth.cpp": [],
 }
+GXX = ["-O3", "-std=c++17", "-fPIC", "-pthread", "-I", CSRC, "-I", os.path.join(ROOT, "include")]
 
 
 def nvcc() -> str:
@@ -50,15 +52,18 @@ def build(verbose: bool = False, force: bool = False) -> str:
         src = os.path.join(CSRC, unit)
         if not os.path.exists(src):
             continue
-        obj = os.path.join(BUILD, unit.replace(".cu", ".o"))
+        obj = os.path.join(BUILD, os.path.splitext(unit)[0] + ".o")
         objs.append(obj)
         if force or _stale(obj, [src] + headers):
-            cmd = [nvcc(), *ARCH, *COMMON, *flags, "-c", src, "-o", obj]
+            if unit.endswith(".cpp"):
+                cmd = [os.environ.get("CXX", "g++"), *GXX, *flags, "-c", src, "-o", obj]
+            else:
+                cmd = [nvcc(), *ARCH, *COMMON, *flags, "-c", src, "-o", obj]
             if verbose:
                 print(" ".join(cmd), flush=True)
             subprocess.run(cmd, check=True)
     if force or _stale(LIB, objs):
-        cmd = [nvcc(), *ARCH, "-shared", "-o", LIB, *objs]
+        cmd = [nvcc(), *ARCH, "-shared", "-o", LIB, *objs, "-lpthread"]
         if verbose:
             print(" ".join(cmd), flush=True)
         subprocess.run(cmd, check=True)

@@ -259,6 +259,34 @@ struct samelda_cu_ctx {
   int64_t W = 0, D = 0;
   DevBuf theta, phi;  // D x K, W x K
 
+  // doc-sharded runs: global id of local doc 0 (Philox keys use global ids)
+  int64_t doc_base = 0;
+
+  // optional per-kernel CUDA-event timing (bench roofline)
+  bool profile = false;
+  enum { kSample = 0, kSddmm = 1, kMstep = 2, kKinds = 3 };
+  std::vector<std::pair<cudaEvent_t, cudaEvent_t>> events[kKinds];
+  size_t events_used[kKinds] = {0, 0, 0};
+  int64_t prof_nnz = 0, prof_docs = 0;
+
+  void tick(int kind, bool start) {
+    if (!profile) return;
+    auto& v = events[kind];
+    size_t& used = events_used[kind];
+    if (start) {
+      if (used == v.size()) {
+        cudaEvent_t a, b;
+        ck(cudaEventCreate(&a), "event");
+        ck(cudaEventCreate(&b), "event");
+        v.emplace_back(a, b);
+      }
+      ck(cudaEventRecord(v[used].first, stream), "event record");
+    } else {
+      ck(cudaEventRecord(v[used].second, stream), "event record");
+      ++used;
+    }
+  }
+
   // per-period state
   int64_t B = 0, nnzB = 0;
   double m_t = 1.0;
@@ -273,6 +301,11 @@ struct samelda_cu_ctx {
   int64_t h_cap = 0;
 
   ~samelda_cu_ctx() {
+    for (auto& v : events)
+      for (auto& e : v) {
+        cudaEventDestroy(e.first);
+        cudaEventDestroy(e.second);
+      }
     if (h_batch) cudaFreeHost(h_batch);
     if (h_prefix) cudaFreeHost(h_prefix);
     if (own_stream) cudaStreamDestroy(own_stream);
@@ -329,6 +362,7 @@ struct samelda_cu_ctx {
     bv.batch_prefix = dp;
     bv.B = B_;
     bv.nnz = h_prefix[B_];
+    bv.doc_base = 0;
     return bv;
   }
 
@@ -348,22 +382,30 @@ struct samelda_cu_ctx {
   void sample_sweep(const scu::BatchView& bv, const double* theta_b, const double* phi_wk,
                     const double* mu_d, int K_, int64_t W_, double m_t_, uint64_t seed,
                     int64_t t, int sweep, int mode) {
+    if (profile) {
+      prof_nnz += bv.nnz;
+      prof_docs += bv.B;
+    }
     if (mode == SAMELDA_CU_MODE_EXPECTED) {
       double* tf_ = ensure<double>(tf, bv.B * K_);
       double* pf_ = ensure<double>(pf, W_ * K_);
       ck(cudaMemsetAsync(tf_, 0, sizeof(double) * std::max<int64_t>(bv.B * K_, 1), stream), "zero tf");
       ck(cudaMemsetAsync(pf_, 0, sizeof(double) * std::max<int64_t>(W_ * K_, 1), stream), "zero pf");
+      tick(kSample, true);
       launches += scu::launch_sample(bv, theta_b, phi_wk, mu_d, K_, m_t_, seed,
                                      static_cast<uint32_t>(t), static_cast<uint32_t>(sweep), mode,
                                      nullptr, nullptr, tf_, pf_, d_err(), stream);
+      tick(kSample, false);
     } else {
       auto* tc_ = ensure<unsigned long long>(tc, bv.B * K_);
       auto* pc_ = ensure<unsigned long long>(pc, W_ * K_);
       ck(cudaMemsetAsync(tc_, 0, sizeof(unsigned long long) * std::max<int64_t>(bv.B * K_, 1), stream), "zero tc");
       ck(cudaMemsetAsync(pc_, 0, sizeof(unsigned long long) * std::max<int64_t>(W_ * K_, 1), stream), "zero pc");
+      tick(kSample, true);
       launches += scu::launch_sample(bv, theta_b, phi_wk, mu_d, K_, m_t_, seed,
                                      static_cast<uint32_t>(t), static_cast<uint32_t>(sweep), mode,
                                      tc_, pc_, nullptr, nullptr, d_err(), stream);
+      tick(kSample, false);
     }
   }
 
@@ -797,7 +839,8 @@ int samelda_cu_period_sample(samelda_cu_ctx* ctx, const int32_t* doc_ids, int64_
     const samelda_cu_config& c = ctx->cfg;
     const int K = ctx->K;
     cudaStream_t st = ctx->stream;
-    const scu::BatchView bv = ctx->upload_batch(ctx->train, doc_ids, B);
+    scu::BatchView bv = ctx->upload_batch(ctx->train, doc_ids, B);
+    bv.doc_base = ctx->doc_base;
     ctx->B = B;
     ctx->nnzB = bv.nnz;
     ctx->m_t = m_t;
@@ -806,7 +849,9 @@ int samelda_cu_period_sample(samelda_cu_ctx* ctx, const int32_t* doc_ids, int64_
     ctx->reset_err();
     ctx->launches += scu::launch_gather_theta(ctx->theta.as<double>(), bv.batch_docs, B, K, thb, st);
     for (int64_t sweep = 0; sweep < c.inner_sweeps; ++sweep) {
+      ctx->tick(samelda_cu_ctx::kSddmm, true);
       ctx->launches += scu::launch_sddmm(bv, thb, ctx->phi.as<double>(), K, mu, st);
+      ctx->tick(samelda_cu_ctx::kSddmm, false);
       ctx->sample_sweep(bv, thb, ctx->phi.as<double>(), mu, K, ctx->W, m_t, c.seed, t,
                         static_cast<int>(sweep), c.mode);
       if (sweep + 1 < c.inner_sweeps) {
@@ -835,11 +880,13 @@ int samelda_cu_period_update(samelda_cu_ctx* ctx, double rho_t) {
     const auto* pcu = f ? nullptr : ctx->pc.as<unsigned long long>();
     const double* tcf = f ? ctx->tf.as<double>() : nullptr;
     const double* pcf = f ? ctx->pf.as<double>() : nullptr;
+    ctx->tick(samelda_cu_ctx::kMstep, true);
     ctx->launches += scu::launch_theta_persist(tcu, tcf, ctx->batch.as<int32_t>(), ctx->B, K, ctx->m_t, c.alpha,
                                                ctx->theta.as<double>(), st);
     ctx->launches += scu::launch_phi_mstep(pcu, pcf, ctx->W, K, ctx->m_t, c.beta, rho_t, ctx->phi.as<double>(),
                                            ensure<double>(ctx->cand, ctx->W * K), ensure<double>(ctx->totals, K),
                                            ctx->d_err(), st);
+    ctx->tick(samelda_cu_ctx::kMstep, false);
     ctx->check_err("period");
   });
 }
@@ -849,6 +896,42 @@ int samelda_cu_period(samelda_cu_ctx* ctx, const int32_t* doc_ids, int64_t B, in
   int rc = samelda_cu_period_sample(ctx, doc_ids, B, t, m_t);
   if (rc) return rc;
   return samelda_cu_period_update(ctx, rho_t);
+}
+
+int samelda_cu_set_doc_base(samelda_cu_ctx* ctx, int64_t doc_base) {
+  return guarded(ctx, [&] {
+    if (doc_base < 0) fail(SAMELDA_CU_CONFIG, "doc_base must be >= 0");
+    ctx->doc_base = doc_base;
+  });
+}
+
+int samelda_cu_profile(samelda_cu_ctx* ctx, int32_t enable) {
+  return guarded(ctx, [&] {
+    ctx->profile = enable != 0;
+    for (auto& u : ctx->events_used) u = 0;
+    ctx->prof_nnz = ctx->prof_docs = 0;
+  });
+}
+
+int samelda_cu_profile_read(samelda_cu_ctx* ctx, double* ms_out, int64_t* launches_out,
+                            int64_t* nnz_sampled, int64_t* docs_sampled) {
+  return guarded(ctx, [&] {
+    ck(cudaStreamSynchronize(ctx->stream), "profile sync");
+    for (int k = 0; k < samelda_cu_ctx::kKinds; ++k) {
+      double total = 0.0;
+      for (size_t i = 0; i < ctx->events_used[k]; ++i) {
+        float ms = 0.0f;
+        ck(cudaEventElapsedTime(&ms, ctx->events[k][i].first, ctx->events[k][i].second), "elapsed");
+        total += ms;
+      }
+      ms_out[k] = total;
+      launches_out[k] = static_cast<int64_t>(ctx->events_used[k]);
+      ctx->events_used[k] = 0;
+    }
+    *nnz_sampled = ctx->prof_nnz;
+    *docs_sampled = ctx->prof_docs;
+    ctx->prof_nnz = ctx->prof_docs = 0;
+  });
 }
 
 int samelda_cu_phi_counts_device(samelda_cu_ctx* ctx, void** ptr, int64_t* n_elems,

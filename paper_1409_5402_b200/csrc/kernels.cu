@@ -144,7 +144,7 @@ __global__ void __launch_bounds__(kSampleBlock) k_sample(
     const int n_here = static_cast<int>(min(static_cast<int64_t>(kWarp), p1 - g0));
     for (int i = 0; i < n_here; ++i) {
       const int64_t bi = __shfl_sync(0xffffffffu, b, i);
-      const uint32_t di = static_cast<uint32_t>(__shfl_sync(0xffffffffu, d, i));
+      const uint32_t di = static_cast<uint32_t>(__shfl_sync(0xffffffffu, d, i) + bv.doc_base);
       const int32_t wi = __shfl_sync(0xffffffffu, w, i);
       const int32_t ci = __shfl_sync(0xffffffffu, c, i);
       const double mui = __shfl_sync(0xffffffffu, mu_v, i);

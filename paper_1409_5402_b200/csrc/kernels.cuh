@@ -29,7 +29,8 @@ struct BatchView {
   const int32_t* batch_docs;
   const int64_t* batch_prefix;
   int64_t B;
-  int64_t nnz;  // batch_prefix[B]
+  int64_t nnz;       // batch_prefix[B]
+  int64_t doc_base;  // global id of local doc 0 (doc-sharded runs): Philox keys use global ids
 };
 
 // theta_batch[b,:] = theta[batch_docs[b],:]            (sampler.cpp:313-317)

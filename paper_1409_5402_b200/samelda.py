@@ -111,6 +111,9 @@ SIGNATURES = [
     ("samelda_cu_phi_counts_device", C.c_int, [_P, C.POINTER(C.c_void_p), C.POINTER(_I64),
                                                C.POINTER(_I32), C.POINTER(_I32)]),
     ("samelda_cu_batch_theta", C.c_int, [_P, _P, _I64]),
+    ("samelda_cu_set_doc_base", C.c_int, [_P, _I64]),
+    ("samelda_cu_profile", C.c_int, [_P, _I32]),
+    ("samelda_cu_profile_read", C.c_int, [_P, _P, _P, C.POINTER(_I64), C.POINTER(_I64)]),
     ("samelda_cu_count_totals", C.c_int, [_P, C.POINTER(_I64), C.POINTER(_I64)]),
     ("samelda_cu_evaluate", C.c_int, [_P, C.POINTER(_D)]),
     ("samelda_cu_model_download", C.c_int, [_P, _P, _P]),
@@ -524,6 +527,22 @@ class Trainer:
         self.ctx.check(self.ctx.lib.samelda_cu_phi_counts_device(
             self.ctx.h, C.byref(p), C.byref(n), C.byref(eb), C.byref(fl)))
         return p.value, n.value, eb.value, bool(fl.value)
+
+    def set_doc_base(self, base: int):
+        self.ctx.check(self.ctx.lib.samelda_cu_set_doc_base(self.ctx.h, int(base)))
+
+    def profile(self, enable: bool = True):
+        self.ctx.check(self.ctx.lib.samelda_cu_profile(self.ctx.h, 1 if enable else 0))
+
+    def profile_read(self) -> dict:
+        ms = np.zeros(3)
+        n = np.zeros(3, np.int64)
+        nnz, docs = C.c_int64(), C.c_int64()
+        self.ctx.check(self.ctx.lib.samelda_cu_profile_read(self.ctx.h, _ptr(ms), _ptr(n),
+                                                            C.byref(nnz), C.byref(docs)))
+        return dict(sample_ms=ms[0], sddmm_ms=ms[1], mstep_ms=ms[2], sample_launches=int(n[0]),
+                    sddmm_launches=int(n[1]), mstep_launches=int(n[2]), nnz=nnz.value,
+                    docs=docs.value)
 
     def count_totals(self):
         a, b = C.c_int64(), C.c_int64()

@@ -1,0 +1,59 @@
+"""Synthetic corpora at the BASELINE.json shapes (include/samelda_synth.h).
+
+NYTimes shape: D=300,000, W=102,660, ~100M tokens (~333/doc), nnz/token ~0.70.
+PubMed shape:  D=8.2M,    W=141,043, ~730M tokens (~89/doc),  nnz/token ~0.66.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+import numpy as np
+
+from .samelda import Corpus, load_library
+
+
+class _Params(C.Structure):
+    _fields_ = [("n_docs", C.c_int64), ("n_words", C.c_int64), ("n_topics_gen", C.c_int64),
+                ("mean_len", C.c_double), ("len_shape", C.c_double), ("zipf_s", C.c_double),
+                ("background", C.c_double), ("topics_per_doc", C.c_double),
+                ("seed", C.c_uint64), ("first_doc", C.c_int64)]
+
+
+PRESETS = {
+    "nytimes": dict(n_docs=300_000, n_words=102_660, n_topics_gen=200, mean_len=333.0,
+                    len_shape=2.0, zipf_s=1.06, background=0.3, topics_per_doc=2.0),
+    "pubmed": dict(n_docs=8_200_000, n_words=141_043, n_topics_gen=200, mean_len=89.0,
+                   len_shape=3.0, zipf_s=1.07, background=0.3, topics_per_doc=1.5),
+}
+
+
+def generate(n_docs, n_words, n_topics_gen=200, mean_len=333.0, len_shape=2.0, zipf_s=1.07,
+             background=0.3, topics_per_doc=2.0, seed=1, n_threads=None,
+             first_doc=0) -> Corpus:
+    lib = load_library()
+    lib.samelda_synth_generate.restype = C.c_int
+    lib.samelda_synth_generate.argtypes = [C.POINTER(_Params), C.c_int, C.POINTER(C.c_void_p),
+                                           C.POINTER(C.c_int64), C.POINTER(C.c_int64)]
+    lib.samelda_synth_copy.argtypes = [C.c_void_p] * 4
+    lib.samelda_synth_free.argtypes = [C.c_void_p]
+    p = _Params(n_docs, n_words, n_topics_gen, mean_len, len_shape, zipf_s, background,
+                topics_per_doc, seed, first_doc)
+    h, nnz, tok = C.c_void_p(), C.c_int64(), C.c_int64()
+    rc = lib.samelda_synth_generate(C.byref(p), int(n_threads or os.cpu_count() or 1),
+                                    C.byref(h), C.byref(nnz), C.byref(tok))
+    if rc:
+        raise ValueError("samelda_synth_generate: bad parameters")
+    offs = np.empty(n_docs + 1, np.int64)
+    words = np.empty(max(nnz.value, 1), np.int32)
+    counts = np.empty(max(nnz.value, 1), np.int32)
+    lib.samelda_synth_copy(h, offs.ctypes.data, words.ctypes.data, counts.ctypes.data)
+    lib.samelda_synth_free(h)
+    return Corpus(offs, words[:nnz.value], counts[:nnz.value], n_words)
+
+
+def preset(name: str, seed: int = 1, scale: float = 1.0, n_threads=None, shard: int = 0) -> Corpus:
+    """Preset corpus; `shard` s generates global docs [s*D, (s+1)*D) (weak-scaling shards)."""
+    kw = dict(PRESETS[name])
+    kw["n_docs"] = max(2, int(kw["n_docs"] * scale))
+    return generate(seed=seed, n_threads=n_threads, first_doc=shard * kw["n_docs"], **kw)
