@@ -257,7 +257,8 @@ struct samelda_cu_ctx {
   samelda_cu_config cfg{};
   int K = 0;
   int64_t W = 0, D = 0;
-  DevBuf theta, phi;  // D x K, W x K
+  DevBuf theta, phi;  // D x K, W x K (f64)
+  DevBuf phi32;       // W x K f32 shadow of phi (sampler fast path)
 
   // doc-sharded runs: global id of local doc 0 (Philox keys use global ids)
   int64_t doc_base = 0;
@@ -294,8 +295,8 @@ struct samelda_cu_ctx {
   bool counts_float = false;
 
   // scratch
-  DevBuf batch, prefix, theta_batch, mu, tc, pc, tf, pf, cand, totals, err, ll, phi_call,
-      phi_call_wk, theta_call, eval_scratch, theta_rows;
+  DevBuf batch, prefix, theta_batch, theta_batch32, mu, tc, pc, tf, pf, totals, err, ll,
+      phi_call, phi_call_wk, phi_call32, theta_call, theta_call32, eval_scratch, theta_rows;
   int32_t* h_batch = nullptr;
   int64_t* h_prefix = nullptr;
   int64_t h_cap = 0;
@@ -366,8 +367,8 @@ struct samelda_cu_ctx {
     return bv;
   }
 
-  // phi K x W host -> W x K device (per-call boundary)
-  double* upload_phi(const double* phi_kw, int64_t K_, int64_t W_) {
+  // phi K x W host -> W x K device (per-call boundary), plus its f32 shadow
+  double* upload_phi(const double* phi_kw, int64_t K_, int64_t W_, float** out32 = nullptr) {
     double* tmp = ensure<double>(phi_call, K_ * W_);
     double* out = ensure<double>(phi_call_wk, K_ * W_);
     if (K_ * W_ > 0) {
@@ -375,13 +376,18 @@ struct samelda_cu_ctx {
          "upload phi");
       launches += scu::launch_transpose(tmp, K_, W_, out, stream);
     }
+    if (out32) {
+      *out32 = ensure<float>(phi_call32, K_ * W_);
+      launches += scu::launch_to_f32(out, K_ * W_, *out32, stream);
+    }
     return out;
   }
 
   // one sweep's sampling into tc/pc (or tf/pf): zeroes the count buffers first
-  void sample_sweep(const scu::BatchView& bv, const double* theta_b, const double* phi_wk,
-                    const double* mu_d, int K_, int64_t W_, double m_t_, uint64_t seed,
-                    int64_t t, int sweep, int mode) {
+  // mu_d: the caller's mu (per-call API) or nullptr (the kernel forms mu)
+  void sample_sweep(const scu::BatchView& bv, const double* theta_b, const float* theta_b32,
+                    const double* phi_wk, const float* phi_wk32, const double* mu_d, int K_,
+                    int64_t W_, double m_t_, uint64_t seed, int64_t t, int sweep, int mode) {
     if (profile) {
       prof_nnz += bv.nnz;
       prof_docs += bv.B;
@@ -402,9 +408,9 @@ struct samelda_cu_ctx {
       ck(cudaMemsetAsync(tc_, 0, sizeof(unsigned long long) * std::max<int64_t>(bv.B * K_, 1), stream), "zero tc");
       ck(cudaMemsetAsync(pc_, 0, sizeof(unsigned long long) * std::max<int64_t>(W_ * K_, 1), stream), "zero pc");
       tick(kSample, true);
-      launches += scu::launch_sample(bv, theta_b, phi_wk, mu_d, K_, m_t_, seed,
-                                     static_cast<uint32_t>(t), static_cast<uint32_t>(sweep), mode,
-                                     tc_, pc_, nullptr, nullptr, d_err(), stream);
+      launches += scu::launch_sample_fast(bv, theta_b, theta_b32, phi_wk, phi_wk32, mu_d, K_,
+                                          m_t_, seed, static_cast<uint32_t>(t),
+                                          static_cast<uint32_t>(sweep), tc_, pc_, d_err(), stream);
       tick(kSample, false);
     }
   }
@@ -581,12 +587,15 @@ static void sample_call(samelda_cu_ctx* ctx, const samelda_cu_corpus* corpus,
   const scu::BatchView bv = ctx->upload_batch(ctx->train, doc_ids, B);
   double* th = ensure<double>(ctx->theta_call, B * K);
   ck(cudaMemcpyAsync(th, theta_batch, sizeof(double) * B * K, cudaMemcpyHostToDevice, ctx->stream), "upload theta");
-  const double* phi_wk = ctx->upload_phi(phi, K, W);
+  float* th32 = ensure<float>(ctx->theta_call32, B * K);
+  ctx->launches += scu::launch_to_f32(th, B * K, th32, ctx->stream);
+  float* phi32 = nullptr;
+  const double* phi_wk = ctx->upload_phi(phi, K, W, &phi32);
   double* mu_d = ensure<double>(ctx->mu, nnz);
   if (nnz > 0)
     ck(cudaMemcpyAsync(mu_d, mu, sizeof(double) * nnz, cudaMemcpyHostToDevice, ctx->stream), "upload mu");
   ctx->reset_err();
-  ctx->sample_sweep(bv, th, phi_wk, mu_d, static_cast<int>(K), W, m_t, seed, t, sweep, mode);
+  ctx->sample_sweep(bv, th, th32, phi_wk, phi32, mu_d, static_cast<int>(K), W, m_t, seed, t, sweep, mode);
   ctx->check_err("sample_counts");
   const void* tsrc = mode == SAMELDA_CU_MODE_EXPECTED ? ctx->tf.p : ctx->tc.p;
   const void* psrc = mode == SAMELDA_CU_MODE_EXPECTED ? ctx->pf.p : ctx->pc.p;
@@ -638,11 +647,11 @@ static void update_call(samelda_cu_ctx* ctx, double* theta, int64_t D, double* p
     if (expected) {
       double* tf = ensure<double>(ctx->tf, B * K);
       ck(cudaMemcpyAsync(tf, tcounts, sizeof(double) * B * K, cudaMemcpyHostToDevice, st), "upload tf");
-      ctx->launches += scu::launch_theta_from_counts(nullptr, tf, B * K, m_t, alpha, rows, st);
+      ctx->launches += scu::launch_theta_from_counts(nullptr, tf, B * K, m_t, alpha, rows, nullptr, st);
     } else {
       auto* tc = ensure<unsigned long long>(ctx->tc, B * K);
       ck(cudaMemcpyAsync(tc, tcounts, sizeof(int64_t) * B * K, cudaMemcpyHostToDevice, st), "upload tc");
-      ctx->launches += scu::launch_theta_from_counts(tc, nullptr, B * K, m_t, alpha, rows, st);
+      ctx->launches += scu::launch_theta_from_counts(tc, nullptr, B * K, m_t, alpha, rows, nullptr, st);
     }
     std::vector<double> h(static_cast<size_t>(B * K));
     ck(cudaMemcpyAsync(h.data(), rows, sizeof(double) * B * K, cudaMemcpyDeviceToHost, st), "download rows");
@@ -652,16 +661,15 @@ static void update_call(samelda_cu_ctx* ctx, double* theta, int64_t D, double* p
   }
   if (W * K == 0) return;
   double* phi_wk = ctx->upload_phi(phi, K, W);
-  double* cand = ensure<double>(ctx->cand, W * K);
   double* totals = ensure<double>(ctx->totals, K);
   if (expected) {
     double* pf = ensure<double>(ctx->pf, W * K);
     ck(cudaMemcpyAsync(pf, pcounts, sizeof(double) * W * K, cudaMemcpyHostToDevice, st), "upload pf");
-    ctx->launches += scu::launch_phi_mstep(nullptr, pf, W, Ki, m_t, beta, rho_t, phi_wk, cand, totals, ctx->d_err(), st);
+    ctx->launches += scu::launch_phi_mstep(nullptr, pf, W, Ki, m_t, beta, rho_t, phi_wk, nullptr, totals, ctx->d_err(), st);
   } else {
     auto* pc = ensure<unsigned long long>(ctx->pc, W * K);
     ck(cudaMemcpyAsync(pc, pcounts, sizeof(int64_t) * W * K, cudaMemcpyHostToDevice, st), "upload pc");
-    ctx->launches += scu::launch_phi_mstep(pc, nullptr, W, Ki, m_t, beta, rho_t, phi_wk, cand, totals, ctx->d_err(), st);
+    ctx->launches += scu::launch_phi_mstep(pc, nullptr, W, Ki, m_t, beta, rho_t, phi_wk, nullptr, totals, ctx->d_err(), st);
   }
   double* back = ensure<double>(ctx->phi_call, K * W);
   ctx->launches += scu::launch_transpose(phi_wk, W, K, back, st);
@@ -812,6 +820,7 @@ int samelda_cu_train_begin(samelda_cu_ctx* ctx, const samelda_cu_corpus* corpus,
     ctx->launches += scu::launch_fill(th, ctx->D * K, config->alpha + 1.0 / static_cast<double>(K), ctx->stream);
     ctx->launches += scu::launch_phi_init(ph, ctx->W, ctx->K, config->t_max > 0 ? config->init_noise : 0.0,
                                           config->seed, ensure<double>(ctx->totals, K), ctx->stream);
+    ctx->launches += scu::launch_to_f32(ph, ctx->W * K, ensure<float>(ctx->phi32, ctx->W * K), ctx->stream);
     ck(cudaStreamSynchronize(ctx->stream), "train_begin");
     ck(cudaGetLastError(), "train_begin");
     ctx->model_ready = true;
@@ -845,21 +854,28 @@ int samelda_cu_period_sample(samelda_cu_ctx* ctx, const int32_t* doc_ids, int64_
     ctx->nnzB = bv.nnz;
     ctx->m_t = m_t;
     double* thb = ensure<double>(ctx->theta_batch, B * K);
-    double* mu = ensure<double>(ctx->mu, bv.nnz);
+    float* thb32 = ensure<float>(ctx->theta_batch32, B * K);
+    const bool expected = c.mode == SAMELDA_CU_MODE_EXPECTED;
+    double* mu = expected ? ensure<double>(ctx->mu, bv.nnz) : nullptr;
     ctx->reset_err();
-    ctx->launches += scu::launch_gather_theta(ctx->theta.as<double>(), bv.batch_docs, B, K, thb, st);
+    ctx->launches += scu::launch_gather_theta(ctx->theta.as<double>(), bv.batch_docs, B, K, thb, thb32, st);
     for (int64_t sweep = 0; sweep < c.inner_sweeps; ++sweep) {
-      ctx->tick(samelda_cu_ctx::kSddmm, true);
-      ctx->launches += scu::launch_sddmm(bv, thb, ctx->phi.as<double>(), K, mu, st);
-      ctx->tick(samelda_cu_ctx::kSddmm, false);
-      ctx->sample_sweep(bv, thb, ctx->phi.as<double>(), mu, K, ctx->W, m_t, c.seed, t,
-                        static_cast<int>(sweep), c.mode);
+      if (expected) {
+        // the expected-count kernel consumes an explicit mu (sampler.cpp:321)
+        ctx->tick(samelda_cu_ctx::kSddmm, true);
+        ctx->launches += scu::launch_sddmm(bv, thb, ctx->phi.as<double>(), K, mu, st);
+        ctx->tick(samelda_cu_ctx::kSddmm, false);
+      }
+      // parity mode: the SDDMM is fused into the sampling kernel (mu == nullptr)
+      ctx->sample_sweep(bv, thb, thb32, ctx->phi.as<double>(), ctx->phi32.as<float>(), mu, K, ctx->W,
+                        m_t, c.seed, t, static_cast<int>(sweep), c.mode);
       if (sweep + 1 < c.inner_sweeps) {
-        if (c.mode == SAMELDA_CU_MODE_EXPECTED)
-          ctx->launches += scu::launch_theta_from_counts(nullptr, ctx->tf.as<double>(), B * K, m_t, c.alpha, thb, st);
+        if (expected)
+          ctx->launches += scu::launch_theta_from_counts(nullptr, ctx->tf.as<double>(), B * K, m_t, c.alpha, thb,
+                                                         thb32, st);
         else
           ctx->launches += scu::launch_theta_from_counts(ctx->tc.as<unsigned long long>(), nullptr, B * K, m_t,
-                                                         c.alpha, thb, st);
+                                                         c.alpha, thb, thb32, st);
       }
     }
     ck(cudaGetLastError(), "period sample launch");
@@ -884,7 +900,7 @@ int samelda_cu_period_update(samelda_cu_ctx* ctx, double rho_t) {
     ctx->launches += scu::launch_theta_persist(tcu, tcf, ctx->batch.as<int32_t>(), ctx->B, K, ctx->m_t, c.alpha,
                                                ctx->theta.as<double>(), st);
     ctx->launches += scu::launch_phi_mstep(pcu, pcf, ctx->W, K, ctx->m_t, c.beta, rho_t, ctx->phi.as<double>(),
-                                           ensure<double>(ctx->cand, ctx->W * K), ensure<double>(ctx->totals, K),
+                                           ctx->phi32.as<float>(), ensure<double>(ctx->totals, K),
                                            ctx->d_err(), st);
     ctx->tick(samelda_cu_ctx::kMstep, false);
     ctx->check_err("period");
@@ -952,7 +968,7 @@ int samelda_cu_batch_theta(samelda_cu_ctx* ctx, double* out, int64_t cap) {
     if (cap < n) fail(SAMELDA_CU_CONFIG, "batch_theta: buffer too small");
     double* rows = ensure<double>(ctx->theta_rows, n);
     ctx->launches += scu::launch_gather_theta(ctx->theta.as<double>(), ctx->batch.as<int32_t>(), ctx->B, ctx->K,
-                                              rows, ctx->stream);
+                                              rows, nullptr, ctx->stream);
     if (n > 0)
       ck(cudaMemcpyAsync(out, rows, sizeof(double) * n, cudaMemcpyDeviceToHost, ctx->stream), "download rows");
     ck(cudaStreamSynchronize(ctx->stream), "batch_theta");
@@ -1007,6 +1023,7 @@ int samelda_cu_model_upload(samelda_cu_ctx* ctx, const double* phi, const double
     if (phi) {
       const double* wk = ctx->upload_phi(phi, K, ctx->W);
       ck(cudaMemcpyAsync(ctx->phi.p, wk, sizeof(double) * K * ctx->W, cudaMemcpyDeviceToDevice, ctx->stream), "phi");
+      ctx->launches += scu::launch_to_f32(ctx->phi.as<double>(), K * ctx->W, ctx->phi32.as<float>(), ctx->stream);
     }
     if (theta)
       ck(cudaMemcpyAsync(ctx->theta.p, theta, sizeof(double) * ctx->D * K, cudaMemcpyHostToDevice, ctx->stream), "theta");

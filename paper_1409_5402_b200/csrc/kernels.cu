@@ -35,12 +35,14 @@ inline unsigned grid_for(int64_t threads, int block) {
 
 __global__ void k_gather_theta(const double* __restrict__ theta,
                                const int32_t* __restrict__ batch_docs, int64_t B, int K,
-                               double* __restrict__ out) {
+                               double* __restrict__ out, float* __restrict__ out32) {
   const int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
   if (i >= B * K) return;
   const int64_t b = i / K;
   const int k = static_cast<int>(i - b * K);
-  out[i] = theta[static_cast<int64_t>(batch_docs[b]) * K + k];
+  const double v = theta[static_cast<int64_t>(batch_docs[b]) * K + k];
+  out[i] = v;
+  if (out32) out32[i] = __double2float_rn(v);
 }
 
 // -------------------------------------------------------------------- sddmm
@@ -201,16 +203,278 @@ __global__ void __launch_bounds__(kSampleBlock) k_sample(
   flush(cur_b);
 }
 
+// ------------------------------------------------------ sample (fast-exact)
+// Same draws as k_sample, bit for bit, at a fraction of the cost.  A draw's
+// outcome z is the first k with u <= cdf_k, where u is the stream's first
+// uniform and cdf_k the reference's f64 inversion recurrence (rng.cpp:39-52).
+// The fast path evaluates rate, exp and the recurrence in f32 with a
+// rigorous relative error bound r(lambda, k) and decides each comparison only
+// when u lies outside [cdf - m, cdf + m]; otherwise (probability ~1e-5 per
+// draw), or for lambda >= 9.5 (PTRS territory), non-finite / negative /
+// denormal inputs, or k > 40, the lane recomputes that draw exactly like
+// k_sample: sequential f64 mu, __ddiv_rn rate, full Philox block, exact
+// inversion or PTRS.  Error budget (u32 = 2^-24 unit roundoff):
+//   lambda_f: theta, phi rounded to f32 (2u), product (u), mu by tree sum of
+//     positive terms (<= 16u), cs/mu (3u), lambda (u)  -> |dl| <= 1.5e-6 lambda
+//   exp:  __expf max error (2 + 1.2 lambda) ulp       -> <= (1.2e-7 + 7e-8 lambda)
+//   step k: pmf *= lambda/k (+ dl + 3u), cdf += pmf (+u)
+//   r = 3e-6 + 4e-6 lambda + 4e-6 k  (>= 2x the sum above);  u from the high
+//   word alone: |u - u_f| <= 6.1e-8 -> m = cdf * r + 1.2e-7.
+// The mu used is the caller's mu array when given (per-call sample_counts),
+// else the warp computes it (f32 tree for the fast path, exact f64
+// sequential sum on fallback, cached per lane and nonzero).
+
+constexpr int kFastBlock = 256;
+
+struct Philox1 {
+  // round-1 specialisation for counter {0, w, d, t}: M0 * 0 = 0, so the
+  // only per-draw work in round 1 is one xor; M1 * d is per nonzero
+  uint32_t hw;  // hi(M1 * d) ^ w
+  uint32_t lo;  // lo(M1 * d)
+};
+
+__device__ __forceinline__ uint32_t philox_y(const Philox1 r1, uint32_t k0, uint32_t k1,
+                                             uint32_t p2lo, uint32_t p2hi) {
+  // round 1 -> c = {hw ^ k0, lo, t ^ k1, 0}; round 2 with M1 * (t ^ k1) = p2
+  uint32_t c0 = r1.hw ^ k0;
+  k0 += kPhiloxW0;
+  k1 += kPhiloxW1;
+  uint32_t lo0, hi0;
+  mulhilo(kPhiloxM0, c0, lo0, hi0);
+  uint32_t x0 = p2hi ^ r1.lo ^ k0, x1 = p2lo, x2 = hi0 ^ k1, x3 = lo0;
+#pragma unroll
+  for (int r = 2; r < 9; ++r) {
+    k0 += kPhiloxW0;
+    k1 += kPhiloxW1;
+    uint32_t a0, b0, a1, b1;
+    mulhilo(kPhiloxM0, x0, a0, b0);
+    mulhilo(kPhiloxM1, x2, a1, b1);
+    const uint32_t n0 = b1 ^ x1 ^ k0, n2 = b0 ^ x3 ^ k1;
+    x0 = n0;
+    x1 = a1;
+    x2 = n2;
+    x3 = a0;
+  }
+  // round 10: output word y = lo(M1 * x2)
+  return kPhiloxM1 * x2;
+}
+
+// Exact draw (the k_sample arithmetic), for fallback lanes.  Returns z >= 0, or
+// -1 for a non-finite / negative rate (NumericalError).
+__device__ __noinline__ long long exact_draw(const double* __restrict__ th_row,
+                                             const double* __restrict__ ph_row, int K, int k,
+                                             double cs, double uniform_weight, double mu_given,
+                                             int have_mu, double* mu_cache, int* mu_valid,
+                                             uint64_t seed, uint32_t t, uint32_t d, uint32_t w,
+                                             uint32_t sweep) {
+  double mu;
+  if (have_mu) {
+    mu = mu_given;
+  } else {
+    if (!*mu_valid) {
+      double dot = 0.0;
+      for (int kk = 0; kk < K; ++kk) dot = __dadd_rn(dot, __dmul_rn(th_row[kk], ph_row[kk]));
+      *mu_cache = dot;
+      *mu_valid = 1;
+    }
+    mu = *mu_cache;
+  }
+  const bool degenerate = mu < 1e-30;
+  const double weight = degenerate ? uniform_weight : __ddiv_rn(__dmul_rn(th_row[k], ph_row[k]), mu);
+  const double rate = __dmul_rn(weight, cs);
+  if (!(rate >= 0.0) || isinf(rate)) return -1;
+  if (rate == 0.0) return 0;
+  const uint32_t tag = make_tag(kPoissonCounts, sweep, static_cast<uint32_t>(k));
+  uint32_t k0, k1;
+  stream_key(seed, tag, k0, k1);
+  const U4 blk = philox10(U4{0u, w, d, t}, k0, k1);
+  if (rate < 10.0) return poisson_inversion(rate, u64_to_uniform(join64(blk.x, blk.y)));
+  Stream s;
+  s.init_with_block0(seed, t, d, w, tag, blk, 0);
+  return poisson_ptrs(rate, s);
+}
+
+template <int KPL>
+__global__ void __launch_bounds__(kFastBlock) k_sample_fast(
+    BatchView bv, const double* __restrict__ theta_b64, const float* __restrict__ theta_b32,
+    const double* __restrict__ phi64, const float* __restrict__ phi32,
+    const double* __restrict__ mu_in, int K, double m_t, uint64_t seed, uint32_t t,
+    uint32_t sweep, int64_t chunk, int n_slices, unsigned long long* __restrict__ theta_counts,
+    unsigned long long* __restrict__ phi_counts, int* __restrict__ err) {
+  const int lane = threadIdx.x & 31;
+  const int64_t gw = (blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x) >> 5;
+  const int64_t item = gw / n_slices;
+  const int slice = static_cast<int>(gw - item * n_slices);
+  const int64_t p0 = item * chunk;
+  if (p0 >= bv.nnz) return;
+  const int64_t p1 = min(p0 + chunk, bv.nnz);
+  const int kbase = slice * kWarp * KPL;
+  const double uniform_weight = 1.0 / static_cast<double>(K);
+  const int have_mu = mu_in != nullptr;
+
+  // per-topic stream keys and the round-2 product M1 * (t ^ k1), fixed for the
+  // whole item
+  uint32_t key0[KPL], key1[KPL], p2lo[KPL], p2hi[KPL];
+#pragma unroll
+  for (int j = 0; j < KPL; ++j) {
+    const uint32_t k = static_cast<uint32_t>(kbase + lane + kWarp * j);
+    stream_key(seed, make_tag(kPoissonCounts, sweep, k), key0[j], key1[j]);
+    mulhilo(kPhiloxM1, t ^ key1[j], p2lo[j], p2hi[j]);
+  }
+
+  int64_t cur_b = -1;
+  float th[KPL];
+  uint32_t acc[KPL];
+#pragma unroll
+  for (int j = 0; j < KPL; ++j) {
+    th[j] = 0.0f;
+    acc[j] = 0u;
+  }
+
+  for (int64_t g0 = p0; g0 < p1; g0 += kWarp) {
+    const int64_t p = g0 + lane;
+    int64_t b = 0;
+    int32_t d = 0, w = 0, c = 0;
+    double mu_v = 0.0;
+    if (p < p1) {
+      b = find_row(bv.batch_prefix, bv.B, p);
+      d = __ldg(bv.batch_docs + b);
+      const int64_t gi = __ldg(bv.doc_offsets + d) + (p - __ldg(bv.batch_prefix + b));
+      w = __ldg(bv.word_ids + gi);
+      c = __ldg(bv.counts + gi);
+      if (have_mu) mu_v = __ldg(mu_in + p);
+    }
+    const int n_here = static_cast<int>(min(static_cast<int64_t>(kWarp), p1 - g0));
+    for (int i = 0; i < n_here; ++i) {
+      const int64_t bi = __shfl_sync(0xffffffffu, b, i);
+      const int32_t dl = __shfl_sync(0xffffffffu, d, i);
+      const uint32_t di = static_cast<uint32_t>(dl + bv.doc_base);
+      const int32_t wi = __shfl_sync(0xffffffffu, w, i);
+      const int32_t ci = __shfl_sync(0xffffffffu, c, i);
+      const double mui = __shfl_sync(0xffffffffu, mu_v, i);
+      if (bi != cur_b) {
+        if (cur_b >= 0) {
+#pragma unroll
+          for (int j = 0; j < KPL; ++j) {
+            const int k = kbase + lane + kWarp * j;
+            if (k < K && acc[j]) atomicAdd(theta_counts + cur_b * K + k, static_cast<unsigned long long>(acc[j]));
+          }
+        }
+        cur_b = bi;
+#pragma unroll
+        for (int j = 0; j < KPL; ++j) {
+          const int k = kbase + lane + kWarp * j;
+          th[j] = k < K ? __ldg(theta_b32 + bi * K + k) : 0.0f;
+          acc[j] = 0u;
+        }
+      }
+      const float* prow = phi32 + static_cast<int64_t>(wi) * K;
+      float prod[KPL];
+      float part = 0.0f;
+#pragma unroll
+      for (int j = 0; j < KPL; ++j) {
+        const int k = kbase + lane + kWarp * j;
+        prod[j] = k < K ? __fmul_rn(th[j], __ldg(prow + k)) : 0.0f;
+        part = __fadd_rn(part, prod[j]);
+      }
+      float mu_f;
+      if (have_mu) {
+        mu_f = __double2float_rn(mui);
+      } else {
+        // slices of a wide K each see a partial sum only: use the exact path
+        mu_f = part;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) mu_f = __fadd_rn(mu_f, __shfl_xor_sync(0xffffffffu, mu_f, o));
+        if (n_slices > 1) mu_f = 0.0f;
+      }
+      const double cs = __dmul_rn(m_t, static_cast<double>(ci));
+      const bool nz_exact = !(mu_f >= 1e-20f) || isinf(mu_f);
+      const float scale = __fdiv_rn(__double2float_rn(cs), mu_f);
+      uint32_t m1lo, m1hi;
+      mulhilo(kPhiloxM1, di, m1lo, m1hi);
+      const Philox1 r1{m1hi ^ static_cast<uint32_t>(wi), m1lo};
+      double mu_cache = 0.0;
+      int mu_valid = 0;
+#pragma unroll
+      for (int j = 0; j < KPL; ++j) {
+        const int k = kbase + lane + kWarp * j;
+        if (k >= K) continue;
+        const float lam = __fmul_rn(prod[j], scale);
+        long long z = 0;
+        bool exact = nz_exact || !(prod[j] >= 1e-30f) || !(lam < 9.5f);
+        if (!exact) {
+          const uint32_t y = philox_y(r1, key0[j], key1[j], p2lo[j], p2hi[j]);
+          const float u = __uint2float_rn(y) * 2.3283064365386963e-10f;
+          float pmf = __expf(-lam);
+          float cdf = pmf;
+          const float base = __fadd_rn(3e-6f, __fmul_rn(4e-6f, lam));
+          int kk = 0;
+          for (;;) {
+            const float r = __fadd_rn(base, __fmul_rn(4e-6f, static_cast<float>(kk)));
+            const float mrg = __fadd_rn(__fmul_rn(cdf, r), 1.2e-7f);
+            if (u <= __fsub_rn(cdf, mrg)) break;
+            if (!(u > __fadd_rn(cdf, mrg)) || kk >= 40) {
+              exact = true;
+              break;
+            }
+            ++kk;
+            pmf = __fmul_rn(pmf, __fdiv_rn(lam, static_cast<float>(kk)));
+            cdf = __fadd_rn(cdf, pmf);
+          }
+          z = kk;
+        }
+        if (exact) {
+          z = exact_draw(theta_b64 + bi * K, phi64 + static_cast<int64_t>(wi) * K, K, k, cs,
+                         uniform_weight, mui, have_mu, &mu_cache, &mu_valid, seed, t, di,
+                         static_cast<uint32_t>(wi), sweep);
+          if (z < 0) {
+            atomicOr(err, kErrNumerical);
+            z = 0;
+          }
+        }
+        if (z != 0) {
+          acc[j] += static_cast<uint32_t>(z);
+          atomicAdd(phi_counts + static_cast<int64_t>(wi) * K + k, static_cast<unsigned long long>(z));
+        }
+      }
+    }
+  }
+  if (cur_b >= 0) {
+#pragma unroll
+    for (int j = 0; j < KPL; ++j) {
+      const int k = kbase + lane + kWarp * j;
+      if (k < K && acc[j]) atomicAdd(theta_counts + cur_b * K + k, static_cast<unsigned long long>(acc[j]));
+    }
+  }
+}
+
+template <int KPL>
+int launch_fast_kpl(const BatchView& bv, const double* tb64, const float* tb32, const double* phi64,
+                    const float* phi32, const double* mu, int K, double m_t, uint64_t seed,
+                    uint32_t t, uint32_t sweep, unsigned long long* tc, unsigned long long* pc,
+                    int* err, cudaStream_t st) {
+  const int n_slices = (K + kWarp * KPL - 1) / (kWarp * KPL);
+  const int64_t chunk = 128;
+  const int64_t items = (bv.nnz + chunk - 1) / chunk;
+  const int64_t threads = items * n_slices * kWarp;
+  k_sample_fast<KPL><<<grid_for(threads, kFastBlock), kFastBlock, 0, st>>>(
+      bv, tb64, tb32, phi64, phi32, mu, K, m_t, seed, t, sweep, chunk, n_slices, tc, pc, err);
+  return 1;
+}
+
 // ------------------------------------------------------------------- M-step
 
 __global__ void k_theta_from_counts(const unsigned long long* __restrict__ cu,
                                     const double* __restrict__ cf, int64_t n, double m_t,
-                                    double alpha, double* __restrict__ out) {
+                                    double alpha, double* __restrict__ out,
+                                    float* __restrict__ out32) {
   const int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
   if (i >= n) return;
   const double hat = cu ? __ddiv_rn(static_cast<double>(static_cast<long long>(cu[i])), m_t)
                         : __ddiv_rn(cf[i], m_t);
-  out[i] = __dadd_rn(hat, alpha);
+  const double v = __dadd_rn(hat, alpha);
+  out[i] = v;
+  if (out32) out32[i] = __double2float_rn(v);
 }
 
 __global__ void k_theta_persist(const unsigned long long* __restrict__ cu,
@@ -226,47 +490,60 @@ __global__ void k_theta_persist(const unsigned long long* __restrict__ cu,
   theta[static_cast<int64_t>(batch_docs[b]) * K + k] = __dadd_rn(hat, alpha);
 }
 
-__global__ void k_phi_candidate(const unsigned long long* __restrict__ cu,
-                                const double* __restrict__ cf, int64_t n, double m_t,
-                                double beta, double* __restrict__ cand) {
-  const int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
-  if (i >= n) return;
-  const double hat = cu ? __ddiv_rn(static_cast<double>(static_cast<long long>(cu[i])), m_t)
-                        : __ddiv_rn(cf[i], m_t);
-  cand[i] = __dadd_rn(hat, beta);
-}
-
-// total[k] = sum over w in order of x[w,k] (sampler.cpp:214-218): one thread
-// per topic, the chain of adds is sequential, loads are independent and
-// coalesced across the topic threads.
-__global__ void k_col_totals_seq(const double* __restrict__ x, int64_t W, int K,
-                                 double* __restrict__ totals, int* __restrict__ err,
-                                 int check) {
-  const int k = blockIdx.x * blockDim.x + threadIdx.x;
+// total[k] = sum over w, in order, of x[w,k] (sampler.cpp:214-218): one warp
+// per topic.  The 32 lanes fetch and convert 32 consecutive words in
+// parallel (x = count/m_t + beta, the reference's `value`), then every lane
+// runs the same sequential add chain over the 32 broadcast values, so the
+// summation order is exactly the reference's and the total is warp-uniform.
+template <int SRC>  // 0: u64 counts, 1: f64 expected counts, 2: plain f64 values
+__global__ void __launch_bounds__(256) k_col_totals(const unsigned long long* __restrict__ cu,
+                                                    const double* __restrict__ cf, int64_t W,
+                                                    int K, double m_t, double beta,
+                                                    double* __restrict__ totals,
+                                                    int* __restrict__ err) {
+  const int lane = threadIdx.x & 31;
+  const int k = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   if (k >= K) return;
   double total = 0.0;
-  int64_t w = 0;
-  for (; w + 8 <= W; w += 8) {
-    double v[8];
-#pragma unroll
-    for (int u = 0; u < 8; ++u) v[u] = __ldg(x + (w + u) * K + k);
-#pragma unroll
-    for (int u = 0; u < 8; ++u) total = __dadd_rn(total, v[u]);
+  for (int64_t w0 = 0; w0 < W; w0 += 32) {
+    const int64_t w = w0 + lane;
+    double v = 0.0;
+    if (w < W) {
+      const int64_t i = w * K + k;
+      if (SRC == 0) v = __dadd_rn(__ddiv_rn(static_cast<double>(static_cast<long long>(cu[i])), m_t), beta);
+      else if (SRC == 1) v = __dadd_rn(__ddiv_rn(cf[i], m_t), beta);
+      else v = cf[i];
+    }
+    const int n = static_cast<int>(min(static_cast<int64_t>(32), W - w0));
+    for (int j = 0; j < n; ++j) total = __dadd_rn(total, __shfl_sync(0xffffffffu, v, j));
   }
-  for (; w < W; ++w) total = __dadd_rn(total, __ldg(x + w * K + k));
-  totals[k] = total;
-  if (check && (!(total > 0.0) || isinf(total))) atomicOr(err, kErrNumerical);
+  if (lane == 0) {
+    totals[k] = total;
+    if (err && (!(total > 0.0) || isinf(total))) atomicOr(err, kErrNumerical);
+  }
 }
 
-__global__ void k_phi_blend(const double* __restrict__ cand, const double* __restrict__ totals,
-                            int64_t n, int K, double one_minus_rho, double rho,
-                            double* __restrict__ phi_wk) {
+// phi = (1 - rho) * phi + rho * cand / total, cand = count/m_t + beta
+// (sampler.cpp:209-226); also refreshes the f32 copy the sampler reads.
+__global__ void k_phi_blend(const unsigned long long* __restrict__ cu,
+                            const double* __restrict__ cf, const double* __restrict__ totals,
+                            int64_t n, int K, double m_t, double beta, double one_minus_rho,
+                            double rho, double* __restrict__ phi_wk, float* __restrict__ phi32) {
   const int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
   if (i >= n) return;
   const int k = static_cast<int>(i % K);
-  // (1 - rho) * phi + rho * cand / total   (sampler.cpp:224-226)
-  phi_wk[i] = __dadd_rn(__dmul_rn(one_minus_rho, phi_wk[i]),
-                        __ddiv_rn(__dmul_rn(rho, cand[i]), totals[k]));
+  const double hat = cu ? __ddiv_rn(static_cast<double>(static_cast<long long>(cu[i])), m_t)
+                        : __ddiv_rn(cf[i], m_t);
+  const double cand = __dadd_rn(hat, beta);
+  const double v = __dadd_rn(__dmul_rn(one_minus_rho, phi_wk[i]),
+                             __ddiv_rn(__dmul_rn(rho, cand), totals[k]));
+  phi_wk[i] = v;
+  if (phi32) phi32[i] = __double2float_rn(v);
+}
+
+__global__ void k_to_f32(const double* __restrict__ x, int64_t n, float* __restrict__ y) {
+  const int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+  if (i < n) y[i] = __double2float_rn(x[i]);
 }
 
 // ---------------------------------------------------------------- init phi
@@ -506,9 +783,10 @@ constexpr size_t kEvalSmemMax = 200 * 1024;
 // ------------------------------------------------------------- launchers
 
 int launch_gather_theta(const double* theta, const int32_t* batch_docs, int64_t B, int K,
-                        double* theta_batch, cudaStream_t st) {
+                        double* theta_batch, float* theta_batch32, cudaStream_t st) {
   if (B * K == 0) return 0;
-  k_gather_theta<<<grid_for(B * K, 256), 256, 0, st>>>(theta, batch_docs, B, K, theta_batch);
+  k_gather_theta<<<grid_for(B * K, 256), 256, 0, st>>>(theta, batch_docs, B, K, theta_batch,
+                                                      theta_batch32);
   return 1;
 }
 
@@ -537,10 +815,30 @@ int launch_sample(const BatchView& bv, const double* theta_batch, const double* 
                               tf, pf, err, st);
 }
 
+int launch_sample_fast(const BatchView& bv, const double* theta_b64, const float* theta_b32,
+                       const double* phi64, const float* phi32, const double* mu, int K,
+                       double m_t, uint64_t seed, uint32_t t, uint32_t sweep,
+                       unsigned long long* tc, unsigned long long* pc, int* err,
+                       cudaStream_t st) {
+  if (bv.nnz == 0) return 0;
+  if (K <= 32)
+    return launch_fast_kpl<1>(bv, theta_b64, theta_b32, phi64, phi32, mu, K, m_t, seed, t, sweep,
+                              tc, pc, err, st);
+  if (K <= 64)
+    return launch_fast_kpl<2>(bv, theta_b64, theta_b32, phi64, phi32, mu, K, m_t, seed, t, sweep,
+                              tc, pc, err, st);
+  if (K <= 128)
+    return launch_fast_kpl<4>(bv, theta_b64, theta_b32, phi64, phi32, mu, K, m_t, seed, t, sweep,
+                              tc, pc, err, st);
+  return launch_fast_kpl<8>(bv, theta_b64, theta_b32, phi64, phi32, mu, K, m_t, seed, t, sweep,
+                            tc, pc, err, st);
+}
+
 int launch_theta_from_counts(const unsigned long long* cu, const double* cf, int64_t n,
-                             double m_t, double alpha, double* out, cudaStream_t st) {
+                             double m_t, double alpha, double* out, float* out32,
+                             cudaStream_t st) {
   if (n == 0) return 0;
-  k_theta_from_counts<<<grid_for(n, 256), 256, 0, st>>>(cu, cf, n, m_t, alpha, out);
+  k_theta_from_counts<<<grid_for(n, 256), 256, 0, st>>>(cu, cf, n, m_t, alpha, out, out32);
   return 1;
 }
 
@@ -554,14 +852,23 @@ int launch_theta_persist(const unsigned long long* cu, const double* cf,
 }
 
 int launch_phi_mstep(const unsigned long long* cu, const double* cf, int64_t W, int K,
-                     double m_t, double beta, double rho, double* phi_wk, double* cand,
+                     double m_t, double beta, double rho, double* phi_wk, float* phi32,
                      double* totals, int* err, cudaStream_t st) {
   const int64_t n = W * K;
   if (n == 0) return 0;
-  k_phi_candidate<<<grid_for(n, 256), 256, 0, st>>>(cu, cf, n, m_t, beta, cand);
-  k_col_totals_seq<<<grid_for(K, 32), 32, 0, st>>>(cand, W, K, totals, err, 1);
-  k_phi_blend<<<grid_for(n, 256), 256, 0, st>>>(cand, totals, n, K, 1.0 - rho, rho, phi_wk);
-  return 3;
+  if (cu)
+    k_col_totals<0><<<grid_for(static_cast<int64_t>(K) * 32, 256), 256, 0, st>>>(cu, cf, W, K, m_t, beta, totals, err);
+  else
+    k_col_totals<1><<<grid_for(static_cast<int64_t>(K) * 32, 256), 256, 0, st>>>(cu, cf, W, K, m_t, beta, totals, err);
+  k_phi_blend<<<grid_for(n, 256), 256, 0, st>>>(cu, cf, totals, n, K, m_t, beta, 1.0 - rho, rho,
+                                               phi_wk, phi32);
+  return 2;
+}
+
+int launch_to_f32(const double* x, int64_t n, float* y, cudaStream_t st) {
+  if (n == 0) return 0;
+  k_to_f32<<<grid_for(n, 256), 256, 0, st>>>(x, n, y);
+  return 1;
 }
 
 int launch_phi_init(double* phi_wk, int64_t W, int K, double init_noise, uint64_t seed,
@@ -575,7 +882,7 @@ int launch_phi_init(double* phi_wk, int64_t W, int K, double init_noise, uint64_
   uint32_t k0, k1;
   stream_key(seed, make_tag(kPhiInit, 0, 0), k0, k1);
   k_phi_init_values<<<grid_for(n, 256), 256, 0, st>>>(phi_wk, W, K, init_noise, k0, k1);
-  k_col_totals_seq<<<grid_for(K, 32), 32, 0, st>>>(phi_wk, W, K, totals, nullptr, 0);
+  k_col_totals<2><<<grid_for(static_cast<int64_t>(K) * 32, 256), 256, 0, st>>>(nullptr, phi_wk, W, K, 1.0, 0.0, totals, nullptr);
   k_div_cols<<<grid_for(n, 256), 256, 0, st>>>(phi_wk, n, K, totals);
   return 3;
 }

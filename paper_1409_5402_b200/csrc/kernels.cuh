@@ -35,7 +35,7 @@ struct BatchView {
 
 // theta_batch[b,:] = theta[batch_docs[b],:]            (sampler.cpp:313-317)
 int launch_gather_theta(const double* theta, const int32_t* batch_docs, int64_t B, int K,
-                         double* theta_batch, cudaStream_t st);
+                        double* theta_batch, float* theta_batch32, cudaStream_t st);
 
 // mu[p] = sum_k theta_batch[b,k] * phi[w,k], sequential k  (sampler.cpp:88-123)
 int launch_sddmm(const BatchView& bv, const double* theta_batch, const double* phi_wk, int K,
@@ -50,10 +50,18 @@ int launch_sample(const BatchView& bv, const double* theta_batch, const double* 
                    unsigned long long* phi_counts, double* theta_exp, double* phi_exp,
                    int* err, cudaStream_t st);
 
+// Same draws, bit for bit, through an f32 fast path with exact f64 fallback
+// (see kernels.cu).  mu == nullptr: the kernel forms mu itself (period path).
+int launch_sample_fast(const BatchView& bv, const double* theta_b64, const float* theta_b32,
+                       const double* phi64, const float* phi32, const double* mu, int K,
+                       double m_t, uint64_t seed, uint32_t t, uint32_t sweep,
+                       unsigned long long* theta_counts, unsigned long long* phi_counts,
+                       int* err, cudaStream_t st);
+
 // out[i] = counts[i] / m_t + alpha over n entries       (sampler.cpp:324-330)
 int launch_theta_from_counts(const unsigned long long* counts_u, const double* counts_f,
-                              int64_t n, double m_t, double alpha, double* out,
-                              cudaStream_t st);
+                             int64_t n, double m_t, double alpha, double* out, float* out32,
+                             cudaStream_t st);
 
 // theta[batch_docs[b],k] = counts[b,k] / m_t + alpha     (sampler.cpp:204-210)
 int launch_theta_persist(const unsigned long long* counts_u, const double* counts_f,
@@ -61,11 +69,14 @@ int launch_theta_persist(const unsigned long long* counts_u, const double* count
                           double alpha, double* theta, cudaStream_t st);
 
 // M-step for phi (sampler.cpp:211-228):
-//   cand[w,k] = counts[w,k]/m_t + beta; total[k] = sum_w cand (sequential w);
+//   cand[w,k] = counts[w,k]/m_t + beta; total[k] = sum_w cand (sequential w, warp per topic);
 //   phi = (1-rho) phi + rho cand / total
 int launch_phi_mstep(const unsigned long long* counts_u, const double* counts_f, int64_t W,
-                      int K, double m_t, double beta, double rho, double* phi_wk,
-                      double* cand_scratch, double* totals, int* err, cudaStream_t st);
+                     int K, double m_t, double beta, double rho, double* phi_wk, float* phi32,
+                     double* totals, int* err, cudaStream_t st);
+
+// f32 shadow copy (the sampler's fast path reads f32 theta / phi)
+int launch_to_f32(const double* x, int64_t n, float* y, cudaStream_t st);
 
 // phi init with seeded perturbation (model.cpp:41-52, sampler.cpp:285-298)
 int launch_phi_init(double* phi_wk, int64_t W, int K, double init_noise, uint64_t seed,
