@@ -296,7 +296,8 @@ struct samelda_cu_ctx {
 
   // scratch
   DevBuf batch, prefix, theta_batch, theta_batch32, mu, tc, pc, tf, pf, totals, err, ll,
-      phi_call, phi_call_wk, phi_call32, theta_call, theta_call32, eval_scratch, theta_rows;
+      phi_call, phi_call_wk, phi_call32, theta_call, theta_call32, eval_scratch, theta_rows,
+      deferred, n_deferred;
   int32_t* h_batch = nullptr;
   int64_t* h_prefix = nullptr;
   int64_t h_cap = 0;
@@ -408,9 +409,12 @@ struct samelda_cu_ctx {
       ck(cudaMemsetAsync(tc_, 0, sizeof(unsigned long long) * std::max<int64_t>(bv.B * K_, 1), stream), "zero tc");
       ck(cudaMemsetAsync(pc_, 0, sizeof(unsigned long long) * std::max<int64_t>(W_ * K_, 1), stream), "zero pc");
       tick(kSample, true);
+      const int64_t slices = (K_ + 255) / 256;
+      void* rec = ensure<unsigned char>(deferred, bv.nnz * slices * scu::deferred_record_bytes());
       launches += scu::launch_sample_fast(bv, theta_b, theta_b32, phi_wk, phi_wk32, mu_d, K_,
                                           m_t_, seed, static_cast<uint32_t>(t),
-                                          static_cast<uint32_t>(sweep), tc_, pc_, d_err(), stream);
+                                          static_cast<uint32_t>(sweep), tc_, pc_, rec,
+                                          ensure<unsigned long long>(n_deferred, 1), d_err(), stream);
       tick(kSample, false);
     }
   }

@@ -218,8 +218,9 @@ __global__ void __launch_bounds__(kSampleBlock) k_sample(
 //     positive terms (<= 16u), cs/mu (3u), lambda (u)  -> |dl| <= 1.5e-6 lambda
 //   exp:  __expf max error (2 + 1.2 lambda) ulp       -> <= (1.2e-7 + 7e-8 lambda)
 //   step k: pmf *= lambda/k (+ dl + 3u), cdf += pmf (+u)
-//   r = 3e-6 + 4e-6 lambda + 4e-6 k  (>= 2x the sum above);  u from the high
-//   word alone: |u - u_f| <= 6.1e-8 -> m = cdf * r + 1.2e-7.
+//   __fdividef steps add <= 2 ulp each
+//   r = 4e-6 + 4e-6 lambda + 6e-6 k  (>= 2x the sum above);  u from the top
+//   23 bits of the high word: u - u_f in [0, 2^-23) -> m = cdf * r + 2.5e-7.
 // The mu used is the caller's mu array when given (per-call sample_counts),
 // else the warp computes it (f32 tree for the fast path, exact f64
 // sequential sum on fallback, cached per lane and nonzero).
@@ -259,48 +260,23 @@ __device__ __forceinline__ uint32_t philox_y(const Philox1 r1, uint32_t k0, uint
   return kPhiloxM1 * x2;
 }
 
-// Exact draw (the k_sample arithmetic), for fallback lanes.  Returns z >= 0, or
-// -1 for a non-finite / negative rate (NumericalError).
-__device__ __noinline__ long long exact_draw(const double* __restrict__ th_row,
-                                             const double* __restrict__ ph_row, int K, int k,
-                                             double cs, double uniform_weight, double mu_given,
-                                             int have_mu, double* mu_cache, int* mu_valid,
-                                             uint64_t seed, uint32_t t, uint32_t d, uint32_t w,
-                                             uint32_t sweep) {
-  double mu;
-  if (have_mu) {
-    mu = mu_given;
-  } else {
-    if (!*mu_valid) {
-      double dot = 0.0;
-      for (int kk = 0; kk < K; ++kk) dot = __dadd_rn(dot, __dmul_rn(th_row[kk], ph_row[kk]));
-      *mu_cache = dot;
-      *mu_valid = 1;
-    }
-    mu = *mu_cache;
-  }
-  const bool degenerate = mu < 1e-30;
-  const double weight = degenerate ? uniform_weight : __ddiv_rn(__dmul_rn(th_row[k], ph_row[k]), mu);
-  const double rate = __dmul_rn(weight, cs);
-  if (!(rate >= 0.0) || isinf(rate)) return -1;
-  if (rate == 0.0) return 0;
-  const uint32_t tag = make_tag(kPoissonCounts, sweep, static_cast<uint32_t>(k));
-  uint32_t k0, k1;
-  stream_key(seed, tag, k0, k1);
-  const U4 blk = philox10(U4{0u, w, d, t}, k0, k1);
-  if (rate < 10.0) return poisson_inversion(rate, u64_to_uniform(join64(blk.x, blk.y)));
-  Stream s;
-  s.init_with_block0(seed, t, d, w, tag, blk, 0);
-  return poisson_ptrs(rate, s);
-}
+// Deferred exact draws: one record per (nonzero, topic slice) that has at
+// least one draw the fast path could not decide (PTRS range lambda >= 9.5,
+// an ambiguous comparison, z > 40, or non-finite / tiny inputs).
+struct Deferred {
+  int64_t p;          // batch nonzero index
+  int32_t b, w, c;    // batch row, word id, token count
+  int32_t kbase;      // first topic of the slice
+  uint32_t mask[8];   // bit lane of mask[j]: topic kbase + lane + 32 j
+};
 
-template <int KPL>
-__global__ void __launch_bounds__(kFastBlock) k_sample_fast(
-    BatchView bv, const double* __restrict__ theta_b64, const float* __restrict__ theta_b32,
-    const double* __restrict__ phi64, const float* __restrict__ phi32,
+template <int KPL, bool FULL>
+__global__ void __launch_bounds__(kFastBlock, 2) k_sample_fast(
+    BatchView bv, const float* __restrict__ theta_b32, const float* __restrict__ phi32,
     const double* __restrict__ mu_in, int K, double m_t, uint64_t seed, uint32_t t,
     uint32_t sweep, int64_t chunk, int n_slices, unsigned long long* __restrict__ theta_counts,
-    unsigned long long* __restrict__ phi_counts, int* __restrict__ err) {
+    unsigned long long* __restrict__ phi_counts, Deferred* __restrict__ deferred,
+    unsigned long long* __restrict__ n_deferred) {
   const int lane = threadIdx.x & 31;
   const int64_t gw = (blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x) >> 5;
   const int64_t item = gw / n_slices;
@@ -309,17 +285,14 @@ __global__ void __launch_bounds__(kFastBlock) k_sample_fast(
   if (p0 >= bv.nnz) return;
   const int64_t p1 = min(p0 + chunk, bv.nnz);
   const int kbase = slice * kWarp * KPL;
-  const double uniform_weight = 1.0 / static_cast<double>(K);
   const int have_mu = mu_in != nullptr;
 
-  // per-topic stream keys and the round-2 product M1 * (t ^ k1), fixed for the
-  // whole item
-  uint32_t key0[KPL], key1[KPL], p2lo[KPL], p2hi[KPL];
+  // per-topic stream keys, fixed for the whole item
+  uint32_t key0[KPL], key1[KPL];
 #pragma unroll
   for (int j = 0; j < KPL; ++j) {
     const uint32_t k = static_cast<uint32_t>(kbase + lane + kWarp * j);
     stream_key(seed, make_tag(kPoissonCounts, sweep, k), key0[j], key1[j]);
-    mulhilo(kPhiloxM1, t ^ key1[j], p2lo[j], p2hi[j]);
   }
 
   int64_t cur_b = -1;
@@ -345,6 +318,17 @@ __global__ void __launch_bounds__(kFastBlock) k_sample_fast(
       if (have_mu) mu_v = __ldg(mu_in + p);
     }
     const int n_here = static_cast<int>(min(static_cast<int64_t>(kWarp), p1 - g0));
+    // software pipeline: phi slice of nonzero i+1 is in flight while i draws
+    float ph_next[KPL];
+    {
+      const int32_t w0 = __shfl_sync(0xffffffffu, w, 0);
+      const float* prow = phi32 + static_cast<int64_t>(w0) * K;
+#pragma unroll
+      for (int j = 0; j < KPL; ++j) {
+        const int k = kbase + lane + kWarp * j;
+        ph_next[j] = (FULL || k < K) ? __ldg(prow + k) : 0.0f;
+      }
+    }
     for (int i = 0; i < n_here; ++i) {
       const int64_t bi = __shfl_sync(0xffffffffu, b, i);
       const int32_t dl = __shfl_sync(0xffffffffu, d, i);
@@ -352,89 +336,116 @@ __global__ void __launch_bounds__(kFastBlock) k_sample_fast(
       const int32_t wi = __shfl_sync(0xffffffffu, w, i);
       const int32_t ci = __shfl_sync(0xffffffffu, c, i);
       const double mui = __shfl_sync(0xffffffffu, mu_v, i);
+      float ph[KPL];
+#pragma unroll
+      for (int j = 0; j < KPL; ++j) ph[j] = ph_next[j];
+      {
+        const int32_t wn = __shfl_sync(0xffffffffu, w, (i + 1) & 31);
+        if (i + 1 < n_here) {
+          const float* prow = phi32 + static_cast<int64_t>(wn) * K;
+#pragma unroll
+          for (int j = 0; j < KPL; ++j) {
+            const int k = kbase + lane + kWarp * j;
+            ph_next[j] = (FULL || k < K) ? __ldg(prow + k) : 0.0f;
+          }
+        }
+      }
       if (bi != cur_b) {
         if (cur_b >= 0) {
 #pragma unroll
           for (int j = 0; j < KPL; ++j) {
             const int k = kbase + lane + kWarp * j;
-            if (k < K && acc[j]) atomicAdd(theta_counts + cur_b * K + k, static_cast<unsigned long long>(acc[j]));
+            if ((FULL || k < K) && acc[j])
+              atomicAdd(theta_counts + cur_b * K + k, static_cast<unsigned long long>(acc[j]));
           }
         }
         cur_b = bi;
 #pragma unroll
         for (int j = 0; j < KPL; ++j) {
           const int k = kbase + lane + kWarp * j;
-          th[j] = k < K ? __ldg(theta_b32 + bi * K + k) : 0.0f;
+          th[j] = (FULL || k < K) ? __ldg(theta_b32 + bi * K + k) : 0.0f;
           acc[j] = 0u;
         }
       }
-      const float* prow = phi32 + static_cast<int64_t>(wi) * K;
       float prod[KPL];
       float part = 0.0f;
 #pragma unroll
       for (int j = 0; j < KPL; ++j) {
-        const int k = kbase + lane + kWarp * j;
-        prod[j] = k < K ? __fmul_rn(th[j], __ldg(prow + k)) : 0.0f;
+        prod[j] = __fmul_rn(th[j], ph[j]);
         part = __fadd_rn(part, prod[j]);
       }
       float mu_f;
       if (have_mu) {
         mu_f = __double2float_rn(mui);
       } else {
-        // slices of a wide K each see a partial sum only: use the exact path
         mu_f = part;
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) mu_f = __fadd_rn(mu_f, __shfl_xor_sync(0xffffffffu, mu_f, o));
-        if (n_slices > 1) mu_f = 0.0f;
+        if (n_slices > 1) mu_f = 0.0f;  // partial sums only: defer the nonzero
       }
-      const double cs = __dmul_rn(m_t, static_cast<double>(ci));
       const bool nz_exact = !(mu_f >= 1e-20f) || isinf(mu_f);
-      const float scale = __fdiv_rn(__double2float_rn(cs), mu_f);
+      const float scale = __fdividef(__double2float_rn(__dmul_rn(m_t, static_cast<double>(ci))), mu_f);
       uint32_t m1lo, m1hi;
       mulhilo(kPhiloxM1, di, m1lo, m1hi);
       const Philox1 r1{m1hi ^ static_cast<uint32_t>(wi), m1lo};
-      double mu_cache = 0.0;
-      int mu_valid = 0;
+      // phase 1: every topic's uniform (independent Philox chains -> ILP)
+      uint32_t y[KPL];
+#pragma unroll
+      for (int j = 0; j < KPL; ++j) {
+        uint32_t p2lo, p2hi;
+        mulhilo(kPhiloxM1, t ^ key1[j], p2lo, p2hi);
+        y[j] = philox_y(r1, key0[j], key1[j], p2lo, p2hi);
+      }
+      // phase 2: decisions; undecidable draws are deferred
+      uint32_t defer_bits = 0;
 #pragma unroll
       for (int j = 0; j < KPL; ++j) {
         const int k = kbase + lane + kWarp * j;
-        if (k >= K) continue;
         const float lam = __fmul_rn(prod[j], scale);
-        long long z = 0;
+        int z = 0;
         bool exact = nz_exact || !(prod[j] >= 1e-30f) || !(lam < 9.5f);
-        if (!exact) {
-          const uint32_t y = philox_y(r1, key0[j], key1[j], p2lo[j], p2hi[j]);
-          const float u = __uint2float_rn(y) * 2.3283064365386963e-10f;
+        if (!FULL && k >= K) exact = false;
+        else if (!exact) {
+          // u in [u_f, u_f + 2^-23): top 23 bits of the high word, no I2F
+          const float u = __fsub_rn(__int_as_float(0x3f800000 | (y[j] >> 9)), 1.0f);
           float pmf = __expf(-lam);
           float cdf = pmf;
-          const float base = __fadd_rn(3e-6f, __fmul_rn(4e-6f, lam));
-          int kk = 0;
+          float r = __fadd_rn(4e-6f, __fmul_rn(4e-6f, lam));
           for (;;) {
-            const float r = __fadd_rn(base, __fmul_rn(4e-6f, static_cast<float>(kk)));
-            const float mrg = __fadd_rn(__fmul_rn(cdf, r), 1.2e-7f);
+            const float mrg = __fadd_rn(__fmul_rn(cdf, r), 2.5e-7f);
             if (u <= __fsub_rn(cdf, mrg)) break;
-            if (!(u > __fadd_rn(cdf, mrg)) || kk >= 40) {
+            if (!(u > __fadd_rn(cdf, mrg)) || z >= 40) {
               exact = true;
+              z = 0;
               break;
             }
-            ++kk;
-            pmf = __fmul_rn(pmf, __fdiv_rn(lam, static_cast<float>(kk)));
+            ++z;
+            pmf = __fmul_rn(pmf, __fdividef(lam, static_cast<float>(z)));
             cdf = __fadd_rn(cdf, pmf);
+            r = __fadd_rn(r, 6e-6f);
           }
-          z = kk;
-        }
-        if (exact) {
-          z = exact_draw(theta_b64 + bi * K, phi64 + static_cast<int64_t>(wi) * K, K, k, cs,
-                         uniform_weight, mui, have_mu, &mu_cache, &mu_valid, seed, t, di,
-                         static_cast<uint32_t>(wi), sweep);
-          if (z < 0) {
-            atomicOr(err, kErrNumerical);
-            z = 0;
+          if (z != 0) {
+            acc[j] += static_cast<uint32_t>(z);
+            atomicAdd(phi_counts + static_cast<int64_t>(wi) * K + k, static_cast<unsigned long long>(z));
           }
         }
-        if (z != 0) {
-          acc[j] += static_cast<uint32_t>(z);
-          atomicAdd(phi_counts + static_cast<int64_t>(wi) * K + k, static_cast<unsigned long long>(z));
+        if (exact) defer_bits |= 1u << j;
+      }
+      if (__any_sync(0xffffffffu, defer_bits != 0)) {
+        uint32_t masks[8];
+#pragma unroll
+        for (int j = 0; j < 8; ++j) masks[j] = j < KPL ? __ballot_sync(0xffffffffu, (defer_bits >> j) & 1u) : 0u;
+        if (lane == 0) {
+          const unsigned long long slot = atomicAdd(n_deferred, 1ull);
+          Deferred rec;
+          rec.p = g0 + i;
+          rec.b = static_cast<int32_t>(bi);
+          rec.w = wi;
+          rec.c = ci;
+          rec.kbase = kbase;
+#pragma unroll
+          for (int j = 0; j < 8; ++j) rec.mask[j] = masks[j];
+          deferred[slot] = rec;
         }
       }
     }
@@ -443,7 +454,72 @@ __global__ void __launch_bounds__(kFastBlock) k_sample_fast(
 #pragma unroll
     for (int j = 0; j < KPL; ++j) {
       const int k = kbase + lane + kWarp * j;
-      if (k < K && acc[j]) atomicAdd(theta_counts + cur_b * K + k, static_cast<unsigned long long>(acc[j]));
+      if ((FULL || k < K) && acc[j])
+        atomicAdd(theta_counts + cur_b * K + k, static_cast<unsigned long long>(acc[j]));
+    }
+  }
+}
+
+// One warp per deferred record: exact mu (sequential k order, coalesced row
+// loads, warp-broadcast add chain) unless the caller supplied mu, then each
+// flagged draw exactly as k_sample: __ddiv_rn rate, full Philox block, exact
+// inversion or PTRS (rng.cpp:39-86).
+__global__ void __launch_bounds__(256) k_sample_deferred(
+    BatchView bv, const double* __restrict__ theta_b64, const double* __restrict__ phi64,
+    const double* __restrict__ mu_in, int K, double m_t, uint64_t seed, uint32_t t,
+    uint32_t sweep, const Deferred* __restrict__ deferred,
+    const unsigned long long* __restrict__ n_deferred,
+    unsigned long long* __restrict__ theta_counts, unsigned long long* __restrict__ phi_counts,
+    int* __restrict__ err) {
+  const int lane = threadIdx.x & 31;
+  const int64_t n = static_cast<int64_t>(*n_deferred);
+  const double uniform_weight = 1.0 / static_cast<double>(K);
+  for (int64_t r = (blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x) >> 5; r < n;
+       r += (static_cast<int64_t>(gridDim.x) * blockDim.x) >> 5) {
+    const Deferred rec = deferred[r];
+    const double* th = theta_b64 + static_cast<int64_t>(rec.b) * K;
+    const double* ph = phi64 + static_cast<int64_t>(rec.w) * K;
+    double mu;
+    if (mu_in) {
+      mu = mu_in[rec.p];
+    } else {
+      mu = 0.0;
+      for (int k0 = 0; k0 < K; k0 += 32) {
+        const int k = k0 + lane;
+        const double prod = k < K ? __dmul_rn(__ldg(th + k), __ldg(ph + k)) : 0.0;
+        const int m = min(32, K - k0);
+        for (int l = 0; l < m; ++l) mu = __dadd_rn(mu, __shfl_sync(0xffffffffu, prod, l));
+      }
+    }
+    const uint32_t d = static_cast<uint32_t>(__ldg(bv.batch_docs + rec.b) + bv.doc_base);
+    const double cs = __dmul_rn(m_t, static_cast<double>(rec.c));
+    const bool degenerate = mu < 1e-30;
+    for (int j = 0; j < 8; ++j) {
+      if (!((rec.mask[j] >> lane) & 1u)) continue;
+      const int k = rec.kbase + lane + 32 * j;
+      const double weight = degenerate ? uniform_weight : __ddiv_rn(__dmul_rn(__ldg(th + k), __ldg(ph + k)), mu);
+      const double rate = __dmul_rn(weight, cs);
+      if (!(rate >= 0.0) || isinf(rate)) {
+        atomicOr(err, kErrNumerical);
+        continue;
+      }
+      if (rate == 0.0) continue;
+      const uint32_t tag = make_tag(kPoissonCounts, sweep, static_cast<uint32_t>(k));
+      uint32_t k0, k1;
+      stream_key(seed, tag, k0, k1);
+      const U4 blk = philox10(U4{0u, static_cast<uint32_t>(rec.w), d, t}, k0, k1);
+      long long z;
+      if (rate < 10.0) {
+        z = poisson_inversion(rate, u64_to_uniform(join64(blk.x, blk.y)));
+      } else {
+        Stream s;
+        s.init_with_block0(seed, t, d, static_cast<uint32_t>(rec.w), tag, blk, 0);
+        z = poisson_ptrs(rate, s);
+      }
+      if (z != 0) {
+        atomicAdd(theta_counts + static_cast<int64_t>(rec.b) * K + k, static_cast<unsigned long long>(z));
+        atomicAdd(phi_counts + static_cast<int64_t>(rec.w) * K + k, static_cast<unsigned long long>(z));
+      }
     }
   }
 }
@@ -452,14 +528,22 @@ template <int KPL>
 int launch_fast_kpl(const BatchView& bv, const double* tb64, const float* tb32, const double* phi64,
                     const float* phi32, const double* mu, int K, double m_t, uint64_t seed,
                     uint32_t t, uint32_t sweep, unsigned long long* tc, unsigned long long* pc,
-                    int* err, cudaStream_t st) {
+                    void* deferred, unsigned long long* n_deferred, int* err, cudaStream_t st) {
   const int n_slices = (K + kWarp * KPL - 1) / (kWarp * KPL);
   const int64_t chunk = 128;
   const int64_t items = (bv.nnz + chunk - 1) / chunk;
   const int64_t threads = items * n_slices * kWarp;
-  k_sample_fast<KPL><<<grid_for(threads, kFastBlock), kFastBlock, 0, st>>>(
-      bv, tb64, tb32, phi64, phi32, mu, K, m_t, seed, t, sweep, chunk, n_slices, tc, pc, err);
-  return 1;
+  cudaMemsetAsync(n_deferred, 0, sizeof(unsigned long long), st);
+  auto* rec = static_cast<Deferred*>(deferred);
+  if (K % (kWarp * KPL) == 0)
+    k_sample_fast<KPL, true><<<grid_for(threads, kFastBlock), kFastBlock, 0, st>>>(
+        bv, tb32, phi32, mu, K, m_t, seed, t, sweep, chunk, n_slices, tc, pc, rec, n_deferred);
+  else
+    k_sample_fast<KPL, false><<<grid_for(threads, kFastBlock), kFastBlock, 0, st>>>(
+        bv, tb32, phi32, mu, K, m_t, seed, t, sweep, chunk, n_slices, tc, pc, rec, n_deferred);
+  k_sample_deferred<<<148 * 8, 256, 0, st>>>(bv, tb64, phi64, mu, K, m_t, seed, t, sweep, rec,
+                                             n_deferred, tc, pc, err);
+  return 2;
 }
 
 // ------------------------------------------------------------------- M-step
@@ -815,23 +899,25 @@ int launch_sample(const BatchView& bv, const double* theta_batch, const double* 
                               tf, pf, err, st);
 }
 
+int64_t deferred_record_bytes() { return static_cast<int64_t>(sizeof(Deferred)); }
+
 int launch_sample_fast(const BatchView& bv, const double* theta_b64, const float* theta_b32,
                        const double* phi64, const float* phi32, const double* mu, int K,
                        double m_t, uint64_t seed, uint32_t t, uint32_t sweep,
-                       unsigned long long* tc, unsigned long long* pc, int* err,
-                       cudaStream_t st) {
+                       unsigned long long* tc, unsigned long long* pc, void* deferred,
+                       unsigned long long* n_deferred, int* err, cudaStream_t st) {
   if (bv.nnz == 0) return 0;
   if (K <= 32)
     return launch_fast_kpl<1>(bv, theta_b64, theta_b32, phi64, phi32, mu, K, m_t, seed, t, sweep,
-                              tc, pc, err, st);
+                              tc, pc, deferred, n_deferred, err, st);
   if (K <= 64)
     return launch_fast_kpl<2>(bv, theta_b64, theta_b32, phi64, phi32, mu, K, m_t, seed, t, sweep,
-                              tc, pc, err, st);
+                              tc, pc, deferred, n_deferred, err, st);
   if (K <= 128)
     return launch_fast_kpl<4>(bv, theta_b64, theta_b32, phi64, phi32, mu, K, m_t, seed, t, sweep,
-                              tc, pc, err, st);
+                              tc, pc, deferred, n_deferred, err, st);
   return launch_fast_kpl<8>(bv, theta_b64, theta_b32, phi64, phi32, mu, K, m_t, seed, t, sweep,
-                            tc, pc, err, st);
+                            tc, pc, deferred, n_deferred, err, st);
 }
 
 int launch_theta_from_counts(const unsigned long long* cu, const double* cf, int64_t n,

@@ -40,8 +40,9 @@ SCU_HD uint32_t make_tag(uint32_t purpose, uint32_t sub, uint32_t index) {
 
 SCU_HD void mulhilo(uint32_t a, uint32_t b, uint32_t& lo, uint32_t& hi) {
 #if defined(__CUDA_ARCH__)
-  lo = a * b;
-  hi = __umulhi(a, b);
+  const uint64_t p = static_cast<uint64_t>(a) * b;  // one IMAD.WIDE.U32
+  lo = static_cast<uint32_t>(p);
+  hi = static_cast<uint32_t>(p >> 32);
 #else
   const uint64_t p = static_cast<uint64_t>(a) * b;
   lo = static_cast<uint32_t>(p);
