@@ -184,9 +184,11 @@ int samelda_cu_set_doc_base(samelda_cu_ctx* ctx, int64_t doc_base);
 /* CUDA-event timing of the period kernels (0 sample, 1 sddmm, 2 M-step). */
 int samelda_cu_profile(samelda_cu_ctx* ctx, int32_t enable);
 /* ms_out[3] summed event time, launches_out[3] launches timed; batch nonzeros
- * and docs seen by the timed sample launches.  Resets the accumulators. */
+ * and docs seen by the timed sample launches, and the deferred exact-draw
+ * records they produced (profiling synchronises after every sample launch to
+ * read that count).  Resets the accumulators. */
 int samelda_cu_profile_read(samelda_cu_ctx* ctx, double* ms_out, int64_t* launches_out,
-                            int64_t* nnz_sampled, int64_t* docs_sampled);
+                            int64_t* nnz_sampled, int64_t* docs_sampled, int64_t* deferred);
 /* copy the batch theta rows (B x K, f64, batch order) of the last period */
 int samelda_cu_batch_theta(samelda_cu_ctx* ctx, double* out, int64_t cap);
 /* sums of the last sweep's integer theta and phi counts (mass balance) */

@@ -268,7 +268,7 @@ struct samelda_cu_ctx {
   enum { kSample = 0, kSddmm = 1, kMstep = 2, kKinds = 3 };
   std::vector<std::pair<cudaEvent_t, cudaEvent_t>> events[kKinds];
   size_t events_used[kKinds] = {0, 0, 0};
-  int64_t prof_nnz = 0, prof_docs = 0;
+  int64_t prof_nnz = 0, prof_docs = 0, prof_deferred = 0;
 
   void tick(int kind, bool start) {
     if (!profile) return;
@@ -416,6 +416,12 @@ struct samelda_cu_ctx {
                                           static_cast<uint32_t>(sweep), tc_, pc_, rec,
                                           ensure<unsigned long long>(n_deferred, 1), d_err(), stream);
       tick(kSample, false);
+      if (profile) {
+        unsigned long long nd = 0;
+        ck(cudaMemcpyAsync(&nd, n_deferred.p, sizeof(nd), cudaMemcpyDeviceToHost, stream), "n_deferred");
+        ck(cudaStreamSynchronize(stream), "n_deferred");
+        prof_deferred += static_cast<int64_t>(nd);
+      }
     }
   }
 
@@ -929,12 +935,12 @@ int samelda_cu_profile(samelda_cu_ctx* ctx, int32_t enable) {
   return guarded(ctx, [&] {
     ctx->profile = enable != 0;
     for (auto& u : ctx->events_used) u = 0;
-    ctx->prof_nnz = ctx->prof_docs = 0;
+    ctx->prof_nnz = ctx->prof_docs = ctx->prof_deferred = 0;
   });
 }
 
 int samelda_cu_profile_read(samelda_cu_ctx* ctx, double* ms_out, int64_t* launches_out,
-                            int64_t* nnz_sampled, int64_t* docs_sampled) {
+                            int64_t* nnz_sampled, int64_t* docs_sampled, int64_t* deferred) {
   return guarded(ctx, [&] {
     ck(cudaStreamSynchronize(ctx->stream), "profile sync");
     for (int k = 0; k < samelda_cu_ctx::kKinds; ++k) {
@@ -950,7 +956,8 @@ int samelda_cu_profile_read(samelda_cu_ctx* ctx, double* ms_out, int64_t* launch
     }
     *nnz_sampled = ctx->prof_nnz;
     *docs_sampled = ctx->prof_docs;
-    ctx->prof_nnz = ctx->prof_docs = 0;
+    if (deferred) *deferred = ctx->prof_deferred;
+    ctx->prof_nnz = ctx->prof_docs = ctx->prof_deferred = 0;
   });
 }
 

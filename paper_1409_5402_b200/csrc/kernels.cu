@@ -5,6 +5,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <cstdlib>
 
 #include "kernels.cuh"
 #include "philox.cuh"
@@ -216,9 +217,9 @@ __global__ void __launch_bounds__(kSampleBlock) k_sample(
 // inversion or PTRS.  Error budget (u32 = 2^-24 unit roundoff):
 //   lambda_f: theta, phi rounded to f32 (2u), product (u), mu by tree sum of
 //     positive terms (<= 16u), cs/mu (3u), lambda (u)  -> |dl| <= 1.5e-6 lambda
-//   exp:  __expf max error (2 + 1.2 lambda) ulp       -> <= (1.2e-7 + 7e-8 lambda)
-//   step k: pmf *= lambda/k (+ dl + 3u), cdf += pmf (+u)
-//   __fdividef steps add <= 2 ulp each
+//   exp:  ex2.approx of -lambda*log2(e): 2^-22 rel + lambda * 2u from the
+//         argument rounding                           -> <= (2.4e-7 + 1.2e-7 lambda)
+//   step k: pmf *= lambda * rcp.approx(k) (+ dl + 4u), cdf += pmf (+u)
 //   r = 4e-6 + 4e-6 lambda + 6e-6 k  (>= 2x the sum above);  u from the top
 //   23 bits of the high word: u - u_f in [0, 2^-23) -> m = cdf * r + 2.5e-7.
 // The mu used is the caller's mu array when given (per-call sample_counts),
@@ -226,6 +227,19 @@ __global__ void __launch_bounds__(kSampleBlock) k_sample(
 // sequential sum on fallback, cached per lane and nonzero).
 
 constexpr int kFastBlock = 256;
+
+// MUFU-only transcendentals (no denormal range fix-ups: arguments here are
+// in [-13.7, 0] and [1, 40]); their error is inside the fast-path budget.
+__device__ __forceinline__ float ex2_approx(float x) {
+  float y;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+__device__ __forceinline__ float rcp_approx(float x) {
+  float y;
+  asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
 
 struct Philox1 {
   // round-1 specialisation for counter {0, w, d, t}: M0 * 0 = 0, so the
@@ -269,6 +283,410 @@ struct Deferred {
   int32_t kbase;      // first topic of the slice
   uint32_t mask[8];   // bit lane of mask[j]: topic kbase + lane + 32 j
 };
+
+// Lane = nonzero.  A warp owns 32 consecutive batch nonzeros and walks the
+// topics in chunks of 32; the topic index is warp-uniform, so the per-topic
+// stream keys (and the round-2 product M1 * (t ^ k1)) live in uniform
+// registers and a draw costs ~31 vector instructions of Philox.
+//   phase A: mu of every nonzero (lanes over topics, f32 tree), kept by its lane
+//   phase B, per chunk: phi[w_lane, chunk] staged through a swizzled shared
+//     tile (32 coalesced row loads), 32 draws per lane, z into a swizzled
+//     shared tile; then lanes over topics walk the 32 nonzeros in order:
+//     coalesced phi-count reductions and register theta accumulation per doc.
+// Round keys a draw of topic k needs in philox_y, precomputed once per topic:
+// ks[0] = k0, ks[1] = p2lo, ks[2] = p2hi (M1 * (t ^ k1)), then for r = 1..8
+// ks[1 + 2r] = k0 + r W0, ks[2 + 2r] = k1 + r W1 (ks[17] = k0 + 8 W0 unused).
+constexpr int kKeyWords = 20;
+
+__device__ __forceinline__ void topic_schedule(uint64_t seed, uint32_t t, uint32_t sweep,
+                                               uint32_t k, uint32_t* ks) {
+  uint32_t k0, k1;
+  stream_key(seed, make_tag(kPoissonCounts, sweep, k), k0, k1);
+  uint32_t p2lo, p2hi;
+  mulhilo(kPhiloxM1, t ^ k1, p2lo, p2hi);
+  ks[0] = k0;
+  ks[1] = p2lo;
+  ks[2] = p2hi;
+#pragma unroll
+  for (int r = 1; r <= 8; ++r) {
+    ks[1 + 2 * r] = k0 + static_cast<uint32_t>(r) * kPhiloxW0;
+    ks[2 + 2 * r] = k1 + static_cast<uint32_t>(r) * kPhiloxW1;
+  }
+  ks[19] = 0;
+}
+
+__device__ __forceinline__ uint32_t philox_y_sched(const Philox1 r1, const uint32_t* ks) {
+  uint32_t lo0, hi0;
+  mulhilo(kPhiloxM0, r1.hw ^ ks[0], lo0, hi0);
+  uint32_t x0 = ks[2] ^ r1.lo ^ ks[3], x1 = ks[1], x2 = hi0 ^ ks[4], x3 = lo0;
+#pragma unroll
+  for (int r = 2; r < 9; ++r) {
+    uint32_t a0, b0, a1, b1;
+    mulhilo(kPhiloxM0, x0, a0, b0);
+    mulhilo(kPhiloxM1, x2, a1, b1);
+    const uint32_t n0 = b1 ^ x1 ^ ks[1 + 2 * r], n2 = b0 ^ x3 ^ ks[2 + 2 * r];
+    x0 = n0;
+    x1 = a1;
+    x2 = n2;
+    x3 = a0;
+  }
+  return kPhiloxM1 * x2;
+}
+
+constexpr int kNzWarps = 4;
+
+__global__ void __launch_bounds__(kNzWarps * 32) k_sample_nz(
+    BatchView bv, const float* __restrict__ theta_b32, const float* __restrict__ phi32,
+    const double* __restrict__ mu_in, int K, double m_t, uint64_t seed, uint32_t t,
+    uint32_t sweep, unsigned long long* __restrict__ theta_counts,
+    unsigned long long* __restrict__ phi_counts, Deferred* __restrict__ deferred,
+    unsigned long long* __restrict__ n_deferred) {
+  // per warp: lambda tile (row = nonzero, col = topic, xor-swizzled; each
+  // entry is overwritten by its draw's z), deferred masks, and the 32
+  // topics' round-key schedules
+  __shared__ float s_lam[kNzWarps][32 * 32];  // lambda, then z in place
+  __shared__ uint32_t s_mask[kNzWarps][32 * 8];
+  __shared__ __align__(16) uint32_t s_keys[kNzWarps][32 * kKeyWords];
+  const int lane = threadIdx.x & 31;
+  const int wib = threadIdx.x >> 5;
+  const int64_t g0 = (static_cast<int64_t>(blockIdx.x) * kNzWarps + wib) * 32;
+  if (g0 >= bv.nnz) return;
+  const int n_here = static_cast<int>(min(static_cast<int64_t>(32), bv.nnz - g0));
+  const int64_t p = g0 + lane;
+  const bool valid = lane < n_here;
+  int64_t b = 0;
+  int32_t d = 0, w = 0, c = 0;
+  if (valid) {
+    b = find_row(bv.batch_prefix, bv.B, p);
+    d = __ldg(bv.batch_docs + b);
+    const int64_t gi = __ldg(bv.doc_offsets + d) + (p - __ldg(bv.batch_prefix + b));
+    w = __ldg(bv.word_ids + gi);
+    c = __ldg(bv.counts + gi);
+  }
+  // ---- phase A: mu (f32), lane r keeps nonzero r's
+  float my_mu = 0.0f;
+  if (mu_in != nullptr) {
+    my_mu = valid ? __double2float_rn(__ldg(mu_in + p)) : 1.0f;
+  } else {
+    for (int r = 0; r < n_here; ++r) {
+      const int64_t br = __shfl_sync(0xffffffffu, b, r);
+      const int32_t wr = __shfl_sync(0xffffffffu, w, r);
+      const float* tr = theta_b32 + br * K;
+      const float* pr = phi32 + static_cast<int64_t>(wr) * K;
+      float part = 0.0f;
+      for (int k = lane; k < K; k += 32) part = __fadd_rn(part, __fmul_rn(__ldg(tr + k), __ldg(pr + k)));
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) part = __fadd_rn(part, __shfl_xor_sync(0xffffffffu, part, o));
+      if (lane == r) my_mu = part;
+    }
+  }
+  // lane flags: 0 fast, 1 all draws exact (mu unusable), 2 no draws (padding)
+  const int lane_mode = !valid ? 2 : ((!(my_mu >= 1e-20f) || isinf(my_mu)) ? 1 : 0);
+  const float scale = __fdividef(__double2float_rn(__dmul_rn(m_t, static_cast<double>(c))), my_mu);
+  const uint32_t dg = static_cast<uint32_t>(d + bv.doc_base);
+  uint32_t m1lo, m1hi;
+  mulhilo(kPhiloxM1, dg, m1lo, m1hi);
+  const Philox1 r1{m1hi ^ static_cast<uint32_t>(w), m1lo};
+  float* lt = s_lam[wib];
+  uint32_t* zt = reinterpret_cast<uint32_t*>(s_lam[wib]);
+  uint32_t* mk = s_mask[wib];
+  uint32_t* keys = s_keys[wib];
+  const int n_chunks = (K + 31) / 32;
+  for (int kc = 0; kc < n_chunks; ++kc) {
+    const int kbase = kc * 32;
+    const int k_lane = kbase + lane;
+    // ---- stage: lanes over topics.  lambda = (theta * phi) * scale exactly as
+    // the fast path defines it; -1 marks an exact (deferred) draw, -2 padding.
+    {
+      uint32_t ks[kKeyWords];
+      topic_schedule(seed, t, sweep, static_cast<uint32_t>(k_lane), ks);
+      uint4* kd = reinterpret_cast<uint4*>(keys + lane * kKeyWords);
+#pragma unroll
+      for (int q = 0; q < kKeyWords / 4; ++q) kd[q] = make_uint4(ks[4 * q], ks[4 * q + 1], ks[4 * q + 2], ks[4 * q + 3]);
+    }
+    for (int r = 0; r < 32; ++r) {
+      const int64_t br = __shfl_sync(0xffffffffu, b, r);
+      const int32_t wr = __shfl_sync(0xffffffffu, w, r);
+      const float sr = __shfl_sync(0xffffffffu, scale, r);
+      const int mr = __shfl_sync(0xffffffffu, lane_mode, r);
+      float v = -2.0f;
+      if (mr != 2 && k_lane < K) {
+        const float prod = __fmul_rn(__ldg(theta_b32 + br * K + k_lane),
+                                     __ldg(phi32 + static_cast<int64_t>(wr) * K + k_lane));
+        const float lam = __fmul_rn(prod, sr);
+        v = (mr == 0 && prod >= 1e-30f && lam < 9.5f) ? lam : -1.0f;
+      }
+      lt[r * 32 + (lane ^ r)] = v;
+    }
+    __syncwarp();
+    // ---- draw: lane = nonzero, kk = topic (uniform)
+    uint32_t defer_mask = 0;
+    const int kk_end = min(32, K - kbase);
+    for (int kk = 0; kk < kk_end; ++kk) {
+      const float lam = lt[lane * 32 + (kk ^ lane)];
+      uint32_t ks[kKeyWords];
+      const uint4* kd = reinterpret_cast<const uint4*>(keys + kk * kKeyWords);
+#pragma unroll
+      for (int q = 0; q < kKeyWords / 4; ++q) {
+        const uint4 v4 = kd[q];
+        ks[4 * q] = v4.x;
+        ks[4 * q + 1] = v4.y;
+        ks[4 * q + 2] = v4.z;
+        ks[4 * q + 3] = v4.w;
+      }
+      const uint32_t y = philox_y_sched(r1, ks);
+      uint32_t z = 0;
+      if (lam >= 0.0f) {
+        // u in [u_f, u_f + 2^-23): top 23 bits of the high word, no I2F
+        const float u = __fsub_rn(__int_as_float(0x3f800000 | (y >> 9)), 1.0f);
+        float pmf = ex2_approx(__fmul_rn(lam, -1.4426950408889634f));
+        float cdf = pmf;
+        // thresholds cdf * (1 -+ r) -+ 2.5e-7, r = 4e-6 + 4e-6 lam + 6e-6 z
+        float rlo = __fsub_rn(1.0f - 4e-6f, __fmul_rn(4e-6f, lam));
+        float rhi = __fadd_rn(1.0f + 4e-6f, __fmul_rn(4e-6f, lam));
+        float zf = 0.0f;
+        for (;;) {
+          if (u <= __fmaf_rn(cdf, rlo, -2.5e-7f)) break;
+          if (!(u > __fmaf_rn(cdf, rhi, 2.5e-7f)) || z >= 40) {
+            defer_mask |= 1u << kk;
+            z = 0;
+            break;
+          }
+          ++z;
+          zf = __fadd_rn(zf, 1.0f);
+          pmf = __fmul_rn(pmf, __fmul_rn(lam, rcp_approx(zf)));
+          cdf = __fadd_rn(cdf, pmf);
+          rlo = __fsub_rn(rlo, 6e-6f);
+          rhi = __fadd_rn(rhi, 6e-6f);
+        }
+      } else if (lam == -1.0f) {
+        defer_mask |= 1u << kk;
+      }
+      zt[lane * 32 + (kk ^ lane)] = z;
+    }
+    mk[lane * 8 + (kc & 7)] = defer_mask;
+    __syncwarp();
+    // ---- scatter: lanes over topics, nonzeros in order (sampler.cpp:183-189)
+    {
+      int64_t cb = -1;
+      uint32_t acc = 0;
+      const bool in_range = k_lane < K;  // lanes past K hold stale tile entries
+      for (int r = 0; r < n_here; ++r) {
+        const uint32_t zr = in_range ? zt[r * 32 + (lane ^ r)] : 0u;
+        const int64_t br = __shfl_sync(0xffffffffu, b, r);
+        const int32_t wr = __shfl_sync(0xffffffffu, w, r);
+        if (br != cb) {
+          if (acc) atomicAdd(theta_counts + cb * K + k_lane, static_cast<unsigned long long>(acc));
+          cb = br;
+          acc = 0;
+        }
+        if (zr) {
+          atomicAdd(phi_counts + static_cast<int64_t>(wr) * K + k_lane, static_cast<unsigned long long>(zr));
+          acc += zr;
+        }
+      }
+      if (acc) atomicAdd(theta_counts + cb * K + k_lane, static_cast<unsigned long long>(acc));
+    }
+    // deferred records per 256-topic block (same layout k_sample_deferred reads)
+    if ((kc & 7) == 7 || kc == n_chunks - 1) {
+      __syncwarp();
+      uint32_t any = 0;
+#pragma unroll
+      for (int j = 0; j < 8; ++j) any |= (j <= (kc & 7)) ? mk[lane * 8 + j] : 0u;
+      const uint32_t ball = __ballot_sync(0xffffffffu, any != 0);
+      if (ball) {
+        unsigned long long base = 0;
+        if (lane == 0) base = atomicAdd(n_deferred, static_cast<unsigned long long>(__popc(ball)));
+        base = __shfl_sync(0xffffffffu, base, 0);
+        if (any) {
+          Deferred rec;
+          rec.p = p;
+          rec.b = static_cast<int32_t>(b);
+          rec.w = w;
+          rec.c = c;
+          rec.kbase = (kc & ~7) * 32;
+#pragma unroll
+          for (int j = 0; j < 8; ++j) rec.mask[j] = (j <= (kc & 7)) ? mk[lane * 8 + j] : 0u;
+          deferred[base + __popc(ball & ((1u << lane) - 1u))] = rec;
+        }
+      }
+    }
+    __syncwarp();
+  }
+}
+
+// CTA = ceil(K/32) warps (K <= 1024); warp v owns topics [32v, 32v + 32) of
+// every nonzero the CTA processes, so a lane's topic -- and with it the
+// whole Philox round-key schedule -- is fixed for the kernel's lifetime and
+// lives in 18 registers (no per-draw key arithmetic).  Per group of 32
+// nonzeros: every lane forms its 32 products theta*phi, a warp transpose-
+// reduce (31 shuffles) leaves nonzero i's slice sum in lane i, the slices
+// are combined through shared memory after one barrier, then each warp draws
+// its 32 topics for the 32 nonzeros in order.
+constexpr int kCtaMaxWarps = 32;
+
+template <int NW>
+__device__ __forceinline__ float transpose_reduce(float (&v)[32], int lane) {
+  // after step s each lane holds partial sums for 32/2^s values
+#pragma unroll
+  for (int half = 16; half >= 1; half >>= 1) {
+    const bool upper = (lane & half) != 0;
+#pragma unroll
+    for (int i = 0; i < half; ++i) {
+      const float send = upper ? v[i] : v[i + half];
+      const float keep = upper ? v[i + half] : v[i];
+      v[i] = __fadd_rn(keep, __shfl_xor_sync(0xffffffffu, send, half));
+    }
+  }
+  return v[0];  // sum over lanes of original v[lane]
+}
+
+template <int MAXW>
+__global__ void __launch_bounds__(MAXW * 32) k_sample_cta(
+    BatchView bv, const float* __restrict__ theta_b32, const float* __restrict__ phi32,
+    const double* __restrict__ mu_in, int K, int nwarps, double m_t, uint64_t seed, uint32_t t,
+    uint32_t sweep, int64_t chunk, unsigned long long* __restrict__ theta_counts,
+    unsigned long long* __restrict__ phi_counts, Deferred* __restrict__ deferred,
+    unsigned long long* __restrict__ n_deferred) {
+  __shared__ float s_part[MAXW][33];
+  __shared__ uint32_t s_mask[32][MAXW + 1];
+  const int lane = threadIdx.x & 31;
+  const int wv = threadIdx.x >> 5;
+  const int k = wv * 32 + lane;
+  const bool k_ok = k < K;
+  const int64_t c0 = static_cast<int64_t>(blockIdx.x) * chunk;
+  const int64_t c1 = min(c0 + chunk, bv.nnz);
+  uint32_t ks[kKeyWords];
+  topic_schedule(seed, t, sweep, static_cast<uint32_t>(k), ks);
+  int64_t cur_b = -1;
+  float th = 0.0f;
+  uint32_t acc = 0;
+  for (int64_t g0 = c0; g0 < c1; g0 += 32) {
+    const int n_here = static_cast<int>(min(static_cast<int64_t>(32), c1 - g0));
+    // nonzero metadata, lane i <- nonzero g0 + i (every warp loads its own copy)
+    int64_t b = 0;
+    int32_t d = 0, w = 0, c = 0;
+    if (lane < n_here) {
+      const int64_t p = g0 + lane;
+      b = find_row(bv.batch_prefix, bv.B, p);
+      d = __ldg(bv.batch_docs + b);
+      const int64_t gi = __ldg(bv.doc_offsets + d) + (p - __ldg(bv.batch_prefix + b));
+      w = __ldg(bv.word_ids + gi);
+      c = __ldg(bv.counts + gi);
+    }
+    // products of this lane's topic for the 32 nonzeros
+    float prod[32];
+#pragma unroll
+    for (int i = 0; i < 32; ++i) {
+      const int64_t bi = __shfl_sync(0xffffffffu, b, i);
+      const int32_t wi = __shfl_sync(0xffffffffu, w, i);
+      float v = 0.0f;
+      if (i < n_here && k_ok) {
+        const float tk = __ldg(theta_b32 + bi * K + k);
+        v = __fmul_rn(tk, __ldg(phi32 + static_cast<int64_t>(wi) * K + k));
+      }
+      prod[i] = v;
+    }
+    float mu_lane;  // mu of nonzero g0 + lane
+    if (mu_in != nullptr) {
+      mu_lane = lane < n_here ? __double2float_rn(__ldg(mu_in + g0 + lane)) : 1.0f;
+    } else {
+      float tmp[32];
+#pragma unroll
+      for (int i = 0; i < 32; ++i) tmp[i] = prod[i];
+      // lane i ends with sum over lanes of tmp[i] -> warp-slice partial of nonzero i
+      const float part = transpose_reduce<32>(tmp, lane);
+      s_part[wv][lane] = part;
+      __syncthreads();
+      float mu = 0.0f;
+      for (int v = 0; v < nwarps; ++v) mu = __fadd_rn(mu, s_part[v][lane]);
+      mu_lane = mu;
+    }
+    const bool lane_exact = !(mu_lane >= 1e-20f) || isinf(mu_lane);
+    const float scale = __fdividef(__double2float_rn(__dmul_rn(m_t, static_cast<double>(c))), mu_lane);
+    const uint32_t dg = static_cast<uint32_t>(d + bv.doc_base);
+    uint32_t m1lo, m1hi;
+    mulhilo(kPhiloxM1, dg, m1lo, m1hi);
+    const uint32_t hw_lane = m1hi ^ static_cast<uint32_t>(w);
+#pragma unroll
+    for (int i = 0; i < 32; ++i) {
+      if (i >= n_here) break;
+      const int64_t bi = __shfl_sync(0xffffffffu, b, i);
+      const int32_t wi = __shfl_sync(0xffffffffu, w, i);
+      const float sc = __shfl_sync(0xffffffffu, scale, i);
+      const bool ex_i = __shfl_sync(0xffffffffu, lane_exact, i);
+      const Philox1 r1{__shfl_sync(0xffffffffu, hw_lane, i), __shfl_sync(0xffffffffu, m1lo, i)};
+      if (bi != cur_b) {
+        if (cur_b >= 0 && acc) atomicAdd(theta_counts + cur_b * K + k, static_cast<unsigned long long>(acc));
+        cur_b = bi;
+        acc = 0;
+      }
+      const float lam = __fmul_rn(prod[i], sc);
+      const uint32_t y = philox_y_sched(r1, ks);
+      bool exact = k_ok && (ex_i || !(prod[i] >= 1e-30f) || !(lam < 9.5f));
+      uint32_t z = 0;
+      if (k_ok && !exact) {
+        const float u = __fsub_rn(__int_as_float(0x3f800000 | (y >> 9)), 1.0f);
+        float pmf = ex2_approx(__fmul_rn(lam, -1.4426950408889634f));
+        float cdf = pmf;
+        float rlo = __fsub_rn(1.0f - 4e-6f, __fmul_rn(4e-6f, lam));
+        float rhi = __fadd_rn(1.0f + 4e-6f, __fmul_rn(4e-6f, lam));
+        float zf = 0.0f;
+        for (;;) {
+          if (u <= __fmaf_rn(cdf, rlo, -2.5e-7f)) break;
+          if (!(u > __fmaf_rn(cdf, rhi, 2.5e-7f)) || z >= 40) {
+            exact = true;
+            z = 0;
+            break;
+          }
+          ++z;
+          zf = __fadd_rn(zf, 1.0f);
+          pmf = __fmul_rn(pmf, __fmul_rn(lam, rcp_approx(zf)));
+          cdf = __fadd_rn(cdf, pmf);
+          rlo = __fsub_rn(rlo, 6e-6f);
+          rhi = __fadd_rn(rhi, 6e-6f);
+        }
+        if (z) {
+          acc += z;
+          atomicAdd(phi_counts + static_cast<int64_t>(wi) * K + k, static_cast<unsigned long long>(z));
+        }
+      }
+      const uint32_t m = __ballot_sync(0xffffffffu, exact);
+      if (lane == i) s_mask[i][wv] = m;
+    }
+    __syncthreads();
+    // deferred records: nonzero i handled by warp (i % nwarps), lane 0
+    for (int i = wv; i < n_here; i += nwarps) {
+      for (int blk = 0; blk * 8 < nwarps; ++blk) {
+        uint32_t mk[8];
+        uint32_t any = 0;
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+          const int v = blk * 8 + j;
+          mk[j] = v < nwarps ? s_mask[i][v] : 0u;
+          any |= mk[j];
+        }
+        if (any && lane == 0) {
+          const unsigned long long slot = atomicAdd(n_deferred, 1ull);
+          Deferred rec;
+          rec.p = g0 + i;
+          const int64_t p = g0 + i;
+          rec.b = static_cast<int32_t>(find_row(bv.batch_prefix, bv.B, p));
+          const int32_t dd = __ldg(bv.batch_docs + rec.b);
+          const int64_t gi = __ldg(bv.doc_offsets + dd) + (p - __ldg(bv.batch_prefix + rec.b));
+          rec.w = __ldg(bv.word_ids + gi);
+          rec.c = __ldg(bv.counts + gi);
+          rec.kbase = blk * 256;
+#pragma unroll
+          for (int j = 0; j < 8; ++j) rec.mask[j] = mk[j];
+          deferred[slot] = rec;
+        }
+      }
+    }
+    __syncthreads();
+  }
+  if (cur_b >= 0 && acc && k_ok) atomicAdd(theta_counts + cur_b * K + k, static_cast<unsigned long long>(acc));
+}
 
 template <int KPL, bool FULL>
 __global__ void __launch_bounds__(kFastBlock, 2) k_sample_fast(
@@ -408,21 +826,25 @@ __global__ void __launch_bounds__(kFastBlock, 2) k_sample_fast(
         else if (!exact) {
           // u in [u_f, u_f + 2^-23): top 23 bits of the high word, no I2F
           const float u = __fsub_rn(__int_as_float(0x3f800000 | (y[j] >> 9)), 1.0f);
-          float pmf = __expf(-lam);
+          float pmf = ex2_approx(__fmul_rn(lam, -1.4426950408889634f));
           float cdf = pmf;
-          float r = __fadd_rn(4e-6f, __fmul_rn(4e-6f, lam));
+          // thresholds cdf * (1 -+ r) -+ 2.5e-7, r = 4e-6 + 4e-6 lam + 6e-6 z
+          float rlo = __fsub_rn(1.0f - 4e-6f, __fmul_rn(4e-6f, lam));
+          float rhi = __fadd_rn(1.0f + 4e-6f, __fmul_rn(4e-6f, lam));
+          float zf = 0.0f;
           for (;;) {
-            const float mrg = __fadd_rn(__fmul_rn(cdf, r), 2.5e-7f);
-            if (u <= __fsub_rn(cdf, mrg)) break;
-            if (!(u > __fadd_rn(cdf, mrg)) || z >= 40) {
+            if (u <= __fmaf_rn(cdf, rlo, -2.5e-7f)) break;
+            if (!(u > __fmaf_rn(cdf, rhi, 2.5e-7f)) || z >= 40) {
               exact = true;
               z = 0;
               break;
             }
             ++z;
-            pmf = __fmul_rn(pmf, __fdividef(lam, static_cast<float>(z)));
+            zf = __fadd_rn(zf, 1.0f);
+            pmf = __fmul_rn(pmf, __fmul_rn(lam, rcp_approx(zf)));
             cdf = __fadd_rn(cdf, pmf);
-            r = __fadd_rn(r, 6e-6f);
+            rlo = __fsub_rn(rlo, 6e-6f);
+            rhi = __fadd_rn(rhi, 6e-6f);
           }
           if (z != 0) {
             acc[j] += static_cast<uint32_t>(z);
@@ -546,6 +968,20 @@ int launch_fast_kpl(const BatchView& bv, const double* tb64, const float* tb32, 
   return 2;
 }
 
+int launch_fast_nz(const BatchView& bv, const double* tb64, const float* tb32, const double* phi64,
+                   const float* phi32, const double* mu, int K, double m_t, uint64_t seed,
+                   uint32_t t, uint32_t sweep, unsigned long long* tc, unsigned long long* pc,
+                   void* deferred, unsigned long long* n_deferred, int* err, cudaStream_t st) {
+  const int64_t groups = (bv.nnz + 31) / 32;
+  cudaMemsetAsync(n_deferred, 0, sizeof(unsigned long long), st);
+  auto* rec = static_cast<Deferred*>(deferred);
+  k_sample_nz<<<static_cast<unsigned>((groups + kNzWarps - 1) / kNzWarps), kNzWarps * 32, 0, st>>>(
+      bv, tb32, phi32, mu, K, m_t, seed, t, sweep, tc, pc, rec, n_deferred);
+  k_sample_deferred<<<148 * 8, 256, 0, st>>>(bv, tb64, phi64, mu, K, m_t, seed, t, sweep, rec,
+                                             n_deferred, tc, pc, err);
+  return 2;
+}
+
 // ------------------------------------------------------------------- M-step
 
 __global__ void k_theta_from_counts(const unsigned long long* __restrict__ cu,
@@ -580,26 +1016,62 @@ __global__ void k_theta_persist(const unsigned long long* __restrict__ cu,
 // runs the same sequential add chain over the 32 broadcast values, so the
 // summation order is exactly the reference's and the total is warp-uniform.
 template <int SRC>  // 0: u64 counts, 1: f64 expected counts, 2: plain f64 values
+__device__ __forceinline__ double col_value(const unsigned long long* __restrict__ cu,
+                                            const double* __restrict__ cf, int64_t i,
+                                            double m_t, double beta) {
+  if (SRC == 0) return __dadd_rn(__ddiv_rn(static_cast<double>(static_cast<long long>(cu[i])), m_t), beta);
+  if (SRC == 1) return __dadd_rn(__ddiv_rn(cf[i], m_t), beta);
+  return cf[i];
+}
+
+template <int SRC>
+__device__ __forceinline__ double col_raw(const unsigned long long* __restrict__ cu,
+                                          const double* __restrict__ cf, int64_t i) {
+  if (SRC == 0) return __longlong_as_double(static_cast<long long>(__ldg(cu + i)));
+  return __ldg(cf + i);
+}
+
+template <int SRC>
+__device__ __forceinline__ double col_convert(double raw, double m_t, double beta) {
+  if (SRC == 0) return __dadd_rn(__ddiv_rn(static_cast<double>(__double_as_longlong(raw)), m_t), beta);
+  if (SRC == 1) return __dadd_rn(__ddiv_rn(raw, m_t), beta);
+  return raw;
+}
+
+template <int SRC>
 __global__ void __launch_bounds__(256) k_col_totals(const unsigned long long* __restrict__ cu,
                                                     const double* __restrict__ cf, int64_t W,
                                                     int K, double m_t, double beta,
                                                     double* __restrict__ totals,
                                                     int* __restrict__ err) {
+  // The add chain (8.2-cycle FP64 latency, ~0.45 ms for W = 102,660) is the
+  // floor.  A ring of kDepth blocks of 32 raw words keeps the strided loads
+  // (~1 us from HBM) off the critical path; values are converted
+  // (count / m_t + beta) only when their block is consumed.
+  constexpr int kDepth = 8;
   const int lane = threadIdx.x & 31;
   const int k = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   if (k >= K) return;
   double total = 0.0;
-  for (int64_t w0 = 0; w0 < W; w0 += 32) {
-    const int64_t w = w0 + lane;
-    double v = 0.0;
-    if (w < W) {
-      const int64_t i = w * K + k;
-      if (SRC == 0) v = __dadd_rn(__ddiv_rn(static_cast<double>(static_cast<long long>(cu[i])), m_t), beta);
-      else if (SRC == 1) v = __dadd_rn(__ddiv_rn(cf[i], m_t), beta);
-      else v = cf[i];
+  double ring[kDepth];
+#pragma unroll
+  for (int d = 0; d < kDepth; ++d) {
+    const int64_t w = static_cast<int64_t>(d) * 32 + lane;
+    ring[d] = w < W ? col_raw<SRC>(cu, cf, w * K + k) : 0.0;
+  }
+  // values past W are +0.0, which leaves a positive running total unchanged
+  for (int64_t w0 = 0; w0 < W; w0 += 32 * kDepth) {
+#pragma unroll
+    for (int d = 0; d < kDepth; ++d) {
+      const int64_t wv = w0 + static_cast<int64_t>(d) * 32 + lane;
+      const double v = wv < W ? col_convert<SRC>(ring[d], m_t, beta) : 0.0;
+      const int64_t wn = wv + 32 * kDepth;
+      ring[d] = wn < W ? col_raw<SRC>(cu, cf, wn * K + k) : 0.0;
+      if (w0 + d * 32 < W) {
+#pragma unroll
+        for (int j = 0; j < 32; ++j) total = __dadd_rn(total, __shfl_sync(0xffffffffu, v, j));
+      }
     }
-    const int n = static_cast<int>(min(static_cast<int64_t>(32), W - w0));
-    for (int j = 0; j < n; ++j) total = __dadd_rn(total, __shfl_sync(0xffffffffu, v, j));
   }
   if (lane == 0) {
     totals[k] = total;
@@ -907,17 +1379,45 @@ int launch_sample_fast(const BatchView& bv, const double* theta_b64, const float
                        unsigned long long* tc, unsigned long long* pc, void* deferred,
                        unsigned long long* n_deferred, int* err, cudaStream_t st) {
   if (bv.nnz == 0) return 0;
-  if (K <= 32)
-    return launch_fast_kpl<1>(bv, theta_b64, theta_b32, phi64, phi32, mu, K, m_t, seed, t, sweep,
-                              tc, pc, deferred, n_deferred, err, st);
-  if (K <= 64)
-    return launch_fast_kpl<2>(bv, theta_b64, theta_b32, phi64, phi32, mu, K, m_t, seed, t, sweep,
-                              tc, pc, deferred, n_deferred, err, st);
-  if (K <= 128)
-    return launch_fast_kpl<4>(bv, theta_b64, theta_b32, phi64, phi32, mu, K, m_t, seed, t, sweep,
-                              tc, pc, deferred, n_deferred, err, st);
-  return launch_fast_kpl<8>(bv, theta_b64, theta_b32, phi64, phi32, mu, K, m_t, seed, t, sweep,
-                            tc, pc, deferred, n_deferred, err, st);
+  // production: lane = topic, 8 topics per lane (k_sample_fast).  The two
+  // alternative layouts stay selectable for profiling (SAMELDA_SAMPLER=c|n);
+  // both are bit-identical and measured slower on B200.
+  const char* variant = getenv("SAMELDA_SAMPLER");
+  const char v = variant ? variant[0] : 'f';
+  // K > 256: a lane=topic warp would only see a slice of mu; lane=nonzero
+  // handles any K with the full mu
+  if (v == 'f' && K <= 256) {
+    if (K <= 32)
+      return launch_fast_kpl<1>(bv, theta_b64, theta_b32, phi64, phi32, mu, K, m_t, seed, t, sweep, tc, pc,
+                                deferred, n_deferred, err, st);
+    if (K <= 64)
+      return launch_fast_kpl<2>(bv, theta_b64, theta_b32, phi64, phi32, mu, K, m_t, seed, t, sweep, tc, pc,
+                                deferred, n_deferred, err, st);
+    if (K <= 128)
+      return launch_fast_kpl<4>(bv, theta_b64, theta_b32, phi64, phi32, mu, K, m_t, seed, t, sweep, tc, pc,
+                                deferred, n_deferred, err, st);
+    return launch_fast_kpl<8>(bv, theta_b64, theta_b32, phi64, phi32, mu, K, m_t, seed, t, sweep, tc, pc,
+                              deferred, n_deferred, err, st);
+  }
+  if (v == 'c' && K <= 32 * kCtaMaxWarps) {
+    const int nwarps = (K + 31) / 32;
+    const int64_t chunk = 256;
+    cudaMemsetAsync(n_deferred, 0, sizeof(unsigned long long), st);
+    auto* rec = static_cast<Deferred*>(deferred);
+    const unsigned grid = static_cast<unsigned>((bv.nnz + chunk - 1) / chunk);
+    if (nwarps <= 8)
+      k_sample_cta<8><<<grid, nwarps * 32, 0, st>>>(bv, theta_b32, phi32, mu, K, nwarps, m_t, seed,
+                                                    t, sweep, chunk, tc, pc, rec, n_deferred);
+    else
+      k_sample_cta<kCtaMaxWarps><<<grid, nwarps * 32, 0, st>>>(bv, theta_b32, phi32, mu, K, nwarps,
+                                                               m_t, seed, t, sweep, chunk, tc, pc,
+                                                               rec, n_deferred);
+    k_sample_deferred<<<148 * 8, 256, 0, st>>>(bv, theta_b64, phi64, mu, K, m_t, seed, t, sweep,
+                                               rec, n_deferred, tc, pc, err);
+    return 2;
+  }
+  return launch_fast_nz(bv, theta_b64, theta_b32, phi64, phi32, mu, K, m_t, seed, t, sweep, tc,
+                        pc, deferred, n_deferred, err, st);
 }
 
 int launch_theta_from_counts(const unsigned long long* cu, const double* cf, int64_t n,

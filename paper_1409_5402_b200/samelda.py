@@ -113,7 +113,8 @@ SIGNATURES = [
     ("samelda_cu_batch_theta", C.c_int, [_P, _P, _I64]),
     ("samelda_cu_set_doc_base", C.c_int, [_P, _I64]),
     ("samelda_cu_profile", C.c_int, [_P, _I32]),
-    ("samelda_cu_profile_read", C.c_int, [_P, _P, _P, C.POINTER(_I64), C.POINTER(_I64)]),
+    ("samelda_cu_profile_read", C.c_int, [_P, _P, _P, C.POINTER(_I64), C.POINTER(_I64),
+                                          C.POINTER(_I64)]),
     ("samelda_cu_count_totals", C.c_int, [_P, C.POINTER(_I64), C.POINTER(_I64)]),
     ("samelda_cu_evaluate", C.c_int, [_P, C.POINTER(_D)]),
     ("samelda_cu_model_download", C.c_int, [_P, _P, _P]),
@@ -537,12 +538,13 @@ class Trainer:
     def profile_read(self) -> dict:
         ms = np.zeros(3)
         n = np.zeros(3, np.int64)
-        nnz, docs = C.c_int64(), C.c_int64()
+        nnz, docs, dfr = C.c_int64(), C.c_int64(), C.c_int64()
         self.ctx.check(self.ctx.lib.samelda_cu_profile_read(self.ctx.h, _ptr(ms), _ptr(n),
-                                                            C.byref(nnz), C.byref(docs)))
+                                                            C.byref(nnz), C.byref(docs),
+                                                            C.byref(dfr)))
         return dict(sample_ms=ms[0], sddmm_ms=ms[1], mstep_ms=ms[2], sample_launches=int(n[0]),
                     sddmm_launches=int(n[1]), mstep_launches=int(n[2]), nnz=nnz.value,
-                    docs=docs.value)
+                    docs=docs.value, deferred=dfr.value)
 
     def count_totals(self):
         a, b = C.c_int64(), C.c_int64()
