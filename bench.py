@@ -19,7 +19,6 @@ all-reduced over NCCL once per period, the M-step is replicated.
 from __future__ import annotations
 
 import argparse
-import ctypes as C
 import json
 import os
 import statistics
@@ -144,14 +143,6 @@ def split_heldout(corpus, frac=0.1):
     test = Corpus(o[cut:] - o[cut], corpus.word_ids[o[cut]:], corpus.counts[o[cut]:],
                   corpus.n_words)
     return train, test
-
-
-class _CAI:
-    """__cuda_array_interface__ view of a device buffer owned by the C ABI context."""
-
-    def __init__(self, ptr: int, n: int, typestr: str):
-        self.__cuda_array_interface__ = {"shape": (n,), "typestr": typestr, "data": (ptr, False),
-                                         "version": 2, "strides": None}
 
 
 # --------------------------------------------------------- reference arm
@@ -291,32 +282,17 @@ def run_ours(args, cfg):
     trainer.set_doc_base(doc_base)
     if rank == 0:
         trainer.set_heldout(heldout, seed=1)
-    batches = S.MinibatchStream(D_global, cfg["batch_fraction"], 1)
-    doc_tokens = train.doc_tokens()
-    t_max = scfg.t_max
-
-    pc_tensor = None
+    from paper_1409_5402_b200 import distributed as DIST
+    engine = DIST.CudaEngine(trainer, local)
+    sharded = DIST.ShardedTrainer(engine, D_global, doc_base, doc_base + D_local,
+                                  train.doc_tokens(), cfg["batch_fraction"], 1, cfg["m"],
+                                  cfg["schedule"], scfg.t_max)
 
     def period(t, with_result=False):
-        nonlocal pc_tensor
-        batch = batches.next()
-        own = batch[(batch >= doc_base) & (batch < doc_base + D_local)] - doc_base
-        m_t = S.anneal_m(cfg["schedule"], t + 1, t_max, cfg["m"])
-        rho = S.rho_schedule(t, 1.0, 0.5)
-        if world == 1:
-            trainer.period(own, t, m_t, rho)
-        else:
-            import torch.distributed as dist
-            trainer.period_sample(own, t, m_t)
-            if pc_tensor is None:
-                ptr, n, _, is_f = trainer.phi_counts_device()
-                pc_tensor = torch.as_tensor(_CAI(ptr, n, "<f8" if is_f else "<i8"),
-                                            device=f"cuda:{local}")
-            dist.all_reduce(pc_tensor)
-            trainer.period_update(rho)
-        out = trainer.batch_theta(len(own)) if with_result else None
-        tokens = float(doc_tokens[own].sum())
-        return tokens, m_t, len(own), out
+        assert t == sharded.t
+        st = sharded.period()
+        out = trainer.batch_theta(st.owned_docs) if with_result else None
+        return st.owned_tokens, st.m_t, st.owned_docs, out
 
     def barrier():
         torch.cuda.synchronize()

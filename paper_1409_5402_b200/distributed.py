@@ -1,0 +1,114 @@
+"""Document-sharded SAME training across ranks (one process per GPU).
+
+Documents are independent given phi, so rank r owns a
+contiguous range of documents -- their CSR rows, theta rows and theta counts.
+Every rank runs the same global MinibatchStream (corpus.cpp:252-285) and
+samples only the batch documents it owns; Philox keys use the GLOBAL doc id
+(`samelda_cu_set_doc_base`), so each rank draws exactly what one GPU would.
+The one exchange per period is a sum all-reduce of the W x K topic-word
+counts of the last inner sweep (sampler.cpp:320-332); integer addition is
+associative, so the reduced counts -- and the replicated M-step's phi -- are
+bit-identical to a single-GPU run.
+
+`torch.distributed` is the plumbing (NCCL on B200s, gloo in the CPU tests);
+the per-rank compute is an *engine*: `CudaEngine` (the product, over
+libsamelda_cuda.so) or a test engine built on the oracle.
+"""
+from __future__ import annotations
+
+from dataclasses import dataclass
+
+import numpy as np
+
+
+def shard_ranges(doc_offsets: np.ndarray, world: int) -> list[tuple[int, int]]:
+    """Contiguous doc ranges balanced by nonzeros (parallel.hpp:29-43's idea)."""
+    doc_offsets = np.asarray(doc_offsets, np.int64)
+    D = len(doc_offsets) - 1
+    total = int(doc_offsets[-1])
+    bounds = [0]
+    for i in range(1, world):
+        target = total * i // world
+        pos = int(np.searchsorted(doc_offsets[:D], target, side="left"))
+        bounds.append(max(bounds[-1], min(pos, D)))
+    bounds.append(D)
+    return [(bounds[i], bounds[i + 1]) for i in range(world)]
+
+
+def owned(batch: np.ndarray, lo: int, hi: int) -> np.ndarray:
+    """Batch docs in [lo, hi) as local ids, batch order preserved."""
+    batch = np.asarray(batch)
+    sel = batch[(batch >= lo) & (batch < hi)]
+    return (sel - lo).astype(np.int32)
+
+
+class _CAI:
+    def __init__(self, ptr: int, n: int, typestr: str):
+        self.__cuda_array_interface__ = {"shape": (n,), "typestr": typestr,
+                                         "data": (ptr, False), "version": 2, "strides": None}
+
+
+class CudaEngine:
+    """Per-rank engine over the device-resident trainer (samelda.Trainer)."""
+
+    def __init__(self, trainer, device: int):
+        self.trainer = trainer
+        self.device = device
+        self._counts = None
+
+    def sample(self, local_ids, t, m_t):
+        self.trainer.period_sample(local_ids, t, m_t)
+
+    def counts(self):
+        if self._counts is None:
+            import torch
+            ptr, n, _, is_f = self.trainer.phi_counts_device()
+            self._counts = torch.as_tensor(_CAI(ptr, n, "<f8" if is_f else "<i8"),
+                                           device=f"cuda:{self.device}")
+        return self._counts
+
+    def update(self, rho_t):
+        self.trainer.period_update(rho_t)
+
+
+@dataclass
+class PeriodStats:
+    t: int
+    m_t: float
+    rho_t: float
+    batch_docs: int
+    owned_docs: int
+    owned_tokens: float
+
+
+class ShardedTrainer:
+    """The train() period loop (sampler.cpp:307-339) over doc shards."""
+
+    def __init__(self, engine, n_docs_global: int, doc_lo: int, doc_hi: int,
+                 local_doc_tokens: np.ndarray, batch_fraction: float, seed: int, m: float,
+                 schedule: str, t_max: int, tau0: float = 1.0, gamma: float = 0.5,
+                 group=None):
+        from . import samelda as S
+        self.S = S
+        self.engine = engine
+        self.lo, self.hi = doc_lo, doc_hi
+        self.doc_tokens = np.asarray(local_doc_tokens, np.float64)
+        self.batches = S.MinibatchStream(n_docs_global, batch_fraction, seed)
+        self.m, self.schedule, self.t_max = m, schedule, t_max
+        self.tau0, self.gamma = tau0, gamma
+        self.group = group
+        self.t = 0
+
+    def period(self) -> PeriodStats:
+        import torch.distributed as dist
+        t = self.t
+        batch = self.batches.next()
+        own = owned(batch, self.lo, self.hi)
+        m_t = self.S.anneal_m(self.schedule, t + 1, self.t_max, self.m)
+        rho = self.S.rho_schedule(t, self.tau0, self.gamma)
+        self.engine.sample(own, t, m_t)
+        if dist.is_available() and dist.is_initialized() and dist.get_world_size(self.group) > 1:
+            dist.all_reduce(self.engine.counts(), group=self.group)
+        self.engine.update(rho)
+        self.t += 1
+        return PeriodStats(t, m_t, rho, len(batch), len(own), float(self.doc_tokens[own].sum()))
