@@ -241,6 +241,54 @@ __device__ __forceinline__ float rcp_approx(float x) {
   return y;
 }
 
+// Fast-path Poisson decision (see the error budget above).  Returns z, or
+// sets *undecided when u falls inside a threshold's uncertainty band or the
+// search passes z = 40.  The first three thresholds (z in {0, 1, 2}, ~99% of
+// draws at lambda ~ 0.4) are evaluated branch-free; only u beyond cdf_2
+// enters the sequential search.  Terms: t1 = e0 lambda, t2 = t1 lambda / 2
+// (the reference recurrence pmf *= lambda / k with an exact 1/2).
+__device__ __forceinline__ uint32_t fast_poisson(float lam, uint32_t y, bool* undecided) {
+  // u in [u_f, u_f + 2^-23): top 23 bits of the high word, no I2F
+  const float u = __fsub_rn(__int_as_float(0x3f800000 | (y >> 9)), 1.0f);
+  const float e0 = ex2_approx(__fmul_rn(lam, -1.4426950408889634f));
+  const float t1 = __fmul_rn(e0, lam);
+  const float c1 = __fadd_rn(e0, t1);
+  const float t2 = __fmul_rn(__fmul_rn(t1, lam), 0.5f);
+  const float c2 = __fadd_rn(c1, t2);
+  // relative bound r_k = 4e-6 + 4e-6 lambda + 6e-6 k; absolute 2.5e-7 for u
+  const float r0 = __fmaf_rn(4e-6f, lam, 4e-6f);
+  const float a0 = __fsub_rn(1.0f, r0), b0 = __fadd_rn(1.0f, r0);
+  const float lo0 = __fmaf_rn(e0, a0, -2.5e-7f), hi0 = __fmaf_rn(e0, b0, 2.5e-7f);
+  const float lo1 = __fmaf_rn(c1, __fsub_rn(a0, 6e-6f), -2.5e-7f);
+  const float hi1 = __fmaf_rn(c1, __fadd_rn(b0, 6e-6f), 2.5e-7f);
+  const float lo2 = __fmaf_rn(c2, __fsub_rn(a0, 1.2e-5f), -2.5e-7f);
+  const float hi2 = __fmaf_rn(c2, __fadd_rn(b0, 1.2e-5f), 2.5e-7f);
+  const bool amb = (u > lo0 && u <= hi0) || (u > lo1 && u <= hi1) || (u > lo2 && u <= hi2);
+  uint32_t z = (u > hi0) + (u > hi1) + (u > hi2);
+  if (amb) {
+    *undecided = true;
+    return 0;
+  }
+  if (z < 3) return z;
+  // sequential search from k = 3
+  float pmf = t2, cdf = c2, zf = 2.0f;
+  float rlo = __fsub_rn(a0, 1.2e-5f), rhi = __fadd_rn(b0, 1.2e-5f);
+  z = 2;
+  for (;;) {
+    ++z;
+    zf = __fadd_rn(zf, 1.0f);
+    pmf = __fmul_rn(pmf, __fmul_rn(lam, rcp_approx(zf)));
+    cdf = __fadd_rn(cdf, pmf);
+    rlo = __fsub_rn(rlo, 6e-6f);
+    rhi = __fadd_rn(rhi, 6e-6f);
+    if (u <= __fmaf_rn(cdf, rlo, -2.5e-7f)) return z;
+    if (!(u > __fmaf_rn(cdf, rhi, 2.5e-7f)) || z >= 40) {
+      *undecided = true;
+      return 0;
+    }
+  }
+}
+
 struct Philox1 {
   // round-1 specialisation for counter {0, w, d, t}: M0 * 0 = 0, so the
   // only per-draw work in round 1 is one xor; M1 * d is per nonzero
@@ -437,27 +485,11 @@ __global__ void __launch_bounds__(kNzWarps * 32) k_sample_nz(
       const uint32_t y = philox_y_sched(r1, ks);
       uint32_t z = 0;
       if (lam >= 0.0f) {
-        // u in [u_f, u_f + 2^-23): top 23 bits of the high word, no I2F
-        const float u = __fsub_rn(__int_as_float(0x3f800000 | (y >> 9)), 1.0f);
-        float pmf = ex2_approx(__fmul_rn(lam, -1.4426950408889634f));
-        float cdf = pmf;
-        // thresholds cdf * (1 -+ r) -+ 2.5e-7, r = 4e-6 + 4e-6 lam + 6e-6 z
-        float rlo = __fsub_rn(1.0f - 4e-6f, __fmul_rn(4e-6f, lam));
-        float rhi = __fadd_rn(1.0f + 4e-6f, __fmul_rn(4e-6f, lam));
-        float zf = 0.0f;
-        for (;;) {
-          if (u <= __fmaf_rn(cdf, rlo, -2.5e-7f)) break;
-          if (!(u > __fmaf_rn(cdf, rhi, 2.5e-7f)) || z >= 40) {
-            defer_mask |= 1u << kk;
-            z = 0;
-            break;
-          }
-          ++z;
-          zf = __fadd_rn(zf, 1.0f);
-          pmf = __fmul_rn(pmf, __fmul_rn(lam, rcp_approx(zf)));
-          cdf = __fadd_rn(cdf, pmf);
-          rlo = __fsub_rn(rlo, 6e-6f);
-          rhi = __fadd_rn(rhi, 6e-6f);
+        bool undecided = false;
+        z = fast_poisson(lam, y, &undecided);
+        if (undecided) {
+          defer_mask |= 1u << kk;
+          z = 0;
         }
       } else if (lam == -1.0f) {
         defer_mask |= 1u << kk;
@@ -626,25 +658,11 @@ __global__ void __launch_bounds__(MAXW * 32) k_sample_cta(
       bool exact = k_ok && (ex_i || !(prod[i] >= 1e-30f) || !(lam < 9.5f));
       uint32_t z = 0;
       if (k_ok && !exact) {
-        const float u = __fsub_rn(__int_as_float(0x3f800000 | (y >> 9)), 1.0f);
-        float pmf = ex2_approx(__fmul_rn(lam, -1.4426950408889634f));
-        float cdf = pmf;
-        float rlo = __fsub_rn(1.0f - 4e-6f, __fmul_rn(4e-6f, lam));
-        float rhi = __fadd_rn(1.0f + 4e-6f, __fmul_rn(4e-6f, lam));
-        float zf = 0.0f;
-        for (;;) {
-          if (u <= __fmaf_rn(cdf, rlo, -2.5e-7f)) break;
-          if (!(u > __fmaf_rn(cdf, rhi, 2.5e-7f)) || z >= 40) {
-            exact = true;
-            z = 0;
-            break;
-          }
-          ++z;
-          zf = __fadd_rn(zf, 1.0f);
-          pmf = __fmul_rn(pmf, __fmul_rn(lam, rcp_approx(zf)));
-          cdf = __fadd_rn(cdf, pmf);
-          rlo = __fsub_rn(rlo, 6e-6f);
-          rhi = __fadd_rn(rhi, 6e-6f);
+        bool undecided = false;
+        z = fast_poisson(lam, y, &undecided);
+        if (undecided) {
+          exact = true;
+          z = 0;
         }
         if (z) {
           acc += z;
@@ -824,27 +842,11 @@ __global__ void __launch_bounds__(kFastBlock, 2) k_sample_fast(
         bool exact = nz_exact || !(prod[j] >= 1e-30f) || !(lam < 9.5f);
         if (!FULL && k >= K) exact = false;
         else if (!exact) {
-          // u in [u_f, u_f + 2^-23): top 23 bits of the high word, no I2F
-          const float u = __fsub_rn(__int_as_float(0x3f800000 | (y[j] >> 9)), 1.0f);
-          float pmf = ex2_approx(__fmul_rn(lam, -1.4426950408889634f));
-          float cdf = pmf;
-          // thresholds cdf * (1 -+ r) -+ 2.5e-7, r = 4e-6 + 4e-6 lam + 6e-6 z
-          float rlo = __fsub_rn(1.0f - 4e-6f, __fmul_rn(4e-6f, lam));
-          float rhi = __fadd_rn(1.0f + 4e-6f, __fmul_rn(4e-6f, lam));
-          float zf = 0.0f;
-          for (;;) {
-            if (u <= __fmaf_rn(cdf, rlo, -2.5e-7f)) break;
-            if (!(u > __fmaf_rn(cdf, rhi, 2.5e-7f)) || z >= 40) {
-              exact = true;
-              z = 0;
-              break;
-            }
-            ++z;
-            zf = __fadd_rn(zf, 1.0f);
-            pmf = __fmul_rn(pmf, __fmul_rn(lam, rcp_approx(zf)));
-            cdf = __fadd_rn(cdf, pmf);
-            rlo = __fsub_rn(rlo, 6e-6f);
-            rhi = __fadd_rn(rhi, 6e-6f);
+          bool undecided = false;
+          z = fast_poisson(lam, y[j], &undecided);
+          if (undecided) {
+            exact = true;
+            z = 0;
           }
           if (z != 0) {
             acc[j] += static_cast<uint32_t>(z);
@@ -1190,6 +1192,24 @@ __device__ __forceinline__ double warp_max(double v) {
 // f64 sums accumulate in the reference's order.
 constexpr int kEvalWarps = 4;
 
+// sum_k th[k] * row[k] in sequential k order (product then add, no FMA),
+// 16-byte loads when the row is 16-byte aligned (K even)
+__device__ __forceinline__ double seq_dot(const double* __restrict__ th,
+                                          const double* __restrict__ row, int K) {
+  double dot = 0.0;
+  if ((K & 1) == 0) {
+    const double2* r2 = reinterpret_cast<const double2*>(row);
+    for (int k2 = 0; k2 < (K >> 1); ++k2) {
+      const double2 v = __ldg(r2 + k2);
+      dot = __dadd_rn(dot, __dmul_rn(th[2 * k2], v.x));
+      dot = __dadd_rn(dot, __dmul_rn(th[2 * k2 + 1], v.y));
+    }
+  } else {
+    for (int k = 0; k < K; ++k) dot = __dadd_rn(dot, __dmul_rn(th[k], __ldg(row + k)));
+  }
+  return dot;
+}
+
 __global__ void __launch_bounds__(kEvalWarps * 32) k_eval_docs(
     const int64_t* __restrict__ doc_offsets, const int32_t* __restrict__ word_ids,
     const int32_t* __restrict__ fold_counts, const int32_t* __restrict__ score_counts,
@@ -1219,9 +1239,7 @@ __global__ void __launch_bounds__(kEvalWarps * 32) k_eval_docs(
           const int32_t fc = fold_counts[base + i];
           w = word_ids[base + i];
           if (fc != 0) {  // a zero-count cell adds exactly +0 (eval.cpp:43-47)
-            const double* ph = phi_wk + static_cast<int64_t>(w) * K;
-            double mu = 0.0;
-            for (int k = 0; k < K; ++k) mu = __dadd_rn(mu, __dmul_rn(th[k], __ldg(ph + k)));
+            const double mu = seq_dot(th, phi_wk + static_cast<int64_t>(w) * K, K);
             if (mu > 0.0) {
               scale = __ddiv_rn(static_cast<double>(fc), mu);
               use = true;
@@ -1265,9 +1283,7 @@ __global__ void __launch_bounds__(kEvalWarps * 32) k_eval_docs(
       if (i < n) {
         sc = score_counts[base + i];
         if (sc != 0) {
-          const double* ph = phi_wk + static_cast<int64_t>(word_ids[base + i]) * K;
-          double p = 0.0;
-          for (int k = 0; k < K; ++k) p = __dadd_rn(p, __dmul_rn(th[k], __ldg(ph + k)));
+          const double p = seq_dot(th, phi_wk + static_cast<int64_t>(word_ids[base + i]) * K, K);
           if (!(p > 0.0)) atomicOr(err, kErrNumerical);
           term = __dmul_rn(static_cast<double>(sc), log(p));
         }
