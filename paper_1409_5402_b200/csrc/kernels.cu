@@ -707,7 +707,10 @@ __global__ void __launch_bounds__(MAXW * 32) k_sample_cta(
 }
 
 template <int KPL, bool FULL>
-__global__ void __launch_bounds__(kFastBlock, 2) k_sample_fast(
+#ifndef SAMELDA_FAST_MINB
+#define SAMELDA_FAST_MINB 4
+#endif
+__global__ void __launch_bounds__(kFastBlock, SAMELDA_FAST_MINB) k_sample_fast(
     BatchView bv, const float* __restrict__ theta_b32, const float* __restrict__ phi32,
     const double* __restrict__ mu_in, int K, double m_t, uint64_t seed, uint32_t t,
     uint32_t sweep, int64_t chunk, int n_slices, unsigned long long* __restrict__ theta_counts,
@@ -723,13 +726,11 @@ __global__ void __launch_bounds__(kFastBlock, 2) k_sample_fast(
   const int kbase = slice * kWarp * KPL;
   const int have_mu = mu_in != nullptr;
 
-  // per-topic stream keys, fixed for the whole item
-  uint32_t key0[KPL], key1[KPL];
-#pragma unroll
-  for (int j = 0; j < KPL; ++j) {
-    const uint32_t k = static_cast<uint32_t>(kbase + lane + kWarp * j);
-    stream_key(seed, make_tag(kPoissonCounts, sweep, k), key0[j], key1[j]);
-  }
+  // stream key of topic k (rng.cpp:92-94): tag(k) * M = tag(k0) * M + 32 j M,
+  // so each draw's key is one add and one xor away from two per-lane bases
+  const uint32_t tag0 = make_tag(kPoissonCounts, sweep, static_cast<uint32_t>(kbase + lane));
+  const uint32_t kb0 = tag0 * kPhiloxM0, kb1 = tag0 * kPhiloxM1;
+  const uint32_t seed_lo = static_cast<uint32_t>(seed), seed_hi = static_cast<uint32_t>(seed >> 32);
 
   int64_t cur_b = -1;
   float th[KPL];
@@ -754,17 +755,6 @@ __global__ void __launch_bounds__(kFastBlock, 2) k_sample_fast(
       if (have_mu) mu_v = __ldg(mu_in + p);
     }
     const int n_here = static_cast<int>(min(static_cast<int64_t>(kWarp), p1 - g0));
-    // software pipeline: phi slice of nonzero i+1 is in flight while i draws
-    float ph_next[KPL];
-    {
-      const int32_t w0 = __shfl_sync(0xffffffffu, w, 0);
-      const float* prow = phi32 + static_cast<int64_t>(w0) * K;
-#pragma unroll
-      for (int j = 0; j < KPL; ++j) {
-        const int k = kbase + lane + kWarp * j;
-        ph_next[j] = (FULL || k < K) ? __ldg(prow + k) : 0.0f;
-      }
-    }
     for (int i = 0; i < n_here; ++i) {
       const int64_t bi = __shfl_sync(0xffffffffu, b, i);
       const int32_t dl = __shfl_sync(0xffffffffu, d, i);
@@ -772,18 +762,14 @@ __global__ void __launch_bounds__(kFastBlock, 2) k_sample_fast(
       const int32_t wi = __shfl_sync(0xffffffffu, w, i);
       const int32_t ci = __shfl_sync(0xffffffffu, c, i);
       const double mui = __shfl_sync(0xffffffffu, mu_v, i);
+      // phi[w, slice]: 32 lanes x KPL coalesced loads (occupancy hides latency)
       float ph[KPL];
-#pragma unroll
-      for (int j = 0; j < KPL; ++j) ph[j] = ph_next[j];
       {
-        const int32_t wn = __shfl_sync(0xffffffffu, w, (i + 1) & 31);
-        if (i + 1 < n_here) {
-          const float* prow = phi32 + static_cast<int64_t>(wn) * K;
+        const float* prow = phi32 + static_cast<int64_t>(wi) * K;
 #pragma unroll
-          for (int j = 0; j < KPL; ++j) {
-            const int k = kbase + lane + kWarp * j;
-            ph_next[j] = (FULL || k < K) ? __ldg(prow + k) : 0.0f;
-          }
+        for (int j = 0; j < KPL; ++j) {
+          const int k = kbase + lane + kWarp * j;
+          ph[j] = (FULL || k < K) ? __ldg(prow + k) : 0.0f;
         }
       }
       if (bi != cur_b) {
@@ -828,9 +814,11 @@ __global__ void __launch_bounds__(kFastBlock, 2) k_sample_fast(
       uint32_t y[KPL];
 #pragma unroll
       for (int j = 0; j < KPL; ++j) {
+        const uint32_t key0 = seed_lo ^ (kb0 + static_cast<uint32_t>(kWarp * j) * kPhiloxM0);
+        const uint32_t key1 = seed_hi ^ (kb1 + static_cast<uint32_t>(kWarp * j) * kPhiloxM1);
         uint32_t p2lo, p2hi;
-        mulhilo(kPhiloxM1, t ^ key1[j], p2lo, p2hi);
-        y[j] = philox_y(r1, key0[j], key1[j], p2lo, p2hi);
+        mulhilo(kPhiloxM1, t ^ key1, p2lo, p2hi);
+        y[j] = philox_y(r1, key0, key1, p2lo, p2hi);
       }
       // phase 2: decisions; undecidable draws are deferred
       uint32_t defer_bits = 0;
@@ -884,10 +872,12 @@ __global__ void __launch_bounds__(kFastBlock, 2) k_sample_fast(
   }
 }
 
-// One warp per deferred record: exact mu (sequential k order, coalesced row
-// loads, warp-broadcast add chain) unless the caller supplied mu, then each
-// flagged draw exactly as k_sample: __ddiv_rn rate, full Philox block, exact
-// inversion or PTRS (rng.cpp:39-86).
+// Deferred exact draws, one warp per 32 records.  Phase A: lane l computes
+// record l's exact mu -- the reference's sequential-k f64 dot
+// (sampler.cpp:111-119) -- so 32 independent add chains run side by side
+// (unless the caller supplied mu).  Phase B: record by record, lanes over the
+// flagged topics redraw exactly as k_sample: __ddiv_rn rate, full Philox
+// block, f64 inversion or PTRS (rng.cpp:39-86).
 __global__ void __launch_bounds__(256) k_sample_deferred(
     BatchView bv, const double* __restrict__ theta_b64, const double* __restrict__ phi64,
     const double* __restrict__ mu_in, int K, double m_t, uint64_t seed, uint32_t t,
@@ -898,51 +888,65 @@ __global__ void __launch_bounds__(256) k_sample_deferred(
   const int lane = threadIdx.x & 31;
   const int64_t n = static_cast<int64_t>(*n_deferred);
   const double uniform_weight = 1.0 / static_cast<double>(K);
-  for (int64_t r = (blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x) >> 5; r < n;
-       r += (static_cast<int64_t>(gridDim.x) * blockDim.x) >> 5) {
-    const Deferred rec = deferred[r];
-    const double* th = theta_b64 + static_cast<int64_t>(rec.b) * K;
-    const double* ph = phi64 + static_cast<int64_t>(rec.w) * K;
-    double mu;
-    if (mu_in) {
-      mu = mu_in[rec.p];
-    } else {
-      mu = 0.0;
-      for (int k0 = 0; k0 < K; k0 += 32) {
-        const int k = k0 + lane;
-        const double prod = k < K ? __dmul_rn(__ldg(th + k), __ldg(ph + k)) : 0.0;
-        const int m = min(32, K - k0);
-        for (int l = 0; l < m; ++l) mu = __dadd_rn(mu, __shfl_sync(0xffffffffu, prod, l));
+  const int64_t warps = (static_cast<int64_t>(gridDim.x) * blockDim.x) >> 5;
+  for (int64_t r0 = ((blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x) >> 5) * 32;
+       r0 < n; r0 += warps * 32) {
+    const int n_here = static_cast<int>(min(static_cast<int64_t>(32), n - r0));
+    double my_mu = 0.0;
+    if (lane < n_here) {
+      const Deferred& me = deferred[r0 + lane];
+      if (mu_in) {
+        my_mu = mu_in[me.p];
+      } else {
+        const double* th = theta_b64 + static_cast<int64_t>(me.b) * K;
+        const double* ph = phi64 + static_cast<int64_t>(me.w) * K;
+        if ((K & 1) == 0) {
+          const double2* t2 = reinterpret_cast<const double2*>(th);
+          const double2* p2 = reinterpret_cast<const double2*>(ph);
+          for (int k2 = 0; k2 < (K >> 1); ++k2) {
+            const double2 a = __ldg(t2 + k2), c = __ldg(p2 + k2);
+            my_mu = __dadd_rn(my_mu, __dmul_rn(a.x, c.x));
+            my_mu = __dadd_rn(my_mu, __dmul_rn(a.y, c.y));
+          }
+        } else {
+          for (int k = 0; k < K; ++k) my_mu = __dadd_rn(my_mu, __dmul_rn(__ldg(th + k), __ldg(ph + k)));
+        }
       }
     }
-    const uint32_t d = static_cast<uint32_t>(__ldg(bv.batch_docs + rec.b) + bv.doc_base);
-    const double cs = __dmul_rn(m_t, static_cast<double>(rec.c));
-    const bool degenerate = mu < 1e-30;
-    for (int j = 0; j < 8; ++j) {
-      if (!((rec.mask[j] >> lane) & 1u)) continue;
-      const int k = rec.kbase + lane + 32 * j;
-      const double weight = degenerate ? uniform_weight : __ddiv_rn(__dmul_rn(__ldg(th + k), __ldg(ph + k)), mu);
-      const double rate = __dmul_rn(weight, cs);
-      if (!(rate >= 0.0) || isinf(rate)) {
-        atomicOr(err, kErrNumerical);
-        continue;
-      }
-      if (rate == 0.0) continue;
-      const uint32_t tag = make_tag(kPoissonCounts, sweep, static_cast<uint32_t>(k));
-      uint32_t k0, k1;
-      stream_key(seed, tag, k0, k1);
-      const U4 blk = philox10(U4{0u, static_cast<uint32_t>(rec.w), d, t}, k0, k1);
-      long long z;
-      if (rate < 10.0) {
-        z = poisson_inversion(rate, u64_to_uniform(join64(blk.x, blk.y)));
-      } else {
-        Stream s;
-        s.init_with_block0(seed, t, d, static_cast<uint32_t>(rec.w), tag, blk, 0);
-        z = poisson_ptrs(rate, s);
-      }
-      if (z != 0) {
-        atomicAdd(theta_counts + static_cast<int64_t>(rec.b) * K + k, static_cast<unsigned long long>(z));
-        atomicAdd(phi_counts + static_cast<int64_t>(rec.w) * K + k, static_cast<unsigned long long>(z));
+    for (int i = 0; i < n_here; ++i) {
+      const Deferred rec = deferred[r0 + i];
+      const double mu = __shfl_sync(0xffffffffu, my_mu, i);
+      const double* th = theta_b64 + static_cast<int64_t>(rec.b) * K;
+      const double* ph = phi64 + static_cast<int64_t>(rec.w) * K;
+      const uint32_t d = static_cast<uint32_t>(__ldg(bv.batch_docs + rec.b) + bv.doc_base);
+      const double cs = __dmul_rn(m_t, static_cast<double>(rec.c));
+      const bool degenerate = mu < 1e-30;
+      for (int j = 0; j < 8; ++j) {
+        if (!((rec.mask[j] >> lane) & 1u)) continue;
+        const int k = rec.kbase + lane + 32 * j;
+        const double weight = degenerate ? uniform_weight : __ddiv_rn(__dmul_rn(__ldg(th + k), __ldg(ph + k)), mu);
+        const double rate = __dmul_rn(weight, cs);
+        if (!(rate >= 0.0) || isinf(rate)) {
+          atomicOr(err, kErrNumerical);
+          continue;
+        }
+        if (rate == 0.0) continue;
+        const uint32_t tag = make_tag(kPoissonCounts, sweep, static_cast<uint32_t>(k));
+        uint32_t k0, k1;
+        stream_key(seed, tag, k0, k1);
+        const U4 blk = philox10(U4{0u, static_cast<uint32_t>(rec.w), d, t}, k0, k1);
+        long long z;
+        if (rate < 10.0) {
+          z = poisson_inversion(rate, u64_to_uniform(join64(blk.x, blk.y)));
+        } else {
+          Stream s;
+          s.init_with_block0(seed, t, d, static_cast<uint32_t>(rec.w), tag, blk, 0);
+          z = poisson_ptrs(rate, s);
+        }
+        if (z != 0) {
+          atomicAdd(theta_counts + static_cast<int64_t>(rec.b) * K + k, static_cast<unsigned long long>(z));
+          atomicAdd(phi_counts + static_cast<int64_t>(rec.w) * K + k, static_cast<unsigned long long>(z));
+        }
       }
     }
   }

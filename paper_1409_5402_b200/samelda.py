@@ -126,9 +126,12 @@ SIGNATURES = [
 _lib = None
 
 
-def load_library(path: str = _LIB_PATH) -> C.CDLL:
-    """Load libsamelda_cuda.so (raises if it was not built -- no fallback)."""
+def load_library(path: str | None = None) -> C.CDLL:
+    """Load libsamelda_cuda.so (raises if it was not built -- no fallback).
+
+    SAMELDA_CUDA_LIB overrides the path (profiling of alternative builds)."""
     global _lib
+    path = path or os.environ.get("SAMELDA_CUDA_LIB") or _LIB_PATH
     if _lib is None:
         if not os.path.exists(path):
             raise ImportError(f"{path} is missing: run `python -m paper_1409_5402_b200.build` "
