@@ -263,14 +263,13 @@ __device__ __forceinline__ uint32_t fast_poisson(float lam, uint32_t y, bool* un
   const float hi1 = __fmaf_rn(c1, __fadd_rn(b0, 6e-6f), 2.5e-7f);
   const float lo2 = __fmaf_rn(c2, __fsub_rn(a0, 1.2e-5f), -2.5e-7f);
   const float hi2 = __fmaf_rn(c2, __fadd_rn(b0, 1.2e-5f), 2.5e-7f);
-  const bool amb = (u > lo0 && u <= hi0) || (u > lo1 && u <= hi1) || (u > lo2 && u <= hi2);
+  // u sits in an uncertainty band iff it passes a lower bound but not the
+  // matching upper one: count both ways, compare
+  const uint32_t z_lo = (u > lo0) + (u > lo1) + (u > lo2);
   uint32_t z = (u > hi0) + (u > hi1) + (u > hi2);
-  if (amb) {
-    *undecided = true;
-    return 0;
-  }
-  if (z < 3) return z;
-  // sequential search from k = 3
+  *undecided = *undecided || (z_lo != z);
+  if (z < 3 || *undecided) return z;
+  // sequential search from k = 3 (u beyond cdf_2)
   float pmf = t2, cdf = c2, zf = 2.0f;
   float rlo = __fsub_rn(a0, 1.2e-5f), rhi = __fadd_rn(b0, 1.2e-5f);
   z = 2;
@@ -820,28 +819,29 @@ __global__ void __launch_bounds__(kFastBlock, SAMELDA_FAST_MINB) k_sample_fast(
         mulhilo(kPhiloxM1, t ^ key1, p2lo, p2hi);
         y[j] = philox_y(r1, key0, key1, p2lo, p2hi);
       }
-      // phase 2: decisions; undecidable draws are deferred
+      // keep the KPL independent Philox chains here, interleaved, instead of
+      // letting the compiler sink each into its (divergent) decision below
+#pragma unroll
+      for (int j = 0; j < KPL; ++j) asm volatile("" : "+r"(y[j]));
+      // phase 2: decisions; undecidable draws are deferred.  Ineligible draws
+      // (lambda >= 9.5: PTRS; tiny / non-finite products; unusable mu) enter
+      // undecided, which fast_poisson keeps and which skips its search loop.
       uint32_t defer_bits = 0;
 #pragma unroll
       for (int j = 0; j < KPL; ++j) {
         const int k = kbase + lane + kWarp * j;
         const float lam = __fmul_rn(prod[j], scale);
-        int z = 0;
-        bool exact = nz_exact || !(prod[j] >= 1e-30f) || !(lam < 9.5f);
-        if (!FULL && k >= K) exact = false;
-        else if (!exact) {
-          bool undecided = false;
-          z = fast_poisson(lam, y[j], &undecided);
-          if (undecided) {
-            exact = true;
-            z = 0;
-          }
-          if (z != 0) {
-            acc[j] += static_cast<uint32_t>(z);
-            atomicAdd(phi_counts + static_cast<int64_t>(wi) * K + k, static_cast<unsigned long long>(z));
-          }
+        bool undecided = nz_exact || !(prod[j] >= 1e-30f) || !(lam < 9.5f);
+        uint32_t z = fast_poisson(lam, y[j], &undecided);
+        if (!FULL && k >= K) undecided = false, z = 0;
+        if (undecided) {
+          defer_bits |= 1u << j;
+          z = 0;
         }
-        if (exact) defer_bits |= 1u << j;
+        if (z != 0) {
+          acc[j] += z;
+          atomicAdd(phi_counts + static_cast<int64_t>(wi) * K + k, static_cast<unsigned long long>(z));
+        }
       }
       if (__any_sync(0xffffffffu, defer_bits != 0)) {
         uint32_t masks[8];
