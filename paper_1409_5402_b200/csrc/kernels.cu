@@ -720,17 +720,24 @@ __global__ void __launch_bounds__(kFastBlock, SAMELDA_FAST_MINB) k_sample_fast(
   const int64_t item = gw / n_slices;
   const int slice = static_cast<int>(gw - item * n_slices);
   const int64_t p0 = item * chunk;
-  if (p0 >= bv.nnz) return;
   const int64_t p1 = min(p0 + chunk, bv.nnz);
   const int kbase = slice * kWarp * KPL;
   const int have_mu = mu_in != nullptr;
 
-  // stream key of topic k (rng.cpp:92-94): tag(k) * M = tag(k0) * M + 32 j M,
-  // so each draw's key is one add and one xor away from two per-lane bases
-  const uint32_t tag0 = make_tag(kPoissonCounts, sweep, static_cast<uint32_t>(kbase + lane));
-  const uint32_t kb0 = tag0 * kPhiloxM0, kb1 = tag0 * kPhiloxM1;
-  const uint32_t seed_lo = static_cast<uint32_t>(seed), seed_hi = static_cast<uint32_t>(seed >> 32);
-
+  // Round-key schedules of the block's topics (rng.cpp:92-94 keys, bumped
+  // per round as in rng.cpp:31-32), built once per block into shared memory:
+  // every warp of the block works on the same topic slice, so topic
+  // kbase + lane + 32 j reads words [j][q][lane] -- conflict-free LDS.128.
+  __shared__ uint4 s_keys[KPL][kKeyWords / 4][kWarp];
+  for (int e = threadIdx.x; e < KPL * kWarp; e += blockDim.x) {
+    const int jj = e / kWarp, ll = e % kWarp;
+    uint32_t ks[kKeyWords];
+    topic_schedule(seed, t, sweep, static_cast<uint32_t>(kbase + ll + kWarp * jj), ks);
+#pragma unroll
+    for (int q = 0; q < kKeyWords / 4; ++q)
+      s_keys[jj][q][ll] = make_uint4(ks[4 * q], ks[4 * q + 1], ks[4 * q + 2], ks[4 * q + 3]);
+  }
+  __syncthreads();
   int64_t cur_b = -1;
   float th[KPL];
   uint32_t acc[KPL];
@@ -813,11 +820,16 @@ __global__ void __launch_bounds__(kFastBlock, SAMELDA_FAST_MINB) k_sample_fast(
       uint32_t y[KPL];
 #pragma unroll
       for (int j = 0; j < KPL; ++j) {
-        const uint32_t key0 = seed_lo ^ (kb0 + static_cast<uint32_t>(kWarp * j) * kPhiloxM0);
-        const uint32_t key1 = seed_hi ^ (kb1 + static_cast<uint32_t>(kWarp * j) * kPhiloxM1);
-        uint32_t p2lo, p2hi;
-        mulhilo(kPhiloxM1, t ^ key1, p2lo, p2hi);
-        y[j] = philox_y(r1, key0, key1, p2lo, p2hi);
+        uint32_t ks[kKeyWords];
+#pragma unroll
+        for (int q = 0; q < kKeyWords / 4; ++q) {
+          const uint4 v = s_keys[j][q][lane];
+          ks[4 * q] = v.x;
+          ks[4 * q + 1] = v.y;
+          ks[4 * q + 2] = v.z;
+          ks[4 * q + 3] = v.w;
+        }
+        y[j] = philox_y_sched(r1, ks);
       }
       // keep the KPL independent Philox chains here, interleaved, instead of
       // letting the compiler sink each into its (divergent) decision below
