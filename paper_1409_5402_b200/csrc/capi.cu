@@ -297,7 +297,7 @@ struct samelda_cu_ctx {
   // scratch
   DevBuf batch, prefix, theta_batch, theta_batch32, mu, tc, pc, tf, pf, totals, err, ll,
       phi_call, phi_call_wk, phi_call32, theta_call, theta_call32, eval_scratch, theta_rows,
-      deferred, n_deferred;
+      deferred, n_deferred, cand;
   int32_t* h_batch = nullptr;
   int64_t* h_prefix = nullptr;
   int64_t h_cap = 0;
@@ -675,11 +675,13 @@ static void update_call(samelda_cu_ctx* ctx, double* theta, int64_t D, double* p
   if (expected) {
     double* pf = ensure<double>(ctx->pf, W * K);
     ck(cudaMemcpyAsync(pf, pcounts, sizeof(double) * W * K, cudaMemcpyHostToDevice, st), "upload pf");
-    ctx->launches += scu::launch_phi_mstep(nullptr, pf, W, Ki, m_t, beta, rho_t, phi_wk, nullptr, totals, ctx->d_err(), st);
+    ctx->launches += scu::launch_phi_mstep(nullptr, pf, W, Ki, m_t, beta, rho_t, phi_wk, nullptr,
+                                           ensure<double>(ctx->cand, W * K), totals, ctx->d_err(), st);
   } else {
     auto* pc = ensure<unsigned long long>(ctx->pc, W * K);
     ck(cudaMemcpyAsync(pc, pcounts, sizeof(int64_t) * W * K, cudaMemcpyHostToDevice, st), "upload pc");
-    ctx->launches += scu::launch_phi_mstep(pc, nullptr, W, Ki, m_t, beta, rho_t, phi_wk, nullptr, totals, ctx->d_err(), st);
+    ctx->launches += scu::launch_phi_mstep(pc, nullptr, W, Ki, m_t, beta, rho_t, phi_wk, nullptr,
+                                           ensure<double>(ctx->cand, W * K), totals, ctx->d_err(), st);
   }
   double* back = ensure<double>(ctx->phi_call, K * W);
   ctx->launches += scu::launch_transpose(phi_wk, W, K, back, st);
@@ -910,8 +912,8 @@ int samelda_cu_period_update(samelda_cu_ctx* ctx, double rho_t) {
     ctx->launches += scu::launch_theta_persist(tcu, tcf, ctx->batch.as<int32_t>(), ctx->B, K, ctx->m_t, c.alpha,
                                                ctx->theta.as<double>(), st);
     ctx->launches += scu::launch_phi_mstep(pcu, pcf, ctx->W, K, ctx->m_t, c.beta, rho_t, ctx->phi.as<double>(),
-                                           ctx->phi32.as<float>(), ensure<double>(ctx->totals, K),
-                                           ctx->d_err(), st);
+                                           ctx->phi32.as<float>(), ensure<double>(ctx->cand, ctx->W * K),
+                                           ensure<double>(ctx->totals, K), ctx->d_err(), st);
     ctx->tick(samelda_cu_ctx::kMstep, false);
     ctx->check_err("period");
   });

@@ -2,6 +2,7 @@
 // expected-count modes).  Compiled with -fmad=false: every f64 expression
 // rounds like the reference's x86-64 (no FMA) build.  Each kernel cites the
 // reference loop it replaces.
+#include <cuda.h>
 #include <cuda_runtime.h>
 
 #include <cstdint>
@@ -1097,6 +1098,152 @@ __global__ void __launch_bounds__(256) k_col_totals(const unsigned long long* __
   }
 }
 
+// total[k] = sum over w, in order, of x[w,k] (sampler.cpp:214-218), with x
+// precomputed in a parallel pass.  One warp per 32 topics, lane = topic:
+// each W-row contributes one coalesced 256 B segment, streamed through a
+// kChainStages-deep cp.async ring.  A lane reads back only the words it
+// copied itself, so cp.async.wait_group is the only synchronisation and the
+// loop runs at the f64 add-chain latency (8.2 cycles per row).
+constexpr int kChainRows = 64;
+constexpr int kChainStages = 8;
+constexpr size_t kChainSmem = sizeof(double) * kChainStages * kChainRows * 32;
+
+__device__ __forceinline__ void cp_async8(void* smem, const void* gmem, int src_bytes) {
+  const unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(smem));
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(s), "l"(gmem), "r"(src_bytes));
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N)); }
+
+__device__ __forceinline__ unsigned smem_addr(const void* p) {
+  return static_cast<unsigned>(__cvta_generic_to_shared(p));
+}
+
+__global__ void __launch_bounds__(32) k_col_chain(const __grid_constant__ CUtensorMap tmap,
+                                                  int64_t W, int K, double* __restrict__ totals,
+                                                  int* __restrict__ err) {
+  // ring[stage][row][32 topics], one 32 x 32 f64 TMA box per stage (rows past
+  // W / topics past K arrive zero-filled: +0.0 leaves the total unchanged).
+  // Lane 0 arms the stage's mbarrier with the box bytes and issues the
+  // tensor copy; the warp waits on the barrier phase and runs the add chain.
+  extern __shared__ __align__(128) double ring[];
+  __shared__ __align__(8) unsigned long long full[kChainStages];
+  const int lane = threadIdx.x;
+  const int k0 = blockIdx.x * 32;
+  const int64_t n_stages = (W + kChainRows - 1) / kChainRows;
+  if (lane == 0) {
+    for (int i = 0; i < kChainStages; ++i)
+      asm volatile("mbarrier.init.shared.b64 [%0], 1;" ::"r"(smem_addr(&full[i])));
+    asm volatile("fence.mbarrier_init.release.cluster;" ::);
+  }
+  __syncwarp();
+  auto issue = [&](int64_t st) {
+    if (lane != 0 || st >= n_stages) return;
+    const int slot = static_cast<int>(st % kChainStages);
+    const unsigned bar = smem_addr(&full[slot]);
+    asm volatile("fence.proxy.async.shared::cta;" ::);
+    asm volatile("mbarrier.arrive.expect_tx.shared.b64 _, [%0], %1;" ::"r"(bar),
+                 "r"(static_cast<unsigned>(kChainRows * 32 * sizeof(double))));
+    const int c0 = k0, c1 = static_cast<int>(st * kChainRows);
+    asm volatile(
+        "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes"
+        " [%0], [%1, {%2, %3}], [%4];" ::"r"(smem_addr(ring + static_cast<int64_t>(slot) * kChainRows * 32)),
+        "l"(reinterpret_cast<uint64_t>(&tmap)), "r"(c0), "r"(c1), "r"(bar)
+        : "memory");
+  };
+  for (int st = 0; st < kChainStages - 1; ++st) issue(st);
+  double total = 0.0;
+  for (int64_t st = 0; st < n_stages; ++st) {
+    issue(st + kChainStages - 1);
+    const int slot = static_cast<int>(st % kChainStages);
+    const unsigned parity = static_cast<unsigned>((st / kChainStages) & 1);
+    const unsigned bar = smem_addr(&full[slot]);
+    unsigned done = 0;
+    while (!done) {
+      asm volatile(
+          "{ .reg .pred p; mbarrier.try_wait.parity.shared.b64 p, [%1], %2; selp.u32 %0, 1, 0, p; }"
+          : "=r"(done)
+          : "r"(bar), "r"(parity)
+          : "memory");
+    }
+    const double* src = ring + static_cast<int64_t>(slot) * kChainRows * 32;
+#pragma unroll
+    for (int r = 0; r < kChainRows; ++r) total = __dadd_rn(total, src[r * 32 + lane]);
+    __syncwarp();
+  }
+  if (k0 + lane < K) {
+    totals[k0 + lane] = total;
+    if (err && (!(total > 0.0) || isinf(total))) atomicOr(err, kErrNumerical);
+  }
+}
+
+// 2-D tensor map over x[W][K] (f64), 32 x 32 boxes, zero fill out of bounds.
+bool make_chain_map(const double* x, int64_t W, int K, CUtensorMap* map) {
+  using EncodeFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
+                                const cuuint64_t*, const cuuint64_t*, const cuuint32_t*,
+                                const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
+                                CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+  static EncodeFn encode = nullptr;
+  if (encode == nullptr) {
+    void* fn = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess || fn == nullptr)
+      return false;
+    encode = reinterpret_cast<EncodeFn>(fn);
+  }
+  const cuuint64_t dims[2] = {static_cast<cuuint64_t>(K), static_cast<cuuint64_t>(W)};
+  const cuuint64_t strides[1] = {static_cast<cuuint64_t>(K) * sizeof(double)};
+  const cuuint32_t box[2] = {32, static_cast<cuuint32_t>(kChainRows)};
+  const cuuint32_t estr[2] = {1, 1};
+  return encode(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, const_cast<double*>(x), dims, strides, box,
+                estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+// sequential column totals of x[W][K]: TMA chain when a tensor map can be
+// made (row stride a multiple of 16 B), else the warp-per-topic kernel
+int launch_col_sums(const double* x, int64_t W, int K, double* totals, int* err, cudaStream_t st) {
+  CUtensorMap map;
+  if ((K & 1) == 0 && make_chain_map(x, W, K, &map)) {
+    static bool configured = false;
+    if (!configured) {
+      cudaFuncSetAttribute(k_col_chain, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           static_cast<int>(kChainSmem));
+      configured = true;
+    }
+    k_col_chain<<<static_cast<unsigned>((K + 31) / 32), 32, kChainSmem, st>>>(map, W, K, totals, err);
+  } else {
+    k_col_totals<2><<<grid_for(static_cast<int64_t>(K) * 32, 256), 256, 0, st>>>(nullptr, x, W, K, 1.0, 0.0, totals, err);
+  }
+  return 1;
+}
+
+// phi = (1 - rho) * phi + rho * cand / total (sampler.cpp:224-226); also
+// refreshes the f32 copy the sampler reads.
+__global__ void k_phi_blend_cand(const double* __restrict__ cand, const double* __restrict__ totals,
+                                 int64_t n, int K, double one_minus_rho, double rho,
+                                 double* __restrict__ phi_wk, float* __restrict__ phi32) {
+  const int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+  if (i >= n) return;
+  const double v = __dadd_rn(__dmul_rn(one_minus_rho, phi_wk[i]),
+                             __ddiv_rn(__dmul_rn(rho, cand[i]), totals[static_cast<int>(i % K)]));
+  phi_wk[i] = v;
+  if (phi32) phi32[i] = __double2float_rn(v);
+}
+
+// cand[w,k] = count / m_t + beta (the reference's `value`, sampler.cpp:209)
+__global__ void k_phi_candidate(const unsigned long long* __restrict__ cu,
+                                const double* __restrict__ cf, int64_t n, double m_t,
+                                double beta, double* __restrict__ cand) {
+  const int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+  if (i >= n) return;
+  const double hat = cu ? __ddiv_rn(static_cast<double>(static_cast<long long>(cu[i])), m_t)
+                        : __ddiv_rn(cf[i], m_t);
+  cand[i] = __dadd_rn(hat, beta);
+}
+
 // phi = (1 - rho) * phi + rho * cand / total, cand = count/m_t + beta
 // (sampler.cpp:209-226); also refreshes the f32 copy the sampler reads.
 __global__ void k_phi_blend(const unsigned long long* __restrict__ cu,
@@ -1471,16 +1618,14 @@ int launch_theta_persist(const unsigned long long* cu, const double* cf,
 
 int launch_phi_mstep(const unsigned long long* cu, const double* cf, int64_t W, int K,
                      double m_t, double beta, double rho, double* phi_wk, float* phi32,
-                     double* totals, int* err, cudaStream_t st) {
+                     double* cand, double* totals, int* err, cudaStream_t st) {
   const int64_t n = W * K;
   if (n == 0) return 0;
-  if (cu)
-    k_col_totals<0><<<grid_for(static_cast<int64_t>(K) * 32, 256), 256, 0, st>>>(cu, cf, W, K, m_t, beta, totals, err);
-  else
-    k_col_totals<1><<<grid_for(static_cast<int64_t>(K) * 32, 256), 256, 0, st>>>(cu, cf, W, K, m_t, beta, totals, err);
-  k_phi_blend<<<grid_for(n, 256), 256, 0, st>>>(cu, cf, totals, n, K, m_t, beta, 1.0 - rho, rho,
-                                               phi_wk, phi32);
-  return 2;
+  k_phi_candidate<<<grid_for(n, 256), 256, 0, st>>>(cu, cf, n, m_t, beta, cand);
+  launch_col_sums(cand, W, K, totals, err, st);
+  k_phi_blend_cand<<<grid_for(n, 256), 256, 0, st>>>(cand, totals, n, K, 1.0 - rho, rho, phi_wk,
+                                                     phi32);
+  return 3;
 }
 
 int launch_to_f32(const double* x, int64_t n, float* y, cudaStream_t st) {
@@ -1500,7 +1645,7 @@ int launch_phi_init(double* phi_wk, int64_t W, int K, double init_noise, uint64_
   uint32_t k0, k1;
   stream_key(seed, make_tag(kPhiInit, 0, 0), k0, k1);
   k_phi_init_values<<<grid_for(n, 256), 256, 0, st>>>(phi_wk, W, K, init_noise, k0, k1);
-  k_col_totals<2><<<grid_for(static_cast<int64_t>(K) * 32, 256), 256, 0, st>>>(nullptr, phi_wk, W, K, 1.0, 0.0, totals, nullptr);
+  launch_col_sums(phi_wk, W, K, totals, nullptr, st);
   k_div_cols<<<grid_for(n, 256), 256, 0, st>>>(phi_wk, n, K, totals);
   return 3;
 }

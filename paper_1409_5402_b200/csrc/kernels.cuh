@@ -77,7 +77,7 @@ int launch_theta_persist(const unsigned long long* counts_u, const double* count
 //   phi = (1-rho) phi + rho cand / total
 int launch_phi_mstep(const unsigned long long* counts_u, const double* counts_f, int64_t W,
                      int K, double m_t, double beta, double rho, double* phi_wk, float* phi32,
-                     double* totals, int* err, cudaStream_t st);
+                     double* cand_scratch, double* totals, int* err, cudaStream_t st);
 
 // f32 shadow copy (the sampler's fast path reads f32 theta / phi)
 int launch_to_f32(const double* x, int64_t n, float* y, cudaStream_t st);
