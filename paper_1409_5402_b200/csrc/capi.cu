@@ -13,6 +13,7 @@
 #include <cmath>
 #include <cstdarg>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -297,7 +298,7 @@ struct samelda_cu_ctx {
   // scratch
   DevBuf batch, prefix, theta_batch, theta_batch32, mu, tc, pc, tf, pf, totals, err, ll,
       phi_call, phi_call_wk, phi_call32, theta_call, theta_call32, eval_scratch, theta_rows,
-      deferred, n_deferred, cand;
+      deferred, n_deferred, cand, deferred_aux;
   int32_t* h_batch = nullptr;
   int64_t* h_prefix = nullptr;
   int64_t h_cap = 0;
@@ -409,12 +410,17 @@ struct samelda_cu_ctx {
       ck(cudaMemsetAsync(tc_, 0, sizeof(unsigned long long) * std::max<int64_t>(bv.B * K_, 1), stream), "zero tc");
       ck(cudaMemsetAsync(pc_, 0, sizeof(unsigned long long) * std::max<int64_t>(W_ * K_, 1), stream), "zero pc");
       tick(kSample, true);
-      const int64_t slices = (K_ + 255) / 256;
-      void* rec = ensure<unsigned char>(deferred, bv.nnz * slices * scu::deferred_record_bytes());
+      const int64_t records = bv.nnz * ((K_ + 255) / 256);
+      // flat deferred-draw list: 32 per possible record, at most 64 Mi entries
+      int64_t draw_cap = std::min<int64_t>(records * 32, int64_t{1} << 26);
+      if (const char* cap = std::getenv("SAMELDA_DRAW_CAP")) draw_cap = std::atoll(cap);  // tests
+      void* rec = ensure<unsigned char>(deferred, records * scu::deferred_record_bytes());
+      void* aux = ensure<unsigned char>(deferred_aux, scu::deferred_aux_bytes(records, draw_cap));
       launches += scu::launch_sample_fast(bv, theta_b, theta_b32, phi_wk, phi_wk32, mu_d, K_,
                                           m_t_, seed, static_cast<uint32_t>(t),
                                           static_cast<uint32_t>(sweep), tc_, pc_, rec,
-                                          ensure<unsigned long long>(n_deferred, 1), d_err(), stream);
+                                          ensure<unsigned long long>(n_deferred, 1), aux, draw_cap,
+                                          d_err(), stream);
       tick(kSample, false);
       if (profile) {
         unsigned long long nd = 0;

@@ -885,91 +885,151 @@ __global__ void __launch_bounds__(kFastBlock, SAMELDA_FAST_MINB) k_sample_fast(
   }
 }
 
-// Deferred exact draws, one warp per 32 records.  Phase A: lane l computes
-// record l's exact mu -- the reference's sequential-k f64 dot
-// (sampler.cpp:111-119) -- so 32 independent add chains run side by side
-// (unless the caller supplied mu).  Phase B: record by record, lanes over the
-// flagged topics redraw exactly as k_sample: __ddiv_rn rate, full Philox
-// block, f64 inversion or PTRS (rng.cpp:39-86).
-__global__ void __launch_bounds__(256) k_sample_deferred(
+// Deferred exact draws in two passes.
+// Phase A (k_deferred_expand), lane = record: the record's exact mu -- the
+// reference's sequential-k f64 dot (sampler.cpp:111-119), unless the caller
+// supplied mu -- and one flat-list entry per flagged topic (slots reserved
+// with one atomic per record; integer count scatter makes order irrelevant).
+// Phase B (k_deferred_draw), thread = draw: rate with __ddiv_rn, full Philox
+// block, f64 inversion or PTRS (rng.cpp:39-86), exactly as k_sample.
+struct DeferredDraw {
+  uint32_t rec;
+  uint32_t k;
+};
+
+__device__ __forceinline__ void deferred_one(const BatchView& bv, const Deferred& rec, double mu,
+                                             int k, const double* __restrict__ theta_b64,
+                                             const double* __restrict__ phi64, int K, double m_t,
+                                             uint64_t seed, uint32_t t, uint32_t sweep,
+                                             unsigned long long* __restrict__ theta_counts,
+                                             unsigned long long* __restrict__ phi_counts,
+                                             int* __restrict__ err) {
+  const uint32_t d = static_cast<uint32_t>(__ldg(bv.batch_docs + rec.b) + bv.doc_base);
+  const double cs = __dmul_rn(m_t, static_cast<double>(rec.c));
+  const double weight =
+      mu < 1e-30 ? 1.0 / static_cast<double>(K)
+                 : __ddiv_rn(__dmul_rn(__ldg(theta_b64 + static_cast<int64_t>(rec.b) * K + k),
+                                       __ldg(phi64 + static_cast<int64_t>(rec.w) * K + k)),
+                             mu);
+  const double rate = __dmul_rn(weight, cs);
+  if (!(rate >= 0.0) || isinf(rate)) {
+    atomicOr(err, kErrNumerical);
+    return;
+  }
+  if (rate == 0.0) return;
+  const uint32_t tag = make_tag(kPoissonCounts, sweep, static_cast<uint32_t>(k));
+  uint32_t k0, k1;
+  stream_key(seed, tag, k0, k1);
+  const U4 blk = philox10(U4{0u, static_cast<uint32_t>(rec.w), d, t}, k0, k1);
+  long long z;
+  if (rate < 10.0) {
+    z = poisson_inversion(rate, u64_to_uniform(join64(blk.x, blk.y)));
+  } else {
+    Stream st;
+    st.init_with_block0(seed, t, d, static_cast<uint32_t>(rec.w), tag, blk, 0);
+    z = poisson_ptrs(rate, st);
+  }
+  if (z != 0) {
+    atomicAdd(theta_counts + static_cast<int64_t>(rec.b) * K + k, static_cast<unsigned long long>(z));
+    atomicAdd(phi_counts + static_cast<int64_t>(rec.w) * K + k, static_cast<unsigned long long>(z));
+  }
+}
+
+__global__ void __launch_bounds__(256) k_deferred_expand(
     BatchView bv, const double* __restrict__ theta_b64, const double* __restrict__ phi64,
     const double* __restrict__ mu_in, int K, double m_t, uint64_t seed, uint32_t t,
     uint32_t sweep, const Deferred* __restrict__ deferred,
-    const unsigned long long* __restrict__ n_deferred,
-    unsigned long long* __restrict__ theta_counts, unsigned long long* __restrict__ phi_counts,
-    int* __restrict__ err) {
-  const int lane = threadIdx.x & 31;
+    const unsigned long long* __restrict__ n_deferred, double* __restrict__ rec_mu,
+    DeferredDraw* __restrict__ draws, unsigned long long* __restrict__ n_draws,
+    unsigned long long draw_cap, unsigned long long* __restrict__ theta_counts,
+    unsigned long long* __restrict__ phi_counts, int* __restrict__ err) {
   const int64_t n = static_cast<int64_t>(*n_deferred);
-  const double uniform_weight = 1.0 / static_cast<double>(K);
-  const int64_t warps = (static_cast<int64_t>(gridDim.x) * blockDim.x) >> 5;
-  for (int64_t r0 = ((blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x) >> 5) * 32;
-       r0 < n; r0 += warps * 32) {
-    const int n_here = static_cast<int>(min(static_cast<int64_t>(32), n - r0));
-    double my_mu = 0.0;
-    if (lane < n_here) {
-      const Deferred& me = deferred[r0 + lane];
-      if (mu_in) {
-        my_mu = mu_in[me.p];
-      } else {
-        const double* th = theta_b64 + static_cast<int64_t>(me.b) * K;
-        const double* ph = phi64 + static_cast<int64_t>(me.w) * K;
-        if ((K & 1) == 0) {
-          const double2* t2 = reinterpret_cast<const double2*>(th);
-          const double2* p2 = reinterpret_cast<const double2*>(ph);
-          for (int k2 = 0; k2 < (K >> 1); ++k2) {
-            const double2 a = __ldg(t2 + k2), c = __ldg(p2 + k2);
-            my_mu = __dadd_rn(my_mu, __dmul_rn(a.x, c.x));
-            my_mu = __dadd_rn(my_mu, __dmul_rn(a.y, c.y));
-          }
-        } else {
-          for (int k = 0; k < K; ++k) my_mu = __dadd_rn(my_mu, __dmul_rn(__ldg(th + k), __ldg(ph + k)));
+  for (int64_t r = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; r < n;
+       r += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const Deferred& me = deferred[r];
+    double mu = 0.0;
+    if (mu_in) {
+      mu = mu_in[me.p];
+    } else {
+      const double* th = theta_b64 + static_cast<int64_t>(me.b) * K;
+      const double* ph = phi64 + static_cast<int64_t>(me.w) * K;
+      if ((K & 1) == 0) {
+        const double2* t2 = reinterpret_cast<const double2*>(th);
+        const double2* p2 = reinterpret_cast<const double2*>(ph);
+        for (int k2 = 0; k2 < (K >> 1); ++k2) {
+          const double2 a = __ldg(t2 + k2), c = __ldg(p2 + k2);
+          mu = __dadd_rn(mu, __dmul_rn(a.x, c.x));
+          mu = __dadd_rn(mu, __dmul_rn(a.y, c.y));
         }
+      } else {
+        for (int k = 0; k < K; ++k) mu = __dadd_rn(mu, __dmul_rn(__ldg(th + k), __ldg(ph + k)));
       }
     }
-    for (int i = 0; i < n_here; ++i) {
-      const Deferred rec = deferred[r0 + i];
-      const double mu = __shfl_sync(0xffffffffu, my_mu, i);
-      const double* th = theta_b64 + static_cast<int64_t>(rec.b) * K;
-      const double* ph = phi64 + static_cast<int64_t>(rec.w) * K;
-      const uint32_t d = static_cast<uint32_t>(__ldg(bv.batch_docs + rec.b) + bv.doc_base);
-      const double cs = __dmul_rn(m_t, static_cast<double>(rec.c));
-      const bool degenerate = mu < 1e-30;
-      for (int j = 0; j < 8; ++j) {
-        if (!((rec.mask[j] >> lane) & 1u)) continue;
-        const int k = rec.kbase + lane + 32 * j;
-        const double weight = degenerate ? uniform_weight : __ddiv_rn(__dmul_rn(__ldg(th + k), __ldg(ph + k)), mu);
-        const double rate = __dmul_rn(weight, cs);
-        if (!(rate >= 0.0) || isinf(rate)) {
-          atomicOr(err, kErrNumerical);
-          continue;
-        }
-        if (rate == 0.0) continue;
-        const uint32_t tag = make_tag(kPoissonCounts, sweep, static_cast<uint32_t>(k));
-        uint32_t k0, k1;
-        stream_key(seed, tag, k0, k1);
-        const U4 blk = philox10(U4{0u, static_cast<uint32_t>(rec.w), d, t}, k0, k1);
-        long long z;
-        if (rate < 10.0) {
-          z = poisson_inversion(rate, u64_to_uniform(join64(blk.x, blk.y)));
-        } else {
-          Stream s;
-          s.init_with_block0(seed, t, d, static_cast<uint32_t>(rec.w), tag, blk, 0);
-          z = poisson_ptrs(rate, s);
-        }
-        if (z != 0) {
-          atomicAdd(theta_counts + static_cast<int64_t>(rec.b) * K + k, static_cast<unsigned long long>(z));
-          atomicAdd(phi_counts + static_cast<int64_t>(rec.w) * K + k, static_cast<unsigned long long>(z));
-        }
+    rec_mu[r] = mu;
+    uint32_t cnt = 0;
+#pragma unroll
+    for (int j = 0; j < 8; ++j) cnt += __popc(me.mask[j]);
+    // reserve cnt list slots; every reserved slot below draw_cap is written
+    // (phase B reads exactly [0, min(n_draws, draw_cap))), the rest is drawn here
+    unsigned long long slot = atomicAdd(n_draws, static_cast<unsigned long long>(cnt));
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      uint32_t m = me.mask[j];
+      while (m) {
+        const int bit = __ffs(m) - 1;
+        m &= m - 1;
+        const int k = me.kbase + bit + 32 * j;
+        if (slot < draw_cap)
+          draws[slot] = DeferredDraw{static_cast<uint32_t>(r), static_cast<uint32_t>(k)};
+        else
+          deferred_one(bv, me, mu, k, theta_b64, phi64, K, m_t, seed, t, sweep, theta_counts,
+                       phi_counts, err);
+        ++slot;
       }
     }
   }
+}
+
+__global__ void __launch_bounds__(256) k_deferred_draw(
+    BatchView bv, const double* __restrict__ theta_b64, const double* __restrict__ phi64, int K,
+    double m_t, uint64_t seed, uint32_t t, uint32_t sweep, const Deferred* __restrict__ deferred,
+    const double* __restrict__ rec_mu, const DeferredDraw* __restrict__ draws,
+    const unsigned long long* __restrict__ n_draws, unsigned long long draw_cap,
+    unsigned long long* __restrict__ theta_counts, unsigned long long* __restrict__ phi_counts,
+    int* __restrict__ err) {
+  const int64_t n = static_cast<int64_t>(min(*n_draws, draw_cap));
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const DeferredDraw dd = draws[i];
+    deferred_one(bv, deferred[dd.rec], rec_mu[dd.rec], static_cast<int>(dd.k), theta_b64, phi64, K,
+                 m_t, seed, t, sweep, theta_counts, phi_counts, err);
+  }
+}
+
+// Both passes.  aux = [rec_mu: max_records f64][n_draws: u64][pad][draws: draw_cap]
+void launch_deferred(const BatchView& bv, const double* tb64, const double* phi64, const double* mu,
+                     int K, double m_t, uint64_t seed, uint32_t t, uint32_t sweep, Deferred* rec,
+                     unsigned long long* n_deferred, void* aux, int64_t max_records,
+                     int64_t draw_cap, unsigned long long* tc, unsigned long long* pc, int* err,
+                     cudaStream_t st) {
+  double* rec_mu = static_cast<double*>(aux);
+  auto* n_draws = reinterpret_cast<unsigned long long*>(rec_mu + max_records);
+  auto* draws = reinterpret_cast<DeferredDraw*>(n_draws + 2);
+  cudaMemsetAsync(n_draws, 0, sizeof(unsigned long long), st);
+  k_deferred_expand<<<148 * 4, 256, 0, st>>>(bv, tb64, phi64, mu, K, m_t, seed, t, sweep, rec,
+                                             n_deferred, rec_mu, draws, n_draws,
+                                             static_cast<unsigned long long>(draw_cap), tc, pc, err);
+  k_deferred_draw<<<148 * 16, 256, 0, st>>>(bv, tb64, phi64, K, m_t, seed, t, sweep, rec, rec_mu,
+                                            draws, n_draws, static_cast<unsigned long long>(draw_cap),
+                                            tc, pc, err);
 }
 
 template <int KPL>
 int launch_fast_kpl(const BatchView& bv, const double* tb64, const float* tb32, const double* phi64,
                     const float* phi32, const double* mu, int K, double m_t, uint64_t seed,
                     uint32_t t, uint32_t sweep, unsigned long long* tc, unsigned long long* pc,
-                    void* deferred, unsigned long long* n_deferred, int* err, cudaStream_t st) {
+                    void* deferred, unsigned long long* n_deferred, void* aux, int64_t draw_cap,
+                    int* err, cudaStream_t st) {
   const int n_slices = (K + kWarp * KPL - 1) / (kWarp * KPL);
   const int64_t chunk = 128;
   const int64_t items = (bv.nnz + chunk - 1) / chunk;
@@ -982,23 +1042,24 @@ int launch_fast_kpl(const BatchView& bv, const double* tb64, const float* tb32, 
   else
     k_sample_fast<KPL, false><<<grid_for(threads, kFastBlock), kFastBlock, 0, st>>>(
         bv, tb32, phi32, mu, K, m_t, seed, t, sweep, chunk, n_slices, tc, pc, rec, n_deferred);
-  k_sample_deferred<<<148 * 8, 256, 0, st>>>(bv, tb64, phi64, mu, K, m_t, seed, t, sweep, rec,
-                                             n_deferred, tc, pc, err);
-  return 2;
+  launch_deferred(bv, tb64, phi64, mu, K, m_t, seed, t, sweep, rec, n_deferred, aux,
+                  bv.nnz * ((K + 255) / 256), draw_cap, tc, pc, err, st);
+  return 3;
 }
 
 int launch_fast_nz(const BatchView& bv, const double* tb64, const float* tb32, const double* phi64,
                    const float* phi32, const double* mu, int K, double m_t, uint64_t seed,
                    uint32_t t, uint32_t sweep, unsigned long long* tc, unsigned long long* pc,
-                   void* deferred, unsigned long long* n_deferred, int* err, cudaStream_t st) {
+                   void* deferred, unsigned long long* n_deferred, void* aux, int64_t draw_cap,
+                   int* err, cudaStream_t st) {
   const int64_t groups = (bv.nnz + 31) / 32;
   cudaMemsetAsync(n_deferred, 0, sizeof(unsigned long long), st);
   auto* rec = static_cast<Deferred*>(deferred);
   k_sample_nz<<<static_cast<unsigned>((groups + kNzWarps - 1) / kNzWarps), kNzWarps * 32, 0, st>>>(
       bv, tb32, phi32, mu, K, m_t, seed, t, sweep, tc, pc, rec, n_deferred);
-  k_sample_deferred<<<148 * 8, 256, 0, st>>>(bv, tb64, phi64, mu, K, m_t, seed, t, sweep, rec,
-                                             n_deferred, tc, pc, err);
-  return 2;
+  launch_deferred(bv, tb64, phi64, mu, K, m_t, seed, t, sweep, rec, n_deferred, aux,
+                  bv.nnz * ((K + 255) / 256), draw_cap, tc, pc, err, st);
+  return 3;
 }
 
 // ------------------------------------------------------------------- M-step
@@ -1550,13 +1611,22 @@ int launch_sample(const BatchView& bv, const double* theta_batch, const double* 
                               tf, pf, err, st);
 }
 
+
+
+// per (nonzero, 256-topic block): the record, its mu, and up to 256 flat draws
 int64_t deferred_record_bytes() { return static_cast<int64_t>(sizeof(Deferred)); }
+
+int64_t deferred_aux_bytes(int64_t max_records, int64_t draw_cap) {
+  return max_records * static_cast<int64_t>(sizeof(double)) + 16 +
+         draw_cap * static_cast<int64_t>(sizeof(DeferredDraw));
+}
 
 int launch_sample_fast(const BatchView& bv, const double* theta_b64, const float* theta_b32,
                        const double* phi64, const float* phi32, const double* mu, int K,
                        double m_t, uint64_t seed, uint32_t t, uint32_t sweep,
                        unsigned long long* tc, unsigned long long* pc, void* deferred,
-                       unsigned long long* n_deferred, int* err, cudaStream_t st) {
+                       unsigned long long* n_deferred, void* aux, int64_t draw_cap, int* err,
+                       cudaStream_t st) {
   if (bv.nnz == 0) return 0;
   // production: lane = topic, 8 topics per lane (k_sample_fast).  The two
   // alternative layouts stay selectable for profiling (SAMELDA_SAMPLER=c|n);
@@ -1568,15 +1638,15 @@ int launch_sample_fast(const BatchView& bv, const double* theta_b64, const float
   if (v == 'f' && K <= 256) {
     if (K <= 32)
       return launch_fast_kpl<1>(bv, theta_b64, theta_b32, phi64, phi32, mu, K, m_t, seed, t, sweep, tc, pc,
-                                deferred, n_deferred, err, st);
+                                deferred, n_deferred, aux, draw_cap, err, st);
     if (K <= 64)
       return launch_fast_kpl<2>(bv, theta_b64, theta_b32, phi64, phi32, mu, K, m_t, seed, t, sweep, tc, pc,
-                                deferred, n_deferred, err, st);
+                                deferred, n_deferred, aux, draw_cap, err, st);
     if (K <= 128)
       return launch_fast_kpl<4>(bv, theta_b64, theta_b32, phi64, phi32, mu, K, m_t, seed, t, sweep, tc, pc,
-                                deferred, n_deferred, err, st);
+                                deferred, n_deferred, aux, draw_cap, err, st);
     return launch_fast_kpl<8>(bv, theta_b64, theta_b32, phi64, phi32, mu, K, m_t, seed, t, sweep, tc, pc,
-                              deferred, n_deferred, err, st);
+                              deferred, n_deferred, aux, draw_cap, err, st);
   }
   if (v == 'c' && K <= 32 * kCtaMaxWarps) {
     const int nwarps = (K + 31) / 32;
@@ -1591,12 +1661,12 @@ int launch_sample_fast(const BatchView& bv, const double* theta_b64, const float
       k_sample_cta<kCtaMaxWarps><<<grid, nwarps * 32, 0, st>>>(bv, theta_b32, phi32, mu, K, nwarps,
                                                                m_t, seed, t, sweep, chunk, tc, pc,
                                                                rec, n_deferred);
-    k_sample_deferred<<<148 * 8, 256, 0, st>>>(bv, theta_b64, phi64, mu, K, m_t, seed, t, sweep,
-                                               rec, n_deferred, tc, pc, err);
-    return 2;
+    launch_deferred(bv, theta_b64, phi64, mu, K, m_t, seed, t, sweep, rec, n_deferred, aux,
+                    bv.nnz * ((K + 255) / 256), draw_cap, tc, pc, err, st);
+    return 3;
   }
   return launch_fast_nz(bv, theta_b64, theta_b32, phi64, phi32, mu, K, m_t, seed, t, sweep, tc,
-                        pc, deferred, n_deferred, err, st);
+                        pc, deferred, n_deferred, aux, draw_cap, err, st);
 }
 
 int launch_theta_from_counts(const unsigned long long* cu, const double* cf, int64_t n,

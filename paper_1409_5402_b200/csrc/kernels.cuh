@@ -53,14 +53,17 @@ int launch_sample(const BatchView& bv, const double* theta_batch, const double* 
 // Same draws, bit for bit, through an f32 fast path with exact f64 fallback
 // (see kernels.cu).  mu == nullptr: the kernel forms mu itself (period path).
 // `deferred` holds up to nnz * ceil(K / 256) records of
-// deferred_record_bytes() each; n_deferred is one u64 of scratch.
+// deferred_record_bytes() each; n_deferred is one u64 of scratch; `aux` holds
+// deferred_aux_bytes(records, draw_cap) (per-record mu + a flat list of up to
+// draw_cap deferred draws; overflow is drawn inline, never dropped).
 int launch_sample_fast(const BatchView& bv, const double* theta_b64, const float* theta_b32,
                        const double* phi64, const float* phi32, const double* mu, int K,
                        double m_t, uint64_t seed, uint32_t t, uint32_t sweep,
                        unsigned long long* theta_counts, unsigned long long* phi_counts,
-                       void* deferred, unsigned long long* n_deferred, int* err,
-                       cudaStream_t st);
+                       void* deferred, unsigned long long* n_deferred, void* aux,
+                       int64_t draw_cap, int* err, cudaStream_t st);
 int64_t deferred_record_bytes();
+int64_t deferred_aux_bytes(int64_t max_records, int64_t draw_cap);
 
 // out[i] = counts[i] / m_t + alpha over n entries       (sampler.cpp:324-330)
 int launch_theta_from_counts(const unsigned long long* counts_u, const double* counts_f,

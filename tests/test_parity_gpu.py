@@ -369,3 +369,21 @@ def test_eval_errors(port):
         S.perword_loglik(np.full((1, 9), 1 / 9), g, 0.1, 3)
     with pytest.raises(S.NumericalError):
         S.perword_loglik(np.zeros((1, 8)), g, 0.1, 3)
+
+
+def test_deferred_overflow_path_bit_exact(port, monkeypatch):
+    """A full deferred-draw list makes records draw inline: results unchanged."""
+    g = port.make_corpus(60, 50, 4, 60.0, 9)
+    rng = np.random.default_rng(3)
+    K = 64
+    theta = rng.gamma(0.3, 1.0, size=(g.n_docs, K)) + 1e-3
+    phi = rng.gamma(0.2, 1.0, size=(K, g.n_words)) + 1e-9
+    phi /= phi.sum(1, keepdims=True)
+    batch = all_docs(g)
+    mu = port.sddmm(theta, phi, g, batch)
+    otc, opc = port.sample_counts(theta, phi, mu, g, batch, 400.0, 5, 2, 1)  # many PTRS draws
+    for cap in ("0", "7"):
+        monkeypatch.setenv("SAMELDA_DRAW_CAP", cap)
+        sc = S.sample_counts(theta, phi, mu, g, batch, 400.0, 5, 2, 1)
+        np.testing.assert_array_equal(sc.theta_counts, otc)
+        np.testing.assert_array_equal(sc.phi_counts, opc)
