@@ -256,20 +256,17 @@ __device__ __forceinline__ uint32_t fast_poisson(float lam, uint32_t y, bool* un
   const float c1 = __fadd_rn(e0, t1);
   const float t2 = __fmul_rn(__fmul_rn(t1, lam), 0.5f);
   const float c2 = __fadd_rn(c1, t2);
-  // relative bound r_k = 4e-6 + 4e-6 lambda + 6e-6 k; absolute 2.5e-7 for u
+  // relative bound r_k = 4e-6 + 4e-6 lambda + 6e-6 k, absolute 2.5e-7 for u:
+  // u is decided against cdf_k unless |u - cdf_k| <= m_k = cdf_k r_k + 2.5e-7
   const float r0 = __fmaf_rn(4e-6f, lam, 4e-6f);
-  const float a0 = __fsub_rn(1.0f, r0), b0 = __fadd_rn(1.0f, r0);
-  const float lo0 = __fmaf_rn(e0, a0, -2.5e-7f), hi0 = __fmaf_rn(e0, b0, 2.5e-7f);
-  const float lo1 = __fmaf_rn(c1, __fsub_rn(a0, 6e-6f), -2.5e-7f);
-  const float hi1 = __fmaf_rn(c1, __fadd_rn(b0, 6e-6f), 2.5e-7f);
-  const float lo2 = __fmaf_rn(c2, __fsub_rn(a0, 1.2e-5f), -2.5e-7f);
-  const float hi2 = __fmaf_rn(c2, __fadd_rn(b0, 1.2e-5f), 2.5e-7f);
-  // u sits in an uncertainty band iff it passes a lower bound but not the
-  // matching upper one: count both ways, compare
-  const uint32_t z_lo = (u > lo0) + (u > lo1) + (u > lo2);
-  uint32_t z = (u > hi0) + (u > hi1) + (u > hi2);
-  *undecided = *undecided || (z_lo != z);
+  const float m0 = __fmaf_rn(e0, r0, 2.5e-7f);
+  const float m1 = __fmaf_rn(c1, __fadd_rn(r0, 6e-6f), 2.5e-7f);
+  const float m2 = __fmaf_rn(c2, __fadd_rn(r0, 1.2e-5f), 2.5e-7f);
+  const float d0 = __fsub_rn(u, e0), d1 = __fsub_rn(u, c1), d2 = __fsub_rn(u, c2);
+  *undecided = *undecided || (fabsf(d0) <= m0) || (fabsf(d1) <= m1) || (fabsf(d2) <= m2);
+  uint32_t z = (d0 > m0) + (d1 > m1) + (d2 > m2);
   if (z < 3 || *undecided) return z;
+  const float a0 = __fsub_rn(1.0f, r0), b0 = __fadd_rn(1.0f, r0);
   // sequential search from k = 3 (u beyond cdf_2)
   float pmf = t2, cdf = c2, zf = 2.0f;
   float rlo = __fsub_rn(a0, 1.2e-5f), rhi = __fadd_rn(b0, 1.2e-5f);
