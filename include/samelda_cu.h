@@ -164,7 +164,11 @@ int samelda_cu_train_begin(samelda_cu_ctx* ctx, const samelda_cu_corpus* corpus,
 int samelda_cu_heldout(samelda_cu_ctx* ctx, const samelda_cu_corpus* test, uint64_t seed);
 
 /* One period (sampler.cpp:307-333) on the resident model: gather theta rows,
- * inner_sweeps x (sddmm, sample), persist theta, M-step on phi. */
+ * inner_sweeps x (sddmm, sample), persist theta, M-step on phi.
+ * Asynchronous: the host does not wait for the device; a NumericalError raised
+ * on the device (non-finite rate, bad phi row mass) is reported by the next
+ * period call or by the next synchronising call (samelda_cu_synchronize,
+ * _evaluate, _model_download, _batch_theta, _count_totals). */
 int samelda_cu_period(samelda_cu_ctx* ctx, const int32_t* doc_ids, int64_t B, int64_t t,
                       double m_t, double rho_t);
 /* The same period split at the topic-word count exchange, for doc-sharded

@@ -299,9 +299,21 @@ struct samelda_cu_ctx {
   DevBuf batch, prefix, theta_batch, theta_batch32, mu, tc, pc, tf, pf, totals, err, ll,
       phi_call, phi_call_wk, phi_call32, theta_call, theta_call32, eval_scratch, theta_rows,
       deferred, n_deferred, cand, deferred_aux;
-  int32_t* h_batch = nullptr;
-  int64_t* h_prefix = nullptr;
-  int64_t h_cap = 0;
+  // double-buffered pinned staging of batch ids / prefixes: the host may run
+  // periods ahead of the device; a buffer is reused only after the copies of
+  // two periods ago have executed (event)
+  struct Staging {
+    int32_t* batch = nullptr;
+    int64_t* prefix = nullptr;
+    int64_t cap = 0;
+    cudaEvent_t done = nullptr;
+  };
+  Staging stg[2];
+  int stg_next = 0;
+  // sticky device error flag, read back asynchronously after each period
+  int* h_err = nullptr;
+  cudaEvent_t err_event = nullptr;
+  bool err_pending = false;
 
   ~samelda_cu_ctx() {
     for (auto& v : events)
@@ -309,14 +321,55 @@ struct samelda_cu_ctx {
         cudaEventDestroy(e.first);
         cudaEventDestroy(e.second);
       }
-    if (h_batch) cudaFreeHost(h_batch);
-    if (h_prefix) cudaFreeHost(h_prefix);
+    for (auto& sb : stg) {
+      if (sb.batch) cudaFreeHost(sb.batch);
+      if (sb.prefix) cudaFreeHost(sb.prefix);
+      if (sb.done) cudaEventDestroy(sb.done);
+    }
+    if (h_err) cudaFreeHost(h_err);
+    if (err_event) cudaEventDestroy(err_event);
     if (own_stream) cudaStreamDestroy(own_stream);
   }
 
-  int* d_err() { return ensure<int>(err, 1); }
+  int* d_err() {
+    if (err.p == nullptr) {
+      ensure<int>(err, 1);
+      ck(cudaMemsetAsync(err.p, 0, sizeof(int), stream), "zero error flag");
+    }
+    return err.as<int>();
+  }
 
-  void reset_err() { ck(cudaMemsetAsync(d_err(), 0, sizeof(int), stream), "reset error flag"); }
+  // enqueue the read-back of the sticky error flag (no host wait)
+  void post_err_check() {
+    if (h_err == nullptr) ck(cudaHostAlloc(&h_err, sizeof(int), cudaHostAllocDefault), "pinned err");
+    if (err_event == nullptr) ck(cudaEventCreateWithFlags(&err_event, cudaEventDisableTiming), "err event");
+    ck(cudaMemcpyAsync(h_err, d_err(), sizeof(int), cudaMemcpyDeviceToHost, stream), "read error flag");
+    ck(cudaEventRecord(err_event, stream), "err event");
+    err_pending = true;
+  }
+
+  // report a pending device error (NumericalError) once its read-back landed;
+  // wait == true blocks for it
+  void poll_err(bool wait, const char* what) {
+    if (!err_pending) return;
+    if (wait) {
+      ck(cudaEventSynchronize(err_event), what);
+    } else if (cudaEventQuery(err_event) == cudaErrorNotReady) {
+      cudaGetLastError();
+      return;
+    }
+    err_pending = false;
+    if (*h_err & scu::kErrNumerical) {
+      *h_err = 0;
+      ck(cudaMemsetAsync(d_err(), 0, sizeof(int), stream), "reset error flag");
+      fail(SAMELDA_CU_NUMERICAL, "%s: nonfinite or negative value (NumericalError)", what);
+    }
+  }
+
+  void reset_err() {
+    poll_err(true, "previous period");  // never clear an unreported device error
+    ck(cudaMemsetAsync(d_err(), 0, sizeof(int), stream), "reset error flag");
+  }
 
   void check_err(const char* what) {
     int h = 0;
@@ -326,22 +379,26 @@ struct samelda_cu_ctx {
     if (h & scu::kErrNumerical) fail(SAMELDA_CU_NUMERICAL, "%s: nonfinite or negative value", what);
   }
 
-  void stage(int64_t B_) {
-    if (h_cap < B_ + 1) {
-      if (h_batch) cudaFreeHost(h_batch);
-      if (h_prefix) cudaFreeHost(h_prefix);
-      h_cap = std::max<int64_t>(B_ + 1, 1024);
-      ck(cudaHostAlloc(&h_batch, sizeof(int32_t) * h_cap, cudaHostAllocDefault), "pinned batch");
-      ck(cudaHostAlloc(&h_prefix, sizeof(int64_t) * h_cap, cudaHostAllocDefault), "pinned prefix");
+  Staging& stage(int64_t B_) {
+    Staging& sb = stg[stg_next];
+    stg_next ^= 1;
+    if (sb.done) ck(cudaEventSynchronize(sb.done), "batch staging");
+    else ck(cudaEventCreateWithFlags(&sb.done, cudaEventDisableTiming), "staging event");
+    if (sb.cap < B_ + 1) {
+      if (sb.batch) cudaFreeHost(sb.batch);
+      if (sb.prefix) cudaFreeHost(sb.prefix);
+      sb.cap = std::max<int64_t>(B_ + 1, 1024);
+      ck(cudaHostAlloc(&sb.batch, sizeof(int32_t) * sb.cap, cudaHostAllocDefault), "pinned batch");
+      ck(cudaHostAlloc(&sb.prefix, sizeof(int64_t) * sb.cap, cudaHostAllocDefault), "pinned prefix");
     }
+    return sb;
   }
 
   // Upload a batch of doc ids of `slot` and its nonzero prefix (sampler.cpp:18-24).
   scu::BatchView upload_batch(const CorpusSlot& slot, const int32_t* doc_ids, int64_t B_) {
-    // the previous period's async copies out of the pinned staging buffers
-    // must have landed before they are overwritten
-    ck(cudaStreamSynchronize(stream), "batch staging");
-    stage(B_);
+    Staging& sb = stage(B_);
+    int32_t* h_batch = sb.batch;
+    int64_t* h_prefix = sb.prefix;
     h_prefix[0] = 0;
     for (int64_t b = 0; b < B_; ++b) {
       const int32_t d = doc_ids[b];
@@ -357,6 +414,7 @@ struct samelda_cu_ctx {
          "upload batch");
     ck(cudaMemcpyAsync(dp, h_prefix, sizeof(int64_t) * (B_ + 1), cudaMemcpyHostToDevice, stream),
        "upload prefix");
+    ck(cudaEventRecord(sb.done, stream), "staging event");
     scu::BatchView bv;
     bv.doc_offsets = slot.offs.as<int64_t>();
     bv.word_ids = slot.words.as<int32_t>();
@@ -545,7 +603,10 @@ int samelda_cu_set_stream(samelda_cu_ctx* ctx, void* cuda_stream) {
 }
 
 int samelda_cu_synchronize(samelda_cu_ctx* ctx) {
-  return guarded(ctx, [&] { ck(cudaStreamSynchronize(ctx->stream), "synchronize"); });
+  return guarded(ctx, [&] {
+    ck(cudaStreamSynchronize(ctx->stream), "synchronize");
+    ctx->poll_err(true, "period");
+  });
 }
 
 int64_t samelda_cu_launch_count(const samelda_cu_ctx* ctx) { return ctx ? ctx->launches : 0; }
@@ -866,6 +927,7 @@ int samelda_cu_period_sample(samelda_cu_ctx* ctx, const int32_t* doc_ids, int64_
     const samelda_cu_config& c = ctx->cfg;
     const int K = ctx->K;
     cudaStream_t st = ctx->stream;
+    ctx->poll_err(false, "period");
     scu::BatchView bv = ctx->upload_batch(ctx->train, doc_ids, B);
     bv.doc_base = ctx->doc_base;
     ctx->B = B;
@@ -875,7 +937,6 @@ int samelda_cu_period_sample(samelda_cu_ctx* ctx, const int32_t* doc_ids, int64_
     float* thb32 = ensure<float>(ctx->theta_batch32, B * K);
     const bool expected = c.mode == SAMELDA_CU_MODE_EXPECTED;
     double* mu = expected ? ensure<double>(ctx->mu, bv.nnz) : nullptr;
-    ctx->reset_err();
     ctx->launches += scu::launch_gather_theta(ctx->theta.as<double>(), bv.batch_docs, B, K, thb, thb32, st);
     for (int64_t sweep = 0; sweep < c.inner_sweeps; ++sweep) {
       if (expected) {
@@ -921,7 +982,10 @@ int samelda_cu_period_update(samelda_cu_ctx* ctx, double rho_t) {
                                            ctx->phi32.as<float>(), ensure<double>(ctx->cand, ctx->W * K),
                                            ensure<double>(ctx->totals, K), ctx->d_err(), st);
     ctx->tick(samelda_cu_ctx::kMstep, false);
-    ctx->check_err("period");
+    ck(cudaGetLastError(), "period launch");
+    // no host wait: the flag is read back asynchronously and reported by the
+    // next call (NumericalError), or at the next synchronising call
+    ctx->post_err_check();
   });
 }
 
@@ -982,6 +1046,7 @@ int samelda_cu_phi_counts_device(samelda_cu_ctx* ctx, void** ptr, int64_t* n_ele
 
 int samelda_cu_batch_theta(samelda_cu_ctx* ctx, double* out, int64_t cap) {
   return guarded(ctx, [&] {
+    ctx->poll_err(true, "period");
     if (!ctx->model_ready) fail(SAMELDA_CU_CONFIG, "no model");
     const int64_t n = ctx->B * ctx->K;
     if (cap < n) fail(SAMELDA_CU_CONFIG, "batch_theta: buffer too small");
@@ -996,6 +1061,7 @@ int samelda_cu_batch_theta(samelda_cu_ctx* ctx, double* out, int64_t cap) {
 
 int samelda_cu_count_totals(samelda_cu_ctx* ctx, int64_t* theta_total, int64_t* phi_total) {
   return guarded(ctx, [&] {
+    ctx->poll_err(true, "period");
     if (!ctx->counts_ready || ctx->counts_float) fail(SAMELDA_CU_CONFIG, "no integer counts");
     std::vector<int64_t> a(static_cast<size_t>(std::max<int64_t>(ctx->B * ctx->K, 1)));
     std::vector<int64_t> b(static_cast<size_t>(std::max<int64_t>(ctx->W * ctx->K, 1)));
@@ -1021,6 +1087,7 @@ int samelda_cu_evaluate(samelda_cu_ctx* ctx, double* ll_out) {
 
 int samelda_cu_model_download(samelda_cu_ctx* ctx, double* phi, double* theta) {
   return guarded(ctx, [&] {
+    ctx->poll_err(true, "period");
     if (!ctx->model_ready) fail(SAMELDA_CU_CONFIG, "no model");
     const int64_t K = ctx->K;
     if (phi) {

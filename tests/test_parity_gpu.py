@@ -387,3 +387,17 @@ def test_deferred_overflow_path_bit_exact(port, monkeypatch):
         sc = S.sample_counts(theta, phi, mu, g, batch, 400.0, 5, 2, 1)
         np.testing.assert_array_equal(sc.theta_counts, otc)
         np.testing.assert_array_equal(sc.phi_counts, opc)
+
+
+def test_trainer_reports_device_error_asynchronously(port):
+    """A period that hits a non-finite rate raises NumericalError by the next
+    synchronising call (periods are asynchronous)."""
+    g = port.make_corpus(20, 15, 3, 10.0, 4)
+    tr = S.Trainer(g, S.SamplerConfig(n_topics=3, m=5.0, t_max=4, batch_fraction=1.0, seed=2))
+    model = tr.model()
+    model.phi[:] = np.nan
+    tr.ctx.check(tr.ctx.lib.samelda_cu_model_upload(tr.ctx.h, S._ptr(np.ascontiguousarray(model.phi)), None))
+    tr.period(np.arange(g.n_docs, dtype=np.int32), 0, 5.0, 1.0)
+    with pytest.raises(S.NumericalError):
+        tr.ctx.synchronize()
+    tr.ctx.synchronize()  # reported once, then cleared
