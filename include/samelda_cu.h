@@ -85,8 +85,11 @@ int samelda_cu_create(int device, samelda_cu_ctx** out);
 void samelda_cu_destroy(samelda_cu_ctx* ctx);
 const char* samelda_cu_last_error(const samelda_cu_ctx* ctx);
 /* Run every kernel of this context on `cuda_stream` (a cudaStream_t), e.g.
- * the caller's framework stream; NULL restores the context's own stream. */
+ * the caller's framework stream; NULL is the legacy default stream.  A new
+ * context runs on its own non-blocking stream; samelda_cu_use_own_stream
+ * returns to it. */
 int samelda_cu_set_stream(samelda_cu_ctx* ctx, void* cuda_stream);
+int samelda_cu_use_own_stream(samelda_cu_ctx* ctx);
 int samelda_cu_synchronize(samelda_cu_ctx* ctx);
 /* number of kernel launches this context issued since creation */
 int64_t samelda_cu_launch_count(const samelda_cu_ctx* ctx);

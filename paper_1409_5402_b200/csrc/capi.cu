@@ -598,7 +598,15 @@ const char* samelda_cu_last_error(const samelda_cu_ctx* ctx) {
 int samelda_cu_set_stream(samelda_cu_ctx* ctx, void* cuda_stream) {
   return guarded(ctx, [&] {
     ck(cudaStreamSynchronize(ctx->stream), "sync old stream");
-    ctx->stream = cuda_stream ? static_cast<cudaStream_t>(cuda_stream) : ctx->own_stream;
+    // NULL is the legacy default stream (e.g. torch's default stream), not "own"
+    ctx->stream = static_cast<cudaStream_t>(cuda_stream);
+  });
+}
+
+int samelda_cu_use_own_stream(samelda_cu_ctx* ctx) {
+  return guarded(ctx, [&] {
+    ck(cudaStreamSynchronize(ctx->stream), "sync old stream");
+    ctx->stream = ctx->own_stream;
   });
 }
 

@@ -82,6 +82,7 @@ SIGNATURES = [
     ("samelda_cu_destroy", None, [_P]),
     ("samelda_cu_last_error", C.c_char_p, [_P]),
     ("samelda_cu_set_stream", C.c_int, [_P, _P]),
+    ("samelda_cu_use_own_stream", C.c_int, [_P]),
     ("samelda_cu_synchronize", C.c_int, [_P]),
     ("samelda_cu_launch_count", _I64, [_P]),
     ("samelda_cu_sddmm", C.c_int, [_P, _CP, _P, _I64, _I64, _P, _I64, _I64, _P, _P, _I64,
@@ -295,8 +296,13 @@ class Context:
             msg = self.lib.samelda_cu_last_error(self.h).decode(errors="replace")
             raise _CODES.get(rc, SameldaError)(msg)
 
-    def set_stream(self, stream_handle: int | None):
-        self.check(self.lib.samelda_cu_set_stream(self.h, stream_handle))
+    def set_stream(self, stream_handle: int):
+        """Run on a caller's cudaStream_t handle (0 = the legacy default stream,
+        which is torch's default stream)."""
+        self.check(self.lib.samelda_cu_set_stream(self.h, C.c_void_p(int(stream_handle))))
+
+    def use_own_stream(self):
+        self.check(self.lib.samelda_cu_use_own_stream(self.h))
 
     def synchronize(self):
         self.check(self.lib.samelda_cu_synchronize(self.h))

@@ -1,0 +1,87 @@
+"""Two ranks on the GPU box (both on cuda:0, gloo for the collective since one
+device cannot host two NCCL ranks): real kernels, real doc sharding, real
+all-reduce of the device phi-count buffer through distributed.ShardedTrainer.
+The sharded phi must equal single-process training bit for bit -- the
+property the NCCL run on 8 B200s relies on."""
+from __future__ import annotations
+
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+pytestmark = pytest.mark.gpu
+
+K, SEED, M, T_MAX, BF = 8, 7, 20.0, 5, 0.25
+
+
+def _corpus():
+    from oracle import Port
+    port = Port()
+    return port.make_corpus(120, 60, 4, 30.0, 3)
+
+
+def _worker(rank, world, port_no, out_path):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port_no))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    torch.cuda.set_device(0)
+    from paper_1409_5402_b200 import distributed as D
+    from paper_1409_5402_b200 import samelda as S
+    g = _corpus()
+    lo, hi = D.shard_ranges(g.doc_offsets, world)[rank]
+    offs = g.doc_offsets[lo:hi + 1] - g.doc_offsets[lo]
+    local = S.Corpus(offs, g.word_ids[g.doc_offsets[lo]:g.doc_offsets[hi]],
+                     g.counts[g.doc_offsets[lo]:g.doc_offsets[hi]], g.n_words)
+    ctx = S.Context(0)
+    stream = torch.cuda.Stream(device=0)
+    torch.cuda.set_stream(stream)
+    ctx.set_stream(stream.cuda_stream)
+    cfg = S.SamplerConfig(n_topics=K, m=M, schedule="invlinear", t_max=T_MAX, batch_fraction=BF,
+                          seed=SEED)
+    tr = S.Trainer(local, cfg, ctx=ctx)
+    tr.set_doc_base(lo)
+
+    class GlooEngine(D.CudaEngine):
+        """gloo reduces host tensors: stage the device counts through the host."""
+
+        def counts(self):
+            self._host = super().counts().cpu()
+            return self._host
+
+        def update(self, rho):
+            super().counts().copy_(self._host)
+            super().update(rho)
+
+    st = D.ShardedTrainer(GlooEngine(tr, 0), g.n_docs, lo, hi, local.doc_tokens(), BF, SEED, M,
+                          "invlinear", T_MAX)
+    for _ in range(T_MAX):
+        st.period()
+    model = tr.model()
+    if rank == 0:
+        np.savez(out_path, phi=model.phi, theta_rows=model.theta)
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+@pytest.mark.timeout(600)
+def test_two_rank_sharded_training_equals_single_gpu(tmp_path):
+    from paper_1409_5402_b200 import samelda as S
+    out = str(tmp_path / "rank0.npz")
+    mp.start_processes(_worker, args=(2, _free_port(), out), nprocs=2, start_method="spawn")
+    got = np.load(out)
+    g = _corpus()
+    model, _ = S.train(g, S.SamplerConfig(n_topics=K, m=M, schedule="invlinear", t_max=T_MAX,
+                                          batch_fraction=BF, seed=SEED))
+    np.testing.assert_array_equal(got["phi"], model.phi)
