@@ -298,7 +298,7 @@ struct samelda_cu_ctx {
   // scratch
   DevBuf batch, prefix, theta_batch, theta_batch32, mu, tc, pc, tf, pf, totals, err, ll,
       phi_call, phi_call_wk, phi_call32, theta_call, theta_call32, eval_scratch, theta_rows,
-      deferred, n_deferred, cand, deferred_aux;
+      deferred, n_deferred, cand, deferred_aux, mu_f32;
   // double-buffered pinned staging of batch ids / prefixes: the host may run
   // periods ahead of the device; a buffer is reused only after the copies of
   // two periods ago have executed (event)
@@ -478,7 +478,8 @@ struct samelda_cu_ctx {
                                           m_t_, seed, static_cast<uint32_t>(t),
                                           static_cast<uint32_t>(sweep), tc_, pc_, rec,
                                           ensure<unsigned long long>(n_deferred, 1), aux, draw_cap,
-                                          d_err(), stream);
+                                          K_ > 256 ? ensure<float>(mu_f32, bv.nnz) : nullptr, d_err(),
+                                          stream);
       tick(kSample, false);
       if (profile) {
         unsigned long long nd = 0;

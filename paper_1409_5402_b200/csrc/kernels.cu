@@ -703,20 +703,55 @@ __global__ void __launch_bounds__(MAXW * 32) k_sample_cta(
   if (cur_b >= 0 && acc && k_ok) atomicAdd(theta_counts + cur_b * K + k, static_cast<unsigned long long>(acc));
 }
 
-template <int KPL, bool FULL>
+// f32 mu of every batch nonzero over all K topics (fast path only; the exact
+// f64 mu of deferred draws is computed separately).  Warp per 32 nonzeros:
+// lanes over topics, shuffle tree per nonzero, lane i keeps nonzero i's.
+__global__ void __launch_bounds__(256) k_mu_f32(BatchView bv, const float* __restrict__ theta_b32,
+                                                const float* __restrict__ phi32, int K,
+                                                float* __restrict__ mu_f) {
+  const int lane = threadIdx.x & 31;
+  const int64_t g0 = ((blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x) >> 5) * 32;
+  if (g0 >= bv.nnz) return;
+  const int n_here = static_cast<int>(min(static_cast<int64_t>(32), bv.nnz - g0));
+  int64_t b = 0;
+  int32_t w = 0;
+  if (lane < n_here) {
+    const int64_t p = g0 + lane;
+    b = find_row(bv.batch_prefix, bv.B, p);
+    const int32_t d = __ldg(bv.batch_docs + b);
+    w = __ldg(bv.word_ids + __ldg(bv.doc_offsets + d) + (p - __ldg(bv.batch_prefix + b)));
+  }
+  float mine = 0.0f;
+  for (int i = 0; i < n_here; ++i) {
+    const int64_t bi = __shfl_sync(0xffffffffu, b, i);
+    const int32_t wi = __shfl_sync(0xffffffffu, w, i);
+    const float* tr = theta_b32 + bi * K;
+    const float* pr = phi32 + static_cast<int64_t>(wi) * K;
+    float part = 0.0f;
+    for (int k = lane; k < K; k += 32) part = __fadd_rn(part, __fmul_rn(__ldg(tr + k), __ldg(pr + k)));
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) part = __fadd_rn(part, __shfl_xor_sync(0xffffffffu, part, o));
+    if (lane == i) mine = part;
+  }
+  if (lane < n_here) mu_f[g0 + lane] = mine;
+}
+
 #ifndef SAMELDA_FAST_MINB
 #define SAMELDA_FAST_MINB 4
 #endif
+template <int KPL, bool FULL>
 __global__ void __launch_bounds__(kFastBlock, SAMELDA_FAST_MINB) k_sample_fast(
     BatchView bv, const float* __restrict__ theta_b32, const float* __restrict__ phi32,
-    const double* __restrict__ mu_in, int K, double m_t, uint64_t seed, uint32_t t,
-    uint32_t sweep, int64_t chunk, int n_slices, unsigned long long* __restrict__ theta_counts,
+    const double* __restrict__ mu_in, const float* __restrict__ mu_f_in, int K, double m_t,
+    uint64_t seed, uint32_t t, uint32_t sweep, int64_t chunk, int n_slices,
+    unsigned long long* __restrict__ theta_counts,
     unsigned long long* __restrict__ phi_counts, Deferred* __restrict__ deferred,
     unsigned long long* __restrict__ n_deferred) {
   const int lane = threadIdx.x & 31;
-  const int64_t gw = (blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x) >> 5;
-  const int64_t item = gw / n_slices;
-  const int slice = static_cast<int>(gw - item * n_slices);
+  // blockIdx.y = topic slice (all warps of a block share it, and with it the
+  // round-key table); blockIdx.x * warps + warp = nonzero chunk
+  const int64_t item = static_cast<int64_t>(blockIdx.x) * (kFastBlock / kWarp) + (threadIdx.x >> 5);
+  const int slice = static_cast<int>(blockIdx.y);
   const int64_t p0 = item * chunk;
   const int64_t p1 = min(p0 + chunk, bv.nnz);
   const int kbase = slice * kWarp * KPL;
@@ -750,6 +785,7 @@ __global__ void __launch_bounds__(kFastBlock, SAMELDA_FAST_MINB) k_sample_fast(
     int64_t b = 0;
     int32_t d = 0, w = 0, c = 0;
     double mu_v = 0.0;
+    float muf_v = 0.0f;
     if (p < p1) {
       b = find_row(bv.batch_prefix, bv.B, p);
       d = __ldg(bv.batch_docs + b);
@@ -757,6 +793,7 @@ __global__ void __launch_bounds__(kFastBlock, SAMELDA_FAST_MINB) k_sample_fast(
       w = __ldg(bv.word_ids + gi);
       c = __ldg(bv.counts + gi);
       if (have_mu) mu_v = __ldg(mu_in + p);
+      if (mu_f_in) muf_v = __ldg(mu_f_in + p);
     }
     const int n_here = static_cast<int>(min(static_cast<int64_t>(kWarp), p1 - g0));
     for (int i = 0; i < n_here; ++i) {
@@ -766,6 +803,7 @@ __global__ void __launch_bounds__(kFastBlock, SAMELDA_FAST_MINB) k_sample_fast(
       const int32_t wi = __shfl_sync(0xffffffffu, w, i);
       const int32_t ci = __shfl_sync(0xffffffffu, c, i);
       const double mui = __shfl_sync(0xffffffffu, mu_v, i);
+      const float mufi = __shfl_sync(0xffffffffu, muf_v, i);
       // phi[w, slice]: 32 lanes x KPL coalesced loads (occupancy hides latency)
       float ph[KPL];
       {
@@ -803,6 +841,8 @@ __global__ void __launch_bounds__(kFastBlock, SAMELDA_FAST_MINB) k_sample_fast(
       float mu_f;
       if (have_mu) {
         mu_f = __double2float_rn(mui);
+      } else if (mu_f_in) {
+        mu_f = mufi;  // full-K mu from k_mu_f32 (sliced K > 256)
       } else {
         mu_f = part;
 #pragma unroll
@@ -1026,22 +1066,30 @@ int launch_fast_kpl(const BatchView& bv, const double* tb64, const float* tb32, 
                     const float* phi32, const double* mu, int K, double m_t, uint64_t seed,
                     uint32_t t, uint32_t sweep, unsigned long long* tc, unsigned long long* pc,
                     void* deferred, unsigned long long* n_deferred, void* aux, int64_t draw_cap,
-                    int* err, cudaStream_t st) {
+                    float* mu_f, int* err, cudaStream_t st) {
   const int n_slices = (K + kWarp * KPL - 1) / (kWarp * KPL);
   const int64_t chunk = 128;
   const int64_t items = (bv.nnz + chunk - 1) / chunk;
-  const int64_t threads = items * n_slices * kWarp;
+  const int warps = kFastBlock / kWarp;
+  int launched = 0;
   cudaMemsetAsync(n_deferred, 0, sizeof(unsigned long long), st);
+  const float* muf = nullptr;
+  if (n_slices > 1 && mu == nullptr) {
+    k_mu_f32<<<grid_for((bv.nnz + 31) / 32 * 32, 256), 256, 0, st>>>(bv, tb32, phi32, K, mu_f);
+    muf = mu_f;
+    ++launched;
+  }
   auto* rec = static_cast<Deferred*>(deferred);
+  const dim3 grid(static_cast<unsigned>((items + warps - 1) / warps), static_cast<unsigned>(n_slices));
   if (K % (kWarp * KPL) == 0)
-    k_sample_fast<KPL, true><<<grid_for(threads, kFastBlock), kFastBlock, 0, st>>>(
-        bv, tb32, phi32, mu, K, m_t, seed, t, sweep, chunk, n_slices, tc, pc, rec, n_deferred);
+    k_sample_fast<KPL, true><<<grid, kFastBlock, 0, st>>>(
+        bv, tb32, phi32, mu, muf, K, m_t, seed, t, sweep, chunk, n_slices, tc, pc, rec, n_deferred);
   else
-    k_sample_fast<KPL, false><<<grid_for(threads, kFastBlock), kFastBlock, 0, st>>>(
-        bv, tb32, phi32, mu, K, m_t, seed, t, sweep, chunk, n_slices, tc, pc, rec, n_deferred);
+    k_sample_fast<KPL, false><<<grid, kFastBlock, 0, st>>>(
+        bv, tb32, phi32, mu, muf, K, m_t, seed, t, sweep, chunk, n_slices, tc, pc, rec, n_deferred);
   launch_deferred(bv, tb64, phi64, mu, K, m_t, seed, t, sweep, rec, n_deferred, aux,
                   bv.nnz * ((K + 255) / 256), draw_cap, tc, pc, err, st);
-  return 3;
+  return launched + 3;
 }
 
 int launch_fast_nz(const BatchView& bv, const double* tb64, const float* tb32, const double* phi64,
@@ -1622,28 +1670,27 @@ int launch_sample_fast(const BatchView& bv, const double* theta_b64, const float
                        const double* phi64, const float* phi32, const double* mu, int K,
                        double m_t, uint64_t seed, uint32_t t, uint32_t sweep,
                        unsigned long long* tc, unsigned long long* pc, void* deferred,
-                       unsigned long long* n_deferred, void* aux, int64_t draw_cap, int* err,
-                       cudaStream_t st) {
+                       unsigned long long* n_deferred, void* aux, int64_t draw_cap, float* mu_f,
+                       int* err, cudaStream_t st) {
   if (bv.nnz == 0) return 0;
   // production: lane = topic, 8 topics per lane (k_sample_fast).  The two
   // alternative layouts stay selectable for profiling (SAMELDA_SAMPLER=c|n);
   // both are bit-identical and measured slower on B200.
   const char* variant = getenv("SAMELDA_SAMPLER");
   const char v = variant ? variant[0] : 'f';
-  // K > 256: a lane=topic warp would only see a slice of mu; lane=nonzero
-  // handles any K with the full mu
-  if (v == 'f' && K <= 256) {
+  // K > 256: topic slices of 256 with the full mu from a k_mu_f32 pre-pass
+  if (v == 'f') {
     if (K <= 32)
       return launch_fast_kpl<1>(bv, theta_b64, theta_b32, phi64, phi32, mu, K, m_t, seed, t, sweep, tc, pc,
-                                deferred, n_deferred, aux, draw_cap, err, st);
+                                deferred, n_deferred, aux, draw_cap, mu_f, err, st);
     if (K <= 64)
       return launch_fast_kpl<2>(bv, theta_b64, theta_b32, phi64, phi32, mu, K, m_t, seed, t, sweep, tc, pc,
-                                deferred, n_deferred, aux, draw_cap, err, st);
+                                deferred, n_deferred, aux, draw_cap, mu_f, err, st);
     if (K <= 128)
       return launch_fast_kpl<4>(bv, theta_b64, theta_b32, phi64, phi32, mu, K, m_t, seed, t, sweep, tc, pc,
-                                deferred, n_deferred, aux, draw_cap, err, st);
+                                deferred, n_deferred, aux, draw_cap, mu_f, err, st);
     return launch_fast_kpl<8>(bv, theta_b64, theta_b32, phi64, phi32, mu, K, m_t, seed, t, sweep, tc, pc,
-                              deferred, n_deferred, aux, draw_cap, err, st);
+                              deferred, n_deferred, aux, draw_cap, mu_f, err, st);
   }
   if (v == 'c' && K <= 32 * kCtaMaxWarps) {
     const int nwarps = (K + 31) / 32;

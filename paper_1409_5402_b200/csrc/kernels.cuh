@@ -52,6 +52,7 @@ int launch_sample(const BatchView& bv, const double* theta_batch, const double* 
 
 // Same draws, bit for bit, through an f32 fast path with exact f64 fallback
 // (see kernels.cu).  mu == nullptr: the kernel forms mu itself (period path).
+// mu_f_scratch: nnz floats (used when K > 256).
 // `deferred` holds up to nnz * ceil(K / 256) records of
 // deferred_record_bytes() each; n_deferred is one u64 of scratch; `aux` holds
 // deferred_aux_bytes(records, draw_cap) (per-record mu + a flat list of up to
@@ -61,7 +62,7 @@ int launch_sample_fast(const BatchView& bv, const double* theta_b64, const float
                        double m_t, uint64_t seed, uint32_t t, uint32_t sweep,
                        unsigned long long* theta_counts, unsigned long long* phi_counts,
                        void* deferred, unsigned long long* n_deferred, void* aux,
-                       int64_t draw_cap, int* err, cudaStream_t st);
+                       int64_t draw_cap, float* mu_f_scratch, int* err, cudaStream_t st);
 int64_t deferred_record_bytes();
 int64_t deferred_aux_bytes(int64_t max_records, int64_t draw_cap);
 

@@ -401,3 +401,16 @@ def test_trainer_reports_device_error_asynchronously(port):
     with pytest.raises(S.NumericalError):
         tr.ctx.synchronize()
     tr.ctx.synchronize()  # reported once, then cleared
+
+
+@pytest.mark.parametrize("K", [300, 520])
+def test_train_sliced_k_bit_exact(port, K):
+    """K > 256 on the period path: topic slices with the k_mu_f32 pre-pass."""
+    g = port.make_corpus(50, 80, 5, 40.0, 17)
+    tr, te = port.split_holdout(g, 0.2, 4)
+    cfg = dict(n_topics=K, m=30.0, t_max=3, batch_fraction=0.5, seed=8)
+    model, trace = S.train(tr, S.SamplerConfig(**cfg), te, 3)
+    ophi, otheta, otrace = port.train(tr, TrainConfig(**cfg), te, 3)
+    np.testing.assert_array_equal(model.phi, ophi)
+    np.testing.assert_array_equal(model.theta, otheta)
+    np.testing.assert_allclose([r["ll"] for r in trace], [r["ll"] for r in otrace], rtol=1e-12)
