@@ -391,8 +391,13 @@ def run_ours(args, cfg):
 
     # ---- roofline of the dominant kernel (sampling), algorithmic bytes
     K = cfg["n_topics"]
-    per_nnz = 8 + 8 + 8 * K + 8 * K        # (word,count) + mu + phi column f64 + u64 count row
-    per_doc = 8 + 8 * K + 8 * K            # batch entry + theta row f64 + u64 theta counts
+    # SURVEY.md 8(d) per-unit figure at parity-mode element sizes (phi f64
+    # "use 8 in place of 4", int32 counts): per batch nonzero 8 (word id +
+    # count) + 8K (phi column) + 4K (phi-count column); per batch doc
+    # 8 + 8K (theta row) + 4K (theta counts).  This build moves the same
+    # 12K + 8 per nonzero (phi32 4K + u64 counts 8K).
+    per_nnz = 8 + 12 * K
+    per_doc = 8 + 12 * K
     alg_bytes = prof["nnz"] * per_nnz + prof["docs"] * per_doc
     sample_ms = prof["sample_ms"]
     peaks, peaks_kind = load_peaks()
