@@ -209,28 +209,38 @@ __global__ void __launch_bounds__(kSampleBlock) k_sample(
 // Same draws as k_sample, bit for bit, at a fraction of the cost.  A draw's
 // outcome z is the first k with u <= cdf_k, where u is the stream's first
 // uniform and cdf_k the reference's f64 inversion recurrence (rng.cpp:39-52).
-// The fast path evaluates rate, exp and the recurrence in f32 with a
-// rigorous relative error bound r(lambda, k) and decides each comparison only
-// when u lies outside [cdf - m, cdf + m]; otherwise (probability ~1e-5 per
-// draw), or for lambda >= 9.5 (PTRS territory), non-finite / negative /
-// denormal inputs, or k > 40, the lane recomputes that draw exactly like
-// k_sample: sequential f64 mu, __ddiv_rn rate, full Philox block, exact
-// inversion or PTRS.  Error budget (u32 = 2^-24 unit roundoff):
+// The fast path evaluates rate, exp and the recurrence in f32 and decides a
+// comparison only when u lies outside [cdf_k - m_k, cdf_k + m_k], m_k a
+// rigorous bound on |cdf_f32 - cdf_ref| (below); otherwise (~3e-5 per draw),
+// for lambda near or above 10 (PTRS), non-finite / tiny inputs, or k > 40,
+// the draw is deferred to the exact path (k_deferred_*): sequential f64 mu,
+// __ddiv_rn rate, full Philox block, exact inversion or PTRS.
+// Error bound (u = 2^-24):
 //   lambda_f: theta, phi rounded to f32 (2u), product (u), mu by tree sum of
-//     positive terms (<= 16u), cs/mu (3u), lambda (u)  -> |dl| <= 1.5e-6 lambda
-//   exp:  ex2.approx of -lambda*log2(e): 2^-22 rel + lambda * 2u from the
-//         argument rounding                           -> <= (2.4e-7 + 1.2e-7 lambda)
-//   step k: pmf *= lambda * rcp.approx(k) (+ dl + 4u), cdf += pmf (+u)
-//   r = 4e-6 + 4e-6 lambda + 6e-6 k  (>= 2x the sum above);  u from the top
-//   23 bits of the high word: u - u_f in [0, 2^-23) -> m = cdf * r + 2.5e-7.
+//     positive terms (<= 12u), m*c (u), __fdividef (4u), lambda (u)
+//     -> |lambda_f - lambda| <= dl = 24u lambda = 1.43e-6 lambda
+//   |cdf_f32(k; lambda_f) - cdf_ref(k; lambda)| <=
+//       |cdf_f32(k; lambda_f) - F_k(lambda_f)|       f32 evaluation
+//     + |F_k(lambda_f) - F_k(lambda)|                 <= dl pmf_k (dF_k/dl = -pmf_k)
+//     + |F_k(lambda) - cdf_ref(k; lambda)|            f64, < 1e-14
+//   f32 evaluation: e0 = ex2.approx(-lambda log2 e): 2^-22 + 1.5u lambda
+//     = eps0 <= 2.4e-7 + 1.2e-7 lambda; pmf_i carries eps0 + 4u i (rcp.approx
+//     1 ulp + 2 roundings per step); each cdf add one rounding
+//     -> <= cdf_k (eps0 + 5u k) = cdf_k (2.4e-7 + 1.2e-7 lambda + 3e-7 k)
+//   m_k = 2 x the sum = cdf_k (4.8e-7 + 2.4e-7 lambda + 6e-7 k)
+//         + 3e-6 lambda pmf_k + 2.5e-7
+//   (2.5e-7 >= 2x the u quantisation: u is taken from the top 23 bits of the
+//   high word, true u in [u_f, u_f + 2^-23)).
 // The mu used is the caller's mu array when given (per-call sample_counts),
-// else the warp computes it (f32 tree for the fast path, exact f64
-// sequential sum on fallback, cached per lane and nonzero).
+// else the warp computes it (f32 tree).
 
 constexpr int kFastBlock = 256;
+// inversion below 10 (rng.cpp:139-150): decided only when lambda_f's whole
+// error interval (1.5e-6 relative, 2x) lies below 10; PTRS draws defer
+constexpr float kInvMax = 9.99997f;
 
 // MUFU-only transcendentals (no denormal range fix-ups: arguments here are
-// in [-13.7, 0] and [1, 40]); their error is inside the fast-path budget.
+// in [-14.5, 0] and [1, 40]); their error is inside the fast-path budget.
 __device__ __forceinline__ float ex2_approx(float x) {
   float y;
   asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
@@ -242,7 +252,7 @@ __device__ __forceinline__ float rcp_approx(float x) {
   return y;
 }
 
-// Fast-path Poisson decision (see the error budget above).  Returns z, or
+// Fast-path Poisson decision (see the error bound above).  Returns z, or
 // sets *undecided when u falls inside a threshold's uncertainty band or the
 // search passes z = 40.  The first three thresholds (z in {0, 1, 2}, ~99% of
 // draws at lambda ~ 0.4) are evaluated branch-free; only u beyond cdf_2
@@ -256,35 +266,51 @@ __device__ __forceinline__ uint32_t fast_poisson(float lam, uint32_t y, bool* un
   const float c1 = __fadd_rn(e0, t1);
   const float t2 = __fmul_rn(__fmul_rn(t1, lam), 0.5f);
   const float c2 = __fadd_rn(c1, t2);
-  // relative bound r_k = 4e-6 + 4e-6 lambda + 6e-6 k, absolute 2.5e-7 for u:
-  // u is decided against cdf_k unless |u - cdf_k| <= m_k = cdf_k r_k + 2.5e-7
-  const float r0 = __fmaf_rn(4e-6f, lam, 4e-6f);
-  const float m0 = __fmaf_rn(e0, r0, 2.5e-7f);
-  const float m1 = __fmaf_rn(c1, __fadd_rn(r0, 6e-6f), 2.5e-7f);
-  const float m2 = __fmaf_rn(c2, __fadd_rn(r0, 1.2e-5f), 2.5e-7f);
+  // m_k = cdf_k (r0 + 6e-7 k) + pl pmf_k + 2.5e-7
+  const float r0 = __fmaf_rn(2.4e-7f, lam, 4.8e-7f);
+  const float pl = __fmul_rn(3e-6f, lam);
+  const float m0 = __fmaf_rn(e0, __fadd_rn(r0, pl), 2.5e-7f);
+  const float m1 = __fmaf_rn(c1, __fadd_rn(r0, 6e-7f), __fmaf_rn(t1, pl, 2.5e-7f));
+  const float m2 = __fmaf_rn(c2, __fadd_rn(r0, 1.2e-6f), __fmaf_rn(t2, pl, 2.5e-7f));
   const float d0 = __fsub_rn(u, e0), d1 = __fsub_rn(u, c1), d2 = __fsub_rn(u, c2);
   *undecided = *undecided || (fabsf(d0) <= m0) || (fabsf(d1) <= m1) || (fabsf(d2) <= m2);
   uint32_t z = (d0 > m0) + (d1 > m1) + (d2 > m2);
   if (z < 3 || *undecided) return z;
-  const float a0 = __fsub_rn(1.0f, r0), b0 = __fadd_rn(1.0f, r0);
   // sequential search from k = 3 (u beyond cdf_2)
   float pmf = t2, cdf = c2, zf = 2.0f;
-  float rlo = __fsub_rn(a0, 1.2e-5f), rhi = __fadd_rn(b0, 1.2e-5f);
+  float rk = __fadd_rn(r0, 1.2e-6f);
   z = 2;
   for (;;) {
     ++z;
     zf = __fadd_rn(zf, 1.0f);
     pmf = __fmul_rn(pmf, __fmul_rn(lam, rcp_approx(zf)));
     cdf = __fadd_rn(cdf, pmf);
-    rlo = __fsub_rn(rlo, 6e-6f);
-    rhi = __fadd_rn(rhi, 6e-6f);
-    if (u <= __fmaf_rn(cdf, rlo, -2.5e-7f)) return z;
-    if (!(u > __fmaf_rn(cdf, rhi, 2.5e-7f)) || z >= 40) {
+    rk = __fadd_rn(rk, 6e-7f);
+    const float mk = __fmaf_rn(cdf, rk, __fmaf_rn(pmf, pl, 2.5e-7f));
+    const float dk = __fsub_rn(u, cdf);
+    if (dk < -mk) return z;
+    if (!(dk > mk) || z >= 40) {
       *undecided = true;
       return 0;
     }
   }
 }
+
+#ifdef SAMELDA_DEFER_STATS
+// Diagnostics build only (tools/defer_stats.sh): why draws defer.
+//   [0] nz_exact  [1] tiny product  [2] lambda >= kInvMax  [3] band / search
+//   [8 + b]  deferred draws by lambda bin b = floor(log2 lambda) + 20
+//   [48 + b] all draws with lambda >= 2^-4, by the same bins
+__device__ unsigned long long g_defer_stats[96];
+__device__ __forceinline__ void defer_stats(bool nz_exact, float prod, float lam, bool undecided) {
+  const int bin = lam > 0.0f ? max(0, min(39, static_cast<int>(floorf(log2f(lam))) + 20)) : 0;
+  if (lam >= 0.0625f) atomicAdd(&g_defer_stats[48 + bin], 1ull);
+  if (!undecided) return;
+  const int cat = nz_exact ? 0 : !(prod >= 1e-30f) ? 1 : !(lam < kInvMax) ? 2 : 3;
+  atomicAdd(&g_defer_stats[cat], 1ull);
+  atomicAdd(&g_defer_stats[8 + bin], 1ull);
+}
+#endif
 
 struct Philox1 {
   // round-1 specialisation for counter {0, w, d, t}: M0 * 0 = 0, so the
@@ -320,7 +346,7 @@ __device__ __forceinline__ uint32_t philox_y(const Philox1 r1, uint32_t k0, uint
 }
 
 // Deferred exact draws: one record per (nonzero, topic slice) that has at
-// least one draw the fast path could not decide (PTRS range lambda >= 9.5,
+// least one draw the fast path could not decide (a PTRS decision inside its band,
 // an ambiguous comparison, z > 40, or non-finite / tiny inputs).
 struct Deferred {
   int64_t p;          // batch nonzero index
@@ -418,11 +444,13 @@ __global__ void __launch_bounds__(kNzWarps * 32) k_sample_nz(
       const int32_t wr = __shfl_sync(0xffffffffu, w, r);
       const float* tr = theta_b32 + br * K;
       const float* pr = phi32 + static_cast<int64_t>(wr) * K;
-      float part = 0.0f;
-      for (int k = lane; k < K; k += 32) part = __fadd_rn(part, __fmul_rn(__ldg(tr + k), __ldg(pr + k)));
+      // f64 sum of exact f32 x f32 products (error budget: any K)
+      double part = 0.0;
+      for (int k = lane; k < K; k += 32)
+        part = __dadd_rn(part, static_cast<double>(__ldg(tr + k)) * static_cast<double>(__ldg(pr + k)));
 #pragma unroll
-      for (int o = 16; o > 0; o >>= 1) part = __fadd_rn(part, __shfl_xor_sync(0xffffffffu, part, o));
-      if (lane == r) my_mu = part;
+      for (int o = 16; o > 0; o >>= 1) part = __dadd_rn(part, __shfl_xor_sync(0xffffffffu, part, o));
+      if (lane == r) my_mu = __double2float_rn(part);
     }
   }
   // lane flags: 0 fast, 1 all draws exact (mu unusable), 2 no draws (padding)
@@ -459,7 +487,7 @@ __global__ void __launch_bounds__(kNzWarps * 32) k_sample_nz(
         const float prod = __fmul_rn(__ldg(theta_b32 + br * K + k_lane),
                                      __ldg(phi32 + static_cast<int64_t>(wr) * K + k_lane));
         const float lam = __fmul_rn(prod, sr);
-        v = (mr == 0 && prod >= 1e-30f && lam < 9.5f) ? lam : -1.0f;
+        v = (mr == 0 && prod >= 1e-30f && lam < kInvMax) ? lam : -1.0f;
       }
       lt[r * 32 + (lane ^ r)] = v;
     }
@@ -627,9 +655,9 @@ __global__ void __launch_bounds__(MAXW * 32) k_sample_cta(
       const float part = transpose_reduce<32>(tmp, lane);
       s_part[wv][lane] = part;
       __syncthreads();
-      float mu = 0.0f;
-      for (int v = 0; v < nwarps; ++v) mu = __fadd_rn(mu, s_part[v][lane]);
-      mu_lane = mu;
+      double mu = 0.0;  // f64 across warps: <= 5u + u for any K (error budget)
+      for (int v = 0; v < nwarps; ++v) mu = __dadd_rn(mu, static_cast<double>(s_part[v][lane]));
+      mu_lane = __double2float_rn(mu);
     }
     const bool lane_exact = !(mu_lane >= 1e-20f) || isinf(mu_lane);
     const float scale = __fdividef(__double2float_rn(__dmul_rn(m_t, static_cast<double>(c))), mu_lane);
@@ -652,7 +680,7 @@ __global__ void __launch_bounds__(MAXW * 32) k_sample_cta(
       }
       const float lam = __fmul_rn(prod[i], sc);
       const uint32_t y = philox_y_sched(r1, ks);
-      bool exact = k_ok && (ex_i || !(prod[i] >= 1e-30f) || !(lam < 9.5f));
+      bool exact = k_ok && (ex_i || !(prod[i] >= 1e-30f) || !(lam < kInvMax));
       uint32_t z = 0;
       if (k_ok && !exact) {
         bool undecided = false;
@@ -727,11 +755,14 @@ __global__ void __launch_bounds__(256) k_mu_f32(BatchView bv, const float* __res
     const int32_t wi = __shfl_sync(0xffffffffu, w, i);
     const float* tr = theta_b32 + bi * K;
     const float* pr = phi32 + static_cast<int64_t>(wi) * K;
-    float part = 0.0f;
-    for (int k = lane; k < K; k += 32) part = __fadd_rn(part, __fmul_rn(__ldg(tr + k), __ldg(pr + k)));
+    // f64 accumulation of the exact f32 x f32 products: mu_f is then within
+    // ~1 ulp of the f32-input dot for any K (the fast-path budget assumes 16u)
+    double part = 0.0;
+    for (int k = lane; k < K; k += 32)
+      part = __dadd_rn(part, static_cast<double>(__ldg(tr + k)) * static_cast<double>(__ldg(pr + k)));
 #pragma unroll
-    for (int o = 16; o > 0; o >>= 1) part = __fadd_rn(part, __shfl_xor_sync(0xffffffffu, part, o));
-    if (lane == i) mine = part;
+    for (int o = 16; o > 0; o >>= 1) part = __dadd_rn(part, __shfl_xor_sync(0xffffffffu, part, o));
+    if (lane == i) mine = __double2float_rn(part);
   }
   if (lane < n_here) mu_f[g0 + lane] = mine;
 }
@@ -874,16 +905,23 @@ __global__ void __launch_bounds__(kFastBlock, SAMELDA_FAST_MINB) k_sample_fast(
 #pragma unroll
       for (int j = 0; j < KPL; ++j) asm volatile("" : "+r"(y[j]));
       // phase 2: decisions; undecidable draws are deferred.  Ineligible draws
-      // (lambda >= 9.5: PTRS; tiny / non-finite products; unusable mu) enter
-      // undecided, which fast_poisson keeps and which skips its search loop.
+      // (lambda near or above 10: PTRS; tiny / non-finite products; unusable
+      // mu) enter undecided, which fast_poisson keeps and which skips
+      // its search loop.
       uint32_t defer_bits = 0;
 #pragma unroll
       for (int j = 0; j < KPL; ++j) {
         const int k = kbase + lane + kWarp * j;
         const float lam = __fmul_rn(prod[j], scale);
-        bool undecided = nz_exact || !(prod[j] >= 1e-30f) || !(lam < 9.5f);
+        const bool lam_ok = !nz_exact && (prod[j] >= 1e-30f);
+        bool undecided = !lam_ok || !(lam < kInvMax);
         uint32_t z = fast_poisson(lam, y[j], &undecided);
-        if (!FULL && k >= K) undecided = false, z = 0;
+        if (!FULL && k >= K) {
+          undecided = false, z = 0;
+        }
+#ifdef SAMELDA_DEFER_STATS
+        if (FULL || k < K) defer_stats(nz_exact, prod[j], lam, undecided);
+#endif
         if (undecided) {
           defer_bits |= 1u << j;
           z = 0;
@@ -1834,3 +1872,14 @@ int launch_ordered_ll(const double* doc_logp, const int64_t* doc_scored, int64_t
 }
 
 }  // namespace scu
+
+#ifdef SAMELDA_DEFER_STATS
+extern "C" int samelda_debug_defer_stats(unsigned long long* out, int reset) {
+  if (cudaMemcpyFromSymbol(out, scu::g_defer_stats, sizeof(scu::g_defer_stats)) != cudaSuccess) return 4;
+  if (reset) {
+    static const unsigned long long zero[96] = {};
+    cudaMemcpyToSymbol(scu::g_defer_stats, zero, sizeof(zero));
+  }
+  return 0;
+}
+#endif
