@@ -15,6 +15,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <functional>
 #include <string>
 #include <vector>
 
@@ -443,6 +444,40 @@ struct samelda_cu_ctx {
     return out;
   }
 
+  // flat deferred-draw list: 32 per possible record, at most 64 Mi entries
+  static int64_t draw_cap_for(int64_t records) {
+    if (const char* cap = std::getenv("SAMELDA_DRAW_CAP")) return std::atoll(cap);  // tests
+    return std::min<int64_t>(records * 32, int64_t{1} << 26);
+  }
+
+  // Size every per-batch device buffer (and both pinned staging buffers) for
+  // batches of up to B_ documents and nnz_ nonzeros, so that no period has to
+  // grow one: a grow is a cudaFree (device-wide sync) plus a fresh allocation
+  // of up to ~1 GB for the deferred queues, milliseconds inside a period.
+  void reserve_batches(int64_t B_, int64_t nnz_, int K_, int64_t W_, int mode) {
+    ensure<int32_t>(batch, B_);
+    ensure<int64_t>(prefix, B_ + 1);
+    ensure<double>(theta_batch, B_ * K_);
+    ensure<float>(theta_batch32, B_ * K_);
+    ensure<double>(theta_rows, B_ * K_);
+    ensure<double>(cand, W_ * K_);
+    ensure<double>(totals, K_);
+    if (mode == SAMELDA_CU_MODE_EXPECTED) {
+      ensure<double>(mu, nnz_);
+      ensure<double>(tf, B_ * K_);
+      ensure<double>(pf, W_ * K_);
+    } else {
+      ensure<unsigned long long>(tc, B_ * K_);
+      ensure<unsigned long long>(pc, W_ * K_);
+      const int64_t records = nnz_ * ((K_ + 255) / 256);
+      ensure<unsigned char>(deferred, records * scu::deferred_record_bytes());
+      ensure<unsigned char>(deferred_aux, scu::deferred_aux_bytes(records, draw_cap_for(records)));
+      ensure<unsigned long long>(n_deferred, 1);
+      if (K_ > 256) ensure<float>(mu_f32, nnz_);
+    }
+    for (int i = 0; i < 2; ++i) stage(B_);
+  }
+
   // one sweep's sampling into tc/pc (or tf/pf): zeroes the count buffers first
   // mu_d: the caller's mu (per-call API) or nullptr (the kernel forms mu)
   void sample_sweep(const scu::BatchView& bv, const double* theta_b, const float* theta_b32,
@@ -469,9 +504,7 @@ struct samelda_cu_ctx {
       ck(cudaMemsetAsync(pc_, 0, sizeof(unsigned long long) * std::max<int64_t>(W_ * K_, 1), stream), "zero pc");
       tick(kSample, true);
       const int64_t records = bv.nnz * ((K_ + 255) / 256);
-      // flat deferred-draw list: 32 per possible record, at most 64 Mi entries
-      int64_t draw_cap = std::min<int64_t>(records * 32, int64_t{1} << 26);
-      if (const char* cap = std::getenv("SAMELDA_DRAW_CAP")) draw_cap = std::atoll(cap);  // tests
+      const int64_t draw_cap = draw_cap_for(records);
       void* rec = ensure<unsigned char>(deferred, records * scu::deferred_record_bytes());
       void* aux = ensure<unsigned char>(deferred_aux, scu::deferred_aux_bytes(records, draw_cap));
       launches += scu::launch_sample_fast(bv, theta_b, theta_b32, phi_wk, phi_wk32, mu_d, K_,
@@ -909,6 +942,20 @@ int samelda_cu_train_begin(samelda_cu_ctx* ctx, const samelda_cu_corpus* corpus,
     ctx->launches += scu::launch_phi_init(ph, ctx->W, ctx->K, config->t_max > 0 ? config->init_noise : 0.0,
                                           config->seed, ensure<double>(ctx->totals, K), ctx->stream);
     ctx->launches += scu::launch_to_f32(ph, ctx->W * K, ensure<float>(ctx->phi32, ctx->W * K), ctx->stream);
+    // per-batch buffers for the largest batch the minibatch stream can draw:
+    // its size (samelda_cu_batches_create) times the longest documents
+    {
+      const int64_t bsz = std::min<int64_t>(
+          ctx->D, std::max<int64_t>(1, static_cast<int64_t>(std::llround(
+                                             config->batch_fraction * static_cast<double>(ctx->D)))));
+      std::vector<int64_t> len(static_cast<size_t>(ctx->D));
+      for (int64_t d = 0; d < ctx->D; ++d)
+        len[static_cast<size_t>(d)] = corpus->doc_offsets[d + 1] - corpus->doc_offsets[d];
+      std::nth_element(len.begin(), len.begin() + (bsz - 1), len.end(), std::greater<int64_t>());
+      int64_t nnz_max = 0;
+      for (int64_t i = 0; i < bsz; ++i) nnz_max += len[static_cast<size_t>(i)];
+      ctx->reserve_batches(bsz, nnz_max, ctx->K, ctx->W, config->mode);
+    }
     ck(cudaStreamSynchronize(ctx->stream), "train_begin");
     ck(cudaGetLastError(), "train_begin");
     ctx->model_ready = true;
