@@ -1010,6 +1010,18 @@ __device__ __forceinline__ void deferred_one(const BatchView& bv, const Deferred
   }
 }
 
+// Block tile = 32 records.  Product phase: the 8 warps load the records'
+// theta / phi row segments coalesced (lanes over topics, kExpKC topics per
+// chunk) and write the exact products to a shared [32][kExpKC + 1] tile.
+// Sum phase: warp 0, lane = record, extends each record's sequential f64 sum
+// over the chunk in the reference's k order (sampler.cpp:111-119) -- 32
+// independent chains, one DADD per topic per 32 records.  Then one atomic
+// reserves the tile's draw-list slots and warp v writes the entries of
+// records v, v + 8, ... (lane = topic bit, positions from popc prefixes).
+constexpr int kExpKC = 256;
+constexpr int kExpStride = kExpKC + 1;  // 2-way (optimal) f64 bank pattern
+constexpr size_t kExpSmem = sizeof(double) * 32 * kExpStride;
+
 __global__ void __launch_bounds__(256) k_deferred_expand(
     BatchView bv, const double* __restrict__ theta_b64, const double* __restrict__ phi64,
     const double* __restrict__ mu_in, int K, double m_t, uint64_t seed, uint32_t t,
@@ -1018,50 +1030,88 @@ __global__ void __launch_bounds__(256) k_deferred_expand(
     DeferredDraw* __restrict__ draws, unsigned long long* __restrict__ n_draws,
     unsigned long long draw_cap, unsigned long long* __restrict__ theta_counts,
     unsigned long long* __restrict__ phi_counts, int* __restrict__ err) {
+  extern __shared__ double s_prod[];  // [32][kExpStride]
+  __shared__ double s_mu[32];
+  __shared__ unsigned long long s_pre[33];
+  const int lane = threadIdx.x & 31;
+  const int wib = threadIdx.x >> 5;
+  const int nw = blockDim.x >> 5;
   const int64_t n = static_cast<int64_t>(*n_deferred);
-  for (int64_t r = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; r < n;
-       r += static_cast<int64_t>(gridDim.x) * blockDim.x) {
-    const Deferred& me = deferred[r];
-    double mu = 0.0;
+  for (int64_t tile = blockIdx.x; tile * 32 < n; tile += gridDim.x) {
+    const int64_t r0 = tile * 32;
+    const int nh = static_cast<int>(min(static_cast<int64_t>(32), n - r0));
     if (mu_in) {
-      mu = mu_in[me.p];
+      if (threadIdx.x < nh) s_mu[threadIdx.x] = mu_in[deferred[r0 + threadIdx.x].p];
     } else {
-      const double* th = theta_b64 + static_cast<int64_t>(me.b) * K;
-      const double* ph = phi64 + static_cast<int64_t>(me.w) * K;
-      if ((K & 1) == 0) {
-        const double2* t2 = reinterpret_cast<const double2*>(th);
-        const double2* p2 = reinterpret_cast<const double2*>(ph);
-        for (int k2 = 0; k2 < (K >> 1); ++k2) {
-          const double2 a = __ldg(t2 + k2), c = __ldg(p2 + k2);
-          mu = __dadd_rn(mu, __dmul_rn(a.x, c.x));
-          mu = __dadd_rn(mu, __dmul_rn(a.y, c.y));
+      double mu = 0.0;  // warp 0: lane = record
+      for (int kc = 0; kc < K; kc += kExpKC) {
+        const int kn = min(kExpKC, K - kc);
+        for (int i = wib; i < nh; i += nw) {
+          const int32_t b = deferred[r0 + i].b, w = deferred[r0 + i].w;
+          const double* th = theta_b64 + static_cast<int64_t>(b) * K + kc;
+          const double* ph = phi64 + static_cast<int64_t>(w) * K + kc;
+          double* row = s_prod + i * kExpStride;
+#pragma unroll
+          for (int j = 0; j < kExpKC / 32; ++j) {
+            const int k = lane + 32 * j;
+            if (k < kn) row[k] = __dmul_rn(__ldg(th + k), __ldg(ph + k));
+          }
         }
-      } else {
-        for (int k = 0; k < K; ++k) mu = __dadd_rn(mu, __dmul_rn(__ldg(th + k), __ldg(ph + k)));
+        __syncthreads();
+        if (wib == 0 && lane < nh) {
+          const double* row = s_prod + lane * kExpStride;
+#pragma unroll 8
+          for (int k = 0; k < kn; ++k) mu = __dadd_rn(mu, row[k]);
+        }
+        __syncthreads();
+      }
+      if (wib == 0 && lane < nh) s_mu[lane] = mu;
+    }
+    // one atomic reserves the tile's slots; every reserved slot below draw_cap
+    // is written (phase B reads exactly [0, min(n_draws, draw_cap))), the rest
+    // is drawn here
+    if (wib == 0) {
+      uint32_t cnt = 0;
+      if (lane < nh) {
+        const Deferred& me = deferred[r0 + lane];
+#pragma unroll
+        for (int j = 0; j < 8; ++j) cnt += __popc(me.mask[j]);
+      }
+      uint32_t inc = cnt;  // inclusive warp scan
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t v = __shfl_up_sync(0xffffffffu, inc, o);
+        if (lane >= o) inc += v;
+      }
+      unsigned long long b0 = 0;
+      if (lane == 31) b0 = atomicAdd(n_draws, static_cast<unsigned long long>(inc));
+      b0 = __shfl_sync(0xffffffffu, b0, 31);
+      s_pre[lane] = b0 + inc - cnt;
+    }
+    __syncthreads();
+    const uint32_t below = (1u << lane) - 1u;
+    for (int i = wib; i < nh; i += nw) {
+      const int64_t r = r0 + i;
+      const Deferred me = deferred[r];
+      const double mu = s_mu[i];
+      if (lane == 0) rec_mu[r] = mu;
+      unsigned long long base = s_pre[i];
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        const uint32_t m = me.mask[j];
+        if ((m >> lane) & 1u) {
+          const unsigned long long slot = base + __popc(m & below);
+          const int k = me.kbase + lane + 32 * j;
+          if (slot < draw_cap)
+            draws[slot] = DeferredDraw{static_cast<uint32_t>(r), static_cast<uint32_t>(k)};
+          else
+            deferred_one(bv, me, mu, k, theta_b64, phi64, K, m_t, seed, t, sweep, theta_counts,
+                         phi_counts, err);
+        }
+        base += __popc(m);
       }
     }
-    rec_mu[r] = mu;
-    uint32_t cnt = 0;
-#pragma unroll
-    for (int j = 0; j < 8; ++j) cnt += __popc(me.mask[j]);
-    // reserve cnt list slots; every reserved slot below draw_cap is written
-    // (phase B reads exactly [0, min(n_draws, draw_cap))), the rest is drawn here
-    unsigned long long slot = atomicAdd(n_draws, static_cast<unsigned long long>(cnt));
-#pragma unroll
-    for (int j = 0; j < 8; ++j) {
-      uint32_t m = me.mask[j];
-      while (m) {
-        const int bit = __ffs(m) - 1;
-        m &= m - 1;
-        const int k = me.kbase + bit + 32 * j;
-        if (slot < draw_cap)
-          draws[slot] = DeferredDraw{static_cast<uint32_t>(r), static_cast<uint32_t>(k)};
-        else
-          deferred_one(bv, me, mu, k, theta_b64, phi64, K, m_t, seed, t, sweep, theta_counts,
-                       phi_counts, err);
-        ++slot;
-      }
-    }
+    __syncthreads();  // s_prod / s_mu / s_pre are rewritten by the next tile
   }
 }
 
@@ -1091,7 +1141,15 @@ void launch_deferred(const BatchView& bv, const double* tb64, const double* phi6
   auto* n_draws = reinterpret_cast<unsigned long long*>(rec_mu + max_records);
   auto* draws = reinterpret_cast<DeferredDraw*>(n_draws + 2);
   cudaMemsetAsync(n_draws, 0, sizeof(unsigned long long), st);
-  k_deferred_expand<<<148 * 4, 256, 0, st>>>(bv, tb64, phi64, mu, K, m_t, seed, t, sweep, rec,
+  static unsigned long long attr_set = 0;  // per device: dynamic smem opt-in
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (dev >= 64 || !((attr_set >> dev) & 1ull)) {
+    cudaFuncSetAttribute(k_deferred_expand, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         static_cast<int>(kExpSmem));
+    if (dev < 64) attr_set |= 1ull << dev;
+  }
+  k_deferred_expand<<<148 * 3, 256, kExpSmem, st>>>(bv, tb64, phi64, mu, K, m_t, seed, t, sweep, rec,
                                              n_deferred, rec_mu, draws, n_draws,
                                              static_cast<unsigned long long>(draw_cap), tc, pc, err);
   k_deferred_draw<<<148 * 16, 256, 0, st>>>(bv, tb64, phi64, K, m_t, seed, t, sweep, rec, rec_mu,
