@@ -229,6 +229,8 @@ __global__ void __launch_bounds__(kSampleBlock) k_sample(
 //     -> <= cdf_k (eps0 + 5u k) = cdf_k (2.4e-7 + 1.2e-7 lambda + 3e-7 k)
 //   m_k = 2 x the sum = cdf_k (4.8e-7 + 2.4e-7 lambda + 6e-7 k)
 //         + 3e-6 lambda pmf_k + 2.5e-7
+//   (k <= 2 share the upper bound M = 2e-6 + 3.3e-6 lambda >= m_0, m_1, m_2:
+//   one FFMA instead of ten instructions, at ~1.3x the deferral rate)
 //   (2.5e-7 >= 2x the u quantisation: u is taken from the top 23 bits of the
 //   high word, true u in [u_f, u_f + 2^-23)).
 // The mu used is the caller's mu array when given (per-call sample_counts),
@@ -266,17 +268,17 @@ __device__ __forceinline__ uint32_t fast_poisson(float lam, uint32_t y, bool* un
   const float c1 = __fadd_rn(e0, t1);
   const float t2 = __fmul_rn(__fmul_rn(t1, lam), 0.5f);
   const float c2 = __fadd_rn(c1, t2);
-  // m_k = cdf_k (r0 + 6e-7 k) + pl pmf_k + 2.5e-7
+  // one band for k = 0, 1, 2: with cdf_k, pmf_k <= 1 (+ rounding slack),
+  // m_k <= (r0 + 1.2e-6) + pl + 2.5e-7 = 1.93e-6 + 3.24e-6 lambda <= M
+  const float M = __fmaf_rn(3.3e-6f, lam, 2e-6f);
+  const float d0 = __fsub_rn(u, e0), d1 = __fsub_rn(u, c1), d2 = __fsub_rn(u, c2);
+  *undecided = *undecided || (fabsf(d0) <= M) || (fabsf(d1) <= M) || (fabsf(d2) <= M);
+  uint32_t z = (d0 > M) + (d1 > M) + (d2 > M);
+  if (z < 3 || *undecided) return z;
+  // sequential search from k = 3 (u beyond cdf_2): m_k = cdf_k (r0 + 6e-7 k)
+  // + pl pmf_k + 2.5e-7
   const float r0 = __fmaf_rn(2.4e-7f, lam, 4.8e-7f);
   const float pl = __fmul_rn(3e-6f, lam);
-  const float m0 = __fmaf_rn(e0, __fadd_rn(r0, pl), 2.5e-7f);
-  const float m1 = __fmaf_rn(c1, __fadd_rn(r0, 6e-7f), __fmaf_rn(t1, pl, 2.5e-7f));
-  const float m2 = __fmaf_rn(c2, __fadd_rn(r0, 1.2e-6f), __fmaf_rn(t2, pl, 2.5e-7f));
-  const float d0 = __fsub_rn(u, e0), d1 = __fsub_rn(u, c1), d2 = __fsub_rn(u, c2);
-  *undecided = *undecided || (fabsf(d0) <= m0) || (fabsf(d1) <= m1) || (fabsf(d2) <= m2);
-  uint32_t z = (d0 > m0) + (d1 > m1) + (d2 > m2);
-  if (z < 3 || *undecided) return z;
-  // sequential search from k = 3 (u beyond cdf_2)
   float pmf = t2, cdf = c2, zf = 2.0f;
   float rk = __fadd_rn(r0, 1.2e-6f);
   z = 2;
@@ -311,6 +313,15 @@ __device__ __forceinline__ void defer_stats(bool nz_exact, float prod, float lam
   atomicAdd(&g_defer_stats[8 + bin], 1ull);
 }
 #endif
+
+// phi-count scatter without a divergent branch: one predicated RED
+__device__ __forceinline__ void red_add_nz(unsigned long long* addr, uint32_t z) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\tsetp.ne.u32 p, %1, 0;\n\t"
+      "@p red.relaxed.gpu.global.add.u64 [%0], %2;\n\t}"
+      :
+      : "l"(addr), "r"(z), "l"(static_cast<unsigned long long>(z)));
+}
 
 struct Philox1 {
   // round-1 specialisation for counter {0, w, d, t}: M0 * 0 = 0, so the
@@ -926,10 +937,8 @@ __global__ void __launch_bounds__(kFastBlock, SAMELDA_FAST_MINB) k_sample_fast(
           defer_bits |= 1u << j;
           z = 0;
         }
-        if (z != 0) {
-          acc[j] += z;
-          atomicAdd(phi_counts + static_cast<int64_t>(wi) * K + k, static_cast<unsigned long long>(z));
-        }
+        acc[j] += z;
+        red_add_nz(phi_counts + static_cast<int64_t>(wi) * K + k, z);
       }
       if (__any_sync(0xffffffffu, defer_bits != 0)) {
         uint32_t masks[8];
