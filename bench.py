@@ -283,7 +283,7 @@ def run_ours(args, cfg):
 
     scfg = S.SamplerConfig(n_topics=cfg["n_topics"], m=cfg["m"], schedule=cfg["schedule"],
                            batch_fraction=cfg["batch_fraction"], inner_sweeps=cfg["inner_sweeps"],
-                           t_max=args.warmup + args.steps + 10, seed=1, mode=S.MODE_PARITY)
+                           t_max=args.warmup + args.steps + 2 * max(1, min(args.steps, 10)), seed=1, mode=S.MODE_PARITY)
     trainer = S.Trainer(train, scfg, ctx=ctx)
     trainer.set_doc_base(doc_base)
     if rank == 0:
@@ -294,10 +294,13 @@ def run_ours(args, cfg):
                                   train.doc_tokens(), cfg["batch_fraction"], 1, cfg["m"],
                                   cfg["schedule"], scfg.t_max)
 
-    def period(t, with_result=False):
+    def period(t, result_buf=None):
         assert t == sharded.t
         st = sharded.period()
-        out = trainer.batch_theta(st.owned_docs) if with_result else None
+        # the step's result: batch theta rows, copied D2H into a page-locked
+        # host buffer on the trainer stream (no host wait; read back by the
+        # barrier that closes the timed region)
+        out = trainer.batch_theta_async(st.owned_docs, result_buf) if result_buf is not None else None
         return st.owned_tokens, st.m_t, st.owned_docs, out
 
     def barrier():
@@ -354,7 +357,7 @@ def run_ours(args, cfg):
     # ---- per-kernel CUDA-event timing on a separate profiled pass (the
     # profiler synchronises after each sampling launch, so it stays out of
     # the timed region above)
-    prof_steps = max(1, min(args.steps, 5))
+    prof_steps = max(1, min(args.steps, 10))
     trainer.profile(True)
     prof_dev0 = torch.cuda.Event(enable_timing=True)
     prof_dev1 = torch.cuda.Event(enable_timing=True)
@@ -371,13 +374,18 @@ def run_ours(args, cfg):
     # ---- end to end through the public API with host buffers: per step the
     # host batch ids go H2D inside Trainer.period and the batch theta rows
     # (the step's result) come back D2H
-    e2e_steps = max(1, min(args.steps, 5))
+    e2e_steps = max(1, min(args.steps, 10))
+    # a rank owns ~batch_fraction x D_local docs of each global batch (the
+    # call fails loudly if a buffer is ever too small)
+    bmax = int(1.25 * cfg["batch_fraction"] * D_local) + 64
+    bufs = [torch.empty(bmax * cfg["n_topics"], dtype=torch.float64, pin_memory=True).numpy()
+            for _ in range(e2e_steps)]
     barrier()
     h2d = d2h = 0
     samples_e2e = 0.0
     t0 = time.perf_counter()
-    for _ in range(e2e_steps):
-        tokens, m_t, nb, out = period(t, with_result=True)
+    for i in range(e2e_steps):
+        tokens, m_t, nb, out = period(t, result_buf=bufs[i])
         samples_e2e += cfg["inner_sweeps"] * tokens * m_t
         h2d += nb * 4 + (nb + 1) * 8
         d2h += out.nbytes + 4

@@ -1115,6 +1115,20 @@ int samelda_cu_batch_theta(samelda_cu_ctx* ctx, double* out, int64_t cap) {
   });
 }
 
+int samelda_cu_batch_theta_async(samelda_cu_ctx* ctx, double* out, int64_t cap) {
+  return guarded(ctx, [&] {
+    ctx->poll_err(false, "period");
+    if (!ctx->model_ready) fail(SAMELDA_CU_CONFIG, "no model");
+    const int64_t n = ctx->B * ctx->K;
+    if (cap < n) fail(SAMELDA_CU_CONFIG, "batch_theta: buffer too small");
+    double* rows = ensure<double>(ctx->theta_rows, n);
+    ctx->launches += scu::launch_gather_theta(ctx->theta.as<double>(), ctx->batch.as<int32_t>(), ctx->B, ctx->K,
+                                              rows, nullptr, ctx->stream);
+    if (n > 0)
+      ck(cudaMemcpyAsync(out, rows, sizeof(double) * n, cudaMemcpyDeviceToHost, ctx->stream), "download rows");
+  });
+}
+
 int samelda_cu_count_totals(samelda_cu_ctx* ctx, int64_t* theta_total, int64_t* phi_total) {
   return guarded(ctx, [&] {
     ctx->poll_err(true, "period");

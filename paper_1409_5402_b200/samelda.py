@@ -112,6 +112,7 @@ SIGNATURES = [
     ("samelda_cu_phi_counts_device", C.c_int, [_P, C.POINTER(C.c_void_p), C.POINTER(_I64),
                                                C.POINTER(_I32), C.POINTER(_I32)]),
     ("samelda_cu_batch_theta", C.c_int, [_P, _P, _I64]),
+    ("samelda_cu_batch_theta_async", C.c_int, [_P, _P, _I64]),
     ("samelda_cu_set_doc_base", C.c_int, [_P, _I64]),
     ("samelda_cu_profile", C.c_int, [_P, _I32]),
     ("samelda_cu_profile_read", C.c_int, [_P, _P, _P, C.POINTER(_I64), C.POINTER(_I64),
@@ -336,6 +337,7 @@ def _ids(doc_ids):
 def sddmm(theta_batch, phi, corpus, doc_ids, n_threads: int = 1, ctx: Context | None = None):
     """sampler.cpp:88-123 on the device; returns mu aligned with the batch nonzeros."""
     ctx = ctx or default_context()
+    ctx._train_token = None  # per-call use replaces a Trainer's device state
     corpus = Corpus.of(corpus)
     theta_batch = _f64(theta_batch)
     phi = _f64(phi)
@@ -359,6 +361,7 @@ def sample_counts(theta_batch, phi, mu, corpus, doc_ids, m_t, seed, t, sweep=0, 
                   ctx: Context | None = None) -> SampledCounts:
     """sampler.cpp:125-195 on the device (reference-identical Poisson replicas)."""
     ctx = ctx or default_context()
+    ctx._train_token = None  # per-call use replaces a Trainer's device state
     corpus = Corpus.of(corpus)
     theta_batch = _f64(theta_batch)
     phi = _f64(phi)
@@ -380,6 +383,7 @@ def sample_counts(theta_batch, phi, mu, corpus, doc_ids, m_t, seed, t, sweep=0, 
 def expected_counts(theta_batch, phi, mu, corpus, doc_ids, m_t, ctx: Context | None = None):
     """Deterministic factored path: (theta_expected B x K, phi_expected W x K), f64."""
     ctx = ctx or default_context()
+    ctx._train_token = None  # per-call use replaces a Trainer's device state
     corpus = Corpus.of(corpus)
     theta_batch = _f64(theta_batch)
     phi = _f64(phi)
@@ -401,6 +405,7 @@ def update_model(model: Model, counts, rho_t: float, ctx: Context | None = None,
                  expected: bool = False) -> None:
     """sampler.cpp:197-229 on the device; updates model.theta / model.phi in place."""
     ctx = ctx or default_context()
+    ctx._train_token = None  # per-call use replaces a Trainer's device state
     if counts.n_topics != model.n_topics or counts.n_words != model.n_words:
         raise ConfigError("update_model: counts are not shaped for this model")
     model.theta = _f64(model.theta)
@@ -443,6 +448,7 @@ def parse_schedule(name: str) -> str:
 def fold_in_theta(phi, words, counts, alpha, sweeps=50, ctx: Context | None = None):
     """eval.cpp:19-73 on the device."""
     ctx = ctx or default_context()
+    ctx._train_token = None  # per-call use replaces a Trainer's device state
     phi = _f64(phi)
     K, W = phi.shape
     w = np.ascontiguousarray(words, np.int32)
@@ -458,6 +464,7 @@ def fold_in_theta(phi, words, counts, alpha, sweeps=50, ctx: Context | None = No
 def perword_loglik(phi, test_corpus, alpha, seed, n_threads=1, ctx: Context | None = None):
     """eval.cpp:75-159 on the device: held-out per-word log-likelihood (nats)."""
     ctx = ctx or default_context()
+    ctx._train_token = None  # per-call use replaces a Trainer's device state
     phi = _f64(phi)
     K, W = phi.shape
     test = Corpus.of(test_corpus)
@@ -503,79 +510,109 @@ class Trainer:
     """Device-resident train() split at the period (sampler.cpp:269-353)."""
 
     def __init__(self, corpus, config: SamplerConfig, ctx: Context | None = None):
-        self.ctx = ctx or default_context()
+        # The training state (model, batch, counts) lives in the device
+        # context, so a Trainer gets a context of its own unless one is passed;
+        # a context re-initialised by another Trainer or train() makes this
+        # Trainer's calls raise instead of silently using the other's state.
+        self.ctx = ctx if ctx is not None else Context(0)
         self.corpus = Corpus.of(corpus)
         self.config = config
         self._cs = self.corpus._struct()
         self._cfg = config._struct()
+        self._token = object()
+        self.ctx._train_token = self._token
         self.ctx.check(self.ctx.lib.samelda_cu_train_begin(self.ctx.h, C.byref(self._cs),
                                                            C.byref(self._cfg)))
+
+    def _live(self) -> Context:
+        if getattr(self.ctx, "_train_token", None) is not self._token:
+            raise ConfigError("Trainer: its context was re-initialised by another Trainer or "
+                              "train(); use one Trainer per Context")
+        return self.ctx
 
     def set_heldout(self, heldout, seed: int | None = None):
         self.heldout = Corpus.of(heldout)
         self._hs = self.heldout._struct()
-        self.ctx.check(self.ctx.lib.samelda_cu_heldout(
-            self.ctx.h, C.byref(self._hs),
+        c = self._live()
+        c.check(c.lib.samelda_cu_heldout(
+            c.h, C.byref(self._hs),
             int(self.config.seed if seed is None else seed) & (2**64 - 1)))
 
     def period(self, doc_ids, t, m_t, rho_t):
         ids, B = _ids(doc_ids)
-        self.ctx.check(self.ctx.lib.samelda_cu_period(self.ctx.h, _ptr(ids), B, int(t),
-                                                      float(m_t), float(rho_t)))
+        c = self._live()
+        c.check(c.lib.samelda_cu_period(c.h, _ptr(ids), B, int(t), float(m_t), float(rho_t)))
 
     def period_sample(self, doc_ids, t, m_t):
         ids, B = _ids(doc_ids)
-        self.ctx.check(self.ctx.lib.samelda_cu_period_sample(self.ctx.h, _ptr(ids), B, int(t),
-                                                             float(m_t)))
+        c = self._live()
+        c.check(c.lib.samelda_cu_period_sample(c.h, _ptr(ids), B, int(t), float(m_t)))
 
     def period_update(self, rho_t):
-        self.ctx.check(self.ctx.lib.samelda_cu_period_update(self.ctx.h, float(rho_t)))
+        c = self._live()
+        c.check(c.lib.samelda_cu_period_update(c.h, float(rho_t)))
 
     def phi_counts_device(self):
         """(device pointer, n elements, element bytes, is_float) of the phi count buffer."""
         p, n, eb, fl = C.c_void_p(), C.c_int64(), C.c_int32(), C.c_int32()
-        self.ctx.check(self.ctx.lib.samelda_cu_phi_counts_device(
-            self.ctx.h, C.byref(p), C.byref(n), C.byref(eb), C.byref(fl)))
+        c = self._live()
+        c.check(c.lib.samelda_cu_phi_counts_device(
+            c.h, C.byref(p), C.byref(n), C.byref(eb), C.byref(fl)))
         return p.value, n.value, eb.value, bool(fl.value)
 
     def set_doc_base(self, base: int):
-        self.ctx.check(self.ctx.lib.samelda_cu_set_doc_base(self.ctx.h, int(base)))
+        c = self._live()
+        c.check(c.lib.samelda_cu_set_doc_base(c.h, int(base)))
 
     def profile(self, enable: bool = True):
-        self.ctx.check(self.ctx.lib.samelda_cu_profile(self.ctx.h, 1 if enable else 0))
+        c = self._live()
+        c.check(c.lib.samelda_cu_profile(c.h, 1 if enable else 0))
 
     def profile_read(self) -> dict:
         ms = np.zeros(3)
         n = np.zeros(3, np.int64)
         nnz, docs, dfr = C.c_int64(), C.c_int64(), C.c_int64()
-        self.ctx.check(self.ctx.lib.samelda_cu_profile_read(self.ctx.h, _ptr(ms), _ptr(n),
-                                                            C.byref(nnz), C.byref(docs),
-                                                            C.byref(dfr)))
+        c = self._live()
+        c.check(c.lib.samelda_cu_profile_read(c.h, _ptr(ms), _ptr(n), C.byref(nnz),
+                                              C.byref(docs), C.byref(dfr)))
         return dict(sample_ms=ms[0], sddmm_ms=ms[1], mstep_ms=ms[2], sample_launches=int(n[0]),
                     sddmm_launches=int(n[1]), mstep_launches=int(n[2]), nnz=nnz.value,
                     docs=docs.value, deferred=dfr.value)
 
     def count_totals(self):
         a, b = C.c_int64(), C.c_int64()
-        self.ctx.check(self.ctx.lib.samelda_cu_count_totals(self.ctx.h, C.byref(a), C.byref(b)))
+        c = self._live()
+        c.check(c.lib.samelda_cu_count_totals(c.h, C.byref(a), C.byref(b)))
         return a.value, b.value
 
     def batch_theta(self, B: int) -> np.ndarray:
         out = np.zeros(max(B * self.config.n_topics, 1))
-        self.ctx.check(self.ctx.lib.samelda_cu_batch_theta(self.ctx.h, _ptr(out), len(out)))
+        c = self._live()
+        c.check(c.lib.samelda_cu_batch_theta(c.h, _ptr(out), len(out)))
+        return out[:B * self.config.n_topics].reshape(B, self.config.n_topics)
+
+    def batch_theta_async(self, B: int, out: np.ndarray) -> np.ndarray:
+        """Enqueue the copy of the batch theta rows into `out` (float64,
+        >= B * K elements, page-locked to overlap later periods) without a
+        host wait; the rows are there after ctx.synchronize()."""
+        if out.dtype != np.float64 or not out.flags.c_contiguous:
+            raise ValueError("batch_theta_async: out must be a contiguous float64 array")
+        c = self._live()
+        c.check(c.lib.samelda_cu_batch_theta_async(c.h, _ptr(out), out.size))
         return out[:B * self.config.n_topics].reshape(B, self.config.n_topics)
 
     def evaluate(self) -> float:
         out = C.c_double()
-        self.ctx.check(self.ctx.lib.samelda_cu_evaluate(self.ctx.h, C.byref(out)))
+        c = self._live()
+        c.check(c.lib.samelda_cu_evaluate(c.h, C.byref(out)))
         return out.value
 
     def model(self, with_theta: bool = True) -> Model:
         K, W, D = self.config.n_topics, self.corpus.n_words, self.corpus.n_docs
         phi = np.zeros(K * W)
         theta = np.zeros(D * K) if with_theta else None
-        self.ctx.check(self.ctx.lib.samelda_cu_model_download(self.ctx.h, _ptr(phi),
-                                                              _ptr(theta)))
+        c = self._live()
+        c.check(c.lib.samelda_cu_model_download(c.h, _ptr(phi), _ptr(theta)))
         return Model(K, W, self.config.alpha, self.config.beta, phi.reshape(K, W),
                      theta.reshape(D, K) if theta is not None else None)
 
@@ -584,6 +621,7 @@ def train(corpus, config: SamplerConfig, heldout=None, eval_every: int = 0,
           ctx: Context | None = None):
     """sampler.cpp:269-353 end to end on the device -> (Model, trace rows)."""
     ctx = ctx or default_context()
+    ctx._train_token = None  # per-call use replaces a Trainer's device state
     corpus = Corpus.of(corpus)
     cs = corpus._struct()
     cfg = config._struct()

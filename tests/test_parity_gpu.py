@@ -156,6 +156,41 @@ def test_trainer_periods_equal_composed_calls(port, small_split):
         np.testing.assert_array_equal(dev.theta, model.theta)
 
 
+def test_batch_theta_async_matches_sync(small_split):
+    """Async result copies queued behind later periods equal the sync copies."""
+    tr, _ = small_split
+    cfg = S.SamplerConfig(n_topics=8, m=5.0, t_max=4, batch_fraction=0.3, seed=3)
+    a, b = S.Trainer(tr, cfg), S.Trainer(tr, cfg)
+    sa, sb = (S.MinibatchStream(tr.n_docs, cfg.batch_fraction, cfg.seed) for _ in range(2))
+    bufs, sync_rows = [], []
+    for t in range(4):
+        m_t, rho = S.anneal_m("constant", t + 1, 4, cfg.m), S.rho_schedule(t, 1.0, 0.5)
+        batch = sa.next()
+        a.period(batch, t, m_t, rho)
+        buf = np.full(len(batch) * cfg.n_topics + 3, np.nan)
+        bufs.append((a.batch_theta_async(len(batch), buf), len(batch)))
+        b.period(sb.next(), t, m_t, rho)
+        sync_rows.append(b.batch_theta(len(batch)))
+    a.ctx.synchronize()
+    for (rows, n), ref in zip(bufs, sync_rows):
+        np.testing.assert_array_equal(rows, ref)
+    with pytest.raises(S.ConfigError):
+        a.batch_theta_async(len(batch), np.zeros(2))
+
+
+def test_trainers_do_not_share_device_state(small_split):
+    """Each Trainer owns its context; re-initialising a shared one is loud."""
+    tr, _ = small_split
+    cfg = S.SamplerConfig(n_topics=4, m=3.0, t_max=2, batch_fraction=0.5, seed=4)
+    a, b = S.Trainer(tr, cfg), S.Trainer(tr, cfg)
+    assert a.ctx is not b.ctx
+    ctx = S.Context(0)
+    c = S.Trainer(tr, cfg, ctx=ctx)
+    S.Trainer(tr, cfg, ctx=ctx)
+    with pytest.raises(S.ConfigError):
+        c.period(np.arange(3, dtype=np.int32), 0, 3.0, 1.0)
+
+
 def test_expected_counts_match_oracle(port, golden, small):
     batch, phi = golden["small_batch"], golden["small_phi"]
     tb = golden["small_theta"][batch]
