@@ -969,6 +969,238 @@ __global__ void __launch_bounds__(kFastBlock, SAMELDA_FAST_MINB) k_sample_fast(
   }
 }
 
+// ---------------------------------------------- sample (fast-exact, v2)
+// k_sample_v2: the same draws as k_sample_fast, bit for bit, with about a
+// third fewer instructions per draw (the kernel is issue-bound; ncu on the
+// fast kernel: 110 warp instructions per draw of which ~38 are the Philox
+// rounds and their round keys).  Differences:
+//   * the mu source is a template parameter (the period path's fused tree
+//     carries no mu shuffles or branches);
+//   * Philox chains run in groups of KG topics (register pressure: no spills
+//     at 64 registers), decisions follow each group;
+//   * decision: c2 by one FFMA (one rounding instead of two: inside the same
+//     bound), the count z = #(d_k > M) from three set.gt (0 / -1) and one
+//     IADD3 instead of predicate selects;
+//   * the phi-count scatter address is formed once per nonzero and every
+//     draw issues one unpredicated RED with an immediate offset (a warp-wide
+//     RED is issued for virtually every draw anyway; lanes with z = 0 add 0);
+//   * theta counts accumulate as packed u16 pairs (per lane and topic a
+//     chunk holds <= 128 nonzeros x z <= 40 < 2^16), flushed per doc.
+
+__device__ __forceinline__ void red_add_u64(unsigned long long* addr, uint32_t z) {
+  asm volatile("red.relaxed.gpu.global.add.u64 [%0], %1;" ::"l"(addr),
+               "l"(static_cast<unsigned long long>(z)));
+}
+
+// z in {0, 1, 2} decided branch-free, 3 = continue the search from k = 3
+// (see fast_poisson for the bound; c2 = fma(t1, lambda/2, c1) rounds once)
+__device__ __forceinline__ uint32_t fast_poisson3(float lam, float M, float u, bool& und,
+                                                  float& t1_out, float& c2_out) {
+  const float e0 = ex2_approx(__fmul_rn(lam, -1.4426950408889634f));
+  const float t1 = __fmul_rn(e0, lam);
+  const float c1 = __fadd_rn(e0, t1);
+  const float c2 = __fmaf_rn(t1, __fmul_rn(lam, 0.5f), c1);
+  const float d0 = __fsub_rn(u, e0), d1 = __fsub_rn(u, c1), d2 = __fsub_rn(u, c2);
+  und = und || (fabsf(d0) <= M) || (fabsf(d1) <= M) || (fabsf(d2) <= M);
+  t1_out = t1;
+  c2_out = c2;
+  // d0 >= d1 >= d2 (the cdf terms are non-decreasing): nested selects
+  return d2 > M ? 3u : (d1 > M ? 2u : (d0 > M ? 1u : 0u));
+}
+
+// sequential search from k = 3 (u beyond cdf_2 + M): fast_poisson's loop,
+// same arithmetic and bound; returns z or sets *und
+__device__ __forceinline__ uint32_t fast_poisson_tail(float lam, float u, float t1, float c2,
+                                                      bool* und) {
+  const float r0 = __fmaf_rn(2.4e-7f, lam, 4.8e-7f);
+  const float pl = __fmul_rn(3e-6f, lam);
+  float pmf = __fmul_rn(t1, __fmul_rn(lam, 0.5f)), cdf = c2, zf = 2.0f;
+  float rk = __fadd_rn(r0, 1.2e-6f);
+  uint32_t z = 2;
+  for (;;) {
+    ++z;
+    zf = __fadd_rn(zf, 1.0f);
+    pmf = __fmul_rn(pmf, __fmul_rn(lam, rcp_approx(zf)));
+    cdf = __fadd_rn(cdf, pmf);
+    rk = __fadd_rn(rk, 6e-7f);
+    const float mk = __fmaf_rn(cdf, rk, __fmaf_rn(pmf, pl, 2.5e-7f));
+    const float dk = __fsub_rn(u, cdf);
+    if (dk < -mk) return z;
+    if (!(dk > mk) || z >= 40) {
+      *und = true;
+      return 0;
+    }
+  }
+}
+
+template <int KPL, bool FULL, int MUSRC, int MINB>
+__global__ void __launch_bounds__(kFastBlock, MINB) k_sample_v2(
+    BatchView bv, const float* __restrict__ theta_b32, const float* __restrict__ phi32,
+    const double* __restrict__ mu_in, const float* __restrict__ mu_f_in, int K, double m_t,
+    uint64_t seed, uint32_t t, uint32_t sweep, int64_t chunk,
+    unsigned long long* __restrict__ theta_counts, unsigned long long* __restrict__ phi_counts,
+    Deferred* __restrict__ deferred, unsigned long long* __restrict__ n_deferred) {
+  constexpr int KG = KPL < 4 ? KPL : 4;  // Philox chains in flight per group
+  const int lane = threadIdx.x & 31;
+  const int64_t item = static_cast<int64_t>(blockIdx.x) * (kFastBlock / kWarp) + (threadIdx.x >> 5);
+  const int kbase = static_cast<int>(blockIdx.y) * kWarp * KPL;
+  const int64_t p0 = item * chunk;
+  const int64_t p1 = min(p0 + chunk, bv.nnz);
+
+  __shared__ uint4 s_keys[KPL][kKeyWords / 4][kWarp];
+  for (int e = threadIdx.x; e < KPL * kWarp; e += blockDim.x) {
+    const int jj = e / kWarp, ll = e % kWarp;
+    uint32_t ks[kKeyWords];
+    topic_schedule(seed, t, sweep, static_cast<uint32_t>(kbase + ll + kWarp * jj), ks);
+#pragma unroll
+    for (int q = 0; q < kKeyWords / 4; ++q)
+      s_keys[jj][q][ll] = make_uint4(ks[4 * q], ks[4 * q + 1], ks[4 * q + 2], ks[4 * q + 3]);
+  }
+  __syncthreads();
+  if (p0 >= p1) return;
+
+  int cur_b = -1;
+  float th[KPL];
+  uint32_t acc[(KPL + 1) / 2];
+#pragma unroll
+  for (int j = 0; j < KPL; ++j) th[j] = 0.0f;
+#pragma unroll
+  for (int j = 0; j < (KPL + 1) / 2; ++j) acc[j] = 0u;
+
+  auto flush = [&](int b) {
+#pragma unroll
+    for (int j = 0; j < KPL; ++j) {
+      const int k = kbase + lane + kWarp * j;
+      const uint32_t v = (j & 1) ? (acc[j >> 1] >> 16) : (acc[j >> 1] & 0xffffu);
+      if ((FULL || k < K) && v)
+        atomicAdd(theta_counts + static_cast<int64_t>(b) * K + k, static_cast<unsigned long long>(v));
+    }
+  };
+
+  for (int64_t g0 = p0; g0 < p1; g0 += kWarp) {
+    const int64_t p = g0 + lane;
+    int32_t b = 0, d = 0, w = 0, c = 0;
+    double mu_v = 0.0;
+    float muf_v = 0.0f;
+    if (p < p1) {
+      b = static_cast<int32_t>(find_row(bv.batch_prefix, bv.B, p));
+      d = __ldg(bv.batch_docs + b);
+      const int64_t gi = __ldg(bv.doc_offsets + d) + (p - __ldg(bv.batch_prefix + b));
+      w = __ldg(bv.word_ids + gi);
+      c = __ldg(bv.counts + gi);
+      if (MUSRC == 1) mu_v = __ldg(mu_in + p);
+      if (MUSRC == 2) muf_v = __ldg(mu_f_in + p);
+    }
+    const int n_here = static_cast<int>(min(static_cast<int64_t>(kWarp), p1 - g0));
+    for (int i = 0; i < n_here; ++i) {
+      const int32_t bi = __shfl_sync(0xffffffffu, b, i);
+      const uint32_t di = static_cast<uint32_t>(__shfl_sync(0xffffffffu, d, i) + static_cast<int32_t>(bv.doc_base));
+      const int32_t wi = __shfl_sync(0xffffffffu, w, i);
+      const int32_t ci = __shfl_sync(0xffffffffu, c, i);
+      float ph[KPL];
+      {
+        const float* prow = phi32 + static_cast<int64_t>(wi) * K + kbase + lane;
+#pragma unroll
+        for (int j = 0; j < KPL; ++j) ph[j] = (FULL || kbase + lane + kWarp * j < K) ? __ldg(prow + kWarp * j) : 0.0f;
+      }
+      if (bi != cur_b) {
+        if (cur_b >= 0) flush(cur_b);
+        cur_b = bi;
+        const float* trow = theta_b32 + static_cast<int64_t>(bi) * K + kbase + lane;
+#pragma unroll
+        for (int j = 0; j < KPL; ++j) th[j] = (FULL || kbase + lane + kWarp * j < K) ? __ldg(trow + kWarp * j) : 0.0f;
+#pragma unroll
+        for (int j = 0; j < (KPL + 1) / 2; ++j) acc[j] = 0u;
+      }
+      float prod[KPL];
+#pragma unroll
+      for (int j = 0; j < KPL; ++j) prod[j] = __fmul_rn(th[j], ph[j]);
+      float mu_f;
+      if (MUSRC == 1) {
+        mu_f = __double2float_rn(__shfl_sync(0xffffffffu, mu_v, i));
+      } else if (MUSRC == 2) {
+        mu_f = __shfl_sync(0xffffffffu, muf_v, i);
+      } else {
+        mu_f = 0.0f;
+#pragma unroll
+        for (int j = 0; j < KPL; ++j) mu_f = __fadd_rn(mu_f, prod[j]);
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) mu_f = __fadd_rn(mu_f, __shfl_xor_sync(0xffffffffu, mu_f, o));
+      }
+      const bool nz_exact = !(mu_f >= 1e-20f) || isinf(mu_f);
+      const float scale = __fdividef(__double2float_rn(__dmul_rn(m_t, static_cast<double>(ci))), mu_f);
+      // band slope per nonzero: M = prod (3.3e-6 scale) + 2e-6 is within 2.4e-7
+      // relative of 3.3e-6 lambda + 2e-6 >= 3.24e-6 lambda + 1.93e-6 >= m_0..2
+      const float mslope = __fmul_rn(scale, 3.3e-6f);
+      uint32_t m1lo, m1hi;
+      mulhilo(kPhiloxM1, di, m1lo, m1hi);
+      const Philox1 r1{m1hi ^ static_cast<uint32_t>(wi), m1lo};
+      unsigned long long* pc = phi_counts + static_cast<int64_t>(wi) * K + kbase + lane;
+      uint32_t defer_bits = 0;
+#pragma unroll
+      for (int g = 0; g < KPL; g += KG) {
+        uint32_t y[KG];
+#pragma unroll
+        for (int jj = 0; jj < KG; ++jj) {
+          uint32_t ks[kKeyWords];
+#pragma unroll
+          for (int q = 0; q < kKeyWords / 4; ++q) {
+            const uint4 v = s_keys[g + jj][q][lane];
+            ks[4 * q] = v.x;
+            ks[4 * q + 1] = v.y;
+            ks[4 * q + 2] = v.z;
+            ks[4 * q + 3] = v.w;
+          }
+          y[jj] = philox_y_sched(r1, ks);
+        }
+#pragma unroll
+        for (int jj = 0; jj < KG; ++jj) asm volatile("" : "+r"(y[jj]));
+#pragma unroll
+        for (int jj = 0; jj < KG; ++jj) {
+          const int j = g + jj;
+          const float lam = __fmul_rn(prod[j], scale);
+          bool und = nz_exact || !(prod[j] >= 1e-30f) || !(lam < kInvMax);
+          const float u = __fsub_rn(__int_as_float(0x3f800000 | (y[jj] >> 9)), 1.0f);
+          float t1, c2;
+          uint32_t z = fast_poisson3(lam, __fmaf_rn(prod[j], mslope, 2e-6f), u, und, t1, c2);
+          if (z == 3 && !und) z = fast_poisson_tail(lam, u, t1, c2, &und);
+          if (!FULL && kbase + lane + kWarp * j >= K) {
+            und = false;
+            z = 0;
+          }
+#ifdef SAMELDA_DEFER_STATS
+          if (FULL || kbase + lane + kWarp * j < K) defer_stats(nz_exact, prod[j], lam, und);
+#endif
+          if (und) {
+            defer_bits |= 1u << j;
+            z = 0;
+          }
+          acc[j >> 1] += (j & 1) ? (z << 16) : z;
+          if (FULL || kbase + lane + kWarp * j < K) red_add_u64(pc + kWarp * j, z);
+        }
+      }
+      if (__any_sync(0xffffffffu, defer_bits != 0)) {
+        uint32_t masks[8];
+#pragma unroll
+        for (int j = 0; j < 8; ++j) masks[j] = j < KPL ? __ballot_sync(0xffffffffu, (defer_bits >> j) & 1u) : 0u;
+        if (lane == 0) {
+          const unsigned long long slot = atomicAdd(n_deferred, 1ull);
+          Deferred rec;
+          rec.p = g0 + i;
+          rec.b = bi;
+          rec.w = wi;
+          rec.c = ci;
+          rec.kbase = kbase;
+#pragma unroll
+          for (int j = 0; j < 8; ++j) rec.mask[j] = masks[j];
+          deferred[slot] = rec;
+        }
+      }
+    }
+  }
+  if (cur_b >= 0) flush(cur_b);
+}
+
 // Deferred exact draws in two passes.
 // Phase A (k_deferred_expand), lane = record: the record's exact mu -- the
 // reference's sequential-k f64 dot (sampler.cpp:111-119), unless the caller
@@ -1186,7 +1418,32 @@ int launch_fast_kpl(const BatchView& bv, const double* tb64, const float* tb32, 
   }
   auto* rec = static_cast<Deferred*>(deferred);
   const dim3 grid(static_cast<unsigned>((items + warps - 1) / warps), static_cast<unsigned>(n_slices));
-  if (K % (kWarp * KPL) == 0)
+  const char* variant = getenv("SAMELDA_SAMPLER");
+  const bool v1 = variant && variant[0] == 'o';  // the previous kernel, for A/B profiling
+  if (!v1) {
+    const int musrc = mu ? 1 : (muf ? 2 : 0);
+    const bool full = K % (kWarp * KPL) == 0;
+    const char* minb_env = getenv("SAMELDA_MINB");
+    const int minb = minb_env ? atoi(minb_env) : 4;
+#define SCU_V2(FULLV, MS)                                                                        \
+  do {                                                                                           \
+    if constexpr (KPL == 8 && FULLV && MS == 0) {                                                \
+      if (minb == 3) {                                                                           \
+        k_sample_v2<KPL, FULLV, MS, 3><<<grid, kFastBlock, 0, st>>>(                             \
+            bv, tb32, phi32, mu, muf, K, m_t, seed, t, sweep, chunk, tc, pc, rec, n_deferred);   \
+        break;                                                                                   \
+      }                                                                                          \
+    }                                                                                            \
+      k_sample_v2<KPL, FULLV, MS, 4><<<grid, kFastBlock, 0, st>>>(                               \
+          bv, tb32, phi32, mu, muf, K, m_t, seed, t, sweep, chunk, tc, pc, rec, n_deferred);     \
+  } while (0)
+    if (full) {
+      if (musrc == 0) SCU_V2(true, 0); else if (musrc == 1) SCU_V2(true, 1); else SCU_V2(true, 2);
+    } else {
+      if (musrc == 0) SCU_V2(false, 0); else if (musrc == 1) SCU_V2(false, 1); else SCU_V2(false, 2);
+    }
+#undef SCU_V2
+  } else if (K % (kWarp * KPL) == 0)
     k_sample_fast<KPL, true><<<grid, kFastBlock, 0, st>>>(
         bv, tb32, phi32, mu, muf, K, m_t, seed, t, sweep, chunk, n_slices, tc, pc, rec, n_deferred);
   else
@@ -1784,7 +2041,7 @@ int launch_sample_fast(const BatchView& bv, const double* theta_b64, const float
   const char* variant = getenv("SAMELDA_SAMPLER");
   const char v = variant ? variant[0] : 'f';
   // K > 256: topic slices of 256 with the full mu from a k_mu_f32 pre-pass
-  if (v == 'f') {
+  if (v == 'f' || v == 'o') {
     if (K <= 32)
       return launch_fast_kpl<1>(bv, theta_b64, theta_b32, phi64, phi32, mu, K, m_t, seed, t, sweep, tc, pc,
                                 deferred, n_deferred, aux, draw_cap, mu_f, err, st);
