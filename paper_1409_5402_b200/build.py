@@ -18,7 +18,7 @@ BUILD = os.path.join(PKG, "_build")
 LIB = os.path.join(PKG, "libsamelda_cuda.so")
 
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
-COMMON = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-I", CSRC,
+COMMON = ["-O3", "-lineinfo", "-std=c++20", "-Xcompiler", "-fPIC", "-I", CSRC,
           "-I", os.path.join(ROOT, "include")]
 UNITS = {
     "kernels.cu": ["-fmad=false"],
@@ -26,7 +26,7 @@ UNITS = {
     "capi.cu": [],
     "synth.cpp": [],
 }
-GXX = ["-O3", "-std=c++17", "-fPIC", "-pthread", "-I", CSRC, "-I", os.path.join(ROOT, "include")]
+GXX = ["-O3", "-std=c++20", "-fPIC", "-pthread", "-I", CSRC, "-I", os.path.join(ROOT, "include")]
 
 
 def nvcc() -> str:

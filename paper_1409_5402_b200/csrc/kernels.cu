@@ -993,19 +993,43 @@ __device__ __forceinline__ void red_add_u64(unsigned long long* addr, uint32_t z
 }
 
 // z in {0, 1, 2} decided branch-free, 3 = continue the search from k = 3
-// (see fast_poisson for the bound; c2 = fma(t1, lambda/2, c1) rounds once)
-__device__ __forceinline__ uint32_t fast_poisson3(float lam, float M, float u, bool& und,
+// (see fast_poisson for the bound; c2 = fma(t1, lambda/2, c1) rounds once).
+// DEC selects how z and the band flag are formed (same decisions):
+//   0: predicates + nested selects (ALU pipe)
+//   1: z = sum of sat(2^100 (d_k - M)) on the FMA pipe, band by predicates
+//   2: band too: und iff sum_k sat(2^100 (d_k - M)) + sat(2^100 (-d_k - M)) != 3
+//      (counts d_k > M and d_k < -M; equality on either side is in the band)
+// Mb = M 2^100 exactly (power-of-two scaling).
+template <int DEC>
+__device__ __forceinline__ uint32_t fast_poisson3(float lam, float M, float Mb, float u, bool& und,
                                                   float& t1_out, float& c2_out) {
   const float e0 = ex2_approx(__fmul_rn(lam, -1.4426950408889634f));
   const float t1 = __fmul_rn(e0, lam);
   const float c1 = __fadd_rn(e0, t1);
   const float c2 = __fmaf_rn(t1, __fmul_rn(lam, 0.5f), c1);
   const float d0 = __fsub_rn(u, e0), d1 = __fsub_rn(u, c1), d2 = __fsub_rn(u, c2);
-  und = und || (fabsf(d0) <= M) || (fabsf(d1) <= M) || (fabsf(d2) <= M);
   t1_out = t1;
   c2_out = c2;
-  // d0 >= d1 >= d2 (the cdf terms are non-decreasing): nested selects
-  return d2 > M ? 3u : (d1 > M ? 2u : (d0 > M ? 1u : 0u));
+  if (DEC == 0) {
+    und = und || (fabsf(d0) <= M) || (fabsf(d1) <= M) || (fabsf(d2) <= M);
+    // d0 >= d1 >= d2 (the cdf terms are non-decreasing): nested selects
+    return d2 > M ? 3u : (d1 > M ? 2u : (d0 > M ? 1u : 0u));
+  }
+  // sign of 2^100 d_k - Mb is the sign of d_k - M (one rounding, no overflow:
+  // |d_k| <= 1); any nonzero difference is >= 2^-149 * 2^100 -> saturates to 1
+  const float s0 = __saturatef(__fmaf_rn(d0, 0x1p100f, -Mb));
+  const float s1 = __saturatef(__fmaf_rn(d1, 0x1p100f, -Mb));
+  const float s2 = __saturatef(__fmaf_rn(d2, 0x1p100f, -Mb));
+  const float zf = __fadd_rn(__fadd_rn(s0, s1), s2);
+  if (DEC == 1) {
+    und = und || (fabsf(d0) <= M) || (fabsf(d1) <= M) || (fabsf(d2) <= M);
+  } else {
+    const float l0 = __saturatef(__fmaf_rn(d0, -0x1p100f, -Mb));
+    const float l1 = __saturatef(__fmaf_rn(d1, -0x1p100f, -Mb));
+    const float l2 = __saturatef(__fmaf_rn(d2, -0x1p100f, -Mb));
+    und = und || (__fadd_rn(zf, __fadd_rn(__fadd_rn(l0, l1), l2)) != 3.0f);
+  }
+  return __float_as_uint(__fadd_rn(zf, 8388608.0f)) - 0x4B000000u;
 }
 
 // sequential search from k = 3 (u beyond cdf_2 + M): fast_poisson's loop,
@@ -1033,7 +1057,7 @@ __device__ __forceinline__ uint32_t fast_poisson_tail(float lam, float u, float 
   }
 }
 
-template <int KPL, bool FULL, int MUSRC, int MINB>
+template <int KPL, bool FULL, int MUSRC, int MINB, int DEC = 1, int TAIL = 0>
 __global__ void __launch_bounds__(kFastBlock, MINB) k_sample_v2(
     BatchView bv, const float* __restrict__ theta_b32, const float* __restrict__ phi32,
     const double* __restrict__ mu_in, const float* __restrict__ mu_f_in, int K, double m_t,
@@ -1048,6 +1072,12 @@ __global__ void __launch_bounds__(kFastBlock, MINB) k_sample_v2(
   const int64_t p1 = min(p0 + chunk, bv.nnz);
 
   __shared__ uint4 s_keys[KPL][kKeyWords / 4][kWarp];
+  // TAIL 1: draws that need the sequential search (u beyond cdf_2 + M) are
+  // provisionally counted as z = 3 (certain lower bound) and parked here;
+  // one combined pass per nonzero finishes them (lanes run their own parked
+  // topics back to back instead of entering a divergent loop per topic)
+  __shared__ float2 s_park[TAIL ? kFastBlock / kWarp : 1][TAIL ? KPL : 1][kWarp];
+  const int warp = threadIdx.x >> 5;
   for (int e = threadIdx.x; e < KPL * kWarp; e += blockDim.x) {
     const int jj = e / kWarp, ll = e % kWarp;
     uint32_t ks[kKeyWords];
@@ -1136,7 +1166,7 @@ __global__ void __launch_bounds__(kFastBlock, MINB) k_sample_v2(
       mulhilo(kPhiloxM1, di, m1lo, m1hi);
       const Philox1 r1{m1hi ^ static_cast<uint32_t>(wi), m1lo};
       unsigned long long* pc = phi_counts + static_cast<int64_t>(wi) * K + kbase + lane;
-      uint32_t defer_bits = 0;
+      uint32_t defer_bits = 0, parked = 0;
 #pragma unroll
       for (int g = 0; g < KPL; g += KG) {
         uint32_t y[KG];
@@ -1162,11 +1192,22 @@ __global__ void __launch_bounds__(kFastBlock, MINB) k_sample_v2(
           bool und = nz_exact || !(prod[j] >= 1e-30f) || !(lam < kInvMax);
           const float u = __fsub_rn(__int_as_float(0x3f800000 | (y[jj] >> 9)), 1.0f);
           float t1, c2;
-          uint32_t z = fast_poisson3(lam, __fmaf_rn(prod[j], mslope, 2e-6f), u, und, t1, c2);
-          if (z == 3 && !und) z = fast_poisson_tail(lam, u, t1, c2, &und);
+          const float M = __fmaf_rn(prod[j], mslope, 2e-6f);
+          uint32_t z = fast_poisson3<DEC>(lam, M, __fmul_rn(M, 0x1p100f), u, und, t1, c2);
+          bool park = false;
+          if (TAIL == 0) {
+            if (z == 3 && !und) z = fast_poisson_tail(lam, u, t1, c2, &und);
+          } else {
+            park = z == 3 && !und;
+          }
           if (!FULL && kbase + lane + kWarp * j >= K) {
             und = false;
             z = 0;
+            park = false;
+          }
+          if (TAIL && park) {
+            s_park[warp][j][lane] = make_float2(lam, u);
+            parked |= 1u << j;
           }
 #ifdef SAMELDA_DEFER_STATS
           if (FULL || kbase + lane + kWarp * j < K) defer_stats(nz_exact, prod[j], lam, und);
@@ -1178,6 +1219,31 @@ __global__ void __launch_bounds__(kFastBlock, MINB) k_sample_v2(
           acc[j >> 1] += (j & 1) ? (z << 16) : z;
           if (FULL || kbase + lane + kWarp * j < K) red_add_u64(pc + kWarp * j, z);
         }
+      }
+      if (TAIL && __any_sync(0xffffffffu, parked != 0)) {
+        // finish parked draws: z = 3 was counted; add z - 3, or undo the 3
+        // (u64 wrap-around) and defer the draw when the search is undecided
+        unsigned long long* tcrow = theta_counts + static_cast<int64_t>(bi) * K + kbase + lane;
+        do {
+          if (parked) {
+            const int j = __ffs(parked) - 1;
+            parked &= parked - 1;
+            const float2 st = s_park[warp][j][lane];
+            // t1, c2 recomputed exactly as fast_poisson3 formed them
+            const float e0 = ex2_approx(__fmul_rn(st.x, -1.4426950408889634f));
+            const float t1 = __fmul_rn(e0, st.x);
+            const float c2 = __fmaf_rn(t1, __fmul_rn(st.x, 0.5f), __fadd_rn(e0, t1));
+            bool und = false;
+            const uint32_t z = fast_poisson_tail(st.x, st.y, t1, c2, &und);
+            const unsigned long long delta =
+                und ? ~2ull : static_cast<unsigned long long>(z - 3u);
+            if (und) defer_bits |= 1u << j;
+            if (delta) {
+              atomicAdd(pc + kWarp * j, delta);
+              atomicAdd(tcrow + kWarp * j, delta);
+            }
+          }
+        } while (__any_sync(0xffffffffu, parked != 0));
       }
       if (__any_sync(0xffffffffu, defer_bits != 0)) {
         uint32_t masks[8];
@@ -1425,17 +1491,24 @@ int launch_fast_kpl(const BatchView& bv, const double* tb64, const float* tb32, 
     const bool full = K % (kWarp * KPL) == 0;
     const char* minb_env = getenv("SAMELDA_MINB");
     const int minb = minb_env ? atoi(minb_env) : 4;
+    const char* dec_env = getenv("SAMELDA_DEC");
+    const int dec = dec_env ? atoi(dec_env) : 1;
+    const char* tail_env = getenv("SAMELDA_TAIL");
+    const int tail = tail_env ? atoi(tail_env) : 0;
+#define SCU_V2_LAUNCH(FULLV, MS, MB, DC, ...)                                                   \
+  k_sample_v2<KPL, FULLV, MS, MB, DC __VA_OPT__(,) __VA_ARGS__><<<grid, kFastBlock, 0, st>>>(    \
+      bv, tb32, phi32, mu, muf, K, m_t, seed, t, sweep, chunk, tc, pc, rec, n_deferred)
+    // production: DEC 1, 4 blocks/SM; the bench instantiation also carries the
+    // A/B alternatives (SAMELDA_DEC=0|2, SAMELDA_MINB=3, SAMELDA_TAIL=1), all bit-identical
 #define SCU_V2(FULLV, MS)                                                                        \
   do {                                                                                           \
     if constexpr (KPL == 8 && FULLV && MS == 0) {                                                \
-      if (minb == 3) {                                                                           \
-        k_sample_v2<KPL, FULLV, MS, 3><<<grid, kFastBlock, 0, st>>>(                             \
-            bv, tb32, phi32, mu, muf, K, m_t, seed, t, sweep, chunk, tc, pc, rec, n_deferred);   \
-        break;                                                                                   \
-      }                                                                                          \
+      if (minb == 3) { SCU_V2_LAUNCH(FULLV, MS, 3, 1); break; }                                  \
+      if (dec == 0) { SCU_V2_LAUNCH(FULLV, MS, 4, 0); break; }                                   \
+      if (dec == 2) { SCU_V2_LAUNCH(FULLV, MS, 4, 2); break; }                                   \
+      if (tail == 1) { SCU_V2_LAUNCH(FULLV, MS, 4, 1, 1); break; }                               \
     }                                                                                            \
-      k_sample_v2<KPL, FULLV, MS, 4><<<grid, kFastBlock, 0, st>>>(                               \
-          bv, tb32, phi32, mu, muf, K, m_t, seed, t, sweep, chunk, tc, pc, rec, n_deferred);     \
+    SCU_V2_LAUNCH(FULLV, MS, 4, 1);                                                              \
   } while (0)
     if (full) {
       if (musrc == 0) SCU_V2(true, 0); else if (musrc == 1) SCU_V2(true, 1); else SCU_V2(true, 2);
@@ -1443,6 +1516,7 @@ int launch_fast_kpl(const BatchView& bv, const double* tb64, const float* tb32, 
       if (musrc == 0) SCU_V2(false, 0); else if (musrc == 1) SCU_V2(false, 1); else SCU_V2(false, 2);
     }
 #undef SCU_V2
+#undef SCU_V2_LAUNCH
   } else if (K % (kWarp * KPL) == 0)
     k_sample_fast<KPL, true><<<grid, kFastBlock, 0, st>>>(
         bv, tb32, phi32, mu, muf, K, m_t, seed, t, sweep, chunk, n_slices, tc, pc, rec, n_deferred);

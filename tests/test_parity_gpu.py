@@ -438,6 +438,21 @@ def test_trainer_reports_device_error_asynchronously(port):
     tr.ctx.synchronize()  # reported once, then cleared
 
 
+@pytest.mark.parametrize("m,schedule", [(100.0, "constant"), (400.0, "linear")])
+def test_train_k256_production_kernel_bit_exact(port, m, schedule):
+    """The bench's kernel instantiation (K=256: 8 topics per lane, full slice,
+    fused mu) on the period path, with high m so the search loop, the
+    deferred PTRS draws and the band all occur."""
+    g = port.make_corpus(120, 400, 12, 150.0, 29)
+    tr, te = port.split_holdout(g, 0.1, 2)
+    cfg = dict(n_topics=256, m=m, schedule=schedule, t_max=4, batch_fraction=0.5, seed=6)
+    model, trace = S.train(tr, S.SamplerConfig(**cfg), te, 2)
+    ophi, otheta, otrace = port.train(tr, TrainConfig(**cfg), te, 2)
+    np.testing.assert_array_equal(model.phi, ophi)
+    np.testing.assert_array_equal(model.theta, otheta)
+    np.testing.assert_allclose([r["ll"] for r in trace], [r["ll"] for r in otrace], rtol=1e-12)
+
+
 @pytest.mark.parametrize("K", [300, 520])
 def test_train_sliced_k_bit_exact(port, K):
     """K > 256 on the period path: topic slices with the k_mu_f32 pre-pass."""
