@@ -1904,6 +1904,8 @@ __device__ __forceinline__ double seq_dot(const double* __restrict__ th,
   double dot = 0.0;
   if ((K & 1) == 0) {
     const double2* r2 = reinterpret_cast<const double2*>(row);
+    // unrolled so several row loads are in flight ahead of the (sequential) adds
+#pragma unroll 8
     for (int k2 = 0; k2 < (K >> 1); ++k2) {
       const double2 v = __ldg(r2 + k2);
       dot = __dadd_rn(dot, __dmul_rn(th[2 * k2], v.x));
@@ -2010,6 +2012,133 @@ __global__ void __launch_bounds__(kEvalWarps * 32) k_eval_docs(
     if (theta_out)
       for (int k = lane; k < K; k += 32) theta_out[doc * K + k] = th[k];
     __syncwarp();
+  }
+}
+
+// CTA per test document (K <= kEvalCtaMaxK): the same arithmetic in the same
+// order as k_eval_docs / eval.cpp:19-64, laid out so a document's phi rows
+// stay L2-resident across its fold-in sweeps (~600 documents in flight, their
+// fold rows ~90 MB) and every step has block-wide parallelism:
+//   phase 1, thread = cell: mu_i = sequential-k dot (eval.cpp:38-41), scale
+//     c_i / mu_i for the cells that inform theta;
+//   phase 2, thread = topic: next[k] += (scale_i theta[k]) phi[w_i][k] over
+//     the chunk's cells in cell order (eval.cpp:45-49) -- coalesced rows;
+//   phase 3: total in sequential k order (one thread), theta = next / total,
+//     block max of |delta| (eval.cpp:51-60).
+// Scoring: thread = cell dot, doc log p summed in cell order by one thread.
+constexpr int kEvalCtaThreads = 256;
+constexpr int kEvalCtaMaxK = 4096;
+
+__global__ void __launch_bounds__(kEvalCtaThreads) k_eval_cta(
+    const int64_t* __restrict__ doc_offsets, const int32_t* __restrict__ word_ids,
+    const int32_t* __restrict__ fold_counts, const int32_t* __restrict__ score_counts,
+    int64_t n_docs, const double* __restrict__ phi_wk, int K, double alpha, int sweeps,
+    double* __restrict__ doc_logp, int64_t* __restrict__ doc_scored,
+    double* __restrict__ theta_out, int* __restrict__ err) {
+  extern __shared__ double smem[];
+  double* th = smem;                 // K
+  double* nx = th + K;               // K
+  double* cs = nx + K;               // [256] cell scale (0 = skip) / score term
+  int32_t* cw = reinterpret_cast<int32_t*>(cs + kEvalCtaThreads);  // [256] cell word
+  __shared__ double s_red[kEvalCtaThreads / 32];
+  __shared__ int64_t s_cnt[kEvalCtaThreads];
+  __shared__ double s_total;
+  __shared__ int s_done;
+  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  const double inv_k = 1.0 / static_cast<double>(K);
+  for (int64_t doc = blockIdx.x; doc < n_docs; doc += gridDim.x) {
+    const int64_t base = doc_offsets[doc];
+    const int64_t n = doc_offsets[doc + 1] - base;
+    for (int k = tid; k < K; k += kEvalCtaThreads) th[k] = inv_k;
+    __syncthreads();
+    for (int sweep = 0; sweep < sweeps && n > 0; ++sweep) {
+      for (int k = tid; k < K; k += kEvalCtaThreads) nx[k] = alpha;
+      for (int64_t i0 = 0; i0 < n; i0 += kEvalCtaThreads) {
+        const int n_here = static_cast<int>(min(static_cast<int64_t>(kEvalCtaThreads), n - i0));
+        if (tid < n_here) {
+          const int64_t i = base + i0 + tid;
+          const int32_t fc = __ldg(fold_counts + i);
+          const int32_t w = __ldg(word_ids + i);
+          double scale = 0.0;
+          if (fc != 0) {  // a zero-count cell adds exactly +0 (eval.cpp:43-47)
+            const double mu = seq_dot(th, phi_wk + static_cast<int64_t>(w) * K, K);
+            if (mu > 0.0) scale = __ddiv_rn(static_cast<double>(fc), mu);
+          }
+          cs[tid] = scale;
+          cw[tid] = w;
+        }
+        __syncthreads();
+        for (int k = tid; k < K; k += kEvalCtaThreads) {
+          double acc = nx[k];
+          const double tk = th[k];
+#pragma unroll 4
+          for (int c = 0; c < n_here; ++c) {
+            const double sc = cs[c];
+            if (sc != 0.0)
+              acc = __dadd_rn(acc, __dmul_rn(__dmul_rn(sc, tk),
+                                             __ldg(phi_wk + static_cast<int64_t>(cw[c]) * K + k)));
+          }
+          nx[k] = acc;
+        }
+        __syncthreads();
+      }
+      if (tid == 0) {
+        double total = 0.0;
+        for (int k = 0; k < K; ++k) total = __dadd_rn(total, nx[k]);
+        s_total = total;
+      }
+      __syncthreads();
+      const double total = s_total;
+      double delta = 0.0;
+      for (int k = tid; k < K; k += kEvalCtaThreads) {
+        const double v = __ddiv_rn(nx[k], total);
+        delta = fmax(delta, fabs(__dadd_rn(v, -th[k])));
+        th[k] = v;
+      }
+      delta = warp_max(delta);
+      if (lane == 0) s_red[wid] = delta;
+      __syncthreads();
+      if (tid == 0) {
+        double d = s_red[0];
+        for (int w = 1; w < kEvalCtaThreads / 32; ++w) d = fmax(d, s_red[w]);
+        s_done = d < 1e-12;
+      }
+      __syncthreads();
+      if (s_done) break;
+    }
+    // score the held-back half (eval.cpp:125-145), log p summed in cell order
+    double logp = 0.0;
+    int64_t scored = 0;
+    for (int64_t i0 = 0; i0 < n; i0 += kEvalCtaThreads) {
+      const int n_here = static_cast<int>(min(static_cast<int64_t>(kEvalCtaThreads), n - i0));
+      if (tid < n_here) {
+        const int64_t i = base + i0 + tid;
+        const int32_t sc = __ldg(score_counts + i);
+        double term = 0.0;
+        if (sc != 0) {
+          const double pr = seq_dot(th, phi_wk + static_cast<int64_t>(__ldg(word_ids + i)) * K, K);
+          if (!(pr > 0.0)) atomicOr(err, kErrNumerical);
+          term = __dmul_rn(static_cast<double>(sc), log(pr));
+        }
+        cs[tid] = term;
+        s_cnt[tid] = sc;
+      }
+      __syncthreads();
+      if (tid == 0)
+        for (int c = 0; c < n_here; ++c)
+          if (s_cnt[c] != 0) {
+            logp = __dadd_rn(logp, cs[c]);
+            scored += s_cnt[c];
+          }
+      __syncthreads();
+    }
+    if (tid == 0) {
+      doc_logp[doc] = logp;
+      doc_scored[doc] = scored;
+    }
+    if (theta_out)
+      for (int k = tid; k < K; k += kEvalCtaThreads) theta_out[doc * K + k] = th[k];
+    __syncthreads();
   }
 }
 
@@ -2239,6 +2368,22 @@ int launch_eval_docs(const int64_t* doc_offsets, const int32_t* word_ids,
                      int64_t* doc_scored, double* theta_out, double* scratch,
                      int64_t scratch_doubles, int* err, cudaStream_t st) {
   if (n_docs == 0) return 0;
+  if (K <= kEvalCtaMaxK && !getenv("SAMELDA_EVAL_WARP")) {
+    const size_t smem_c = (2 * static_cast<size_t>(K) + kEvalCtaThreads) * sizeof(double) +
+                          kEvalCtaThreads * sizeof(int32_t);
+    static size_t configured_c = 48 * 1024;
+    if (smem_c > configured_c) {
+      cudaFuncSetAttribute(k_eval_cta, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           static_cast<int>(smem_c));
+      configured_c = smem_c;
+    }
+    // ~600 documents in flight: their fold rows stay L2-resident across sweeps
+    const int64_t blocks = min(n_docs, static_cast<int64_t>(148 * 4));
+    k_eval_cta<<<static_cast<unsigned>(blocks), kEvalCtaThreads, smem_c, st>>>(
+        doc_offsets, word_ids, fold_counts, score_counts, n_docs, phi_wk, K, alpha, sweeps,
+        doc_logp, doc_scored, theta_out, err);
+    return 1;
+  }
   const size_t smem = static_cast<size_t>(kEvalWarps) * 2 * K * sizeof(double);
   int64_t blocks = (n_docs + kEvalWarps - 1) / kEvalWarps;
   if (smem <= kEvalSmemMax) {
