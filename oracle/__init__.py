@@ -38,6 +38,7 @@ class OracleError(RuntimeError):
     def __init__(self, code: int, msg: str = ""):
         super().__init__(f"{ERRORS.get(code, code)}: {msg}")
         self.code = code
+        self.msg = msg
         self.kind = ERRORS.get(code, "Error")
 
 
@@ -564,6 +565,89 @@ class Ref:
         self._chk(self.lib.ref_train(corpus.doc_offsets, corpus.word_ids, corpus.counts, D, W,
                                      *ho, C.byref(s), eval_every, phi, theta, rows, C.byref(n)))
         return phi.reshape(K, W), theta.reshape(D, K), _trace_to_list(rows, n.value)
+
+
+    # ---- data formats: the reference's own load/save
+    def _io_sigs(self):
+        L = self.lib
+        if getattr(self, "_io_ready", False):
+            return L
+        L.ref_load_uci.restype = C.c_void_p
+        L.ref_load_uci.argtypes = [C.c_char_p, C.c_char_p, C.POINTER(C.c_int)]
+        L.ref_loaded_dims.argtypes = [C.c_void_p] + [C.POINTER(C.c_int64)] * 5
+        L.ref_loaded_copy.argtypes = [C.c_void_p, _i64p, _i32p, _i32p, C.c_char_p]
+        L.ref_loaded_free.argtypes = [C.c_void_p]
+        L.ref_save_uci.argtypes = [_i64p, _i32p, _i32p, C.c_int64, C.c_int64, C.c_char_p,
+                                   C.c_int64, C.c_char_p, C.c_char_p]
+        L.ref_save_checkpoint.argtypes = [C.c_char_p, C.c_int64, C.c_int64, C.c_double,
+                                          C.c_double, _f64p]
+        L.ref_load_checkpoint.argtypes = [C.c_char_p] + [C.POINTER(C.c_int64)] * 2 + [
+            C.POINTER(C.c_double)] * 2 + [C.c_void_p, C.c_int64]
+        L.ref_write_metrics_csv.argtypes = [C.c_char_p, C.POINTER(_TraceRow), C.c_int64]
+        L.ref_read_metrics_csv.argtypes = [C.c_char_p, C.POINTER(_TraceRow), C.c_int64,
+                                           C.POINTER(C.c_int64)]
+        self._io_ready = True
+        return L
+
+    def load_uci_bow(self, docword: str, vocab: str):
+        """corpus.cpp:62-183 -> (offsets, words, counts, n_words, n_tokens, vocab list)."""
+        L = self._io_sigs()
+        rc = C.c_int()
+        h = L.ref_load_uci(docword.encode(), vocab.encode(), C.byref(rc))
+        self._chk(rc.value)
+        try:
+            d, w, nnz, tok, vb = (C.c_int64() for _ in range(5))
+            L.ref_loaded_dims(h, C.byref(d), C.byref(w), C.byref(nnz), C.byref(tok), C.byref(vb))
+            off = np.zeros(d.value + 1, np.int64)
+            wid = np.zeros(nnz.value, np.int32)
+            cnt = np.zeros(nnz.value, np.int32)
+            buf = C.create_string_buffer(vb.value + 1)
+            L.ref_loaded_copy(h, off, wid, cnt, buf)
+            vocab_list = buf.raw[:vb.value].decode("utf-8", "surrogateescape").split("\n")[:-1]
+            return off, wid, cnt, w.value, tok.value, vocab_list
+        finally:
+            L.ref_loaded_free(h)
+
+    def save_uci_bow(self, corpus, vocab_list, docword: str, vocab: str):
+        L = self._io_sigs()
+        vb = "".join(v + "\n" for v in vocab_list).encode("utf-8", "surrogateescape")
+        self._chk(L.ref_save_uci(np.ascontiguousarray(corpus.doc_offsets, np.int64),
+                                 np.ascontiguousarray(corpus.word_ids, np.int32),
+                                 np.ascontiguousarray(corpus.counts, np.int32),
+                                 len(corpus.doc_offsets) - 1, int(corpus.n_words), vb, len(vb),
+                                 docword.encode(), vocab.encode()))
+
+    def save_checkpoint(self, path: str, phi: np.ndarray, alpha: float, beta: float):
+        L = self._io_sigs()
+        phi = np.ascontiguousarray(phi, np.float64)
+        self._chk(L.ref_save_checkpoint(path.encode(), phi.shape[0], phi.shape[1], alpha, beta,
+                                        phi))
+
+    def load_checkpoint(self, path: str):
+        L = self._io_sigs()
+        k, w, a, b = C.c_int64(), C.c_int64(), C.c_double(), C.c_double()
+        self._chk(L.ref_load_checkpoint(path.encode(), C.byref(k), C.byref(w), C.byref(a),
+                                        C.byref(b), None, 0))
+        phi = np.zeros((k.value, w.value))
+        self._chk(L.ref_load_checkpoint(path.encode(), C.byref(k), C.byref(w), C.byref(a),
+                                        C.byref(b), phi.ctypes.data, phi.size))
+        return phi, a.value, b.value
+
+    def write_metrics_csv(self, path: str, trace):
+        L = self._io_sigs()
+        rows = (_TraceRow * max(len(trace), 1))()
+        for i, r in enumerate(trace):
+            rows[i] = _TraceRow(int(r["t"]), r["passes"], r["samples_per_word"], r["ll"],
+                                r["wall_seconds"], r["m_t"])
+        self._chk(L.ref_write_metrics_csv(path.encode(), rows, len(trace)))
+
+    def read_metrics_csv(self, path: str):
+        L = self._io_sigs()
+        n = C.c_int64()
+        self._chk(L.ref_read_metrics_csv(path.encode(), None, 0, C.byref(n)))
+        rows = (_TraceRow * max(n.value, 1))()
+        self._chk(L.ref_read_metrics_csv(path.encode(), rows, n.value, C.byref(n)))
+        return _trace_to_list(rows, n.value)
 
 
 def have_ref() -> bool:

@@ -14,6 +14,7 @@
 #include <cstdint>
 #include <cstring>
 #include <exception>
+#include <string>
 #include <vector>
 
 #include "samelda/corpus.hpp"
@@ -331,6 +332,115 @@ int ref_train(const int64_t* offsets, const int32_t* words, const int32_t* count
       trace_out[i] = {trace[i].t, trace[i].passes, trace[i].samples_per_word, trace[i].ll,
                       trace[i].wall_seconds, trace[i].m_t};
     }
+  });
+}
+
+// ---- data formats: the reference's own I/O
+struct LoadedCorpus {
+  Corpus c;
+  std::string vocab;  // '\n'-terminated lines
+};
+
+void* ref_load_uci(const char* docword, const char* vocab, int* rc) {
+  LoadedCorpus* out = nullptr;
+  *rc = guarded([&] {
+    auto* l = new LoadedCorpus{load_uci_bow(docword, vocab), {}};
+    for (const auto& v : l->c.vocab) {
+      l->vocab += v;
+      l->vocab.push_back('\n');
+    }
+    out = l;
+  });
+  return out;
+}
+
+void ref_loaded_dims(void* h, int64_t* n_docs, int64_t* n_words, int64_t* nnz, int64_t* n_tokens,
+                     int64_t* vocab_bytes) {
+  auto* l = static_cast<LoadedCorpus*>(h);
+  *n_docs = l->c.n_docs;
+  *n_words = l->c.n_words;
+  *nnz = l->c.nnz();
+  *n_tokens = l->c.n_tokens;
+  *vocab_bytes = static_cast<int64_t>(l->vocab.size());
+}
+
+void ref_loaded_copy(void* h, int64_t* offsets, int32_t* words, int32_t* counts, char* vocab) {
+  auto* l = static_cast<LoadedCorpus*>(h);
+  std::memcpy(offsets, l->c.doc_offsets.data(), sizeof(int64_t) * l->c.doc_offsets.size());
+  std::memcpy(words, l->c.word_ids.data(), sizeof(int32_t) * l->c.word_ids.size());
+  std::memcpy(counts, l->c.counts.data(), sizeof(int32_t) * l->c.counts.size());
+  std::memcpy(vocab, l->vocab.data(), l->vocab.size());
+}
+
+void ref_loaded_free(void* h) { delete static_cast<LoadedCorpus*>(h); }
+
+int ref_save_uci(const int64_t* offsets, const int32_t* words, const int32_t* counts,
+                 int64_t n_docs, int64_t n_words, const char* vocab, int64_t vocab_bytes,
+                 const char* docword, const char* vocab_path) {
+  return guarded([&] {
+    Corpus c = make_corpus(offsets, words, counts, n_docs, n_words);
+    std::string cur;
+    for (int64_t i = 0; i < vocab_bytes; ++i) {
+      if (vocab[i] == '\n') {
+        c.vocab.push_back(cur);
+        cur.clear();
+      } else {
+        cur.push_back(vocab[i]);
+      }
+    }
+    save_uci_bow(c, docword, vocab_path);
+  });
+}
+
+int ref_save_checkpoint(const char* path, int64_t K, int64_t W, double alpha, double beta,
+                        const double* phi) {
+  return guarded([&] {
+    Model m;
+    m.n_topics = K;
+    m.n_words = W;
+    m.alpha = alpha;
+    m.beta = beta;
+    m.phi = DenseMatrix(K, W);
+    std::memcpy(m.phi.data.data(), phi, sizeof(double) * K * W);
+    save_checkpoint(m, path);
+  });
+}
+
+int ref_load_checkpoint(const char* path, int64_t* K, int64_t* W, double* alpha, double* beta,
+                        double* phi, int64_t cap) {
+  return guarded([&] {
+    const Model m = load_checkpoint(path);
+    *K = m.n_topics;
+    *W = m.n_words;
+    *alpha = m.alpha;
+    *beta = m.beta;
+    if (phi && cap >= m.n_topics * m.n_words)
+      std::memcpy(phi, m.phi.data.data(), sizeof(double) * m.phi.data.size());
+  });
+}
+
+struct RefTraceRow {
+  int64_t t;
+  double passes, samples_per_word, ll, wall_seconds, m_t;
+};
+
+int ref_write_metrics_csv(const char* path, const RefTraceRow* rows, int64_t n) {
+  return guarded([&] {
+    MetricsTrace tr;
+    for (int64_t i = 0; i < n; ++i)
+      tr.push_back(TraceRow{rows[i].t, rows[i].passes, rows[i].samples_per_word, rows[i].ll,
+                            rows[i].wall_seconds, rows[i].m_t});
+    write_metrics_csv(tr, path);
+  });
+}
+
+int ref_read_metrics_csv(const char* path, RefTraceRow* rows, int64_t cap, int64_t* n) {
+  return guarded([&] {
+    const MetricsTrace tr = read_metrics_csv(path);
+    *n = static_cast<int64_t>(tr.size());
+    for (int64_t i = 0; i < *n && i < cap; ++i)
+      rows[i] = RefTraceRow{tr[i].t, tr[i].passes, tr[i].samples_per_word, tr[i].ll,
+                            tr[i].wall_seconds, tr[i].m_t};
   });
 }
 

@@ -25,6 +25,7 @@ UNITS = {
     "fast_kernels.cu": [],
     "capi.cu": [],
     "synth.cpp": [],
+    "corpus_io.cpp": [],
 }
 GXX = ["-O3", "-std=c++20", "-fPIC", "-pthread", "-I", CSRC, "-I", os.path.join(ROOT, "include")]
 

@@ -123,6 +123,22 @@ SIGNATURES = [
     ("samelda_cu_model_upload", C.c_int, [_P, _P, _P]),
     ("samelda_cu_train", C.c_int, [_P, _CP, C.POINTER(_Config), _CP, _I64, _P, _P,
                                    C.POINTER(_TraceRow), _I64, C.POINTER(_I64)]),
+    # data formats (include/samelda_io.h)
+    ("samelda_io_last_error", C.c_char_p, []),
+    ("samelda_io_load_uci", C.c_int, [C.c_char_p, C.c_char_p, C.c_int, C.POINTER(C.c_void_p)]),
+    ("samelda_io_save_csr", C.c_int, [C.c_char_p, _CP, C.c_char_p, _I64]),
+    ("samelda_io_load_csr", C.c_int, [C.c_char_p, C.c_int, C.POINTER(C.c_void_p)]),
+    ("samelda_io_corpus_dims", None, [_P] + [C.POINTER(_I64)] * 6),
+    ("samelda_io_corpus_view", None, [_P, _CP, C.POINTER(C.c_void_p)]),
+    ("samelda_io_corpus_free", None, [_P]),
+    ("samelda_io_save_uci", C.c_int, [_CP, C.c_char_p, _I64, C.c_char_p, C.c_char_p]),
+    ("samelda_io_save_checkpoint", C.c_int, [C.c_char_p, _I64, _I64, _D, _D, _P]),
+    ("samelda_io_checkpoint_header", C.c_int, [C.c_char_p, C.POINTER(_I64), C.POINTER(_I64),
+                                               C.POINTER(_D), C.POINTER(_D)]),
+    ("samelda_io_load_checkpoint", C.c_int, [C.c_char_p, _P, _I64]),
+    ("samelda_io_write_metrics_csv", C.c_int, [C.c_char_p, C.POINTER(_TraceRow), _I64]),
+    ("samelda_io_read_metrics_csv", C.c_int, [C.c_char_p, C.POINTER(_TraceRow), _I64,
+                                              C.POINTER(_I64)]),
 ]
 
 _lib = None
@@ -159,6 +175,7 @@ class Corpus:
     word_ids: np.ndarray
     counts: np.ndarray
     n_words: int
+    vocab: list | None = None  # n_words tokens (corpus.hpp:23), when loaded from files
 
     def __post_init__(self):
         self.doc_offsets = np.ascontiguousarray(self.doc_offsets, np.int64)
@@ -171,7 +188,7 @@ class Corpus:
     @classmethod
     def of(cls, c) -> "Corpus":
         return c if isinstance(c, Corpus) else cls(c.doc_offsets, c.word_ids, c.counts,
-                                                   int(c.n_words))
+                                                   int(c.n_words), getattr(c, "vocab", None))
 
     @property
     def n_docs(self) -> int:
@@ -640,3 +657,121 @@ def train(corpus, config: SamplerConfig, heldout=None, eval_every: int = 0,
              for i in range(n.value)]
     return Model(K, W, config.alpha, config.beta, phi[:K * W].reshape(K, W),
                  theta[:D * K].reshape(D, K)), trace
+
+
+# ------------------------------------------------------------ data formats
+# corpus ingest, binary CSR cache, checkpoint and metrics files
+# (include/samelda_io.h)
+
+def _io_check(rc: int):
+    if rc:
+        lib = load_library()
+        msg = (lib.samelda_io_last_error() or b"").decode(errors="replace")
+        raise _CODES.get(rc, SameldaError)(msg)
+
+
+def _enc(path) -> bytes:
+    return os.fsencode(os.fspath(path))
+
+
+def _vocab_bytes(vocab, n_words: int) -> bytes:
+    if vocab is None:
+        vocab = [str(i) for i in range(n_words)]
+    return "".join(v + "\n" for v in vocab).encode("utf-8", "surrogateescape")
+
+
+def _take_io_corpus(h) -> Corpus:
+    lib = load_library()
+    try:
+        d, w, nnz, tok, vb, dropped = (C.c_int64() for _ in range(6))
+        lib.samelda_io_corpus_dims(h, C.byref(d), C.byref(w), C.byref(nnz), C.byref(tok),
+                                   C.byref(vb), C.byref(dropped))
+        view = _Corpus()
+        vptr = C.c_void_p()
+        lib.samelda_io_corpus_view(h, C.byref(view), C.byref(vptr))
+        off = np.ctypeslib.as_array(C.cast(view.doc_offsets, C.POINTER(C.c_int64)),
+                                    (d.value + 1,)).copy()
+        if nnz.value:
+            wid = np.ctypeslib.as_array(C.cast(view.word_ids, C.POINTER(C.c_int32)),
+                                        (nnz.value,)).copy()
+            cnt = np.ctypeslib.as_array(C.cast(view.counts, C.POINTER(C.c_int32)),
+                                        (nnz.value,)).copy()
+        else:
+            wid = np.zeros(0, np.int32)
+            cnt = np.zeros(0, np.int32)
+        raw = C.string_at(vptr, vb.value) if vb.value else b""
+        vocab = raw.decode("utf-8", "surrogateescape").split("\n")[:-1]
+        return Corpus(off, wid, cnt, int(w.value), vocab)
+    finally:
+        lib.samelda_io_corpus_free(h)
+
+
+def load_uci_bow(docword_path, vocab_path, n_threads: int = 0) -> Corpus:
+    """corpus.cpp:62-183 (parallel mmap parser; same result and IoErrors)."""
+    h = C.c_void_p()
+    _io_check(load_library().samelda_io_load_uci(_enc(docword_path), _enc(vocab_path),
+                                                 int(n_threads), C.byref(h)))
+    return _take_io_corpus(h)
+
+
+def save_uci_bow(corpus, docword_path, vocab_path) -> None:
+    """corpus.cpp:186-213 (same bytes)."""
+    c = Corpus.of(corpus)
+    vb = _vocab_bytes(c.vocab, c.n_words)
+    s = c._struct()
+    _io_check(load_library().samelda_io_save_uci(C.byref(s), vb, len(vb), _enc(docword_path),
+                                                 _enc(vocab_path)))
+
+
+def save_corpus_cache(corpus, path) -> None:
+    """Binary CSR cache (header + offsets + word ids + counts + vocab)."""
+    c = Corpus.of(corpus)
+    vb = _vocab_bytes(c.vocab, c.n_words)
+    s = c._struct()
+    _io_check(load_library().samelda_io_save_csr(_enc(path), C.byref(s), vb, len(vb)))
+
+
+def load_corpus_cache(path, n_threads: int = 0) -> Corpus:
+    h = C.c_void_p()
+    _io_check(load_library().samelda_io_load_csr(_enc(path), int(n_threads), C.byref(h)))
+    return _take_io_corpus(h)
+
+
+def save_checkpoint(model: Model, path) -> None:
+    """model.cpp:54-69 (same bytes; phi K x W)."""
+    phi = np.ascontiguousarray(model.phi, np.float64)
+    _io_check(load_library().samelda_io_save_checkpoint(
+        _enc(path), int(model.n_topics), int(model.n_words), float(model.alpha),
+        float(model.beta), _ptr(phi)))
+
+
+def load_checkpoint(path) -> Model:
+    """model.cpp:71-111 (same checks and IoErrors); theta is not stored."""
+    lib = load_library()
+    k, w, a, b = C.c_int64(), C.c_int64(), C.c_double(), C.c_double()
+    _io_check(lib.samelda_io_checkpoint_header(_enc(path), C.byref(k), C.byref(w), C.byref(a),
+                                               C.byref(b)))
+    phi = np.zeros((k.value, w.value))
+    _io_check(lib.samelda_io_load_checkpoint(_enc(path), _ptr(phi), phi.size))
+    return Model(int(k.value), int(w.value), a.value, b.value, phi, None)
+
+
+def write_metrics_csv(trace, path) -> None:
+    """eval.cpp:161-177 (same bytes)."""
+    rows = (_TraceRow * max(len(trace), 1))()
+    for i, r in enumerate(trace):
+        rows[i] = _TraceRow(int(r["t"]), float(r["passes"]), float(r["samples_per_word"]),
+                            float(r["ll"]), float(r["wall_seconds"]), float(r["m_t"]))
+    _io_check(load_library().samelda_io_write_metrics_csv(_enc(path), rows, len(trace)))
+
+
+def read_metrics_csv(path) -> list:
+    """eval.cpp:179-208."""
+    lib = load_library()
+    n = C.c_int64()
+    _io_check(lib.samelda_io_read_metrics_csv(_enc(path), None, 0, C.byref(n)))
+    rows = (_TraceRow * max(n.value, 1))()
+    _io_check(lib.samelda_io_read_metrics_csv(_enc(path), rows, n.value, C.byref(n)))
+    return [dict(t=rows[i].t, passes=rows[i].passes, samples_per_word=rows[i].samples_per_word,
+                 ll=rows[i].ll, wall_seconds=rows[i].wall_seconds, m_t=rows[i].m_t)
+            for i in range(n.value)]
