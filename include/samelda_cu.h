@@ -198,9 +198,10 @@ int samelda_cu_profile_read(samelda_cu_ctx* ctx, double* ms_out, int64_t* launch
                             int64_t* nnz_sampled, int64_t* docs_sampled, int64_t* deferred);
 /* copy the batch theta rows (B x K, f64, batch order) of the last period */
 int samelda_cu_batch_theta(samelda_cu_ctx* ctx, double* out, int64_t cap);
-/* the same copy, enqueued on the context stream without a host wait: `out`
- * (page-locked for the copy to overlap later periods) holds the rows after
- * samelda_cu_synchronize or any other synchronising call. */
+/* the same copy without a host wait: the rows are gathered on the context
+ * stream and copied on a context-owned copy stream, so the transfer overlaps
+ * the next periods' kernels (two row buffers rotate); `out` (page-locked)
+ * holds the rows after samelda_cu_synchronize or a device-wide synchronize. */
 int samelda_cu_batch_theta_async(samelda_cu_ctx* ctx, double* out, int64_t cap);
 /* sums of the last sweep's integer theta and phi counts (mass balance) */
 int samelda_cu_count_totals(samelda_cu_ctx* ctx, int64_t* theta_total, int64_t* phi_total);

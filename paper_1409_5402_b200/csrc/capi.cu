@@ -311,6 +311,14 @@ struct samelda_cu_ctx {
   };
   Staging stg[2];
   int stg_next = 0;
+  // batch-theta read-back (samelda_cu_batch_theta_async): the D2H copy runs
+  // on its own stream so it overlaps the next period's kernels; two row
+  // buffers, each reused only after its previous copy has finished
+  cudaStream_t copy_stream = nullptr;
+  DevBuf rows2[2];
+  cudaEvent_t rows_ready[2] = {nullptr, nullptr};
+  cudaEvent_t rows_copied[2] = {nullptr, nullptr};
+  int rows_next = 0;
   // sticky device error flag, read back asynchronously after each period
   int* h_err = nullptr;
   cudaEvent_t err_event = nullptr;
@@ -329,6 +337,14 @@ struct samelda_cu_ctx {
     }
     if (h_err) cudaFreeHost(h_err);
     if (err_event) cudaEventDestroy(err_event);
+    for (int i = 0; i < 2; ++i) {
+      if (rows_ready[i]) cudaEventDestroy(rows_ready[i]);
+      if (rows_copied[i]) cudaEventDestroy(rows_copied[i]);
+    }
+    if (copy_stream) {
+      cudaStreamSynchronize(copy_stream);
+      cudaStreamDestroy(copy_stream);
+    }
     if (own_stream) cudaStreamDestroy(own_stream);
   }
 
@@ -647,6 +663,7 @@ int samelda_cu_use_own_stream(samelda_cu_ctx* ctx) {
 int samelda_cu_synchronize(samelda_cu_ctx* ctx) {
   return guarded(ctx, [&] {
     ck(cudaStreamSynchronize(ctx->stream), "synchronize");
+    if (ctx->copy_stream) ck(cudaStreamSynchronize(ctx->copy_stream), "synchronize copies");
     ctx->poll_err(true, "period");
   });
 }
@@ -1121,11 +1138,27 @@ int samelda_cu_batch_theta_async(samelda_cu_ctx* ctx, double* out, int64_t cap) 
     if (!ctx->model_ready) fail(SAMELDA_CU_CONFIG, "no model");
     const int64_t n = ctx->B * ctx->K;
     if (cap < n) fail(SAMELDA_CU_CONFIG, "batch_theta: buffer too small");
-    double* rows = ensure<double>(ctx->theta_rows, n);
+    if (n == 0) return;
+    if (!ctx->copy_stream) {
+      ck(cudaStreamCreateWithFlags(&ctx->copy_stream, cudaStreamNonBlocking), "copy stream");
+      for (int i = 0; i < 2; ++i) {
+        ck(cudaEventCreateWithFlags(&ctx->rows_ready[i], cudaEventDisableTiming), "event");
+        ck(cudaEventCreateWithFlags(&ctx->rows_copied[i], cudaEventDisableTiming), "event");
+        ck(cudaEventRecord(ctx->rows_copied[i], ctx->copy_stream), "event");
+      }
+    }
+    const int i = ctx->rows_next;
+    ctx->rows_next ^= 1;
+    // rows2[i] may still be the source of the copy two calls ago
+    ck(cudaStreamWaitEvent(ctx->stream, ctx->rows_copied[i], 0), "wait copy");
+    double* rows = ensure<double>(ctx->rows2[i], n);
     ctx->launches += scu::launch_gather_theta(ctx->theta.as<double>(), ctx->batch.as<int32_t>(), ctx->B, ctx->K,
                                               rows, nullptr, ctx->stream);
-    if (n > 0)
-      ck(cudaMemcpyAsync(out, rows, sizeof(double) * n, cudaMemcpyDeviceToHost, ctx->stream), "download rows");
+    ck(cudaEventRecord(ctx->rows_ready[i], ctx->stream), "rows ready");
+    ck(cudaStreamWaitEvent(ctx->copy_stream, ctx->rows_ready[i], 0), "wait rows");
+    ck(cudaMemcpyAsync(out, rows, sizeof(double) * n, cudaMemcpyDeviceToHost, ctx->copy_stream),
+       "download rows");
+    ck(cudaEventRecord(ctx->rows_copied[i], ctx->copy_stream), "rows copied");
   });
 }
 

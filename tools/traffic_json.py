@@ -1,0 +1,34 @@
+"""profiles/sample_kernel_traffic.json from an ncu launch list (DRAM bytes of
+the sampling launch group k_sample_v2 + k_deferred_expand + k_deferred_draw,
+averaged per launch).  usage: python tools/traffic_json.py launches.csv [config]"""
+import csv
+import json
+import os
+import sys
+from collections import defaultdict
+
+path = sys.argv[1]
+config = sys.argv[2] if len(sys.argv) > 2 else "nytimes"
+rows = [r for r in csv.reader(open(path)) if len(r) > 10]
+hdr = rows[0]
+ik, iid, im, iv = (hdr.index(x) for x in ("Kernel Name", "ID", "Metric Name", "Metric Value"))
+per = defaultdict(lambda: defaultdict(dict))
+for r in rows[1:]:
+    name = r[ik].split("(")[0].replace("scu::<unnamed>::", "").replace("void ", "").split("<")[0]
+    per[name][r[iid]][r[im]] = float(r[iv].replace(",", ""))
+group = ["k_sample_v2", "k_deferred_expand", "k_deferred_draw"]
+out = {"_doc": "DRAM traffic (dram__bytes_read.sum + dram__bytes_write.sum) per sampling launch "
+               "group (" + " + ".join(group) + "), averaged over the launches in " + path +
+               "; bench.py reports it as roofline.traffic.", config: {"source": path}}
+total = 0.0
+for k in group:
+    launches = per.get(k, {})
+    if not launches:
+        continue
+    rd = sum(v.get("dram__bytes_read.sum", 0) for v in launches.values()) / len(launches)
+    wr = sum(v.get("dram__bytes_write.sum", 0) for v in launches.values()) / len(launches)
+    t = sum(v.get("gpu__time_duration.sum", 0) for v in launches.values()) / len(launches)
+    out[config][k] = {"read": int(rd), "write": int(wr), "mean_ns": int(t), "launches": len(launches)}
+    total += rd + wr
+out[config]["dram_bytes_per_launch"] = int(total)
+print(json.dumps(out, indent=1))
