@@ -14,7 +14,7 @@ hdr = rows[0]
 ik, iid, im, iv = (hdr.index(x) for x in ("Kernel Name", "ID", "Metric Name", "Metric Value"))
 per = defaultdict(lambda: defaultdict(dict))
 for r in rows[1:]:
-    name = r[ik].split("(")[0].replace("scu::<unnamed>::", "").replace("void ", "").split("<")[0]
+    name = r[ik].split("(")[0].split("<")[0].split("::")[-1].replace("void ", "").strip()
     per[name][r[iid]][r[im]] = float(r[iv].replace(",", ""))
 group = ["k_sample_v2", "k_deferred_expand", "k_deferred_draw"]
 out = {"_doc": "DRAM traffic (dram__bytes_read.sum + dram__bytes_write.sum) per sampling launch "
