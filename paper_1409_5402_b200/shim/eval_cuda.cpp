@@ -1,10 +1,9 @@
 // eval_cuda.cpp -- drop-in replacement for the reference's src/eval.cpp.
 //
 // fold_in_theta and perword_loglik run on the device through the C ABI
-// (include/samelda_cu.h); the metrics-CSV pair is the reference's host file
-// format (eval.hpp:45-49: header "t,passes,samples_per_word,ll,wall_seconds,m_t",
-// %.17g fields) restated here because this translation unit replaces eval.cpp
-// as a whole.
+// (include/samelda_cu.h); the metrics-CSV pair (eval.hpp:45-49) goes through
+// the library's host formats (include/samelda_io.h), since this translation
+// unit replaces eval.cpp as a whole.
 #include <cstdio>
 #include <cstdlib>
 #include <fstream>
@@ -15,6 +14,7 @@
 #include "samelda/errors.hpp"
 #include "samelda/eval.hpp"
 #include "samelda_cu.h"
+#include "samelda_io.h"
 
 namespace samelda {
 namespace cuda_shim {
@@ -53,40 +53,26 @@ double perword_loglik(const DenseMatrix& phi, const Corpus& test_corpus, double 
   return ll;
 }
 
+// eval.cpp:161-210 -- the metrics-CSV pair through include/samelda_io.h
+// (byte-identical files, same IoErrors)
 void write_metrics_csv(const MetricsTrace& trace, const std::string& path) {
-  std::ofstream out(path);
-  if (!out) throw IoError("cannot write metrics csv: " + path);
-  out << "t,passes,samples_per_word,ll,wall_seconds,m_t\n";
-  char line[256];
-  for (const auto& row : trace) {
-    std::snprintf(line, sizeof(line), "%lld,%.17g,%.17g,%.17g,%.17g,%.17g\n",
-                  static_cast<long long>(row.t), row.passes, row.samples_per_word, row.ll,
-                  row.wall_seconds, row.m_t);
-    out << line;
-  }
-  if (!out) throw IoError("write failed: " + path);
+  std::vector<samelda_cu_trace_row> rows(trace.size());
+  for (std::size_t i = 0; i < trace.size(); ++i)
+    rows[i] = {trace[i].t, trace[i].passes, trace[i].samples_per_word, trace[i].ll,
+               trace[i].wall_seconds, trace[i].m_t};
+  if (samelda_io_write_metrics_csv(path.c_str(), rows.data(), static_cast<int64_t>(rows.size())))
+    throw IoError(samelda_io_last_error());
 }
 
 MetricsTrace read_metrics_csv(const std::string& path) {
-  std::ifstream in(path);
-  if (!in) throw IoError("cannot open metrics csv: " + path);
-  std::string header;
-  if (!std::getline(in, header) || header != "t,passes,samples_per_word,ll,wall_seconds,m_t")
-    throw IoError("unexpected metrics csv header in " + path);
+  int64_t n = 0;
+  if (samelda_io_read_metrics_csv(path.c_str(), nullptr, 0, &n)) throw IoError(samelda_io_last_error());
+  std::vector<samelda_cu_trace_row> rows(static_cast<std::size_t>(n));
+  if (samelda_io_read_metrics_csv(path.c_str(), rows.data(), n, &n))
+    throw IoError(samelda_io_last_error());
   MetricsTrace trace;
-  std::string line;
-  while (std::getline(in, line)) {
-    if (line.empty()) continue;
-    TraceRow row;
-    char* end = nullptr;
-    row.t = std::strtoll(line.c_str(), &end, 10);
-    double* fields[] = {&row.passes, &row.samples_per_word, &row.ll, &row.wall_seconds, &row.m_t};
-    for (double* f : fields) {
-      if (*end != ',') throw IoError("malformed metrics csv row in " + path);
-      *f = std::strtod(end + 1, &end);
-    }
-    trace.push_back(row);
-  }
+  for (const auto& r : rows)
+    trace.push_back(TraceRow{r.t, r.passes, r.samples_per_word, r.ll, r.wall_seconds, r.m_t});
   return trace;
 }
 
