@@ -5,7 +5,7 @@ set -e
 cd "$(dirname "$0")/.."
 P=paper_1409_5402_b200
 mkdir -p /tmp/samelda_stats
-nvcc -gencode arch=compute_100a,code=sm_100a -O3 -lineinfo -std=c++17 -Xcompiler -fPIC \
+nvcc -gencode arch=compute_100a,code=sm_100a -O3 -lineinfo -std=c++20 -Xcompiler -fPIC \
   -I $P/csrc -I include -fmad=false -DSAMELDA_DEFER_STATS -c $P/csrc/kernels.cu -o /tmp/samelda_stats/kernels.o
 nvcc -gencode arch=compute_100a,code=sm_100a -shared -o $P/libsamelda_cuda_stats.so \
-  /tmp/samelda_stats/kernels.o $P/_build/capi.o $P/_build/synth.o -lpthread
+  /tmp/samelda_stats/kernels.o $P/_build/capi.o $P/_build/synth.o $P/_build/corpus_io.o -lpthread
