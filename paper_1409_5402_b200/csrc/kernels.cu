@@ -1158,7 +1158,10 @@ __global__ void __launch_bounds__(kFastBlock, MINB) k_sample_v2(
         for (int o = 16; o > 0; o >>= 1) mu_f = __fadd_rn(mu_f, __shfl_xor_sync(0xffffffffu, mu_f, o));
       }
       const bool nz_exact = !(mu_f >= 1e-20f) || isinf(mu_f);
-      const float scale = __fdividef(__double2float_rn(__dmul_rn(m_t, static_cast<double>(ci))), mu_f);
+      // an unusable mu defers the whole nonzero: scale = NaN makes every
+      // lambda fail the lambda < kInvMax eligibility test (no per-draw flag)
+      const float scale = nz_exact ? __int_as_float(0x7fffffff)
+                                   : __fdividef(__double2float_rn(__dmul_rn(m_t, static_cast<double>(ci))), mu_f);
       // band slope per nonzero: M = prod (3.3e-6 scale) + 2e-6 is within 2.4e-7
       // relative of 3.3e-6 lambda + 2e-6 >= 3.24e-6 lambda + 1.93e-6 >= m_0..2
       const float mslope = __fmul_rn(scale, 3.3e-6f);
@@ -1189,7 +1192,7 @@ __global__ void __launch_bounds__(kFastBlock, MINB) k_sample_v2(
         for (int jj = 0; jj < KG; ++jj) {
           const int j = g + jj;
           const float lam = __fmul_rn(prod[j], scale);
-          bool und = nz_exact || !(prod[j] >= 1e-30f) || !(lam < kInvMax);
+          bool und = !(prod[j] >= 1e-30f) || !(lam < kInvMax);
           const float u = __fsub_rn(__int_as_float(0x3f800000 | (y[jj] >> 9)), 1.0f);
           float t1, c2;
           const float M = __fmaf_rn(prod[j], mslope, 2e-6f);
