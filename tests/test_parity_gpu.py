@@ -464,3 +464,98 @@ def test_train_sliced_k_bit_exact(port, K):
     np.testing.assert_array_equal(model.phi, ophi)
     np.testing.assert_array_equal(model.theta, otheta)
     np.testing.assert_allclose([r["ll"] for r in trace], [r["ll"] for r in otrace], rtol=1e-12)
+
+
+# ------------------- statistical / invariance cases (test_sampler.cpp, test_eval.cpp)
+
+def _greedy_matched_mean_tv(phi, phi_true):
+    """tests/support/oracles.cpp greedy_matched_mean_tv: rows paired greedily by
+    smallest total-variation distance, mean over the pairs."""
+    tv = 0.5 * np.abs(phi[:, None, :] - phi_true[None, :, :]).sum(-1)
+    used_a, used_b, total = set(), set(), []
+    for flat in np.argsort(tv, axis=None):
+        a, b = divmod(int(flat), tv.shape[1])
+        if a in used_a or b in used_b:
+            continue
+        used_a.add(a)
+        used_b.add(b)
+        total.append(tv[a, b])
+    return float(np.mean(total))
+
+
+def test_learned_topics_approach_generating_ones(port):
+    """test_sampler.cpp:439-454 (10 passes, K=5, m=100, bf=0.05)."""
+    g = port.make_corpus(2000, 100, 5, 50.0, 817)
+    model, _ = S.train(g, S.SamplerConfig(n_topics=5, m=100.0, batch_fraction=0.05, t_max=200,
+                                          seed=4))
+    assert _greedy_matched_mean_tv(model.phi, g.phi_true) < 0.15
+
+
+def test_larger_replica_counts_shrink_estimator_variance():
+    """test_sampler.cpp:456-479: spread of phi(0,0) over 100 seeds falls as
+    m rises 1 -> 10 -> 100."""
+    c = S.Corpus(np.array([0, 2]), np.array([0, 1], np.int32), np.array([2, 1], np.int32), 2)
+    spread = []
+    for m in (1.0, 10.0, 100.0):
+        est = [S.train(c, S.SamplerConfig(n_topics=2, m=m, t_max=1, batch_fraction=1.0,
+                                          inner_sweeps=1, seed=run))[0].phi[0, 0]
+               for run in range(100)]
+        spread.append(np.var(est))
+    assert spread[0] > spread[1] > spread[2]
+
+
+def test_fold_in_fixed_point(port):
+    """test_eval.cpp:41-50: 60 and 200 sweeps agree to 1e-10."""
+    g = port.make_corpus(1, 10, 3, 40.0, 61)
+    w = g.word_ids[g.doc_offsets[0]:g.doc_offsets[1]]
+    c = g.counts[g.doc_offsets[0]:g.doc_offsets[1]]
+    a = S.fold_in_theta(g.phi_true, w, c, 0.1, 60)
+    b = S.fold_in_theta(g.phi_true, w, c, 0.1, 200)
+    assert np.abs(a - b).max() < 1e-10
+    np.testing.assert_array_equal(a, port.fold_in_theta(g.phi_true, w, c, 0.1, 60))
+
+
+def test_scaling_counts_leaves_the_score_unchanged(port):
+    """test_eval.cpp:67-94."""
+    g = port.make_corpus(10, 12, 3, 9.0, 72)
+    doubled = S.Corpus(g.doc_offsets, g.word_ids, g.counts * 2, g.n_words)
+    uniform = np.full((3, 12), 1.0 / 12)
+    assert S.perword_loglik(uniform, g, 0.1, 5) == S.perword_loglik(uniform, doubled, 0.1, 5)
+    big = port.make_corpus(100, 20, 3, 80.0, 72)
+    big2 = S.Corpus(big.doc_offsets, big.word_ids, big.counts * 2, big.n_words)
+    base = S.perword_loglik(big.phi_true, big, 0.1, 5)
+    scaled = S.perword_loglik(big.phi_true, big2, 0.1, 5)
+    assert abs(base - scaled) < 0.05 and base <= 0.0 and scaled <= 0.0
+    assert base == pytest.approx(port.perword_loglik(big.phi_true, big, 0.1, 5), rel=1e-12)
+
+
+def test_generating_model_beats_uniform(port):
+    """test_eval.cpp:96-105."""
+    g = port.make_corpus(200, 40, 4, 30.0, 73)
+    _, te = port.split_holdout(g, 0.25, 7)
+    ll_true = S.perword_loglik(g.phi_true, te, 0.1, 11)
+    ll_uniform = S.perword_loglik(np.full((4, 40), 0.025), te, 0.1, 11)
+    assert ll_true > ll_uniform and ll_true <= 0.0
+    assert ll_uniform == pytest.approx(-math.log(40.0), rel=1e-9)
+
+
+def test_evaluation_is_pure_and_repeatable(port):
+    """test_eval.cpp:107-114 (n_threads cannot change the result; phi untouched)."""
+    g = port.make_corpus(25, 10, 2, 8.0, 74)
+    before = g.phi_true.copy()
+    a = S.perword_loglik(g.phi_true, g, 0.1, 9, 1)
+    b = S.perword_loglik(g.phi_true, g, 0.1, 9, 3)
+    assert a == b
+    np.testing.assert_array_equal(g.phi_true, before)
+
+
+def test_eval_long_documents_multi_chunk(port):
+    """k_eval_cta walks cells in chunks of 256 threads: documents with several
+    hundred distinct words, K=256, against the oracle (eval.cpp:75-159)."""
+    g = port.make_corpus(24, 3000, 6, 900.0, 5)
+    assert np.diff(g.doc_offsets).max() > 512  # three 256-cell chunks
+    rng = np.random.default_rng(8)
+    phi = rng.gamma(0.3, 1.0, size=(256, g.n_words)) + 1e-12
+    phi /= phi.sum(1, keepdims=True)
+    ll = S.perword_loglik(phi, g, 0.1, 13)
+    assert ll == pytest.approx(port.perword_loglik(phi, g, 0.1, 13), rel=1e-12, abs=0)
