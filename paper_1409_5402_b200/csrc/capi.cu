@@ -393,7 +393,13 @@ struct samelda_cu_ctx {
     ck(cudaMemcpyAsync(&h, err.p, sizeof(int), cudaMemcpyDeviceToHost, stream), "read error flag");
     ck(cudaStreamSynchronize(stream), what);
     ck(cudaGetLastError(), what);
-    if (h & scu::kErrNumerical) fail(SAMELDA_CU_NUMERICAL, "%s: nonfinite or negative value", what);
+    if (h & scu::kErrNumerical) {
+      // reported here, once: a stale flag must not surface as a later
+      // period's error (the period path reads the same sticky flag)
+      ck(cudaMemsetAsync(err.p, 0, sizeof(int), stream), "reset error flag");
+      ck(cudaStreamSynchronize(stream), what);
+      fail(SAMELDA_CU_NUMERICAL, "%s: nonfinite or negative value", what);
+    }
   }
 
   Staging& stage(int64_t B_) {

@@ -6,6 +6,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <algorithm>
 #include <cstdlib>
 
 #include "kernels.cuh"
@@ -2145,6 +2146,185 @@ __global__ void __launch_bounds__(kEvalCtaThreads) k_eval_cta(
   }
 }
 
+// k_eval_stage: k_eval_cta with a document's first R fold rows staged in
+// shared memory once per document, so the 2 x sweeps row reads of those cells
+// come from shared memory instead of L2 (the fold-in is L2-bound: 845 GB at
+// NYTimes shape).  Fold cells (fold count > 0; a zero-count cell adds exactly
+// +0, eval.cpp:43-47) are compacted per window of <= kEvalFoldMax in cell
+// order; arithmetic and order are k_eval_cta's (eval.cpp:19-64):
+//   phase 1, thread = fold cell: sequential-k mu, scale = c / mu (or skip);
+//   phase 2, thread = topic: next[k] += (scale theta[k]) phi[w][k] in fold order;
+//   phase 3: sequential total (one thread), theta = next / total, max |delta|.
+// Staged rows use an odd stride (K | 1 doubles): the thread-per-cell dots hit
+// distinct banks.
+constexpr int kEvalFoldMax = 1024;
+
+__device__ __forceinline__ double seq_dot_stride1(const double* __restrict__ th,
+                                                  const double* row, int K) {
+  double dot = 0.0;
+#pragma unroll 8
+  for (int k = 0; k < K; ++k) dot = __dadd_rn(dot, __dmul_rn(th[k], row[k]));
+  return dot;
+}
+
+__global__ void __launch_bounds__(kEvalCtaThreads) k_eval_stage(
+    const int64_t* __restrict__ doc_offsets, const int32_t* __restrict__ word_ids,
+    const int32_t* __restrict__ fold_counts, const int32_t* __restrict__ score_counts,
+    int64_t n_docs, const double* __restrict__ phi_wk, int K, double alpha, int sweeps,
+    int R, double* __restrict__ doc_logp, int64_t* __restrict__ doc_scored,
+    double* __restrict__ theta_out, int* __restrict__ err) {
+  extern __shared__ double smem[];
+  const int KP = K | 1;
+  double* th = smem;                     // K
+  double* nx = th + K;                   // K
+  double* fs = nx + K;                   // [kEvalFoldMax] scale per fold cell
+  int32_t* fw = reinterpret_cast<int32_t*>(fs + kEvalFoldMax);  // word per fold cell
+  int32_t* fc = fw + kEvalFoldMax;                              // fold count per fold cell
+  double* rows = reinterpret_cast<double*>(fc + kEvalFoldMax);   // R x KP staged rows
+  __shared__ double s_red[kEvalCtaThreads / 32];
+  __shared__ int s_wc[kEvalCtaThreads / 32];
+  __shared__ int64_t s_cnt[kEvalCtaThreads];
+  __shared__ double s_total;
+  __shared__ int s_done;
+  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  const double inv_k = 1.0 / static_cast<double>(K);
+
+  for (int64_t doc = blockIdx.x; doc < n_docs; doc += gridDim.x) {
+    const int64_t base = doc_offsets[doc];
+    const int64_t n = doc_offsets[doc + 1] - base;
+    // compact the fold cells of cells [c_begin, ...) into fw/fc, whole chunks
+    // of 256 cells while they fit; returns the first cell not taken
+    auto build = [&](int64_t c_begin, int& nf) -> int64_t {
+      nf = 0;
+      int64_t c0 = c_begin;
+      while (c0 < n && nf + kEvalCtaThreads <= kEvalFoldMax) {
+        const int64_t c = c0 + tid;
+        const int32_t f = c < n ? __ldg(fold_counts + base + c) : 0;
+        const unsigned bal = __ballot_sync(0xffffffffu, f > 0);
+        if (lane == 0) s_wc[wid] = __popc(bal);
+        __syncthreads();
+        int before = 0, total = 0;
+#pragma unroll
+        for (int w = 0; w < kEvalCtaThreads / 32; ++w) {
+          before += w < wid ? s_wc[w] : 0;
+          total += s_wc[w];
+        }
+        if (f > 0) {
+          const int pos = nf + before + __popc(bal & ((1u << lane) - 1u));
+          fw[pos] = __ldg(word_ids + base + c);
+          fc[pos] = f;
+        }
+        nf += total;
+        c0 += kEvalCtaThreads;
+        __syncthreads();
+      }
+      return c0;
+    };
+    int nf0 = 0;
+    const int64_t end0 = build(0, nf0);
+    const bool multi = end0 < n;
+    const int Reff = min(nf0, R);
+    for (int i = tid; i < Reff * K; i += kEvalCtaThreads) {
+      const int f = i / K, k = i - f * K;
+      rows[f * KP + k] = __ldg(phi_wk + static_cast<int64_t>(fw[f]) * K + k);
+    }
+    for (int k = tid; k < K; k += kEvalCtaThreads) th[k] = inv_k;
+    __syncthreads();
+    for (int sweep = 0; sweep < sweeps && n > 0; ++sweep) {
+      for (int k = tid; k < K; k += kEvalCtaThreads) nx[k] = alpha;
+      int64_t cw0 = 0;
+      bool first = true;
+      while (cw0 < n) {
+        int nf = nf0;
+        int64_t cnext = end0;
+        if (multi) cnext = build(cw0, nf);  // lists of later windows overwrite window 0's
+        const int rs = first ? Reff : 0;     // staged rows belong to window 0
+        for (int f0 = 0; f0 < nf; f0 += kEvalCtaThreads) {
+          const int f = f0 + tid;
+          if (f < nf) {
+            const double mu = f < rs ? seq_dot_stride1(th, rows + f * KP, K)
+                                     : seq_dot(th, phi_wk + static_cast<int64_t>(fw[f]) * K, K);
+            fs[f] = mu > 0.0 ? __ddiv_rn(static_cast<double>(fc[f]), mu) : 0.0;
+          }
+        }
+        __syncthreads();
+        for (int k = tid; k < K; k += kEvalCtaThreads) {
+          double acc = nx[k];
+          const double tk = th[k];
+          // branch-free (scale 0 adds +0 exactly), loads batch across iterations
+#pragma unroll 8
+          for (int f = 0; f < rs; ++f)
+            acc = __dadd_rn(acc, __dmul_rn(__dmul_rn(fs[f], tk), rows[f * KP + k]));
+#pragma unroll 8
+          for (int f = rs; f < nf; ++f)
+            acc = __dadd_rn(acc, __dmul_rn(__dmul_rn(fs[f], tk),
+                                           __ldg(phi_wk + static_cast<int64_t>(fw[f]) * K + k)));
+          nx[k] = acc;
+        }
+        __syncthreads();
+        cw0 = cnext;
+        first = false;
+      }
+      if (tid == 0) {
+        double total = 0.0;
+        for (int k = 0; k < K; ++k) total = __dadd_rn(total, nx[k]);
+        s_total = total;
+      }
+      __syncthreads();
+      const double total = s_total;
+      double delta = 0.0;
+      for (int k = tid; k < K; k += kEvalCtaThreads) {
+        const double v = __ddiv_rn(nx[k], total);
+        delta = fmax(delta, fabs(__dadd_rn(v, -th[k])));
+        th[k] = v;
+      }
+      delta = warp_max(delta);
+      if (lane == 0) s_red[wid] = delta;
+      __syncthreads();
+      if (tid == 0) {
+        double d = s_red[0];
+        for (int w = 1; w < kEvalCtaThreads / 32; ++w) d = fmax(d, s_red[w]);
+        s_done = d < 1e-12;
+      }
+      __syncthreads();
+      if (s_done) break;
+    }
+    // score the held-back half (eval.cpp:125-145), log p summed in cell order
+    double logp = 0.0;
+    int64_t scored = 0;
+    for (int64_t i0 = 0; i0 < n; i0 += kEvalCtaThreads) {
+      const int n_here = static_cast<int>(min(static_cast<int64_t>(kEvalCtaThreads), n - i0));
+      if (tid < n_here) {
+        const int64_t i = base + i0 + tid;
+        const int32_t sc = __ldg(score_counts + i);
+        double term = 0.0;
+        if (sc != 0) {
+          const double pr = seq_dot(th, phi_wk + static_cast<int64_t>(__ldg(word_ids + i)) * K, K);
+          if (!(pr > 0.0)) atomicOr(err, kErrNumerical);
+          term = __dmul_rn(static_cast<double>(sc), log(pr));
+        }
+        fs[tid] = term;
+        s_cnt[tid] = sc;
+      }
+      __syncthreads();
+      if (tid == 0)
+        for (int c = 0; c < n_here; ++c)
+          if (s_cnt[c] != 0) {
+            logp = __dadd_rn(logp, fs[c]);
+            scored += s_cnt[c];
+          }
+      __syncthreads();
+    }
+    if (tid == 0) {
+      doc_logp[doc] = logp;
+      doc_scored[doc] = scored;
+    }
+    if (theta_out)
+      for (int k = tid; k < K; k += kEvalCtaThreads) theta_out[doc * K + k] = th[k];
+    __syncthreads();
+  }
+}
+
 __global__ void k_ordered_ll(const double* __restrict__ doc_logp,
                              const int64_t* __restrict__ doc_scored, int64_t n_docs,
                              double* __restrict__ ll_out, int* __restrict__ err) {
@@ -2371,7 +2551,34 @@ int launch_eval_docs(const int64_t* doc_offsets, const int32_t* word_ids,
                      int64_t* doc_scored, double* theta_out, double* scratch,
                      int64_t scratch_doubles, int* err, cudaStream_t st) {
   if (n_docs == 0) return 0;
-  if (K <= kEvalCtaMaxK && !getenv("SAMELDA_EVAL_WARP")) {
+  const char* ev = getenv("SAMELDA_EVAL");  // A/B: "cta", "warp"; default staged
+  if (K <= 1024 && !(ev && (ev[0] == 'c' || ev[0] == 'w')) && !getenv("SAMELDA_EVAL_WARP")) {
+    // staged rows: 3 CTAs per SM share (almost) all of shared memory
+    // (measured: 1 / 2 / 3 CTAs 176 / 148 / 139 ms at NYTimes shape;
+    // SAMELDA_EVAL_CTAS_PER_SM overrides)
+    const char* cps_env = getenv("SAMELDA_EVAL_CTAS_PER_SM");
+    const int cps = cps_env ? max(1, atoi(cps_env)) : 3;
+    const int KP = K | 1;
+    const size_t fixed = (2 * static_cast<size_t>(K) + kEvalFoldMax) * sizeof(double) +
+                         2 * kEvalFoldMax * sizeof(int32_t);
+    const size_t budget = (220u * 1024u) / static_cast<size_t>(cps);
+    if (budget > fixed + static_cast<size_t>(KP) * sizeof(double)) {
+      const int R = static_cast<int>(std::min<size_t>((budget - fixed) / (KP * sizeof(double)), static_cast<size_t>(kEvalFoldMax)));
+      const size_t smem_s = fixed + static_cast<size_t>(R) * KP * sizeof(double);
+      static size_t configured_s = 48 * 1024;
+      if (smem_s > configured_s) {
+        cudaFuncSetAttribute(k_eval_stage, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             static_cast<int>(220 * 1024));
+        configured_s = 220 * 1024;
+      }
+      const int64_t blocks = min(n_docs, static_cast<int64_t>(148 * cps));
+      k_eval_stage<<<static_cast<unsigned>(blocks), kEvalCtaThreads, smem_s, st>>>(
+          doc_offsets, word_ids, fold_counts, score_counts, n_docs, phi_wk, K, alpha, sweeps, R,
+          doc_logp, doc_scored, theta_out, err);
+      return 1;
+    }
+  }
+  if (K <= kEvalCtaMaxK && !(ev && ev[0] == 'w') && !getenv("SAMELDA_EVAL_WARP")) {
     const size_t smem_c = (2 * static_cast<size_t>(K) + kEvalCtaThreads) * sizeof(double) +
                           kEvalCtaThreads * sizeof(int32_t);
     static size_t configured_c = 48 * 1024;

@@ -559,3 +559,16 @@ def test_eval_long_documents_multi_chunk(port):
     phi /= phi.sum(1, keepdims=True)
     ll = S.perword_loglik(phi, g, 0.1, 13)
     assert ll == pytest.approx(port.perword_loglik(phi, g, 0.1, 13), rel=1e-12, abs=0)
+
+
+def test_reported_eval_error_does_not_leak_into_training(port):
+    """A NumericalError raised by perword_loglik is reported once: the next
+    training run on the same context starts with a clean device flag."""
+    g = port.make_corpus(20, 8, 2, 12.0, 71)
+    ctx = S.Context(0)
+    with pytest.raises(S.NumericalError):
+        S.perword_loglik(np.zeros((2, 8)), g, 0.1, 3, ctx=ctx)
+    model, _ = S.train(g, S.SamplerConfig(n_topics=2, m=5.0, t_max=2, batch_fraction=1.0, seed=1),
+                       ctx=ctx)
+    ophi, _, _ = port.train(g, TrainConfig(n_topics=2, m=5.0, t_max=2, batch_fraction=1.0, seed=1))
+    np.testing.assert_array_equal(model.phi, ophi)

@@ -1,5 +1,6 @@
-"""Held-out evaluation (perword_loglik) timing on the bench workload, for the
-CTA-per-document kernel and the warp-per-document one (SAMELDA_EVAL_WARP=1).
+"""Held-out evaluation (perword_loglik) timing on the bench workload: the
+staged-row kernel (1, 2, 3 CTAs per SM), the CTA-per-document kernel and the
+warp-per-document one (SAMELDA_EVAL=cta|warp).
 
     python tools/eval_timing.py [--config nytimes] [--periods 6]
 """
@@ -28,11 +29,14 @@ for t in range(args.periods):
     tr.period(stream.next(), t, cfg["m"], S.rho_schedule(t, 1.0, 0.5))
 tr.ctx.synchronize()
 res = {}
-for name, env in (("cta", None), ("warp", "1")):
-    if env:
-        os.environ["SAMELDA_EVAL_WARP"] = env
-    else:
-        os.environ.pop("SAMELDA_EVAL_WARP", None)
+variants = (("stage3", {}), ("stage1", {"SAMELDA_EVAL_CTAS_PER_SM": "1"}),
+            ("stage2", {"SAMELDA_EVAL_CTAS_PER_SM": "2"}),
+            ("stage4", {"SAMELDA_EVAL_CTAS_PER_SM": "4"}), ("cta", {"SAMELDA_EVAL": "cta"}),
+            ("warp", {"SAMELDA_EVAL": "warp"}))
+for name, env in variants:
+    for key in ("SAMELDA_EVAL", "SAMELDA_EVAL_CTAS_PER_SM"):
+        os.environ.pop(key, None)
+    os.environ.update(env)
     tr.evaluate()  # warm (split computed once)
     t0 = time.perf_counter()
     ll = tr.evaluate()
@@ -40,4 +44,4 @@ for name, env in (("cta", None), ("warp", "1")):
     res[name] = ll
     print(f"{name}: ll={ll!r} {dt * 1e3:.2f} ms  (test docs {heldout.n_docs}, nnz {heldout.nnz})",
           flush=True)
-print("rel diff", abs(res["cta"] - res["warp"]) / abs(res["warp"]))
+print("max rel diff vs warp", max(abs(v - res["warp"]) / abs(res["warp"]) for v in res.values()))
