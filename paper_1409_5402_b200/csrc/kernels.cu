@@ -1033,29 +1033,42 @@ __device__ __forceinline__ uint32_t fast_poisson3(float lam, float M, float Mb, 
   return __float_as_uint(__fadd_rn(zf, 8388608.0f)) - 0x4B000000u;
 }
 
-// sequential search from k = 3 (u beyond cdf_2 + M): fast_poisson's loop,
-// same arithmetic and bound; returns z or sets *und
+// sequential search from k = 3 (u beyond cdf_2 + M): fast_poisson's loop and
+// bound, with 1/k and the bound's k-term r_k - r_0 = 1.2e-6 + 6e-7 (k - 2)
+// read from constant tables (the step index is the same for every lane still
+// searching: one broadcast load) instead of rcp.approx and running sums; the
+// correctly rounded 1/k is within the 1-ulp rcp.approx the budget assumed.
+// Returns z, or sets *und (also at z = 40, like fast_poisson).
+__constant__ float c_tail_inv[41] = {
+    0.0f,        1.0f,         0.5f,         1.0f / 3,  0.25f,     0.2f,      1.0f / 6,
+    1.0f / 7,    0.125f,       1.0f / 9,     0.1f,      1.0f / 11, 1.0f / 12, 1.0f / 13,
+    1.0f / 14,   1.0f / 15,    0.0625f,      1.0f / 17, 1.0f / 18, 1.0f / 19, 0.05f,
+    1.0f / 21,   1.0f / 22,    1.0f / 23,    1.0f / 24, 0.04f,     1.0f / 26, 1.0f / 27,
+    1.0f / 28,   1.0f / 29,    1.0f / 30,    1.0f / 31, 0.03125f,  1.0f / 33, 1.0f / 34,
+    1.0f / 35,   1.0f / 36,    1.0f / 37,    1.0f / 38, 1.0f / 39, 0.025f};
+__constant__ float c_tail_rk[41] = {
+    0.0f,     0.0f,     1.2e-6f,  1.8e-6f,  2.4e-6f,  3.0e-6f,  3.6e-6f,  4.2e-6f,  4.8e-6f,
+    5.4e-6f,  6.0e-6f,  6.6e-6f,  7.2e-6f,  7.8e-6f,  8.4e-6f,  9.0e-6f,  9.6e-6f,  1.02e-5f,
+    1.08e-5f, 1.14e-5f, 1.2e-5f,  1.26e-5f, 1.32e-5f, 1.38e-5f, 1.44e-5f, 1.5e-5f,  1.56e-5f,
+    1.62e-5f, 1.68e-5f, 1.74e-5f, 1.8e-5f,  1.86e-5f, 1.92e-5f, 1.98e-5f, 2.04e-5f, 2.1e-5f,
+    2.16e-5f, 2.22e-5f, 2.28e-5f, 2.34e-5f, 2.4e-5f};
+
 __device__ __forceinline__ uint32_t fast_poisson_tail(float lam, float u, float t1, float c2,
                                                       bool* und) {
   const float r0 = __fmaf_rn(2.4e-7f, lam, 4.8e-7f);
   const float pl = __fmul_rn(3e-6f, lam);
-  float pmf = __fmul_rn(t1, __fmul_rn(lam, 0.5f)), cdf = c2, zf = 2.0f;
-  float rk = __fadd_rn(r0, 1.2e-6f);
-  uint32_t z = 2;
-  for (;;) {
-    ++z;
-    zf = __fadd_rn(zf, 1.0f);
-    pmf = __fmul_rn(pmf, __fmul_rn(lam, rcp_approx(zf)));
+  float pmf = __fmul_rn(t1, __fmul_rn(lam, 0.5f)), cdf = c2;
+#pragma unroll 1
+  for (uint32_t k = 3; k <= 40; ++k) {
+    pmf = __fmul_rn(pmf, __fmul_rn(lam, c_tail_inv[k]));
     cdf = __fadd_rn(cdf, pmf);
-    rk = __fadd_rn(rk, 6e-7f);
-    const float mk = __fmaf_rn(cdf, rk, __fmaf_rn(pmf, pl, 2.5e-7f));
+    const float mk = __fmaf_rn(cdf, __fadd_rn(r0, c_tail_rk[k]), __fmaf_rn(pmf, pl, 2.5e-7f));
     const float dk = __fsub_rn(u, cdf);
-    if (dk < -mk) return z;
-    if (!(dk > mk) || z >= 40) {
-      *und = true;
-      return 0;
-    }
+    if (dk < -mk) return k;
+    if (!(dk > mk)) break;
   }
+  *und = true;
+  return 0;
 }
 
 template <int KPL, bool FULL, int MUSRC, int MINB, int DEC = 1, int TAIL = 0>
