@@ -1659,12 +1659,14 @@ __global__ void __launch_bounds__(256) k_col_totals(const unsigned long long* __
 
 // total[k] = sum over w, in order, of x[w,k] (sampler.cpp:214-218), with x
 // precomputed in a parallel pass.  One warp per 32 topics, lane = topic:
-// each W-row contributes one coalesced 256 B segment, streamed through a
-// kChainStages-deep cp.async ring.  A lane reads back only the words it
-// copied itself, so cp.async.wait_group is the only synchronisation and the
-// loop runs at the f64 add-chain latency (8.2 cycles per row).
-constexpr int kChainRows = 64;
-constexpr int kChainStages = 8;
+// 2-D TMA boxes of kChainRows W-rows x 32 topics stream through a
+// kChainStages-deep shared ring (k_col_chain).  The loop runs at the f64
+// add-chain latency (8.2 cycles per row) except for one barrier wait per box:
+// 256-row boxes (64 KB, 3 stages) put that overhead at ~5% (64-row boxes,
+// 8 stages: 0.63 ms; 128 x 6: 0.53 ms; 256 x 3: 0.48 ms at W = 102,660;
+// floor 0.44 ms).
+constexpr int kChainRows = 256;
+constexpr int kChainStages = 3;
 constexpr size_t kChainSmem = sizeof(double) * kChainStages * kChainRows * 32;
 
 __device__ __forceinline__ void cp_async8(void* smem, const void* gmem, int src_bytes) {
