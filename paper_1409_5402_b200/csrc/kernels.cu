@@ -331,32 +331,6 @@ struct Philox1 {
   uint32_t lo;  // lo(M1 * d)
 };
 
-__device__ __forceinline__ uint32_t philox_y(const Philox1 r1, uint32_t k0, uint32_t k1,
-                                             uint32_t p2lo, uint32_t p2hi) {
-  // round 1 -> c = {hw ^ k0, lo, t ^ k1, 0}; round 2 with M1 * (t ^ k1) = p2
-  uint32_t c0 = r1.hw ^ k0;
-  k0 += kPhiloxW0;
-  k1 += kPhiloxW1;
-  uint32_t lo0, hi0;
-  mulhilo(kPhiloxM0, c0, lo0, hi0);
-  uint32_t x0 = p2hi ^ r1.lo ^ k0, x1 = p2lo, x2 = hi0 ^ k1, x3 = lo0;
-#pragma unroll
-  for (int r = 2; r < 9; ++r) {
-    k0 += kPhiloxW0;
-    k1 += kPhiloxW1;
-    uint32_t a0, b0, a1, b1;
-    mulhilo(kPhiloxM0, x0, a0, b0);
-    mulhilo(kPhiloxM1, x2, a1, b1);
-    const uint32_t n0 = b1 ^ x1 ^ k0, n2 = b0 ^ x3 ^ k1;
-    x0 = n0;
-    x1 = a1;
-    x2 = n2;
-    x3 = a0;
-  }
-  // round 10: output word y = lo(M1 * x2)
-  return kPhiloxM1 * x2;
-}
-
 // Deferred exact draws: one record per (nonzero, topic slice) that has at
 // least one draw the fast path could not decide (a PTRS decision inside its band,
 // an ambiguous comparison, z > 40, or non-finite / tiny inputs).
@@ -628,7 +602,6 @@ __global__ void __launch_bounds__(MAXW * 32) k_sample_cta(
   uint32_t ks[kKeyWords];
   topic_schedule(seed, t, sweep, static_cast<uint32_t>(k), ks);
   int64_t cur_b = -1;
-  float th = 0.0f;
   uint32_t acc = 0;
   for (int64_t g0 = c0; g0 < c1; g0 += 32) {
     const int n_here = static_cast<int>(min(static_cast<int64_t>(32), c1 - g0));
@@ -1669,14 +1642,6 @@ constexpr int kChainRows = 256;
 constexpr int kChainStages = 3;
 constexpr size_t kChainSmem = sizeof(double) * kChainStages * kChainRows * 32;
 
-__device__ __forceinline__ void cp_async8(void* smem, const void* gmem, int src_bytes) {
-  const unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(smem));
-  asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(s), "l"(gmem), "r"(src_bytes));
-}
-__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
-template <int N>
-__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N)); }
-
 __device__ __forceinline__ unsigned smem_addr(const void* p) {
   return static_cast<unsigned>(__cvta_generic_to_shared(p));
 }
@@ -1803,24 +1768,6 @@ __global__ void k_phi_candidate(const unsigned long long* __restrict__ cu,
   const double hat = cu ? __ddiv_rn(static_cast<double>(static_cast<long long>(cu[i])), m_t)
                         : __ddiv_rn(cf[i], m_t);
   cand[i] = __dadd_rn(hat, beta);
-}
-
-// phi = (1 - rho) * phi + rho * cand / total, cand = count/m_t + beta
-// (sampler.cpp:209-226); also refreshes the f32 copy the sampler reads.
-__global__ void k_phi_blend(const unsigned long long* __restrict__ cu,
-                            const double* __restrict__ cf, const double* __restrict__ totals,
-                            int64_t n, int K, double m_t, double beta, double one_minus_rho,
-                            double rho, double* __restrict__ phi_wk, float* __restrict__ phi32) {
-  const int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
-  if (i >= n) return;
-  const int k = static_cast<int>(i % K);
-  const double hat = cu ? __ddiv_rn(static_cast<double>(static_cast<long long>(cu[i])), m_t)
-                        : __ddiv_rn(cf[i], m_t);
-  const double cand = __dadd_rn(hat, beta);
-  const double v = __dadd_rn(__dmul_rn(one_minus_rho, phi_wk[i]),
-                             __ddiv_rn(__dmul_rn(rho, cand), totals[k]));
-  phi_wk[i] = v;
-  if (phi32) phi32[i] = __double2float_rn(v);
 }
 
 __global__ void k_to_f32(const double* __restrict__ x, int64_t n, float* __restrict__ y) {
