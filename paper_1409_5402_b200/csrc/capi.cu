@@ -504,7 +504,8 @@ struct samelda_cu_ctx {
   // mu_d: the caller's mu (per-call API) or nullptr (the kernel forms mu)
   void sample_sweep(const scu::BatchView& bv, const double* theta_b, const float* theta_b32,
                     const double* phi_wk, const float* phi_wk32, const double* mu_d, int K_,
-                    int64_t W_, double m_t_, uint64_t seed, int64_t t, int sweep, int mode) {
+                    int64_t W_, double m_t_, uint64_t seed, int64_t t, int sweep, int mode,
+                    bool need_phi = true) {
     if (profile) {
       prof_nnz += bv.nnz;
       prof_docs += bv.B;
@@ -523,7 +524,11 @@ struct samelda_cu_ctx {
       auto* tc_ = ensure<unsigned long long>(tc, bv.B * K_);
       auto* pc_ = ensure<unsigned long long>(pc, W_ * K_);
       ck(cudaMemsetAsync(tc_, 0, sizeof(unsigned long long) * std::max<int64_t>(bv.B * K_, 1), stream), "zero tc");
-      ck(cudaMemsetAsync(pc_, 0, sizeof(unsigned long long) * std::max<int64_t>(W_ * K_, 1), stream), "zero pc");
+      // a non-final inner sweep of the K = 256 period kernel skips the phi-count
+      // scatter (only the last sweep's phi counts feed update_model)
+      const bool skip_phi = !need_phi && K_ == 256 && mu_d == nullptr;
+      if (skip_phi) pc_ = nullptr;
+      else ck(cudaMemsetAsync(pc_, 0, sizeof(unsigned long long) * std::max<int64_t>(W_ * K_, 1), stream), "zero pc");
       tick(kSample, true);
       const int64_t records = bv.nnz * ((K_ + 255) / 256);
       const int64_t draw_cap = draw_cap_for(records);
@@ -1026,7 +1031,8 @@ int samelda_cu_period_sample(samelda_cu_ctx* ctx, const int32_t* doc_ids, int64_
       }
       // parity mode: the SDDMM is fused into the sampling kernel (mu == nullptr)
       ctx->sample_sweep(bv, thb, thb32, ctx->phi.as<double>(), ctx->phi32.as<float>(), mu, K, ctx->W,
-                        m_t, c.seed, t, static_cast<int>(sweep), c.mode);
+                        m_t, c.seed, t, static_cast<int>(sweep), c.mode,
+                        /*need_phi=*/sweep + 1 == c.inner_sweeps);
       if (sweep + 1 < c.inner_sweeps) {
         if (expected)
           ctx->launches += scu::launch_theta_from_counts(nullptr, ctx->tf.as<double>(), B * K, m_t, c.alpha, thb,

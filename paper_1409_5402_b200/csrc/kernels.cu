@@ -1044,7 +1044,9 @@ __device__ __forceinline__ uint32_t fast_poisson_tail(float lam, float u, float 
   return 0;
 }
 
-template <int KPL, bool FULL, int MUSRC, int MINB, int DEC = 1, int TAIL = 0>
+// PHI = false: a non-final inner sweep -- only the last sweep's phi counts feed
+// update_model (sampler.cpp:320-332), so the phi-count scatter is skipped.
+template <int KPL, bool FULL, int MUSRC, int MINB, int DEC = 1, int TAIL = 0, bool PHI = true>
 __global__ void __launch_bounds__(kFastBlock, MINB) k_sample_v2(
     BatchView bv, const float* __restrict__ theta_b32, const float* __restrict__ phi32,
     const double* __restrict__ mu_in, const float* __restrict__ mu_f_in, int K, double m_t,
@@ -1207,7 +1209,7 @@ __global__ void __launch_bounds__(kFastBlock, MINB) k_sample_v2(
             z = 0;
           }
           acc[j >> 1] += (j & 1) ? (z << 16) : z;
-          if (FULL || kbase + lane + kWarp * j < K) red_add_u64(pc + kWarp * j, z);
+          if (PHI && (FULL || kbase + lane + kWarp * j < K)) red_add_u64(pc + kWarp * j, z);
         }
       }
       if (TAIL && __any_sync(0xffffffffu, parked != 0)) {
@@ -1229,7 +1231,7 @@ __global__ void __launch_bounds__(kFastBlock, MINB) k_sample_v2(
                 und ? ~2ull : static_cast<unsigned long long>(z - 3u);
             if (und) defer_bits |= 1u << j;
             if (delta) {
-              atomicAdd(pc + kWarp * j, delta);
+              if (PHI) atomicAdd(pc + kWarp * j, delta);
               atomicAdd(tcrow + kWarp * j, delta);
             }
           }
@@ -1303,7 +1305,8 @@ __device__ __forceinline__ void deferred_one(const BatchView& bv, const Deferred
   }
   if (z != 0) {
     atomicAdd(theta_counts + static_cast<int64_t>(rec.b) * K + k, static_cast<unsigned long long>(z));
-    atomicAdd(phi_counts + static_cast<int64_t>(rec.w) * K + k, static_cast<unsigned long long>(z));
+    if (phi_counts)  // null for a non-final inner sweep (only theta counts are used)
+      atomicAdd(phi_counts + static_cast<int64_t>(rec.w) * K + k, static_cast<unsigned long long>(z));
   }
 }
 
@@ -1475,10 +1478,24 @@ int launch_fast_kpl(const BatchView& bv, const double* tb64, const float* tb32, 
   auto* rec = static_cast<Deferred*>(deferred);
   const dim3 grid(static_cast<unsigned>((items + warps - 1) / warps), static_cast<unsigned>(n_slices));
   const char* variant = getenv("SAMELDA_SAMPLER");
-  const bool v1 = variant && variant[0] == 'o';  // the previous kernel, for A/B profiling
+  // the previous kernel, for A/B profiling (it always scatters phi counts)
+  const bool v1 = variant && variant[0] == 'o' && pc != nullptr;
   if (!v1) {
     const int musrc = mu ? 1 : (muf ? 2 : 0);
     const bool full = K % (kWarp * KPL) == 0;
+    if (pc == nullptr) {
+      // non-final inner sweep (theta counts only): the K = 256 period kernel
+      if constexpr (KPL == 8) {
+        if (full && musrc == 0 && n_slices == 1) {
+          k_sample_v2<8, true, 0, 4, 1, 0, false><<<grid, kFastBlock, 0, st>>>(
+              bv, tb32, phi32, mu, muf, K, m_t, seed, t, sweep, chunk, tc, pc, rec, n_deferred);
+          launch_deferred(bv, tb64, phi64, mu, K, m_t, seed, t, sweep, rec, n_deferred, aux,
+                          bv.nnz * ((K + 255) / 256), draw_cap, tc, pc, err, st);
+          return launched + 3;
+        }
+      }
+      return -1;  // caller passes phi counts for every other shape
+    }
     const char* minb_env = getenv("SAMELDA_MINB");
     const int minb = minb_env ? atoi(minb_env) : 4;
     const char* dec_env = getenv("SAMELDA_DEC");
@@ -2389,7 +2406,7 @@ int launch_sample_fast(const BatchView& bv, const double* theta_b64, const float
   const char* variant = getenv("SAMELDA_SAMPLER");
   const char v = variant ? variant[0] : 'f';
   // K > 256: topic slices of 256 with the full mu from a k_mu_f32 pre-pass
-  if (v == 'f' || v == 'o') {
+  if (v == 'f' || v == 'o' || pc == nullptr) {
     if (K <= 32)
       return launch_fast_kpl<1>(bv, theta_b64, theta_b32, phi64, phi32, mu, K, m_t, seed, t, sweep, tc, pc,
                                 deferred, n_deferred, aux, draw_cap, mu_f, err, st);
