@@ -43,6 +43,11 @@ CONFIGS = {
                    schedule="constant",
                    workload="PubMed-shaped synthetic corpus (8.2M docs, 141,043 vocab, ~730M "
                             "tokens), K=256, m=100, bf=0.05"),
+    # the deterministic factored expected-count path (north star (3); z := rate)
+    "nytimes-expected": dict(corpus="nytimes", n_topics=256, m=100.0, batch_fraction=0.05,
+                             inner_sweeps=2, schedule="constant", mode="expected",
+                             workload="NYTimes-shaped synthetic corpus, K=256, m=100, bf=0.05, "
+                                      "2 inner sweeps, expected-count mode"),
     # BASELINE.json configs[4]
     "k1024": dict(corpus="nytimes", n_topics=1024, m=50.0, batch_fraction=0.05, inner_sweeps=2,
                   schedule="constant",
@@ -283,7 +288,8 @@ def run_ours(args, cfg):
 
     scfg = S.SamplerConfig(n_topics=cfg["n_topics"], m=cfg["m"], schedule=cfg["schedule"],
                            batch_fraction=cfg["batch_fraction"], inner_sweeps=cfg["inner_sweeps"],
-                           t_max=args.warmup + args.steps + 2 * max(1, min(args.steps, 10)), seed=1, mode=S.MODE_PARITY)
+                           t_max=args.warmup + args.steps + 2 * max(1, min(args.steps, 10)), seed=1,
+                           mode=S.MODE_EXPECTED if cfg.get("mode") == "expected" else S.MODE_PARITY)
     trainer = S.Trainer(train, scfg, ctx=ctx)
     trainer.set_doc_base(doc_base)
     if rank == 0:
@@ -404,8 +410,9 @@ def run_ours(args, cfg):
     # count) + 8K (phi column) + 4K (phi-count column); per batch doc
     # 8 + 8K (theta row) + 4K (theta counts).  This build moves the same
     # 12K + 8 per nonzero (phi32 4K + u64 counts 8K).
-    per_nnz = 8 + 12 * K
-    per_doc = 8 + 12 * K
+    # (expected-count mode: f64 rates -- 8K phi row + 8K f64 RED per nonzero)
+    per_nnz = 8 + (16 if cfg.get("mode") == "expected" else 12) * K
+    per_doc = 8 + (16 if cfg.get("mode") == "expected" else 12) * K
     alg_bytes = prof["nnz"] * per_nnz + prof["docs"] * per_doc
     sample_ms = prof["sample_ms"]
     peaks, peaks_kind = load_peaks()
@@ -447,7 +454,7 @@ def run_ours(args, cfg):
             "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "config": {"workload": cfg["workload"], "K": K, "m": cfg["m"],
                        "batch_fraction": cfg["batch_fraction"],
-                       "inner_sweeps": cfg["inner_sweeps"], "mode": "parity",
+                       "inner_sweeps": cfg["inner_sweeps"], "mode": cfg.get("mode", "parity"),
                        "docs_per_gpu": D_local, "nnz_per_gpu": train.nnz,
                        "tokens_per_gpu": train.n_tokens, "parallelism": f"doc-shard x{world}",
                        "l2": "inputs larger than L2 (phi 210 MB f64 + theta 553 MB per GPU; "
@@ -455,7 +462,7 @@ def run_ours(args, cfg):
                        "corpus_gen_s": round(gen_s, 2)},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak if peak else None, "traffic": traffic,
-                         "kernel": "k_sample (parity)", "peak_kind": peaks_kind,
+                         "kernel": "k_expected" if cfg.get("mode") == "expected" else "k_sample_v2 + deferred (parity)", "peak_kind": peaks_kind,
                          "alg_bytes_per_launch": alg_bytes / max(prof["sample_launches"], 1),
                          "avg_launch_ms": sample_ms / max(prof["sample_launches"], 1),
                          "sample_share_of_step": sample_ms / prof_ms if prof_ms else None,

@@ -1023,14 +1023,16 @@ int samelda_cu_period_sample(samelda_cu_ctx* ctx, const int32_t* doc_ids, int64_
     double* mu = expected ? ensure<double>(ctx->mu, bv.nnz) : nullptr;
     ctx->launches += scu::launch_gather_theta(ctx->theta.as<double>(), bv.batch_docs, B, K, thb, thb32, st);
     for (int64_t sweep = 0; sweep < c.inner_sweeps; ++sweep) {
-      if (expected) {
-        // the expected-count kernel consumes an explicit mu (sampler.cpp:321)
+      if (expected && K > 256) {
+        // K <= 256: the expected-count kernel forms mu itself (f64 tree);
+        // wider K takes an explicit mu (sampler.cpp:321)
         ctx->tick(samelda_cu_ctx::kSddmm, true);
         ctx->launches += scu::launch_sddmm(bv, thb, ctx->phi.as<double>(), K, mu, st);
         ctx->tick(samelda_cu_ctx::kSddmm, false);
       }
       // parity mode: the SDDMM is fused into the sampling kernel (mu == nullptr)
-      ctx->sample_sweep(bv, thb, thb32, ctx->phi.as<double>(), ctx->phi32.as<float>(), mu, K, ctx->W,
+      ctx->sample_sweep(bv, thb, thb32, ctx->phi.as<double>(), ctx->phi32.as<float>(),
+                        expected && K <= 256 ? nullptr : mu, K, ctx->W,
                         m_t, c.seed, t, static_cast<int>(sweep), c.mode,
                         /*need_phi=*/sweep + 1 == c.inner_sweeps);
       if (sweep + 1 < c.inner_sweeps) {

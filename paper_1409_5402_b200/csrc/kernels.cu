@@ -2322,6 +2322,102 @@ __global__ void k_ordered_ll(const double* __restrict__ doc_logp,
   *ll_out = __ddiv_rn(total, static_cast<double>(scored));
 }
 
+// k_expected: the deterministic expected-count path (z := rate,
+// sampler.cpp:151-193 with poisson_sample replaced by its mean; tolerance 1e-5
+// relative against the oracle) in the period kernel's layout: lane = topic,
+// 8 topics per lane, warp = 128 consecutive batch nonzeros.  FUSED: mu is the
+// f64 tree sum of the row's products (no separate SDDMM pass); else the
+// caller's mu.  The per-nonzero scale m c / mu is formed once; a draw is one
+// DMUL, a register add into the document's theta row and one coalesced f64
+// RED into the word's phi row.
+template <int KPL, bool FULL, bool FUSED>
+__global__ void __launch_bounds__(256) k_expected(
+    BatchView bv, const double* __restrict__ theta_batch, const double* __restrict__ phi_wk,
+    const double* __restrict__ mu_in, int K, double m_t, int64_t chunk,
+    double* __restrict__ theta_exp, double* __restrict__ phi_exp, int* __restrict__ err) {
+  const int lane = threadIdx.x & 31;
+  const int64_t item = static_cast<int64_t>(blockIdx.x) * 8 + (threadIdx.x >> 5);
+  const int kbase = static_cast<int>(blockIdx.y) * kWarp * KPL;
+  const int64_t p0 = item * chunk;
+  if (p0 >= bv.nnz) return;
+  const int64_t p1 = min(p0 + chunk, bv.nnz);
+  const double uniform_weight = 1.0 / static_cast<double>(K);
+  int64_t cur_b = -1;
+  double th[KPL], acc[KPL];
+#pragma unroll
+  for (int j = 0; j < KPL; ++j) th[j] = acc[j] = 0.0;
+  auto flush = [&](int64_t b) {
+#pragma unroll
+    for (int j = 0; j < KPL; ++j) {
+      const int k = kbase + lane + kWarp * j;
+      if ((FULL || k < K) && acc[j] != 0.0) atomicAdd(theta_exp + b * K + k, acc[j]);
+    }
+  };
+  for (int64_t g0 = p0; g0 < p1; g0 += kWarp) {
+    const int64_t p = g0 + lane;
+    int64_t b = 0;
+    int32_t w = 0, c = 0;
+    double mu_v = 0.0;
+    if (p < p1) {
+      b = find_row(bv.batch_prefix, bv.B, p);
+      const int32_t d = __ldg(bv.batch_docs + b);
+      const int64_t gi = __ldg(bv.doc_offsets + d) + (p - __ldg(bv.batch_prefix + b));
+      w = __ldg(bv.word_ids + gi);
+      c = __ldg(bv.counts + gi);
+      if (!FUSED) mu_v = __ldg(mu_in + p);
+    }
+    const int n_here = static_cast<int>(min(static_cast<int64_t>(kWarp), p1 - g0));
+    for (int i = 0; i < n_here; ++i) {
+      const int64_t bi = __shfl_sync(0xffffffffu, b, i);
+      const int32_t wi = __shfl_sync(0xffffffffu, w, i);
+      const int32_t ci = __shfl_sync(0xffffffffu, c, i);
+      double ph[KPL];
+      const double* prow = phi_wk + static_cast<int64_t>(wi) * K + kbase + lane;
+#pragma unroll
+      for (int j = 0; j < KPL; ++j) ph[j] = (FULL || kbase + lane + kWarp * j < K) ? __ldg(prow + kWarp * j) : 0.0;
+      if (bi != cur_b) {
+        if (cur_b >= 0) flush(cur_b);
+        cur_b = bi;
+        const double* trow = theta_batch + bi * K + kbase + lane;
+#pragma unroll
+        for (int j = 0; j < KPL; ++j) {
+          th[j] = (FULL || kbase + lane + kWarp * j < K) ? __ldg(trow + kWarp * j) : 0.0;
+          acc[j] = 0.0;
+        }
+      }
+      double prod[KPL];
+#pragma unroll
+      for (int j = 0; j < KPL; ++j) prod[j] = __dmul_rn(th[j], ph[j]);
+      double mu;
+      if (FUSED) {
+        mu = 0.0;
+#pragma unroll
+        for (int j = 0; j < KPL; ++j) mu = __dadd_rn(mu, prod[j]);
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) mu = __dadd_rn(mu, __shfl_xor_sync(0xffffffffu, mu, o));
+      } else {
+        mu = __shfl_sync(0xffffffffu, mu_v, i);
+      }
+      const double cell_scale = __dmul_rn(m_t, static_cast<double>(ci));
+      const bool degenerate = mu < 1e-30;  // sampler.cpp:164, 0/0 guard
+      const double scale = degenerate ? 0.0 : __ddiv_rn(cell_scale, mu);
+      const double uni = __dmul_rn(uniform_weight, cell_scale);
+      double* prow_out = phi_exp + static_cast<int64_t>(wi) * K + kbase + lane;
+      bool bad = false;
+#pragma unroll
+      for (int j = 0; j < KPL; ++j) {
+        if (!FULL && kbase + lane + kWarp * j >= K) continue;
+        const double rate = degenerate ? uni : __dmul_rn(prod[j], scale);
+        bad = bad || !(rate >= 0.0) || isinf(rate);  // sampler.cpp:173-175
+        acc[j] = __dadd_rn(acc[j], rate);
+        atomicAdd(prow_out + kWarp * j, rate);
+      }
+      if (bad) atomicOr(err, kErrNumerical);
+    }
+  }
+  if (cur_b >= 0) flush(cur_b);
+}
+
 template <int KPL>
 int launch_sample_kpl(const BatchView& bv, const double* theta_batch, const double* phi_wk,
                       const double* mu, int K, double m_t, uint64_t seed, uint32_t t,
@@ -2333,9 +2429,22 @@ int launch_sample_kpl(const BatchView& bv, const double* theta_batch, const doub
   const int64_t threads = items * n_slices * kWarp;
   const int block = kSampleBlock;
   if (mode == kModeExpected) {
-    k_sample<KPL, kModeExpected><<<grid_for(threads, block), block, 0, st>>>(
-        bv, theta_batch, phi_wk, mu, K, m_t, seed, t, sweep, chunk, n_slices, tc, pc, tf, pf,
-        err);
+    // mu == nullptr (period path): fused f64 tree mu, one topic slice only
+    const dim3 grid(static_cast<unsigned>((items + 7) / 8), static_cast<unsigned>(n_slices));
+    const bool full = K % (kWarp * KPL) == 0;
+    if (mu == nullptr && n_slices == 1) {
+      if (full)
+        k_expected<KPL, true, true><<<grid, 256, 0, st>>>(bv, theta_batch, phi_wk, mu, K, m_t, chunk, tf, pf, err);
+      else
+        k_expected<KPL, false, true><<<grid, 256, 0, st>>>(bv, theta_batch, phi_wk, mu, K, m_t, chunk, tf, pf, err);
+    } else if (mu != nullptr) {
+      if (full)
+        k_expected<KPL, true, false><<<grid, 256, 0, st>>>(bv, theta_batch, phi_wk, mu, K, m_t, chunk, tf, pf, err);
+      else
+        k_expected<KPL, false, false><<<grid, 256, 0, st>>>(bv, theta_batch, phi_wk, mu, K, m_t, chunk, tf, pf, err);
+    } else {
+      return -1;  // K > 256 needs the caller's mu
+    }
   } else {
     k_sample<KPL, kModeParity><<<grid_for(threads, block), block, 0, st>>>(
         bv, theta_batch, phi_wk, mu, K, m_t, seed, t, sweep, chunk, n_slices, tc, pc, tf, pf,

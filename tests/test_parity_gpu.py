@@ -213,6 +213,21 @@ def test_expected_train_within_1e5(port, small_split):
     np.testing.assert_allclose([r["ll"] for r in trace], [r["ll"] for r in otrace], rtol=1e-9)
 
 
+@pytest.mark.parametrize("K", [256, 200, 300])
+def test_expected_train_wide_k_within_1e5(port, K):
+    """The period path's expected-count kernel (k_expected: 8 topics per lane,
+    fused f64 mu for K <= 256, full and partial slices; K > 256 takes the
+    SDDMM's mu) against the oracle."""
+    g = port.make_corpus(80, 150, 6, 60.0, 12)
+    tr, te = port.split_holdout(g, 0.15, 3)
+    kw = dict(n_topics=K, m=20.0, t_max=3, batch_fraction=0.5, seed=5)
+    model, trace = S.train(tr, S.SamplerConfig(mode=S.MODE_EXPECTED, **kw), te, 3)
+    ophi, otheta, otrace = port.train(tr, TrainConfig(**kw), te, 3, expected=True)
+    np.testing.assert_allclose(model.phi, ophi, rtol=1e-5, atol=1e-12)
+    np.testing.assert_allclose(model.theta, otheta, rtol=1e-5, atol=1e-12)
+    np.testing.assert_allclose([r["ll"] for r in trace], [r["ll"] for r in otrace], rtol=1e-9)
+
+
 def test_random_larger_case_bit_exact(port):
     """K=256 (8 topics per lane), multi-chunk docs, random theta/phi: counts bit-exact."""
     g = port.make_corpus(300, 700, 8, 120.0, 21)
