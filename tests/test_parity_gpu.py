@@ -587,3 +587,40 @@ def test_reported_eval_error_does_not_leak_into_training(port):
                        ctx=ctx)
     ophi, _, _ = port.train(g, TrainConfig(n_topics=2, m=5.0, t_max=2, batch_fraction=1.0, seed=1))
     np.testing.assert_array_equal(model.phi, ophi)
+
+
+# ------------------------------------------------ rate extremes on the K=256 period kernel
+
+@pytest.mark.parametrize("m", [1e-3, 0.37, 1e4])
+def test_train_rate_extremes_bit_exact(port, m):
+    """Tiny rates (every draw decided at z = 0 or deferred as tiny), and huge
+    rates (almost every draw in PTRS territory: deferred exact path, z far
+    beyond the fast path's 40), K = 256, against the oracle."""
+    g = port.make_corpus(60, 300, 10, 120.0, 44)
+    kw = dict(n_topics=256, m=m, t_max=2, batch_fraction=0.6, seed=9)
+    model, _ = S.train(g, S.SamplerConfig(**kw))
+    ophi, otheta, _ = port.train(g, TrainConfig(**kw))
+    np.testing.assert_array_equal(model.phi, ophi)
+    np.testing.assert_array_equal(model.theta, otheta)
+
+
+def test_large_counts_and_long_documents_bit_exact(port):
+    """Cells with counts in the hundreds (lambda = m c w >> 10) and documents
+    spanning many 128-nonzero warp chunks (the per-lane packed theta counts
+    are flushed per chunk), K = 256."""
+    rng = np.random.default_rng(17)
+    D, W = 6, 900
+    offsets, words, counts = [0], [], []
+    for d in range(D):
+        n = int(rng.integers(300, 700))
+        ws = np.sort(rng.choice(W, size=n, replace=False)).astype(np.int32)
+        cs = rng.integers(1, 400, size=n).astype(np.int32)
+        words.append(ws)
+        counts.append(cs)
+        offsets.append(offsets[-1] + n)
+    g = S.Corpus(np.array(offsets), np.concatenate(words), np.concatenate(counts), W)
+    kw = dict(n_topics=256, m=5.0, t_max=2, batch_fraction=1.0, seed=2)
+    model, _ = S.train(g, S.SamplerConfig(**kw))
+    ophi, otheta, _ = port.train(g, TrainConfig(**kw))
+    np.testing.assert_array_equal(model.phi, ophi)
+    np.testing.assert_array_equal(model.theta, otheta)
