@@ -2304,16 +2304,36 @@ __global__ void __launch_bounds__(kEvalCtaThreads) k_eval_stage(
   }
 }
 
-__global__ void k_ordered_ll(const double* __restrict__ doc_logp,
-                             const int64_t* __restrict__ doc_scored, int64_t n_docs,
-                             double* __restrict__ ll_out, int* __restrict__ err) {
-  if (threadIdx.x != 0 || blockIdx.x != 0) return;
+// eval.cpp:148-158: the document-order reduction.  The block stages 1024
+// documents at a time in shared memory (coalesced); one thread then adds
+// them in document order at the f64 add latency instead of a global-load
+// latency per document.
+constexpr int kOrderedBlock = 1024;
+
+__global__ void __launch_bounds__(kOrderedBlock) k_ordered_ll(
+    const double* __restrict__ doc_logp, const int64_t* __restrict__ doc_scored, int64_t n_docs,
+    double* __restrict__ ll_out, int* __restrict__ err) {
+  __shared__ double s_lp[kOrderedBlock];
+  __shared__ int64_t s_sc[kOrderedBlock];
   double total = 0.0;
   int64_t scored = 0;
-  for (int64_t d = 0; d < n_docs; ++d) {
-    total = __dadd_rn(total, doc_logp[d]);
-    scored += doc_scored[d];
+  for (int64_t d0 = 0; d0 < n_docs; d0 += kOrderedBlock) {
+    const int n = static_cast<int>(min(static_cast<int64_t>(kOrderedBlock), n_docs - d0));
+    if (threadIdx.x < n) {
+      s_lp[threadIdx.x] = doc_logp[d0 + threadIdx.x];
+      s_sc[threadIdx.x] = doc_scored[d0 + threadIdx.x];
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+#pragma unroll 8
+      for (int i = 0; i < n; ++i) {
+        total = __dadd_rn(total, s_lp[i]);
+        scored += s_sc[i];
+      }
+    }
+    __syncthreads();
   }
+  if (threadIdx.x != 0) return;
   if (scored == 0) {
     atomicOr(err, kErrNumerical);
     *ll_out = 0.0;
@@ -2708,7 +2728,7 @@ int launch_eval_docs(const int64_t* doc_offsets, const int32_t* word_ids,
 
 int launch_ordered_ll(const double* doc_logp, const int64_t* doc_scored, int64_t n_docs,
                       double* ll_out, int* err, cudaStream_t st) {
-  k_ordered_ll<<<1, 32, 0, st>>>(doc_logp, doc_scored, n_docs, ll_out, err);
+  k_ordered_ll<<<1, kOrderedBlock, 0, st>>>(doc_logp, doc_scored, n_docs, ll_out, err);
   return 1;
 }
 
