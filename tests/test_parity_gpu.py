@@ -624,3 +624,35 @@ def test_large_counts_and_long_documents_bit_exact(port):
     ophi, otheta, _ = port.train(g, TrainConfig(**kw))
     np.testing.assert_array_equal(model.phi, ophi)
     np.testing.assert_array_equal(model.theta, otheta)
+
+
+# ------------------------------------------------ BASELINE size (NYTimes shape)
+
+@pytest.mark.skipif(not __import__("oracle").have_ref(), reason="oracle/_ref not built")
+def test_nytimes_scale_sweep_matches_compiled_reference():
+    """One full-size sampling sweep at BASELINE configs[1] shape (NYTimes-shaped
+    corpus, a 13,500-document minibatch, K=256, m=100) on a model trained for
+    a few periods on the device: theta and phi counts bit-exact against the
+    compiled reference's sample_counts (oracle/_ref, all host threads), and
+    the sweep's mass balance."""
+    import bench
+    from oracle import Ref
+    corpus = bench.make_corpus("nytimes", 0)
+    train, _ = bench.split_heldout(corpus)
+    cfg = S.SamplerConfig(n_topics=256, m=100.0, batch_fraction=0.05, t_max=4, seed=1)
+    tr = S.Trainer(train, cfg)
+    stream = S.MinibatchStream(train.n_docs, 0.05, 1)
+    for t in range(3):
+        tr.period(stream.next(), t, 100.0, S.rho_schedule(t, 1.0, 0.5))
+    model = tr.model()
+    batch = stream.next()
+    tb = np.ascontiguousarray(model.theta[batch])
+    ctx = tr.ctx
+    mu = S.sddmm(tb, model.phi, train, batch, ctx=ctx)
+    sc = S.sample_counts(tb, model.phi, mu, train, batch, 100.0, 1, 3, 1, ctx=ctx)
+    ref = Ref()
+    otc, opc = ref.sample_counts(tb, model.phi, mu, train, batch, 100.0, 1, 3, 1,
+                                 n_threads=os.cpu_count() or 1)
+    np.testing.assert_array_equal(sc.theta_counts, otc)
+    np.testing.assert_array_equal(sc.phi_counts, opc)
+    assert sc.theta_counts.sum() == sc.phi_counts.sum()
