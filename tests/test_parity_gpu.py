@@ -656,3 +656,23 @@ def test_nytimes_scale_sweep_matches_compiled_reference():
     np.testing.assert_array_equal(sc.theta_counts, otc)
     np.testing.assert_array_equal(sc.phi_counts, opc)
     assert sc.theta_counts.sum() == sc.phi_counts.sum()
+
+
+def test_eval_documents_beyond_one_fold_window(port):
+    """k_eval_stage compacts fold cells per window of 1024 (cell order kept,
+    lists rebuilt every sweep, staged rows only for window 0): documents with
+    2,000-4,000 distinct words, K=64, against the oracle."""
+    rng = np.random.default_rng(23)
+    W = 6000
+    offsets, words, counts = [0], [], []
+    for n in (4000, 120, 2500, 1030, 3100):
+        ws = np.sort(rng.choice(W, size=n, replace=False)).astype(np.int32)
+        cs = rng.integers(1, 4, size=n).astype(np.int32)
+        words.append(ws)
+        counts.append(cs)
+        offsets.append(offsets[-1] + n)
+    g = S.Corpus(np.array(offsets), np.concatenate(words), np.concatenate(counts), W)
+    phi = rng.gamma(0.5, 1.0, size=(64, W)) + 1e-12
+    phi /= phi.sum(1, keepdims=True)
+    ll = S.perword_loglik(phi, g, 0.1, 19)
+    assert ll == pytest.approx(port.perword_loglik(phi, g, 0.1, 19), rel=1e-12, abs=0)
