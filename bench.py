@@ -223,6 +223,11 @@ def run_reference(args, cfg):
     world, rank, _ = dist_env()
     if rank != 0:
         return
+    if cfg.get("mode") == "expected":
+        print(json.dumps({"impl": "reference",
+                          "unavailable": "the reference has no expected-count mode "
+                                         "(sampler.cpp draws Poisson replicas only)"}), flush=True)
+        return
     n_threads = os.cpu_count() or 1
     corpus = make_corpus(cfg["corpus"], 0)
     train, _ = split_heldout(corpus)
