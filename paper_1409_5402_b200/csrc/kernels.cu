@@ -1777,14 +1777,30 @@ __global__ void k_phi_blend_cand(const double* __restrict__ cand, const double* 
 }
 
 // cand[w,k] = count / m_t + beta (the reference's `value`, sampler.cpp:209)
+// cand = count / m_t + beta (sampler.cpp:211-218), two elements per thread
+// with 16-byte loads and stores (n is W x K; an odd tail is handled singly)
 __global__ void k_phi_candidate(const unsigned long long* __restrict__ cu,
                                 const double* __restrict__ cf, int64_t n, double m_t,
                                 double beta, double* __restrict__ cand) {
-  const int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
-  if (i >= n) return;
-  const double hat = cu ? __ddiv_rn(static_cast<double>(static_cast<long long>(cu[i])), m_t)
-                        : __ddiv_rn(cf[i], m_t);
-  cand[i] = __dadd_rn(hat, beta);
+  const int64_t i2 = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+  const int64_t i = 2 * i2;
+  if (i + 1 < n) {
+    double a, b;
+    if (cu) {
+      const ulonglong2 v = __ldg(reinterpret_cast<const ulonglong2*>(cu) + i2);
+      a = __ddiv_rn(static_cast<double>(static_cast<long long>(v.x)), m_t);
+      b = __ddiv_rn(static_cast<double>(static_cast<long long>(v.y)), m_t);
+    } else {
+      const double2 v = __ldg(reinterpret_cast<const double2*>(cf) + i2);
+      a = __ddiv_rn(v.x, m_t);
+      b = __ddiv_rn(v.y, m_t);
+    }
+    reinterpret_cast<double2*>(cand)[i2] = make_double2(__dadd_rn(a, beta), __dadd_rn(b, beta));
+  } else if (i < n) {
+    const double hat = cu ? __ddiv_rn(static_cast<double>(static_cast<long long>(cu[i])), m_t)
+                          : __ddiv_rn(cf[i], m_t);
+    cand[i] = __dadd_rn(hat, beta);
+  }
 }
 
 __global__ void k_to_f32(const double* __restrict__ x, int64_t n, float* __restrict__ y) {
@@ -2591,7 +2607,7 @@ int launch_phi_mstep(const unsigned long long* cu, const double* cf, int64_t W, 
                      double* cand, double* totals, int* err, cudaStream_t st) {
   const int64_t n = W * K;
   if (n == 0) return 0;
-  k_phi_candidate<<<grid_for(n, 256), 256, 0, st>>>(cu, cf, n, m_t, beta, cand);
+  k_phi_candidate<<<grid_for((n + 1) / 2, 256), 256, 0, st>>>(cu, cf, n, m_t, beta, cand);
   launch_col_sums(cand, W, K, totals, err, st);
   k_phi_blend_cand<<<grid_for(n, 256), 256, 0, st>>>(cand, totals, n, K, 1.0 - rho, rho, phi_wk,
                                                      phi32);
