@@ -571,7 +571,7 @@ struct samelda_cu_ctx {
   double eval_ll(const double* phi_wk, int K_, double alpha) {
     const int64_t nd = heldout.n_docs;
     double* lp = ensure<double>(doc_logp, nd);
-    int64_t* sc = ensure<int64_t>(doc_scored, nd);
+    int64_t* sc = ensure<int64_t>(doc_scored, nd + 1);  // + the eval kernel's work counter
     const int64_t need = scu::eval_scratch_doubles(K_);
     double* scratch = need > 0 ? ensure<double>(eval_scratch, need) : nullptr;
     reset_err();
@@ -888,7 +888,7 @@ int samelda_cu_fold_in_theta(samelda_cu_ctx* ctx, const double* phi, int64_t K, 
     }
     ctx->split_ready = false;  // fold/score buffers now hold this call's counts
     double* lp = ensure<double>(ctx->doc_logp, 1);
-    int64_t* scd = ensure<int64_t>(ctx->doc_scored, 1);
+    int64_t* scd = ensure<int64_t>(ctx->doc_scored, 2);  // + the eval kernel's work counter
     double* th = ensure<double>(ctx->theta_rows, K);
     const int64_t need = scu::eval_scratch_doubles(static_cast<int>(K));
     double* scratch = need > 0 ? ensure<double>(ctx->eval_scratch, need) : nullptr;

@@ -2184,7 +2184,16 @@ __global__ void __launch_bounds__(kEvalCtaThreads) k_eval_stage(
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
   const double inv_k = 1.0 / static_cast<double>(K);
 
-  for (int64_t doc = blockIdx.x; doc < n_docs; doc += gridDim.x) {
+  // documents are handed out dynamically (their fold-in lengths differ:
+  // 1 to 50 sweeps, tens to thousands of cells): counter at doc_scored[n_docs]
+  __shared__ int64_t s_doc;
+  unsigned long long* next_doc = reinterpret_cast<unsigned long long*>(doc_scored + n_docs);
+  for (;;) {
+    if (threadIdx.x == 0) s_doc = static_cast<int64_t>(atomicAdd(next_doc, 1ull));
+    __syncthreads();
+    const int64_t doc = s_doc;
+    __syncthreads();
+    if (doc >= n_docs) break;
     const int64_t base = doc_offsets[doc];
     const int64_t n = doc_offsets[doc + 1] - base;
     // compact the fold cells of cells [c_begin, ...) into fw/fc, whole chunks
@@ -2696,6 +2705,8 @@ int launch_eval_docs(const int64_t* doc_offsets, const int32_t* word_ids,
         configured_s = 220 * 1024;
       }
       const int64_t blocks = min(n_docs, static_cast<int64_t>(148 * cps));
+      // the dynamic document counter lives one past the per-document results
+      cudaMemsetAsync(doc_scored + n_docs, 0, sizeof(int64_t), st);
       k_eval_stage<<<static_cast<unsigned>(blocks), kEvalCtaThreads, smem_s, st>>>(
           doc_offsets, word_ids, fold_counts, score_counts, n_docs, phi_wk, K, alpha, sweeps, R,
           doc_logp, doc_scored, theta_out, err);
