@@ -676,3 +676,28 @@ def test_eval_documents_beyond_one_fold_window(port):
     phi /= phi.sum(1, keepdims=True)
     ll = S.perword_loglik(phi, g, 0.1, 19)
     assert ll == pytest.approx(port.perword_loglik(phi, g, 0.1, 19), rel=1e-12, abs=0)
+
+
+@pytest.mark.skipif(not __import__("oracle").have_ref(), reason="oracle/_ref not built")
+def test_model_bin_and_metrics_csv_match_reference_training(port, tmp_path):
+    """End to end through the output formats: a device
+    training run written with save_checkpoint / write_metrics_csv against the
+    compiled reference's own train() + save_checkpoint / write_metrics_csv:
+    model.bin byte-equal, metrics.csv equal except the wall-clock column."""
+    from oracle import Ref
+    ref = Ref()
+    g = port.make_corpus(150, 90, 5, 40.0, 77)
+    tr, te = port.split_holdout(g, 0.2, 3)
+    kw = dict(n_topics=16, m=30.0, t_max=6, batch_fraction=0.25, seed=11)
+    model, trace = S.train(tr, S.SamplerConfig(**kw), te, 2)
+    rphi, _, rtrace = ref.train(tr, TrainConfig(**kw), te, 2)
+    ours, theirs = str(tmp_path / "ours.bin"), str(tmp_path / "ref.bin")
+    S.save_checkpoint(model, ours)
+    ref.save_checkpoint(theirs, rphi, model.alpha, model.beta)
+    assert open(ours, "rb").read() == open(theirs, "rb").read()
+    oc, rc = str(tmp_path / "ours.csv"), str(tmp_path / "ref.csv")
+    S.write_metrics_csv(trace, oc)
+    ref.write_metrics_csv(rc, rtrace)
+    drop_wall = lambda path: [ln.split(",")[:4] + ln.split(",")[5:]
+                              for ln in open(path).read().splitlines()]
+    assert drop_wall(oc) == drop_wall(rc)
