@@ -269,10 +269,19 @@ def run_reference(args, cfg):
 def run_ours(args, cfg):
     import torch
     world, rank, local = dist_env()
+    # BENCH_SHARE_GPU=1 (testing the multi-rank path on a one-GPU box): every
+    # rank on cuda:0 over gloo -- NCCL refuses two ranks on one device; the
+    # numbers of such a run are not a measurement
+    share = os.environ.get("BENCH_SHARE_GPU") == "1"
+    if share:
+        local = 0
     torch.cuda.set_device(local)
     if world > 1:
         import torch.distributed as dist
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if share:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     from paper_1409_5402_b200 import samelda as S
 
     ctx = S.Context(local)

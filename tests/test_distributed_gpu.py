@@ -85,3 +85,29 @@ def test_two_rank_sharded_training_equals_single_gpu(tmp_path):
     model, _ = S.train(g, S.SamplerConfig(n_topics=K, m=M, schedule="invlinear", t_max=T_MAX,
                                           batch_fraction=BF, seed=SEED))
     np.testing.assert_array_equal(got["phi"], model.phi)
+
+
+def test_bench_two_rank_path_runs(tmp_path):
+    """bench.py's torchrun path (N=2, weak scaling, one global minibatch
+    stream, per-period count all-reduce) end to end on the one-GPU box
+    (BENCH_SHARE_GPU: both ranks on cuda:0 over gloo); the JSON line is
+    well-formed and reports the aggregate over ranks."""
+    import json
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = dict(os.environ, BENCH_SHARE_GPU="1", BENCH_NO_CLOCKS="1")
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port_no = s.getsockname()[1]
+    out = subprocess.run(
+        [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2",
+         "--master-addr", "127.0.0.1", "--master-port", str(port_no), "bench.py", "--gpus", "2",
+         "--steps", "2", "--warmup", "3", "--no-cpu-baseline"],
+        cwd=root, env=env, capture_output=True, text=True, timeout=600)
+    assert out.returncode == 0, out.stderr[-2000:]
+    lines = [ln for ln in out.stdout.splitlines() if ln.startswith("{")]
+    assert len(lines) == 1
+    line = json.loads(lines[0])
+    assert line["n_gpus"] == 2 and line["value"] > 0 and line["e2e"]["value"] > 0
+    assert line["config"]["parallelism"] == "doc-shard x2"
