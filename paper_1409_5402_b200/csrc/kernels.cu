@@ -743,8 +743,22 @@ __global__ void __launch_bounds__(256) k_mu_f32(BatchView bv, const float* __res
     // f64 accumulation of the exact f32 x f32 products: mu_f is then within
     // ~1 ulp of the f32-input dot for any K (the fast-path budget assumes 16u)
     double part = 0.0;
-    for (int k = lane; k < K; k += 32)
-      part = __dadd_rn(part, static_cast<double>(__ldg(tr + k)) * static_cast<double>(__ldg(pr + k)));
+    if ((K & 3) == 0) {
+      // 16-byte loads: lane takes topics 4 lane .. 4 lane + 3 of each 128
+      const float4* t4 = reinterpret_cast<const float4*>(tr);
+      const float4* p4 = reinterpret_cast<const float4*>(pr);
+#pragma unroll 4
+      for (int q = lane; q < (K >> 2); q += 32) {
+        const float4 a = __ldg(t4 + q), b = __ldg(p4 + q);
+        part = __dadd_rn(part, static_cast<double>(a.x) * static_cast<double>(b.x));
+        part = __dadd_rn(part, static_cast<double>(a.y) * static_cast<double>(b.y));
+        part = __dadd_rn(part, static_cast<double>(a.z) * static_cast<double>(b.z));
+        part = __dadd_rn(part, static_cast<double>(a.w) * static_cast<double>(b.w));
+      }
+    } else {
+      for (int k = lane; k < K; k += 32)
+        part = __dadd_rn(part, static_cast<double>(__ldg(tr + k)) * static_cast<double>(__ldg(pr + k)));
+    }
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) part = __dadd_rn(part, __shfl_xor_sync(0xffffffffu, part, o));
     if (lane == i) mine = __double2float_rn(part);
