@@ -475,6 +475,10 @@ def run_ours(args, cfg):
                              "random minibatch docs each step)",
                        "corpus_gen_s": round(gen_s, 2)},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                         "model": "SURVEY 8(d) per-nonzero gather bytes (phi row + count row per "
+                                  "nonzero, theta rows per doc); rows re-read from L2 are counted, "
+                                  "so frac can exceed 1 for an L2-resident kernel -- see traffic "
+                                  "for DRAM bytes",
                          "frac": achieved / peak if peak else None, "traffic": traffic,
                          "kernel": "k_expected" if cfg.get("mode") == "expected" else "k_sample_v2 + deferred (parity)", "peak_kind": peaks_kind,
                          "alg_bytes_per_launch": alg_bytes / max(prof["sample_launches"], 1),
