@@ -232,7 +232,10 @@ def run_reference(args, cfg):
     corpus = make_corpus(cfg["corpus"], 0)
     train, _ = split_heldout(corpus)
     ref, a, b = calibrate_reference(train, cfg, n_threads)
-    sub = reference_sub_batch(train, cfg, a, b, budget_s=max(3.0, 180.0 / max(args.steps, 1)))
+    budget = max(3.0, 180.0 / max(args.steps, 1))
+    if os.environ.get("BENCH_REF_BUDGET_S"):  # tests: cap the per-step CPU sample
+        budget = float(os.environ["BENCH_REF_BUDGET_S"])
+    sub = reference_sub_batch(train, cfg, a, b, budget_s=budget)
     step = reference_step_fn(ref, train, cfg, sub, n_threads)
     warm = reference_step_fn(ref, train, cfg, 64, n_threads, seed=3)
     for _ in range(args.warmup):  # CPU code needs no warm-up; keep these cheap
