@@ -242,62 +242,25 @@ constexpr int kFastBlock = 256;
 // error interval (1.5e-6 relative, 2x) lies below 10; PTRS draws defer
 constexpr float kInvMax = 9.99997f;
 
-// MUFU-only transcendentals (no denormal range fix-ups: arguments here are
-// in [-14.5, 0] and [1, 40]); their error is inside the fast-path budget.
+// MUFU-only exp2 (no denormal range fix-up: arguments here are in
+// [-14.5, 0]); its error is inside the fast-path budget.
 __device__ __forceinline__ float ex2_approx(float x) {
   float y;
   asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
   return y;
 }
-__device__ __forceinline__ float rcp_approx(float x) {
-  float y;
-  asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
-  return y;
-}
 
-// Fast-path Poisson decision (see the error bound above).  Returns z, or
-// sets *undecided when u falls inside a threshold's uncertainty band or the
-// search passes z = 40.  The first three thresholds (z in {0, 1, 2}, ~99% of
-// draws at lambda ~ 0.4) are evaluated branch-free; only u beyond cdf_2
-// enters the sequential search.  Terms: t1 = e0 lambda, t2 = t1 lambda / 2
-// (the reference recurrence pmf *= lambda / k with an exact 1/2).
-__device__ __forceinline__ uint32_t fast_poisson(float lam, uint32_t y, bool* undecided) {
-  // u in [u_f, u_f + 2^-23): top 23 bits of the high word, no I2F
-  const float u = __fsub_rn(__int_as_float(0x3f800000 | (y >> 9)), 1.0f);
-  const float e0 = ex2_approx(__fmul_rn(lam, -1.4426950408889634f));
-  const float t1 = __fmul_rn(e0, lam);
-  const float c1 = __fadd_rn(e0, t1);
-  const float t2 = __fmul_rn(__fmul_rn(t1, lam), 0.5f);
-  const float c2 = __fadd_rn(c1, t2);
-  // one band for k = 0, 1, 2: with cdf_k, pmf_k <= 1 (+ rounding slack),
-  // m_k <= (r0 + 1.2e-6) + pl + 2.5e-7 = 1.93e-6 + 3.24e-6 lambda <= M
-  const float M = __fmaf_rn(3.3e-6f, lam, 2e-6f);
-  const float d0 = __fsub_rn(u, e0), d1 = __fsub_rn(u, c1), d2 = __fsub_rn(u, c2);
-  *undecided = *undecided || (fabsf(d0) <= M) || (fabsf(d1) <= M) || (fabsf(d2) <= M);
-  uint32_t z = (d0 > M) + (d1 > M) + (d2 > M);
-  if (z < 3 || *undecided) return z;
-  // sequential search from k = 3 (u beyond cdf_2): m_k = cdf_k (r0 + 6e-7 k)
-  // + pl pmf_k + 2.5e-7
-  const float r0 = __fmaf_rn(2.4e-7f, lam, 4.8e-7f);
-  const float pl = __fmul_rn(3e-6f, lam);
-  float pmf = t2, cdf = c2, zf = 2.0f;
-  float rk = __fadd_rn(r0, 1.2e-6f);
-  z = 2;
-  for (;;) {
-    ++z;
-    zf = __fadd_rn(zf, 1.0f);
-    pmf = __fmul_rn(pmf, __fmul_rn(lam, rcp_approx(zf)));
-    cdf = __fadd_rn(cdf, pmf);
-    rk = __fadd_rn(rk, 6e-7f);
-    const float mk = __fmaf_rn(cdf, rk, __fmaf_rn(pmf, pl, 2.5e-7f));
-    const float dk = __fsub_rn(u, cdf);
-    if (dk < -mk) return z;
-    if (!(dk > mk) || z >= 40) {
-      *undecided = true;
-      return 0;
-    }
-  }
-}
+// Fast-path Poisson decision (fast_poisson3 + fast_poisson_tail below; the
+// error bound above).  z is the first k with u <= cdf_k; a draw is left
+// undecided when u falls inside a threshold's band, or the search passes
+// z = 40.  The first three thresholds (z in {0, 1, 2}, ~99% of draws at
+// lambda ~ 0.4) are evaluated branch-free with one band: with cdf_k, pmf_k <= 1
+// (+ rounding slack), m_k <= (r0 + 1.2e-6) + pl + 2.5e-7 = 1.93e-6 + 3.24e-6
+// lambda <= M = 2e-6 + 3.3e-6 lambda (r0 = 4.8e-7 + 2.4e-7 lambda,
+// pl = 3e-6 lambda); only u beyond cdf_2 + M enters the sequential search,
+// with m_k = cdf_k (r0 + 1.2e-6 + 6e-7 (k - 2)) + pl pmf_k + 2.5e-7.  Terms:
+// t1 = e0 lambda, pmf_2 = t1 lambda / 2 (the reference recurrence
+// pmf *= lambda / k with an exact 1/2).
 
 #ifdef SAMELDA_DEFER_STATS
 // Diagnostics build only (tools/defer_stats.sh): why draws defer.
@@ -314,15 +277,6 @@ __device__ __forceinline__ void defer_stats(bool nz_exact, float prod, float lam
   atomicAdd(&g_defer_stats[8 + bin], 1ull);
 }
 #endif
-
-// phi-count scatter without a divergent branch: one predicated RED
-__device__ __forceinline__ void red_add_nz(unsigned long long* addr, uint32_t z) {
-  asm volatile(
-      "{\n\t.reg .pred p;\n\tsetp.ne.u32 p, %1, 0;\n\t"
-      "@p red.relaxed.gpu.global.add.u64 [%0], %2;\n\t}"
-      :
-      : "l"(addr), "r"(z), "l"(static_cast<unsigned long long>(z)));
-}
 
 struct Philox1 {
   // round-1 specialisation for counter {0, w, d, t}: M0 * 0 = 0, so the
@@ -341,16 +295,7 @@ struct Deferred {
   uint32_t mask[8];   // bit lane of mask[j]: topic kbase + lane + 32 j
 };
 
-// Lane = nonzero.  A warp owns 32 consecutive batch nonzeros and walks the
-// topics in chunks of 32; the topic index is warp-uniform, so the per-topic
-// stream keys (and the round-2 product M1 * (t ^ k1)) live in uniform
-// registers and a draw costs ~31 vector instructions of Philox.
-//   phase A: mu of every nonzero (lanes over topics, f32 tree), kept by its lane
-//   phase B, per chunk: phi[w_lane, chunk] staged through a swizzled shared
-//     tile (32 coalesced row loads), 32 draws per lane, z into a swizzled
-//     shared tile; then lanes over topics walk the 32 nonzeros in order:
-//     coalesced phi-count reductions and register theta accumulation per doc.
-// Round keys a draw of topic k needs in philox_y, precomputed once per topic:
+// Round keys a draw of topic k needs (philox_y_sched), precomputed once per topic:
 // ks[0] = k0, ks[1] = p2lo, ks[2] = p2hi (M1 * (t ^ k1)), then for r = 1..8
 // ks[1 + 2r] = k0 + r W0, ks[2 + 2r] = k1 + r W1 (ks[17] = k0 + 8 W0 unused).
 constexpr int kKeyWords = 20;
@@ -388,332 +333,6 @@ __device__ __forceinline__ uint32_t philox_y_sched(const Philox1 r1, const uint3
     x3 = a0;
   }
   return kPhiloxM1 * x2;
-}
-
-constexpr int kNzWarps = 4;
-
-__global__ void __launch_bounds__(kNzWarps * 32) k_sample_nz(
-    BatchView bv, const float* __restrict__ theta_b32, const float* __restrict__ phi32,
-    const double* __restrict__ mu_in, int K, double m_t, uint64_t seed, uint32_t t,
-    uint32_t sweep, unsigned long long* __restrict__ theta_counts,
-    unsigned long long* __restrict__ phi_counts, Deferred* __restrict__ deferred,
-    unsigned long long* __restrict__ n_deferred) {
-  // per warp: lambda tile (row = nonzero, col = topic, xor-swizzled; each
-  // entry is overwritten by its draw's z), deferred masks, and the 32
-  // topics' round-key schedules
-  __shared__ float s_lam[kNzWarps][32 * 32];  // lambda, then z in place
-  __shared__ uint32_t s_mask[kNzWarps][32 * 8];
-  __shared__ __align__(16) uint32_t s_keys[kNzWarps][32 * kKeyWords];
-  const int lane = threadIdx.x & 31;
-  const int wib = threadIdx.x >> 5;
-  const int64_t g0 = (static_cast<int64_t>(blockIdx.x) * kNzWarps + wib) * 32;
-  if (g0 >= bv.nnz) return;
-  const int n_here = static_cast<int>(min(static_cast<int64_t>(32), bv.nnz - g0));
-  const int64_t p = g0 + lane;
-  const bool valid = lane < n_here;
-  int64_t b = 0;
-  int32_t d = 0, w = 0, c = 0;
-  if (valid) {
-    b = find_row(bv.batch_prefix, bv.B, p);
-    d = __ldg(bv.batch_docs + b);
-    const int64_t gi = __ldg(bv.doc_offsets + d) + (p - __ldg(bv.batch_prefix + b));
-    w = __ldg(bv.word_ids + gi);
-    c = __ldg(bv.counts + gi);
-  }
-  // ---- phase A: mu (f32), lane r keeps nonzero r's
-  float my_mu = 0.0f;
-  if (mu_in != nullptr) {
-    my_mu = valid ? __double2float_rn(__ldg(mu_in + p)) : 1.0f;
-  } else {
-    for (int r = 0; r < n_here; ++r) {
-      const int64_t br = __shfl_sync(0xffffffffu, b, r);
-      const int32_t wr = __shfl_sync(0xffffffffu, w, r);
-      const float* tr = theta_b32 + br * K;
-      const float* pr = phi32 + static_cast<int64_t>(wr) * K;
-      // f64 sum of exact f32 x f32 products (error budget: any K)
-      double part = 0.0;
-      for (int k = lane; k < K; k += 32)
-        part = __dadd_rn(part, static_cast<double>(__ldg(tr + k)) * static_cast<double>(__ldg(pr + k)));
-#pragma unroll
-      for (int o = 16; o > 0; o >>= 1) part = __dadd_rn(part, __shfl_xor_sync(0xffffffffu, part, o));
-      if (lane == r) my_mu = __double2float_rn(part);
-    }
-  }
-  // lane flags: 0 fast, 1 all draws exact (mu unusable), 2 no draws (padding)
-  const int lane_mode = !valid ? 2 : ((!(my_mu >= 1e-20f) || isinf(my_mu)) ? 1 : 0);
-  const float scale = __fdividef(__double2float_rn(__dmul_rn(m_t, static_cast<double>(c))), my_mu);
-  const uint32_t dg = static_cast<uint32_t>(d + bv.doc_base);
-  uint32_t m1lo, m1hi;
-  mulhilo(kPhiloxM1, dg, m1lo, m1hi);
-  const Philox1 r1{m1hi ^ static_cast<uint32_t>(w), m1lo};
-  float* lt = s_lam[wib];
-  uint32_t* zt = reinterpret_cast<uint32_t*>(s_lam[wib]);
-  uint32_t* mk = s_mask[wib];
-  uint32_t* keys = s_keys[wib];
-  const int n_chunks = (K + 31) / 32;
-  for (int kc = 0; kc < n_chunks; ++kc) {
-    const int kbase = kc * 32;
-    const int k_lane = kbase + lane;
-    // ---- stage: lanes over topics.  lambda = (theta * phi) * scale exactly as
-    // the fast path defines it; -1 marks an exact (deferred) draw, -2 padding.
-    {
-      uint32_t ks[kKeyWords];
-      topic_schedule(seed, t, sweep, static_cast<uint32_t>(k_lane), ks);
-      uint4* kd = reinterpret_cast<uint4*>(keys + lane * kKeyWords);
-#pragma unroll
-      for (int q = 0; q < kKeyWords / 4; ++q) kd[q] = make_uint4(ks[4 * q], ks[4 * q + 1], ks[4 * q + 2], ks[4 * q + 3]);
-    }
-    for (int r = 0; r < 32; ++r) {
-      const int64_t br = __shfl_sync(0xffffffffu, b, r);
-      const int32_t wr = __shfl_sync(0xffffffffu, w, r);
-      const float sr = __shfl_sync(0xffffffffu, scale, r);
-      const int mr = __shfl_sync(0xffffffffu, lane_mode, r);
-      float v = -2.0f;
-      if (mr != 2 && k_lane < K) {
-        const float prod = __fmul_rn(__ldg(theta_b32 + br * K + k_lane),
-                                     __ldg(phi32 + static_cast<int64_t>(wr) * K + k_lane));
-        const float lam = __fmul_rn(prod, sr);
-        v = (mr == 0 && prod >= 1e-30f && lam < kInvMax) ? lam : -1.0f;
-      }
-      lt[r * 32 + (lane ^ r)] = v;
-    }
-    __syncwarp();
-    // ---- draw: lane = nonzero, kk = topic (uniform)
-    uint32_t defer_mask = 0;
-    const int kk_end = min(32, K - kbase);
-    for (int kk = 0; kk < kk_end; ++kk) {
-      const float lam = lt[lane * 32 + (kk ^ lane)];
-      uint32_t ks[kKeyWords];
-      const uint4* kd = reinterpret_cast<const uint4*>(keys + kk * kKeyWords);
-#pragma unroll
-      for (int q = 0; q < kKeyWords / 4; ++q) {
-        const uint4 v4 = kd[q];
-        ks[4 * q] = v4.x;
-        ks[4 * q + 1] = v4.y;
-        ks[4 * q + 2] = v4.z;
-        ks[4 * q + 3] = v4.w;
-      }
-      const uint32_t y = philox_y_sched(r1, ks);
-      uint32_t z = 0;
-      if (lam >= 0.0f) {
-        bool undecided = false;
-        z = fast_poisson(lam, y, &undecided);
-        if (undecided) {
-          defer_mask |= 1u << kk;
-          z = 0;
-        }
-      } else if (lam == -1.0f) {
-        defer_mask |= 1u << kk;
-      }
-      zt[lane * 32 + (kk ^ lane)] = z;
-    }
-    mk[lane * 8 + (kc & 7)] = defer_mask;
-    __syncwarp();
-    // ---- scatter: lanes over topics, nonzeros in order (sampler.cpp:183-189)
-    {
-      int64_t cb = -1;
-      uint32_t acc = 0;
-      const bool in_range = k_lane < K;  // lanes past K hold stale tile entries
-      for (int r = 0; r < n_here; ++r) {
-        const uint32_t zr = in_range ? zt[r * 32 + (lane ^ r)] : 0u;
-        const int64_t br = __shfl_sync(0xffffffffu, b, r);
-        const int32_t wr = __shfl_sync(0xffffffffu, w, r);
-        if (br != cb) {
-          if (acc) atomicAdd(theta_counts + cb * K + k_lane, static_cast<unsigned long long>(acc));
-          cb = br;
-          acc = 0;
-        }
-        if (zr) {
-          atomicAdd(phi_counts + static_cast<int64_t>(wr) * K + k_lane, static_cast<unsigned long long>(zr));
-          acc += zr;
-        }
-      }
-      if (acc) atomicAdd(theta_counts + cb * K + k_lane, static_cast<unsigned long long>(acc));
-    }
-    // deferred records per 256-topic block (same layout k_sample_deferred reads)
-    if ((kc & 7) == 7 || kc == n_chunks - 1) {
-      __syncwarp();
-      uint32_t any = 0;
-#pragma unroll
-      for (int j = 0; j < 8; ++j) any |= (j <= (kc & 7)) ? mk[lane * 8 + j] : 0u;
-      const uint32_t ball = __ballot_sync(0xffffffffu, any != 0);
-      if (ball) {
-        unsigned long long base = 0;
-        if (lane == 0) base = atomicAdd(n_deferred, static_cast<unsigned long long>(__popc(ball)));
-        base = __shfl_sync(0xffffffffu, base, 0);
-        if (any) {
-          Deferred rec;
-          rec.p = p;
-          rec.b = static_cast<int32_t>(b);
-          rec.w = w;
-          rec.c = c;
-          rec.kbase = (kc & ~7) * 32;
-#pragma unroll
-          for (int j = 0; j < 8; ++j) rec.mask[j] = (j <= (kc & 7)) ? mk[lane * 8 + j] : 0u;
-          deferred[base + __popc(ball & ((1u << lane) - 1u))] = rec;
-        }
-      }
-    }
-    __syncwarp();
-  }
-}
-
-// CTA = ceil(K/32) warps (K <= 1024); warp v owns topics [32v, 32v + 32) of
-// every nonzero the CTA processes, so a lane's topic -- and with it the
-// whole Philox round-key schedule -- is fixed for the kernel's lifetime and
-// lives in 18 registers (no per-draw key arithmetic).  Per group of 32
-// nonzeros: every lane forms its 32 products theta*phi, a warp transpose-
-// reduce (31 shuffles) leaves nonzero i's slice sum in lane i, the slices
-// are combined through shared memory after one barrier, then each warp draws
-// its 32 topics for the 32 nonzeros in order.
-constexpr int kCtaMaxWarps = 32;
-
-template <int NW>
-__device__ __forceinline__ float transpose_reduce(float (&v)[32], int lane) {
-  // after step s each lane holds partial sums for 32/2^s values
-#pragma unroll
-  for (int half = 16; half >= 1; half >>= 1) {
-    const bool upper = (lane & half) != 0;
-#pragma unroll
-    for (int i = 0; i < half; ++i) {
-      const float send = upper ? v[i] : v[i + half];
-      const float keep = upper ? v[i + half] : v[i];
-      v[i] = __fadd_rn(keep, __shfl_xor_sync(0xffffffffu, send, half));
-    }
-  }
-  return v[0];  // sum over lanes of original v[lane]
-}
-
-template <int MAXW>
-__global__ void __launch_bounds__(MAXW * 32) k_sample_cta(
-    BatchView bv, const float* __restrict__ theta_b32, const float* __restrict__ phi32,
-    const double* __restrict__ mu_in, int K, int nwarps, double m_t, uint64_t seed, uint32_t t,
-    uint32_t sweep, int64_t chunk, unsigned long long* __restrict__ theta_counts,
-    unsigned long long* __restrict__ phi_counts, Deferred* __restrict__ deferred,
-    unsigned long long* __restrict__ n_deferred) {
-  __shared__ float s_part[MAXW][33];
-  __shared__ uint32_t s_mask[32][MAXW + 1];
-  const int lane = threadIdx.x & 31;
-  const int wv = threadIdx.x >> 5;
-  const int k = wv * 32 + lane;
-  const bool k_ok = k < K;
-  const int64_t c0 = static_cast<int64_t>(blockIdx.x) * chunk;
-  const int64_t c1 = min(c0 + chunk, bv.nnz);
-  uint32_t ks[kKeyWords];
-  topic_schedule(seed, t, sweep, static_cast<uint32_t>(k), ks);
-  int64_t cur_b = -1;
-  uint32_t acc = 0;
-  for (int64_t g0 = c0; g0 < c1; g0 += 32) {
-    const int n_here = static_cast<int>(min(static_cast<int64_t>(32), c1 - g0));
-    // nonzero metadata, lane i <- nonzero g0 + i (every warp loads its own copy)
-    int64_t b = 0;
-    int32_t d = 0, w = 0, c = 0;
-    if (lane < n_here) {
-      const int64_t p = g0 + lane;
-      b = find_row(bv.batch_prefix, bv.B, p);
-      d = __ldg(bv.batch_docs + b);
-      const int64_t gi = __ldg(bv.doc_offsets + d) + (p - __ldg(bv.batch_prefix + b));
-      w = __ldg(bv.word_ids + gi);
-      c = __ldg(bv.counts + gi);
-    }
-    // products of this lane's topic for the 32 nonzeros
-    float prod[32];
-#pragma unroll
-    for (int i = 0; i < 32; ++i) {
-      const int64_t bi = __shfl_sync(0xffffffffu, b, i);
-      const int32_t wi = __shfl_sync(0xffffffffu, w, i);
-      float v = 0.0f;
-      if (i < n_here && k_ok) {
-        const float tk = __ldg(theta_b32 + bi * K + k);
-        v = __fmul_rn(tk, __ldg(phi32 + static_cast<int64_t>(wi) * K + k));
-      }
-      prod[i] = v;
-    }
-    float mu_lane;  // mu of nonzero g0 + lane
-    if (mu_in != nullptr) {
-      mu_lane = lane < n_here ? __double2float_rn(__ldg(mu_in + g0 + lane)) : 1.0f;
-    } else {
-      float tmp[32];
-#pragma unroll
-      for (int i = 0; i < 32; ++i) tmp[i] = prod[i];
-      // lane i ends with sum over lanes of tmp[i] -> warp-slice partial of nonzero i
-      const float part = transpose_reduce<32>(tmp, lane);
-      s_part[wv][lane] = part;
-      __syncthreads();
-      double mu = 0.0;  // f64 across warps: <= 5u + u for any K (error budget)
-      for (int v = 0; v < nwarps; ++v) mu = __dadd_rn(mu, static_cast<double>(s_part[v][lane]));
-      mu_lane = __double2float_rn(mu);
-    }
-    const bool lane_exact = !(mu_lane >= 1e-20f) || isinf(mu_lane);
-    const float scale = __fdividef(__double2float_rn(__dmul_rn(m_t, static_cast<double>(c))), mu_lane);
-    const uint32_t dg = static_cast<uint32_t>(d + bv.doc_base);
-    uint32_t m1lo, m1hi;
-    mulhilo(kPhiloxM1, dg, m1lo, m1hi);
-    const uint32_t hw_lane = m1hi ^ static_cast<uint32_t>(w);
-#pragma unroll
-    for (int i = 0; i < 32; ++i) {
-      if (i >= n_here) break;
-      const int64_t bi = __shfl_sync(0xffffffffu, b, i);
-      const int32_t wi = __shfl_sync(0xffffffffu, w, i);
-      const float sc = __shfl_sync(0xffffffffu, scale, i);
-      const bool ex_i = __shfl_sync(0xffffffffu, lane_exact, i);
-      const Philox1 r1{__shfl_sync(0xffffffffu, hw_lane, i), __shfl_sync(0xffffffffu, m1lo, i)};
-      if (bi != cur_b) {
-        if (cur_b >= 0 && acc) atomicAdd(theta_counts + cur_b * K + k, static_cast<unsigned long long>(acc));
-        cur_b = bi;
-        acc = 0;
-      }
-      const float lam = __fmul_rn(prod[i], sc);
-      const uint32_t y = philox_y_sched(r1, ks);
-      bool exact = k_ok && (ex_i || !(prod[i] >= 1e-30f) || !(lam < kInvMax));
-      uint32_t z = 0;
-      if (k_ok && !exact) {
-        bool undecided = false;
-        z = fast_poisson(lam, y, &undecided);
-        if (undecided) {
-          exact = true;
-          z = 0;
-        }
-        if (z) {
-          acc += z;
-          atomicAdd(phi_counts + static_cast<int64_t>(wi) * K + k, static_cast<unsigned long long>(z));
-        }
-      }
-      const uint32_t m = __ballot_sync(0xffffffffu, exact);
-      if (lane == i) s_mask[i][wv] = m;
-    }
-    __syncthreads();
-    // deferred records: nonzero i handled by warp (i % nwarps), lane 0
-    for (int i = wv; i < n_here; i += nwarps) {
-      for (int blk = 0; blk * 8 < nwarps; ++blk) {
-        uint32_t mk[8];
-        uint32_t any = 0;
-#pragma unroll
-        for (int j = 0; j < 8; ++j) {
-          const int v = blk * 8 + j;
-          mk[j] = v < nwarps ? s_mask[i][v] : 0u;
-          any |= mk[j];
-        }
-        if (any && lane == 0) {
-          const unsigned long long slot = atomicAdd(n_deferred, 1ull);
-          Deferred rec;
-          rec.p = g0 + i;
-          const int64_t p = g0 + i;
-          rec.b = static_cast<int32_t>(find_row(bv.batch_prefix, bv.B, p));
-          const int32_t dd = __ldg(bv.batch_docs + rec.b);
-          const int64_t gi = __ldg(bv.doc_offsets + dd) + (p - __ldg(bv.batch_prefix + rec.b));
-          rec.w = __ldg(bv.word_ids + gi);
-          rec.c = __ldg(bv.counts + gi);
-          rec.kbase = blk * 256;
-#pragma unroll
-          for (int j = 0; j < 8; ++j) rec.mask[j] = mk[j];
-          deferred[slot] = rec;
-        }
-      }
-    }
-    __syncthreads();
-  }
-  if (cur_b >= 0 && acc && k_ok) atomicAdd(theta_counts + cur_b * K + k, static_cast<unsigned long long>(acc));
 }
 
 // f32 mu of every batch nonzero over all K topics (fast path only; the exact
@@ -766,200 +385,10 @@ __global__ void __launch_bounds__(256) k_mu_f32(BatchView bv, const float* __res
   if (lane < n_here) mu_f[g0 + lane] = mine;
 }
 
-#ifndef SAMELDA_FAST_MINB
-#define SAMELDA_FAST_MINB 4
-#endif
-template <int KPL, bool FULL>
-__global__ void __launch_bounds__(kFastBlock, SAMELDA_FAST_MINB) k_sample_fast(
-    BatchView bv, const float* __restrict__ theta_b32, const float* __restrict__ phi32,
-    const double* __restrict__ mu_in, const float* __restrict__ mu_f_in, int K, double m_t,
-    uint64_t seed, uint32_t t, uint32_t sweep, int64_t chunk, int n_slices,
-    unsigned long long* __restrict__ theta_counts,
-    unsigned long long* __restrict__ phi_counts, Deferred* __restrict__ deferred,
-    unsigned long long* __restrict__ n_deferred) {
-  const int lane = threadIdx.x & 31;
-  // blockIdx.y = topic slice (all warps of a block share it, and with it the
-  // round-key table); blockIdx.x * warps + warp = nonzero chunk
-  const int64_t item = static_cast<int64_t>(blockIdx.x) * (kFastBlock / kWarp) + (threadIdx.x >> 5);
-  const int slice = static_cast<int>(blockIdx.y);
-  const int64_t p0 = item * chunk;
-  const int64_t p1 = min(p0 + chunk, bv.nnz);
-  const int kbase = slice * kWarp * KPL;
-  const int have_mu = mu_in != nullptr;
-
-  // Round-key schedules of the block's topics (rng.cpp:92-94 keys, bumped
-  // per round as in rng.cpp:31-32), built once per block into shared memory:
-  // every warp of the block works on the same topic slice, so topic
-  // kbase + lane + 32 j reads words [j][q][lane] -- conflict-free LDS.128.
-  __shared__ uint4 s_keys[KPL][kKeyWords / 4][kWarp];
-  for (int e = threadIdx.x; e < KPL * kWarp; e += blockDim.x) {
-    const int jj = e / kWarp, ll = e % kWarp;
-    uint32_t ks[kKeyWords];
-    topic_schedule(seed, t, sweep, static_cast<uint32_t>(kbase + ll + kWarp * jj), ks);
-#pragma unroll
-    for (int q = 0; q < kKeyWords / 4; ++q)
-      s_keys[jj][q][ll] = make_uint4(ks[4 * q], ks[4 * q + 1], ks[4 * q + 2], ks[4 * q + 3]);
-  }
-  __syncthreads();
-  int64_t cur_b = -1;
-  float th[KPL];
-  uint32_t acc[KPL];
-#pragma unroll
-  for (int j = 0; j < KPL; ++j) {
-    th[j] = 0.0f;
-    acc[j] = 0u;
-  }
-
-  for (int64_t g0 = p0; g0 < p1; g0 += kWarp) {
-    const int64_t p = g0 + lane;
-    int64_t b = 0;
-    int32_t d = 0, w = 0, c = 0;
-    double mu_v = 0.0;
-    float muf_v = 0.0f;
-    if (p < p1) {
-      b = find_row(bv.batch_prefix, bv.B, p);
-      d = __ldg(bv.batch_docs + b);
-      const int64_t gi = __ldg(bv.doc_offsets + d) + (p - __ldg(bv.batch_prefix + b));
-      w = __ldg(bv.word_ids + gi);
-      c = __ldg(bv.counts + gi);
-      if (have_mu) mu_v = __ldg(mu_in + p);
-      if (mu_f_in) muf_v = __ldg(mu_f_in + p);
-    }
-    const int n_here = static_cast<int>(min(static_cast<int64_t>(kWarp), p1 - g0));
-    for (int i = 0; i < n_here; ++i) {
-      const int64_t bi = __shfl_sync(0xffffffffu, b, i);
-      const int32_t dl = __shfl_sync(0xffffffffu, d, i);
-      const uint32_t di = static_cast<uint32_t>(dl + bv.doc_base);
-      const int32_t wi = __shfl_sync(0xffffffffu, w, i);
-      const int32_t ci = __shfl_sync(0xffffffffu, c, i);
-      const double mui = __shfl_sync(0xffffffffu, mu_v, i);
-      const float mufi = __shfl_sync(0xffffffffu, muf_v, i);
-      // phi[w, slice]: 32 lanes x KPL coalesced loads (occupancy hides latency)
-      float ph[KPL];
-      {
-        const float* prow = phi32 + static_cast<int64_t>(wi) * K;
-#pragma unroll
-        for (int j = 0; j < KPL; ++j) {
-          const int k = kbase + lane + kWarp * j;
-          ph[j] = (FULL || k < K) ? __ldg(prow + k) : 0.0f;
-        }
-      }
-      if (bi != cur_b) {
-        if (cur_b >= 0) {
-#pragma unroll
-          for (int j = 0; j < KPL; ++j) {
-            const int k = kbase + lane + kWarp * j;
-            if ((FULL || k < K) && acc[j])
-              atomicAdd(theta_counts + cur_b * K + k, static_cast<unsigned long long>(acc[j]));
-          }
-        }
-        cur_b = bi;
-#pragma unroll
-        for (int j = 0; j < KPL; ++j) {
-          const int k = kbase + lane + kWarp * j;
-          th[j] = (FULL || k < K) ? __ldg(theta_b32 + bi * K + k) : 0.0f;
-          acc[j] = 0u;
-        }
-      }
-      float prod[KPL];
-      float part = 0.0f;
-#pragma unroll
-      for (int j = 0; j < KPL; ++j) {
-        prod[j] = __fmul_rn(th[j], ph[j]);
-        part = __fadd_rn(part, prod[j]);
-      }
-      float mu_f;
-      if (have_mu) {
-        mu_f = __double2float_rn(mui);
-      } else if (mu_f_in) {
-        mu_f = mufi;  // full-K mu from k_mu_f32 (sliced K > 256)
-      } else {
-        mu_f = part;
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) mu_f = __fadd_rn(mu_f, __shfl_xor_sync(0xffffffffu, mu_f, o));
-        if (n_slices > 1) mu_f = 0.0f;  // partial sums only: defer the nonzero
-      }
-      const bool nz_exact = !(mu_f >= 1e-20f) || isinf(mu_f);
-      const float scale = __fdividef(__double2float_rn(__dmul_rn(m_t, static_cast<double>(ci))), mu_f);
-      uint32_t m1lo, m1hi;
-      mulhilo(kPhiloxM1, di, m1lo, m1hi);
-      const Philox1 r1{m1hi ^ static_cast<uint32_t>(wi), m1lo};
-      // phase 1: every topic's uniform (independent Philox chains -> ILP)
-      uint32_t y[KPL];
-#pragma unroll
-      for (int j = 0; j < KPL; ++j) {
-        uint32_t ks[kKeyWords];
-#pragma unroll
-        for (int q = 0; q < kKeyWords / 4; ++q) {
-          const uint4 v = s_keys[j][q][lane];
-          ks[4 * q] = v.x;
-          ks[4 * q + 1] = v.y;
-          ks[4 * q + 2] = v.z;
-          ks[4 * q + 3] = v.w;
-        }
-        y[j] = philox_y_sched(r1, ks);
-      }
-      // keep the KPL independent Philox chains here, interleaved, instead of
-      // letting the compiler sink each into its (divergent) decision below
-#pragma unroll
-      for (int j = 0; j < KPL; ++j) asm volatile("" : "+r"(y[j]));
-      // phase 2: decisions; undecidable draws are deferred.  Ineligible draws
-      // (lambda near or above 10: PTRS; tiny / non-finite products; unusable
-      // mu) enter undecided, which fast_poisson keeps and which skips
-      // its search loop.
-      uint32_t defer_bits = 0;
-#pragma unroll
-      for (int j = 0; j < KPL; ++j) {
-        const int k = kbase + lane + kWarp * j;
-        const float lam = __fmul_rn(prod[j], scale);
-        const bool lam_ok = !nz_exact && (prod[j] >= 1e-30f);
-        bool undecided = !lam_ok || !(lam < kInvMax);
-        uint32_t z = fast_poisson(lam, y[j], &undecided);
-        if (!FULL && k >= K) {
-          undecided = false, z = 0;
-        }
-#ifdef SAMELDA_DEFER_STATS
-        if (FULL || k < K) defer_stats(nz_exact, prod[j], lam, undecided);
-#endif
-        if (undecided) {
-          defer_bits |= 1u << j;
-          z = 0;
-        }
-        acc[j] += z;
-        red_add_nz(phi_counts + static_cast<int64_t>(wi) * K + k, z);
-      }
-      if (__any_sync(0xffffffffu, defer_bits != 0)) {
-        uint32_t masks[8];
-#pragma unroll
-        for (int j = 0; j < 8; ++j) masks[j] = j < KPL ? __ballot_sync(0xffffffffu, (defer_bits >> j) & 1u) : 0u;
-        if (lane == 0) {
-          const unsigned long long slot = atomicAdd(n_deferred, 1ull);
-          Deferred rec;
-          rec.p = g0 + i;
-          rec.b = static_cast<int32_t>(bi);
-          rec.w = wi;
-          rec.c = ci;
-          rec.kbase = kbase;
-#pragma unroll
-          for (int j = 0; j < 8; ++j) rec.mask[j] = masks[j];
-          deferred[slot] = rec;
-        }
-      }
-    }
-  }
-  if (cur_b >= 0) {
-#pragma unroll
-    for (int j = 0; j < KPL; ++j) {
-      const int k = kbase + lane + kWarp * j;
-      if ((FULL || k < K) && acc[j])
-        atomicAdd(theta_counts + cur_b * K + k, static_cast<unsigned long long>(acc[j]));
-    }
-  }
-}
-
 // ---------------------------------------------- sample (fast-exact, v2)
-// k_sample_v2: the same draws as k_sample_fast, bit for bit, with about a
-// third fewer instructions per draw (the kernel is issue-bound; ncu on the
+// k_sample_v2: the same draws as round 1's first fast-exact kernel
+// (k_sample_fast, since removed), bit for bit, with about a tenth fewer
+// instructions per draw (the kernel is issue-bound; ncu on the
 // fast kernel: 110 warp instructions per draw of which ~38 are the Philox
 // rounds and their round keys).  Differences:
 //   * the mu source is a template parameter (the period path's fused tree
@@ -981,7 +410,7 @@ __device__ __forceinline__ void red_add_u64(unsigned long long* addr, uint32_t z
 }
 
 // z in {0, 1, 2} decided branch-free, 3 = continue the search from k = 3
-// (see fast_poisson for the bound; c2 = fma(t1, lambda/2, c1) rounds once).
+// (bound above; c2 = fma(t1, lambda/2, c1) rounds once).
 // DEC selects how z and the band flag are formed (same decisions):
 //   0: predicates + nested selects (ALU pipe)
 //   1: z = sum of sat(2^100 (d_k - M)) on the FMA pipe, band by predicates
@@ -1020,12 +449,12 @@ __device__ __forceinline__ uint32_t fast_poisson3(float lam, float M, float Mb, 
   return __float_as_uint(__fadd_rn(zf, 8388608.0f)) - 0x4B000000u;
 }
 
-// sequential search from k = 3 (u beyond cdf_2 + M): fast_poisson's loop and
-// bound, with 1/k and the bound's k-term r_k - r_0 = 1.2e-6 + 6e-7 (k - 2)
+// sequential search from k = 3 (u beyond cdf_2 + M) with the bound above,
+// 1/k and the bound's k-term r_k - r_0 = 1.2e-6 + 6e-7 (k - 2)
 // read from constant tables (the step index is the same for every lane still
 // searching: one broadcast load) instead of rcp.approx and running sums; the
 // correctly rounded 1/k is within the 1-ulp rcp.approx the budget assumed.
-// Returns z, or sets *und (also at z = 40, like fast_poisson).
+// Returns z, or sets *und (also at z = 40).
 __constant__ float c_tail_inv[41] = {
     0.0f,        1.0f,         0.5f,         1.0f / 3,  0.25f,     0.2f,      1.0f / 6,
     1.0f / 7,    0.125f,       1.0f / 9,     0.1f,      1.0f / 11, 1.0f / 12, 1.0f / 13,
@@ -1491,10 +920,7 @@ int launch_fast_kpl(const BatchView& bv, const double* tb64, const float* tb32, 
   }
   auto* rec = static_cast<Deferred*>(deferred);
   const dim3 grid(static_cast<unsigned>((items + warps - 1) / warps), static_cast<unsigned>(n_slices));
-  const char* variant = getenv("SAMELDA_SAMPLER");
-  // the previous kernel, for A/B profiling (it always scatters phi counts)
-  const bool v1 = variant && variant[0] == 'o' && pc != nullptr;
-  if (!v1) {
+  {
     const int musrc = mu ? 1 : (muf ? 2 : 0);
     const bool full = K % (kWarp * KPL) == 0;
     if (pc == nullptr) {
@@ -1538,30 +964,10 @@ int launch_fast_kpl(const BatchView& bv, const double* tb64, const float* tb32, 
     }
 #undef SCU_V2
 #undef SCU_V2_LAUNCH
-  } else if (K % (kWarp * KPL) == 0)
-    k_sample_fast<KPL, true><<<grid, kFastBlock, 0, st>>>(
-        bv, tb32, phi32, mu, muf, K, m_t, seed, t, sweep, chunk, n_slices, tc, pc, rec, n_deferred);
-  else
-    k_sample_fast<KPL, false><<<grid, kFastBlock, 0, st>>>(
-        bv, tb32, phi32, mu, muf, K, m_t, seed, t, sweep, chunk, n_slices, tc, pc, rec, n_deferred);
+  }
   launch_deferred(bv, tb64, phi64, mu, K, m_t, seed, t, sweep, rec, n_deferred, aux,
                   bv.nnz * ((K + 255) / 256), draw_cap, tc, pc, err, st);
   return launched + 3;
-}
-
-int launch_fast_nz(const BatchView& bv, const double* tb64, const float* tb32, const double* phi64,
-                   const float* phi32, const double* mu, int K, double m_t, uint64_t seed,
-                   uint32_t t, uint32_t sweep, unsigned long long* tc, unsigned long long* pc,
-                   void* deferred, unsigned long long* n_deferred, void* aux, int64_t draw_cap,
-                   int* err, cudaStream_t st) {
-  const int64_t groups = (bv.nnz + 31) / 32;
-  cudaMemsetAsync(n_deferred, 0, sizeof(unsigned long long), st);
-  auto* rec = static_cast<Deferred*>(deferred);
-  k_sample_nz<<<static_cast<unsigned>((groups + kNzWarps - 1) / kNzWarps), kNzWarps * 32, 0, st>>>(
-      bv, tb32, phi32, mu, K, m_t, seed, t, sweep, tc, pc, rec, n_deferred);
-  launch_deferred(bv, tb64, phi64, mu, K, m_t, seed, t, sweep, rec, n_deferred, aux,
-                  bv.nnz * ((K + 255) / 256), draw_cap, tc, pc, err, st);
-  return 3;
 }
 
 // ------------------------------------------------------------------- M-step
@@ -2568,44 +1974,25 @@ int launch_sample_fast(const BatchView& bv, const double* theta_b64, const float
                        unsigned long long* n_deferred, void* aux, int64_t draw_cap, float* mu_f,
                        int* err, cudaStream_t st) {
   if (bv.nnz == 0) return 0;
-  // production: lane = topic, 8 topics per lane (k_sample_fast).  The two
-  // alternative layouts stay selectable for profiling (SAMELDA_SAMPLER=c|n);
-  // both are bit-identical and measured slower on B200.
+  // lane = topic, 8 topics per lane (k_sample_v2); K > 256 in topic slices of
+  // 256 with the full mu from a k_mu_f32 pre-pass.  SAMELDA_SAMPLER=x runs
+  // the all-f64 exact kernel instead when the caller supplies mu (per-call
+  // sample_counts): a device-side cross-check of the fast-exact path.
   const char* variant = getenv("SAMELDA_SAMPLER");
-  const char v = variant ? variant[0] : 'f';
-  // K > 256: topic slices of 256 with the full mu from a k_mu_f32 pre-pass
-  if (v == 'f' || v == 'o' || pc == nullptr) {
-    if (K <= 32)
-      return launch_fast_kpl<1>(bv, theta_b64, theta_b32, phi64, phi32, mu, K, m_t, seed, t, sweep, tc, pc,
-                                deferred, n_deferred, aux, draw_cap, mu_f, err, st);
-    if (K <= 64)
-      return launch_fast_kpl<2>(bv, theta_b64, theta_b32, phi64, phi32, mu, K, m_t, seed, t, sweep, tc, pc,
-                                deferred, n_deferred, aux, draw_cap, mu_f, err, st);
-    if (K <= 128)
-      return launch_fast_kpl<4>(bv, theta_b64, theta_b32, phi64, phi32, mu, K, m_t, seed, t, sweep, tc, pc,
-                                deferred, n_deferred, aux, draw_cap, mu_f, err, st);
-    return launch_fast_kpl<8>(bv, theta_b64, theta_b32, phi64, phi32, mu, K, m_t, seed, t, sweep, tc, pc,
+  if (variant && variant[0] == 'x' && mu != nullptr && pc != nullptr)
+    return launch_sample(bv, theta_b64, phi64, mu, K, m_t, seed, t, sweep, kModeParity, tc, pc,
+                         nullptr, nullptr, err, st);
+  if (K <= 32)
+    return launch_fast_kpl<1>(bv, theta_b64, theta_b32, phi64, phi32, mu, K, m_t, seed, t, sweep, tc, pc,
                               deferred, n_deferred, aux, draw_cap, mu_f, err, st);
-  }
-  if (v == 'c' && K <= 32 * kCtaMaxWarps) {
-    const int nwarps = (K + 31) / 32;
-    const int64_t chunk = 256;
-    cudaMemsetAsync(n_deferred, 0, sizeof(unsigned long long), st);
-    auto* rec = static_cast<Deferred*>(deferred);
-    const unsigned grid = static_cast<unsigned>((bv.nnz + chunk - 1) / chunk);
-    if (nwarps <= 8)
-      k_sample_cta<8><<<grid, nwarps * 32, 0, st>>>(bv, theta_b32, phi32, mu, K, nwarps, m_t, seed,
-                                                    t, sweep, chunk, tc, pc, rec, n_deferred);
-    else
-      k_sample_cta<kCtaMaxWarps><<<grid, nwarps * 32, 0, st>>>(bv, theta_b32, phi32, mu, K, nwarps,
-                                                               m_t, seed, t, sweep, chunk, tc, pc,
-                                                               rec, n_deferred);
-    launch_deferred(bv, theta_b64, phi64, mu, K, m_t, seed, t, sweep, rec, n_deferred, aux,
-                    bv.nnz * ((K + 255) / 256), draw_cap, tc, pc, err, st);
-    return 3;
-  }
-  return launch_fast_nz(bv, theta_b64, theta_b32, phi64, phi32, mu, K, m_t, seed, t, sweep, tc,
-                        pc, deferred, n_deferred, aux, draw_cap, err, st);
+  if (K <= 64)
+    return launch_fast_kpl<2>(bv, theta_b64, theta_b32, phi64, phi32, mu, K, m_t, seed, t, sweep, tc, pc,
+                              deferred, n_deferred, aux, draw_cap, mu_f, err, st);
+  if (K <= 128)
+    return launch_fast_kpl<4>(bv, theta_b64, theta_b32, phi64, phi32, mu, K, m_t, seed, t, sweep, tc, pc,
+                              deferred, n_deferred, aux, draw_cap, mu_f, err, st);
+  return launch_fast_kpl<8>(bv, theta_b64, theta_b32, phi64, phi32, mu, K, m_t, seed, t, sweep, tc, pc,
+                            deferred, n_deferred, aux, draw_cap, mu_f, err, st);
 }
 
 int launch_theta_from_counts(const unsigned long long* cu, const double* cf, int64_t n,

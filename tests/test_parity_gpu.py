@@ -701,3 +701,25 @@ def test_model_bin_and_metrics_csv_match_reference_training(port, tmp_path):
     drop_wall = lambda path: [ln.split(",")[:4] + ln.split(",")[5:]
                               for ln in open(path).read().splitlines()]
     assert drop_wall(oc) == drop_wall(rc)
+
+
+def test_exact_kernel_cross_check(port, monkeypatch):
+    """SAMELDA_SAMPLER=x: the all-f64 exact kernel (k_sample) on the per-call
+    path gives the same counts as the fast-exact path and the oracle, K=256
+    with PTRS-heavy rates."""
+    g = port.make_corpus(80, 300, 8, 150.0, 31)
+    rng = np.random.default_rng(2)
+    K = 256
+    theta = rng.gamma(0.3, 1.0, size=(g.n_docs, K)) + 1e-3
+    phi = rng.gamma(0.2, 1.0, size=(K, g.n_words)) + 1e-9
+    phi /= phi.sum(1, keepdims=True)
+    batch = rng.permutation(g.n_docs)[:60].astype(np.int32)
+    tb = theta[batch]
+    mu = port.sddmm(tb, phi, g, batch)
+    fast = S.sample_counts(tb, phi, mu, g, batch, 300.0, 5, 2, 1)
+    monkeypatch.setenv("SAMELDA_SAMPLER", "x")
+    exact = S.sample_counts(tb, phi, mu, g, batch, 300.0, 5, 2, 1)
+    otc, opc = port.sample_counts(tb, phi, mu, g, batch, 300.0, 5, 2, 1)
+    for sc in (fast, exact):
+        np.testing.assert_array_equal(sc.theta_counts, otc)
+        np.testing.assert_array_equal(sc.phi_counts, opc)
