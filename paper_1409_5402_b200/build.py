@@ -2,7 +2,7 @@
 
     python -m paper_1409_5402_b200.build
 
-kernels.cu is compiled with -fmad=false (reference-identical f64 rounding:
+the kernels_*.cu units are compiled with -fmad=false (reference-identical f64 rounding:
 the reference is an x86-64 build without FMA); capi.cu is host code.
 """
 from __future__ import annotations
@@ -21,8 +21,9 @@ ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 COMMON = ["-O3", "-lineinfo", "-std=c++20", "-Xcompiler", "-fPIC", "-I", CSRC,
           "-I", os.path.join(ROOT, "include")]
 UNITS = {
-    "kernels.cu": ["-fmad=false"],
-    "fast_kernels.cu": [],
+    "kernels_sample.cu": ["-fmad=false"],
+    "kernels_mstep.cu": ["-fmad=false"],
+    "kernels_eval.cu": ["-fmad=false"],
     "capi.cu": [],
     "synth.cpp": [],
     "corpus_io.cpp": [],

@@ -4,7 +4,7 @@
 // feeds the hot path (MinibatchStream corpus.cpp:252-285, anneal_m /
 // rho_schedule sampler.cpp:231-267, the train() period loop and its trace
 // bookkeeping sampler.cpp:269-353); every arithmetic step of the hot path
-// itself runs in the kernels of kernels.cu.  There is no CPU fallback: a
+// itself runs in the kernels of kernels_{sample,mstep,eval}.cu.  There is no CPU fallback: a
 // missing device is an error.
 #include <cuda_runtime.h>
 

@@ -735,22 +735,19 @@ int samelda_io_save_uci(const samelda_cu_corpus* corpus, const char* vocab, int6
         for (int64_t t = b; t < e; ++t) {
           std::string& s = bufs[t];
           const int64_t lo = d0 + t * step, hi = std::min(D, lo + step);
-          char line[80];
-          for (int64_t d = lo; d < hi; ++d) {
-            char dbuf[24];
-            const auto dn = std::to_chars(dbuf, dbuf + sizeof dbuf, d + 1).ptr - dbuf;
+          // "d w c\n": three integers of <= 20 digits each
+          char num[24];
+          auto put = [&](int64_t v, char sep) {
+            const auto r = std::to_chars(num, num + sizeof num, v);
+            s.append(num, static_cast<size_t>(r.ptr - num));
+            s.push_back(sep);
+          };
+          for (int64_t d = lo; d < hi; ++d)
             for (int64_t i = corpus->doc_offsets[d]; i < corpus->doc_offsets[d + 1]; ++i) {
-              char* q = line;
-              std::memcpy(q, dbuf, static_cast<size_t>(dn));
-              q += dn;
-              *q++ = ' ';
-              q = std::to_chars(q, line + sizeof line, static_cast<int64_t>(corpus->word_ids[i]) + 1).ptr;
-              *q++ = ' ';
-              q = std::to_chars(q, line + sizeof line, corpus->counts[i]).ptr;
-              *q++ = '\n';
-              s.append(line, static_cast<size_t>(q - line));
+              put(d + 1, ' ');
+              put(static_cast<int64_t>(corpus->word_ids[i]) + 1, ' ');
+              put(corpus->counts[i], '\n');
             }
-          }
         }
       });
       for (auto& s : bufs) ok = ok && std::fwrite(s.data(), 1, s.size(), f) == s.size();

@@ -51,7 +51,7 @@ int launch_sample(const BatchView& bv, const double* theta_batch, const double* 
                    int* err, cudaStream_t st);
 
 // Same draws, bit for bit, through an f32 fast path with exact f64 fallback
-// (see kernels.cu).  mu == nullptr: the kernel forms mu itself (period path).
+// (see kernels_sample.cu).  mu == nullptr: the kernel forms mu itself (period path).
 // mu_f_scratch: nnz floats (used when K > 256).
 // `deferred` holds up to nnz * ceil(K / 256) records of
 // deferred_record_bytes() each; n_deferred is one u64 of scratch; `aux` holds

@@ -1,38 +1,13 @@
-// kernels.cu -- sm_100a kernels for the SAME factored Gibbs sampler (parity and
-// expected-count modes).  Compiled with -fmad=false: every f64 expression
-// rounds like the reference's x86-64 (no FMA) build.  Each kernel cites the
-// reference loop it replaces.
-#include <cuda.h>
-#include <cuda_runtime.h>
-
-#include <cstdint>
-#include <algorithm>
-#include <cstdlib>
-
-#include "kernels.cuh"
-#include "philox.cuh"
+// kernels_sample.cu -- sm_100a sampling kernels: theta gather, SDDMM, the
+// exact f64 sampler, the fast-exact period sampler (k_sample_v2) with its
+// deferred exact passes, the K > 256 mu pre-pass and the expected-count
+// kernel.  Each kernel cites the reference loop it replaces.
+#include "kernels_common.cuh"
 #include "poisson.cuh"
 
 namespace scu {
 
 namespace {
-
-constexpr int kWarp = 32;
-
-__device__ __forceinline__ int64_t find_row(const int64_t* __restrict__ prefix, int64_t B,
-                                            int64_t p) {
-  // largest b in [0, B) with prefix[b] <= p; prefix[B] > p by construction
-  int64_t lo = 0, hi = B;
-  while (hi - lo > 1) {
-    const int64_t mid = (lo + hi) >> 1;
-    if (__ldg(prefix + mid) <= p) lo = mid; else hi = mid;
-  }
-  return lo;
-}
-
-inline unsigned grid_for(int64_t threads, int block) {
-  return static_cast<unsigned>((threads + block - 1) / block);
-}
 
 // ------------------------------------------------------------------- gather
 
@@ -970,823 +945,6 @@ int launch_fast_kpl(const BatchView& bv, const double* tb64, const float* tb32, 
   return launched + 3;
 }
 
-// ------------------------------------------------------------------- M-step
-
-__global__ void k_theta_from_counts(const unsigned long long* __restrict__ cu,
-                                    const double* __restrict__ cf, int64_t n, double m_t,
-                                    double alpha, double* __restrict__ out,
-                                    float* __restrict__ out32) {
-  const int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
-  if (i >= n) return;
-  const double hat = cu ? __ddiv_rn(static_cast<double>(static_cast<long long>(cu[i])), m_t)
-                        : __ddiv_rn(cf[i], m_t);
-  const double v = __dadd_rn(hat, alpha);
-  out[i] = v;
-  if (out32) out32[i] = __double2float_rn(v);
-}
-
-__global__ void k_theta_persist(const unsigned long long* __restrict__ cu,
-                                const double* __restrict__ cf,
-                                const int32_t* __restrict__ batch_docs, int64_t B, int K,
-                                double m_t, double alpha, double* __restrict__ theta) {
-  const int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
-  if (i >= B * K) return;
-  const int64_t b = i / K;
-  const int k = static_cast<int>(i - b * K);
-  const double hat = cu ? __ddiv_rn(static_cast<double>(static_cast<long long>(cu[i])), m_t)
-                        : __ddiv_rn(cf[i], m_t);
-  theta[static_cast<int64_t>(batch_docs[b]) * K + k] = __dadd_rn(hat, alpha);
-}
-
-// total[k] = sum over w, in order, of x[w,k] (sampler.cpp:214-218): one warp
-// per topic.  The 32 lanes fetch and convert 32 consecutive words in
-// parallel (x = count/m_t + beta, the reference's `value`), then every lane
-// runs the same sequential add chain over the 32 broadcast values, so the
-// summation order is exactly the reference's and the total is warp-uniform.
-template <int SRC>  // 0: u64 counts, 1: f64 expected counts, 2: plain f64 values
-__device__ __forceinline__ double col_value(const unsigned long long* __restrict__ cu,
-                                            const double* __restrict__ cf, int64_t i,
-                                            double m_t, double beta) {
-  if (SRC == 0) return __dadd_rn(__ddiv_rn(static_cast<double>(static_cast<long long>(cu[i])), m_t), beta);
-  if (SRC == 1) return __dadd_rn(__ddiv_rn(cf[i], m_t), beta);
-  return cf[i];
-}
-
-template <int SRC>
-__device__ __forceinline__ double col_raw(const unsigned long long* __restrict__ cu,
-                                          const double* __restrict__ cf, int64_t i) {
-  if (SRC == 0) return __longlong_as_double(static_cast<long long>(__ldg(cu + i)));
-  return __ldg(cf + i);
-}
-
-template <int SRC>
-__device__ __forceinline__ double col_convert(double raw, double m_t, double beta) {
-  if (SRC == 0) return __dadd_rn(__ddiv_rn(static_cast<double>(__double_as_longlong(raw)), m_t), beta);
-  if (SRC == 1) return __dadd_rn(__ddiv_rn(raw, m_t), beta);
-  return raw;
-}
-
-template <int SRC>
-__global__ void __launch_bounds__(256) k_col_totals(const unsigned long long* __restrict__ cu,
-                                                    const double* __restrict__ cf, int64_t W,
-                                                    int K, double m_t, double beta,
-                                                    double* __restrict__ totals,
-                                                    int* __restrict__ err) {
-  // The add chain (8.2-cycle FP64 latency, ~0.45 ms for W = 102,660) is the
-  // floor.  A ring of kDepth blocks of 32 raw words keeps the strided loads
-  // (~1 us from HBM) off the critical path; values are converted
-  // (count / m_t + beta) only when their block is consumed.
-  constexpr int kDepth = 8;
-  const int lane = threadIdx.x & 31;
-  const int k = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  if (k >= K) return;
-  double total = 0.0;
-  double ring[kDepth];
-#pragma unroll
-  for (int d = 0; d < kDepth; ++d) {
-    const int64_t w = static_cast<int64_t>(d) * 32 + lane;
-    ring[d] = w < W ? col_raw<SRC>(cu, cf, w * K + k) : 0.0;
-  }
-  // values past W are +0.0, which leaves a positive running total unchanged
-  for (int64_t w0 = 0; w0 < W; w0 += 32 * kDepth) {
-#pragma unroll
-    for (int d = 0; d < kDepth; ++d) {
-      const int64_t wv = w0 + static_cast<int64_t>(d) * 32 + lane;
-      const double v = wv < W ? col_convert<SRC>(ring[d], m_t, beta) : 0.0;
-      const int64_t wn = wv + 32 * kDepth;
-      ring[d] = wn < W ? col_raw<SRC>(cu, cf, wn * K + k) : 0.0;
-      if (w0 + d * 32 < W) {
-#pragma unroll
-        for (int j = 0; j < 32; ++j) total = __dadd_rn(total, __shfl_sync(0xffffffffu, v, j));
-      }
-    }
-  }
-  if (lane == 0) {
-    totals[k] = total;
-    if (err && (!(total > 0.0) || isinf(total))) atomicOr(err, kErrNumerical);
-  }
-}
-
-// total[k] = sum over w, in order, of x[w,k] (sampler.cpp:214-218), with x
-// precomputed in a parallel pass.  One warp per 32 topics, lane = topic:
-// 2-D TMA boxes of kChainRows W-rows x 32 topics stream through a
-// kChainStages-deep shared ring (k_col_chain).  The loop runs at the f64
-// add-chain latency (8.2 cycles per row) except for one barrier wait per box:
-// 256-row boxes (64 KB, 3 stages) put that overhead at ~5% (64-row boxes,
-// 8 stages: 0.63 ms; 128 x 6: 0.53 ms; 256 x 3: 0.48 ms at W = 102,660;
-// floor 0.44 ms).
-constexpr int kChainRows = 256;
-constexpr int kChainStages = 3;
-constexpr size_t kChainSmem = sizeof(double) * kChainStages * kChainRows * 32;
-
-__device__ __forceinline__ unsigned smem_addr(const void* p) {
-  return static_cast<unsigned>(__cvta_generic_to_shared(p));
-}
-
-__global__ void __launch_bounds__(32) k_col_chain(const __grid_constant__ CUtensorMap tmap,
-                                                  int64_t W, int K, double* __restrict__ totals,
-                                                  int* __restrict__ err) {
-  // ring[stage][row][32 topics], one 32 x 32 f64 TMA box per stage (rows past
-  // W / topics past K arrive zero-filled: +0.0 leaves the total unchanged).
-  // Lane 0 arms the stage's mbarrier with the box bytes and issues the
-  // tensor copy; the warp waits on the barrier phase and runs the add chain.
-  extern __shared__ __align__(128) double ring[];
-  __shared__ __align__(8) unsigned long long full[kChainStages];
-  const int lane = threadIdx.x;
-  const int k0 = blockIdx.x * 32;
-  const int64_t n_stages = (W + kChainRows - 1) / kChainRows;
-  if (lane == 0) {
-    for (int i = 0; i < kChainStages; ++i)
-      asm volatile("mbarrier.init.shared.b64 [%0], 1;" ::"r"(smem_addr(&full[i])));
-    asm volatile("fence.mbarrier_init.release.cluster;" ::);
-  }
-  __syncwarp();
-  auto issue = [&](int64_t st) {
-    if (lane != 0 || st >= n_stages) return;
-    const int slot = static_cast<int>(st % kChainStages);
-    const unsigned bar = smem_addr(&full[slot]);
-    asm volatile("fence.proxy.async.shared::cta;" ::);
-    asm volatile("mbarrier.arrive.expect_tx.shared.b64 _, [%0], %1;" ::"r"(bar),
-                 "r"(static_cast<unsigned>(kChainRows * 32 * sizeof(double))));
-    const int c0 = k0, c1 = static_cast<int>(st * kChainRows);
-    asm volatile(
-        "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes"
-        " [%0], [%1, {%2, %3}], [%4];" ::"r"(smem_addr(ring + static_cast<int64_t>(slot) * kChainRows * 32)),
-        "l"(reinterpret_cast<uint64_t>(&tmap)), "r"(c0), "r"(c1), "r"(bar)
-        : "memory");
-  };
-  for (int st = 0; st < kChainStages - 1; ++st) issue(st);
-  double total = 0.0;
-  for (int64_t st = 0; st < n_stages; ++st) {
-    issue(st + kChainStages - 1);
-    const int slot = static_cast<int>(st % kChainStages);
-    const unsigned parity = static_cast<unsigned>((st / kChainStages) & 1);
-    const unsigned bar = smem_addr(&full[slot]);
-    unsigned done = 0;
-    while (!done) {
-      asm volatile(
-          "{ .reg .pred p; mbarrier.try_wait.parity.shared.b64 p, [%1], %2; selp.u32 %0, 1, 0, p; }"
-          : "=r"(done)
-          : "r"(bar), "r"(parity)
-          : "memory");
-    }
-    const double* src = ring + static_cast<int64_t>(slot) * kChainRows * 32;
-#pragma unroll
-    for (int r = 0; r < kChainRows; ++r) total = __dadd_rn(total, src[r * 32 + lane]);
-    __syncwarp();
-  }
-  if (k0 + lane < K) {
-    totals[k0 + lane] = total;
-    if (err && (!(total > 0.0) || isinf(total))) atomicOr(err, kErrNumerical);
-  }
-}
-
-// 2-D tensor map over x[W][K] (f64), 32 x 32 boxes, zero fill out of bounds.
-bool make_chain_map(const double* x, int64_t W, int K, CUtensorMap* map) {
-  using EncodeFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
-                                const cuuint64_t*, const cuuint64_t*, const cuuint32_t*,
-                                const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
-                                CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
-  static EncodeFn encode = nullptr;
-  if (encode == nullptr) {
-    void* fn = nullptr;
-    cudaDriverEntryPointQueryResult q;
-    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) != cudaSuccess ||
-        q != cudaDriverEntryPointSuccess || fn == nullptr)
-      return false;
-    encode = reinterpret_cast<EncodeFn>(fn);
-  }
-  const cuuint64_t dims[2] = {static_cast<cuuint64_t>(K), static_cast<cuuint64_t>(W)};
-  const cuuint64_t strides[1] = {static_cast<cuuint64_t>(K) * sizeof(double)};
-  const cuuint32_t box[2] = {32, static_cast<cuuint32_t>(kChainRows)};
-  const cuuint32_t estr[2] = {1, 1};
-  return encode(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, const_cast<double*>(x), dims, strides, box,
-                estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
-                CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
-}
-
-// sequential column totals of x[W][K]: TMA chain when a tensor map can be
-// made (row stride a multiple of 16 B), else the warp-per-topic kernel
-int launch_col_sums(const double* x, int64_t W, int K, double* totals, int* err, cudaStream_t st) {
-  CUtensorMap map;
-  if ((K & 1) == 0 && make_chain_map(x, W, K, &map)) {
-    static bool configured = false;
-    if (!configured) {
-      cudaFuncSetAttribute(k_col_chain, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                           static_cast<int>(kChainSmem));
-      configured = true;
-    }
-    k_col_chain<<<static_cast<unsigned>((K + 31) / 32), 32, kChainSmem, st>>>(map, W, K, totals, err);
-  } else {
-    k_col_totals<2><<<grid_for(static_cast<int64_t>(K) * 32, 256), 256, 0, st>>>(nullptr, x, W, K, 1.0, 0.0, totals, err);
-  }
-  return 1;
-}
-
-// phi = (1 - rho) * phi + rho * cand / total (sampler.cpp:224-226); also
-// refreshes the f32 copy the sampler reads.
-__global__ void k_phi_blend_cand(const double* __restrict__ cand, const double* __restrict__ totals,
-                                 int64_t n, int K, double one_minus_rho, double rho,
-                                 double* __restrict__ phi_wk, float* __restrict__ phi32) {
-  const int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
-  if (i >= n) return;
-  const double v = __dadd_rn(__dmul_rn(one_minus_rho, phi_wk[i]),
-                             __ddiv_rn(__dmul_rn(rho, cand[i]), totals[static_cast<int>(i % K)]));
-  phi_wk[i] = v;
-  if (phi32) phi32[i] = __double2float_rn(v);
-}
-
-// cand[w,k] = count / m_t + beta (the reference's `value`, sampler.cpp:209)
-// cand = count / m_t + beta (sampler.cpp:211-218), two elements per thread
-// with 16-byte loads and stores (n is W x K; an odd tail is handled singly)
-__global__ void k_phi_candidate(const unsigned long long* __restrict__ cu,
-                                const double* __restrict__ cf, int64_t n, double m_t,
-                                double beta, double* __restrict__ cand) {
-  const int64_t i2 = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
-  const int64_t i = 2 * i2;
-  if (i + 1 < n) {
-    double a, b;
-    if (cu) {
-      const ulonglong2 v = __ldg(reinterpret_cast<const ulonglong2*>(cu) + i2);
-      a = __ddiv_rn(static_cast<double>(static_cast<long long>(v.x)), m_t);
-      b = __ddiv_rn(static_cast<double>(static_cast<long long>(v.y)), m_t);
-    } else {
-      const double2 v = __ldg(reinterpret_cast<const double2*>(cf) + i2);
-      a = __ddiv_rn(v.x, m_t);
-      b = __ddiv_rn(v.y, m_t);
-    }
-    reinterpret_cast<double2*>(cand)[i2] = make_double2(__dadd_rn(a, beta), __dadd_rn(b, beta));
-  } else if (i < n) {
-    const double hat = cu ? __ddiv_rn(static_cast<double>(static_cast<long long>(cu[i])), m_t)
-                          : __ddiv_rn(cf[i], m_t);
-    cand[i] = __dadd_rn(hat, beta);
-  }
-}
-
-__global__ void k_to_f32(const double* __restrict__ x, int64_t n, float* __restrict__ y) {
-  const int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
-  if (i < n) y[i] = __double2float_rn(x[i]);
-}
-
-// ---------------------------------------------------------------- init phi
-// Entry (k, w) of the reference's row-major K x W walk is uniform number
-// i = k*W + w of one stream keyed (0,0,0,phi_init): block i/2, words
-// 2(i%2), 2(i%2)+1.  Written into the word-major layout.
-__global__ void k_phi_init_values(double* __restrict__ phi_wk, int64_t W, int K,
-                                  double init_noise, uint32_t k0, uint32_t k1) {
-  const int64_t idx = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
-  if (idx >= W * K) return;
-  const int64_t w = idx / K;
-  const int k = static_cast<int>(idx - w * K);
-  const uint64_t i = static_cast<uint64_t>(k) * static_cast<uint64_t>(W) + w;
-  const U4 r = philox10(U4{static_cast<uint32_t>(i >> 1), 0u, 0u, 0u}, k0, k1);
-  const uint64_t x = (i & 1) ? join64(r.z, r.w) : join64(r.x, r.y);
-  phi_wk[idx] = __dadd_rn(1.0, __dmul_rn(init_noise, u64_to_uniform(x)));
-}
-
-__global__ void k_div_cols(double* __restrict__ x, int64_t n, int K,
-                           const double* __restrict__ totals) {
-  const int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
-  if (i >= n) return;
-  x[i] = __ddiv_rn(x[i], totals[i % K]);
-}
-
-__global__ void k_fill(double* __restrict__ p, int64_t n, double v) {
-  const int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
-  if (i < n) p[i] = v;
-}
-
-__global__ void k_transpose(const double* __restrict__ in, int64_t rows, int64_t cols,
-                            double* __restrict__ out) {
-  __shared__ double tile[32][33];
-  const int64_t c0 = blockIdx.x * 32ll, r0 = blockIdx.y * 32ll;
-  for (int dy = threadIdx.y; dy < 32; dy += blockDim.y) {
-    const int64_t r = r0 + dy, c = c0 + threadIdx.x;
-    if (r < rows && c < cols) tile[dy][threadIdx.x] = in[r * cols + c];
-  }
-  __syncthreads();
-  for (int dy = threadIdx.y; dy < 32; dy += blockDim.y) {
-    const int64_t c = c0 + dy, r = r0 + threadIdx.x;
-    if (r < rows && c < cols) out[c * rows + r] = tile[threadIdx.x][dy];
-  }
-}
-
-// --------------------------------------------------------------------- eval
-// eval.cpp:99-121, one thread per test document.
-__global__ void k_eval_split(const int64_t* __restrict__ doc_offsets,
-                             const int32_t* __restrict__ counts,
-                             const int64_t* __restrict__ token_offsets, int64_t n_docs,
-                             uint64_t seed, int32_t* __restrict__ slots,
-                             int32_t* __restrict__ fold_counts,
-                             int32_t* __restrict__ score_counts) {
-  const int64_t d = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
-  if (d >= n_docs) return;
-  const int64_t begin = doc_offsets[d], end = doc_offsets[d + 1];
-  int32_t* sl = slots + token_offsets[d];
-  int64_t pos = 0;
-  for (int64_t i = begin; i < end; ++i) {
-    fold_counts[i] = 0;
-    score_counts[i] = 0;
-    for (int32_t r = 0; r < counts[i]; ++r) sl[pos++] = static_cast<int32_t>(i - begin);
-  }
-  const int64_t n_tokens = pos;
-  Stream s;
-  s.init(seed, 0u, static_cast<uint32_t>(d), 0u, make_tag(kEvalSplit, 0, 0));
-  for (int64_t i = n_tokens - 1; i > 0; --i) {
-    const int64_t j = static_cast<int64_t>(s.uniform_below(static_cast<uint64_t>(i) + 1));
-    const int32_t tmp = sl[i];
-    sl[i] = sl[j];
-    sl[j] = tmp;
-  }
-  const int64_t n_fold = (n_tokens + 1) / 2;
-  for (int64_t i = 0; i < n_tokens; ++i) {
-    if (i < n_fold) ++fold_counts[begin + sl[i]]; else ++score_counts[begin + sl[i]];
-  }
-}
-
-__device__ __forceinline__ double warp_max(double v) {
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) v = fmax(v, __shfl_xor_sync(0xffffffffu, v, o));
-  return v;
-}
-
-// One warp per test document: fold-in (eval.cpp:19-64) then scoring
-// (eval.cpp:125-145).  Dot products mu / p run lane-per-cell in sequential k
-// order; the responsibility update runs lane-per-topic in cell order, so all
-// f64 sums accumulate in the reference's order.
-constexpr int kEvalWarps = 4;
-
-// sum_k th[k] * row[k] in sequential k order (product then add, no FMA),
-// 16-byte loads when the row is 16-byte aligned (K even)
-__device__ __forceinline__ double seq_dot(const double* __restrict__ th,
-                                          const double* __restrict__ row, int K) {
-  double dot = 0.0;
-  if ((K & 1) == 0) {
-    const double2* r2 = reinterpret_cast<const double2*>(row);
-    // unrolled so several row loads are in flight ahead of the (sequential) adds
-#pragma unroll 8
-    for (int k2 = 0; k2 < (K >> 1); ++k2) {
-      const double2 v = __ldg(r2 + k2);
-      dot = __dadd_rn(dot, __dmul_rn(th[2 * k2], v.x));
-      dot = __dadd_rn(dot, __dmul_rn(th[2 * k2 + 1], v.y));
-    }
-  } else {
-    for (int k = 0; k < K; ++k) dot = __dadd_rn(dot, __dmul_rn(th[k], __ldg(row + k)));
-  }
-  return dot;
-}
-
-__global__ void __launch_bounds__(kEvalWarps * 32) k_eval_docs(
-    const int64_t* __restrict__ doc_offsets, const int32_t* __restrict__ word_ids,
-    const int32_t* __restrict__ fold_counts, const int32_t* __restrict__ score_counts,
-    int64_t n_docs, const double* __restrict__ phi_wk, int K, double alpha, int sweeps,
-    double* __restrict__ doc_logp, int64_t* __restrict__ doc_scored,
-    double* __restrict__ theta_out, double* __restrict__ scratch, int* __restrict__ err) {
-  extern __shared__ double smem[];
-  const int wib = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int64_t slot = blockIdx.x * static_cast<int64_t>(kEvalWarps) + wib;
-  const int64_t per = 2 * static_cast<int64_t>(K);
-  double* th = scratch ? scratch + slot * per : smem + wib * per;
-  double* nx = th + K;
-  const double inv_k = 1.0 / static_cast<double>(K);
-  for (int64_t doc = slot; doc < n_docs; doc += static_cast<int64_t>(gridDim.x) * kEvalWarps) {
-    const int64_t base = doc_offsets[doc];
-    const int64_t n = doc_offsets[doc + 1] - base;
-    for (int k = lane; k < K; k += 32) th[k] = inv_k;
-    __syncwarp();
-    for (int sweep = 0; sweep < sweeps && n > 0; ++sweep) {
-      for (int k = lane; k < K; k += 32) nx[k] = alpha;
-      for (int64_t i0 = 0; i0 < n; i0 += 32) {
-        const int64_t i = i0 + lane;
-        int32_t w = 0;
-        double scale = 0.0;
-        bool use = false;
-        if (i < n) {
-          const int32_t fc = fold_counts[base + i];
-          w = word_ids[base + i];
-          if (fc != 0) {  // a zero-count cell adds exactly +0 (eval.cpp:43-47)
-            const double mu = seq_dot(th, phi_wk + static_cast<int64_t>(w) * K, K);
-            if (mu > 0.0) {
-              scale = __ddiv_rn(static_cast<double>(fc), mu);
-              use = true;
-            }
-          }
-        }
-        unsigned mask = __ballot_sync(0xffffffffu, use);
-        __syncwarp();
-        while (mask) {
-          const int src = __ffs(mask) - 1;
-          mask &= mask - 1;
-          const double s = __shfl_sync(0xffffffffu, scale, src);
-          const int32_t ww = __shfl_sync(0xffffffffu, w, src);
-          const double* ph = phi_wk + static_cast<int64_t>(ww) * K;
-          for (int k = lane; k < K; k += 32)
-            nx[k] = __dadd_rn(nx[k], __dmul_rn(__dmul_rn(s, th[k]), __ldg(ph + k)));
-        }
-      }
-      __syncwarp();
-      double total = 0.0;
-      if (lane == 0)
-        for (int k = 0; k < K; ++k) total = __dadd_rn(total, nx[k]);
-      total = __shfl_sync(0xffffffffu, total, 0);
-      double delta = 0.0;
-      for (int k = lane; k < K; k += 32) {
-        const double v = __ddiv_rn(nx[k], total);
-        delta = fmax(delta, fabs(__dadd_rn(v, -th[k])));
-        th[k] = v;
-      }
-      delta = warp_max(delta);
-      __syncwarp();
-      if (delta < 1e-12) break;
-    }
-    // score the held-back half in cell order
-    double logp = 0.0;
-    int64_t scored = 0;
-    for (int64_t i0 = 0; i0 < n; i0 += 32) {
-      const int64_t i = i0 + lane;
-      int32_t sc = 0;
-      double term = 0.0;
-      if (i < n) {
-        sc = score_counts[base + i];
-        if (sc != 0) {
-          const double p = seq_dot(th, phi_wk + static_cast<int64_t>(word_ids[base + i]) * K, K);
-          if (!(p > 0.0)) atomicOr(err, kErrNumerical);
-          term = __dmul_rn(static_cast<double>(sc), log(p));
-        }
-      }
-      const int n_here = static_cast<int>(min(static_cast<int64_t>(32), n - i0));
-      for (int j = 0; j < n_here; ++j) {
-        const int32_t scj = __shfl_sync(0xffffffffu, sc, j);
-        const double tj = __shfl_sync(0xffffffffu, term, j);
-        if (scj != 0) {
-          logp = __dadd_rn(logp, tj);
-          scored += scj;
-        }
-      }
-    }
-    if (lane == 0) {
-      doc_logp[doc] = logp;
-      doc_scored[doc] = scored;
-    }
-    if (theta_out)
-      for (int k = lane; k < K; k += 32) theta_out[doc * K + k] = th[k];
-    __syncwarp();
-  }
-}
-
-// CTA per test document (K <= kEvalCtaMaxK): the same arithmetic in the same
-// order as k_eval_docs / eval.cpp:19-64, laid out so a document's phi rows
-// stay L2-resident across its fold-in sweeps (~600 documents in flight, their
-// fold rows ~90 MB) and every step has block-wide parallelism:
-//   phase 1, thread = cell: mu_i = sequential-k dot (eval.cpp:38-41), scale
-//     c_i / mu_i for the cells that inform theta;
-//   phase 2, thread = topic: next[k] += (scale_i theta[k]) phi[w_i][k] over
-//     the chunk's cells in cell order (eval.cpp:45-49) -- coalesced rows;
-//   phase 3: total in sequential k order (one thread), theta = next / total,
-//     block max of |delta| (eval.cpp:51-60).
-// Scoring: thread = cell dot, doc log p summed in cell order by one thread.
-constexpr int kEvalCtaThreads = 256;
-constexpr int kEvalCtaMaxK = 4096;
-
-__global__ void __launch_bounds__(kEvalCtaThreads) k_eval_cta(
-    const int64_t* __restrict__ doc_offsets, const int32_t* __restrict__ word_ids,
-    const int32_t* __restrict__ fold_counts, const int32_t* __restrict__ score_counts,
-    int64_t n_docs, const double* __restrict__ phi_wk, int K, double alpha, int sweeps,
-    double* __restrict__ doc_logp, int64_t* __restrict__ doc_scored,
-    double* __restrict__ theta_out, int* __restrict__ err) {
-  extern __shared__ double smem[];
-  double* th = smem;                 // K
-  double* nx = th + K;               // K
-  double* cs = nx + K;               // [256] cell scale (0 = skip) / score term
-  int32_t* cw = reinterpret_cast<int32_t*>(cs + kEvalCtaThreads);  // [256] cell word
-  __shared__ double s_red[kEvalCtaThreads / 32];
-  __shared__ int64_t s_cnt[kEvalCtaThreads];
-  __shared__ double s_total;
-  __shared__ int s_done;
-  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
-  const double inv_k = 1.0 / static_cast<double>(K);
-  for (int64_t doc = blockIdx.x; doc < n_docs; doc += gridDim.x) {
-    const int64_t base = doc_offsets[doc];
-    const int64_t n = doc_offsets[doc + 1] - base;
-    for (int k = tid; k < K; k += kEvalCtaThreads) th[k] = inv_k;
-    __syncthreads();
-    for (int sweep = 0; sweep < sweeps && n > 0; ++sweep) {
-      for (int k = tid; k < K; k += kEvalCtaThreads) nx[k] = alpha;
-      for (int64_t i0 = 0; i0 < n; i0 += kEvalCtaThreads) {
-        const int n_here = static_cast<int>(min(static_cast<int64_t>(kEvalCtaThreads), n - i0));
-        if (tid < n_here) {
-          const int64_t i = base + i0 + tid;
-          const int32_t fc = __ldg(fold_counts + i);
-          const int32_t w = __ldg(word_ids + i);
-          double scale = 0.0;
-          if (fc != 0) {  // a zero-count cell adds exactly +0 (eval.cpp:43-47)
-            const double mu = seq_dot(th, phi_wk + static_cast<int64_t>(w) * K, K);
-            if (mu > 0.0) scale = __ddiv_rn(static_cast<double>(fc), mu);
-          }
-          cs[tid] = scale;
-          cw[tid] = w;
-        }
-        __syncthreads();
-        for (int k = tid; k < K; k += kEvalCtaThreads) {
-          double acc = nx[k];
-          const double tk = th[k];
-#pragma unroll 4
-          for (int c = 0; c < n_here; ++c) {
-            const double sc = cs[c];
-            if (sc != 0.0)
-              acc = __dadd_rn(acc, __dmul_rn(__dmul_rn(sc, tk),
-                                             __ldg(phi_wk + static_cast<int64_t>(cw[c]) * K + k)));
-          }
-          nx[k] = acc;
-        }
-        __syncthreads();
-      }
-      if (tid == 0) {
-        double total = 0.0;
-        for (int k = 0; k < K; ++k) total = __dadd_rn(total, nx[k]);
-        s_total = total;
-      }
-      __syncthreads();
-      const double total = s_total;
-      double delta = 0.0;
-      for (int k = tid; k < K; k += kEvalCtaThreads) {
-        const double v = __ddiv_rn(nx[k], total);
-        delta = fmax(delta, fabs(__dadd_rn(v, -th[k])));
-        th[k] = v;
-      }
-      delta = warp_max(delta);
-      if (lane == 0) s_red[wid] = delta;
-      __syncthreads();
-      if (tid == 0) {
-        double d = s_red[0];
-        for (int w = 1; w < kEvalCtaThreads / 32; ++w) d = fmax(d, s_red[w]);
-        s_done = d < 1e-12;
-      }
-      __syncthreads();
-      if (s_done) break;
-    }
-    // score the held-back half (eval.cpp:125-145), log p summed in cell order
-    double logp = 0.0;
-    int64_t scored = 0;
-    for (int64_t i0 = 0; i0 < n; i0 += kEvalCtaThreads) {
-      const int n_here = static_cast<int>(min(static_cast<int64_t>(kEvalCtaThreads), n - i0));
-      if (tid < n_here) {
-        const int64_t i = base + i0 + tid;
-        const int32_t sc = __ldg(score_counts + i);
-        double term = 0.0;
-        if (sc != 0) {
-          const double pr = seq_dot(th, phi_wk + static_cast<int64_t>(__ldg(word_ids + i)) * K, K);
-          if (!(pr > 0.0)) atomicOr(err, kErrNumerical);
-          term = __dmul_rn(static_cast<double>(sc), log(pr));
-        }
-        cs[tid] = term;
-        s_cnt[tid] = sc;
-      }
-      __syncthreads();
-      if (tid == 0)
-        for (int c = 0; c < n_here; ++c)
-          if (s_cnt[c] != 0) {
-            logp = __dadd_rn(logp, cs[c]);
-            scored += s_cnt[c];
-          }
-      __syncthreads();
-    }
-    if (tid == 0) {
-      doc_logp[doc] = logp;
-      doc_scored[doc] = scored;
-    }
-    if (theta_out)
-      for (int k = tid; k < K; k += kEvalCtaThreads) theta_out[doc * K + k] = th[k];
-    __syncthreads();
-  }
-}
-
-// k_eval_stage: k_eval_cta with a document's first R fold rows staged in
-// shared memory once per document, so the 2 x sweeps row reads of those cells
-// come from shared memory instead of L2 (the fold-in is L2-bound: 845 GB at
-// NYTimes shape).  Fold cells (fold count > 0; a zero-count cell adds exactly
-// +0, eval.cpp:43-47) are compacted per window of <= kEvalFoldMax in cell
-// order; arithmetic and order are k_eval_cta's (eval.cpp:19-64):
-//   phase 1, thread = fold cell: sequential-k mu, scale = c / mu (or skip);
-//   phase 2, thread = topic: next[k] += (scale theta[k]) phi[w][k] in fold order;
-//   phase 3: sequential total (one thread), theta = next / total, max |delta|.
-// Staged rows use an odd stride (K | 1 doubles): the thread-per-cell dots hit
-// distinct banks.
-constexpr int kEvalFoldMax = 1024;
-
-__device__ __forceinline__ double seq_dot_stride1(const double* __restrict__ th,
-                                                  const double* row, int K) {
-  double dot = 0.0;
-#pragma unroll 8
-  for (int k = 0; k < K; ++k) dot = __dadd_rn(dot, __dmul_rn(th[k], row[k]));
-  return dot;
-}
-
-__global__ void __launch_bounds__(kEvalCtaThreads) k_eval_stage(
-    const int64_t* __restrict__ doc_offsets, const int32_t* __restrict__ word_ids,
-    const int32_t* __restrict__ fold_counts, const int32_t* __restrict__ score_counts,
-    int64_t n_docs, const double* __restrict__ phi_wk, int K, double alpha, int sweeps,
-    int R, double* __restrict__ doc_logp, int64_t* __restrict__ doc_scored,
-    double* __restrict__ theta_out, int* __restrict__ err) {
-  extern __shared__ double smem[];
-  const int KP = K | 1;
-  double* th = smem;                     // K
-  double* nx = th + K;                   // K
-  double* fs = nx + K;                   // [kEvalFoldMax] scale per fold cell
-  int32_t* fw = reinterpret_cast<int32_t*>(fs + kEvalFoldMax);  // word per fold cell
-  int32_t* fc = fw + kEvalFoldMax;                              // fold count per fold cell
-  double* rows = reinterpret_cast<double*>(fc + kEvalFoldMax);   // R x KP staged rows
-  __shared__ double s_red[kEvalCtaThreads / 32];
-  __shared__ int s_wc[kEvalCtaThreads / 32];
-  __shared__ int64_t s_cnt[kEvalCtaThreads];
-  __shared__ double s_total;
-  __shared__ int s_done;
-  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
-  const double inv_k = 1.0 / static_cast<double>(K);
-
-  // documents are handed out dynamically (their fold-in lengths differ:
-  // 1 to 50 sweeps, tens to thousands of cells): counter at doc_scored[n_docs]
-  __shared__ int64_t s_doc;
-  unsigned long long* next_doc = reinterpret_cast<unsigned long long*>(doc_scored + n_docs);
-  for (;;) {
-    if (threadIdx.x == 0) s_doc = static_cast<int64_t>(atomicAdd(next_doc, 1ull));
-    __syncthreads();
-    const int64_t doc = s_doc;
-    __syncthreads();
-    if (doc >= n_docs) break;
-    const int64_t base = doc_offsets[doc];
-    const int64_t n = doc_offsets[doc + 1] - base;
-    // compact the fold cells of cells [c_begin, ...) into fw/fc, whole chunks
-    // of 256 cells while they fit; returns the first cell not taken
-    auto build = [&](int64_t c_begin, int& nf) -> int64_t {
-      nf = 0;
-      int64_t c0 = c_begin;
-      while (c0 < n && nf + kEvalCtaThreads <= kEvalFoldMax) {
-        const int64_t c = c0 + tid;
-        const int32_t f = c < n ? __ldg(fold_counts + base + c) : 0;
-        const unsigned bal = __ballot_sync(0xffffffffu, f > 0);
-        if (lane == 0) s_wc[wid] = __popc(bal);
-        __syncthreads();
-        int before = 0, total = 0;
-#pragma unroll
-        for (int w = 0; w < kEvalCtaThreads / 32; ++w) {
-          before += w < wid ? s_wc[w] : 0;
-          total += s_wc[w];
-        }
-        if (f > 0) {
-          const int pos = nf + before + __popc(bal & ((1u << lane) - 1u));
-          fw[pos] = __ldg(word_ids + base + c);
-          fc[pos] = f;
-        }
-        nf += total;
-        c0 += kEvalCtaThreads;
-        __syncthreads();
-      }
-      return c0;
-    };
-    int nf0 = 0;
-    const int64_t end0 = build(0, nf0);
-    const bool multi = end0 < n;
-    const int Reff = min(nf0, R);
-    for (int i = tid; i < Reff * K; i += kEvalCtaThreads) {
-      const int f = i / K, k = i - f * K;
-      rows[f * KP + k] = __ldg(phi_wk + static_cast<int64_t>(fw[f]) * K + k);
-    }
-    for (int k = tid; k < K; k += kEvalCtaThreads) th[k] = inv_k;
-    __syncthreads();
-    for (int sweep = 0; sweep < sweeps && n > 0; ++sweep) {
-      for (int k = tid; k < K; k += kEvalCtaThreads) nx[k] = alpha;
-      int64_t cw0 = 0;
-      bool first = true;
-      while (cw0 < n) {
-        int nf = nf0;
-        int64_t cnext = end0;
-        if (multi) cnext = build(cw0, nf);  // lists of later windows overwrite window 0's
-        const int rs = first ? Reff : 0;     // staged rows belong to window 0
-        for (int f0 = 0; f0 < nf; f0 += kEvalCtaThreads) {
-          const int f = f0 + tid;
-          if (f < nf) {
-            const double mu = f < rs ? seq_dot_stride1(th, rows + f * KP, K)
-                                     : seq_dot(th, phi_wk + static_cast<int64_t>(fw[f]) * K, K);
-            fs[f] = mu > 0.0 ? __ddiv_rn(static_cast<double>(fc[f]), mu) : 0.0;
-          }
-        }
-        __syncthreads();
-        for (int k = tid; k < K; k += kEvalCtaThreads) {
-          double acc = nx[k];
-          const double tk = th[k];
-          // branch-free (scale 0 adds +0 exactly), loads batch across iterations
-#pragma unroll 8
-          for (int f = 0; f < rs; ++f)
-            acc = __dadd_rn(acc, __dmul_rn(__dmul_rn(fs[f], tk), rows[f * KP + k]));
-#pragma unroll 8
-          for (int f = rs; f < nf; ++f)
-            acc = __dadd_rn(acc, __dmul_rn(__dmul_rn(fs[f], tk),
-                                           __ldg(phi_wk + static_cast<int64_t>(fw[f]) * K + k)));
-          nx[k] = acc;
-        }
-        __syncthreads();
-        cw0 = cnext;
-        first = false;
-      }
-      if (tid == 0) {
-        double total = 0.0;
-        for (int k = 0; k < K; ++k) total = __dadd_rn(total, nx[k]);
-        s_total = total;
-      }
-      __syncthreads();
-      const double total = s_total;
-      double delta = 0.0;
-      for (int k = tid; k < K; k += kEvalCtaThreads) {
-        const double v = __ddiv_rn(nx[k], total);
-        delta = fmax(delta, fabs(__dadd_rn(v, -th[k])));
-        th[k] = v;
-      }
-      delta = warp_max(delta);
-      if (lane == 0) s_red[wid] = delta;
-      __syncthreads();
-      if (tid == 0) {
-        double d = s_red[0];
-        for (int w = 1; w < kEvalCtaThreads / 32; ++w) d = fmax(d, s_red[w]);
-        s_done = d < 1e-12;
-      }
-      __syncthreads();
-      if (s_done) break;
-    }
-    // score the held-back half (eval.cpp:125-145), log p summed in cell order
-    double logp = 0.0;
-    int64_t scored = 0;
-    for (int64_t i0 = 0; i0 < n; i0 += kEvalCtaThreads) {
-      const int n_here = static_cast<int>(min(static_cast<int64_t>(kEvalCtaThreads), n - i0));
-      if (tid < n_here) {
-        const int64_t i = base + i0 + tid;
-        const int32_t sc = __ldg(score_counts + i);
-        double term = 0.0;
-        if (sc != 0) {
-          const double pr = seq_dot(th, phi_wk + static_cast<int64_t>(__ldg(word_ids + i)) * K, K);
-          if (!(pr > 0.0)) atomicOr(err, kErrNumerical);
-          term = __dmul_rn(static_cast<double>(sc), log(pr));
-        }
-        fs[tid] = term;
-        s_cnt[tid] = sc;
-      }
-      __syncthreads();
-      if (tid == 0)
-        for (int c = 0; c < n_here; ++c)
-          if (s_cnt[c] != 0) {
-            logp = __dadd_rn(logp, fs[c]);
-            scored += s_cnt[c];
-          }
-      __syncthreads();
-    }
-    if (tid == 0) {
-      doc_logp[doc] = logp;
-      doc_scored[doc] = scored;
-    }
-    if (theta_out)
-      for (int k = tid; k < K; k += kEvalCtaThreads) theta_out[doc * K + k] = th[k];
-    __syncthreads();
-  }
-}
-
-// eval.cpp:148-158: the document-order reduction.  The block stages 1024
-// documents at a time in shared memory (coalesced); one thread then adds
-// them in document order at the f64 add latency instead of a global-load
-// latency per document.
-constexpr int kOrderedBlock = 1024;
-
-__global__ void __launch_bounds__(kOrderedBlock) k_ordered_ll(
-    const double* __restrict__ doc_logp, const int64_t* __restrict__ doc_scored, int64_t n_docs,
-    double* __restrict__ ll_out, int* __restrict__ err) {
-  __shared__ double s_lp[kOrderedBlock];
-  __shared__ int64_t s_sc[kOrderedBlock];
-  double total = 0.0;
-  int64_t scored = 0;
-  for (int64_t d0 = 0; d0 < n_docs; d0 += kOrderedBlock) {
-    const int n = static_cast<int>(min(static_cast<int64_t>(kOrderedBlock), n_docs - d0));
-    if (threadIdx.x < n) {
-      s_lp[threadIdx.x] = doc_logp[d0 + threadIdx.x];
-      s_sc[threadIdx.x] = doc_scored[d0 + threadIdx.x];
-    }
-    __syncthreads();
-    if (threadIdx.x == 0) {
-#pragma unroll 8
-      for (int i = 0; i < n; ++i) {
-        total = __dadd_rn(total, s_lp[i]);
-        scored += s_sc[i];
-      }
-    }
-    __syncthreads();
-  }
-  if (threadIdx.x != 0) return;
-  if (scored == 0) {
-    atomicOr(err, kErrNumerical);
-    *ll_out = 0.0;
-    return;
-  }
-  *ll_out = __ddiv_rn(total, static_cast<double>(scored));
-}
-
 // k_expected: the deterministic expected-count path (z := rate,
 // sampler.cpp:151-193 with poisson_sample replaced by its mean; tolerance 1e-5
 // relative against the oracle) in the period kernel's layout: lane = topic,
@@ -1918,11 +1076,10 @@ int launch_sample_kpl(const BatchView& bv, const double* theta_batch, const doub
   return 1;
 }
 
-constexpr size_t kEvalSmemMax = 200 * 1024;
-
 }  // namespace
 
 // ------------------------------------------------------------- launchers
+
 
 int launch_gather_theta(const double* theta, const int32_t* batch_docs, int64_t B, int K,
                         double* theta_batch, float* theta_batch32, cudaStream_t st) {
@@ -1995,171 +1152,6 @@ int launch_sample_fast(const BatchView& bv, const double* theta_b64, const float
                             deferred, n_deferred, aux, draw_cap, mu_f, err, st);
 }
 
-int launch_theta_from_counts(const unsigned long long* cu, const double* cf, int64_t n,
-                             double m_t, double alpha, double* out, float* out32,
-                             cudaStream_t st) {
-  if (n == 0) return 0;
-  k_theta_from_counts<<<grid_for(n, 256), 256, 0, st>>>(cu, cf, n, m_t, alpha, out, out32);
-  return 1;
-}
-
-int launch_theta_persist(const unsigned long long* cu, const double* cf,
-                         const int32_t* batch_docs, int64_t B, int K, double m_t, double alpha,
-                         double* theta, cudaStream_t st) {
-  if (B * K == 0) return 0;
-  k_theta_persist<<<grid_for(B * K, 256), 256, 0, st>>>(cu, cf, batch_docs, B, K, m_t, alpha,
-                                                       theta);
-  return 1;
-}
-
-int launch_phi_mstep(const unsigned long long* cu, const double* cf, int64_t W, int K,
-                     double m_t, double beta, double rho, double* phi_wk, float* phi32,
-                     double* cand, double* totals, int* err, cudaStream_t st) {
-  const int64_t n = W * K;
-  if (n == 0) return 0;
-  k_phi_candidate<<<grid_for((n + 1) / 2, 256), 256, 0, st>>>(cu, cf, n, m_t, beta, cand);
-  launch_col_sums(cand, W, K, totals, err, st);
-  k_phi_blend_cand<<<grid_for(n, 256), 256, 0, st>>>(cand, totals, n, K, 1.0 - rho, rho, phi_wk,
-                                                     phi32);
-  return 3;
-}
-
-int launch_to_f32(const double* x, int64_t n, float* y, cudaStream_t st) {
-  if (n == 0) return 0;
-  k_to_f32<<<grid_for(n, 256), 256, 0, st>>>(x, n, y);
-  return 1;
-}
-
-int launch_phi_init(double* phi_wk, int64_t W, int K, double init_noise, uint64_t seed,
-                    double* totals, cudaStream_t st) {
-  const int64_t n = W * K;
-  if (n == 0) return 0;
-  if (!(init_noise > 0.0)) {
-    k_fill<<<grid_for(n, 256), 256, 0, st>>>(phi_wk, n, 1.0 / static_cast<double>(W));
-    return 1;
-  }
-  uint32_t k0, k1;
-  stream_key(seed, make_tag(kPhiInit, 0, 0), k0, k1);
-  k_phi_init_values<<<grid_for(n, 256), 256, 0, st>>>(phi_wk, W, K, init_noise, k0, k1);
-  launch_col_sums(phi_wk, W, K, totals, nullptr, st);
-  k_div_cols<<<grid_for(n, 256), 256, 0, st>>>(phi_wk, n, K, totals);
-  return 3;
-}
-
-int launch_fill(double* p, int64_t n, double v, cudaStream_t st) {
-  if (n == 0) return 0;
-  k_fill<<<grid_for(n, 256), 256, 0, st>>>(p, n, v);
-  return 1;
-}
-
-int launch_transpose(const double* in, int64_t rows, int64_t cols, double* out,
-                     cudaStream_t st) {
-  if (rows * cols == 0) return 0;
-  dim3 grid(static_cast<unsigned>((cols + 31) / 32), static_cast<unsigned>((rows + 31) / 32));
-  k_transpose<<<grid, dim3(32, 8), 0, st>>>(in, rows, cols, out);
-  return 1;
-}
-
-int launch_eval_split(const int64_t* doc_offsets, const int32_t* counts,
-                      const int64_t* token_offsets, int64_t n_docs, uint64_t seed,
-                      int32_t* slots, int32_t* fold_counts, int32_t* score_counts,
-                      cudaStream_t st) {
-  if (n_docs == 0) return 0;
-  k_eval_split<<<grid_for(n_docs, 128), 128, 0, st>>>(doc_offsets, counts, token_offsets,
-                                                      n_docs, seed, slots, fold_counts,
-                                                      score_counts);
-  return 1;
-}
-
-int64_t eval_scratch_doubles(int K) {
-  // theta / next (2K doubles per warp) live in shared memory up to
-  // kEvalSmemMax per block; beyond that, a global scratch for a capped grid
-  const size_t smem = static_cast<size_t>(kEvalWarps) * 2 * K * sizeof(double);
-  if (smem <= kEvalSmemMax) return 0;
-  return static_cast<int64_t>(148) * 4 * kEvalWarps * 2 * K;
-}
-
-int launch_eval_docs(const int64_t* doc_offsets, const int32_t* word_ids,
-                     const int32_t* fold_counts, const int32_t* score_counts, int64_t n_docs,
-                     const double* phi_wk, int K, double alpha, int sweeps, double* doc_logp,
-                     int64_t* doc_scored, double* theta_out, double* scratch,
-                     int64_t scratch_doubles, int* err, cudaStream_t st) {
-  if (n_docs == 0) return 0;
-  const char* ev = getenv("SAMELDA_EVAL");  // A/B: "cta", "warp"; default staged
-  if (K <= 1024 && !(ev && (ev[0] == 'c' || ev[0] == 'w')) && !getenv("SAMELDA_EVAL_WARP")) {
-    // staged rows: 3 CTAs per SM share (almost) all of shared memory
-    // (measured: 1 / 2 / 3 CTAs 176 / 148 / 139 ms at NYTimes shape;
-    // SAMELDA_EVAL_CTAS_PER_SM overrides)
-    const char* cps_env = getenv("SAMELDA_EVAL_CTAS_PER_SM");
-    const int cps = cps_env ? max(1, atoi(cps_env)) : 3;
-    const int KP = K | 1;
-    const size_t fixed = (2 * static_cast<size_t>(K) + kEvalFoldMax) * sizeof(double) +
-                         2 * kEvalFoldMax * sizeof(int32_t);
-    const size_t budget = (220u * 1024u) / static_cast<size_t>(cps);
-    if (budget > fixed + static_cast<size_t>(KP) * sizeof(double)) {
-      const int R = static_cast<int>(std::min<size_t>((budget - fixed) / (KP * sizeof(double)), static_cast<size_t>(kEvalFoldMax)));
-      const size_t smem_s = fixed + static_cast<size_t>(R) * KP * sizeof(double);
-      static size_t configured_s = 48 * 1024;
-      if (smem_s > configured_s) {
-        cudaFuncSetAttribute(k_eval_stage, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             static_cast<int>(220 * 1024));
-        configured_s = 220 * 1024;
-      }
-      const int64_t blocks = min(n_docs, static_cast<int64_t>(148 * cps));
-      // the dynamic document counter lives one past the per-document results
-      cudaMemsetAsync(doc_scored + n_docs, 0, sizeof(int64_t), st);
-      k_eval_stage<<<static_cast<unsigned>(blocks), kEvalCtaThreads, smem_s, st>>>(
-          doc_offsets, word_ids, fold_counts, score_counts, n_docs, phi_wk, K, alpha, sweeps, R,
-          doc_logp, doc_scored, theta_out, err);
-      return 1;
-    }
-  }
-  if (K <= kEvalCtaMaxK && !(ev && ev[0] == 'w') && !getenv("SAMELDA_EVAL_WARP")) {
-    const size_t smem_c = (2 * static_cast<size_t>(K) + kEvalCtaThreads) * sizeof(double) +
-                          kEvalCtaThreads * sizeof(int32_t);
-    static size_t configured_c = 48 * 1024;
-    if (smem_c > configured_c) {
-      cudaFuncSetAttribute(k_eval_cta, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                           static_cast<int>(smem_c));
-      configured_c = smem_c;
-    }
-    // ~600 documents in flight: their fold rows stay L2-resident across sweeps
-    const int64_t blocks = min(n_docs, static_cast<int64_t>(148 * 4));
-    k_eval_cta<<<static_cast<unsigned>(blocks), kEvalCtaThreads, smem_c, st>>>(
-        doc_offsets, word_ids, fold_counts, score_counts, n_docs, phi_wk, K, alpha, sweeps,
-        doc_logp, doc_scored, theta_out, err);
-    return 1;
-  }
-  const size_t smem = static_cast<size_t>(kEvalWarps) * 2 * K * sizeof(double);
-  int64_t blocks = (n_docs + kEvalWarps - 1) / kEvalWarps;
-  if (smem <= kEvalSmemMax) {
-    static size_t configured = 48 * 1024;
-    if (smem > configured) {
-      cudaFuncSetAttribute(k_eval_docs, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                           static_cast<int>(kEvalSmemMax));
-      configured = kEvalSmemMax;
-    }
-    k_eval_docs<<<static_cast<unsigned>(blocks), kEvalWarps * 32, smem, st>>>(
-        doc_offsets, word_ids, fold_counts, score_counts, n_docs, phi_wk, K, alpha, sweeps,
-        doc_logp, doc_scored, theta_out, nullptr, err);
-  } else {
-    const int64_t per_block = static_cast<int64_t>(kEvalWarps) * 2 * K;
-    int64_t cap = scratch_doubles / per_block;
-    if (cap < 1) cap = 1;
-    if (blocks > cap) blocks = cap;
-    k_eval_docs<<<static_cast<unsigned>(blocks), kEvalWarps * 32, 0, st>>>(
-        doc_offsets, word_ids, fold_counts, score_counts, n_docs, phi_wk, K, alpha, sweeps,
-        doc_logp, doc_scored, theta_out, scratch, err);
-  }
-  return 1;
-}
-
-int launch_ordered_ll(const double* doc_logp, const int64_t* doc_scored, int64_t n_docs,
-                      double* ll_out, int* err, cudaStream_t st) {
-  k_ordered_ll<<<1, kOrderedBlock, 0, st>>>(doc_logp, doc_scored, n_docs, ll_out, err);
-  return 1;
-}
-
 }  // namespace scu
 
 #ifdef SAMELDA_DEFER_STATS
@@ -2172,3 +1164,4 @@ extern "C" int samelda_debug_defer_stats(unsigned long long* out, int reset) {
   return 0;
 }
 #endif
+
