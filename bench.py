@@ -48,6 +48,12 @@ CONFIGS = {
                              inner_sweeps=2, schedule="constant", mode="expected",
                              workload="NYTimes-shaped synthetic corpus, K=256, m=100, bf=0.05, "
                                       "2 inner sweeps, expected-count mode"),
+    # throughput mode: same sampler, own f32 random streams
+    # (statistical, not bit, parity with the reference)
+    "nytimes-fast": dict(corpus="nytimes", n_topics=256, m=100.0, batch_fraction=0.05,
+                         inner_sweeps=2, schedule="constant", mode="throughput",
+                         workload="NYTimes-shaped synthetic corpus, K=256, m=100, bf=0.05, "
+                                  "2 inner sweeps, throughput mode (f32, own random streams)"),
     # BASELINE.json configs[4]
     "k1024": dict(corpus="nytimes", n_topics=1024, m=50.0, batch_fraction=0.05, inner_sweeps=2,
                   schedule="constant",
@@ -306,7 +312,8 @@ def run_ours(args, cfg):
     scfg = S.SamplerConfig(n_topics=cfg["n_topics"], m=cfg["m"], schedule=cfg["schedule"],
                            batch_fraction=cfg["batch_fraction"], inner_sweeps=cfg["inner_sweeps"],
                            t_max=args.warmup + args.steps + 2 * max(1, min(args.steps, 10)), seed=1,
-                           mode=S.MODE_EXPECTED if cfg.get("mode") == "expected" else S.MODE_PARITY)
+                           mode={"expected": S.MODE_EXPECTED, "throughput": S.MODE_THROUGHPUT}.get(
+                               cfg.get("mode"), S.MODE_PARITY))
     trainer = S.Trainer(train, scfg, ctx=ctx)
     trainer.set_doc_base(doc_base)
     if rank == 0:
@@ -483,7 +490,8 @@ def run_ours(args, cfg):
                                   "so frac can exceed 1 for an L2-resident kernel -- see traffic "
                                   "for DRAM bytes",
                          "frac": achieved / peak if peak else None, "traffic": traffic,
-                         "kernel": "k_expected" if cfg.get("mode") == "expected" else "k_sample_v2 + deferred (parity)", "peak_kind": peaks_kind,
+                         "kernel": {"expected": "k_expected", "throughput": "k_sample_thru"}.get(
+                             cfg.get("mode"), "k_sample_v2 + deferred (parity)"), "peak_kind": peaks_kind,
                          "alg_bytes_per_launch": alg_bytes / max(prof["sample_launches"], 1),
                          "avg_launch_ms": sample_ms / max(prof["sample_launches"], 1),
                          "sample_share_of_step": sample_ms / prof_ms if prof_ms else None,

@@ -33,6 +33,9 @@ extern "C" {
 /* sampling modes */
 #define SAMELDA_CU_MODE_PARITY 0   /* reference-identical Poisson replicas, f64 */
 #define SAMELDA_CU_MODE_EXPECTED 1 /* deterministic factored expected counts, f64 */
+#define SAMELDA_CU_MODE_THROUGHPUT 2 /* the same Poisson replicas on this library's own
+                                        random streams in f32: statistically, not
+                                        bit-for-bit, the reference's sampler */
 
 /* AnnealSchedule (sampler.hpp:17) */
 #define SAMELDA_CU_SCHEDULE_CONSTANT 0

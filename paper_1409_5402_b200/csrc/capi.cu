@@ -208,7 +208,8 @@ void validate_config(const samelda_cu_config* c) {
   if (!(c->alpha > 0.0) || !(c->beta > 0.0)) fail(SAMELDA_CU_CONFIG, "alpha and beta must be positive");
   if (!(c->init_noise >= 0.0) || !std::isfinite(c->init_noise))
     fail(SAMELDA_CU_CONFIG, "init_noise must be finite and >= 0");
-  if (c->mode != SAMELDA_CU_MODE_PARITY && c->mode != SAMELDA_CU_MODE_EXPECTED)
+  if (c->mode != SAMELDA_CU_MODE_PARITY && c->mode != SAMELDA_CU_MODE_EXPECTED &&
+      c->mode != SAMELDA_CU_MODE_THROUGHPUT)
     fail(SAMELDA_CU_CONFIG, "unknown sampling mode %d", c->mode);
   if (c->schedule < 0 || c->schedule > 3) fail(SAMELDA_CU_CONFIG, "unknown schedule %d", c->schedule);
 }
@@ -491,11 +492,15 @@ struct samelda_cu_ctx {
     } else {
       ensure<unsigned long long>(tc, B_ * K_);
       ensure<unsigned long long>(pc, W_ * K_);
+      if (K_ > 256) ensure<float>(mu_f32, nnz_);
+      if (mode == SAMELDA_CU_MODE_THROUGHPUT) {
+        for (int i = 0; i < 2; ++i) stage(B_);
+        return;
+      }
       const int64_t records = nnz_ * ((K_ + 255) / 256);
       ensure<unsigned char>(deferred, records * scu::deferred_record_bytes());
       ensure<unsigned char>(deferred_aux, scu::deferred_aux_bytes(records, draw_cap_for(records)));
       ensure<unsigned long long>(n_deferred, 1);
-      if (K_ > 256) ensure<float>(mu_f32, nnz_);
     }
     for (int i = 0; i < 2; ++i) stage(B_);
   }
@@ -526,10 +531,18 @@ struct samelda_cu_ctx {
       ck(cudaMemsetAsync(tc_, 0, sizeof(unsigned long long) * std::max<int64_t>(bv.B * K_, 1), stream), "zero tc");
       // a non-final inner sweep of the K = 256 period kernel skips the phi-count
       // scatter (only the last sweep's phi counts feed update_model)
-      const bool skip_phi = !need_phi && K_ == 256 && mu_d == nullptr;
+      const bool skip_phi =
+          !need_phi && mu_d == nullptr && (K_ == 256 || mode == SAMELDA_CU_MODE_THROUGHPUT);
       if (skip_phi) pc_ = nullptr;
       else ck(cudaMemsetAsync(pc_, 0, sizeof(unsigned long long) * std::max<int64_t>(W_ * K_, 1), stream), "zero pc");
       tick(kSample, true);
+      if (mode == SAMELDA_CU_MODE_THROUGHPUT) {
+        launches += scu::launch_sample_throughput(
+            bv, theta_b32, phi_wk32, K_, m_t_, seed, static_cast<uint32_t>(t), static_cast<uint32_t>(sweep),
+            tc_, pc_, K_ > 256 ? ensure<float>(mu_f32, bv.nnz) : nullptr, stream);
+        tick(kSample, false);
+        return;
+      }
       const int64_t records = bv.nnz * ((K_ + 255) / 256);
       const int64_t draw_cap = draw_cap_for(records);
       void* rec = ensure<unsigned char>(deferred, records * scu::deferred_record_bytes());

@@ -63,6 +63,13 @@ int launch_sample_fast(const BatchView& bv, const double* theta_b64, const float
                        unsigned long long* theta_counts, unsigned long long* phi_counts,
                        void* deferred, unsigned long long* n_deferred, void* aux,
                        int64_t draw_cap, float* mu_f_scratch, int* err, cudaStream_t st);
+// Throughput mode: the same sampler on its own random
+// streams in f32, four draws per Philox block, no deferral -- statistically,
+// not bit-for-bit, the reference's.  mu_f_scratch: nnz floats when K > 256.
+int launch_sample_throughput(const BatchView& bv, const float* theta_b32, const float* phi32, int K,
+                             double m_t, uint64_t seed, uint32_t t, uint32_t sweep,
+                             unsigned long long* theta_counts, unsigned long long* phi_counts,
+                             float* mu_f_scratch, cudaStream_t st);
 int64_t deferred_record_bytes();
 int64_t deferred_aux_bytes(int64_t max_records, int64_t draw_cap);
 

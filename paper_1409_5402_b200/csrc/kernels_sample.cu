@@ -875,6 +875,229 @@ void launch_deferred(const BatchView& bv, const double* tb64, const double* phi6
                                             tc, pc, err);
 }
 
+// ----------------------------------------------- sample (throughput mode)
+// k_sample_thru: SURVEY 7 step 9's throughput mode -- the same SAME sampler
+// (Poisson replicas of rate (theta phi / mu) m c, counts scattered as in
+// parity mode) on this library's own random streams in f32, so statistically,
+// not bit-for-bit, the reference's sampler.
+//
+//   * one Philox-4x32-10 block per four draws; the stream key is per topic
+//     slice (warp-uniform: the ten round keys live in uniform registers) and
+//     the lane is in the counter {lane << 8 | block, word, doc, period};
+//   * inversion against u = the raw 32-bit word as a float, with the
+//     thresholds scaled by 2^32 (e^-lambda 2^32 = ex2(32 - lambda log2 e)):
+//     z in {0, 1, 2} branch-free;
+//   * draws with z >= 3 or lambda >= 10 are rare but would serialise the warp
+//     (one lane's search costs all 32): they are queued per warp in shared
+//     memory and drained 32 at a time, one per lane -- the sequential search
+//     resumes from z = 3 on the same thresholds; lambda >= 10 takes PTRS
+//     (Hormann 1993, the reference's rng.cpp:57-86 algorithm) in f32 on
+//     blocks {lane << 8 | 2 + 16 j + i} of the same stream.
+constexpr int kThruQueue = 288;  // 31 left over + 8 draws x 32 lanes, + 1 spare
+
+// PTRS conditioned on z >= 3 (rejecting accepted draws below 3 -- exact for
+// the conditional law; P(z < 3) < 3e-3 at lambda >= 10)
+__device__ __forceinline__ uint32_t ptrs_f32_ge3(float lam, uint32_t k0, uint32_t k1, uint32_t blk0,
+                                                 uint32_t w, uint32_t d, uint32_t t) {
+  const float slam = sqrtf(lam), loglam = __logf(lam);
+  const float b = 0.931f + 2.53f * slam;
+  const float a = -0.059f + 0.02483f * b;
+  const float inv_alpha = 1.1239f + 1.1328f / (b - 3.4f);
+  const float v_r = 0.9277f - 3.6224f / (b - 2.0f);
+  for (uint32_t blk = blk0;; ++blk) {
+    const U4 r = philox10(U4{blk, w, d, t}, k0, k1);
+    const uint32_t words[4] = {r.x, r.y, r.z, r.w};
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const float u = (static_cast<float>(words[2 * h] >> 8) + 0.5f) * 0x1p-24f - 0.5f;
+      const float v = (static_cast<float>(words[2 * h + 1] >> 8) + 0.5f) * 0x1p-24f;
+      const float us = 0.5f - fabsf(u);
+      const float g = (2.0f * a / us + b) * u + lam + 0.43f;
+      if (us >= 0.07f && v <= v_r) {
+        if (g >= 3.0f) return static_cast<uint32_t>(g);
+        continue;
+      }
+      if (g < 3.0f || (us < 0.013f && v > us)) continue;
+      const float k = floorf(g);
+      if (logf(v * inv_alpha / (a / (us * us) + b)) <= -lam + k * loglam - lgammaf(k + 1.0f))
+        return static_cast<uint32_t>(k);
+    }
+  }
+}
+
+template <int KPL, bool FULL, int MUSRC, bool PHI, int MINB>
+__global__ void __launch_bounds__(kFastBlock, MINB) k_sample_thru(
+    BatchView bv, const float* __restrict__ theta_b32, const float* __restrict__ phi32,
+    const float* __restrict__ mu_f_in, int K, float m_t, uint64_t seed, uint32_t t,
+    uint32_t sweep, int64_t chunk, unsigned long long* __restrict__ theta_counts,
+    unsigned long long* __restrict__ phi_counts) {
+  static_assert(KPL % 4 == 0 && KPL <= 8, "four draws per Philox block, u16 pairs");
+  constexpr int kWarps = kFastBlock / kWarp;
+  // the per-warp queue of deferred draws (SoA rows: conflict-free per lane):
+  // rate, u, batch row, word, topic
+  __shared__ uint32_t q[kWarps][5][kThruQueue];
+  const int lane = threadIdx.x & 31;
+  const int wq = threadIdx.x >> 5;
+  const int64_t item = static_cast<int64_t>(blockIdx.x) * kWarps + wq;
+  const int kbase = static_cast<int>(blockIdx.y) * kWarp * KPL;
+  const int64_t p0 = item * chunk;
+  if (p0 >= bv.nnz) return;
+  const int64_t p1 = min(p0 + chunk, bv.nnz);
+  uint32_t k0, k1;  // warp-uniform stream key of this topic slice
+  stream_key(seed, make_tag(kThroughput, sweep, blockIdx.y), k0, k1);
+  const uint32_t lt_mask = (1u << lane) - 1u;
+  uint32_t* const qw = &q[wq][0][0];
+
+  int qn = 0;  // warp-uniform queue length
+
+  // drain n (<= 32) queued draws, one per lane, from the top of the queue; a
+  // queued draw has u > c2, which the main path counted as z = 2, so it adds
+  // z - 2 with z drawn from the tail law beyond 2
+  auto drain = [&](int n) {
+    __syncwarp();
+    if (lane < n) {
+      const int e = qn - n + lane;
+      const float lam = __uint_as_float(qw[e]);
+      const float u = __uint_as_float(qw[kThruQueue + e]);
+      const uint32_t b = qw[2 * kThruQueue + e], w = qw[3 * kThruQueue + e];
+      const uint32_t k = qw[4 * kThruQueue + e];
+      uint32_t z;
+      if (lam < 10.0f) {  // resume the search past z = 2 on the same thresholds
+        const float e0 = ex2_approx(__fmaf_rn(lam, -1.4426950408889634f, 32.0f));
+        const float t1 = e0 * lam;
+        float cdf = __fmaf_rn(t1, 0.5f * lam, e0 + t1);
+        float pmf = t1 * 0.5f * lam;
+        z = 3;
+        for (; z < 40; ++z) {
+          pmf *= lam * c_tail_inv[z];
+          cdf += pmf;
+          if (u <= cdf) break;
+        }
+      } else {  // the tail beyond 2 of a large rate: PTRS given z >= 3
+        const uint32_t kl = k - static_cast<uint32_t>(kbase);
+        const uint32_t di = static_cast<uint32_t>(__ldg(bv.batch_docs + b) + static_cast<int32_t>(bv.doc_base));
+        z = ptrs_f32_ge3(lam, k0, k1, ((kl & 31u) << 8) | (2u + 16u * (kl >> 5)), w, di, t);
+      }
+      const unsigned long long dz = z - 2u;  // the main path counted 2
+      atomicAdd(theta_counts + static_cast<int64_t>(b) * K + k, dz);
+      if (PHI)
+        asm volatile("red.relaxed.gpu.global.add.u64 [%0], %1;" ::"l"(phi_counts + static_cast<int64_t>(w) * K + k),
+                     "l"(dz));
+    }
+    qn -= n;
+    __syncwarp();
+  };
+
+  int cur_b = -1;
+  uint32_t acc[KPL / 2];  // this lane's theta counts for the current document, u16 pairs
+#pragma unroll
+  for (int j = 0; j < KPL / 2; ++j) acc[j] = 0u;
+  auto flush = [&](int b) {
+#pragma unroll
+    for (int j = 0; j < KPL; ++j) {
+      const int k = kbase + lane + kWarp * j;
+      const uint32_t z = (acc[j / 2] >> (16 * (j & 1))) & 0xffffu;
+      if ((FULL || k < K) && z)
+        atomicAdd(theta_counts + static_cast<int64_t>(b) * K + k, static_cast<unsigned long long>(z));
+    }
+  };
+  for (int64_t g0 = p0; g0 < p1; g0 += kWarp) {
+    const int64_t p = g0 + lane;
+    int32_t b = 0, d = 0, w = 0, c = 0;
+    float muf_v = 0.0f;
+    if (p < p1) {
+      b = static_cast<int32_t>(find_row(bv.batch_prefix, bv.B, p));
+      d = __ldg(bv.batch_docs + b);
+      const int64_t gi = __ldg(bv.doc_offsets + d) + (p - __ldg(bv.batch_prefix + b));
+      w = __ldg(bv.word_ids + gi);
+      c = __ldg(bv.counts + gi);
+      if (MUSRC == 2) muf_v = __ldg(mu_f_in + p);
+    }
+    const int n_here = static_cast<int>(min(static_cast<int64_t>(kWarp), p1 - g0));
+    for (int i = 0; i < n_here; ++i) {
+      const int32_t bi = __shfl_sync(0xffffffffu, b, i);
+      const uint32_t di = static_cast<uint32_t>(__shfl_sync(0xffffffffu, d, i) + static_cast<int32_t>(bv.doc_base));
+      const int32_t wi = __shfl_sync(0xffffffffu, w, i);
+      const int32_t ci = __shfl_sync(0xffffffffu, c, i);
+      if (bi != cur_b) {
+        if (cur_b >= 0) flush(cur_b);
+        cur_b = bi;
+#pragma unroll
+        for (int j = 0; j < KPL / 2; ++j) acc[j] = 0u;
+      }
+      float prod[KPL];
+      float mu_f = 0.0f;
+      {
+        const float* prow = phi32 + static_cast<int64_t>(wi) * K + kbase + lane;
+        const float* trow = theta_b32 + static_cast<int64_t>(bi) * K + kbase + lane;
+#pragma unroll
+        for (int j = 0; j < KPL; ++j) {
+          prod[j] = FULL || kbase + lane + kWarp * j < K ? __ldg(trow + kWarp * j) * __ldg(prow + kWarp * j) : 0.0f;
+          mu_f += prod[j];
+        }
+      }
+      if (MUSRC == 2) {
+        mu_f = __shfl_sync(0xffffffffu, muf_v, i);
+      } else {
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) mu_f += __shfl_xor_sync(0xffffffffu, mu_f, o);
+      }
+      const float cs = m_t * static_cast<float>(ci);
+      float scale = __fdividef(cs, mu_f);
+      if (!(mu_f >= 1e-30f)) {  // sampler.cpp:164: mu < 1e-30 -> uniform weights 1/K (warp-uniform)
+#pragma unroll
+        for (int j = 0; j < KPL; ++j) prod[j] = (FULL || kbase + lane + kWarp * j < K) ? 1.0f : 0.0f;
+        scale = __fdividef(cs, static_cast<float>(K));
+      }
+      unsigned long long* pc = phi_counts + static_cast<int64_t>(wi) * K + kbase + lane;
+#pragma unroll
+      for (int g = 0; g < KPL; g += 4) {
+        const U4 r = philox10(U4{(static_cast<uint32_t>(lane) << 8) | static_cast<uint32_t>(g / 4),
+                                 static_cast<uint32_t>(wi), di, t},
+                              k0, k1);
+        const uint32_t words[4] = {r.x, r.y, r.z, r.w};
+        uint32_t tm = 0;  // this lane's draws of the group with u > c2
+#pragma unroll
+        for (int jj = 0; jj < 4; ++jj) {
+          const int j = g + jj;
+          const float lam = prod[j] * scale;  // 0 for topics past K (prod = 0)
+          const float u = __uint2float_rn(words[jj]);  // in [0, 2^32]
+          const float e0 = ex2_approx(__fmaf_rn(lam, -1.4426950408889634f, 32.0f));
+          const float t1 = e0 * lam;
+          const float c1 = e0 + t1;
+          const float c2 = __fmaf_rn(t1, 0.5f * lam, c1);
+          uint32_t z = u > e0 ? 1u : 0u;
+          if (u > c1) ++z;
+          acc[j / 2] += z << (16 * (j & 1));
+          if (PHI) red_add_u64(pc + kWarp * j, z);  // unpredicated: z = 0 adds 0
+          if (u > c2) tm |= 1u << jj;  // z >= 3 (for any rate: lambda >= 10 takes PTRS given z >= 3)
+        }
+        if (__any_sync(0xffffffffu, tm != 0u)) {  // queue this group's tails (lambda, u recomputed)
+#pragma unroll
+          for (int jj = 0; jj < 4; ++jj) {
+            const bool tail = (tm >> jj) & 1u;
+            const uint32_t bal = __ballot_sync(0xffffffffu, tail);
+            if (bal != 0u) {
+              if (tail) {
+                uint32_t* const qe = qw + qn + __popc(bal & lt_mask);
+                qe[0] = __float_as_uint(prod[g + jj] * scale);
+                qe[kThruQueue] = __float_as_uint(__uint2float_rn(words[jj]));
+                qe[2 * kThruQueue] = static_cast<uint32_t>(bi);
+                qe[3 * kThruQueue] = static_cast<uint32_t>(wi);
+                qe[4 * kThruQueue] = static_cast<uint32_t>(kbase + lane + kWarp * (g + jj));
+              }
+              qn += __popc(bal);
+            }
+          }
+        }
+      }
+      while (qn >= kWarp) drain(kWarp);
+    }
+  }
+  if (qn > 0) drain(qn);
+  if (cur_b >= 0) flush(cur_b);
+}
+
 template <int KPL>
 int launch_fast_kpl(const BatchView& bv, const double* tb64, const float* tb32, const double* phi64,
                     const float* phi32, const double* mu, int K, double m_t, uint64_t seed,
@@ -1122,6 +1345,52 @@ int64_t deferred_record_bytes() { return static_cast<int64_t>(sizeof(Deferred));
 int64_t deferred_aux_bytes(int64_t max_records, int64_t draw_cap) {
   return max_records * static_cast<int64_t>(sizeof(double)) + 16 +
          draw_cap * static_cast<int64_t>(sizeof(DeferredDraw));
+}
+
+template <bool PHI, int MINB>
+static void launch_thru(const BatchView& bv, const float* theta_b32, const float* phi32, int K,
+                        float m_t, uint64_t seed, uint32_t t, uint32_t sweep,
+                        unsigned long long* tc, unsigned long long* pc, const float* mu_f,
+                        cudaStream_t st) {
+  constexpr int KPL = 8;
+  const int n_slices = (K + kWarp * KPL - 1) / (kWarp * KPL);
+  const int64_t chunk = 128;
+  const int64_t items = (bv.nnz + chunk - 1) / chunk;
+  const int warps = kFastBlock / kWarp;
+  const dim3 grid(static_cast<unsigned>((items + warps - 1) / warps), static_cast<unsigned>(n_slices));
+  const bool full = K % (kWarp * KPL) == 0;
+  if (mu_f != nullptr) {
+    if (full)
+      k_sample_thru<KPL, true, 2, PHI, MINB><<<grid, kFastBlock, 0, st>>>(
+          bv, theta_b32, phi32, mu_f, K, m_t, seed, t, sweep, chunk, tc, pc);
+    else
+      k_sample_thru<KPL, false, 2, PHI, MINB><<<grid, kFastBlock, 0, st>>>(
+          bv, theta_b32, phi32, mu_f, K, m_t, seed, t, sweep, chunk, tc, pc);
+  } else if (full) {
+    k_sample_thru<KPL, true, 0, PHI, MINB><<<grid, kFastBlock, 0, st>>>(
+        bv, theta_b32, phi32, nullptr, K, m_t, seed, t, sweep, chunk, tc, pc);
+  } else {
+    k_sample_thru<KPL, false, 0, PHI, MINB><<<grid, kFastBlock, 0, st>>>(
+        bv, theta_b32, phi32, nullptr, K, m_t, seed, t, sweep, chunk, tc, pc);
+  }
+}
+
+int launch_sample_throughput(const BatchView& bv, const float* theta_b32, const float* phi32, int K,
+                             double m_t, uint64_t seed, uint32_t t, uint32_t sweep,
+                             unsigned long long* tc, unsigned long long* pc, float* mu_f,
+                             cudaStream_t st) {
+  if (bv.nnz == 0) return 0;
+  int launched = 0;
+  const float* mu = nullptr;
+  if (K > kWarp * 8) {  // more than one topic slice: mu from its own pass
+    k_mu_f32<<<grid_for((bv.nnz + 31) / 32 * 32, 256), 256, 0, st>>>(bv, theta_b32, phi32, K, mu_f);
+    mu = mu_f;
+    ++launched;
+  }
+  const float mf = static_cast<float>(m_t);
+  if (pc != nullptr) launch_thru<true, 3>(bv, theta_b32, phi32, K, mf, seed, t, sweep, tc, pc, mu, st);
+  else launch_thru<false, 3>(bv, theta_b32, phi32, K, mf, seed, t, sweep, tc, pc, mu, st);
+  return launched + 1;
 }
 
 int launch_sample_fast(const BatchView& bv, const double* theta_b64, const float* theta_b32,

@@ -29,6 +29,7 @@ _LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "libsamelda
 
 MODE_PARITY = 0
 MODE_EXPECTED = 1
+MODE_THROUGHPUT = 2  # own f32 random streams: statistical (not bit) parity
 SCHEDULES = {"constant": 0, "linear": 1, "log": 2, "invlinear": 3}
 
 

@@ -1,0 +1,108 @@
+"""Throughput mode (SAMELDA_CU_MODE_THROUGHPUT): the same
+Poisson replicas on this library's own random streams in f32.  It is not
+bit-identical to the reference by design, so parity here is statistical:
+
+  * every phi-count cell is Poisson with the factored expected count as its
+    mean (sampler.cpp:150-185's model): the averaged counts over many periods
+    match the oracle's expected counts with Poisson dispersion;
+  * theta and phi counts balance (they count the same draws);
+  * a full train() lands on the parity mode's held-out log-likelihood.
+"""
+from __future__ import annotations
+
+import numpy as np
+import pytest
+
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def S():
+    from paper_1409_5402_b200 import samelda
+    return samelda
+
+
+def _phi_counts(trainer, W, K):
+    import torch
+    from paper_1409_5402_b200.distributed import _CAI
+    ptr, n, _, is_f = trainer.phi_counts_device()
+    assert n >= W * K and not is_f
+    t = torch.as_tensor(_CAI(ptr, n, "<i8"), device="cuda:0")
+    return t[:W * K].cpu().numpy().reshape(W, K).astype(np.float64)
+
+
+@pytest.mark.parametrize("K,m_t", [(64, 3.0), (256, 3.0), (256, 400.0), (300, 40.0), (512, 3.0)])
+def test_phi_counts_poisson_around_expected(S, port, K, m_t):
+    """Mean of T periods' phi counts vs the oracle's expected counts: the
+    normalised dispersion sum((mean - e)^2 / (e / T)) / cells is ~1 for exact
+    Poisson draws (sd sqrt(2 / cells)); m_t = 400 puts many rates on PTRS."""
+    g = port.make_corpus(60, 120, 5, 40.0, 17)
+    cfg = S.SamplerConfig(n_topics=K, m=m_t, t_max=1, batch_fraction=1.0, seed=11,
+                          inner_sweeps=1, mode=S.MODE_THROUGHPUT)
+    tr = S.Trainer(g, cfg)
+    batch = np.arange(g.n_docs, dtype=np.int32)
+    model = tr.model()
+    tb = model.theta[batch]
+    mu = port.sddmm(tb, model.phi, g, batch)
+    _, pf = port.expected_counts(tb, model.phi, mu, g, batch, m_t)
+    T = 64
+    acc = np.zeros_like(pf)
+    for t in range(1, T + 1):
+        tr.period_sample(batch, t, m_t)
+        tc_total, pc_total = tr.count_totals()
+        assert tc_total == pc_total
+        acc += _phi_counts(tr, g.n_words, K)
+    mean = acc / T
+    live = pf > 1e-3
+    disp = float(np.sum((mean[live] - pf[live]) ** 2 / (pf[live] / T)) / live.sum())
+    assert abs(disp - 1.0) < 6 * np.sqrt(2.0 / live.sum()) + 0.02, disp
+    assert np.all(acc[pf == 0.0] == 0.0)
+    tot_obs, tot_exp = acc.sum(), pf.sum() * T
+    assert abs(tot_obs - tot_exp) < 6 * np.sqrt(tot_exp), (tot_obs, tot_exp)
+
+
+def test_inner_sweeps_and_mass_balance(S, port):
+    """inner_sweeps > 1 takes the phi-scatter-free first sweeps; counts still
+    balance and the model stays a set of distributions."""
+    g = port.make_corpus(120, 200, 6, 60.0, 4)
+    cfg = S.SamplerConfig(n_topics=256, m=50.0, t_max=4, batch_fraction=0.5, seed=2,
+                          inner_sweeps=3, mode=S.MODE_THROUGHPUT)
+    tr = S.Trainer(g, cfg)
+    rng = np.random.default_rng(0)
+    for t in range(1, 5):
+        batch = rng.permutation(g.n_docs)[:60].astype(np.int32)
+        tr.period_sample(batch, t, 50.0)
+        a, b = tr.count_totals()
+        assert a == b and a > 0
+        tr.period_update(0.5)
+    m = tr.model()
+    np.testing.assert_allclose(m.phi.sum(1), 1.0, rtol=1e-12)
+    assert np.all(m.phi > 0)
+
+
+@pytest.mark.parametrize("K", [16, 256])
+def test_train_ll_matches_parity_mode(S, port, K):
+    """End to end, the throughput mode's held-out ll lands where the parity
+    mode's (the reference's) does: within the spread of parity runs that
+    differ only in their seed (a different seed is a different, equally
+    valid, random trajectory -- which is all the throughput mode is)."""
+    g = port.make_corpus(400, 500, 8, 80.0, 31)
+    tr, te = port.split_holdout(g, 0.1, 7)
+    kw = dict(n_topics=K, m=100.0, t_max=120, batch_fraction=0.25)
+
+    def final_ll(mode, seed):
+        _, trace = S.train(tr, S.SamplerConfig(mode=mode, seed=seed, **kw), te, 120)
+        return trace[-1]["ll"]
+
+    llp = np.array([final_ll(S.MODE_PARITY, s) for s in (9, 10, 11, 12)])
+    llf = np.array([final_ll(S.MODE_THROUGHPUT, s) for s in (9, 10)])
+    assert np.all(np.isfinite(llf))
+    tol = max(0.02, 4 * llp.std(ddof=1))
+    assert np.all(np.abs(llf - llp.mean()) < tol), (llp, llf, tol)
+
+
+def test_unknown_mode_rejected(S, port):
+    g = port.make_corpus(10, 20, 2, 10.0, 1)
+    with pytest.raises(S.ConfigError):
+        S.Trainer(g, S.SamplerConfig(n_topics=4, mode=3))
