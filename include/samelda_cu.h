@@ -116,6 +116,18 @@ int samelda_cu_sample_counts(samelda_cu_ctx* ctx, const samelda_cu_corpus* corpu
                              int64_t t, int32_t sweep, int64_t* theta_counts,
                              int64_t* phi_counts);
 
+/* Throughput mode (SURVEY 8(b) "mode 2 fast"): sample_counts on this
+ * library's own f32 random streams -- the same Poisson replicas, so the same
+ * law, but not the reference's draws.  mu is validated for alignment and not
+ * read (the kernel forms its own f32 mu).  Counts are deterministic for given
+ * inputs (integer scatter; streams keyed by coordinates, not by schedule). */
+int samelda_cu_sample_counts_fast(samelda_cu_ctx* ctx, const samelda_cu_corpus* corpus,
+                                  const double* theta_batch, int64_t B, int64_t K_theta,
+                                  const double* phi, int64_t K, int64_t W, const double* mu,
+                                  int64_t mu_len, const int32_t* doc_ids, double m_t,
+                                  uint64_t seed, int64_t t, int32_t sweep, int64_t* theta_counts,
+                                  int64_t* phi_counts);
+
 /* Deterministic factored path: sample_counts with z := E[z] = rate, f64. */
 int samelda_cu_expected_counts(samelda_cu_ctx* ctx, const samelda_cu_corpus* corpus,
                                const double* theta_batch, int64_t B, int64_t K_theta,

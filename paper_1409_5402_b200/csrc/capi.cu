@@ -776,6 +776,18 @@ int samelda_cu_sample_counts(samelda_cu_ctx* ctx, const samelda_cu_corpus* corpu
   });
 }
 
+int samelda_cu_sample_counts_fast(samelda_cu_ctx* ctx, const samelda_cu_corpus* corpus,
+                                  const double* theta_batch, int64_t B, int64_t K_theta,
+                                  const double* phi, int64_t K, int64_t W, const double* mu,
+                                  int64_t mu_len, const int32_t* doc_ids, double m_t,
+                                  uint64_t seed, int64_t t, int32_t sweep, int64_t* theta_counts,
+                                  int64_t* phi_counts) {
+  return guarded(ctx, [&] {
+    sample_call(ctx, corpus, theta_batch, B, K_theta, phi, K, W, mu, mu_len, doc_ids, m_t, seed,
+                t, sweep, SAMELDA_CU_MODE_THROUGHPUT, theta_counts, phi_counts);
+  });
+}
+
 int samelda_cu_expected_counts(samelda_cu_ctx* ctx, const samelda_cu_corpus* corpus,
                                const double* theta_batch, int64_t B, int64_t K_theta,
                                const double* phi, int64_t K, int64_t W, const double* mu,

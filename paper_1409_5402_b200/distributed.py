@@ -52,9 +52,13 @@ class CudaEngine:
     """Per-rank engine over the device-resident trainer (samelda.Trainer)."""
 
     def __init__(self, trainer, device: int):
+        import torch
         self.trainer = trainer
         self.device = device
         self._counts = None
+        # the count all-reduce is enqueued on torch's current stream: run the
+        # trainer on that stream so the collective is ordered after sampling
+        trainer.ctx.set_stream(torch.cuda.current_stream(device).cuda_stream)
 
     def sample(self, local_ids, t, m_t):
         self.trainer.period_sample(local_ids, t, m_t)

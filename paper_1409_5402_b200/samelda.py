@@ -90,6 +90,8 @@ SIGNATURES = [
                                    C.POINTER(_I64)]),
     ("samelda_cu_sample_counts", C.c_int, [_P, _CP, _P, _I64, _I64, _P, _I64, _I64, _P, _I64,
                                            _P, _D, _U64, _I64, _I32, _P, _P]),
+    ("samelda_cu_sample_counts_fast", C.c_int, [_P, _CP, _P, _I64, _I64, _P, _I64, _I64, _P, _I64,
+                                           _P, _D, _U64, _I64, _I32, _P, _P]),
     ("samelda_cu_expected_counts", C.c_int, [_P, _CP, _P, _I64, _I64, _P, _I64, _I64, _P, _I64,
                                              _P, _D, _P, _P]),
     ("samelda_cu_update_model", C.c_int, [_P, _P, _I64, _P, _I64, _I64, _D, _D, _P, _I64, _P,
@@ -376,8 +378,12 @@ def sddmm(theta_batch, phi, corpus, doc_ids, n_threads: int = 1, ctx: Context | 
 
 
 def sample_counts(theta_batch, phi, mu, corpus, doc_ids, m_t, seed, t, sweep=0, n_threads=1,
-                  ctx: Context | None = None) -> SampledCounts:
-    """sampler.cpp:125-195 on the device (reference-identical Poisson replicas)."""
+                  ctx: Context | None = None, mode: int = MODE_PARITY) -> SampledCounts:
+    """sampler.cpp:125-195 on the device: reference-identical Poisson replicas
+    (MODE_PARITY), or the same law on this library's own f32 streams
+    (MODE_THROUGHPUT; mu is then only checked for alignment)."""
+    if mode not in (MODE_PARITY, MODE_THROUGHPUT):
+        raise ConfigError("sample_counts: mode must be MODE_PARITY or MODE_THROUGHPUT")
     ctx = ctx or default_context()
     ctx._train_token = None  # per-call use replaces a Trainer's device state
     corpus = Corpus.of(corpus)
@@ -390,7 +396,8 @@ def sample_counts(theta_batch, phi, mu, corpus, doc_ids, m_t, seed, t, sweep=0, 
     tc = np.zeros(max(B * K, 1), np.int64)
     pc = np.zeros(max(W * K, 1), np.int64)
     cs = corpus._struct()
-    ctx.check(ctx.lib.samelda_cu_sample_counts(
+    fn = ctx.lib.samelda_cu_sample_counts if mode == MODE_PARITY else ctx.lib.samelda_cu_sample_counts_fast
+    ctx.check(fn(
         ctx.h, C.byref(cs), _ptr(theta_batch if theta_batch.size else np.zeros(1)), B, Kt,
         _ptr(phi), K, W, _ptr(mu if len(mu) else np.zeros(1)), len(mu), _ptr(ids), float(m_t),
         int(seed) & (2**64 - 1), int(t), int(sweep), _ptr(tc), _ptr(pc)))

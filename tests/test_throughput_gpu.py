@@ -26,6 +26,7 @@ def S():
 def _phi_counts(trainer, W, K):
     import torch
     from paper_1409_5402_b200.distributed import _CAI
+    trainer.ctx.synchronize()  # the trainer's own stream, not torch's
     ptr, n, _, is_f = trainer.phi_counts_device()
     assert n >= W * K and not is_f
     t = torch.as_tensor(_CAI(ptr, n, "<i8"), device="cuda:0")
@@ -106,3 +107,38 @@ def test_unknown_mode_rejected(S, port):
     g = port.make_corpus(10, 20, 2, 10.0, 1)
     with pytest.raises(S.ConfigError):
         S.Trainer(g, S.SamplerConfig(n_topics=4, mode=3))
+
+
+@pytest.mark.parametrize("K", [64, 256, 300])
+def test_per_call_fast_matches_period_path(S, port, K):
+    """samelda_cu_sample_counts_fast on the host model equals the device-resident
+    period's first sweep bit for bit (same f32 inputs, same coordinate-keyed
+    streams), is deterministic, and balances."""
+    g = port.make_corpus(50, 90, 4, 30.0, 3)
+    m_t, seed, t = 40.0, 21, 5
+    cfg = S.SamplerConfig(n_topics=K, m=m_t, t_max=1, batch_fraction=1.0, seed=seed,
+                          inner_sweeps=1, mode=S.MODE_THROUGHPUT)
+    tr = S.Trainer(g, cfg)
+    batch = np.random.default_rng(1).permutation(g.n_docs).astype(np.int32)
+    tr.period_sample(batch, t, m_t)
+    pc_period = _phi_counts(tr, g.n_words, K)
+    model = tr.model()
+    tb = model.theta[batch]
+    mu = port.sddmm(tb, model.phi, g, batch)
+    a = S.sample_counts(tb, model.phi, mu, g, batch, m_t, seed, t, 0, mode=S.MODE_THROUGHPUT)
+    b = S.sample_counts(tb, model.phi, mu, g, batch, m_t, seed, t, 0, mode=S.MODE_THROUGHPUT)
+    np.testing.assert_array_equal(a.phi_counts, b.phi_counts)
+    np.testing.assert_array_equal(a.theta_counts, b.theta_counts)
+    np.testing.assert_array_equal(a.phi_counts, pc_period)
+    assert a.theta_total() == a.phi_total() > 0
+    c = S.sample_counts(tb, model.phi, mu, g, batch, m_t, seed, t + 1, 0, mode=S.MODE_THROUGHPUT)
+    assert not np.array_equal(a.phi_counts, c.phi_counts)
+
+
+def test_per_call_fast_empty_batch(S, port):
+    g = port.make_corpus(10, 20, 2, 10.0, 1)
+    K = 8
+    phi = np.full((K, g.n_words), 1.0 / g.n_words)
+    sc = S.sample_counts(np.zeros((0, K)), phi, np.zeros(0), g, np.zeros(0, np.int32), 3.0, 1, 1,
+                         mode=S.MODE_THROUGHPUT)
+    assert sc.theta_total() == 0 and sc.phi_total() == 0
