@@ -83,24 +83,26 @@ def test_inner_sweeps_and_mass_balance(S, port):
 
 
 @pytest.mark.parametrize("K", [16, 256])
-def test_train_ll_matches_parity_mode(S, port, K):
-    """End to end, the throughput mode's held-out ll lands where the parity
-    mode's (the reference's) does: within the spread of parity runs that
-    differ only in their seed (a different seed is a different, equally
-    valid, random trajectory -- which is all the throughput mode is)."""
+def test_train_ll_trajectory_matches_parity_mode(S, port, K):
+    """the throughput mode's held-out ll trajectory lies within
+    max(0.01 nats/token, 3 sigma of the parity mode's (the reference's) own
+    seed spread) of the parity mean at every evaluation point (a different
+    seed is a different, equally valid trajectory -- which is what the
+    throughput mode's own streams are)."""
     g = port.make_corpus(400, 500, 8, 80.0, 31)
     tr, te = port.split_holdout(g, 0.1, 7)
     kw = dict(n_topics=K, m=100.0, t_max=120, batch_fraction=0.25)
 
-    def final_ll(mode, seed):
-        _, trace = S.train(tr, S.SamplerConfig(mode=mode, seed=seed, **kw), te, 120)
-        return trace[-1]["ll"]
+    def trajectory(mode, seed):
+        _, trace = S.train(tr, S.SamplerConfig(mode=mode, seed=seed, **kw), te, 30)
+        return np.array([r["ll"] for r in trace])
 
-    llp = np.array([final_ll(S.MODE_PARITY, s) for s in (9, 10, 11, 12)])
-    llf = np.array([final_ll(S.MODE_THROUGHPUT, s) for s in (9, 10)])
-    assert np.all(np.isfinite(llf))
-    tol = max(0.02, 4 * llp.std(ddof=1))
-    assert np.all(np.abs(llf - llp.mean()) < tol), (llp, llf, tol)
+    par = np.array([trajectory(S.MODE_PARITY, s) for s in range(9, 17)])
+    fast = np.array([trajectory(S.MODE_THROUGHPUT, s) for s in range(9, 13)])
+    assert np.all(np.isfinite(fast))
+    tol = np.maximum(0.01, 3 * par.std(0, ddof=1))
+    dev = np.abs(fast - par.mean(0))
+    assert np.all(dev <= tol), (par.mean(0), tol, fast)
 
 
 def test_unknown_mode_rejected(S, port):
