@@ -262,6 +262,7 @@ struct samelda_cu_ctx {
   int64_t W = 0, D = 0;
   DevBuf theta, phi;  // D x K, W x K (f64)
   DevBuf phi32;       // W x K f32 shadow of phi (sampler fast path)
+  DevBuf colsum;      // exact parallel column-sum scan (partials, segment items)
 
   // doc-sharded runs: global id of local doc 0 (Philox keys use global ids)
   int64_t doc_base = 0;
@@ -471,6 +472,12 @@ struct samelda_cu_ctx {
   static int64_t draw_cap_for(int64_t records) {
     if (const char* cap = std::getenv("SAMELDA_DRAW_CAP")) return std::atoll(cap);  // tests
     return std::min<int64_t>(records * 32, int64_t{1} << 26);
+  }
+
+  // scratch of the exact parallel column-sum scan (grown at train_begin /
+  // the first per-call M-step, never inside a period)
+  void* colsum_scratch(int64_t W_, int64_t K_) {
+    return ensure<unsigned char>(colsum, scu::colsum_scratch_bytes(W_, static_cast<int>(K_)));
   }
 
   // Size every per-batch device buffer (and both pinned staging buffers) for
@@ -838,12 +845,14 @@ static void update_call(samelda_cu_ctx* ctx, double* theta, int64_t D, double* p
     double* pf = ensure<double>(ctx->pf, W * K);
     ck(cudaMemcpyAsync(pf, pcounts, sizeof(double) * W * K, cudaMemcpyHostToDevice, st), "upload pf");
     ctx->launches += scu::launch_phi_mstep(nullptr, pf, W, Ki, m_t, beta, rho_t, phi_wk, nullptr,
-                                           ensure<double>(ctx->cand, W * K), totals, ctx->d_err(), st);
+                                           ensure<double>(ctx->cand, W * K), totals,
+                                           ctx->colsum_scratch(W, Ki), ctx->d_err(), st);
   } else {
     auto* pc = ensure<unsigned long long>(ctx->pc, W * K);
     ck(cudaMemcpyAsync(pc, pcounts, sizeof(int64_t) * W * K, cudaMemcpyHostToDevice, st), "upload pc");
     ctx->launches += scu::launch_phi_mstep(pc, nullptr, W, Ki, m_t, beta, rho_t, phi_wk, nullptr,
-                                           ensure<double>(ctx->cand, W * K), totals, ctx->d_err(), st);
+                                           ensure<double>(ctx->cand, W * K), totals,
+                                           ctx->colsum_scratch(W, Ki), ctx->d_err(), st);
   }
   double* back = ensure<double>(ctx->phi_call, K * W);
   ctx->launches += scu::launch_transpose(phi_wk, W, K, back, st);
@@ -993,7 +1002,8 @@ int samelda_cu_train_begin(samelda_cu_ctx* ctx, const samelda_cu_corpus* corpus,
     // (sampler.cpp:285-298), which only applies when t_max > 0
     ctx->launches += scu::launch_fill(th, ctx->D * K, config->alpha + 1.0 / static_cast<double>(K), ctx->stream);
     ctx->launches += scu::launch_phi_init(ph, ctx->W, ctx->K, config->t_max > 0 ? config->init_noise : 0.0,
-                                          config->seed, ensure<double>(ctx->totals, K), ctx->stream);
+                                          config->seed, ensure<double>(ctx->totals, K),
+                                          ctx->colsum_scratch(ctx->W, ctx->K), ctx->stream);
     ctx->launches += scu::launch_to_f32(ph, ctx->W * K, ensure<float>(ctx->phi32, ctx->W * K), ctx->stream);
     // per-batch buffers for the largest batch the minibatch stream can draw:
     // its size (samelda_cu_batches_create) times the longest documents
@@ -1092,7 +1102,8 @@ int samelda_cu_period_update(samelda_cu_ctx* ctx, double rho_t) {
                                                ctx->theta.as<double>(), st);
     ctx->launches += scu::launch_phi_mstep(pcu, pcf, ctx->W, K, ctx->m_t, c.beta, rho_t, ctx->phi.as<double>(),
                                            ctx->phi32.as<float>(), ensure<double>(ctx->cand, ctx->W * K),
-                                           ensure<double>(ctx->totals, K), ctx->d_err(), st);
+                                           ensure<double>(ctx->totals, K), ctx->colsum_scratch(ctx->W, K),
+                                           ctx->d_err(), st);
     ctx->tick(samelda_cu_ctx::kMstep, false);
     ck(cudaGetLastError(), "period launch");
     // no host wait: the flag is read back asynchronously and reported by the

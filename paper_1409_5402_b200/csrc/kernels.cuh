@@ -86,16 +86,23 @@ int launch_theta_persist(const unsigned long long* counts_u, const double* count
 // M-step for phi (sampler.cpp:211-228):
 //   cand[w,k] = counts[w,k]/m_t + beta; total[k] = sum_w cand (sequential w, warp per topic);
 //   phi = (1-rho) phi + rho cand / total
+//   colsum_scratch (colsum_scratch_bytes(W, K) bytes): the exact parallel
+//   column-sum scan; nullptr runs the sequential chain kernel
 int launch_phi_mstep(const unsigned long long* counts_u, const double* counts_f, int64_t W,
                      int K, double m_t, double beta, double rho, double* phi_wk, float* phi32,
-                     double* cand_scratch, double* totals, int* err, cudaStream_t st);
+                     double* cand_scratch, double* totals, void* colsum_scratch, int* err,
+                     cudaStream_t st);
+int64_t colsum_scratch_bytes(int64_t W, int K);
+// totals[k] = the reference's sequential sum over w of x[w,k], bit for bit
+int launch_col_sums(const double* x, int64_t W, int K, double* totals, void* colsum_scratch,
+                    int* err, cudaStream_t st);
 
 // f32 shadow copy (the sampler's fast path reads f32 theta / phi)
 int launch_to_f32(const double* x, int64_t n, float* y, cudaStream_t st);
 
 // phi init with seeded perturbation (model.cpp:41-52, sampler.cpp:285-298)
 int launch_phi_init(double* phi_wk, int64_t W, int K, double init_noise, uint64_t seed,
-                     double* totals, cudaStream_t st);
+                     double* totals, void* colsum_scratch, cudaStream_t st);
 
 // theta init alpha + 1/K (model.cpp:41-52)
 int launch_fill(double* p, int64_t n, double v, cudaStream_t st);
