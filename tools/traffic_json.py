@@ -16,7 +16,8 @@ per = defaultdict(lambda: defaultdict(dict))
 for r in rows[1:]:
     name = r[ik].split("(")[0].split("<")[0].split("::")[-1].replace("void ", "").strip()
     per[name][r[iid]][r[im]] = float(r[iv].replace(",", ""))
-group = ["k_sample_v2", "k_deferred_expand", "k_deferred_draw"]
+group = {"nytimes-fast": ["k_sample_thru"], "nytimes-expected": ["k_expected"]}.get(
+    config, ["k_sample_v2", "k_deferred_expand", "k_deferred_draw"])
 out = {"_doc": "DRAM traffic (dram__bytes_read.sum + dram__bytes_write.sum) per sampling launch "
                "group (" + " + ".join(group) + "), averaged over the launches in " + path +
                "; bench.py reports it as roofline.traffic.", config: {"source": path}}
@@ -31,4 +32,15 @@ for k in group:
     out[config][k] = {"read": int(rd), "write": int(wr), "mean_ns": int(t), "launches": len(launches)}
     total += rd + wr
 out[config]["dram_bytes_per_launch"] = int(total)
-print(json.dumps(out, indent=1))
+# merged into profiles/sample_kernel_traffic.json (one entry per bench config)
+dst = "profiles/sample_kernel_traffic.json"
+try:
+    merged = json.load(open(dst))
+except (OSError, ValueError):
+    merged = {}
+merged["_doc"] = ("DRAM traffic (dram__bytes_read.sum + dram__bytes_write.sum) per sampling launch "
+                  "group of each bench config, averaged over the launches of its ncu launch list; "
+                  "bench.py reports it as roofline.traffic.")
+merged[config] = {"kernels": group, **out[config]}
+json.dump(merged, open(dst, "w"), indent=1)
+print(json.dumps(merged[config], indent=1))
