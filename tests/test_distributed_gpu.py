@@ -25,7 +25,7 @@ def _corpus():
     return port.make_corpus(120, 60, 4, 30.0, 3)
 
 
-def _worker(rank, world, port_no, out_path):
+def _worker(rank, world, port_no, out_path, mode=0):
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port_no))
     dist.init_process_group("gloo", rank=rank, world_size=world)
     torch.cuda.set_device(0)
@@ -41,7 +41,7 @@ def _worker(rank, world, port_no, out_path):
     torch.cuda.set_stream(stream)
     ctx.set_stream(stream.cuda_stream)
     cfg = S.SamplerConfig(n_topics=K, m=M, schedule="invlinear", t_max=T_MAX, batch_fraction=BF,
-                          seed=SEED)
+                          seed=SEED, mode=mode)
     tr = S.Trainer(local, cfg, ctx=ctx)
     tr.set_doc_base(lo)
 
@@ -76,14 +76,18 @@ def _free_port():
 
 
 @pytest.mark.timeout(600)
-def test_two_rank_sharded_training_equals_single_gpu(tmp_path):
+@pytest.mark.parametrize("mode", [0, 2], ids=["parity", "throughput"])
+def test_two_rank_sharded_training_equals_single_gpu(tmp_path, mode):
+    """Both modes key their streams by global document ids and scatter
+    integer counts, so the sharded result is the single-GPU result bit for
+    bit (the throughput mode's own streams included)."""
     from paper_1409_5402_b200 import samelda as S
     out = str(tmp_path / "rank0.npz")
-    mp.start_processes(_worker, args=(2, _free_port(), out), nprocs=2, start_method="spawn")
+    mp.start_processes(_worker, args=(2, _free_port(), out, mode), nprocs=2, start_method="spawn")
     got = np.load(out)
     g = _corpus()
     model, _ = S.train(g, S.SamplerConfig(n_topics=K, m=M, schedule="invlinear", t_max=T_MAX,
-                                          batch_fraction=BF, seed=SEED))
+                                          batch_fraction=BF, seed=SEED, mode=mode))
     np.testing.assert_array_equal(got["phi"], model.phi)
 
 
