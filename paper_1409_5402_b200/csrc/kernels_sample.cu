@@ -1069,7 +1069,8 @@ __global__ void __launch_bounds__(BLK, MINB) k_sample_thru(
           uint32_t z = u > e0 ? 1u : 0u;
           if (u > c1) ++z;
           acc[j / 2] += z << (16 * (j & 1));
-          if (PHI) red_add_u64(pc + kWarp * j, z);  // unpredicated: z = 0 adds 0
+          // unpredicated within the row (z = 0 adds 0); topics past K have no cell
+          if (PHI && (FULL || kbase + lane + kWarp * j < K)) red_add_u64(pc + kWarp * j, z);
           if (u > c2) tm |= 1u << jj;  // z >= 3 (for any rate: lambda >= 10 takes PTRS given z >= 3)
         }
         if (__any_sync(0xffffffffu, tm != 0u)) {  // queue this group's tails (lambda, u recomputed)
