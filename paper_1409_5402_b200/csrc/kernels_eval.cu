@@ -191,9 +191,10 @@ __global__ void __launch_bounds__(kEvalCtaThreads) k_eval_cta(
     double* __restrict__ doc_logp, int64_t* __restrict__ doc_scored,
     double* __restrict__ theta_out, int* __restrict__ err) {
   extern __shared__ double smem[];
-  double* th = smem;                 // K
-  double* nx = th + K;               // K
-  double* cs = nx + K;               // [256] cell scale (0 = skip) / score term
+  const int KE = (K + 1) & ~1;       // even padding, as k_eval_stage
+  double* th = smem;                 // K (+ pad)
+  double* nx = th + KE;              // K (+ pad)
+  double* cs = nx + KE;              // [256] cell scale (0 = skip) / score term
   int32_t* cw = reinterpret_cast<int32_t*>(cs + kEvalCtaThreads);  // [256] cell word
   __shared__ double s_red[kEvalCtaThreads / 32];
   __shared__ int64_t s_cnt[kEvalCtaThreads];
@@ -326,9 +327,13 @@ __global__ void __launch_bounds__(kEvalCtaThreads) k_eval_stage(
     double* __restrict__ theta_out, int* __restrict__ err) {
   extern __shared__ double smem[];
   const int KP = K | 1;
-  double* th = smem;                     // K
-  double* nx = th + K;                   // K
-  double* fs = nx + K;                   // [kEvalFoldMax] scale per fold cell
+  // th / nx padded to an even length: the uniform th[k] loads are paired
+  // into 16-byte LDS, which for odd K would touch nx[0] (harmless, but a
+  // racecheck hazard against nx's writes)
+  const int KE = (K + 1) & ~1;
+  double* th = smem;                     // K (+ pad)
+  double* nx = th + KE;                  // K (+ pad)
+  double* fs = nx + KE;                  // [kEvalFoldMax] scale per fold cell
   int32_t* fw = reinterpret_cast<int32_t*>(fs + kEvalFoldMax);  // word per fold cell
   int32_t* fc = fw + kEvalFoldMax;                              // fold count per fold cell
   double* rows = reinterpret_cast<double*>(fc + kEvalFoldMax);   // R x KP staged rows
@@ -562,7 +567,7 @@ int launch_eval_docs(const int64_t* doc_offsets, const int32_t* word_ids,
     const char* cps_env = getenv("SAMELDA_EVAL_CTAS_PER_SM");
     const int cps = cps_env ? max(1, atoi(cps_env)) : 3;
     const int KP = K | 1;
-    const size_t fixed = (2 * static_cast<size_t>(K) + kEvalFoldMax) * sizeof(double) +
+    const size_t fixed = (2 * static_cast<size_t>((K + 1) & ~1) + kEvalFoldMax) * sizeof(double) +
                          2 * kEvalFoldMax * sizeof(int32_t);
     const size_t budget = (220u * 1024u) / static_cast<size_t>(cps);
     if (budget > fixed + static_cast<size_t>(KP) * sizeof(double)) {
@@ -584,7 +589,7 @@ int launch_eval_docs(const int64_t* doc_offsets, const int32_t* word_ids,
     }
   }
   if (K <= kEvalCtaMaxK && !(ev && ev[0] == 'w') && !getenv("SAMELDA_EVAL_WARP")) {
-    const size_t smem_c = (2 * static_cast<size_t>(K) + kEvalCtaThreads) * sizeof(double) +
+    const size_t smem_c = (2 * static_cast<size_t>((K + 1) & ~1) + kEvalCtaThreads) * sizeof(double) +
                           kEvalCtaThreads * sizeof(int32_t);
     static size_t configured_c = 48 * 1024;
     if (smem_c > configured_c) {
