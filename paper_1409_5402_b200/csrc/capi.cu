@@ -655,7 +655,8 @@ int samelda_cu_create(int device, samelda_cu_ctx** out) {
   auto* ctx = new samelda_cu_ctx();
   ctx->device = device;
   if (cudaSetDevice(device) != cudaSuccess ||
-      cudaStreamCreateWithFlags(&ctx->own_stream, cudaStreamNonBlocking) != cudaSuccess) {
+      cudaStreamCreateWithFlags(&ctx->own_stream, cudaStreamNonBlocking) != cudaSuccess ||
+      scu::init_lgamma_table() != 0) {
     delete ctx;
     return SAMELDA_CU_CUDA;
   }

@@ -71,6 +71,8 @@ int launch_sample_throughput(const BatchView& bv, const float* theta_b32, const 
                              unsigned long long* theta_counts, unsigned long long* phi_counts,
                              float* mu_f_scratch, cudaStream_t st);
 int64_t deferred_record_bytes();
+// fills the device's glibc lgamma table (call once per device, after cudaSetDevice)
+int init_lgamma_table();
 int64_t deferred_aux_bytes(int64_t max_records, int64_t draw_cap);
 
 // out[i] = counts[i] / m_t + alpha over n entries       (sampler.cpp:324-330)

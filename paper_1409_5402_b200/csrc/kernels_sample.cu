@@ -2,6 +2,8 @@
 // exact f64 sampler, the fast-exact period sampler (k_sample_v2) with its
 // deferred exact passes, the K > 256 mu pre-pass and the expected-count
 // kernel.  Each kernel cites the reference loop it replaces.
+#include <cmath>
+
 #include "kernels_common.cuh"
 #include "poisson.cuh"
 
@@ -1422,6 +1424,21 @@ int launch_sample_fast(const BatchView& bv, const double* theta_b64, const float
                               deferred, n_deferred, aux, draw_cap, mu_f, err, st);
   return launch_fast_kpl<8>(bv, theta_b64, theta_b32, phi64, phi32, mu, K, m_t, seed, t, sweep, tc, pc,
                             deferred, n_deferred, aux, draw_cap, mu_f, err, st);
+}
+
+// glibc lgamma(k + 1) for the PTRS acceptance test (poisson.cuh), per device
+int init_lgamma_table() {
+  static double tab[kLgammaTab];
+  static bool filled = false;
+  if (!filled) {
+    for (int k = 0; k < kLgammaTab; ++k) tab[k] = std::lgamma(static_cast<double>(k) + 1.0);
+    filled = true;
+  }
+  const int one = 1;
+  if (cudaMemcpyToSymbol(g_lgamma_int, tab, sizeof(tab)) != cudaSuccess ||
+      cudaMemcpyToSymbol(g_lgamma_ready, &one, sizeof(one)) != cudaSuccess)
+    return 1;
+  return 0;
 }
 
 }  // namespace scu

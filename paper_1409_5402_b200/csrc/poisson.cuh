@@ -6,8 +6,9 @@
 //
 // Every f64 operation is written as an explicit round-to-nearest intrinsic
 // (__dmul_rn / __ddiv_rn / __dadd_rn): no FMA contraction may merge them,
-// because the reference is built for x86-64 baseline without FMA.  exp/log/
-// lgamma are CUDA libdevice (<= 1-2 ulp from glibc); a last-ulp difference
+// because the reference is built for x86-64 baseline without FMA.  lgamma of
+// integers below kLgammaTab is glibc's own value (a host-filled table); exp /
+// log are CUDA libdevice (<= 1-2 ulp from glibc); a last-ulp difference
 // can only flip a draw when the uniform lands inside that ulp gap (~1e-16
 // per draw), see DESIGN.md "Parity".
 #pragma once
@@ -31,6 +32,13 @@ __device__ __forceinline__ int64_t poisson_inversion(double lambda, double u) {
   return k;
 }
 
+// lgamma(k + 1) for integer k < kLgammaTab as glibc computes it (the
+// reference's std::lgamma, rng.cpp:81), filled on the host per device by
+// init_lgamma_table (kernels_sample.cu); larger k use libdevice lgamma.
+constexpr int kLgammaTab = 4096;
+__device__ double g_lgamma_int[kLgammaTab];
+__device__ int g_lgamma_ready;
+
 // PTRS for lambda >= 10, consuming the stream exactly like rng.cpp:64-85.
 __device__ __noinline__ int64_t poisson_ptrs(double lambda, Stream& s) {
   const double log_lambda = log(lambda);
@@ -50,9 +58,9 @@ __device__ __noinline__ int64_t poisson_ptrs(double lambda, Stream& s) {
     const int64_t k = static_cast<int64_t>(g);
     const double lhs =
         log(__ddiv_rn(__dmul_rn(v, inv_alpha), __dadd_rn(__ddiv_rn(a, __dmul_rn(us, us)), b)));
-    const double rhs = __dadd_rn(
-        __dadd_rn(-lambda, __dmul_rn(static_cast<double>(k), log_lambda)),
-        -lgamma(__dadd_rn(static_cast<double>(k), 1.0)));
+    const double lg = k < kLgammaTab && g_lgamma_ready ? g_lgamma_int[k]
+                                                       : lgamma(__dadd_rn(static_cast<double>(k), 1.0));
+    const double rhs = __dadd_rn(__dadd_rn(-lambda, __dmul_rn(static_cast<double>(k), log_lambda)), -lg);
     if (lhs <= rhs) return k;
   }
 }
