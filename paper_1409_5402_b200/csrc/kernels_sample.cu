@@ -1427,15 +1427,19 @@ int launch_sample_fast(const BatchView& bv, const double* theta_b64, const float
 }
 
 // glibc lgamma(k + 1) for the PTRS acceptance test (poisson.cuh), per device
-int init_lgamma_table() {
-  static double tab[kLgammaTab];
-  static bool filled = false;
-  if (!filled) {
-    for (int k = 0; k < kLgammaTab; ++k) tab[k] = std::lgamma(static_cast<double>(k) + 1.0);
-    filled = true;
+namespace {
+struct LgammaTab {
+  double v[kLgammaTab];
+  LgammaTab() {
+    for (int k = 0; k < kLgammaTab; ++k) v[k] = std::lgamma(static_cast<double>(k) + 1.0);
   }
+};
+}  // namespace
+
+int init_lgamma_table() {
+  static const LgammaTab tab;  // filled once, thread-safe (static initialisation)
   const int one = 1;
-  if (cudaMemcpyToSymbol(g_lgamma_int, tab, sizeof(tab)) != cudaSuccess ||
+  if (cudaMemcpyToSymbol(g_lgamma_int, tab.v, sizeof(tab.v)) != cudaSuccess ||
       cudaMemcpyToSymbol(g_lgamma_ready, &one, sizeof(one)) != cudaSuccess)
     return 1;
   return 0;
