@@ -22,6 +22,26 @@ enum Mode : int { kModeParity = 0, kModeExpected = 1, kModeFast = 2 };
 
 enum ErrBits : int { kErrNumerical = 1 };
 
+// Process-wide tuning switches, read from the environment ONCE (forced at
+// samelda_cu_create), never per launch.  All of them select bit-identical
+// alternatives or test-only limits:
+//   SAMELDA_SAMPLER=x      per-call sample_counts on the all-f64 exact kernel
+//                          (device-side cross-check of the fast-exact path)
+//   SAMELDA_COLSUM=chain   sequential TMA-chain column sums instead of the scan
+//   SAMELDA_DRAW_CAP=n     deferred-draw list capacity (tests: overflow path)
+//   SAMELDA_EVAL=...       held-out evaluation kernel variant (A/B)
+//   SAMELDA_MINB/DEC/TAIL  k_sample_v2 A/B variants; only in a library built
+//                          with -DSAMELDA_AB_VARIANTS (tools/), else ignored
+struct Tuning {
+  bool sampler_exact = false;
+  bool colsum_chain = false;
+  long long draw_cap = -1;  // < 0: default
+  char eval_variant = 0;    // 0 default, 'c' cta, 'w' warp
+  int eval_ctas_per_sm = 0;
+  int minb = 4, dec = 1, tail = 0;
+};
+const Tuning& tuning();
+
 struct BatchView {
   const int64_t* doc_offsets;
   const int32_t* word_ids;

@@ -8,6 +8,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <atomic>
 #include <cstdint>
 #include <cstdlib>
 
@@ -28,6 +29,19 @@ __device__ __forceinline__ int64_t find_row(const int64_t* __restrict__ prefix, 
     if (__ldg(prefix + mid) <= p) lo = mid; else hi = mid;
   }
   return lo;
+}
+
+// Dynamic shared-memory opt-in of `kernel` on the current device, once per
+// device (the attribute is per device; `done` is the kernel's bitmask of
+// devices already configured, updated atomically).
+template <class Kernel>
+inline void smem_opt_in(Kernel* kernel, int bytes, std::atomic<unsigned long long>& done) {
+  int dev = 0;
+  cudaGetDevice(&dev);
+  const unsigned long long bit = dev < 64 ? 1ull << dev : 0ull;
+  if (bit && (done.load(std::memory_order_acquire) & bit)) return;
+  cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+  if (bit) done.fetch_or(bit, std::memory_order_acq_rel);
 }
 
 inline unsigned grid_for(int64_t threads, int block) {

@@ -559,13 +559,12 @@ int launch_eval_docs(const int64_t* doc_offsets, const int32_t* word_ids,
                      int64_t* doc_scored, double* theta_out, double* scratch,
                      int64_t scratch_doubles, int* err, cudaStream_t st) {
   if (n_docs == 0) return 0;
-  const char* ev = getenv("SAMELDA_EVAL");  // A/B: "cta", "warp"; default staged
-  if (K <= 1024 && !(ev && (ev[0] == 'c' || ev[0] == 'w')) && !getenv("SAMELDA_EVAL_WARP")) {
+  const char ev = tuning().eval_variant;  // A/B: 'c' cta, 'w' warp; default staged
+  if (K <= 1024 && ev != 'c' && ev != 'w') {
     // staged rows: 3 CTAs per SM share (almost) all of shared memory
     // (measured: 1 / 2 / 3 CTAs 176 / 148 / 139 ms at NYTimes shape;
     // SAMELDA_EVAL_CTAS_PER_SM overrides)
-    const char* cps_env = getenv("SAMELDA_EVAL_CTAS_PER_SM");
-    const int cps = cps_env ? max(1, atoi(cps_env)) : 3;
+    const int cps = tuning().eval_ctas_per_sm > 0 ? tuning().eval_ctas_per_sm : 3;
     const int KP = K | 1;
     const size_t fixed = (2 * static_cast<size_t>((K + 1) & ~1) + kEvalFoldMax) * sizeof(double) +
                          2 * kEvalFoldMax * sizeof(int32_t);
@@ -573,12 +572,8 @@ int launch_eval_docs(const int64_t* doc_offsets, const int32_t* word_ids,
     if (budget > fixed + static_cast<size_t>(KP) * sizeof(double)) {
       const int R = static_cast<int>(std::min<size_t>((budget - fixed) / (KP * sizeof(double)), static_cast<size_t>(kEvalFoldMax)));
       const size_t smem_s = fixed + static_cast<size_t>(R) * KP * sizeof(double);
-      static size_t configured_s = 48 * 1024;
-      if (smem_s > configured_s) {
-        cudaFuncSetAttribute(k_eval_stage, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             static_cast<int>(220 * 1024));
-        configured_s = 220 * 1024;
-      }
+      static std::atomic<unsigned long long> configured_s{0};
+      smem_opt_in(k_eval_stage, static_cast<int>(220 * 1024), configured_s);
       const int64_t blocks = min(n_docs, static_cast<int64_t>(148 * cps));
       // the dynamic document counter lives one past the per-document results
       cudaMemsetAsync(doc_scored + n_docs, 0, sizeof(int64_t), st);
@@ -588,15 +583,15 @@ int launch_eval_docs(const int64_t* doc_offsets, const int32_t* word_ids,
       return 1;
     }
   }
-  if (K <= kEvalCtaMaxK && !(ev && ev[0] == 'w') && !getenv("SAMELDA_EVAL_WARP")) {
+  if (K <= kEvalCtaMaxK && ev != 'w') {
     const size_t smem_c = (2 * static_cast<size_t>((K + 1) & ~1) + kEvalCtaThreads) * sizeof(double) +
                           kEvalCtaThreads * sizeof(int32_t);
-    static size_t configured_c = 48 * 1024;
-    if (smem_c > configured_c) {
-      cudaFuncSetAttribute(k_eval_cta, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                           static_cast<int>(smem_c));
-      configured_c = smem_c;
-    }
+    static std::atomic<unsigned long long> configured_c{0};
+    // largest smem_c over K <= kEvalCtaMaxK
+    smem_opt_in(k_eval_cta,
+                static_cast<int>((2 * static_cast<size_t>(kEvalCtaMaxK) + kEvalCtaThreads) * sizeof(double) +
+                                 kEvalCtaThreads * sizeof(int32_t)),
+                configured_c);
     // ~600 documents in flight: their fold rows stay L2-resident across sweeps
     const int64_t blocks = min(n_docs, static_cast<int64_t>(148 * 4));
     k_eval_cta<<<static_cast<unsigned>(blocks), kEvalCtaThreads, smem_c, st>>>(
@@ -607,12 +602,8 @@ int launch_eval_docs(const int64_t* doc_offsets, const int32_t* word_ids,
   const size_t smem = static_cast<size_t>(kEvalWarps) * 2 * K * sizeof(double);
   int64_t blocks = (n_docs + kEvalWarps - 1) / kEvalWarps;
   if (smem <= kEvalSmemMax) {
-    static size_t configured = 48 * 1024;
-    if (smem > configured) {
-      cudaFuncSetAttribute(k_eval_docs, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                           static_cast<int>(kEvalSmemMax));
-      configured = kEvalSmemMax;
-    }
+    static std::atomic<unsigned long long> configured{0};
+    smem_opt_in(k_eval_docs, static_cast<int>(kEvalSmemMax), configured);
     k_eval_docs<<<static_cast<unsigned>(blocks), kEvalWarps * 32, smem, st>>>(
         doc_offsets, word_ids, fold_counts, score_counts, n_docs, phi_wk, K, alpha, sweeps,
         doc_logp, doc_scored, theta_out, nullptr, err);

@@ -861,14 +861,8 @@ void launch_deferred(const BatchView& bv, const double* tb64, const double* phi6
   auto* n_draws = reinterpret_cast<unsigned long long*>(rec_mu + max_records);
   auto* draws = reinterpret_cast<DeferredDraw*>(n_draws + 2);
   cudaMemsetAsync(n_draws, 0, sizeof(unsigned long long), st);
-  static unsigned long long attr_set = 0;  // per device: dynamic smem opt-in
-  int dev = 0;
-  cudaGetDevice(&dev);
-  if (dev >= 64 || !((attr_set >> dev) & 1ull)) {
-    cudaFuncSetAttribute(k_deferred_expand, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         static_cast<int>(kExpSmem));
-    if (dev < 64) attr_set |= 1ull << dev;
-  }
+  static std::atomic<unsigned long long> attr_set{0};
+  smem_opt_in(k_deferred_expand, static_cast<int>(kExpSmem), attr_set);
   k_deferred_expand<<<148 * 3, 256, kExpSmem, st>>>(bv, tb64, phi64, mu, K, m_t, seed, t, sweep, rec,
                                              n_deferred, rec_mu, draws, n_draws,
                                              static_cast<unsigned long long>(draw_cap), tc, pc, err);
@@ -901,7 +895,7 @@ constexpr int kThruQueue = 288;  // 31 left over + 8 draws x 32 lanes, + 1 spare
 // the conditional law; P(z < 3) < 3e-3 at lambda >= 10)
 __device__ __forceinline__ uint32_t ptrs_f32_ge3(float lam, uint32_t k0, uint32_t k1, uint32_t blk0,
                                                  uint32_t w, uint32_t d, uint32_t t) {
-  const float slam = sqrtf(lam), loglam = __logf(lam);
+  const float slam = sqrtf(lam);
   const float b = 0.931f + 2.53f * slam;
   const float a = -0.059f + 0.02483f * b;
   const float inv_alpha = 1.1239f + 1.1328f / (b - 3.4f);
@@ -920,8 +914,13 @@ __device__ __forceinline__ uint32_t ptrs_f32_ge3(float lam, uint32_t k0, uint32_
         continue;
       }
       if (g < 3.0f || (us < 0.013f && v > us)) continue;
-      const float k = floorf(g);
-      if (logf(v * inv_alpha / (a / (us * us) + b)) <= -lam + k * loglam - lgammaf(k + 1.0f))
+      // the (rare) non-squeeze acceptance test in f64: at rates ~1e4 the
+      // right-hand side is a difference of ~1e5-sized terms, where lgammaf's
+      // few-ulp error would move the log acceptance ratio by ~0.1
+      const double k = floor(static_cast<double>(g));
+      const double dl = static_cast<double>(lam);
+      if (log(static_cast<double>(v) * inv_alpha / (a / (us * us) + b)) <=
+          -dl + k * log(dl) - lgamma(k + 1.0))
         return static_cast<uint32_t>(k);
     }
   }
@@ -1073,7 +1072,9 @@ __global__ void __launch_bounds__(BLK, MINB) k_sample_thru(
           acc[j / 2] += z << (16 * (j & 1));
           // unpredicated within the row (z = 0 adds 0); topics past K have no cell
           if (PHI && (FULL || kbase + lane + kWarp * j < K)) red_add_u64(pc + kWarp * j, z);
-          if (u > c2) tm |= 1u << jj;  // z >= 3 (for any rate: lambda >= 10 takes PTRS given z >= 3)
+          // z >= 3 (for any rate: lambda >= 10 takes PTRS given z >= 3); topics
+          // past K never queue, whatever ex2.approx returns at lambda = 0
+          if ((FULL || kbase + lane + kWarp * j < K) && u > c2) tm |= 1u << jj;
         }
         if (__any_sync(0xffffffffu, tm != 0u)) {  // queue this group's tails (lambda, u recomputed)
 #pragma unroll
@@ -1137,27 +1138,28 @@ int launch_fast_kpl(const BatchView& bv, const double* tb64, const float* tb32, 
       }
       return -1;  // caller passes phi counts for every other shape
     }
-    const char* minb_env = getenv("SAMELDA_MINB");
-    const int minb = minb_env ? atoi(minb_env) : 4;
-    const char* dec_env = getenv("SAMELDA_DEC");
-    const int dec = dec_env ? atoi(dec_env) : 1;
-    const char* tail_env = getenv("SAMELDA_TAIL");
-    const int tail = tail_env ? atoi(tail_env) : 0;
 #define SCU_V2_LAUNCH(FULLV, MS, MB, DC, ...)                                                   \
   k_sample_v2<KPL, FULLV, MS, MB, DC __VA_OPT__(,) __VA_ARGS__><<<grid, kFastBlock, 0, st>>>(    \
       bv, tb32, phi32, mu, muf, K, m_t, seed, t, sweep, chunk, tc, pc, rec, n_deferred)
-    // production: DEC 1, 4 blocks/SM; the bench instantiation also carries the
-    // A/B alternatives (SAMELDA_DEC=0|2, SAMELDA_MINB=3, SAMELDA_TAIL=1), all bit-identical
+    // production: DEC 1, 4 blocks/SM.  A library built with
+    // -DSAMELDA_AB_VARIANTS also carries the measured alternatives (all
+    // bit-identical, all slower at K = 256): SAMELDA_DEC=0|2, SAMELDA_MINB=3,
+    // SAMELDA_TAIL=1
+#ifdef SAMELDA_AB_VARIANTS
+    const Tuning& tu = tuning();
 #define SCU_V2(FULLV, MS)                                                                        \
   do {                                                                                           \
     if constexpr (KPL == 8 && FULLV && MS == 0) {                                                \
-      if (minb == 3) { SCU_V2_LAUNCH(FULLV, MS, 3, 1); break; }                                  \
-      if (dec == 0) { SCU_V2_LAUNCH(FULLV, MS, 4, 0); break; }                                   \
-      if (dec == 2) { SCU_V2_LAUNCH(FULLV, MS, 4, 2); break; }                                   \
-      if (tail == 1) { SCU_V2_LAUNCH(FULLV, MS, 4, 1, 1); break; }                               \
+      if (tu.minb == 3) { SCU_V2_LAUNCH(FULLV, MS, 3, 1); break; }                               \
+      if (tu.dec == 0) { SCU_V2_LAUNCH(FULLV, MS, 4, 0); break; }                                \
+      if (tu.dec == 2) { SCU_V2_LAUNCH(FULLV, MS, 4, 2); break; }                                \
+      if (tu.tail == 1) { SCU_V2_LAUNCH(FULLV, MS, 4, 1, 1); break; }                            \
     }                                                                                            \
     SCU_V2_LAUNCH(FULLV, MS, 4, 1);                                                              \
   } while (0)
+#else
+#define SCU_V2(FULLV, MS) SCU_V2_LAUNCH(FULLV, MS, 4, 1)
+#endif
     if (full) {
       if (musrc == 0) SCU_V2(true, 0); else if (musrc == 1) SCU_V2(true, 1); else SCU_V2(true, 2);
     } else {
@@ -1409,8 +1411,7 @@ int launch_sample_fast(const BatchView& bv, const double* theta_b64, const float
   // 256 with the full mu from a k_mu_f32 pre-pass.  SAMELDA_SAMPLER=x runs
   // the all-f64 exact kernel instead when the caller supplies mu (per-call
   // sample_counts): a device-side cross-check of the fast-exact path.
-  const char* variant = getenv("SAMELDA_SAMPLER");
-  if (variant && variant[0] == 'x' && mu != nullptr && pc != nullptr)
+  if (tuning().sampler_exact && mu != nullptr && pc != nullptr)
     return launch_sample(bv, theta_b64, phi64, mu, K, m_t, seed, t, sweep, kModeParity, tc, pc,
                          nullptr, nullptr, err, st);
   if (K <= 32)

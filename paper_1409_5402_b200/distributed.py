@@ -6,9 +6,11 @@ Every rank runs the same global MinibatchStream (corpus.cpp:252-285) and
 samples only the batch documents it owns; Philox keys use the GLOBAL doc id
 (`samelda_cu_set_doc_base`), so each rank draws exactly what one GPU would.
 The one exchange per period is a sum all-reduce of the W x K topic-word
-counts of the last inner sweep (sampler.cpp:320-332); integer addition is
-associative, so the reduced counts -- and the replicated M-step's phi -- are
-bit-identical to a single-GPU run.
+counts of the last inner sweep (sampler.cpp:320-332).  In the integer-count
+modes (parity, throughput) addition is associative, so the reduced counts --
+and the replicated M-step's phi -- are bit-identical to a single-GPU run; the
+expected-count mode all-reduces f64 sums, whose order (and so last bits) the
+collective chooses.
 
 `torch.distributed` is the plumbing (NCCL on B200s, gloo in the CPU tests);
 the per-rank compute is an *engine*: `CudaEngine` (the product, over
@@ -60,6 +62,9 @@ class CudaEngine:
         # trainer on that stream so the collective is ordered after sampling
         trainer.ctx.set_stream(torch.cuda.current_stream(device).cuda_stream)
 
+    def set_doc_base(self, base: int):
+        self.trainer.set_doc_base(base)
+
     def sample(self, local_ids, t, m_t):
         self.trainer.period_sample(local_ids, t, m_t)
 
@@ -102,6 +107,11 @@ class ShardedTrainer:
         self.tau0, self.gamma = tau0, gamma
         self.group = group
         self.t = 0
+        # Philox keys use GLOBAL doc ids: the engine's local doc 0 is global
+        # doc_lo (an engine without the hook keys streams itself, e.g. a test
+        # engine that receives global ids)
+        if hasattr(engine, "set_doc_base"):
+            engine.set_doc_base(doc_lo)
 
     def period(self) -> PeriodStats:
         import torch.distributed as dist

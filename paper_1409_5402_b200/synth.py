@@ -10,7 +10,22 @@ import os
 
 import numpy as np
 
-from .samelda import Corpus, load_library
+from .samelda import Corpus
+
+_LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "libsamelda_synth.so")
+_lib = None
+
+
+def load_library() -> C.CDLL:
+    """libsamelda_synth.so: the generator alone (host C++), so a process that
+    only needs corpora -- bench.py's reference arm -- never maps the CUDA
+    product library."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(_LIB_PATH):
+            raise ImportError(f"{_LIB_PATH} is missing: run `python -m paper_1409_5402_b200.build`")
+        _lib = C.CDLL(_LIB_PATH)
+    return _lib
 
 
 class _Params(C.Structure):
