@@ -1,26 +1,43 @@
-"""SAME factored Gibbs sampler benchmark (BASELINE.json metric and config).
+"""SAME factored Gibbs sampler benchmark (BASELINE.json metric and configs).
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
-                    [--config nytimes|c1|pubmed|k1024]
+                    [--config nytimes|c1|c3|pubmed|k1024|nytimes-expected|nytimes-fast]
+                    [--scaling strong|weak]
 
 A step is one SAME period (Algorithm 3; sampler.cpp:307-333) over one
 minibatch of the synthetic corpus: inner_sweeps x (SDDMM + Poisson replica
 sampling + count scatter) and the M-step.  Metric: sampled token x replica
 samples per second = sum over sweeps of (batch tokens x m_t) / time.
 
-Default workload (BASELINE.json configs[1]): NYTimes-shaped synthetic corpus
-(300K docs, 102,660 words, ~100M tokens, ~70M nonzeros), K=256, m=100,
-batch_fraction 0.05, inner_sweeps 2, parity mode (f64, reference-identical
-draws).  N>1 (torchrun): weak scaling -- rank r holds its own NYTimes-shaped
-shard of a global corpus of N x 300K docs; one global MinibatchStream, each
-rank samples the batch docs it owns, the W x K topic-word counts are
-all-reduced over NCCL once per period, the M-step is replicated.
+Configs (BASELINE.json `configs`):
+  c1       [0] the reference's own synthetic corpus make_corpus(10000, 5000, 32, 100, 1),
+               split_holdout(0.1, 1), K=32, m=10, full-batch periods, eval every 5;
+               e2e = the whole 20-period train() through the C ABI (samelda_cu_train)
+               against the reference's train() on the host cores
+  nytimes  [1] (default) NYTimes-shaped synthetic corpus (300K docs, 102,660 words,
+               ~100M tokens, ~70M nonzeros), K=256, m=100, bf=0.05, 2 inner sweeps
+  c3       [2] the same corpus with the linear annealing schedule: m_t = 2 m t / (T+1),
+               m = 50, T = the periods of the run, so m_t rises from ~1 to ~100
+  pubmed   [3] PubMed-shaped synthetic corpus (8.2M docs, 141,043 words, ~730M tokens)
+  k1024    [4] the NYTimes corpus at K=1024, m=50
+  nytimes-expected / nytimes-fast: the deterministic expected-count path and the
+               throughput mode on config [1]
+
+Multi-GPU: `--gpus N` with N > 1 outside torchrun re-launches this script
+under `torch.distributed.run` (one process per GPU, NCCL; 127.0.0.1).
+Strong scaling (default): the config's corpus is split into N contiguous
+document ranges, each rank generates and holds only its own; all ranks run
+one global MinibatchStream, each samples the batch docs it owns (Philox keys
+use global doc ids, so the draws equal one GPU's), the W x K topic-word
+counts are all-reduced over NCCL once per period, the M-step is replicated.
+`--scaling weak`: every rank holds its own full-size shard (N x the corpus).
 """
 from __future__ import annotations
 
 import argparse
 import json
 import os
+import socket
 import statistics
 import subprocess
 import sys
@@ -32,33 +49,40 @@ import numpy as np
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
+METRIC = "sampled tokens/sec (x m replicas)"
+
 CONFIGS = {
-    # BASELINE.json configs[1]
-    "nytimes": dict(corpus="nytimes", n_topics=256, m=100.0, batch_fraction=0.05,
+    "c1": dict(baseline=0, corpus="c1", n_topics=32, m=10.0, batch_fraction=1.0, inner_sweeps=2,
+               schedule="constant", t_max=20, eval_every=5,
+               workload="reference synthetic corpus make_corpus(10000 docs, 5000 words, 32 topics, "
+                        "len 100, seed 1) split_holdout(0.1, 1), K=32, m=10, full-batch periods "
+                        "(20 iterations), 2 inner sweeps, eval every 5"),
+    "nytimes": dict(baseline=1, corpus="nytimes", n_topics=256, m=100.0, batch_fraction=0.05,
                     inner_sweeps=2, schedule="constant",
                     workload="NYTimes-shaped synthetic corpus (300K docs, 102,660 vocab, ~100M "
                              "tokens), K=256, m=100, bf=0.05, 2 inner sweeps"),
-    # BASELINE.json configs[3] (one GPU holds it; 8xB200 is the published shape)
-    "pubmed": dict(corpus="pubmed", n_topics=256, m=100.0, batch_fraction=0.05, inner_sweeps=2,
-                   schedule="constant",
+    "c3": dict(baseline=2, corpus="nytimes", n_topics=256, m=50.0, batch_fraction=0.05,
+               inner_sweeps=2, schedule="linear",
+               workload="NYTimes-shaped synthetic corpus, K=256, SAME annealing m_t = 2*50*t/(T+1) "
+                        "(~1 to ~100 over the run's T periods), bf=0.05, 2 inner sweeps"),
+    "pubmed": dict(baseline=3, corpus="pubmed", n_topics=256, m=100.0, batch_fraction=0.05,
+                   inner_sweeps=2, schedule="constant",
                    workload="PubMed-shaped synthetic corpus (8.2M docs, 141,043 vocab, ~730M "
                             "tokens), K=256, m=100, bf=0.05"),
-    # the deterministic factored expected-count path (north star (3); z := rate)
-    "nytimes-expected": dict(corpus="nytimes", n_topics=256, m=100.0, batch_fraction=0.05,
-                             inner_sweeps=2, schedule="constant", mode="expected",
+    "k1024": dict(baseline=4, corpus="nytimes", n_topics=1024, m=50.0, batch_fraction=0.05,
+                  inner_sweeps=2, schedule="constant",
+                  workload="NYTimes-shaped synthetic corpus, K=1024, m=50, bf=0.05"),
+    "nytimes-expected": dict(baseline=1, corpus="nytimes", n_topics=256, m=100.0,
+                             batch_fraction=0.05, inner_sweeps=2, schedule="constant",
+                             mode="expected",
                              workload="NYTimes-shaped synthetic corpus, K=256, m=100, bf=0.05, "
                                       "2 inner sweeps, expected-count mode"),
-    # throughput mode: same sampler, own f32 random streams
-    # (statistical, not bit, parity with the reference)
-    "nytimes-fast": dict(corpus="nytimes", n_topics=256, m=100.0, batch_fraction=0.05,
+    "nytimes-fast": dict(baseline=1, corpus="nytimes", n_topics=256, m=100.0, batch_fraction=0.05,
                          inner_sweeps=2, schedule="constant", mode="throughput",
                          workload="NYTimes-shaped synthetic corpus, K=256, m=100, bf=0.05, "
                                   "2 inner sweeps, throughput mode (f32, own random streams)"),
-    # BASELINE.json configs[4]
-    "k1024": dict(corpus="nytimes", n_topics=1024, m=50.0, batch_fraction=0.05, inner_sweeps=2,
-                  schedule="constant",
-                  workload="NYTimes-shaped synthetic corpus, K=1024, m=50, bf=0.05"),
 }
+ALIASES = {"c2": "nytimes", "c4": "pubmed", "c5": "k1024"}
 
 PEAKS_FALLBACK = {"hbm_gbs": 6650.0}
 
@@ -68,7 +92,7 @@ def load_peaks():
         with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
             return json.load(f), "measured"
     except OSError:
-        return PEAKS_FALLBACK, "fallback"
+        return PEAKS_FALLBACK, "fallback (B200_PROFILING.md)"
 
 
 # ----------------------------------------------------------------- clocks
@@ -139,28 +163,91 @@ def dist_env():
     return world, rank, local
 
 
-def make_corpus(name: str, shard: int, n_threads: int | None = None):
-    from paper_1409_5402_b200 import synth
-    return synth.preset(name, seed=1, shard=shard, n_threads=n_threads)
+def relaunch_under_torchrun(n: int) -> int:
+    """One process per GPU: re-exec this script under torch.distributed.run."""
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    env = dict(os.environ)
+    # NCCL communicator setup in the log (rank count per communicator)
+    env.setdefault("NCCL_DEBUG", "INFO")
+    env.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node",
+           str(n), "--master-addr", "127.0.0.1", "--master-port", str(port),
+           os.path.abspath(__file__), *sys.argv[1:]]
+    return subprocess.run(cmd, env=env, cwd=ROOT).returncode
 
 
-def split_heldout(corpus, frac=0.1):
-    """Last `frac` of the (iid) generated docs are held out."""
-    from paper_1409_5402_b200.samelda import Corpus
-    D = corpus.n_docs
-    n_test = max(1, int(round(frac * D)))
-    cut = D - n_test
-    o = corpus.doc_offsets
-    train = Corpus(o[:cut + 1].copy(), corpus.word_ids[:o[cut]], corpus.counts[:o[cut]],
-                   corpus.n_words)
-    test = Corpus(o[cut:] - o[cut], corpus.word_ids[o[cut]:], corpus.counts[o[cut]:],
-                  corpus.n_words)
-    return train, test
+class Workload:
+    """The config's corpus as seen by one rank: its training documents (a contiguous range
+    [doc_lo, doc_lo + D_local) of the global training corpus), the held-out corpus (rank 0),
+    and the global sizes every arm reports."""
+
+    def __init__(self, cfg, world: int, rank: int, scaling: str):
+        from paper_1409_5402_b200 import synth
+        t0 = time.perf_counter()
+        self.world, self.rank = world, rank
+        if cfg["corpus"] == "c1":
+            whole = synth.make_corpus_ref(10000, 5000, 32, 100.0, 1)
+            train, test = synth.split_holdout(whole, 0.1, 1)  # commands.cpp:89-90
+            self.D_global = train.n_docs
+            lo, hi = train.n_docs * rank // world, train.n_docs * (rank + 1) // world
+            self.train = synth.subset(train, np.arange(lo, hi)) if world > 1 else train
+            self.doc_lo = lo
+            self.heldout = test if rank == 0 else None
+            self.total_docs = whole.n_docs
+        else:
+            kw = dict(synth.PRESETS[cfg["corpus"]])
+            D = kw.pop("n_docs")
+            n_test = max(1, int(round(0.1 * D)))  # the last 10% of the (iid) docs are held out
+            cut = D - n_test
+            if scaling == "weak":  # rank r: global docs [r D, (r + 1) D), its own full shard
+                first, lo, hi = rank * D, 0, cut
+                self.D_global = cut * world
+                self.doc_lo = rank * cut
+                self.total_docs = D * world
+            else:  # strong: the one corpus, training docs split into N contiguous ranges
+                first = 0
+                lo, hi = cut * rank // world, cut * (rank + 1) // world
+                self.D_global = cut
+                self.doc_lo = lo
+                self.total_docs = D
+            self.train = synth.generate(seed=1, n_docs=hi - lo, first_doc=first + lo, **kw)
+            self.heldout = (synth.generate(seed=1, n_docs=n_test, first_doc=first + cut, **kw)
+                            if rank == 0 else None)
+        self.gen_s = time.perf_counter() - t0
+
+
+def single_gpu_corpus(config: str = "nytimes"):
+    """(train, heldout) of a config's corpus as one GPU holds it (tests, tools)."""
+    wl = Workload(CONFIGS[ALIASES.get(config, config)], 1, 0, "strong")
+    return wl.train, wl.heldout
+
+
+# --------------------------------------------------------- shared record
+
+def config_record(cfg, world: int, scaling: str) -> dict:
+    """The `config` object -- identical in both arms for the same command line."""
+    return {"workload": cfg["workload"], "baseline_config": cfg["baseline"],
+            "K": cfg["n_topics"], "m": cfg["m"], "schedule": cfg["schedule"],
+            "batch_fraction": cfg["batch_fraction"], "inner_sweeps": cfg["inner_sweeps"],
+            "mode": cfg.get("mode", "parity"), "parallelism": f"doc-shard x{world}",
+            "scaling": scaling,
+            "l2": "inputs larger than L2 (phi + theta resident in HBM; random minibatch docs "
+                  "each step)" if cfg["corpus"] != "c1" else
+                  "C1 model (phi 1.3 MB) is L2-resident by design"}
+
+
+def run_t_max(cfg, args) -> int:
+    """Periods the run performs (warm-up, timed, profiled, end-to-end): the annealing
+    schedule's horizon T (c3: m_t rises over exactly this run)."""
+    prof = max(1, min(args.steps, 10))
+    return max(cfg.get("t_max", 0), args.warmup + args.steps + 2 * prof)
 
 
 # --------------------------------------------------------- reference arm
 
-def reference_step_fn(ref, corpus, cfg, sub_docs: int, n_threads: int, seed: int = 1):
+def reference_step_fn(ref, corpus, cfg, sub_docs: int, n_threads: int, t_max: int, seed: int = 1):
     """One reference period (sampler.cpp:307-333) on a bounded sub-batch, through the
     compiled reference's own sddmm / sample_counts / update_model with n_threads."""
     from oracle import CorpusArrays
@@ -179,12 +266,13 @@ def reference_step_fn(ref, corpus, cfg, sub_docs: int, n_threads: int, seed: int
         local = np.arange(len(ids), dtype=np.int32)
         theta = np.full((len(ids), K), 0.1 + 1.0 / K)
         tb = theta.copy()
-        m_t = cfg["m"]
+        m_t = ref.anneal_m(cfg["schedule"], min(t + 1, t_max), t_max, cfg["m"])
         for sweep in range(cfg["inner_sweeps"]):
             mu = ref.sddmm(tb, phi, sub, local, n_threads)
             tc, pc = ref.sample_counts(tb, phi, mu, sub, local, m_t, seed, t, sweep, n_threads)
             tb = tc / m_t + 0.1
-        theta2, phi2 = ref.update_model(theta, phi, local, tc, pc, m_t, 0.5, 0.1, 0.01)
+        theta2, phi2 = ref.update_model(theta, phi, local, tc, pc, m_t, ref.rho_schedule(t, 1.0, 0.5),
+                                        0.1, 0.01)
         phi[:] = phi2
         tokens = int(sub.counts.astype(np.int64).sum())
         return cfg["inner_sweeps"] * tokens * m_t, int(sub.nnz)
@@ -202,14 +290,14 @@ def _subset(corpus, ids):
         corpus.counts[idx])
 
 
-def calibrate_reference(corpus, cfg, n_threads: int):
+def calibrate_reference(corpus, cfg, n_threads: int, t_max: int):
     """Fit the reference's period time as a + b * docs (a = per-period fixed cost:
     the phi transposes of sddmm/sample_counts, update_model over K x W)."""
     from oracle import Ref
     ref = Ref()
     times = {}
     for n in (64, 512):
-        step = reference_step_fn(ref, corpus, cfg, n, n_threads, seed=7)
+        step = reference_step_fn(ref, corpus, cfg, n, n_threads, t_max, seed=7)
         t0 = time.perf_counter()
         step()
         times[n] = time.perf_counter() - t0
@@ -225,48 +313,78 @@ def reference_sub_batch(corpus, cfg, a, b, budget_s):
     return int(max(64, min(full, (budget_s - a) / b)))
 
 
+def reference_train_c1(wl: Workload, cfg, n_threads: int):
+    """The reference's own train() (sampler.cpp:269-353) on config [0], with eval every 5:
+    (samples per run, wall seconds)."""
+    from oracle import CorpusArrays, Ref, TrainConfig
+    ref = Ref()
+    tr = CorpusArrays(wl.train.doc_offsets, wl.train.word_ids, wl.train.counts, wl.train.n_words)
+    te = CorpusArrays(wl.heldout.doc_offsets, wl.heldout.word_ids, wl.heldout.counts,
+                      wl.heldout.n_words)
+    tc = TrainConfig(n_topics=cfg["n_topics"], m=cfg["m"], schedule=cfg["schedule"],
+                     batch_fraction=cfg["batch_fraction"], t_max=cfg["t_max"],
+                     inner_sweeps=cfg["inner_sweeps"], seed=1, n_threads=n_threads)
+    t0 = time.perf_counter()
+    _, _, trace = ref.train(tr, tc, te, cfg["eval_every"])
+    dt = time.perf_counter() - t0
+    samples = cfg["inner_sweeps"] * cfg["m"] * wl.train.n_tokens * cfg["t_max"]  # full batches
+    return samples, dt, trace
+
+
 def run_reference(args, cfg):
     world, rank, _ = dist_env()
     if rank != 0:
         return
+    scaling = args.scaling
+    record = config_record(cfg, world, scaling)
     if cfg.get("mode") == "expected":
         print(json.dumps({"impl": "reference",
                           "unavailable": "the reference has no expected-count mode "
-                                         "(sampler.cpp draws Poisson replicas only)"}), flush=True)
+                                         "(sampler.cpp draws Poisson replicas only)",
+                          "config": record}), flush=True)
         return
     n_threads = os.cpu_count() or 1
-    corpus = make_corpus(cfg["corpus"], 0)
-    train, _ = split_heldout(corpus)
-    ref, a, b = calibrate_reference(train, cfg, n_threads)
-    budget = max(3.0, 180.0 / max(args.steps, 1))
-    if os.environ.get("BENCH_REF_BUDGET_S"):  # tests: cap the per-step CPU sample
-        budget = float(os.environ["BENCH_REF_BUDGET_S"])
-    sub = reference_sub_batch(train, cfg, a, b, budget_s=budget)
-    step = reference_step_fn(ref, train, cfg, sub, n_threads)
-    warm = reference_step_fn(ref, train, cfg, 64, n_threads, seed=3)
-    for _ in range(args.warmup):  # CPU code needs no warm-up; keep these cheap
-        warm()
-    samples = 0.0
-    t0 = time.perf_counter()
-    for _ in range(args.steps):
-        s, _ = step()
-        samples += s
-    dt = time.perf_counter() - t0
-    value = samples / dt
+    wl = Workload(cfg, 1, 0, "strong")  # the whole corpus on the host
+    t_max = run_t_max(cfg, args)
+    if cfg["corpus"] == "c1":
+        samples, dt, _ = reference_train_c1(wl, cfg, n_threads)
+        value = samples / dt
+        ms = 1000.0 * dt / cfg["t_max"]
+        sample_desc = (f"one complete reference train() (oracle/_ref compiled from proj/src): "
+                       f"{cfg['t_max']} full-batch periods + eval every {cfg['eval_every']}, "
+                       f"{n_threads} threads, {dt:.1f}s")
+    else:
+        train = wl.train
+        ref, a, b = calibrate_reference(train, cfg, n_threads, t_max)
+        budget = max(3.0, 180.0 / max(args.steps, 1))
+        if os.environ.get("BENCH_REF_BUDGET_S"):  # tests: cap the per-step CPU sample
+            budget = float(os.environ["BENCH_REF_BUDGET_S"])
+        sub = reference_sub_batch(train, cfg, a, b, budget_s=budget)
+        step = reference_step_fn(ref, train, cfg, sub, n_threads, t_max)
+        warm = reference_step_fn(ref, train, cfg, 64, n_threads, t_max, seed=3)
+        for _ in range(args.warmup):  # CPU code needs no warm-up; keep these cheap
+            warm()
+        samples = 0.0
+        t0 = time.perf_counter()
+        for _ in range(args.steps):
+            s, _ = step()
+            samples += s
+        dt = time.perf_counter() - t0
+        value = samples / dt
+        ms = 1000.0 * dt / args.steps
+        sample_desc = (f"reference sddmm+sample_counts x{cfg['inner_sweeps']} + update_model per "
+                       f"step on a random {sub}-doc batch (full batch = "
+                       f"{int(round(cfg['batch_fraction'] * train.n_docs))} docs; oracle/_ref "
+                       f"compiled from proj/src, {n_threads} threads; fitted period time "
+                       f"{a:.2f}s + {b * 1e3:.2f}ms/doc)")
     line = {
-        "impl": "reference", "metric": "sampled tokens/sec (x m replicas)", "value": value,
+        "impl": "reference", "metric": METRIC, "value": value,
         "unit": "samples/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
-        "ms_per_step": 1000.0 * dt / args.steps, "higher_is_better": True,
-        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": cfg["workload"], "K": cfg["n_topics"], "m": cfg["m"],
-                   "batch_fraction": cfg["batch_fraction"], "inner_sweeps": cfg["inner_sweeps"]},
+        "ms_per_step": ms, "higher_is_better": True,
+        "scaling": scaling, "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": record,
         "cpu_baseline": {"value": value, "unit": "samples/s", "cores": n_threads,
-                         "kind": "reference",
-                         "sample": f"reference sddmm+sample_counts x{cfg['inner_sweeps']} + "
-                                   f"update_model per step on a random {sub}-doc batch "
-                                   f"(full batch = {int(round(cfg['batch_fraction'] * train.n_docs))}"
-                                   f" docs; oracle/_ref compiled from proj/src, {n_threads} "
-                                   f"threads; fitted period time {a:.2f}s + {b * 1e3:.2f}ms/doc)"},
+                         "kind": "reference", "sample": sample_desc},
         "e2e": {"value": value, "unit": "samples/s", "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
     }
@@ -274,6 +392,23 @@ def run_reference(args, cfg):
 
 
 # --------------------------------------------------------------- our arm
+
+def bytes_per_unit(cfg, final_sweep: bool) -> tuple[int, int]:
+    """SURVEY.md 8(d) algorithmic bytes at the element sizes the mode computes in:
+    per batch nonzero 8 (word id + count) + e_phi K (phi row) [+ e_cnt K (phi-count row),
+    final sweep only: earlier sweeps scatter no phi counts]; per batch doc 8 + e_th K
+    (theta row) + e_cnt K (theta counts).  Parity: f64 phi/theta, int32 counts;
+    expected: f64 rows and f64 counts; throughput: f32 rows, int32 counts."""
+    K = cfg["n_topics"]
+    mode = cfg.get("mode", "parity")
+    e_row, e_cnt = {"expected": (8, 8), "throughput": (4, 4)}.get(mode, (8, 4))
+    # which sweeps scatter phi counts: the final one; every one in expected mode and in
+    # the parity kernel's multi-slice shapes (K != 256)
+    scatter = final_sweep or mode == "expected" or (mode == "parity" and K != 256)
+    per_nnz = 8 + e_row * K + (e_cnt * K if scatter else 0)
+    per_doc = 8 + e_row * K + e_cnt * K
+    return per_nnz, per_doc
+
 
 def run_ours(args, cfg):
     import torch
@@ -291,8 +426,13 @@ def run_ours(args, cfg):
             dist.init_process_group("gloo")
         else:
             dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        nccl_v = torch.cuda.nccl.version() if not share else None
+        print(f"[bench] rank {rank}/{world} cuda:{local} backend "
+              f"{dist.get_backend()} nccl {nccl_v}", file=sys.stderr, flush=True)
+    from paper_1409_5402_b200 import distributed as DIST
     from paper_1409_5402_b200 import samelda as S
 
+    scaling = args.scaling
     ctx = S.Context(local)
     # one dedicated (non-blocking) stream for torch and the context: events,
     # collectives and kernels are all ordered on it, and nothing serialises
@@ -301,28 +441,21 @@ def run_ours(args, cfg):
     torch.cuda.set_stream(stream)
     ctx.set_stream(stream.cuda_stream)
 
-    t_gen = time.perf_counter()
-    corpus = make_corpus(cfg["corpus"], rank)
-    train, heldout = split_heldout(corpus)
-    gen_s = time.perf_counter() - t_gen
-    D_local = train.n_docs
-    D_global = D_local * world
-    doc_base = rank * D_local  # weak scaling: rank r owns global docs [r*D, (r+1)*D)
-
+    wl = Workload(cfg, world, rank, scaling)
+    train = wl.train
+    t_max = run_t_max(cfg, args)
     scfg = S.SamplerConfig(n_topics=cfg["n_topics"], m=cfg["m"], schedule=cfg["schedule"],
                            batch_fraction=cfg["batch_fraction"], inner_sweeps=cfg["inner_sweeps"],
-                           t_max=args.warmup + args.steps + 2 * max(1, min(args.steps, 10)), seed=1,
+                           t_max=t_max, seed=1,
                            mode={"expected": S.MODE_EXPECTED, "throughput": S.MODE_THROUGHPUT}.get(
                                cfg.get("mode"), S.MODE_PARITY))
     trainer = S.Trainer(train, scfg, ctx=ctx)
-    trainer.set_doc_base(doc_base)
     if rank == 0:
-        trainer.set_heldout(heldout, seed=1)
-    from paper_1409_5402_b200 import distributed as DIST
+        trainer.set_heldout(wl.heldout, seed=1)
     engine = DIST.CudaEngine(trainer, local)
-    sharded = DIST.ShardedTrainer(engine, D_global, doc_base, doc_base + D_local,
+    sharded = DIST.ShardedTrainer(engine, wl.D_global, wl.doc_lo, wl.doc_lo + train.n_docs,
                                   train.doc_tokens(), cfg["batch_fraction"], 1, cfg["m"],
-                                  cfg["schedule"], scfg.t_max)
+                                  cfg["schedule"], t_max)
 
     def period(t, result_buf=None):
         assert t == sharded.t
@@ -340,20 +473,12 @@ def run_ours(args, cfg):
             dist.barrier()
             torch.cuda.synchronize()
 
-    def max_over_ranks(x: float) -> float:
+    def over_ranks(x: float, op: str) -> float:
         if world == 1:
             return x
         import torch.distributed as dist
         t = torch.tensor([x], dtype=torch.float64, device=f"cuda:{local}")
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        return float(t.item())
-
-    def sum_over_ranks(x: float) -> float:
-        if world == 1:
-            return x
-        import torch.distributed as dist
-        t = torch.tensor([x], dtype=torch.float64, device=f"cuda:{local}")
-        dist.all_reduce(t)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX if op == "max" else dist.ReduceOp.SUM)
         return float(t.item())
 
     t = 0
@@ -378,10 +503,10 @@ def run_ours(args, cfg):
         t += 1
     ev1.record(stream)
     barrier()
-    dev_ms = max_over_ranks(ev0.elapsed_time(ev1))
+    dev_ms = over_ranks(ev0.elapsed_time(ev1), "max")
     launches = ctx.launches - launches0
     clk = clocks.stop()
-    samples_all = sum_over_ranks(samples)
+    samples_all = over_ranks(samples, "sum")
     value = samples_all / (dev_ms / 1000.0)
 
     # ---- per-kernel CUDA-event timing on a separate profiled pass (the
@@ -405,10 +530,11 @@ def run_ours(args, cfg):
     # host batch ids go H2D inside Trainer.period and the batch theta rows
     # (the step's result) come back D2H
     e2e_steps = max(1, min(args.steps, 10))
-    # a rank owns ~batch_fraction x D_local docs of each global batch (the
-    # call fails loudly if a buffer is ever too small)
-    bmax = int(1.25 * cfg["batch_fraction"] * D_local) + 64
-    bufs = [torch.empty(bmax * cfg["n_topics"], dtype=torch.float64, pin_memory=True).numpy()
+    # a rank owns ~batch_fraction x D_global / N docs of each global batch
+    # (the call fails loudly if a buffer is ever too small)
+    bmax = int(1.25 * cfg["batch_fraction"] * wl.D_global / (world if scaling == "strong" else 1)) + 64
+    bmax = min(bmax, train.n_docs)
+    bufs = [torch.empty(max(bmax, 1) * cfg["n_topics"], dtype=torch.float64, pin_memory=True).numpy()
             for _ in range(e2e_steps)]
     barrier()
     h2d = d2h = 0
@@ -421,32 +547,72 @@ def run_ours(args, cfg):
         d2h += out.nbytes + 4
         t += 1
     barrier()
-    e2e_s = max_over_ranks(time.perf_counter() - t0)
-    e2e_value = sum_over_ranks(samples_e2e) / e2e_s
-
+    e2e_s = over_ranks(time.perf_counter() - t0, "max")
+    e2e_value = over_ranks(samples_e2e, "sum") / e2e_s
+    e2e = {"value": e2e_value, "unit": "samples/s", "h2d_bytes_per_step": h2d // e2e_steps,
+           "d2h_bytes_per_step": d2h // e2e_steps,
+           "how": "Trainer periods through the C ABI: host batch ids H2D, batch theta rows D2H"}
     gc.enable()
+
+    # C1: the whole train() through the drop-in entry point (samelda_cu_train),
+    # host buffers in and out, eval every 5 -- the call the reference's C++
+    # train() shim makes, against the reference's own train()
+    if cfg["corpus"] == "c1" and world == 1:
+        tcfg = S.SamplerConfig(n_topics=cfg["n_topics"], m=cfg["m"], schedule=cfg["schedule"],
+                               batch_fraction=cfg["batch_fraction"],
+                               inner_sweeps=cfg["inner_sweeps"], t_max=cfg["t_max"], seed=1)
+        runs = []
+        for _ in range(3):
+            c2 = S.Context(local)  # fresh context: corpus upload, init, everything
+            t0 = time.perf_counter()
+            _, trace = S.train(train, tcfg, wl.heldout, cfg["eval_every"], ctx=c2)
+            runs.append(time.perf_counter() - t0)
+            c2.close()
+        run_s = min(runs)
+        s_run = cfg["inner_sweeps"] * cfg["m"] * train.n_tokens * cfg["t_max"]
+        corpus_bytes = (train.doc_offsets.nbytes + train.word_ids.nbytes + train.counts.nbytes +
+                        wl.heldout.doc_offsets.nbytes + wl.heldout.word_ids.nbytes +
+                        wl.heldout.counts.nbytes)
+        W, K = train.n_words, cfg["n_topics"]
+        e2e = {"value": s_run / run_s, "unit": "samples/s",
+               "h2d_bytes_per_step": int((corpus_bytes + 4 * train.n_docs * cfg["t_max"]) / cfg["t_max"]),
+               "d2h_bytes_per_step": int(8 * (K * W + train.n_docs * K) / cfg["t_max"]),
+               "how": f"samelda_cu_train (drop-in train(), sampler.cpp:269-353): fresh context, "
+                      f"{cfg['t_max']} periods, eval every {cfg['eval_every']}, model download; "
+                      f"best of 3 runs {run_s:.3f}s", "final_ll": trace[-1]["ll"]}
+
     heldout_ll = trainer.evaluate() if rank == 0 else None
 
-    # ---- roofline of the dominant kernel (sampling), algorithmic bytes
-    K = cfg["n_topics"]
-    # SURVEY.md 8(d) per-unit figure at parity-mode element sizes (phi f64
-    # "use 8 in place of 4", int32 counts): per batch nonzero 8 (word id +
-    # count) + 8K (phi column) + 4K (phi-count column); per batch doc
-    # 8 + 8K (theta row) + 4K (theta counts).  This build moves the same
-    # 12K + 8 per nonzero (phi32 4K + u64 counts 8K).
-    # (expected-count mode: f64 rates -- 8K phi row + 8K f64 RED per nonzero)
-    per_nnz = 8 + (16 if cfg.get("mode") == "expected" else 12) * K
-    per_doc = 8 + (16 if cfg.get("mode") == "expected" else 12) * K
-    alg_bytes = prof["nnz"] * per_nnz + prof["docs"] * per_doc
-    sample_ms = prof["sample_ms"]
+    # ---- roofline of the dominant kernel (sampling), algorithmic bytes per sweep kind
     peaks, peaks_kind = load_peaks()
     peak = float(peaks.get("hbm_gbs", PEAKS_FALLBACK["hbm_gbs"]))
+    n_sweeps = cfg["inner_sweeps"]
+    nnz_per_launch = prof["nnz"] / max(prof["sample_launches"], 1)
+    docs_per_launch = prof["docs"] / max(prof["sample_launches"], 1)
+    sweeps = {}
+    for kind, final in (("first", False), ("last", True)):
+        n = prof[f"sample_{kind}_launches"]
+        if n == 0:
+            continue
+        pn, pd = bytes_per_unit(cfg, final)
+        b = nnz_per_launch * pn + docs_per_launch * pd
+        ms = prof[f"sample_{kind}_ms"] / n
+        sweeps[kind] = {"launches": n, "avg_launch_ms": ms, "alg_bytes_per_launch": b,
+                        "achieved_gbs": b / (ms / 1e3) / 1e9 if ms > 0 else 0.0}
+    alg_bytes = sum(s["alg_bytes_per_launch"] * s["launches"] for s in sweeps.values())
+    sample_ms = prof["sample_ms"]
     achieved = alg_bytes / (sample_ms / 1000.0) / 1e9 if sample_ms > 0 else 0.0
-    traffic = None
+    for s in sweeps.values():
+        s["frac"] = s["achieved_gbs"] / peak
+    traffic = dram = None
     tfile = os.path.join(ROOT, "profiles", "sample_kernel_traffic.json")
     if os.path.exists(tfile):
         try:
-            traffic = json.load(open(tfile)).get(args.config, {}).get("dram_bytes_per_launch")
+            entry = json.load(open(tfile)).get(args.config, {})
+            traffic = entry.get("dram_bytes_per_launch")
+            if traffic:
+                dram_gbs = traffic / (sample_ms / max(prof["sample_launches"], 1) / 1e3) / 1e9
+                dram = {"gbs": dram_gbs, "frac": dram_gbs / peak, "source": entry.get("source")}
         except (OSError, ValueError):
             traffic = None
 
@@ -454,44 +620,52 @@ def run_ours(args, cfg):
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         try:
             n_threads = os.cpu_count() or 1
-            ref, a, b = calibrate_reference(train, cfg, n_threads)
-            sub = reference_sub_batch(train, cfg, a, b, budget_s=25.0)
-            step = reference_step_fn(ref, train, cfg, sub, n_threads)
-            c0 = time.perf_counter()
-            s, _ = step()
-            cdt = time.perf_counter() - c0
-            cpu = {"value": s / cdt, "unit": "samples/s", "cores": n_threads,
-                   "kind": "reference",
-                   "sample": f"1 reference period (sddmm+sample_counts x{cfg['inner_sweeps']} + "
-                             f"update_model) on a random {sub}-doc batch (full batch "
-                             f"{int(round(cfg['batch_fraction'] * train.n_docs))}), oracle/_ref "
-                             f"compiled from proj/src, {n_threads} threads, {cdt:.1f}s"}
+            if cfg["corpus"] == "c1":
+                s_ref, cdt, _ = reference_train_c1(wl, cfg, n_threads)
+                cpu = {"value": s_ref / cdt, "unit": "samples/s", "cores": n_threads,
+                       "kind": "reference",
+                       "sample": f"one complete reference train() ({cfg['t_max']} periods, eval "
+                                 f"every {cfg['eval_every']}), oracle/_ref compiled from proj/src, "
+                                 f"{n_threads} threads, {cdt:.1f}s"}
+            else:
+                ref, a, b = calibrate_reference(train, cfg, n_threads, t_max)
+                sub = reference_sub_batch(train, cfg, a, b, budget_s=25.0)
+                step = reference_step_fn(ref, train, cfg, sub, n_threads, t_max)
+                c0 = time.perf_counter()
+                s, _ = step()
+                cdt = time.perf_counter() - c0
+                cpu = {"value": s / cdt, "unit": "samples/s", "cores": n_threads,
+                       "kind": "reference",
+                       "sample": f"1 reference period (sddmm+sample_counts x{n_sweeps} + "
+                                 f"update_model) on a random {sub}-doc batch (full batch "
+                                 f"{int(round(cfg['batch_fraction'] * train.n_docs))}), oracle/_ref "
+                                 f"compiled from proj/src, {n_threads} threads, {cdt:.1f}s"}
         except Exception as e:  # reported, not fatal
             cpu = {"value": None, "unit": "samples/s", "cores": os.cpu_count(), "kind": "reference",
                    "sample": f"unavailable: {e}"}
 
+    corpus = {"train_docs": wl.D_global, "train_nnz_rank0": train.nnz,
+              "train_tokens_rank0": train.n_tokens, "docs_rank0": train.n_docs,
+              "heldout_docs": wl.heldout.n_docs if wl.heldout is not None else None,
+              "generate_s": round(wl.gen_s, 2)}
     if rank == 0:
         line = {
-            "metric": "sampled tokens/sec (x m replicas)", "value": value, "unit": "samples/s",
+            "metric": METRIC, "value": value, "unit": "samples/s",
             "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
-            "ms_per_step": dev_ms / args.steps, "higher_is_better": True, "scaling": "weak",
-            "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": {"workload": cfg["workload"], "K": K, "m": cfg["m"],
-                       "batch_fraction": cfg["batch_fraction"],
-                       "inner_sweeps": cfg["inner_sweeps"], "mode": cfg.get("mode", "parity"),
-                       "docs_per_gpu": D_local, "nnz_per_gpu": train.nnz,
-                       "tokens_per_gpu": train.n_tokens, "parallelism": f"doc-shard x{world}",
-                       "l2": "inputs larger than L2 (phi 210 MB f64 + theta 553 MB per GPU; "
-                             "random minibatch docs each step)",
-                       "corpus_gen_s": round(gen_s, 2)},
+            "ms_per_step": dev_ms / args.steps, "higher_is_better": True, "scaling": scaling,
+            "vs_baseline": None, "dtype": {"throughput": "f32"}.get(cfg.get("mode"), "f64"),
+            "data": "synthetic",
+            "config": config_record(cfg, world, scaling),
+            "corpus": corpus,
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                         "model": "SURVEY 8(d) per-nonzero gather bytes (phi row + count row per "
-                                  "nonzero, theta rows per doc); rows re-read from L2 are counted, "
-                                  "so frac can exceed 1 for an L2-resident kernel -- see traffic "
-                                  "for DRAM bytes",
                          "frac": achieved / peak if peak else None, "traffic": traffic,
+                         "model": "SURVEY 8(d) algorithmic bytes per launch: per batch nonzero "
+                                  "8 + 8K (f64 phi row) + 4K (int32 phi-count row, final sweep "
+                                  "only), per batch doc 8 + 12K; rows re-read from L2 count, so "
+                                  "frac can exceed the DRAM fraction -- see dram",
                          "kernel": {"expected": "k_expected", "throughput": "k_sample_thru"}.get(
-                             cfg.get("mode"), "k_sample_v2 + deferred (parity)"), "peak_kind": peaks_kind,
+                             cfg.get("mode"), "k_sample_v2 + deferred (parity)"),
+                         "peak_kind": peaks_kind, "per_sweep": sweeps, "dram": dram,
                          "alg_bytes_per_launch": alg_bytes / max(prof["sample_launches"], 1),
                          "avg_launch_ms": sample_ms / max(prof["sample_launches"], 1),
                          "sample_share_of_step": sample_ms / prof_ms if prof_ms else None,
@@ -499,8 +673,7 @@ def run_ours(args, cfg):
                          "deferred_records_per_launch": prof["deferred"] / max(prof["sample_launches"], 1),
                          "profiled_steps": prof_steps},
             "cpu_baseline": cpu,
-            "e2e": {"value": e2e_value, "unit": "samples/s",
-                    "h2d_bytes_per_step": h2d // e2e_steps, "d2h_bytes_per_step": d2h // e2e_steps},
+            "e2e": e2e,
             "gpu_launches": launches,
             "clocks": clk,
             "heldout_ll": heldout_ll,
@@ -517,10 +690,14 @@ def main():
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--config", default="nytimes", choices=sorted(CONFIGS))
+    ap.add_argument("--config", default="nytimes", choices=sorted(CONFIGS) + sorted(ALIASES))
+    ap.add_argument("--scaling", default="strong", choices=["strong", "weak"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     args = ap.parse_args()
+    args.config = ALIASES.get(args.config, args.config)
     cfg = CONFIGS[args.config]
+    if "WORLD_SIZE" not in os.environ and args.gpus > 1:
+        sys.exit(relaunch_under_torchrun(args.gpus))
     if args.impl == "reference":
         run_reference(args, cfg)
     else:

@@ -203,9 +203,11 @@ int samelda_cu_phi_counts_device(samelda_cu_ctx* ctx, void** ptr, int64_t* n_ele
  * of the global corpus under local ids 0..D-1; Philox stream keys use the
  * global id, so every shard draws exactly what a single GPU would. */
 int samelda_cu_set_doc_base(samelda_cu_ctx* ctx, int64_t doc_base);
-/* CUDA-event timing of the period kernels (0 sample, 1 sddmm, 2 M-step). */
+/* CUDA-event timing of the period kernels (0 sampling of a non-final inner
+ * sweep, 1 sddmm, 2 M-step, 3 sampling of the final inner sweep -- the one
+ * that scatters phi counts). */
 int samelda_cu_profile(samelda_cu_ctx* ctx, int32_t enable);
-/* ms_out[3] summed event time, launches_out[3] launches timed; batch nonzeros
+/* ms_out[4] summed event time, launches_out[4] launches timed; batch nonzeros
  * and docs seen by the timed sample launches, and the deferred exact-draw
  * records they produced (profiling synchronises after every sample launch to
  * read that count).  Resets the accumulators. */

@@ -322,9 +322,9 @@ struct samelda_cu_ctx {
 
   // optional per-kernel CUDA-event timing (bench roofline)
   bool profile = false;
-  enum { kSample = 0, kSddmm = 1, kMstep = 2, kKinds = 3 };
+  enum { kSample = 0, kSddmm = 1, kMstep = 2, kSampleLast = 3, kKinds = 4 };
   std::vector<std::pair<cudaEvent_t, cudaEvent_t>> events[kKinds];
-  size_t events_used[kKinds] = {0, 0, 0};
+  size_t events_used[kKinds] = {0, 0, 0, 0};
   int64_t prof_nnz = 0, prof_docs = 0, prof_deferred = 0;
 
   void tick(int kind, bool start) {
@@ -580,11 +580,11 @@ struct samelda_cu_ctx {
       double* pf_ = ensure<double>(pf, W_ * K_);
       ck(cudaMemsetAsync(tf_, 0, sizeof(double) * std::max<int64_t>(bv.B * K_, 1), stream), "zero tf");
       ck(cudaMemsetAsync(pf_, 0, sizeof(double) * std::max<int64_t>(W_ * K_, 1), stream), "zero pf");
-      tick(kSample, true);
+      tick(need_phi ? kSampleLast : kSample, true);
       launches += scu::launch_sample(bv, theta_b, phi_wk, mu_d, K_, m_t_, seed,
                                      static_cast<uint32_t>(t), static_cast<uint32_t>(sweep), mode,
                                      nullptr, nullptr, tf_, pf_, d_err(), stream);
-      tick(kSample, false);
+      tick(need_phi ? kSampleLast : kSample, false);
     } else {
       auto* tc_ = ensure<unsigned long long>(tc, bv.B * K_);
       auto* pc_ = ensure<unsigned long long>(pc, W_ * K_);
@@ -595,12 +595,12 @@ struct samelda_cu_ctx {
           !need_phi && mu_d == nullptr && (K_ == 256 || mode == SAMELDA_CU_MODE_THROUGHPUT);
       if (skip_phi) pc_ = nullptr;
       else ck(cudaMemsetAsync(pc_, 0, sizeof(unsigned long long) * std::max<int64_t>(W_ * K_, 1), stream), "zero pc");
-      tick(kSample, true);
+      tick(need_phi ? kSampleLast : kSample, true);
       if (mode == SAMELDA_CU_MODE_THROUGHPUT) {
         launches += scu::launch_sample_throughput(
             bv, theta_b32, phi_wk32, K_, m_t_, seed, static_cast<uint32_t>(t), static_cast<uint32_t>(sweep),
             tc_, pc_, K_ > 256 ? ensure<float>(mu_f32, bv.nnz) : nullptr, stream);
-        tick(kSample, false);
+        tick(need_phi ? kSampleLast : kSample, false);
         return;
       }
       const int64_t records = bv.nnz * ((K_ + 255) / 256);
@@ -613,7 +613,7 @@ struct samelda_cu_ctx {
                                           ensure<unsigned long long>(n_deferred, 1), aux, draw_cap,
                                           K_ > 256 ? ensure<float>(mu_f32, bv.nnz) : nullptr, d_err(),
                                           stream);
-      tick(kSample, false);
+      tick(need_phi ? kSampleLast : kSample, false);
       if (profile) {
         unsigned long long nd = 0;
         ck(cudaMemcpyAsync(&nd, n_deferred.p, sizeof(nd), cudaMemcpyDeviceToHost, stream), "n_deferred");

@@ -93,6 +93,106 @@ struct Generated {
 
 }  // namespace
 
+// ------------------------------------------------------------------------
+// The reference's own generator, value for value: synthetic::make_corpus
+// (tests/support/synthetic.cpp:61-106) on the reference's streams
+// (rng.cpp:90-137: phi rows from one stream keyed (0,0,0,tag(synthetic,1)),
+// document d from (0,d,0,tag(synthetic,2))), with poisson_sample and
+// categorical_sample (rng.cpp:139-179) restated.  BASELINE.json configs[0]
+// is this corpus at (10000, 5000, 32, 100, seed 1).  Two changes of method,
+// not of result: documents are generated in parallel (each has its own
+// stream), and a token's categorical scan over a phi row is a binary search
+// over that row's running sums, which are the scan's own partial sums
+// (same order, same rounding; they are non-decreasing, so the first index
+// with u < cum is the same).
+namespace refgen {
+
+constexpr uint32_t kSynthetic = 7;
+
+double normal_variate(scu::Stream& s) {  // synthetic.cpp:17-22
+  const double u1 = s.uniform_oo();
+  const double u2 = s.uniform_oo();
+  return std::sqrt(-2.0 * std::log(u1)) * std::cos(2.0 * 3.141592653589793 * u2);
+}
+
+double gamma_variate(double shape, scu::Stream& s) {  // synthetic.cpp:38-58
+  if (shape < 1.0) {
+    const double u = s.uniform_oo();  // drawn BEFORE the recursive variate
+    const double g = gamma_variate(shape + 1.0, s);
+    return g * std::pow(u, 1.0 / shape);
+  }
+  const double d = shape - 1.0 / 3.0;
+  const double c = 1.0 / std::sqrt(9.0 * d);
+  for (;;) {
+    const double x = normal_variate(s);
+    const double t = 1.0 + c * x;
+    if (t <= 0.0) continue;
+    const double v = t * t * t;
+    const double u = s.uniform_oo();
+    if (std::log(u) < 0.5 * x * x + d - d * v + d * std::log(v)) return d * v;
+  }
+}
+
+void dirichlet_variate(int64_t k, double conc, scu::Stream& s, double* out) {  // :24-35
+  double total = 0.0;
+  for (int64_t i = 0; i < k; ++i) {
+    out[i] = gamma_variate(conc, s);
+    total += out[i];
+  }
+  for (int64_t i = 0; i < k; ++i) out[i] /= total;
+}
+
+int64_t poisson_sample(double lambda, scu::Stream& s) {  // rng.cpp:39-86,139-150
+  if (lambda == 0.0) return 0;
+  if (lambda < 10.0) {
+    const double u = s.uniform();
+    double pmf = std::exp(-lambda), cdf = pmf;
+    int64_t k = 0;
+    while (u > cdf && k < 1000) {
+      ++k;
+      pmf *= lambda / static_cast<double>(k);
+      cdf += pmf;
+    }
+    return k;
+  }
+  const double log_lambda = std::log(lambda);
+  const double b = 0.931 + 2.53 * std::sqrt(lambda);
+  const double a = -0.059 + 0.02483 * b;
+  const double inv_alpha = 1.1239 + 1.1328 / (b - 3.4);
+  const double v_r = 0.9277 - 3.6224 / (b - 2.0);
+  for (;;) {
+    const double u = s.uniform_oo() - 0.5;
+    const double v = s.uniform_oo();
+    const double us = 0.5 - std::abs(u);
+    const double g = (2.0 * a / us + b) * u + lambda + 0.43;
+    if (us >= 0.07 && v <= v_r) return static_cast<int64_t>(g);
+    if (g < 0.0 || g > 9.0e18 || (us < 0.013 && v > us)) continue;
+    const int64_t k = static_cast<int64_t>(g);
+    const double lhs = std::log(v * inv_alpha / (a / (us * us) + b));
+    const double rhs = -lambda + static_cast<double>(k) * log_lambda -
+                       std::lgamma(static_cast<double>(k) + 1.0);
+    if (lhs <= rhs) return k;
+  }
+}
+
+// categorical_sample (rng.cpp:152-179) given the weights' running sums
+// cum[0..n-1] (cum[n-1] = the total, summed in the same order)
+int categorical(const double* w, const double* cum, int64_t n, scu::Stream& s) {
+  const double u = s.uniform() * cum[n - 1];
+  // first k < n - 1 with u < cum[k]
+  int64_t lo = 0, hi = n - 1;  // answer in [lo, hi]; hi = n - 1 means "none"
+  while (lo < hi) {
+    const int64_t mid = (lo + hi) / 2;
+    if (u < cum[mid]) hi = mid; else lo = mid + 1;
+  }
+  if (lo < n - 1) return static_cast<int>(lo);
+  for (int64_t k = n; k-- > 0;)
+    if (w[k] > 0.0) return static_cast<int>(k);
+  return 0;
+}
+
+}  // namespace refgen
+
 extern "C" {
 
 int samelda_synth_generate(const samelda_synth_params* p, int n_threads, void** handle,
@@ -212,6 +312,96 @@ int samelda_synth_generate(const samelda_synth_params* p, int n_threads, void** 
   *nnz = base;
   *n_tokens = tok;
   *handle = out;
+  return 0;
+}
+
+int samelda_synth_make_corpus_ref(int64_t n_docs, int64_t n_words, int64_t n_topics,
+                                  double len_mean, uint64_t seed, double theta_conc,
+                                  double phi_conc, int n_threads, void** handle, int64_t* nnz,
+                                  int64_t* n_tokens) {
+  if (n_docs < 1 || n_words < 1 || n_topics < 1 || !(len_mean >= 1.0) || !(theta_conc > 0.0) ||
+      !(phi_conc > 0.0) || handle == nullptr)
+    return 1;
+  const int64_t W = n_words, K = n_topics, D = n_docs;
+  std::vector<double> phi(static_cast<size_t>(K * W)), cum(static_cast<size_t>(K * W));
+  {
+    scu::Stream s;
+    s.init(seed, 0, 0, 0, scu::make_tag(refgen::kSynthetic, 1, 0));
+    for (int64_t k = 0; k < K; ++k) refgen::dirichlet_variate(W, phi_conc, s, phi.data() + k * W);
+  }
+  for (int64_t k = 0; k < K; ++k) {
+    double c = 0.0;
+    for (int64_t w = 0; w < W; ++w) cum[k * W + w] = (c += phi[k * W + w]);
+  }
+  const int nt = std::max(1, n_threads);
+  std::vector<Generated> parts(static_cast<size_t>(nt));
+  std::vector<std::thread> th;
+  for (int t = 0; t < nt; ++t) {
+    th.emplace_back([&, t] {
+      const int64_t lo = D * t / nt, hi = D * (t + 1) / nt;
+      Generated& g = parts[static_cast<size_t>(t)];
+      std::vector<int32_t> word_count(static_cast<size_t>(W));
+      std::vector<double> theta(static_cast<size_t>(K)), tcum(static_cast<size_t>(K));
+      int64_t pos = 0;
+      for (int64_t d = lo; d < hi; ++d) {
+        scu::Stream s;
+        s.init(seed, 0, static_cast<uint32_t>(d), 0, scu::make_tag(refgen::kSynthetic, 2, 0));
+        refgen::dirichlet_variate(K, theta_conc, s, theta.data());
+        double c = 0.0;
+        for (int64_t k = 0; k < K; ++k) tcum[k] = (c += theta[k]);
+        const int64_t length = 1 + refgen::poisson_sample(len_mean - 1.0, s);
+        std::fill(word_count.begin(), word_count.end(), 0);
+        for (int64_t i = 0; i < length; ++i) {
+          const int k = refgen::categorical(theta.data(), tcum.data(), K, s);
+          const int w = refgen::categorical(phi.data() + k * W, cum.data() + k * W, W, s);
+          ++word_count[static_cast<size_t>(w)];
+        }
+        for (int64_t w = 0; w < W; ++w)
+          if (word_count[static_cast<size_t>(w)] > 0) {
+            g.words.push_back(static_cast<int32_t>(w));
+            g.counts.push_back(word_count[static_cast<size_t>(w)]);
+            ++pos;
+          }
+        g.offsets.push_back(pos);
+      }
+    });
+  }
+  for (auto& x : th) x.join();
+  auto* out = new Generated();
+  out->offsets.push_back(0);
+  int64_t base = 0, tok = 0;
+  for (auto& g : parts) {
+    for (int64_t o : g.offsets) out->offsets.push_back(base + o);
+    base += static_cast<int64_t>(g.words.size());
+    out->words.insert(out->words.end(), g.words.begin(), g.words.end());
+    out->counts.insert(out->counts.end(), g.counts.begin(), g.counts.end());
+    for (int32_t c : g.counts) tok += c;
+  }
+  *nnz = base;
+  *n_tokens = tok;
+  *handle = out;
+  return 0;
+}
+
+int samelda_synth_split_holdout(int64_t n_docs, double test_fraction, uint64_t seed,
+                                int32_t* test_ids, int64_t* n_test, int32_t* train_ids) {
+  // corpus.cpp:231-250 (ids only; the caller subsets the CSR)
+  if (!(test_fraction > 0.0 && test_fraction < 1.0) || n_docs < 2) return 1;
+  scu::Stream s;
+  s.init(seed, 0, 0, 0, scu::make_tag(scu::kHoldoutSplit, 0, 0));
+  std::vector<int32_t> order(static_cast<size_t>(n_docs));
+  for (int64_t i = 0; i < n_docs; ++i) order[static_cast<size_t>(i)] = static_cast<int32_t>(i);
+  for (int64_t i = n_docs - 1; i > 0; --i) {  // shuffled_indices, rng.cpp:181-192
+    const int64_t j = static_cast<int64_t>(s.uniform_below(static_cast<uint64_t>(i) + 1));
+    std::swap(order[static_cast<size_t>(i)], order[static_cast<size_t>(j)]);
+  }
+  int64_t nt = static_cast<int64_t>(std::llround(test_fraction * static_cast<double>(n_docs)));
+  nt = std::clamp<int64_t>(nt, 1, n_docs - 1);
+  std::sort(order.begin(), order.begin() + nt);
+  std::sort(order.begin() + nt, order.end());
+  std::memcpy(test_ids, order.data(), sizeof(int32_t) * static_cast<size_t>(nt));
+  std::memcpy(train_ids, order.data() + nt, sizeof(int32_t) * static_cast<size_t>(n_docs - nt));
+  *n_test = nt;
   return 0;
 }
 

@@ -594,14 +594,17 @@ class Trainer:
         c.check(c.lib.samelda_cu_profile(c.h, 1 if enable else 0))
 
     def profile_read(self) -> dict:
-        ms = np.zeros(3)
-        n = np.zeros(3, np.int64)
+        ms = np.zeros(4)
+        n = np.zeros(4, np.int64)
         nnz, docs, dfr = C.c_int64(), C.c_int64(), C.c_int64()
         c = self._live()
         c.check(c.lib.samelda_cu_profile_read(c.h, _ptr(ms), _ptr(n), C.byref(nnz),
                                               C.byref(docs), C.byref(dfr)))
-        return dict(sample_ms=ms[0], sddmm_ms=ms[1], mstep_ms=ms[2], sample_launches=int(n[0]),
-                    sddmm_launches=int(n[1]), mstep_launches=int(n[2]), nnz=nnz.value,
+        # nnz / docs count every timed sampling launch (both kinds)
+        return dict(sample_ms=ms[0] + ms[3], sddmm_ms=ms[1], mstep_ms=ms[2],
+                    sample_launches=int(n[0] + n[3]), sddmm_launches=int(n[1]),
+                    mstep_launches=int(n[2]), sample_first_ms=ms[0], sample_first_launches=int(n[0]),
+                    sample_last_ms=ms[3], sample_last_launches=int(n[3]), nnz=nnz.value,
                     docs=docs.value, deferred=dfr.value)
 
     def count_totals(self):

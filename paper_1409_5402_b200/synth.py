@@ -72,3 +72,61 @@ def preset(name: str, seed: int = 1, scale: float = 1.0, n_threads=None, shard: 
     kw = dict(PRESETS[name])
     kw["n_docs"] = max(2, int(kw["n_docs"] * scale))
     return generate(seed=seed, n_threads=n_threads, first_doc=shard * kw["n_docs"], **kw)
+
+
+def make_corpus_ref(n_docs: int, n_words: int, n_topics: int, len_mean: float, seed: int,
+                    theta_conc: float = 0.2, phi_conc: float = 0.08, n_threads=None) -> Corpus:
+    """The reference's synthetic::make_corpus (tests/support/synthetic.cpp:61-106), value for
+    value; BASELINE.json configs[0] is make_corpus_ref(10000, 5000, 32, 100.0, 1)."""
+    lib = load_library()
+    fn = lib.samelda_synth_make_corpus_ref
+    fn.restype = C.c_int
+    fn.argtypes = [C.c_int64, C.c_int64, C.c_int64, C.c_double, C.c_uint64, C.c_double,
+                   C.c_double, C.c_int, C.POINTER(C.c_void_p), C.POINTER(C.c_int64),
+                   C.POINTER(C.c_int64)]
+    lib.samelda_synth_copy.argtypes = [C.c_void_p] * 4
+    lib.samelda_synth_free.argtypes = [C.c_void_p]
+    h, nnz, tok = C.c_void_p(), C.c_int64(), C.c_int64()
+    rc = fn(n_docs, n_words, n_topics, len_mean, seed, theta_conc, phi_conc,
+            int(n_threads or os.cpu_count() or 1), C.byref(h), C.byref(nnz), C.byref(tok))
+    if rc:
+        raise ValueError("samelda_synth_make_corpus_ref: bad parameters")
+    offs = np.empty(n_docs + 1, np.int64)
+    words = np.empty(max(nnz.value, 1), np.int32)
+    counts = np.empty(max(nnz.value, 1), np.int32)
+    lib.samelda_synth_copy(h, offs.ctypes.data, words.ctypes.data, counts.ctypes.data)
+    lib.samelda_synth_free(h)
+    return Corpus(offs, words[:nnz.value], counts[:nnz.value], n_words)
+
+
+def subset(corpus: Corpus, doc_ids) -> Corpus:
+    """subset_corpus (corpus.cpp): the rows doc_ids, in that order."""
+    ids = np.asarray(doc_ids, np.int64)
+    o = corpus.doc_offsets
+    lens = o[ids + 1] - o[ids]
+    offs = np.zeros(len(ids) + 1, np.int64)
+    np.cumsum(lens, out=offs[1:])
+    if len(ids) and offs[-1]:
+        starts = np.repeat(o[ids] - offs[:-1], lens)
+        idx = starts + np.arange(offs[-1])
+    else:
+        idx = np.zeros(0, np.int64)
+    return Corpus(offs, np.ascontiguousarray(corpus.word_ids[idx]),
+                  np.ascontiguousarray(corpus.counts[idx]), corpus.n_words)
+
+
+def split_holdout(corpus: Corpus, test_fraction: float, seed: int) -> tuple[Corpus, Corpus]:
+    """split_holdout (corpus.cpp:231-250): (train, test), ids sorted within each."""
+    lib = load_library()
+    fn = lib.samelda_synth_split_holdout
+    fn.restype = C.c_int
+    fn.argtypes = [C.c_int64, C.c_double, C.c_uint64, C.c_void_p, C.POINTER(C.c_int64),
+                   C.c_void_p]
+    D = corpus.n_docs
+    test = np.empty(D, np.int32)
+    train = np.empty(D, np.int32)
+    nt = C.c_int64()
+    if fn(D, test_fraction, seed, test.ctypes.data, C.byref(nt), train.ctypes.data):
+        raise ValueError("split_holdout: test_fraction must be in (0,1) and n_docs >= 2")
+    n = nt.value
+    return subset(corpus, train[:D - n]), subset(corpus, test[:n])

@@ -71,4 +71,6 @@ def test_scan_nytimes_shape(lib):
     W, K = 102660, 256
     c = rng.poisson(rng.gamma(0.2, 2.0, size=(W, K)).astype(np.float64))
     x = c / 100.0 + 0.01
-    np.testing.assert_array_equal(gpu_sums(lib, x, 0), gpu_sums(lib, x, 1))
+    ref = seq_sums(x)  # the reference's sequential loop, in numpy (IEEE f64 adds, no FMA)
+    np.testing.assert_array_equal(gpu_sums(lib, x, 0), ref)
+    np.testing.assert_array_equal(gpu_sums(lib, x, 1), ref)

@@ -2,7 +2,9 @@
 device cannot host two NCCL ranks): real kernels, real doc sharding, real
 all-reduce of the device phi-count buffer through distributed.ShardedTrainer.
 The sharded phi must equal single-process training bit for bit -- the
-property the NCCL run on 8 B200s relies on."""
+property the NCCL run on 8 B200s relies on.  On a box with >= 2 GPUs the same
+test runs one rank per GPU over NCCL (the production path, device buffers
+reduced in place)."""
 from __future__ import annotations
 
 import os
@@ -25,10 +27,15 @@ def _corpus():
     return port.make_corpus(120, 60, 4, 30.0, 3)
 
 
-def _worker(rank, world, port_no, out_path, mode=0):
+def _worker(rank, world, port_no, out_path, mode=0, backend="gloo"):
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port_no))
-    dist.init_process_group("gloo", rank=rank, world_size=world)
-    torch.cuda.set_device(0)
+    dev = rank if backend == "nccl" else 0
+    torch.cuda.set_device(dev)
+    if backend == "nccl":
+        dist.init_process_group("nccl", rank=rank, world_size=world,
+                                device_id=torch.device("cuda", dev))
+    else:
+        dist.init_process_group("gloo", rank=rank, world_size=world)
     from paper_1409_5402_b200 import distributed as D
     from paper_1409_5402_b200 import samelda as S
     g = _corpus()
@@ -36,14 +43,13 @@ def _worker(rank, world, port_no, out_path, mode=0):
     offs = g.doc_offsets[lo:hi + 1] - g.doc_offsets[lo]
     local = S.Corpus(offs, g.word_ids[g.doc_offsets[lo]:g.doc_offsets[hi]],
                      g.counts[g.doc_offsets[lo]:g.doc_offsets[hi]], g.n_words)
-    ctx = S.Context(0)
-    stream = torch.cuda.Stream(device=0)
+    ctx = S.Context(dev)
+    stream = torch.cuda.Stream(device=dev)
     torch.cuda.set_stream(stream)
     ctx.set_stream(stream.cuda_stream)
     cfg = S.SamplerConfig(n_topics=K, m=M, schedule="invlinear", t_max=T_MAX, batch_fraction=BF,
                           seed=SEED, mode=mode)
     tr = S.Trainer(local, cfg, ctx=ctx)
-    tr.set_doc_base(lo)
 
     class GlooEngine(D.CudaEngine):
         """gloo reduces host tensors: stage the device counts through the host."""
@@ -56,7 +62,9 @@ def _worker(rank, world, port_no, out_path, mode=0):
             super().counts().copy_(self._host)
             super().update(rho)
 
-    st = D.ShardedTrainer(GlooEngine(tr, 0), g.n_docs, lo, hi, local.doc_tokens(), BF, SEED, M,
+    engine = GlooEngine(tr, 0) if backend == "gloo" else D.CudaEngine(tr, dev)
+    # ShardedTrainer sets the engine's doc base (global Philox doc ids)
+    st = D.ShardedTrainer(engine, g.n_docs, lo, hi, local.doc_tokens(), BF, SEED, M,
                           "invlinear", T_MAX)
     for _ in range(T_MAX):
         st.period()
@@ -107,11 +115,49 @@ def test_bench_two_rank_path_runs(tmp_path):
     out = subprocess.run(
         [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2",
          "--master-addr", "127.0.0.1", "--master-port", str(port_no), "bench.py", "--gpus", "2",
-         "--steps", "2", "--warmup", "3", "--no-cpu-baseline"],
+         "--steps", "2", "--warmup", "3", "--no-cpu-baseline", "--scaling", "weak"],
         cwd=root, env=env, capture_output=True, text=True, timeout=600)
     assert out.returncode == 0, out.stderr[-2000:]
     lines = [ln for ln in out.stdout.splitlines() if ln.startswith("{")]
     assert len(lines) == 1
     line = json.loads(lines[0])
     assert line["n_gpus"] == 2 and line["value"] > 0 and line["e2e"]["value"] > 0
+    assert line["config"]["parallelism"] == "doc-shard x2" and line["scaling"] == "weak"
+
+
+@pytest.mark.timeout(600)
+@pytest.mark.skipif(torch.cuda.device_count() < 2, reason="needs >= 2 GPUs (NCCL ranks)")
+@pytest.mark.parametrize("mode", [0, 2], ids=["parity", "throughput"])
+def test_nccl_ranks_equal_single_gpu(tmp_path, mode):
+    """One rank per GPU over NCCL (the bench's multi-GPU path): phi bit-equal to one GPU."""
+    from paper_1409_5402_b200 import samelda as S
+    out = str(tmp_path / "rank0.npz")
+    mp.start_processes(_worker, args=(2, _free_port(), out, mode, "nccl"), nprocs=2,
+                       start_method="spawn")
+    got = np.load(out)
+    model, _ = S.train(_corpus(), S.SamplerConfig(n_topics=K, m=M, schedule="invlinear",
+                                                  t_max=T_MAX, batch_fraction=BF, seed=SEED,
+                                                  mode=mode))
+    np.testing.assert_array_equal(got["phi"], model.phi)
+
+
+def test_bench_launches_its_own_ranks():
+    """`python bench.py --gpus 2` outside torchrun re-launches itself with one process per
+    rank (here both on cuda:0 over gloo: BENCH_SHARE_GPU) on the stated corpus, strong
+    scaling: the line reports n_gpus 2 and doc-shard x2."""
+    import json
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = {k: v for k, v in os.environ.items() if k not in ("WORLD_SIZE", "RANK", "LOCAL_RANK")}
+    env.update(BENCH_SHARE_GPU="1", BENCH_NO_CLOCKS="1")
+    out = subprocess.run([sys.executable, "bench.py", "--gpus", "2", "--steps", "2", "--warmup",
+                          "3", "--no-cpu-baseline"], cwd=root, env=env, capture_output=True,
+                         text=True, timeout=900)
+    assert out.returncode == 0, out.stderr[-3000:]
+    lines = [ln for ln in out.stdout.splitlines() if ln.startswith("{")]
+    assert len(lines) == 1
+    line = json.loads(lines[0])
+    assert line["n_gpus"] == 2 and line["scaling"] == "strong"
     assert line["config"]["parallelism"] == "doc-shard x2"
+    assert line["corpus"]["train_docs"] == 270000 and line["value"] > 0

@@ -637,8 +637,7 @@ def test_nytimes_scale_sweep_matches_compiled_reference():
     the sweep's mass balance."""
     import bench
     from oracle import Ref
-    corpus = bench.make_corpus("nytimes", 0)
-    train, _ = bench.split_heldout(corpus)
+    train, _ = bench.single_gpu_corpus("nytimes")
     cfg = S.SamplerConfig(n_topics=256, m=100.0, batch_fraction=0.05, t_max=4, seed=1)
     tr = S.Trainer(train, cfg)
     stream = S.MinibatchStream(train.n_docs, 0.05, 1)

@@ -18,8 +18,7 @@ ap.add_argument("--config", default="nytimes")
 ap.add_argument("--periods", type=int, default=6)
 args = ap.parse_args()
 cfg = bench.CONFIGS[args.config]
-corpus = bench.make_corpus(cfg["corpus"], 0)
-train, heldout = bench.split_heldout(corpus)
+train, heldout = bench.single_gpu_corpus(args.config)
 scfg = S.SamplerConfig(n_topics=cfg["n_topics"], m=cfg["m"], batch_fraction=cfg["batch_fraction"],
                        inner_sweeps=cfg["inner_sweeps"], t_max=args.periods, seed=1)
 tr = S.Trainer(train, scfg)

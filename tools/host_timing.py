@@ -8,8 +8,7 @@ import bench
 from paper_1409_5402_b200 import samelda as S, distributed as D
 
 cfg = bench.CONFIGS["nytimes"]
-corpus = bench.make_corpus("nytimes", 0)
-train, _ = bench.split_heldout(corpus)
+train, _ = bench.single_gpu_corpus("nytimes")
 ctx = S.Context(0)
 stream = torch.cuda.Stream(device=0)
 torch.cuda.set_stream(stream)

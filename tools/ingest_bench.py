@@ -27,7 +27,8 @@ ap.add_argument("--dir", default="/tmp/samelda_ingest")
 args = ap.parse_args()
 os.makedirs(args.dir, exist_ok=True)
 cfg = bench.CONFIGS[args.config]
-full = bench.make_corpus(cfg["corpus"], 0)
+from paper_1409_5402_b200 import synth  # noqa: E402
+full = synth.preset(cfg["corpus"], seed=1)
 full.vocab = [f"w{i}" for i in range(full.n_words)]
 dw, vb = os.path.join(args.dir, "docword.txt"), os.path.join(args.dir, "vocab.txt")
 t0 = time.perf_counter()
