@@ -84,6 +84,8 @@ typedef struct {
 
 /* ------------------------------------------------------------ context */
 int samelda_cu_version(void);
+/* number of visible CUDA devices (0 without a usable driver) */
+int samelda_cu_device_count(void);
 int samelda_cu_create(int device, samelda_cu_ctx** out);
 void samelda_cu_destroy(samelda_cu_ctx* ctx);
 const char* samelda_cu_last_error(const samelda_cu_ctx* ctx);
@@ -236,6 +238,40 @@ int samelda_cu_train(samelda_cu_ctx* ctx, const samelda_cu_corpus* corpus,
                      const samelda_cu_config* config, const samelda_cu_corpus* heldout,
                      int64_t eval_every, double* phi_out, double* theta_out,
                      samelda_cu_trace_row* trace, int64_t trace_cap, int64_t* n_trace);
+
+/* ------------------------------------- multi-GPU group (one process, N GPUs)
+ *
+ * SURVEY.md 8(e) behind the ABI: documents are split into contiguous ranges
+ * balanced by nonzeros, one context per device; every period each device
+ * samples the batch documents it owns (Philox keys use global document ids),
+ * the W x K topic-word counts are summed in place over the devices with
+ * ncclAllReduce (communicator from ncclCommInitAll over `devices`; NCCL is
+ * loaded at run time), and the M-step runs replicated.  In the integer-count
+ * modes the model is bit-identical to one GPU's for any device count.
+ * A list that repeats one device (tests on a one-GPU box) exchanges with a
+ * device-side sum instead of NCCL. */
+typedef struct samelda_cu_group samelda_cu_group;
+int samelda_cu_group_create(const int* devices, int n, samelda_cu_group** out);
+void samelda_cu_group_destroy(samelda_cu_group* g);
+const char* samelda_cu_group_last_error(const samelda_cu_group* g);
+int samelda_cu_group_size(const samelda_cu_group* g);
+/* 1 when the exchange runs over an NCCL communicator */
+int samelda_cu_group_uses_nccl(const samelda_cu_group* g);
+/* the sharded counterparts of samelda_cu_train_begin / _heldout / _period /
+ * _synchronize / _evaluate / _model_download (doc ids are GLOBAL ids) */
+int samelda_cu_group_train_begin(samelda_cu_group* g, const samelda_cu_corpus* corpus,
+                                 const samelda_cu_config* config);
+int samelda_cu_group_heldout(samelda_cu_group* g, const samelda_cu_corpus* test, uint64_t seed);
+int samelda_cu_group_period(samelda_cu_group* g, const int32_t* doc_ids, int64_t B, int64_t t,
+                            double m_t, double rho_t);
+int samelda_cu_group_synchronize(samelda_cu_group* g);
+int samelda_cu_group_evaluate(samelda_cu_group* g, double* ll_out);
+int samelda_cu_group_model_download(samelda_cu_group* g, double* phi, double* theta);
+/* replaces samelda::train (sampler.hpp:105-110 / sampler.cpp:269-353) on N GPUs */
+int samelda_cu_group_train(samelda_cu_group* g, const samelda_cu_corpus* corpus,
+                           const samelda_cu_config* config, const samelda_cu_corpus* heldout,
+                           int64_t eval_every, double* phi_out, double* theta_out,
+                           samelda_cu_trace_row* trace, int64_t trace_cap, int64_t* n_trace);
 
 #ifdef __cplusplus
 }

@@ -527,6 +527,12 @@ struct samelda_cu_ctx {
     return std::min<int64_t>(records * 32, int64_t{1} << 26);
   }
 
+  // the materialised M-step candidate: only the sequential-chain column sums
+  // (SAMELDA_COLSUM=chain) read one; the scan recomputes it from the counts
+  double* cand_scratch(int64_t n) {
+    return scu::tuning().colsum_chain ? ensure<double>(cand, n) : nullptr;
+  }
+
   // scratch of the exact parallel column-sum scan (grown at train_begin /
   // the first per-call M-step, never inside a period)
   void* colsum_scratch(int64_t W_, int64_t K_) {
@@ -543,7 +549,7 @@ struct samelda_cu_ctx {
     ensure<double>(theta_batch, B_ * K_);
     ensure<float>(theta_batch32, B_ * K_);
     ensure<double>(theta_rows, B_ * K_);
-    ensure<double>(cand, W_ * K_);
+    cand_scratch(W_ * K_);
     ensure<double>(totals, K_);
     if (mode == SAMELDA_CU_MODE_EXPECTED) {
       ensure<double>(mu, nnz_);
@@ -696,6 +702,15 @@ int64_t batch_nnz_host(const CorpusSlot& s, const int32_t* doc_ids, int64_t B) {
 extern "C" {
 
 int samelda_cu_version(void) { return kVersion; }
+
+int samelda_cu_device_count(void) {
+  int n = 0;
+  if (cudaGetDeviceCount(&n) != cudaSuccess) {
+    cudaGetLastError();
+    return 0;
+  }
+  return n;
+}
 
 int samelda_cu_create(int device, samelda_cu_ctx** out) {
   if (out == nullptr) return SAMELDA_CU_CONFIG;
@@ -900,13 +915,13 @@ static void update_call(samelda_cu_ctx* ctx, double* theta, int64_t D, double* p
     double* pf = ensure<double>(ctx->pf, W * K);
     ck(cudaMemcpyAsync(pf, pcounts, sizeof(double) * W * K, cudaMemcpyHostToDevice, st), "upload pf");
     ctx->launches += scu::launch_phi_mstep(nullptr, pf, W, Ki, m_t, beta, rho_t, phi_wk, nullptr,
-                                           ensure<double>(ctx->cand, W * K), totals,
+                                           ctx->cand_scratch(W * K), totals,
                                            ctx->colsum_scratch(W, Ki), ctx->d_err(), st);
   } else {
     auto* pc = ensure<unsigned long long>(ctx->pc, W * K);
     ck(cudaMemcpyAsync(pc, pcounts, sizeof(int64_t) * W * K, cudaMemcpyHostToDevice, st), "upload pc");
     ctx->launches += scu::launch_phi_mstep(pc, nullptr, W, Ki, m_t, beta, rho_t, phi_wk, nullptr,
-                                           ensure<double>(ctx->cand, W * K), totals,
+                                           ctx->cand_scratch(W * K), totals,
                                            ctx->colsum_scratch(W, Ki), ctx->d_err(), st);
   }
   double* back = ensure<double>(ctx->phi_call, K * W);
@@ -1156,7 +1171,7 @@ int samelda_cu_period_update(samelda_cu_ctx* ctx, double rho_t) {
     ctx->launches += scu::launch_theta_persist(tcu, tcf, ctx->batch.as<int32_t>(), ctx->B, K, ctx->m_t, c.alpha,
                                                ctx->theta.as<double>(), st);
     ctx->launches += scu::launch_phi_mstep(pcu, pcf, ctx->W, K, ctx->m_t, c.beta, rho_t, ctx->phi.as<double>(),
-                                           ctx->phi32.as<float>(), ensure<double>(ctx->cand, ctx->W * K),
+                                           ctx->phi32.as<float>(), ctx->cand_scratch(ctx->W * K),
                                            ensure<double>(ctx->totals, K), ctx->colsum_scratch(ctx->W, K),
                                            ctx->d_err(), st);
     ctx->tick(samelda_cu_ctx::kMstep, false);

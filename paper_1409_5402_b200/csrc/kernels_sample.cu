@@ -215,6 +215,17 @@ __global__ void __launch_bounds__(kSampleBlock) k_sample(
 // else the warp computes it (f32 tree).
 
 constexpr int kFastBlock = 256;
+
+// Nonzeros per warp work item: 128 (the packed u16 theta-count pairs hold
+// <= 128 nonzeros x z <= 40), fewer on small batches so the grid keeps ~4
+// waves of resident warps (148 SMs x 32 warps) -- a C1 sweep (0.87M nonzeros,
+// K = 32, one topic slice) has only 1.4 waves at 128
+inline int64_t work_chunk(int64_t nnz, int n_slices) {
+  const int64_t target_warps = int64_t{148} * 32 * 4;
+  int64_t c = nnz * n_slices / target_warps;
+  c = std::max<int64_t>(32, std::min<int64_t>(128, (c + 31) / 32 * 32));
+  return c;
+}
 // inversion below 10 (rng.cpp:139-150): decided only when lambda_f's whole
 // error interval (1.5e-6 relative, 2x) lies below 10; PTRS draws defer
 constexpr float kInvMax = 9.99997f;
@@ -1109,7 +1120,7 @@ int launch_fast_kpl(const BatchView& bv, const double* tb64, const float* tb32, 
                     void* deferred, unsigned long long* n_deferred, void* aux, int64_t draw_cap,
                     float* mu_f, int* err, cudaStream_t st) {
   const int n_slices = (K + kWarp * KPL - 1) / (kWarp * KPL);
-  const int64_t chunk = 128;
+  const int64_t chunk = work_chunk(bv.nnz, n_slices);
   const int64_t items = (bv.nnz + chunk - 1) / chunk;
   const int warps = kFastBlock / kWarp;
   int launched = 0;
@@ -1275,7 +1286,7 @@ int launch_sample_kpl(const BatchView& bv, const double* theta_batch, const doub
                       uint32_t sweep, int mode, unsigned long long* tc, unsigned long long* pc,
                       double* tf, double* pf, int* err, cudaStream_t st) {
   const int n_slices = (K + kWarp * KPL - 1) / (kWarp * KPL);
-  const int64_t chunk = 128;
+  const int64_t chunk = work_chunk(bv.nnz, n_slices);
   const int64_t items = (bv.nnz + chunk - 1) / chunk;
   const int64_t threads = items * n_slices * kWarp;
   const int block = kSampleBlock;
@@ -1359,7 +1370,7 @@ static void launch_thru(const BatchView& bv, const float* theta_b32, const float
                         cudaStream_t st) {
   constexpr int KPL = 8;
   const int n_slices = (K + kWarp * KPL - 1) / (kWarp * KPL);
-  const int64_t chunk = 128;
+  const int64_t chunk = work_chunk(bv.nnz, n_slices);
   const int64_t items = (bv.nnz + chunk - 1) / chunk;
   const int warps = BLK / kWarp;
   const dim3 grid(static_cast<unsigned>((items + warps - 1) / warps), static_cast<unsigned>(n_slices));

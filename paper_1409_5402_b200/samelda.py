@@ -79,6 +79,7 @@ _P, _I64, _I32, _D, _U64 = C.c_void_p, C.c_int64, C.c_int32, C.c_double, C.c_uin
 _CP = C.POINTER(_Corpus)
 SIGNATURES = [
     ("samelda_cu_version", C.c_int, []),
+    ("samelda_cu_device_count", C.c_int, []),
     ("samelda_cu_create", C.c_int, [C.c_int, C.POINTER(C.c_void_p)]),
     ("samelda_cu_destroy", None, [_P]),
     ("samelda_cu_last_error", C.c_char_p, [_P]),
@@ -126,6 +127,20 @@ SIGNATURES = [
     ("samelda_cu_model_upload", C.c_int, [_P, _P, _P]),
     ("samelda_cu_train", C.c_int, [_P, _CP, C.POINTER(_Config), _CP, _I64, _P, _P,
                                    C.POINTER(_TraceRow), _I64, C.POINTER(_I64)]),
+    # multi-GPU group (one process, N devices)
+    ("samelda_cu_group_create", C.c_int, [_P, C.c_int, C.POINTER(C.c_void_p)]),
+    ("samelda_cu_group_destroy", None, [_P]),
+    ("samelda_cu_group_last_error", C.c_char_p, [_P]),
+    ("samelda_cu_group_size", C.c_int, [_P]),
+    ("samelda_cu_group_uses_nccl", C.c_int, [_P]),
+    ("samelda_cu_group_train_begin", C.c_int, [_P, _CP, C.POINTER(_Config)]),
+    ("samelda_cu_group_heldout", C.c_int, [_P, _CP, _U64]),
+    ("samelda_cu_group_period", C.c_int, [_P, _P, _I64, _I64, _D, _D]),
+    ("samelda_cu_group_synchronize", C.c_int, [_P]),
+    ("samelda_cu_group_evaluate", C.c_int, [_P, C.POINTER(_D)]),
+    ("samelda_cu_group_model_download", C.c_int, [_P, _P, _P]),
+    ("samelda_cu_group_train", C.c_int, [_P, _CP, C.POINTER(_Config), _CP, _I64, _P, _P,
+                                         C.POINTER(_TraceRow), _I64, C.POINTER(_I64)]),
     # data formats (include/samelda_io.h)
     ("samelda_io_last_error", C.c_char_p, []),
     ("samelda_io_load_uci", C.c_int, [C.c_char_p, C.c_char_p, C.c_int, C.POINTER(C.c_void_p)]),
@@ -668,6 +683,65 @@ def train(corpus, config: SamplerConfig, heldout=None, eval_every: int = 0,
              for i in range(n.value)]
     return Model(K, W, config.alpha, config.beta, phi[:K * W].reshape(K, W),
                  theta[:D * K].reshape(D, K)), trace
+
+
+class Group:
+    """One process driving several GPUs (samelda_cu_group_*): documents sharded in
+    contiguous nnz-balanced ranges, the W x K counts summed over the devices with
+    NCCL once per period, the M-step replicated.  A list repeating one device is the
+    one-GPU test mode (device-side sum instead of NCCL)."""
+
+    def __init__(self, devices):
+        self.lib = load_library()
+        devs = (C.c_int * len(devices))(*[int(d) for d in devices])
+        h = C.c_void_p()
+        rc = self.lib.samelda_cu_group_create(devs, len(devices), C.byref(h))
+        if rc:
+            raise _CODES.get(rc, SameldaError)(f"samelda_cu_group_create({list(devices)}) failed "
+                                               f"with code {rc}")
+        self.h = h
+        self.devices = list(devices)
+
+    def close(self):
+        if getattr(self, "h", None):
+            self.lib.samelda_cu_group_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def check(self, rc: int):
+        if rc:
+            msg = self.lib.samelda_cu_group_last_error(self.h).decode(errors="replace")
+            raise _CODES.get(rc, SameldaError)(msg)
+
+    @property
+    def uses_nccl(self) -> bool:
+        return bool(self.lib.samelda_cu_group_uses_nccl(self.h))
+
+    def train(self, corpus, config: SamplerConfig, heldout=None, eval_every: int = 0):
+        """sampler.cpp:269-353 over the group -> (Model, trace rows)."""
+        corpus = Corpus.of(corpus)
+        cs, cfg = corpus._struct(), config._struct()
+        hs = Corpus.of(heldout)._struct() if heldout is not None else None
+        K, W, D = config.n_topics, corpus.n_words, corpus.n_docs
+        phi = np.zeros(max(K * W, 1))
+        theta = np.zeros(max(D * K, 1))
+        cap = max(int(config.t_max), 1)
+        rows = (_TraceRow * cap)()
+        n = C.c_int64()
+        self.check(self.lib.samelda_cu_group_train(self.h, C.byref(cs), C.byref(cfg),
+                                                   C.byref(hs) if hs is not None else None,
+                                                   int(eval_every), _ptr(phi), _ptr(theta), rows,
+                                                   cap, C.byref(n)))
+        trace = [dict(t=rows[i].t, passes=rows[i].passes,
+                      samples_per_word=rows[i].samples_per_word, ll=rows[i].ll,
+                      wall_seconds=rows[i].wall_seconds, m_t=rows[i].m_t) for i in range(n.value)]
+        return Model(K, W, config.alpha, config.beta, phi[:K * W].reshape(K, W),
+                     theta[:D * K].reshape(D, K)), trace
 
 
 # ------------------------------------------------------------ data formats

@@ -8,6 +8,7 @@
 // model, rng, cgs, commands) and its CLI link unchanged.  See INTEGRATION.md.
 #include <cmath>
 #include <cstdint>
+#include <cstdlib>
 #include <mutex>
 #include <numeric>
 #include <stdexcept>
@@ -31,6 +32,43 @@ samelda_cu_ctx* context() {
   });
   if (ctx == nullptr) throw std::runtime_error("samelda_cu: no usable CUDA device");
   return ctx;
+}
+
+// The devices train() shards over: SAMELDA_CU_DEVICES as a
+// comma-separated list of device ids ("0,1,2,3"; repeating one device, e.g.
+// "0,0", is the one-GPU test mode of the group), else every visible device.
+// One device -> the single context above; more -> a samelda_cu_group.  The
+// result does not depend on the choice (global Philox doc ids, integer
+// counts), as the reference's n_threads never changes results.
+samelda_cu_group* group() {
+  static std::once_flag once;
+  static samelda_cu_group* grp = nullptr;
+  static bool single = false;
+  std::call_once(once, [] {
+    std::vector<int> devs;
+    if (const char* e = std::getenv("SAMELDA_CU_DEVICES")) {
+      std::string s(e);
+      size_t pos = 0;
+      while (pos < s.size()) {
+        const size_t comma = s.find(',', pos);
+        const std::string tok = s.substr(pos, comma == std::string::npos ? std::string::npos : comma - pos);
+        if (!tok.empty()) devs.push_back(std::atoi(tok.c_str()));
+        if (comma == std::string::npos) break;
+        pos = comma + 1;
+      }
+    } else {
+      const int n = samelda_cu_device_count();
+      for (int d = 0; d < n; ++d) devs.push_back(d);
+    }
+    if (devs.size() <= 1) {
+      single = true;
+      return;
+    }
+    if (samelda_cu_group_create(devs.data(), static_cast<int>(devs.size()), &grp) != SAMELDA_CU_OK)
+      grp = nullptr;
+  });
+  if (grp == nullptr && !single) throw std::runtime_error("samelda_cu: cannot form the device group (SAMELDA_CU_DEVICES / NCCL)");
+  return grp;
 }
 
 std::mutex& lock() {
@@ -219,10 +257,22 @@ std::pair<Model, MetricsTrace> train(const Corpus& corpus, const SamplerConfig& 
   const samelda_cu_corpus cv = cuda_shim::view(corpus);
   samelda_cu_corpus hv{};
   if (heldout != nullptr) hv = cuda_shim::view(*heldout);
-  check(samelda_cu_train(context(), &cv, &c, heldout != nullptr ? &hv : nullptr, eval_every,
-                         model.phi.data.data(), model.theta.data.data(), rows.data(),
-                         static_cast<std::int64_t>(rows.size()), &n_rows),
-        "train");
+  if (samelda_cu_group* grp = cuda_shim::group()) {
+    const int rc = samelda_cu_group_train(grp, &cv, &c, heldout != nullptr ? &hv : nullptr, eval_every,
+                                          model.phi.data.data(), model.theta.data.data(), rows.data(),
+                                          static_cast<std::int64_t>(rows.size()), &n_rows);
+    if (rc != SAMELDA_CU_OK) {
+      const std::string msg = std::string("train: ") + samelda_cu_group_last_error(grp);
+      if (rc == SAMELDA_CU_CONFIG) throw ConfigError(msg);
+      if (rc == SAMELDA_CU_NUMERICAL) throw NumericalError(msg);
+      throw std::runtime_error(msg);
+    }
+  } else {
+    check(samelda_cu_train(context(), &cv, &c, heldout != nullptr ? &hv : nullptr, eval_every,
+                           model.phi.data.data(), model.theta.data.data(), rows.data(),
+                           static_cast<std::int64_t>(rows.size()), &n_rows),
+          "train");
+  }
   MetricsTrace trace;
   for (std::int64_t i = 0; i < n_rows; ++i) {
     const auto& r = rows[static_cast<std::size_t>(i)];

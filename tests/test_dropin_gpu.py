@@ -5,7 +5,10 @@ sampler.cpp / eval.cpp replaced by the drop-in shim over libsamelda_cuda.so
 unchanged from the reference sources).  The drop-in must pass every criterion
 the reference passes.  Criterion 5 is the reference's known-red trend test
 (proj/README.md:53-60) and 10 needs the real NYTimes files, so both are
-excluded."""
+excluded.  Each criterion runs twice: on one device, and with the reference's
+train() sharded by the drop-in over a device group (SAMELDA_CU_DEVICES=0,0,0:
+three members on this box's one GPU, the group's one-GPU test mode; on a
+multi-GPU box every visible device forms an NCCL group by default)."""
 from __future__ import annotations
 
 import os
@@ -21,8 +24,11 @@ pytestmark = pytest.mark.gpu
 
 
 @pytest.mark.skipif(not os.path.exists(CUDA_BIN), reason="built only where /root/reference exists")
+@pytest.mark.parametrize("devices", ["0", "0,0,0"], ids=["one-gpu", "group3"])
 @pytest.mark.parametrize("criterion", [1, 2, 3, 4, 6, 7, 8, 9])
-def test_reference_acceptance_criterion_on_drop_in(criterion):
-    r = subprocess.run([CUDA_BIN, str(criterion)], capture_output=True, text=True, timeout=900)
+def test_reference_acceptance_criterion_on_drop_in(criterion, devices):
+    env = dict(os.environ, SAMELDA_CU_DEVICES=devices)
+    r = subprocess.run([CUDA_BIN, str(criterion)], capture_output=True, text=True, timeout=900,
+                       env=env)
     line = r.stdout.strip().splitlines()[-1] if r.stdout.strip() else r.stderr
     assert re.search(r"\[PASS\]", line), line
