@@ -1,7 +1,9 @@
-# round-2 GPU check: full -m gpu suite, default + c1 bench, launch list of the default bench
+# round-2 GPU check: -m gpu suite, default + c1 bench, launch list of the default bench
 set -x
-python -m pytest tests -m gpu -x -q 2>&1 | tail -25 > gpurun_out/pytest_r2b.log
-python bench.py --steps 20 --warmup 5 > gpurun_out/bench_r2b.json 2> gpurun_out/bench_r2b.err
-python bench.py --config c1 --steps 20 --warmup 5 > gpurun_out/bench_c1_r2b.json 2> gpurun_out/bench_c1_r2b.err
-ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-file gpurun_out/launches_r2b.csv python bench.py --steps 3 --warmup 2 --no-cpu-baseline > gpurun_out/ncu_bench_r2b.log 2>&1
-tail -3 gpurun_out/pytest_r2b.log
+TAG=${TAG:-r2c}
+python -m pytest tests -m gpu -x -q 2>&1 | tail -25 > gpurun_out/pytest_$TAG.log
+python bench.py --steps 20 --warmup 5 > gpurun_out/bench_$TAG.json 2> gpurun_out/bench_$TAG.err
+python bench.py --config c1 --steps 20 --warmup 5 > gpurun_out/bench_c1_$TAG.json 2> gpurun_out/bench_c1_$TAG.err
+ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-file gpurun_out/launches_$TAG.csv python bench.py --steps 3 --warmup 2 --no-cpu-baseline > gpurun_out/ncu_bench_$TAG.log 2>&1
+ncu --set full --clock-control none --import-source on -k regex:k_eval_stage -c 1 -o gpurun_out/eval_$TAG python tools/eval_timing.py > gpurun_out/ncu_eval_$TAG.log 2>&1
+tail -3 gpurun_out/pytest_$TAG.log
