@@ -527,10 +527,13 @@ struct samelda_cu_ctx {
     return std::min<int64_t>(records * 32, int64_t{1} << 26);
   }
 
-  // the materialised M-step candidate: only the sequential-chain column sums
-  // (SAMELDA_COLSUM=chain) read one; the scan recomputes it from the counts
-  double* cand_scratch(int64_t n) {
-    return scu::tuning().colsum_chain ? ensure<double>(cand, n) : nullptr;
+  // the materialised M-step candidate (count / m_t + beta): needed by the
+  // sequential-chain column sums (SAMELDA_COLSUM=chain), expected counts and
+  // an m_t outside the reciprocal path's range; otherwise the scan recomputes
+  // it from the u64 counts and no W x K candidate exists
+  double* cand_scratch(int64_t n, bool expected, double m_t_) {
+    const bool need = scu::tuning().colsum_chain || expected || !(m_t_ >= 0x1p-900 && m_t_ <= 0x1p900);
+    return need ? ensure<double>(cand, n) : nullptr;
   }
 
   // scratch of the exact parallel column-sum scan (grown at train_begin /
@@ -549,7 +552,7 @@ struct samelda_cu_ctx {
     ensure<double>(theta_batch, B_ * K_);
     ensure<float>(theta_batch32, B_ * K_);
     ensure<double>(theta_rows, B_ * K_);
-    cand_scratch(W_ * K_);
+    cand_scratch(W_ * K_, mode == SAMELDA_CU_MODE_EXPECTED, 1.0);
     ensure<double>(totals, K_);
     if (mode == SAMELDA_CU_MODE_EXPECTED) {
       ensure<double>(mu, nnz_);
@@ -915,13 +918,13 @@ static void update_call(samelda_cu_ctx* ctx, double* theta, int64_t D, double* p
     double* pf = ensure<double>(ctx->pf, W * K);
     ck(cudaMemcpyAsync(pf, pcounts, sizeof(double) * W * K, cudaMemcpyHostToDevice, st), "upload pf");
     ctx->launches += scu::launch_phi_mstep(nullptr, pf, W, Ki, m_t, beta, rho_t, phi_wk, nullptr,
-                                           ctx->cand_scratch(W * K), totals,
+                                           ctx->cand_scratch(W * K, true, m_t), totals,
                                            ctx->colsum_scratch(W, Ki), ctx->d_err(), st);
   } else {
     auto* pc = ensure<unsigned long long>(ctx->pc, W * K);
     ck(cudaMemcpyAsync(pc, pcounts, sizeof(int64_t) * W * K, cudaMemcpyHostToDevice, st), "upload pc");
     ctx->launches += scu::launch_phi_mstep(pc, nullptr, W, Ki, m_t, beta, rho_t, phi_wk, nullptr,
-                                           ctx->cand_scratch(W * K), totals,
+                                           ctx->cand_scratch(W * K, false, m_t), totals,
                                            ctx->colsum_scratch(W, Ki), ctx->d_err(), st);
   }
   double* back = ensure<double>(ctx->phi_call, K * W);
@@ -1171,7 +1174,7 @@ int samelda_cu_period_update(samelda_cu_ctx* ctx, double rho_t) {
     ctx->launches += scu::launch_theta_persist(tcu, tcf, ctx->batch.as<int32_t>(), ctx->B, K, ctx->m_t, c.alpha,
                                                ctx->theta.as<double>(), st);
     ctx->launches += scu::launch_phi_mstep(pcu, pcf, ctx->W, K, ctx->m_t, c.beta, rho_t, ctx->phi.as<double>(),
-                                           ctx->phi32.as<float>(), ctx->cand_scratch(ctx->W * K),
+                                           ctx->phi32.as<float>(), ctx->cand_scratch(ctx->W * K, f, ctx->m_t),
                                            ensure<double>(ctx->totals, K), ctx->colsum_scratch(ctx->W, K),
                                            ctx->d_err(), st);
     ctx->tick(samelda_cu_ctx::kMstep, false);

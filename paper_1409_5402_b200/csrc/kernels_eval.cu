@@ -72,6 +72,38 @@ __device__ __forceinline__ double seq_dot(const double* __restrict__ th,
   return dot;
 }
 
+// seq_dot over a row in global memory with deeper memory-level parallelism:
+// 16-double blocks (8 x 16-byte loads) double-buffered in registers, so the
+// next block's loads are in flight while the current block's sequential
+// adds run (same order, same rounding as seq_dot).  K % 16 == 0.
+__device__ __forceinline__ double seq_dot_pipe(const double* __restrict__ th,
+                                               const double* __restrict__ row, int K) {
+  const double2* r2 = reinterpret_cast<const double2*>(row);
+  double2 cur[8], nxt[8];
+#pragma unroll
+  for (int j = 0; j < 8; ++j) cur[j] = __ldg(r2 + j);
+  double dot = 0.0;
+  for (int b = 0; b < K; b += 16) {
+    if (b + 16 < K) {
+#pragma unroll
+      for (int j = 0; j < 8; ++j) nxt[j] = __ldg(r2 + (b + 16) / 2 + j);
+    }
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      dot = __dadd_rn(dot, __dmul_rn(th[b + 2 * j], cur[j].x));
+      dot = __dadd_rn(dot, __dmul_rn(th[b + 2 * j + 1], cur[j].y));
+    }
+#pragma unroll
+    for (int j = 0; j < 8; ++j) cur[j] = nxt[j];
+  }
+  return dot;
+}
+
+__device__ __forceinline__ double seq_dot_g(const double* __restrict__ th,
+                                            const double* __restrict__ row, int K) {
+  return (K & 15) == 0 ? seq_dot_pipe(th, row, K) : seq_dot(th, row, K);
+}
+
 __global__ void __launch_bounds__(kEvalWarps * 32) k_eval_docs(
     const int64_t* __restrict__ doc_offsets, const int32_t* __restrict__ word_ids,
     const int32_t* __restrict__ fold_counts, const int32_t* __restrict__ score_counts,
@@ -408,7 +440,7 @@ __global__ void __launch_bounds__(kEvalCtaThreads) k_eval_stage(
           const int f = f0 + tid;
           if (f < nf) {
             const double mu = f < rs ? seq_dot_stride1(th, rows + f * KP, K)
-                                     : seq_dot(th, phi_wk + static_cast<int64_t>(fw[f]) * K, K);
+                                     : seq_dot_g(th, phi_wk + static_cast<int64_t>(fw[f]) * K, K);
             fs[f] = mu > 0.0 ? __ddiv_rn(static_cast<double>(fc[f]), mu) : 0.0;
           }
         }
@@ -420,7 +452,7 @@ __global__ void __launch_bounds__(kEvalCtaThreads) k_eval_stage(
 #pragma unroll 8
           for (int f = 0; f < rs; ++f)
             acc = __dadd_rn(acc, __dmul_rn(__dmul_rn(fs[f], tk), rows[f * KP + k]));
-#pragma unroll 8
+#pragma unroll 16
           for (int f = rs; f < nf; ++f)
             acc = __dadd_rn(acc, __dmul_rn(__dmul_rn(fs[f], tk),
                                            __ldg(phi_wk + static_cast<int64_t>(fw[f]) * K + k)));
@@ -464,7 +496,7 @@ __global__ void __launch_bounds__(kEvalCtaThreads) k_eval_stage(
         const int32_t sc = __ldg(score_counts + i);
         double term = 0.0;
         if (sc != 0) {
-          const double pr = seq_dot(th, phi_wk + static_cast<int64_t>(__ldg(word_ids + i)) * K, K);
+          const double pr = seq_dot_g(th, phi_wk + static_cast<int64_t>(__ldg(word_ids + i)) * K, K);
           if (!(pr > 0.0)) atomicOr(err, kErrNumerical);
           term = __dmul_rn(static_cast<double>(sc), log(pr));
         }
@@ -561,10 +593,11 @@ int launch_eval_docs(const int64_t* doc_offsets, const int32_t* word_ids,
   if (n_docs == 0) return 0;
   const char ev = tuning().eval_variant;  // A/B: 'c' cta, 'w' warp; default staged
   if (K <= 1024 && ev != 'c' && ev != 'w') {
-    // staged rows: 3 CTAs per SM share (almost) all of shared memory
-    // (measured: 1 / 2 / 3 CTAs 176 / 148 / 139 ms at NYTimes shape;
+    // staged rows: 2 CTAs per SM share (almost) all of shared memory; the
+    // global-row dots (seq_dot_pipe, 128 registers) allow 2 resident CTAs
+    // (measured at NYTimes shape: 1 / 2 / 3 CTAs 134 / 117 / 126 ms;
     // SAMELDA_EVAL_CTAS_PER_SM overrides)
-    const int cps = tuning().eval_ctas_per_sm > 0 ? tuning().eval_ctas_per_sm : 3;
+    const int cps = tuning().eval_ctas_per_sm > 0 ? tuning().eval_ctas_per_sm : 2;
     const int KP = K | 1;
     const size_t fixed = (2 * static_cast<size_t>((K + 1) & ~1) + kEvalFoldMax) * sizeof(double) +
                          2 * kEvalFoldMax * sizeof(int32_t);
