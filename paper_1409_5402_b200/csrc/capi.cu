@@ -569,7 +569,7 @@ struct samelda_cu_ctx {
       const int64_t records = nnz_ * ((K_ + 255) / 256);
       ensure<unsigned char>(deferred, records * scu::deferred_record_bytes());
       ensure<unsigned char>(deferred_aux, scu::deferred_aux_bytes(records, draw_cap_for(records)));
-      ensure<unsigned long long>(n_deferred, 1);
+      ensure<unsigned long long>(n_deferred, 1 + (K_ + 255) / 256);
     }
     for (int i = 0; i < 2; ++i) stage(B_);
   }
@@ -619,7 +619,7 @@ struct samelda_cu_ctx {
       launches += scu::launch_sample_fast(bv, theta_b, theta_b32, phi_wk, phi_wk32, mu_d, K_,
                                           m_t_, seed, static_cast<uint32_t>(t),
                                           static_cast<uint32_t>(sweep), tc_, pc_, rec,
-                                          ensure<unsigned long long>(n_deferred, 1), aux, draw_cap,
+                                          ensure<unsigned long long>(n_deferred, 1 + (K_ + 255) / 256), aux, draw_cap,
                                           K_ > 256 ? ensure<float>(mu_f32, bv.nnz) : nullptr, d_err(),
                                           stream);
       tick(need_phi ? kSampleLast : kSample, false);

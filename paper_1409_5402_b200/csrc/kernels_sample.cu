@@ -216,8 +216,10 @@ __global__ void __launch_bounds__(kSampleBlock) k_sample(
 
 constexpr int kFastBlock = 256;
 // the decision variant of the production kernel (fast_poisson3 DEC 1: z in
-// {0, 1, 2} branch-free; DEC 3: fast_poisson4, z in {0, ..., 3})
-constexpr int kDecDefault = 3;
+// {0, 1, 2} branch-free, the sequential search beyond; a fourth branch-free
+// threshold was measured equal -- its extra instructions cost what the rarer
+// search saves -- with 9% more deferrals from the wider band)
+constexpr int kDecDefault = 1;
 
 // Nonzeros per warp work item: 128 (the packed u16 theta-count pairs hold
 // <= 128 nonzeros x z <= 40), fewer on small batches so the grid keeps ~4
@@ -440,32 +442,6 @@ __device__ __forceinline__ uint32_t fast_poisson3(float lam, float M, float Mb, 
   return __float_as_uint(__fadd_rn(zf, 8388608.0f)) - 0x4B000000u;
 }
 
-// DEC 3: four thresholds branch-free, z in {0, 1, 2, 3}; 4 = continue the
-// search from k = 4.  The band M must bound m_0..m_3: m_3 <= cdf_3 (r0 +
-// 1.8e-6) + pl pmf_3 + 2.5e-7 <= 2.53e-6 + 3.24e-6 lambda, so the caller forms
-// M = 2.6e-6 + 3.3e-6 lambda.  pmf_2 = t1 (lambda/2) and c2 = c1 + pmf_2 (the
-// reference recurrence, one rounding per step), c3 = fma(pmf_2, lambda/3, c2).
-// Out: p2 = pmf_2 and c3 for the search beyond 3.
-__device__ __forceinline__ uint32_t fast_poisson4(float lam, float M, float Mb, float u, bool& und,
-                                                  float& p2_out, float& c3_out) {
-  const float e0 = ex2_approx(__fmul_rn(lam, -1.4426950408889634f));
-  const float t1 = __fmul_rn(e0, lam);
-  const float c1 = __fadd_rn(e0, t1);
-  const float p2 = __fmul_rn(t1, __fmul_rn(lam, 0.5f));
-  const float c2 = __fadd_rn(c1, p2);
-  const float c3 = __fmaf_rn(p2, __fmul_rn(lam, 0.33333334f), c2);
-  const float d0 = __fsub_rn(u, e0), d1 = __fsub_rn(u, c1), d2 = __fsub_rn(u, c2), d3 = __fsub_rn(u, c3);
-  p2_out = p2;
-  c3_out = c3;
-  const float s0 = __saturatef(__fmaf_rn(d0, 0x1p100f, -Mb));
-  const float s1 = __saturatef(__fmaf_rn(d1, 0x1p100f, -Mb));
-  const float s2 = __saturatef(__fmaf_rn(d2, 0x1p100f, -Mb));
-  const float s3 = __saturatef(__fmaf_rn(d3, 0x1p100f, -Mb));
-  const float zf = __fadd_rn(__fadd_rn(s0, s1), __fadd_rn(s2, s3));
-  und = und || (fabsf(d0) <= M) || (fabsf(d1) <= M) || (fabsf(d2) <= M) || (fabsf(d3) <= M);
-  return __float_as_uint(__fadd_rn(zf, 8388608.0f)) - 0x4B000000u;
-}
-
 // sequential search from k = 3 (u beyond cdf_2 + M) with the bound above,
 // 1/k and the bound's k-term r_k - r_0 = 1.2e-6 + 6e-7 (k - 2)
 // read from constant tables (the step index is the same for every lane still
@@ -485,24 +461,6 @@ __constant__ float c_tail_rk[41] = {
     1.08e-5f, 1.14e-5f, 1.2e-5f,  1.26e-5f, 1.32e-5f, 1.38e-5f, 1.44e-5f, 1.5e-5f,  1.56e-5f,
     1.62e-5f, 1.68e-5f, 1.74e-5f, 1.8e-5f,  1.86e-5f, 1.92e-5f, 1.98e-5f, 2.04e-5f, 2.1e-5f,
     2.16e-5f, 2.22e-5f, 2.28e-5f, 2.34e-5f, 2.4e-5f};
-
-// the search from k = k0 + 1, given pmf_k0 and cdf_k0
-__device__ __forceinline__ uint32_t fast_poisson_search(float lam, float u, float pmf, float cdf,
-                                                        uint32_t k0, bool* und) {
-  const float r0 = __fmaf_rn(2.4e-7f, lam, 4.8e-7f);
-  const float pl = __fmul_rn(3e-6f, lam);
-#pragma unroll 1
-  for (uint32_t k = k0 + 1; k <= 40; ++k) {
-    pmf = __fmul_rn(pmf, __fmul_rn(lam, c_tail_inv[k]));
-    cdf = __fadd_rn(cdf, pmf);
-    const float mk = __fmaf_rn(cdf, __fadd_rn(r0, c_tail_rk[k]), __fmaf_rn(pmf, pl, 2.5e-7f));
-    const float dk = __fsub_rn(u, cdf);
-    if (dk < -mk) return k;
-    if (!(dk > mk)) break;
-  }
-  *und = true;
-  return 0;
-}
 
 __device__ __forceinline__ uint32_t fast_poisson_tail(float lam, float u, float t1, float c2,
                                                       bool* und) {
@@ -530,13 +488,22 @@ __global__ void __launch_bounds__(kFastBlock, MINB) k_sample_v2(
     const double* __restrict__ mu_in, const float* __restrict__ mu_f_in, int K, double m_t,
     uint64_t seed, uint32_t t, uint32_t sweep, int64_t chunk,
     unsigned long long* __restrict__ theta_counts, unsigned long long* __restrict__ phi_counts,
-    Deferred* __restrict__ deferred, unsigned long long* __restrict__ n_deferred) {
+    Deferred* __restrict__ deferred, unsigned long long* __restrict__ n_deferred,
+    unsigned long long* __restrict__ work) {
   constexpr int KG = KPL < 4 ? KPL : 4;  // Philox chains in flight per group
   const int lane = threadIdx.x & 31;
-  const int64_t item = static_cast<int64_t>(blockIdx.x) * (kFastBlock / kWarp) + (threadIdx.x >> 5);
   const int kbase = static_cast<int>(blockIdx.y) * kWarp * KPL;
-  const int64_t p0 = item * chunk;
-  const int64_t p1 = min(p0 + chunk, bv.nnz);
+  // work != nullptr: a persistent grid (a few blocks per SM) whose warps take
+  // chunks from a counter per topic slice until the batch is done -- no
+  // partial last wave, and the topic key table is built once per block;
+  // else one chunk per warp
+  auto next_item = [&]() -> int64_t {
+    if (work == nullptr) return static_cast<int64_t>(blockIdx.x) * (kFastBlock / kWarp) + (threadIdx.x >> 5);
+    unsigned long long v = 0;
+    if (lane == 0) v = atomicAdd(work + blockIdx.y, 1ull);
+    return static_cast<int64_t>(__shfl_sync(0xffffffffu, v, 0));
+  };
+  int64_t item = next_item();
 
   __shared__ uint4 s_keys[KPL][kKeyWords / 4][kWarp];
   // TAIL 1: draws that need the sequential search (u beyond cdf_2 + M) are
@@ -554,6 +521,9 @@ __global__ void __launch_bounds__(kFastBlock, MINB) k_sample_v2(
       s_keys[jj][q][ll] = make_uint4(ks[4 * q], ks[4 * q + 1], ks[4 * q + 2], ks[4 * q + 3]);
   }
   __syncthreads();
+  for (;; item = next_item()) {
+  const int64_t p0 = item * chunk;
+  const int64_t p1 = min(p0 + chunk, bv.nnz);
   if (p0 >= p1) return;
 
   int cur_b = -1;
@@ -662,23 +632,10 @@ __global__ void __launch_bounds__(kFastBlock, MINB) k_sample_v2(
           bool und = !(prod[j] >= 1e-30f) || !(lam < kInvMax);
           const float u = __fsub_rn(__int_as_float(0x3f800000 | (y[jj] >> 9)), 1.0f);
           float t1, c2;
-          uint32_t z;
+          const float M = __fmaf_rn(prod[j], mslope, 2e-6f);
+          uint32_t z = fast_poisson3<DEC>(lam, M, __fmul_rn(M, 0x1p100f), u, und, t1, c2);
           bool park = false;
-          if (DEC == 3) {
-            const float M = __fmaf_rn(prod[j], mslope, 2.6e-6f);
-            float p2, c3;
-            z = fast_poisson4(lam, M, __fmul_rn(M, 0x1p100f), u, und, p2, c3);
-            if (z == 4 && !und) {
-              // pmf_3 formed as the search's recurrence would (pmf_2 lambda / 3)
-              const float p3 = __fmul_rn(p2, __fmul_rn(lam, c_tail_inv[3]));
-              z = fast_poisson_search(lam, u, p3, c3, 3, &und);
-            }
-          } else {
-            const float M = __fmaf_rn(prod[j], mslope, 2e-6f);
-            z = fast_poisson3<DEC>(lam, M, __fmul_rn(M, 0x1p100f), u, und, t1, c2);
-          }
-          if (DEC == 3) {
-          } else if (TAIL == 0) {
+          if (TAIL == 0) {
             if (z == 3 && !und) z = fast_poisson_tail(lam, u, t1, c2, &und);
           } else {
             park = z == 3 && !und;
@@ -748,6 +705,8 @@ __global__ void __launch_bounds__(kFastBlock, MINB) k_sample_v2(
     }
   }
   if (cur_b >= 0) flush(cur_b);
+  if (work == nullptr) return;
+  }  // items
 }
 
 // Deferred exact draws in two passes.
@@ -1184,7 +1143,10 @@ int launch_fast_kpl(const BatchView& bv, const double* tb64, const float* tb32, 
   const int64_t items = (bv.nnz + chunk - 1) / chunk;
   const int warps = kFastBlock / kWarp;
   int launched = 0;
-  cudaMemsetAsync(n_deferred, 0, sizeof(unsigned long long), st);
+  // n_deferred[0]: the deferred-record count; n_deferred[1 + s]: the chunk
+  // counter of topic slice s (persistent grid), all zeroed per launch
+  cudaMemsetAsync(n_deferred, 0, sizeof(unsigned long long) * (1 + n_slices), st);
+  unsigned long long* work = n_deferred + 1;
   const float* muf = nullptr;
   if (n_slices > 1 && mu == nullptr) {
     k_mu_f32<<<grid_for((bv.nnz + 31) / 32 * 32, 256), 256, 0, st>>>(bv, tb32, phi32, K, mu_f);
@@ -1192,7 +1154,9 @@ int launch_fast_kpl(const BatchView& bv, const double* tb64, const float* tb32, 
     ++launched;
   }
   auto* rec = static_cast<Deferred*>(deferred);
-  const dim3 grid(static_cast<unsigned>((items + warps - 1) / warps), static_cast<unsigned>(n_slices));
+  // persistent: at most the resident blocks (4 per SM at 64 registers)
+  const int64_t blocks = std::min<int64_t>((items + warps - 1) / warps, int64_t{148} * 4);
+  const dim3 grid(static_cast<unsigned>(blocks), static_cast<unsigned>(n_slices));
   {
     const int musrc = mu ? 1 : (muf ? 2 : 0);
     const bool full = K % (kWarp * KPL) == 0;
@@ -1201,7 +1165,7 @@ int launch_fast_kpl(const BatchView& bv, const double* tb64, const float* tb32, 
       if constexpr (KPL == 8) {
         if (full && musrc == 0 && n_slices == 1) {
           k_sample_v2<8, true, 0, 4, kDecDefault, 0, false><<<grid, kFastBlock, 0, st>>>(
-              bv, tb32, phi32, mu, muf, K, m_t, seed, t, sweep, chunk, tc, pc, rec, n_deferred);
+              bv, tb32, phi32, mu, muf, K, m_t, seed, t, sweep, chunk, tc, pc, rec, n_deferred, work);
           launch_deferred(bv, tb64, phi64, mu, K, m_t, seed, t, sweep, rec, n_deferred, aux,
                           bv.nnz * ((K + 255) / 256), draw_cap, tc, pc, err, st);
           return launched + 3;
@@ -1211,7 +1175,7 @@ int launch_fast_kpl(const BatchView& bv, const double* tb64, const float* tb32, 
     }
 #define SCU_V2_LAUNCH(FULLV, MS, MB, DC, ...)                                                   \
   k_sample_v2<KPL, FULLV, MS, MB, DC __VA_OPT__(,) __VA_ARGS__><<<grid, kFastBlock, 0, st>>>(    \
-      bv, tb32, phi32, mu, muf, K, m_t, seed, t, sweep, chunk, tc, pc, rec, n_deferred)
+      bv, tb32, phi32, mu, muf, K, m_t, seed, t, sweep, chunk, tc, pc, rec, n_deferred, work)
     // production: DEC 1, 4 blocks/SM.  A library built with
     // -DSAMELDA_AB_VARIANTS also carries the measured alternatives (all
     // bit-identical, all slower at K = 256): SAMELDA_DEC=0|2, SAMELDA_MINB=3,
