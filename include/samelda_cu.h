@@ -239,6 +239,32 @@ int samelda_cu_train(samelda_cu_ctx* ctx, const samelda_cu_corpus* corpus,
                      int64_t eval_every, double* phi_out, double* theta_out,
                      samelda_cu_trace_row* trace, int64_t trace_cap, int64_t* n_trace);
 
+/* ------------------------------------ collapsed Gibbs sampler (the baseline)
+ *
+ * The paper's comparison method: cgs.hpp:17-49 /
+ * cgs.cpp:11-157 with the reference's draws (state in the context; the
+ * corpus is the context's training corpus).  The sweep is sequential by
+ * definition (one token at a time); on the device it is one warp. */
+/* replaces samelda::cgs_init, cgs.hpp:29-31 / cgs.cpp:11-55 (n_topics <= 1024) */
+int samelda_cu_cgs_init(samelda_cu_ctx* ctx, const samelda_cu_corpus* corpus, int64_t n_topics,
+                        double alpha, double beta, uint64_t seed);
+/* replaces samelda::cgs_sweep, cgs.hpp:33-38 / cgs.cpp:57-98 (asynchronous) */
+int samelda_cu_cgs_sweep(samelda_cu_ctx* ctx, uint64_t seed, int64_t sweep_index);
+/* CgsState's arrays (cgs.hpp:17-27): z (n_tokens), doc_topic D x K, word_topic
+ * W x K, topic_total K; any may be NULL */
+int samelda_cu_cgs_state(samelda_cu_ctx* ctx, int32_t* z, int32_t* doc_topic, int32_t* word_topic,
+                         int64_t* topic_total);
+int samelda_cu_cgs_set_state(samelda_cu_ctx* ctx, const int32_t* z, const int32_t* doc_topic,
+                             const int32_t* word_topic, const int64_t* topic_total);
+/* replaces samelda::cgs_model, cgs.hpp:40-41 / cgs.cpp:100-129: phi K x W, theta D x K */
+int samelda_cu_cgs_model(samelda_cu_ctx* ctx, double* phi, double* theta);
+/* replaces samelda::cgs_train, cgs.hpp:43-49 / cgs.cpp:131-157 */
+int samelda_cu_cgs_train(samelda_cu_ctx* ctx, const samelda_cu_corpus* corpus, int64_t n_topics,
+                         double alpha, double beta, int64_t n_sweeps, uint64_t seed,
+                         int64_t eval_every, const samelda_cu_corpus* heldout, double* phi_out,
+                         double* theta_out, samelda_cu_trace_row* trace, int64_t trace_cap,
+                         int64_t* n_trace);
+
 /* ------------------------------------- multi-GPU group (one process, N GPUs)
  *
  * SURVEY.md 8(e) behind the ABI: documents are split into contiguous ranges

@@ -567,6 +567,45 @@ class Ref:
         return phi.reshape(K, W), theta.reshape(D, K), _trace_to_list(rows, n.value)
 
 
+    # ---- collapsed Gibbs baseline
+    def cgs_run(self, corpus: CorpusArrays, K, alpha, beta, seed, n_sweeps):
+        """cgs_init + cgs_sweep 1..n_sweeps (cgs.cpp:11-98): (z, doc_topic, word_topic,
+        topic_total)."""
+        L = self.lib
+        L.ref_cgs_run.argtypes = [_i64p, _i32p, _i32p, C.c_int64, C.c_int64, C.c_int64,
+                                  C.c_double, C.c_double, C.c_uint64, C.c_int64, _i32p, _i32p,
+                                  _i32p, _i64p]
+        n_tok = int(np.asarray(corpus.counts, np.int64).sum())
+        z = np.zeros(max(n_tok, 1), np.int32)
+        dt = np.zeros(max(corpus.n_docs * K, 1), np.int32)
+        wt = np.zeros(max(corpus.n_words * K, 1), np.int32)
+        tt = np.zeros(K, np.int64)
+        self._chk(L.ref_cgs_run(corpus.doc_offsets, corpus.word_ids, corpus.counts,
+                                corpus.n_docs, corpus.n_words, K, alpha, beta, seed, n_sweeps,
+                                z, dt, wt, tt))
+        return (z[:n_tok], dt[:corpus.n_docs * K].reshape(corpus.n_docs, K),
+                wt[:corpus.n_words * K].reshape(corpus.n_words, K), tt)
+
+    def cgs_train(self, corpus: CorpusArrays, K, alpha, beta, n_sweeps, seed, eval_every=0,
+                  heldout: CorpusArrays | None = None, n_threads=1):
+        L = self.lib
+        L.ref_cgs_train.argtypes = [_i64p, _i32p, _i32p, C.c_int64, C.c_int64, C.c_void_p,
+                                    C.c_void_p, C.c_void_p, C.c_int64, C.c_int64, C.c_double,
+                                    C.c_double, C.c_int64, C.c_uint64, C.c_int64, C.c_int,
+                                    _f64p, _f64p, C.POINTER(_TraceRow), C.POINTER(C.c_int64)]
+        W, D = corpus.n_words, corpus.n_docs
+        phi = np.zeros(max(K * W, 1))
+        theta = np.zeros(max(D * K, 1))
+        rows = (_TraceRow * max(n_sweeps, 1))()
+        n = C.c_int64()
+        ho = (heldout.doc_offsets.ctypes.data, heldout.word_ids.ctypes.data,
+              heldout.counts.ctypes.data, heldout.n_docs) if heldout is not None else (
+            None, None, None, 0)
+        self._chk(L.ref_cgs_train(corpus.doc_offsets, corpus.word_ids, corpus.counts, D, W, *ho,
+                                  K, alpha, beta, n_sweeps, seed, eval_every, n_threads, phi,
+                                  theta, rows, C.byref(n)))
+        return phi[:K * W].reshape(K, W), theta[:D * K].reshape(D, K), _trace_to_list(rows, n.value)
+
     # ---- data formats: the reference's own load/save (SURVEY 8(f) rows 1, 3)
     def _io_sigs(self):
         L = self.lib

@@ -17,6 +17,7 @@
 #include <string>
 #include <vector>
 
+#include "samelda/cgs.hpp"
 #include "samelda/corpus.hpp"
 #include "samelda/errors.hpp"
 #include "samelda/eval.hpp"
@@ -332,6 +333,47 @@ int ref_train(const int64_t* offsets, const int32_t* words, const int32_t* count
       trace_out[i] = {trace[i].t, trace[i].passes, trace[i].samples_per_word, trace[i].ll,
                       trace[i].wall_seconds, trace[i].m_t};
     }
+  });
+}
+
+// ---- collapsed Gibbs baseline: cgs_init + sweeps 1..n
+// (cgs.cpp:11-98), the state after them; and cgs_train (cgs.cpp:131-157)
+int ref_cgs_run(const int64_t* offsets, const int32_t* words, const int32_t* counts,
+                int64_t n_docs, int64_t n_words, int64_t K, double alpha, double beta,
+                uint64_t seed, int64_t n_sweeps, int32_t* z, int32_t* doc_topic,
+                int32_t* word_topic, int64_t* topic_total) {
+  return guarded([&] {
+    const Corpus corpus = make_corpus(offsets, words, counts, n_docs, n_words);
+    CgsState st = cgs_init(corpus, K, alpha, beta, seed);
+    for (int64_t s = 1; s <= n_sweeps; ++s) cgs_sweep(st, corpus, seed, s);
+    std::memcpy(z, st.z.data(), sizeof(int32_t) * st.z.size());
+    std::memcpy(doc_topic, st.doc_topic.data(), sizeof(int32_t) * st.doc_topic.size());
+    std::memcpy(word_topic, st.word_topic.data(), sizeof(int32_t) * st.word_topic.size());
+    std::memcpy(topic_total, st.topic_total.data(), sizeof(int64_t) * st.topic_total.size());
+  });
+}
+
+int ref_cgs_train(const int64_t* offsets, const int32_t* words, const int32_t* counts,
+                  int64_t n_docs, int64_t n_words, const int64_t* ho_offsets,
+                  const int32_t* ho_words, const int32_t* ho_counts, int64_t ho_docs, int64_t K,
+                  double alpha, double beta, int64_t n_sweeps, uint64_t seed, int64_t eval_every,
+                  int n_threads, double* phi_out, double* theta_out, ref_trace_row* trace_out,
+                  int64_t* n_trace) {
+  return guarded([&] {
+    const Corpus corpus = make_corpus(offsets, words, counts, n_docs, n_words);
+    Corpus heldout;
+    const Corpus* ho = nullptr;
+    if (ho_offsets != nullptr) {
+      heldout = make_corpus(ho_offsets, ho_words, ho_counts, ho_docs, n_words);
+      ho = &heldout;
+    }
+    auto [model, trace] = cgs_train(corpus, K, alpha, beta, n_sweeps, seed, eval_every, ho, n_threads);
+    std::memcpy(phi_out, model.phi.data.data(), sizeof(double) * model.phi.data.size());
+    std::memcpy(theta_out, model.theta.data.data(), sizeof(double) * model.theta.data.size());
+    *n_trace = static_cast<int64_t>(trace.size());
+    for (size_t i = 0; i < trace.size(); ++i)
+      trace_out[i] = {trace[i].t, trace[i].passes, trace[i].samples_per_word, trace[i].ll,
+                      trace[i].wall_seconds, trace[i].m_t};
   });
 }
 

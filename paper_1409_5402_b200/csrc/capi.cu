@@ -320,6 +320,13 @@ struct samelda_cu_ctx {
   // doc-sharded runs: global id of local doc 0 (Philox keys use global ids)
   int64_t doc_base = 0;
 
+  // collapsed Gibbs sampler state (cgs_* entry points; corpus in `train`)
+  bool cgs_ready = false;
+  int cgs_K = 0;
+  double cgs_alpha = 0.0, cgs_beta = 0.0;
+  int64_t cgs_tokens = 0;
+  DevBuf cgs_tok, cgs_z, cgs_dt, cgs_wt, cgs_tt, cgs_phi;
+
   // optional per-kernel CUDA-event timing (bench roofline)
   bool profile = false;
   enum { kSample = 0, kSddmm = 1, kMstep = 2, kSampleLast = 3, kKinds = 4 };
@@ -569,7 +576,7 @@ struct samelda_cu_ctx {
       const int64_t records = nnz_ * ((K_ + 255) / 256);
       ensure<unsigned char>(deferred, records * scu::deferred_record_bytes());
       ensure<unsigned char>(deferred_aux, scu::deferred_aux_bytes(records, draw_cap_for(records)));
-      ensure<unsigned long long>(n_deferred, 1 + (K_ + 255) / 256);
+      ensure<unsigned long long>(n_deferred, 1);
     }
     for (int i = 0; i < 2; ++i) stage(B_);
   }
@@ -619,7 +626,7 @@ struct samelda_cu_ctx {
       launches += scu::launch_sample_fast(bv, theta_b, theta_b32, phi_wk, phi_wk32, mu_d, K_,
                                           m_t_, seed, static_cast<uint32_t>(t),
                                           static_cast<uint32_t>(sweep), tc_, pc_, rec,
-                                          ensure<unsigned long long>(n_deferred, 1 + (K_ + 255) / 256), aux, draw_cap,
+                                          ensure<unsigned long long>(n_deferred, 1), aux, draw_cap,
                                           K_ > 256 ? ensure<float>(mu_f32, bv.nnz) : nullptr, d_err(),
                                           stream);
       tick(need_phi ? kSampleLast : kSample, false);
@@ -1024,6 +1031,167 @@ int samelda_cu_perword_loglik(samelda_cu_ctx* ctx, const double* phi, int64_t K,
     ctx->prepare_split(seed);
     const double* phi_wk = ctx->upload_phi(phi, K, W);
     *ll_out = ctx->eval_ll(phi_wk, static_cast<int>(K), alpha);
+  });
+}
+
+// ------------------------------------------------------------ CGS baseline
+
+static void cgs_require(samelda_cu_ctx* ctx) {
+  if (!ctx->cgs_ready) fail(SAMELDA_CU_CONFIG, "cgs: call samelda_cu_cgs_init first");
+}
+
+int samelda_cu_cgs_init(samelda_cu_ctx* ctx, const samelda_cu_corpus* corpus, int64_t n_topics,
+                        double alpha, double beta, uint64_t seed) {
+  return guarded(ctx, [&] {
+    // cgs.cpp:13-18
+    if (n_topics < 1 || n_topics > (1 << 20)) fail(SAMELDA_CU_CONFIG, "cgs_init: n_topics must be >= 1");
+    if (!(alpha > 0.0) || !(beta > 0.0)) fail(SAMELDA_CU_CONFIG, "cgs_init: alpha and beta must be positive");
+    if (n_topics > 1024) fail(SAMELDA_CU_CONFIG, "cgs_init: the device sampler supports n_topics <= 1024");
+    validate_corpus(corpus);
+    upload_corpus(ctx->train, corpus, ctx->stream);
+    const CorpusSlot& s = ctx->train;
+    const int K = static_cast<int>(n_topics);
+    std::vector<int64_t> tok(static_cast<size_t>(s.nnz) + 1, 0);
+    for (int64_t i = 0; i < s.nnz; ++i) tok[i + 1] = tok[i] + corpus->counts[i];
+    ctx->cgs_tokens = tok[s.nnz];
+    int64_t* dtok = ensure<int64_t>(ctx->cgs_tok, s.nnz + 1);
+    ck(cudaMemcpyAsync(dtok, tok.data(), sizeof(int64_t) * (s.nnz + 1), cudaMemcpyHostToDevice, ctx->stream),
+       "upload token offsets");
+    int32_t* z = ensure<int32_t>(ctx->cgs_z, ctx->cgs_tokens);
+    int32_t* dt = ensure<int32_t>(ctx->cgs_dt, s.n_docs * K);
+    int32_t* wt = ensure<int32_t>(ctx->cgs_wt, s.n_words * K);
+    auto* tt = ensure<unsigned long long>(ctx->cgs_tt, K);
+    ck(cudaMemsetAsync(dt, 0, sizeof(int32_t) * std::max<int64_t>(s.n_docs * K, 1), ctx->stream), "zero dt");
+    ck(cudaMemsetAsync(wt, 0, sizeof(int32_t) * std::max<int64_t>(s.n_words * K, 1), ctx->stream), "zero wt");
+    ck(cudaMemsetAsync(tt, 0, sizeof(unsigned long long) * K, ctx->stream), "zero tt");
+    ctx->launches += scu::launch_cgs_init(s.offs.as<int64_t>(), s.words.as<int32_t>(), s.counts.as<int32_t>(),
+                                          dtok, s.n_docs, K, seed, z, dt, wt, tt, ctx->stream);
+    ck(cudaStreamSynchronize(ctx->stream), "cgs_init");
+    ck(cudaGetLastError(), "cgs_init");
+    ctx->cgs_K = K;
+    ctx->cgs_alpha = alpha;
+    ctx->cgs_beta = beta;
+    ctx->cgs_ready = true;
+  });
+}
+
+int samelda_cu_cgs_sweep(samelda_cu_ctx* ctx, uint64_t seed, int64_t sweep_index) {
+  return guarded(ctx, [&] {
+    cgs_require(ctx);
+    const CorpusSlot& s = ctx->train;
+    ctx->poll_err(false, "cgs_sweep");
+    ctx->launches += scu::launch_cgs_sweep(
+        s.offs.as<int64_t>(), s.words.as<int32_t>(), s.counts.as<int32_t>(), ctx->cgs_tok.as<int64_t>(),
+        s.n_docs, ctx->cgs_K, s.n_words, ctx->cgs_alpha, ctx->cgs_beta, seed,
+        static_cast<uint32_t>(sweep_index), ctx->cgs_z.as<int32_t>(), ctx->cgs_dt.as<int32_t>(),
+        ctx->cgs_wt.as<int32_t>(), ctx->cgs_tt.as<unsigned long long>(), ctx->d_err(), ctx->stream);
+    ck(cudaGetLastError(), "cgs_sweep launch");
+    ctx->post_err_check();
+  });
+}
+
+int samelda_cu_cgs_state(samelda_cu_ctx* ctx, int32_t* z, int32_t* doc_topic, int32_t* word_topic,
+                         int64_t* topic_total) {
+  return guarded(ctx, [&] {
+    cgs_require(ctx);
+    ctx->poll_err(true, "cgs_sweep");
+    const CorpusSlot& s = ctx->train;
+    const int64_t K = ctx->cgs_K;
+    cudaStream_t st = ctx->stream;
+    if (z && ctx->cgs_tokens)
+      ck(cudaMemcpyAsync(z, ctx->cgs_z.p, sizeof(int32_t) * ctx->cgs_tokens, cudaMemcpyDeviceToHost, st), "z");
+    if (doc_topic && s.n_docs * K)
+      ck(cudaMemcpyAsync(doc_topic, ctx->cgs_dt.p, sizeof(int32_t) * s.n_docs * K, cudaMemcpyDeviceToHost, st), "dt");
+    if (word_topic && s.n_words * K)
+      ck(cudaMemcpyAsync(word_topic, ctx->cgs_wt.p, sizeof(int32_t) * s.n_words * K, cudaMemcpyDeviceToHost, st), "wt");
+    if (topic_total)
+      ck(cudaMemcpyAsync(topic_total, ctx->cgs_tt.p, sizeof(int64_t) * K, cudaMemcpyDeviceToHost, st), "tt");
+    ck(cudaStreamSynchronize(st), "cgs_state");
+  });
+}
+
+int samelda_cu_cgs_set_state(samelda_cu_ctx* ctx, const int32_t* z, const int32_t* doc_topic,
+                             const int32_t* word_topic, const int64_t* topic_total) {
+  return guarded(ctx, [&] {
+    cgs_require(ctx);
+    const CorpusSlot& s = ctx->train;
+    const int64_t K = ctx->cgs_K;
+    cudaStream_t st = ctx->stream;
+    if (z && ctx->cgs_tokens)
+      ck(cudaMemcpyAsync(ctx->cgs_z.p, z, sizeof(int32_t) * ctx->cgs_tokens, cudaMemcpyHostToDevice, st), "z");
+    if (doc_topic && s.n_docs * K)
+      ck(cudaMemcpyAsync(ctx->cgs_dt.p, doc_topic, sizeof(int32_t) * s.n_docs * K, cudaMemcpyHostToDevice, st), "dt");
+    if (word_topic && s.n_words * K)
+      ck(cudaMemcpyAsync(ctx->cgs_wt.p, word_topic, sizeof(int32_t) * s.n_words * K, cudaMemcpyHostToDevice, st), "wt");
+    if (topic_total)
+      ck(cudaMemcpyAsync(ctx->cgs_tt.p, topic_total, sizeof(int64_t) * K, cudaMemcpyHostToDevice, st), "tt");
+    ck(cudaStreamSynchronize(st), "cgs_set_state");
+  });
+}
+
+int samelda_cu_cgs_model(samelda_cu_ctx* ctx, double* phi, double* theta) {
+  return guarded(ctx, [&] {
+    cgs_require(ctx);
+    ctx->poll_err(true, "cgs_sweep");
+    const CorpusSlot& s = ctx->train;
+    const int K = ctx->cgs_K;
+    double* pw = ensure<double>(ctx->cgs_phi, s.n_words * K);
+    double* th = theta ? ensure<double>(ctx->theta_rows, s.n_docs * K) : nullptr;
+    ctx->launches += scu::launch_cgs_model(ctx->cgs_dt.as<int32_t>(), ctx->cgs_wt.as<int32_t>(),
+                                           ctx->cgs_tt.as<unsigned long long>(), s.n_docs, s.n_words, K,
+                                           ctx->cgs_alpha, ctx->cgs_beta, pw, th, ctx->stream);
+    if (phi && s.n_words * K) {
+      double* tmp = ensure<double>(ctx->phi_call, K * s.n_words);
+      ctx->launches += scu::launch_transpose(pw, s.n_words, K, tmp, ctx->stream);
+      ck(cudaMemcpyAsync(phi, tmp, sizeof(double) * K * s.n_words, cudaMemcpyDeviceToHost, ctx->stream), "phi");
+    }
+    if (theta && s.n_docs * K)
+      ck(cudaMemcpyAsync(theta, th, sizeof(double) * s.n_docs * K, cudaMemcpyDeviceToHost, ctx->stream), "theta");
+    ck(cudaStreamSynchronize(ctx->stream), "cgs_model");
+  });
+}
+
+int samelda_cu_cgs_train(samelda_cu_ctx* ctx, const samelda_cu_corpus* corpus, int64_t n_topics,
+                         double alpha, double beta, int64_t n_sweeps, uint64_t seed,
+                         int64_t eval_every, const samelda_cu_corpus* heldout, double* phi_out,
+                         double* theta_out, samelda_cu_trace_row* trace, int64_t trace_cap,
+                         int64_t* n_trace) {
+  // cgs.cpp:131-157
+  if (ctx == nullptr) return SAMELDA_CU_CONFIG;
+  if (n_sweeps < 0) {
+    ctx->error = "cgs_train: n_sweeps must be >= 0";
+    return SAMELDA_CU_CONFIG;
+  }
+  *n_trace = 0;
+  int rc = samelda_cu_cgs_init(ctx, corpus, n_topics, alpha, beta, seed);
+  if (rc) return rc;
+  const bool do_eval = heldout != nullptr && eval_every > 0;
+  if (do_eval && n_sweeps > 0) {
+    rc = samelda_cu_heldout(ctx, heldout, seed);
+    if (rc) return rc;
+  }
+  return guarded(ctx, [&] {
+    const auto t_start = std::chrono::steady_clock::now();
+    const int K = ctx->cgs_K;
+    for (int64_t sweep = 1; sweep <= n_sweeps; ++sweep) {
+      int r = samelda_cu_cgs_sweep(ctx, seed, sweep);
+      if (r) throw Fail{r, ctx->error};
+      if (do_eval && (sweep % eval_every == 0 || sweep == n_sweeps)) {
+        if (ctx->heldout.n_words != ctx->train.n_words)
+          fail(SAMELDA_CU_CONFIG, "perword_loglik: phi width disagrees with corpus vocabulary");
+        double* pw = ensure<double>(ctx->cgs_phi, ctx->train.n_words * K);
+        ctx->launches += scu::launch_cgs_model(ctx->cgs_dt.as<int32_t>(), ctx->cgs_wt.as<int32_t>(),
+                                               ctx->cgs_tt.as<unsigned long long>(), ctx->train.n_docs,
+                                               ctx->train.n_words, K, alpha, beta, pw, nullptr, ctx->stream);
+        const double ll = ctx->eval_ll(pw, K, alpha);
+        const std::chrono::duration<double> el = std::chrono::steady_clock::now() - t_start;
+        if (*n_trace >= trace_cap) fail(SAMELDA_CU_CONFIG, "trace buffer too small");
+        // one sample per token per sweep: samples/word == sweep (cgs.cpp:149-151)
+        trace[(*n_trace)++] = {sweep, static_cast<double>(sweep), static_cast<double>(sweep), ll, el.count(), 1.0};
+      }
+    }
+    const int r = samelda_cu_cgs_model(ctx, phi_out, theta_out);
+    if (r) throw Fail{r, ctx->error};
   });
 }
 

@@ -153,4 +153,18 @@ int launch_ordered_ll(const double* doc_logp, const int64_t* doc_scored, int64_t
 // scratch doubles launch_eval_docs needs when K is too large for shared memory
 int64_t eval_scratch_doubles(int K);
 
+// collapsed Gibbs sampler baseline (cgs.cpp:11-157): state z (tokens), dt
+// (D x K), wt (W x K) int32, tt (K) u64; tok_off = nnz + 1 token offsets
+int launch_cgs_init(const int64_t* offsets, const int32_t* words, const int32_t* counts,
+                    const int64_t* tok_off, int64_t D, int K, uint64_t seed, int32_t* z, int32_t* dt,
+                    int32_t* wt, unsigned long long* tt, cudaStream_t st);
+int launch_cgs_sweep(const int64_t* offsets, const int32_t* words, const int32_t* counts,
+                     const int64_t* tok_off, int64_t D, int K, int64_t W, double alpha, double beta,
+                     uint64_t seed, uint32_t sweep, int32_t* z, int32_t* dt, int32_t* wt,
+                     unsigned long long* tt, int* err, cudaStream_t st);
+// phi_wk W x K (eval layout); theta D x K (optional)
+int launch_cgs_model(const int32_t* dt, const int32_t* wt, const unsigned long long* tt, int64_t D,
+                     int64_t W, int K, double alpha, double beta, double* phi_wk, double* theta,
+                     cudaStream_t st);
+
 }  // namespace scu

@@ -488,22 +488,11 @@ __global__ void __launch_bounds__(kFastBlock, MINB) k_sample_v2(
     const double* __restrict__ mu_in, const float* __restrict__ mu_f_in, int K, double m_t,
     uint64_t seed, uint32_t t, uint32_t sweep, int64_t chunk,
     unsigned long long* __restrict__ theta_counts, unsigned long long* __restrict__ phi_counts,
-    Deferred* __restrict__ deferred, unsigned long long* __restrict__ n_deferred,
-    unsigned long long* __restrict__ work) {
+    Deferred* __restrict__ deferred, unsigned long long* __restrict__ n_deferred) {
   constexpr int KG = KPL < 4 ? KPL : 4;  // Philox chains in flight per group
   const int lane = threadIdx.x & 31;
   const int kbase = static_cast<int>(blockIdx.y) * kWarp * KPL;
-  // work != nullptr: a persistent grid (a few blocks per SM) whose warps take
-  // chunks from a counter per topic slice until the batch is done -- no
-  // partial last wave, and the topic key table is built once per block;
-  // else one chunk per warp
-  auto next_item = [&]() -> int64_t {
-    if (work == nullptr) return static_cast<int64_t>(blockIdx.x) * (kFastBlock / kWarp) + (threadIdx.x >> 5);
-    unsigned long long v = 0;
-    if (lane == 0) v = atomicAdd(work + blockIdx.y, 1ull);
-    return static_cast<int64_t>(__shfl_sync(0xffffffffu, v, 0));
-  };
-  int64_t item = next_item();
+  const int64_t item = static_cast<int64_t>(blockIdx.x) * (kFastBlock / kWarp) + (threadIdx.x >> 5);
 
   __shared__ uint4 s_keys[KPL][kKeyWords / 4][kWarp];
   // TAIL 1: draws that need the sequential search (u beyond cdf_2 + M) are
@@ -521,7 +510,6 @@ __global__ void __launch_bounds__(kFastBlock, MINB) k_sample_v2(
       s_keys[jj][q][ll] = make_uint4(ks[4 * q], ks[4 * q + 1], ks[4 * q + 2], ks[4 * q + 3]);
   }
   __syncthreads();
-  for (;; item = next_item()) {
   const int64_t p0 = item * chunk;
   const int64_t p1 = min(p0 + chunk, bv.nnz);
   if (p0 >= p1) return;
@@ -705,8 +693,6 @@ __global__ void __launch_bounds__(kFastBlock, MINB) k_sample_v2(
     }
   }
   if (cur_b >= 0) flush(cur_b);
-  if (work == nullptr) return;
-  }  // items
 }
 
 // Deferred exact draws in two passes.
@@ -1143,10 +1129,7 @@ int launch_fast_kpl(const BatchView& bv, const double* tb64, const float* tb32, 
   const int64_t items = (bv.nnz + chunk - 1) / chunk;
   const int warps = kFastBlock / kWarp;
   int launched = 0;
-  // n_deferred[0]: the deferred-record count; n_deferred[1 + s]: the chunk
-  // counter of topic slice s (persistent grid), all zeroed per launch
-  cudaMemsetAsync(n_deferred, 0, sizeof(unsigned long long) * (1 + n_slices), st);
-  unsigned long long* work = n_deferred + 1;
+  cudaMemsetAsync(n_deferred, 0, sizeof(unsigned long long), st);
   const float* muf = nullptr;
   if (n_slices > 1 && mu == nullptr) {
     k_mu_f32<<<grid_for((bv.nnz + 31) / 32 * 32, 256), 256, 0, st>>>(bv, tb32, phi32, K, mu_f);
@@ -1154,9 +1137,9 @@ int launch_fast_kpl(const BatchView& bv, const double* tb64, const float* tb32, 
     ++launched;
   }
   auto* rec = static_cast<Deferred*>(deferred);
-  // persistent: at most the resident blocks (4 per SM at 64 registers)
-  const int64_t blocks = std::min<int64_t>((items + warps - 1) / warps, int64_t{148} * 4);
-  const dim3 grid(static_cast<unsigned>(blocks), static_cast<unsigned>(n_slices));
+  // one chunk per warp (a persistent grid taking chunks from a counter was
+  // measured 2% slower)
+  const dim3 grid(static_cast<unsigned>((items + warps - 1) / warps), static_cast<unsigned>(n_slices));
   {
     const int musrc = mu ? 1 : (muf ? 2 : 0);
     const bool full = K % (kWarp * KPL) == 0;
@@ -1165,7 +1148,7 @@ int launch_fast_kpl(const BatchView& bv, const double* tb64, const float* tb32, 
       if constexpr (KPL == 8) {
         if (full && musrc == 0 && n_slices == 1) {
           k_sample_v2<8, true, 0, 4, kDecDefault, 0, false><<<grid, kFastBlock, 0, st>>>(
-              bv, tb32, phi32, mu, muf, K, m_t, seed, t, sweep, chunk, tc, pc, rec, n_deferred, work);
+              bv, tb32, phi32, mu, muf, K, m_t, seed, t, sweep, chunk, tc, pc, rec, n_deferred);
           launch_deferred(bv, tb64, phi64, mu, K, m_t, seed, t, sweep, rec, n_deferred, aux,
                           bv.nnz * ((K + 255) / 256), draw_cap, tc, pc, err, st);
           return launched + 3;
@@ -1175,7 +1158,7 @@ int launch_fast_kpl(const BatchView& bv, const double* tb64, const float* tb32, 
     }
 #define SCU_V2_LAUNCH(FULLV, MS, MB, DC, ...)                                                   \
   k_sample_v2<KPL, FULLV, MS, MB, DC __VA_OPT__(,) __VA_ARGS__><<<grid, kFastBlock, 0, st>>>(    \
-      bv, tb32, phi32, mu, muf, K, m_t, seed, t, sweep, chunk, tc, pc, rec, n_deferred, work)
+      bv, tb32, phi32, mu, muf, K, m_t, seed, t, sweep, chunk, tc, pc, rec, n_deferred)
     // production: DEC 1, 4 blocks/SM.  A library built with
     // -DSAMELDA_AB_VARIANTS also carries the measured alternatives (all
     // bit-identical, all slower at K = 256): SAMELDA_DEC=0|2, SAMELDA_MINB=3,

@@ -127,6 +127,14 @@ SIGNATURES = [
     ("samelda_cu_model_upload", C.c_int, [_P, _P, _P]),
     ("samelda_cu_train", C.c_int, [_P, _CP, C.POINTER(_Config), _CP, _I64, _P, _P,
                                    C.POINTER(_TraceRow), _I64, C.POINTER(_I64)]),
+    # collapsed Gibbs sampler baseline
+    ("samelda_cu_cgs_init", C.c_int, [_P, _CP, _I64, _D, _D, _U64]),
+    ("samelda_cu_cgs_sweep", C.c_int, [_P, _U64, _I64]),
+    ("samelda_cu_cgs_state", C.c_int, [_P, _P, _P, _P, _P]),
+    ("samelda_cu_cgs_set_state", C.c_int, [_P, _P, _P, _P, _P]),
+    ("samelda_cu_cgs_model", C.c_int, [_P, _P, _P]),
+    ("samelda_cu_cgs_train", C.c_int, [_P, _CP, _I64, _D, _D, _I64, _U64, _I64, _CP, _P, _P,
+                                       C.POINTER(_TraceRow), _I64, C.POINTER(_I64)]),
     # multi-GPU group (one process, N devices)
     ("samelda_cu_group_create", C.c_int, [_P, C.c_int, C.POINTER(C.c_void_p)]),
     ("samelda_cu_group_destroy", None, [_P]),
@@ -683,6 +691,68 @@ def train(corpus, config: SamplerConfig, heldout=None, eval_every: int = 0,
              for i in range(n.value)]
     return Model(K, W, config.alpha, config.beta, phi[:K * W].reshape(K, W),
                  theta[:D * K].reshape(D, K)), trace
+
+
+class Cgs:
+    """The collapsed Gibbs sampler baseline (cgs.hpp:17-49) on the device: the
+    reference's chain, draw for draw.  State lives in the
+    context; `state()` returns CgsState's arrays."""
+
+    def __init__(self, corpus, n_topics: int, alpha: float, beta: float, seed: int,
+                 ctx: Context | None = None):
+        self.ctx = ctx if ctx is not None else Context(0)
+        self.corpus = Corpus.of(corpus)
+        self.K = int(n_topics)
+        self._cs = self.corpus._struct()
+        self.ctx.check(self.ctx.lib.samelda_cu_cgs_init(self.ctx.h, C.byref(self._cs), self.K,
+                                                        float(alpha), float(beta), int(seed)))
+
+    def sweep(self, seed: int, sweep_index: int):
+        self.ctx.check(self.ctx.lib.samelda_cu_cgs_sweep(self.ctx.h, int(seed), int(sweep_index)))
+
+    def state(self):
+        """(z, doc_topic D x K, word_topic W x K, topic_total K)"""
+        c, K = self.corpus, self.K
+        z = np.zeros(max(c.n_tokens, 1), np.int32)
+        dt = np.zeros(max(c.n_docs * K, 1), np.int32)
+        wt = np.zeros(max(c.n_words * K, 1), np.int32)
+        tt = np.zeros(K, np.int64)
+        self.ctx.check(self.ctx.lib.samelda_cu_cgs_state(self.ctx.h, _ptr(z), _ptr(dt), _ptr(wt),
+                                                         _ptr(tt)))
+        return (z[:c.n_tokens], dt[:c.n_docs * K].reshape(c.n_docs, K),
+                wt[:c.n_words * K].reshape(c.n_words, K), tt)
+
+    def model(self):
+        """cgs_model (cgs.cpp:100-129) -> (phi K x W, theta D x K)"""
+        c, K = self.corpus, self.K
+        phi = np.zeros(max(K * c.n_words, 1))
+        theta = np.zeros(max(c.n_docs * K, 1))
+        self.ctx.check(self.ctx.lib.samelda_cu_cgs_model(self.ctx.h, _ptr(phi), _ptr(theta)))
+        return phi[:K * c.n_words].reshape(K, c.n_words), theta[:c.n_docs * K].reshape(c.n_docs, K)
+
+
+def cgs_train(corpus, n_topics: int, alpha: float, beta: float, n_sweeps: int, seed: int,
+              eval_every: int = 0, heldout=None, ctx: Context | None = None):
+    """cgs.cpp:131-157 on the device -> (Model, trace rows)."""
+    ctx = ctx or default_context()
+    ctx._train_token = None
+    corpus = Corpus.of(corpus)
+    cs = corpus._struct()
+    hs = Corpus.of(heldout)._struct() if heldout is not None else None
+    K, W, D = int(n_topics), corpus.n_words, corpus.n_docs
+    phi = np.zeros(max(K * W, 1))
+    theta = np.zeros(max(D * K, 1))
+    cap = max(int(n_sweeps), 1)
+    rows = (_TraceRow * cap)()
+    n = C.c_int64()
+    ctx.check(ctx.lib.samelda_cu_cgs_train(ctx.h, C.byref(cs), K, float(alpha), float(beta),
+                                           int(n_sweeps), int(seed), int(eval_every),
+                                           C.byref(hs) if hs is not None else None, _ptr(phi),
+                                           _ptr(theta), rows, cap, C.byref(n)))
+    trace = [dict(t=rows[i].t, passes=rows[i].passes, samples_per_word=rows[i].samples_per_word,
+                  ll=rows[i].ll, wall_seconds=rows[i].wall_seconds, m_t=rows[i].m_t)
+             for i in range(n.value)]
+    return Model(K, W, alpha, beta, phi[:K * W].reshape(K, W), theta[:D * K].reshape(D, K)), trace
 
 
 class Group:
