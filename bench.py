@@ -529,7 +529,7 @@ def run_ours(args, cfg):
     # ---- end to end through the public API with host buffers: per step the
     # host batch ids go H2D inside Trainer.period and the batch theta rows
     # (the step's result) come back D2H
-    e2e_steps = max(1, min(args.steps, 10))
+    e2e_steps = max(1, args.steps)
     # a rank owns ~batch_fraction x D_global / N docs of each global batch
     # (the call fails loudly if a buffer is ever too small)
     bmax = int(1.25 * cfg["batch_fraction"] * wl.D_global / (world if scaling == "strong" else 1)) + 64
