@@ -239,10 +239,12 @@ def config_record(cfg, world: int, scaling: str) -> dict:
 
 
 def run_t_max(cfg, args) -> int:
-    """Periods the run performs (warm-up, timed, profiled, end-to-end): the annealing
-    schedule's horizon T (c3: m_t rises over exactly this run)."""
+    """Periods the run performs (warm-up, timed, profiled, end-to-end over as many
+    periods as the timed region): the annealing schedule's horizon T (c3: m_t rises
+    over exactly this run)."""
     prof = max(1, min(args.steps, 10))
-    return max(cfg.get("t_max", 0), args.warmup + args.steps + 2 * prof)
+    e2e = max(1, args.steps)
+    return max(cfg.get("t_max", 0), args.warmup + args.steps + prof + e2e)
 
 
 # --------------------------------------------------------- reference arm

@@ -133,11 +133,31 @@ int launch_fill(double* p, int64_t n, double v, cudaStream_t st);
 int launch_transpose(const double* in, int64_t rows, int64_t cols, double* out,
                       cudaStream_t st);
 
+// per test document: the cells with a nonzero fold (score) half, compacted in
+// cell order at the document's CSR offset, and their number
+struct EvalLists {
+  int32_t* n_fold;   // [n_docs]
+  int32_t* fold_w;   // [nnz] word ids
+  int32_t* fold_c;   // [nnz] fold counts
+  int32_t* n_score;  // [n_docs]
+  int32_t* score_w;
+  int32_t* score_c;
+};
+
 // eval.cpp:99-121: per-doc seeded token split -> fold / score counts per cell
-int launch_eval_split(const int64_t* doc_offsets, const int32_t* counts,
+// (+ the compacted lists when lists.fold_w != nullptr)
+int launch_eval_split(const int64_t* doc_offsets, const int32_t* word_ids, const int32_t* counts,
                        const int64_t* token_offsets, int64_t n_docs, uint64_t seed,
                        int32_t* slots, int32_t* fold_counts, int32_t* score_counts,
-                       cudaStream_t st);
+                       const EvalLists& lists, cudaStream_t st);
+
+// eval.cpp:19-159 at 1e-12 relative (tree-ordered f64 sums, FMA; see
+// kernels_eval.cu k_eval_fold): per-doc fold-in over the compacted lists,
+// scoring, per-doc log p / scored.  Returns -1 when K > 1024 (use
+// launch_eval_docs).
+int launch_eval_fold(const int64_t* doc_offsets, const EvalLists& lists, int64_t n_docs,
+                      const double* phi_wk, int K, double alpha, int sweeps, double* doc_logp,
+                      int64_t* doc_scored, double* theta_out, int* err, cudaStream_t st);
 
 // eval.cpp:19-64 + 125-145: per-doc fold-in then scoring.  theta_out (optional) n_docs x K.
 int launch_eval_docs(const int64_t* doc_offsets, const int32_t* word_ids,

@@ -9,12 +9,18 @@ namespace {
 
 // --------------------------------------------------------------------- eval
 // eval.cpp:99-121, one thread per test document.
+// Besides the per-cell halves it writes each document's compacted fold and
+// score cell lists (word, count of the cells with a nonzero half, in cell
+// order) at the document's CSR offset, with their lengths per document: the
+// inputs of k_eval_fold.  The split depends only on (test corpus, seed), so it
+// runs once per corpus and seed.
 __global__ void k_eval_split(const int64_t* __restrict__ doc_offsets,
+                             const int32_t* __restrict__ word_ids,
                              const int32_t* __restrict__ counts,
                              const int64_t* __restrict__ token_offsets, int64_t n_docs,
                              uint64_t seed, int32_t* __restrict__ slots,
                              int32_t* __restrict__ fold_counts,
-                             int32_t* __restrict__ score_counts) {
+                             int32_t* __restrict__ score_counts, EvalLists lists) {
   const int64_t d = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
   if (d >= n_docs) return;
   const int64_t begin = doc_offsets[d], end = doc_offsets[d + 1];
@@ -38,6 +44,23 @@ __global__ void k_eval_split(const int64_t* __restrict__ doc_offsets,
   for (int64_t i = 0; i < n_tokens; ++i) {
     if (i < n_fold) ++fold_counts[begin + sl[i]]; else ++score_counts[begin + sl[i]];
   }
+  if (lists.fold_w == nullptr) return;
+  int32_t nf = 0, ns = 0;
+  for (int64_t i = begin; i < end; ++i) {
+    const int32_t w = word_ids[i], f = fold_counts[i], s = score_counts[i];
+    if (f != 0) {
+      lists.fold_w[begin + nf] = w;
+      lists.fold_c[begin + nf] = f;
+      ++nf;
+    }
+    if (s != 0) {
+      lists.score_w[begin + ns] = w;
+      lists.score_c[begin + ns] = s;
+      ++ns;
+    }
+  }
+  lists.n_fold[d] = nf;
+  lists.n_score[d] = ns;
 }
 
 __device__ __forceinline__ double warp_max(double v) {
@@ -560,20 +583,335 @@ __global__ void __launch_bounds__(kOrderedBlock) k_ordered_ll(
   *ll_out = __ddiv_rn(total, static_cast<double>(scored));
 }
 
+// ------------------------------------------------------ fast fold-in (k_eval_fold)
+// perword_loglik / fold_in_theta (eval.cpp:19-159) at SURVEY 8(d)'s tolerance
+// (1e-12 relative on ll) instead of the reference's summation order: the
+// exact kernels above are latency-bound on sequential f64 chains (a K-term
+// chain per fold cell and sweep) and re-read every fold row from L2 twice per
+// sweep.  Here one CTA (8 warps) owns a document at a time:
+//   * lane l owns topics k = 64 j + 2 l + {0, 1} (j < NJ), theta in registers;
+//   * a warp takes groups of G consecutive fold cells (G x 2 NJ = 32 row
+//     values per lane); per group: the lane's partial dots (FMA), one
+//     transposed butterfly that leaves cell c's mu on lanes c << SH ..
+//     (G cells for ~log2(32) shuffles, not 5 each), s = count / mu once per
+//     cell, then g_k += s_c phi[w_c][k] (FMA) from the same registers -- one
+//     read of each row per sweep;
+//   * rows stay on chip across the <= 50 sweeps: the first group of every
+//     warp in registers (RES), the next R rows in shared memory (staged once
+//     per document), the rest re-read from L2;
+//   * next_k = alpha + theta_k g_k (FMA); the block reduces the warps' g,
+//     forms the total, theta = next / total (IEEE division) and max |delta|
+//     (eval.cpp:51-61: same stopping rule, same 1 / K start, no sweeps for a
+//     document without cells).
+// Scoring (eval.cpp:125-145) runs the same group dots over the score cells;
+// log p terms and the scored count are summed per document (doc-order
+// reduction stays k_ordered_ll).  Zero-count cells are absent from the lists:
+// the reference adds exactly +0 for them.
+constexpr int kFoldWarps = 8;
+constexpr int kFoldThreads = kFoldWarps * 32;
+
+// v[0..2H) -> after log2(2H) halving stages and the remaining full stages,
+// v[0] on every lane = sum over the lane's group of the partials of cell
+// (lane >> SH); offsets O, O/2, ..., 1
+template <int H, int O>
+__device__ __forceinline__ void fold_tree(double* v, int lane) {
+  if constexpr (H >= 1) {
+    const bool up = (lane & O) != 0;
+#pragma unroll
+    for (int i = 0; i < H; ++i) {
+      const double send = up ? v[i] : v[i + H];
+      const double keep = up ? v[i + H] : v[i];
+      v[i] = keep + __shfl_xor_sync(0xffffffffu, send, O);
+    }
+    if constexpr (O > 1) fold_tree<H / 2, O / 2>(v, lane);
+  } else {
+    v[0] += __shfl_xor_sync(0xffffffffu, v[0], O);
+    if constexpr (O > 1) fold_tree<0, O / 2>(v, lane);
+  }
+}
+
+__device__ __forceinline__ double2 load_pair_g(const double* __restrict__ row, int k, int K,
+                                               bool keven) {
+  if (keven && k + 1 < K) return __ldg(reinterpret_cast<const double2*>(row + k));
+  double2 v;
+  v.x = k < K ? __ldg(row + k) : 0.0;
+  v.y = k + 1 < K ? __ldg(row + k + 1) : 0.0;
+  return v;
+}
+
+__device__ __forceinline__ double warp_sum_d(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+template <int NJ>
+struct FoldShape {
+  static constexpr int G = NJ >= 16 ? 1 : 16 / NJ;  // cells per group: 32 row values per lane
+  static constexpr int LG = G == 1 ? 0 : G == 2 ? 1 : G == 4 ? 2 : G == 8 ? 3 : 4;
+  static constexpr int SH = 5 - LG;                   // lane >> SH = the lane's cell
+  static constexpr int KP = 64 * NJ;                  // padded topics (row stride in smem)
+  static constexpr int TPT = (KP + kFoldThreads - 1) / kFoldThreads;  // topics per thread
+};
+
+template <int NJ>
+__device__ __forceinline__ void fold_dots(const double2 (&th)[NJ],
+                                          const double2 (&r)[FoldShape<NJ>::G][NJ],
+                                          double (&v)[FoldShape<NJ>::G]) {
+#pragma unroll
+  for (int c = 0; c < FoldShape<NJ>::G; ++c) {
+    double a = 0.0, b = 0.0;
+#pragma unroll
+    for (int j = 0; j < NJ; ++j) {
+      a = __fma_rn(th[j].x, r[c][j].x, a);
+      b = __fma_rn(th[j].y, r[c][j].y, b);
+    }
+    v[c] = a + b;
+  }
+}
+
+template <int NJ, bool RES>
+__global__ void __launch_bounds__(kFoldThreads, 1) k_eval_fold(
+    const int64_t* __restrict__ doc_offsets, EvalLists L, int64_t n_docs,
+    const double* __restrict__ phi_wk, int K, double alpha, int sweeps, int R,
+    double* __restrict__ doc_logp, int64_t* __restrict__ doc_scored,
+    double* __restrict__ theta_out, int* __restrict__ err) {
+  using S = FoldShape<NJ>;
+  constexpr int G = S::G, SH = S::SH, KP = S::KP, TPT = S::TPT;
+  extern __shared__ __align__(16) double smem[];
+  double* th_s = smem;                  // [KP] theta (zero past K)
+  double* red = th_s + KP;              // [kFoldWarps][KP] per-warp g
+  double* rows = red + kFoldWarps * KP; // [R][KP] staged fold rows
+  __shared__ double s_tot[kFoldWarps], s_del[kFoldWarps];
+  __shared__ long long s_cnt[kFoldWarps];
+  __shared__ int64_t s_doc;
+  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  const bool keven = (K & 1) == 0;
+  const double inv_k = 1.0 / static_cast<double>(K);
+  const int s0 = RES ? G * kFoldWarps : 0;  // first shared-memory-resident fold cell
+  unsigned long long* next_doc = reinterpret_cast<unsigned long long*>(doc_scored + n_docs);
+
+  for (;;) {
+    __syncthreads();  // the previous document's shared-memory readers are done
+    if (tid == 0) s_doc = static_cast<int64_t>(atomicAdd(next_doc, 1ull));
+    __syncthreads();
+    const int64_t doc = s_doc;
+    if (doc >= n_docs) break;
+    const int64_t base = doc_offsets[doc];
+    const int64_t ncell = doc_offsets[doc + 1] - base;
+    const int F = L.n_fold[doc];
+    const int32_t* __restrict__ fw = L.fold_w + base;
+    const int32_t* __restrict__ fc = L.fold_c + base;
+
+    // stage: shared-memory rows, theta, register-resident group
+    const int Rn = max(0, min(R, F - s0));
+    for (int i = tid; i < Rn * (KP / 2); i += kFoldThreads) {
+      const int f = i / (KP / 2), k = 2 * (i - f * (KP / 2));
+      *reinterpret_cast<double2*>(rows + f * KP + k) =
+          load_pair_g(phi_wk + static_cast<int64_t>(__ldg(fw + s0 + f)) * K, k, K, keven);
+    }
+    for (int t = tid; t < KP; t += kFoldThreads) th_s[t] = t < K ? inv_k : 0.0;
+    double2 th[NJ];
+#pragma unroll
+    for (int j = 0; j < NJ; ++j) {
+      const int k = 64 * j + 2 * lane;
+      th[j].x = k < K ? inv_k : 0.0;
+      th[j].y = k + 1 < K ? inv_k : 0.0;
+    }
+    double2 res[RES ? G : 1][NJ];
+    if constexpr (RES) {
+#pragma unroll
+      for (int c = 0; c < G; ++c) {
+        const int f = G * wid + c;
+        const double* row = phi_wk + static_cast<int64_t>(f < F ? __ldg(fw + f) : 0) * K;
+#pragma unroll
+        for (int j = 0; j < NJ; ++j)
+          res[c][j] = f < F ? load_pair_g(row, 64 * j + 2 * lane, K, keven) : make_double2(0.0, 0.0);
+      }
+    }
+    __syncthreads();
+
+    const int nsw = ncell > 0 ? sweeps : 0;
+    for (int sweep = 0; sweep < nsw; ++sweep) {
+      double2 acc[NJ];
+#pragma unroll
+      for (int j = 0; j < NJ; ++j) acc[j] = make_double2(0.0, 0.0);
+      for (int f0 = G * wid; f0 < F; f0 += G * kFoldWarps) {
+        double2 r[G][NJ];
+        if (RES && f0 < s0) {
+#pragma unroll
+          for (int c = 0; c < G; ++c)
+#pragma unroll
+            for (int j = 0; j < NJ; ++j) r[c][j] = res[RES ? c : 0][j];
+        } else {
+#pragma unroll
+          for (int c = 0; c < G; ++c) {
+            const int f = f0 + c;
+            if (f - s0 < Rn) {  // staged (f < F holds: Rn <= F - s0)
+#pragma unroll
+              for (int j = 0; j < NJ; ++j)
+                r[c][j] = *reinterpret_cast<const double2*>(rows + (f - s0) * KP + 64 * j + 2 * lane);
+            } else if (f < F) {
+              const double* row = phi_wk + static_cast<int64_t>(__ldg(fw + f)) * K;
+#pragma unroll
+              for (int j = 0; j < NJ; ++j) r[c][j] = load_pair_g(row, 64 * j + 2 * lane, K, keven);
+            } else {
+#pragma unroll
+              for (int j = 0; j < NJ; ++j) r[c][j] = make_double2(0.0, 0.0);
+            }
+          }
+        }
+        double v[G];
+        fold_dots<NJ>(th, r, v);
+        fold_tree<G / 2, 16>(v, lane);
+        const int my = f0 + (lane >> SH);
+        const double cnt = my < F ? static_cast<double>(__ldg(fc + my)) : 0.0;
+        // eval.cpp:42-44: a cell with mu <= 0 (or NaN) cannot inform theta
+        const double s = v[0] > 0.0 ? __ddiv_rn(cnt, v[0]) : 0.0;
+#pragma unroll
+        for (int c = 0; c < G; ++c) {
+          const double sc = __shfl_sync(0xffffffffu, s, c << SH);
+#pragma unroll
+          for (int j = 0; j < NJ; ++j) {
+            acc[j].x = __fma_rn(sc, r[c][j].x, acc[j].x);
+            acc[j].y = __fma_rn(sc, r[c][j].y, acc[j].y);
+          }
+        }
+      }
+#pragma unroll
+      for (int j = 0; j < NJ; ++j)
+        *reinterpret_cast<double2*>(red + wid * KP + 64 * j + 2 * lane) = acc[j];
+      __syncthreads();
+      // next_k = alpha + theta_k g_k (eval.cpp:31-49), total, theta = next / total
+      double nx[TPT];
+      double tot = 0.0;
+#pragma unroll
+      for (int q = 0; q < TPT; ++q) {
+        const int t = tid + q * kFoldThreads;
+        nx[q] = 0.0;
+        if (t < K) {
+          double g = red[t];
+#pragma unroll
+          for (int w = 1; w < kFoldWarps; ++w) g += red[w * KP + t];
+          nx[q] = __fma_rn(th_s[t], g, alpha);
+          tot += nx[q];
+        }
+      }
+      tot = warp_sum_d(tot);
+      if (lane == 0) s_tot[wid] = tot;
+      __syncthreads();
+      double total = s_tot[0];
+#pragma unroll
+      for (int w = 1; w < kFoldWarps; ++w) total += s_tot[w];
+      double dl = 0.0;
+#pragma unroll
+      for (int q = 0; q < TPT; ++q) {
+        const int t = tid + q * kFoldThreads;
+        if (t < K) {
+          const double val = __ddiv_rn(nx[q], total);
+          dl = fmax(dl, fabs(val - th_s[t]));
+          th_s[t] = val;
+        }
+      }
+      dl = warp_max(dl);
+      if (lane == 0) s_del[wid] = dl;
+      __syncthreads();
+      double delta = s_del[0];
+#pragma unroll
+      for (int w = 1; w < kFoldWarps; ++w) delta = fmax(delta, s_del[w]);
+#pragma unroll
+      for (int j = 0; j < NJ; ++j)
+        th[j] = *reinterpret_cast<const double2*>(th_s + 64 * j + 2 * lane);
+      if (delta < 1e-12) break;
+    }
+
+    // scoring (eval.cpp:125-145)
+    const int Sn = L.n_score[doc];
+    const int32_t* __restrict__ sw = L.score_w + base;
+    const int32_t* __restrict__ sc = L.score_c + base;
+    double lp = 0.0;
+    long long scored = 0;
+    for (int f0 = G * wid; f0 < Sn; f0 += G * kFoldWarps) {
+      double2 r[G][NJ];
+#pragma unroll
+      for (int c = 0; c < G; ++c) {
+        const int f = f0 + c;
+        const double* row = phi_wk + static_cast<int64_t>(f < Sn ? __ldg(sw + f) : 0) * K;
+#pragma unroll
+        for (int j = 0; j < NJ; ++j)
+          r[c][j] = f < Sn ? load_pair_g(row, 64 * j + 2 * lane, K, keven) : make_double2(0.0, 0.0);
+      }
+      double v[G];
+      fold_dots<NJ>(th, r, v);
+      fold_tree<G / 2, 16>(v, lane);
+      const int my = f0 + (lane >> SH);
+      if ((lane & ((1 << SH) - 1)) == 0 && my < Sn) {
+        const int32_t c = __ldg(sc + my);
+        if (!(v[0] > 0.0)) atomicOr(err, kErrNumerical);
+        lp = __fma_rn(static_cast<double>(c), log(v[0]), lp);
+        scored += c;
+      }
+    }
+    lp = warp_sum_d(lp);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) scored += __shfl_xor_sync(0xffffffffu, scored, o);
+    if (lane == 0) {
+      s_tot[wid] = lp;
+      s_cnt[wid] = scored;
+    }
+    __syncthreads();
+    if (tid == 0) {
+      double t = s_tot[0];
+      long long n = s_cnt[0];
+      for (int w = 1; w < kFoldWarps; ++w) {
+        t += s_tot[w];
+        n += s_cnt[w];
+      }
+      doc_logp[doc] = t;
+      doc_scored[doc] = n;
+    }
+    if (theta_out)
+      for (int t = tid; t < K; t += kFoldThreads) theta_out[doc * K + t] = th_s[t];
+  }
+}
+
+template <int NJ, bool RES>
+int launch_fold(const int64_t* doc_offsets, const EvalLists& L, int64_t n_docs,
+                const double* phi_wk, int K, double alpha, int sweeps, double* doc_logp,
+                int64_t* doc_scored, double* theta_out, int* err, cudaStream_t st) {
+  constexpr int KP = FoldShape<NJ>::KP;
+  int dev = 0, sms = 148, optin = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+  const size_t fixed = static_cast<size_t>(1 + kFoldWarps) * KP * sizeof(double);
+  const size_t budget = static_cast<size_t>(optin) - 1024;  // static shared memory
+  const int R = budget > fixed ? static_cast<int>((budget - fixed) / (KP * sizeof(double))) : 0;
+  const size_t bytes = fixed + static_cast<size_t>(R) * KP * sizeof(double);
+  static std::atomic<unsigned long long> configured{0};
+  smem_opt_in(k_eval_fold<NJ, RES>, static_cast<int>(bytes), configured);
+  const int64_t blocks = min(n_docs, static_cast<int64_t>(sms));
+  // the dynamic document counter lives one past the per-document results
+  cudaMemsetAsync(doc_scored + n_docs, 0, sizeof(int64_t), st);
+  k_eval_fold<NJ, RES><<<static_cast<unsigned>(blocks), kFoldThreads, bytes, st>>>(
+      doc_offsets, L, n_docs, phi_wk, K, alpha, sweeps, R, doc_logp, doc_scored, theta_out, err);
+  return 1;
+}
+
 constexpr size_t kEvalSmemMax = 200 * 1024;
 
 }  // namespace
 
 // ------------------------------------------------------------- launchers
 
-int launch_eval_split(const int64_t* doc_offsets, const int32_t* counts,
+int launch_eval_split(const int64_t* doc_offsets, const int32_t* word_ids, const int32_t* counts,
                       const int64_t* token_offsets, int64_t n_docs, uint64_t seed,
                       int32_t* slots, int32_t* fold_counts, int32_t* score_counts,
-                      cudaStream_t st) {
+                      const EvalLists& lists, cudaStream_t st) {
   if (n_docs == 0) return 0;
-  k_eval_split<<<grid_for(n_docs, 128), 128, 0, st>>>(doc_offsets, counts, token_offsets,
-                                                      n_docs, seed, slots, fold_counts,
-                                                      score_counts);
+  k_eval_split<<<grid_for(n_docs, 128), 128, 0, st>>>(doc_offsets, word_ids, counts,
+                                                      token_offsets, n_docs, seed, slots,
+                                                      fold_counts, score_counts, lists);
   return 1;
 }
 
@@ -650,6 +988,22 @@ int launch_eval_docs(const int64_t* doc_offsets, const int32_t* word_ids,
         doc_logp, doc_scored, theta_out, scratch, err);
   }
   return 1;
+}
+
+int launch_eval_fold(const int64_t* doc_offsets, const EvalLists& lists, int64_t n_docs,
+                     const double* phi_wk, int K, double alpha, int sweeps, double* doc_logp,
+                     int64_t* doc_scored, double* theta_out, int* err, cudaStream_t st) {
+  if (n_docs == 0) return 0;
+#define SCU_FOLD(NJ, RES) \
+  launch_fold<NJ, RES>(doc_offsets, lists, n_docs, phi_wk, K, alpha, sweeps, doc_logp, doc_scored, \
+                       theta_out, err, st)
+  if (K <= 64) return SCU_FOLD(1, true);
+  if (K <= 128) return SCU_FOLD(2, true);
+  if (K <= 256) return SCU_FOLD(4, true);
+  if (K <= 512) return SCU_FOLD(8, false);
+  if (K <= 1024) return SCU_FOLD(16, false);
+#undef SCU_FOLD
+  return -1;  // K > 1024: the exact kernels
 }
 
 int launch_ordered_ll(const double* doc_logp, const int64_t* doc_scored, int64_t n_docs,

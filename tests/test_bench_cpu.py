@@ -41,3 +41,17 @@ def test_reference_arm_expected_config_unavailable():
     assert out.returncode == 0
     line = json.loads(out.stdout.strip().splitlines()[-1])
     assert line["impl"] == "reference" and "unavailable" in line
+
+
+def test_run_horizon_covers_every_period():
+    """The annealing horizon T must cover warm-up + timed + profiled + end-to-end
+    periods (anneal_m rejects t > T): the driver's --steps 20 run once failed here."""
+    import argparse
+    sys.path.insert(0, ROOT)
+    import bench
+    for warmup, steps in ((3, 10), (5, 20), (1, 1), (3, 50)):
+        args = argparse.Namespace(warmup=warmup, steps=steps)
+        prof = max(1, min(steps, 10))
+        used = warmup + steps + prof + max(1, steps)
+        for name in ("nytimes", "c3"):
+            assert bench.run_t_max(bench.CONFIGS[name], args) >= used
