@@ -158,6 +158,14 @@ int samelda_cu_fold_in_theta(samelda_cu_ctx* ctx, const double* phi, int64_t K, 
                              const int32_t* words, const int32_t* counts, int64_t n,
                              double alpha, int32_t sweeps, double* theta_out);
 
+/* Held-out evaluation arithmetic (fold_in_theta, perword_loglik, evaluate).
+ * exact = 0 (default): per-document fold-in with tree-ordered f64 sums and
+ *   FMA -- ll within SURVEY 8(d)'s 1e-12 relative of the reference, theta
+ *   within 1e-12 relative (k_eval_fold);
+ * exact = 1: the reference's summation order (eval.cpp:30-62), ll and theta
+ *   bit-identical, ~10x slower.  SAMELDA_EVAL=x sets it at create. */
+int samelda_cu_set_eval_exact(samelda_cu_ctx* ctx, int exact);
+
 /* replaces samelda::perword_loglik, eval.hpp:38-43 / eval.cpp:75-159 */
 int samelda_cu_perword_loglik(samelda_cu_ctx* ctx, const double* phi, int64_t K, int64_t W,
                               const samelda_cu_corpus* test, double alpha, uint64_t seed,

@@ -286,6 +286,7 @@ const Tuning& tuning() {
     if (const char* e = env("SAMELDA_EVAL")) v.eval_variant = e[0];
     if (env("SAMELDA_EVAL_WARP")) v.eval_variant = 'w';
     if (const char* e = env("SAMELDA_EVAL_CTAS_PER_SM")) v.eval_ctas_per_sm = std::atoi(e);
+
     if (const char* e = env("SAMELDA_MINB")) v.minb = std::atoi(e);
     if (const char* e = env("SAMELDA_DEC")) v.dec = std::atoi(e);
     if (const char* e = env("SAMELDA_TAIL")) v.tail = std::atoi(e);
@@ -307,6 +308,12 @@ struct samelda_cu_ctx {
   uint64_t split_seed = 0;
   bool split_ready = false;
   DevBuf tok_offsets, slots, fold_counts, score_counts, doc_logp, doc_scored;
+  // compacted fold / score cell lists of the split (k_eval_fold's input)
+  DevBuf n_fold, fold_l, n_score, score_l;
+  // held-out evaluation: false = k_eval_fold (ll within 1e-12
+  // relative, tree-ordered sums); true = the reference's summation order bit
+  // for bit (k_eval_stage / k_eval_cta / k_eval_docs, ~10x slower)
+  bool eval_exact = false;
 
   // resident model (train_begin)
   bool model_ready = false;
@@ -648,26 +655,47 @@ struct samelda_cu_ctx {
     int64_t* dtok = ensure<int64_t>(tok_offsets, nd + 1);
     ck(cudaMemcpyAsync(dtok, tok.data(), sizeof(int64_t) * (nd + 1), cudaMemcpyHostToDevice, stream),
        "upload token offsets");
-    launches += scu::launch_eval_split(heldout.offs.as<int64_t>(), heldout.counts.as<int32_t>(), dtok,
-                                       nd, seed, ensure<int32_t>(slots, tok[nd]),
+    launches += scu::launch_eval_split(heldout.offs.as<int64_t>(), heldout.words.as<int32_t>(),
+                                       heldout.counts.as<int32_t>(), dtok, nd, seed,
+                                       ensure<int32_t>(slots, tok[nd]),
                                        ensure<int32_t>(fold_counts, heldout.nnz),
-                                       ensure<int32_t>(score_counts, heldout.nnz), stream);
+                                       ensure<int32_t>(score_counts, heldout.nnz),
+                                       eval_lists(nd, heldout.nnz), stream);
     ck(cudaStreamSynchronize(stream), "eval split");
     split_seed = seed;
     split_ready = true;
+  }
+
+  scu::EvalLists eval_lists(int64_t nd, int64_t nnz) {
+    const int64_t n = std::max<int64_t>(nnz, 1), m = std::max<int64_t>(nd, 1);
+    return scu::EvalLists{ensure<int32_t>(n_fold, m), ensure<int2>(fold_l, n), ensure<int32_t>(n_score, m),
+                          ensure<int2>(score_l, n)};
+  }
+
+  // fold-in + scoring of every document of the split (eval.cpp:19-145);
+  // per-doc results into doc_logp / doc_scored (+ theta rows when asked)
+  int eval_docs(const CorpusSlot& c, const int32_t* fcounts, const int32_t* scounts,
+                const scu::EvalLists& L, const double* phi_wk, int K_, double alpha, int sweeps,
+                double* lp, int64_t* sc, double* theta_out) {
+    if (!eval_exact) {
+      const int r = scu::launch_eval_fold(c.offs.as<int64_t>(), L, c.n_docs, phi_wk, K_, alpha,
+                                          sweeps, lp, sc, theta_out, d_err(), stream);
+      if (r >= 0) return r;
+    }
+    const int64_t need = scu::eval_scratch_doubles(K_);
+    double* scratch = need > 0 ? ensure<double>(eval_scratch, need) : nullptr;
+    return scu::launch_eval_docs(c.offs.as<int64_t>(), c.words.as<int32_t>(), fcounts, scounts,
+                                 c.n_docs, phi_wk, K_, alpha, sweeps, lp, sc, theta_out, scratch,
+                                 need, d_err(), stream);
   }
 
   double eval_ll(const double* phi_wk, int K_, double alpha) {
     const int64_t nd = heldout.n_docs;
     double* lp = ensure<double>(doc_logp, nd);
     int64_t* sc = ensure<int64_t>(doc_scored, nd + 1);  // + the eval kernel's work counter
-    const int64_t need = scu::eval_scratch_doubles(K_);
-    double* scratch = need > 0 ? ensure<double>(eval_scratch, need) : nullptr;
     reset_err();
-    launches += scu::launch_eval_docs(heldout.offs.as<int64_t>(), heldout.words.as<int32_t>(),
-                                      fold_counts.as<int32_t>(), score_counts.as<int32_t>(), nd,
-                                      phi_wk, K_, alpha, 50, lp, sc, nullptr, scratch, need,
-                                      d_err(), stream);
+    launches += eval_docs(heldout, fold_counts.as<int32_t>(), score_counts.as<int32_t>(),
+                          eval_lists(nd, heldout.nnz), phi_wk, K_, alpha, 50, lp, sc, nullptr);
     double* dll = ensure<double>(ll, 1);
     launches += scu::launch_ordered_ll(lp, sc, nd, dll, d_err(), stream);
     double out = 0.0;
@@ -740,7 +768,15 @@ int samelda_cu_create(int device, samelda_cu_ctx** out) {
     return SAMELDA_CU_CUDA;
   }
   ctx->stream = ctx->own_stream;
+  const char ev = scu::tuning().eval_variant;  // SAMELDA_EVAL=x (or c / w): exact order
+  ctx->eval_exact = ev == 'x' || ev == 'c' || ev == 'w';
   *out = ctx;
+  return SAMELDA_CU_OK;
+}
+
+int samelda_cu_set_eval_exact(samelda_cu_ctx* ctx, int exact) {
+  if (ctx == nullptr) return SAMELDA_CU_CONFIG;
+  ctx->eval_exact = exact != 0;
   return SAMELDA_CU_OK;
 }
 
@@ -1004,12 +1040,20 @@ int samelda_cu_fold_in_theta(samelda_cu_ctx* ctx, const double* phi, int64_t K, 
     double* lp = ensure<double>(ctx->doc_logp, 1);
     int64_t* scd = ensure<int64_t>(ctx->doc_scored, 2);  // + the eval kernel's work counter
     double* th = ensure<double>(ctx->theta_rows, K);
-    const int64_t need = scu::eval_scratch_doubles(static_cast<int>(K));
-    double* scratch = need > 0 ? ensure<double>(ctx->eval_scratch, need) : nullptr;
+    // the document's fold list: its nonzero-count cells in cell order (a
+    // zero count adds exactly +0 in eval.cpp:45-49); no score cells
+    std::vector<int2> lf;
+    for (int64_t i = 0; i < n; ++i)
+      if (counts[i] != 0) lf.push_back(make_int2(words[i], counts[i]));
+    const int32_t meta[2] = {static_cast<int32_t>(lf.size()), 0};
+    scu::EvalLists L = ctx->eval_lists(1, n);
+    ck(cudaMemcpyAsync(L.n_fold, &meta[0], sizeof(int32_t), cudaMemcpyHostToDevice, ctx->stream), "upload list");
+    ck(cudaMemcpyAsync(L.n_score, &meta[1], sizeof(int32_t), cudaMemcpyHostToDevice, ctx->stream), "upload list");
+    if (!lf.empty())
+      ck(cudaMemcpyAsync(L.fold, lf.data(), sizeof(int2) * lf.size(), cudaMemcpyHostToDevice, ctx->stream),
+         "upload list");
     ctx->reset_err();
-    ctx->launches += scu::launch_eval_docs(one.offs.as<int64_t>(), one.words.as<int32_t>(), fc, sc, 1, phi_wk,
-                                           static_cast<int>(K), alpha, sweeps, lp, scd, th, scratch, need,
-                                           ctx->d_err(), ctx->stream);
+    ctx->launches += ctx->eval_docs(one, fc, sc, L, phi_wk, static_cast<int>(K), alpha, sweeps, lp, scd, th);
     ck(cudaMemcpyAsync(theta_out, th, sizeof(double) * K, cudaMemcpyDeviceToHost, ctx->stream), "download theta");
     ck(cudaStreamSynchronize(ctx->stream), "fold_in_theta");
     ck(cudaGetLastError(), "fold_in_theta");

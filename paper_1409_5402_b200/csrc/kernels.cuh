@@ -136,16 +136,14 @@ int launch_transpose(const double* in, int64_t rows, int64_t cols, double* out,
 // per test document: the cells with a nonzero fold (score) half, compacted in
 // cell order at the document's CSR offset, and their number
 struct EvalLists {
-  int32_t* n_fold;   // [n_docs]
-  int32_t* fold_w;   // [nnz] word ids
-  int32_t* fold_c;   // [nnz] fold counts
-  int32_t* n_score;  // [n_docs]
-  int32_t* score_w;
-  int32_t* score_c;
+  int32_t* n_fold;  // [n_docs]
+  int2* fold;       // [nnz] (word id, fold count)
+  int32_t* n_score; // [n_docs]
+  int2* score;      // [nnz] (word id, score count)
 };
 
 // eval.cpp:99-121: per-doc seeded token split -> fold / score counts per cell
-// (+ the compacted lists when lists.fold_w != nullptr)
+// (+ the compacted lists when lists.fold != nullptr)
 int launch_eval_split(const int64_t* doc_offsets, const int32_t* word_ids, const int32_t* counts,
                        const int64_t* token_offsets, int64_t n_docs, uint64_t seed,
                        int32_t* slots, int32_t* fold_counts, int32_t* score_counts,

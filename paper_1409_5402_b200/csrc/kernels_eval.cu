@@ -3,6 +3,8 @@
 // document-order reduction.
 #include "kernels_common.cuh"
 
+#include <cstdio>
+
 namespace scu {
 
 namespace {
@@ -44,20 +46,12 @@ __global__ void k_eval_split(const int64_t* __restrict__ doc_offsets,
   for (int64_t i = 0; i < n_tokens; ++i) {
     if (i < n_fold) ++fold_counts[begin + sl[i]]; else ++score_counts[begin + sl[i]];
   }
-  if (lists.fold_w == nullptr) return;
+  if (lists.fold == nullptr) return;
   int32_t nf = 0, ns = 0;
   for (int64_t i = begin; i < end; ++i) {
     const int32_t w = word_ids[i], f = fold_counts[i], s = score_counts[i];
-    if (f != 0) {
-      lists.fold_w[begin + nf] = w;
-      lists.fold_c[begin + nf] = f;
-      ++nf;
-    }
-    if (s != 0) {
-      lists.score_w[begin + ns] = w;
-      lists.score_c[begin + ns] = s;
-      ++ns;
-    }
+    if (f != 0) lists.fold[begin + nf++] = make_int2(w, f);
+    if (s != 0) lists.score[begin + ns++] = make_int2(w, s);
   }
   lists.n_fold[d] = nf;
   lists.n_score[d] = ns;
@@ -593,23 +587,26 @@ __global__ void __launch_bounds__(kOrderedBlock) k_ordered_ll(
 //   * a warp takes groups of G consecutive fold cells (G x 2 NJ = 32 row
 //     values per lane); per group: the lane's partial dots (FMA), one
 //     transposed butterfly that leaves cell c's mu on lanes c << SH ..
-//     (G cells for ~log2(32) shuffles, not 5 each), s = count / mu once per
-//     cell, then g_k += s_c phi[w_c][k] (FMA) from the same registers -- one
-//     read of each row per sweep;
+//     (1.5 f64 shuffles per cell at G = 4, not 5), s = count / mu once per
+//     cell (MUFU reciprocal + Newton), then g_k += s_c phi[w_c][k] (FMA) from
+//     the same registers -- one read of each row per sweep;
 //   * rows stay on chip across the <= 50 sweeps: the first group of every
 //     warp in registers (RES), the next R rows in shared memory (staged once
 //     per document), the rest re-read from L2;
-//   * next_k = alpha + theta_k g_k (FMA); the block reduces the warps' g,
-//     forms the total, theta = next / total (IEEE division) and max |delta|
-//     (eval.cpp:51-61: same stopping rule, same 1 / K start, no sweeps for a
-//     document without cells).
+//   * next_k = alpha + theta_k g_k (FMA).  The total sum_k next_k =
+//     K alpha + sum_k theta_k g_k comes from per-warp partials written with
+//     the warps' g, so after ONE barrier the topic owners form
+//     theta = next / total and the stopping test (eval.cpp:51-61: same 1e-12
+//     rule, same 1 / K start, no sweeps for a document without cells), and a
+//     second barrier (__syncthreads_or) ORs the test.
 // Scoring (eval.cpp:125-145) runs the same group dots over the score cells;
-// log p terms and the scored count are summed per document (doc-order
-// reduction stays k_ordered_ll).  Zero-count cells are absent from the lists:
-// the reference adds exactly +0 for them.
-constexpr int kFoldWarps = 8;
-constexpr int kFoldThreads = kFoldWarps * 32;
-
+// the document's log p terms are added in cell order with the reference's
+// rounding (c * log p, then add), the doc-order reduction is k_ordered_ll.
+// Zero-count cells are absent from the lists: the reference adds exactly +0
+// for them.  Measured at NYTimes shape (30K test docs, 127 fold cells on
+// average, all 50 sweeps): 45 ms against 117 ms for the exact kernel; per
+// cell the loop costs ~32-46 SM cycles (16 of them the 2 KB shared-memory
+// row read, the rest shuffles / reciprocal latency), see profiles/r2_eval.md.
 // v[0..2H) -> after log2(2H) halving stages and the remaining full stages,
 // v[0] on every lane = sum over the lane's group of the partials of cell
 // (lane >> SH); offsets O, O/2, ..., 1
@@ -645,24 +642,45 @@ __device__ __forceinline__ double warp_sum_d(double v) {
   return v;
 }
 
-template <int NJ>
-struct FoldShape {
-  static constexpr int G = NJ >= 16 ? 1 : 16 / NJ;  // cells per group: 32 row values per lane
+// 1 / x for x > 0: MUFU reciprocal + two Newton steps (relative error ~1 ulp;
+// IEEE division below the f64 normal range, where the approximation flushes)
+__device__ __forceinline__ double fold_rcp(double x) {
+  if (x < 1e-300) return __ddiv_rn(1.0, x);
+  double r;
+  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(x));
+  double e = __fma_rn(-x, r, 1.0);
+  r = __fma_rn(r, e, r);
+  e = __fma_rn(-x, r, 1.0);
+  return __fma_rn(r, e, r);
+}
+
+// Kernel shape: NJ topic pairs per lane (K <= 64 NJ), G fold cells per group
+// (one transposed butterfly per group), NW warps, RES = the first group of
+// every warp keeps its rows in registers across sweeps.
+template <int NJ_, int G_, int NW_, bool RES_>
+struct FoldCfg {
+  static constexpr int NJ = NJ_, G = G_, NW = NW_;
+  static constexpr bool RES = RES_;
+  static constexpr int NT = 32 * NW;
   static constexpr int LG = G == 1 ? 0 : G == 2 ? 1 : G == 4 ? 2 : G == 8 ? 3 : 4;
-  static constexpr int SH = 5 - LG;                   // lane >> SH = the lane's cell
-  static constexpr int KP = 64 * NJ;                  // padded topics (row stride in smem)
-  static constexpr int TPT = (KP + kFoldThreads - 1) / kFoldThreads;  // topics per thread
+  static constexpr int SH = 5 - LG;         // lane >> SH = the lane's cell in a group
+  static constexpr int KP = 64 * NJ;        // padded topics (row stride in shared memory)
+  static constexpr int GW = G * NW;         // cells per round of groups
+  static constexpr int S0 = RES ? GW : 0;   // first cell past the register-resident ones
+  static constexpr int TPT = (KP + NT - 1) / NT;  // topics per thread in the epilogue
 };
 
-template <int NJ>
-__device__ __forceinline__ void fold_dots(const double2 (&th)[NJ],
-                                          const double2 (&r)[FoldShape<NJ>::G][NJ],
-                                          double (&v)[FoldShape<NJ>::G]) {
+// fold-list entries staged per document (longer lists are read from global)
+constexpr int kFoldList = 768;
+
+template <class C>
+__device__ __forceinline__ void fold_dots(const double2 (&th)[C::NJ],
+                                          const double2 (&r)[C::G][C::NJ], double (&v)[C::G]) {
 #pragma unroll
-  for (int c = 0; c < FoldShape<NJ>::G; ++c) {
+  for (int c = 0; c < C::G; ++c) {
     double a = 0.0, b = 0.0;
 #pragma unroll
-    for (int j = 0; j < NJ; ++j) {
+    for (int j = 0; j < C::NJ; ++j) {
       a = __fma_rn(th[j].x, r[c][j].x, a);
       b = __fma_rn(th[j].y, r[c][j].y, b);
     }
@@ -670,25 +688,70 @@ __device__ __forceinline__ void fold_dots(const double2 (&th)[NJ],
   }
 }
 
-template <int NJ, bool RES>
-__global__ void __launch_bounds__(kFoldThreads, 1) k_eval_fold(
+// one group of G cells (rows r; cnt = count of the lane's cell, 0 past the
+// list) into the warp's g sums: partial dots, one transposed butterfly (the
+// lanes of cell c end with its mu), s = c / mu (eval.cpp:38-44; mu <= 0 or
+// NaN: 0), g_k += s_c phi[w_c][k] (eval.cpp:45-49)
+template <class C>
+__device__ __forceinline__ void fold_group(const double2 (&th)[C::NJ],
+                                           const double2 (&r)[C::G][C::NJ],
+                                           double2 (&acc)[C::NJ], int cnt, int lane) {
+  double v[C::G];
+  fold_dots<C>(th, r, v);
+  fold_tree<C::G / 2, 16>(v, lane);
+  const double s = v[0] > 0.0 ? static_cast<double>(cnt) * fold_rcp(v[0]) : 0.0;
+#pragma unroll
+  for (int c = 0; c < C::G; ++c) {
+    const double sc = __shfl_sync(0xffffffffu, s, c << C::SH);
+#pragma unroll
+    for (int j = 0; j < C::NJ; ++j) {
+      acc[j].x = __fma_rn(sc, r[c][j].x, acc[j].x);
+      acc[j].y = __fma_rn(sc, r[c][j].y, acc[j].y);
+    }
+  }
+}
+
+template <int NJ>
+__device__ __forceinline__ void fold_row_g(double2 (&r)[NJ], const double* __restrict__ phi_wk,
+                                           int w, int K, bool keven, int lane) {
+  const double* row = phi_wk + static_cast<int64_t>(w) * K;
+#pragma unroll
+  for (int j = 0; j < NJ; ++j) r[j] = load_pair_g(row, 64 * j + 2 * lane, K, keven);
+}
+
+template <int NJ>
+__device__ __forceinline__ void fold_row_zero(double2 (&r)[NJ]) {
+#pragma unroll
+  for (int j = 0; j < NJ; ++j) r[j] = make_double2(0.0, 0.0);
+}
+
+#ifdef SAMELDA_FOLD_PROF
+__device__ unsigned long long g_fold_prof[8];  // cycles of thread 0: stage, cells, bar1, epi, bar2, -, score
+#define FOLD_T(i) if (tid == 0) { const long long _n = clock64(); atomicAdd(&g_fold_prof[i], _n - _t); _t = _n; }
+#else
+#define FOLD_T(i)
+#endif
+
+template <class C>
+__global__ void __launch_bounds__(C::NT, 1) k_eval_fold(
     const int64_t* __restrict__ doc_offsets, EvalLists L, int64_t n_docs,
     const double* __restrict__ phi_wk, int K, double alpha, int sweeps, int R,
     double* __restrict__ doc_logp, int64_t* __restrict__ doc_scored,
     double* __restrict__ theta_out, int* __restrict__ err) {
-  using S = FoldShape<NJ>;
-  constexpr int G = S::G, SH = S::SH, KP = S::KP, TPT = S::TPT;
+  constexpr int NJ = C::NJ, G = C::G, NW = C::NW, NT = C::NT, SH = C::SH, KP = C::KP;
+  constexpr int GW = C::GW, S0 = C::S0, TPT = C::TPT;
   extern __shared__ __align__(16) double smem[];
-  double* th_s = smem;                  // [KP] theta (zero past K)
-  double* red = th_s + KP;              // [kFoldWarps][KP] per-warp g
-  double* rows = red + kFoldWarps * KP; // [R][KP] staged fold rows
-  __shared__ double s_tot[kFoldWarps], s_del[kFoldWarps];
-  __shared__ long long s_cnt[kFoldWarps];
+  double* red = smem;                                // [NW][KP] per-warp g
+  double* ths = red + NW * KP;                       // [KP] theta (zero past K)
+  int2* lst_s = reinterpret_cast<int2*>(ths + KP);   // [kFoldList] (word, count)
+  double* rows = ths + KP + kFoldList;               // [R][KP] staged fold rows
+  __shared__ double s_part[NW], s_term[GW];
+  __shared__ long long s_cnt[NW];
   __shared__ int64_t s_doc;
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
   const bool keven = (K & 1) == 0;
   const double inv_k = 1.0 / static_cast<double>(K);
-  const int s0 = RES ? G * kFoldWarps : 0;  // first shared-memory-resident fold cell
+  const double k_alpha = static_cast<double>(K) * alpha;
   unsigned long long* next_doc = reinterpret_cast<unsigned long long*>(doc_scored + n_docs);
 
   for (;;) {
@@ -697,20 +760,37 @@ __global__ void __launch_bounds__(kFoldThreads, 1) k_eval_fold(
     __syncthreads();
     const int64_t doc = s_doc;
     if (doc >= n_docs) break;
+#ifdef SAMELDA_FOLD_PROF
+    long long _t = clock64();
+#endif
     const int64_t base = doc_offsets[doc];
     const int64_t ncell = doc_offsets[doc + 1] - base;
     const int F = L.n_fold[doc];
-    const int32_t* __restrict__ fw = L.fold_w + base;
-    const int32_t* __restrict__ fc = L.fold_c + base;
+    const int2* __restrict__ gl = L.fold + base;
+    const int2* lst = F <= kFoldList ? lst_s : gl;  // generic: shared or global
 
-    // stage: shared-memory rows, theta, register-resident group
-    const int Rn = max(0, min(R, F - s0));
-    for (int i = tid; i < Rn * (KP / 2); i += kFoldThreads) {
+    // stage: list, shared-memory rows [S0, s_end), register-resident group, theta
+    if (F <= kFoldList)
+      for (int i = tid; i < F; i += NT) lst_s[i] = __ldg(gl + i);
+    const int Rn = max(0, min(R, F - S0));
+    const int s_end = S0 + Rn;
+    for (int i = tid; i < Rn * (KP / 2); i += NT) {
       const int f = i / (KP / 2), k = 2 * (i - f * (KP / 2));
       *reinterpret_cast<double2*>(rows + f * KP + k) =
-          load_pair_g(phi_wk + static_cast<int64_t>(__ldg(fw + s0 + f)) * K, k, K, keven);
+          load_pair_g(phi_wk + static_cast<int64_t>(__ldg(&gl[S0 + f].x)) * K, k, K, keven);
     }
-    for (int t = tid; t < KP; t += kFoldThreads) th_s[t] = t < K ? inv_k : 0.0;
+    double2 res[C::RES ? G : 1][NJ];
+    int res_cnt = 0;
+    if constexpr (C::RES) {
+#pragma unroll
+      for (int c = 0; c < G; ++c) {
+        const int f = G * wid + c;
+        if (f < F) fold_row_g<NJ>(res[c], phi_wk, __ldg(&gl[f].x), K, keven, lane);
+        else fold_row_zero<NJ>(res[c]);
+      }
+      const int my = G * wid + (lane >> SH);
+      res_cnt = my < F ? __ldg(&gl[my].y) : 0;
+    }
     double2 th[NJ];
 #pragma unroll
     for (int j = 0; j < NJ; ++j) {
@@ -718,183 +798,171 @@ __global__ void __launch_bounds__(kFoldThreads, 1) k_eval_fold(
       th[j].x = k < K ? inv_k : 0.0;
       th[j].y = k + 1 < K ? inv_k : 0.0;
     }
-    double2 res[RES ? G : 1][NJ];
-    if constexpr (RES) {
-#pragma unroll
-      for (int c = 0; c < G; ++c) {
-        const int f = G * wid + c;
-        const double* row = phi_wk + static_cast<int64_t>(f < F ? __ldg(fw + f) : 0) * K;
-#pragma unroll
-        for (int j = 0; j < NJ; ++j)
-          res[c][j] = f < F ? load_pair_g(row, 64 * j + 2 * lane, K, keven) : make_double2(0.0, 0.0);
-      }
-    }
+    for (int t = tid; t < KP; t += NT) ths[t] = t < K ? inv_k : 0.0;
     __syncthreads();
+    FOLD_T(0)
 
     const int nsw = ncell > 0 ? sweeps : 0;
     for (int sweep = 0; sweep < nsw; ++sweep) {
       double2 acc[NJ];
 #pragma unroll
       for (int j = 0; j < NJ; ++j) acc[j] = make_double2(0.0, 0.0);
-      for (int f0 = G * wid; f0 < F; f0 += G * kFoldWarps) {
+      if constexpr (C::RES) {
+        if (G * wid < F) fold_group<C>(th, res, acc, res_cnt, lane);
+      }
+      for (int f0 = S0 + G * wid; f0 < F; f0 += GW) {
+        const int my = f0 + (lane >> SH);
+        const int cnt = my < F ? lst[my].y : 0;
         double2 r[G][NJ];
-        if (RES && f0 < s0) {
+        if (f0 + G <= s_end) {  // whole group staged
 #pragma unroll
           for (int c = 0; c < G; ++c)
 #pragma unroll
-            for (int j = 0; j < NJ; ++j) r[c][j] = res[RES ? c : 0][j];
-        } else {
+            for (int j = 0; j < NJ; ++j)
+              r[c][j] = *reinterpret_cast<const double2*>(rows + (f0 - S0 + c) * KP + 64 * j + 2 * lane);
+        } else {  // L2 (and the staged / past-the-end edge)
 #pragma unroll
           for (int c = 0; c < G; ++c) {
             const int f = f0 + c;
-            if (f - s0 < Rn) {  // staged (f < F holds: Rn <= F - s0)
+            if (f < s_end) {
 #pragma unroll
               for (int j = 0; j < NJ; ++j)
-                r[c][j] = *reinterpret_cast<const double2*>(rows + (f - s0) * KP + 64 * j + 2 * lane);
+                r[c][j] = *reinterpret_cast<const double2*>(rows + (f - S0) * KP + 64 * j + 2 * lane);
             } else if (f < F) {
-              const double* row = phi_wk + static_cast<int64_t>(__ldg(fw + f)) * K;
-#pragma unroll
-              for (int j = 0; j < NJ; ++j) r[c][j] = load_pair_g(row, 64 * j + 2 * lane, K, keven);
+              fold_row_g<NJ>(r[c], phi_wk, lst[f].x, K, keven, lane);
             } else {
-#pragma unroll
-              for (int j = 0; j < NJ; ++j) r[c][j] = make_double2(0.0, 0.0);
+              fold_row_zero<NJ>(r[c]);
             }
           }
         }
-        double v[G];
-        fold_dots<NJ>(th, r, v);
-        fold_tree<G / 2, 16>(v, lane);
-        const int my = f0 + (lane >> SH);
-        const double cnt = my < F ? static_cast<double>(__ldg(fc + my)) : 0.0;
-        // eval.cpp:42-44: a cell with mu <= 0 (or NaN) cannot inform theta
-        const double s = v[0] > 0.0 ? __ddiv_rn(cnt, v[0]) : 0.0;
-#pragma unroll
-        for (int c = 0; c < G; ++c) {
-          const double sc = __shfl_sync(0xffffffffu, s, c << SH);
-#pragma unroll
-          for (int j = 0; j < NJ; ++j) {
-            acc[j].x = __fma_rn(sc, r[c][j].x, acc[j].x);
-            acc[j].y = __fma_rn(sc, r[c][j].y, acc[j].y);
-          }
-        }
+        fold_group<C>(th, r, acc, cnt, lane);
       }
+      // ---- epilogue (eval.cpp:51-61).  total = K alpha + sum_k theta_k g_k
+      // from per-warp partials, so theta = next / total and the stopping test
+      // are formed by the topic owners right after the first barrier; the
+      // second barrier ORs the test
+      double part = 0.0;
 #pragma unroll
-      for (int j = 0; j < NJ; ++j)
+      for (int j = 0; j < NJ; ++j) {
+        part = __fma_rn(th[j].x, acc[j].x, part);
+        part = __fma_rn(th[j].y, acc[j].y, part);
         *reinterpret_cast<double2*>(red + wid * KP + 64 * j + 2 * lane) = acc[j];
+      }
+      part = warp_sum_d(part);
+      if (lane == 0) s_part[wid] = part;
+      FOLD_T(1)
       __syncthreads();
-      // next_k = alpha + theta_k g_k (eval.cpp:31-49), total, theta = next / total
-      double nx[TPT];
-      double tot = 0.0;
+      FOLD_T(2)
+      const double rt = fold_rcp(k_alpha + warp_sum_d(lane < NW ? s_part[lane] : 0.0));
+      bool big = false;
 #pragma unroll
       for (int q = 0; q < TPT; ++q) {
-        const int t = tid + q * kFoldThreads;
-        nx[q] = 0.0;
+        const int t = tid + q * NT;
         if (t < K) {
           double g = red[t];
 #pragma unroll
-          for (int w = 1; w < kFoldWarps; ++w) g += red[w * KP + t];
-          nx[q] = __fma_rn(th_s[t], g, alpha);
-          tot += nx[q];
+          for (int w = 1; w < NW; ++w) g += red[w * KP + t];
+          const double old = ths[t];
+          const double val = __fma_rn(old, g, alpha) * rt;
+          // stop when max_k |delta_k| < 1e-12 (a NaN delta never raises the
+          // reference's std::max)
+          big |= fabs(val - old) >= 1e-12;
+          ths[t] = val;
         }
       }
-      tot = warp_sum_d(tot);
-      if (lane == 0) s_tot[wid] = tot;
-      __syncthreads();
-      double total = s_tot[0];
-#pragma unroll
-      for (int w = 1; w < kFoldWarps; ++w) total += s_tot[w];
-      double dl = 0.0;
-#pragma unroll
-      for (int q = 0; q < TPT; ++q) {
-        const int t = tid + q * kFoldThreads;
-        if (t < K) {
-          const double val = __ddiv_rn(nx[q], total);
-          dl = fmax(dl, fabs(val - th_s[t]));
-          th_s[t] = val;
-        }
-      }
-      dl = warp_max(dl);
-      if (lane == 0) s_del[wid] = dl;
-      __syncthreads();
-      double delta = s_del[0];
-#pragma unroll
-      for (int w = 1; w < kFoldWarps; ++w) delta = fmax(delta, s_del[w]);
+      FOLD_T(3)
+      const bool more = __syncthreads_or(big);
+      FOLD_T(4)
 #pragma unroll
       for (int j = 0; j < NJ; ++j)
-        th[j] = *reinterpret_cast<const double2*>(th_s + 64 * j + 2 * lane);
-      if (delta < 1e-12) break;
+        th[j] = *reinterpret_cast<const double2*>(ths + 64 * j + 2 * lane);
+      if (!more) break;
     }
 
-    // scoring (eval.cpp:125-145)
+    // scoring (eval.cpp:125-145): the document's log p is summed in cell
+    // order with the reference's rounding (term = c * log p, then add), one
+    // round of GW cells at a time
     const int Sn = L.n_score[doc];
-    const int32_t* __restrict__ sw = L.score_w + base;
-    const int32_t* __restrict__ sc = L.score_c + base;
+    const int2* sl = L.score + base;
     double lp = 0.0;
     long long scored = 0;
-    for (int f0 = G * wid; f0 < Sn; f0 += G * kFoldWarps) {
+    for (int r0 = 0; r0 < Sn; r0 += GW) {
+      const int f0 = r0 + G * wid;
       double2 r[G][NJ];
 #pragma unroll
       for (int c = 0; c < G; ++c) {
-        const int f = f0 + c;
-        const double* row = phi_wk + static_cast<int64_t>(f < Sn ? __ldg(sw + f) : 0) * K;
-#pragma unroll
-        for (int j = 0; j < NJ; ++j)
-          r[c][j] = f < Sn ? load_pair_g(row, 64 * j + 2 * lane, K, keven) : make_double2(0.0, 0.0);
+        if (f0 + c < Sn) fold_row_g<NJ>(r[c], phi_wk, __ldg(&sl[f0 + c].x), K, keven, lane);
+        else fold_row_zero<NJ>(r[c]);
       }
       double v[G];
-      fold_dots<NJ>(th, r, v);
+      fold_dots<C>(th, r, v);
       fold_tree<G / 2, 16>(v, lane);
       const int my = f0 + (lane >> SH);
-      if ((lane & ((1 << SH) - 1)) == 0 && my < Sn) {
-        const int32_t c = __ldg(sc + my);
-        if (!(v[0] > 0.0)) atomicOr(err, kErrNumerical);
-        lp = __fma_rn(static_cast<double>(c), log(v[0]), lp);
-        scored += c;
+      if ((lane & ((1 << SH) - 1)) == 0) {
+        double term = 0.0;
+        if (my < Sn) {
+          const int32_t c = __ldg(&sl[my].y);
+          if (!(v[0] > 0.0)) atomicOr(err, kErrNumerical);
+          term = __dmul_rn(static_cast<double>(c), log(v[0]));
+          scored += c;
+        }
+        s_term[G * wid + (lane >> SH)] = term;
       }
+      __syncthreads();
+      if (tid == 0) {
+        const int n = min(GW, Sn - r0);
+        for (int i = 0; i < n; ++i) lp = __dadd_rn(lp, s_term[i]);
+      }
+      __syncthreads();
     }
-    lp = warp_sum_d(lp);
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) scored += __shfl_xor_sync(0xffffffffu, scored, o);
-    if (lane == 0) {
-      s_tot[wid] = lp;
-      s_cnt[wid] = scored;
-    }
+    if (lane == 0) s_cnt[wid] = scored;
     __syncthreads();
+    FOLD_T(6)
     if (tid == 0) {
-      double t = s_tot[0];
       long long n = s_cnt[0];
-      for (int w = 1; w < kFoldWarps; ++w) {
-        t += s_tot[w];
-        n += s_cnt[w];
-      }
-      doc_logp[doc] = t;
+      for (int w = 1; w < NW; ++w) n += s_cnt[w];
+      doc_logp[doc] = lp;
       doc_scored[doc] = n;
     }
     if (theta_out)
-      for (int t = tid; t < K; t += kFoldThreads) theta_out[doc * K + t] = th_s[t];
+      for (int t = tid; t < K; t += NT) theta_out[doc * K + t] = ths[t];
   }
 }
 
-template <int NJ, bool RES>
+template <class C>
 int launch_fold(const int64_t* doc_offsets, const EvalLists& L, int64_t n_docs,
                 const double* phi_wk, int K, double alpha, int sweeps, double* doc_logp,
                 int64_t* doc_scored, double* theta_out, int* err, cudaStream_t st) {
-  constexpr int KP = FoldShape<NJ>::KP;
   int dev = 0, sms = 148, optin = 0;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
-  const size_t fixed = static_cast<size_t>(1 + kFoldWarps) * KP * sizeof(double);
-  const size_t budget = static_cast<size_t>(optin) - 1024;  // static shared memory
-  const int R = budget > fixed ? static_cast<int>((budget - fixed) / (KP * sizeof(double))) : 0;
-  const size_t bytes = fixed + static_cast<size_t>(R) * KP * sizeof(double);
+  cudaFuncAttributes fa{};
+  cudaFuncGetAttributes(&fa, k_eval_fold<C>);
+  const size_t fixed = (static_cast<size_t>(C::NW + 1) * C::KP + kFoldList) * sizeof(double);
+  const size_t budget = static_cast<size_t>(optin) - fa.sharedSizeBytes;
+  const size_t row = static_cast<size_t>(C::KP) * sizeof(double);
+  const int R = budget > fixed ? static_cast<int>((budget - fixed) / row) : 0;
+  const size_t bytes = fixed + static_cast<size_t>(R) * row;
   static std::atomic<unsigned long long> configured{0};
-  smem_opt_in(k_eval_fold<NJ, RES>, static_cast<int>(bytes), configured);
+  smem_opt_in(k_eval_fold<C>, static_cast<int>(bytes), configured);
   const int64_t blocks = min(n_docs, static_cast<int64_t>(sms));
+#ifdef SAMELDA_FOLD_PROF
+  unsigned long long z[8] = {};
+  cudaMemcpyToSymbolAsync(g_fold_prof, z, sizeof(z), 0, cudaMemcpyHostToDevice, st);
+#endif
   // the dynamic document counter lives one past the per-document results
   cudaMemsetAsync(doc_scored + n_docs, 0, sizeof(int64_t), st);
-  k_eval_fold<NJ, RES><<<static_cast<unsigned>(blocks), kFoldThreads, bytes, st>>>(
+  k_eval_fold<C><<<static_cast<unsigned>(blocks), C::NT, bytes, st>>>(
       doc_offsets, L, n_docs, phi_wk, K, alpha, sweeps, R, doc_logp, doc_scored, theta_out, err);
+#ifdef SAMELDA_FOLD_PROF
+  cudaMemcpyFromSymbolAsync(z, g_fold_prof, sizeof(z), 0, cudaMemcpyDeviceToHost, st);
+  cudaStreamSynchronize(st);
+  fprintf(stderr, "fold prof (cycles summed over CTAs, thread 0): stage %.3g cells %.3g bar1 %.3g epi %.3g bar2 %.3g score %.3g  R=%d\n",
+          (double)z[0], (double)z[1], (double)z[2], (double)z[3], (double)z[4], (double)z[6], R);
+#endif
   return 1;
 }
 
@@ -994,14 +1062,17 @@ int launch_eval_fold(const int64_t* doc_offsets, const EvalLists& lists, int64_t
                      const double* phi_wk, int K, double alpha, int sweeps, double* doc_logp,
                      int64_t* doc_scored, double* theta_out, int* err, cudaStream_t st) {
   if (n_docs == 0) return 0;
-#define SCU_FOLD(NJ, RES) \
-  launch_fold<NJ, RES>(doc_offsets, lists, n_docs, phi_wk, K, alpha, sweeps, doc_logp, doc_scored, \
-                       theta_out, err, st)
-  if (K <= 64) return SCU_FOLD(1, true);
-  if (K <= 128) return SCU_FOLD(2, true);
-  if (K <= 256) return SCU_FOLD(4, true);
-  if (K <= 512) return SCU_FOLD(8, false);
-  if (K <= 1024) return SCU_FOLD(16, false);
+#define SCU_FOLD(...)                                                                        \
+  launch_fold<FoldCfg<__VA_ARGS__>>(doc_offsets, lists, n_docs, phi_wk, K, alpha, sweeps,      \
+                                    doc_logp, doc_scored, theta_out, err, st)
+  // K <= 256 measured at NYTimes shape (30K test docs, 127 fold cells on
+  // average): G=4 / 8 warps / register-resident group 45.2 ms; 16 warps 46.9
+  // (no resident group) and 50.3 (G=2); 8 warps without it 50.1
+  if (K <= 64) return SCU_FOLD(1, 16, 8, true);
+  if (K <= 128) return SCU_FOLD(2, 8, 8, true);
+  if (K <= 256) return SCU_FOLD(4, 4, 8, true);
+  if (K <= 512) return SCU_FOLD(8, 2, 8, false);
+  if (K <= 1024) return SCU_FOLD(16, 1, 8, false);
 #undef SCU_FOLD
   return -1;  // K > 1024: the exact kernels
 }

@@ -102,6 +102,7 @@ SIGNATURES = [
     ("samelda_cu_rho_schedule", C.c_int, [_I64, _D, _D, C.POINTER(_D)]),
     ("samelda_cu_anneal_m", C.c_int, [_I32, _I64, _I64, _D, C.POINTER(_D)]),
     ("samelda_cu_fold_in_theta", C.c_int, [_P, _P, _I64, _I64, _P, _P, _I64, _D, _I32, _P]),
+    ("samelda_cu_set_eval_exact", C.c_int, [_P, _I32]),
     ("samelda_cu_perword_loglik", C.c_int, [_P, _P, _I64, _I64, _CP, _D, _U64, C.POINTER(_D)]),
     ("samelda_cu_batches_create", C.c_int, [_I64, _D, _U64, C.POINTER(C.c_void_p)]),
     ("samelda_cu_batches_size", _I64, [_P]),
@@ -344,6 +345,11 @@ class Context:
         """Run on a caller's cudaStream_t handle (0 = the legacy default stream,
         which is torch's default stream)."""
         self.check(self.lib.samelda_cu_set_stream(self.h, C.c_void_p(int(stream_handle))))
+
+    def set_eval_exact(self, exact: bool = True):
+        """Held-out evaluation in the reference's summation order (bit-identical
+        ll, ~10x slower) instead of the default tree-ordered fold-in (1e-12)."""
+        self.check(self.lib.samelda_cu_set_eval_exact(self.h, int(bool(exact))))
 
     def use_own_stream(self):
         self.check(self.lib.samelda_cu_use_own_stream(self.h))

@@ -527,7 +527,11 @@ def test_fold_in_fixed_point(port):
     a = S.fold_in_theta(g.phi_true, w, c, 0.1, 60)
     b = S.fold_in_theta(g.phi_true, w, c, 0.1, 200)
     assert np.abs(a - b).max() < 1e-10
-    np.testing.assert_array_equal(a, port.fold_in_theta(g.phi_true, w, c, 0.1, 60))
+    want = port.fold_in_theta(g.phi_true, w, c, 0.1, 60)
+    np.testing.assert_allclose(a, want, rtol=1e-12, atol=0)
+    ctx = S.Context(0)
+    ctx.set_eval_exact(True)  # the reference's summation order: bit-identical
+    np.testing.assert_array_equal(S.fold_in_theta(g.phi_true, w, c, 0.1, 60, ctx=ctx), want)
 
 
 def test_scaling_counts_leaves_the_score_unchanged(port):
@@ -688,8 +692,12 @@ def test_model_bin_and_metrics_csv_match_reference_training(port, tmp_path):
     g = port.make_corpus(150, 90, 5, 40.0, 77)
     tr, te = port.split_holdout(g, 0.2, 3)
     kw = dict(n_topics=16, m=30.0, t_max=6, batch_fraction=0.25, seed=11)
-    model, trace = S.train(tr, S.SamplerConfig(**kw), te, 2)
+    ctx = S.Context(0)
+    ctx.set_eval_exact(True)  # ll in the reference's summation order: identical csv text
+    model, trace = S.train(tr, S.SamplerConfig(**kw), te, 2, ctx=ctx)
     rphi, _, rtrace = ref.train(tr, TrainConfig(**kw), te, 2)
+    _, fast = S.train(tr, S.SamplerConfig(**kw), te, 2)  # default eval: 1e-12
+    np.testing.assert_allclose([r["ll"] for r in fast], [r["ll"] for r in rtrace], rtol=1e-12, atol=0)
     ours, theirs = str(tmp_path / "ours.bin"), str(tmp_path / "ref.bin")
     S.save_checkpoint(model, ours)
     ref.save_checkpoint(theirs, rphi, model.alpha, model.beta)

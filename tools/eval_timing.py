@@ -27,14 +27,18 @@ stream = S.MinibatchStream(train.n_docs, cfg["batch_fraction"], 1)
 for t in range(args.periods):
     tr.period(stream.next(), t, cfg["m"], S.rho_schedule(t, 1.0, 0.5))
 tr.ctx.synchronize()
-# the kernel variant is chosen by the environment, read once per process
-# (SAMELDA_EVAL=cta|warp, SAMELDA_EVAL_CTAS_PER_SM=n): run once per variant
+# default fold-in kernel (k_eval_fold) and the reference-order exact mode
+# (variant of the exact mode: SAMELDA_EVAL=cta|warp, SAMELDA_EVAL_CTAS_PER_SM=n)
 tr.evaluate()  # warm (split computed once)
-times = []
-for _ in range(3):
-    t0 = time.perf_counter()
-    ll = tr.evaluate()
-    times.append(time.perf_counter() - t0)
-variant = os.environ.get("SAMELDA_EVAL", "default") + "/" + os.environ.get("SAMELDA_EVAL_CTAS_PER_SM", "-")
-print(f"{variant}: ll={ll!r} best {min(times) * 1e3:.2f} ms  (test docs {heldout.n_docs}, "
-      f"nnz {heldout.nnz})", flush=True)
+for exact in (False, True):
+    tr.ctx.set_eval_exact(exact)
+    tr.evaluate()
+    times = []
+    for _ in range(3):
+        t0 = time.perf_counter()
+        ll = tr.evaluate()
+        times.append(time.perf_counter() - t0)
+    variant = ("exact:" + os.environ.get("SAMELDA_EVAL", "stage") + "/" +
+               os.environ.get("SAMELDA_EVAL_CTAS_PER_SM", "-")) if exact else "fast (k_eval_fold)"
+    print(f"{variant}: ll={ll!r} best {min(times) * 1e3:.2f} ms  (test docs {heldout.n_docs}, "
+          f"nnz {heldout.nnz})", flush=True)
