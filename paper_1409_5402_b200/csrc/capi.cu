@@ -580,8 +580,8 @@ struct samelda_cu_ctx {
         for (int i = 0; i < 2; ++i) stage(B_);
         return;
       }
-      const int64_t records = nnz_ * ((K_ + 255) / 256);
-      ensure<unsigned char>(deferred, records * scu::deferred_record_bytes());
+      const int64_t records = scu::deferred_max_records(nnz_, K_);
+      ensure<unsigned char>(deferred, scu::deferred_buffer_bytes(nnz_, K_));
       ensure<unsigned char>(deferred_aux, scu::deferred_aux_bytes(records, draw_cap_for(records)));
       ensure<unsigned long long>(n_deferred, 1);
     }
@@ -626,9 +626,9 @@ struct samelda_cu_ctx {
         tick(need_phi ? kSampleLast : kSample, false);
         return;
       }
-      const int64_t records = bv.nnz * ((K_ + 255) / 256);
+      const int64_t records = scu::deferred_max_records(bv.nnz, K_);
       const int64_t draw_cap = draw_cap_for(records);
-      void* rec = ensure<unsigned char>(deferred, records * scu::deferred_record_bytes());
+      void* rec = ensure<unsigned char>(deferred, scu::deferred_buffer_bytes(bv.nnz, K_));
       void* aux = ensure<unsigned char>(deferred_aux, scu::deferred_aux_bytes(records, draw_cap));
       launches += scu::launch_sample_fast(bv, theta_b, theta_b32, phi_wk, phi_wk32, mu_d, K_,
                                           m_t_, seed, static_cast<uint32_t>(t),

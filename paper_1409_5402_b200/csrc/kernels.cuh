@@ -73,10 +73,11 @@ int launch_sample(const BatchView& bv, const double* theta_batch, const double* 
 // Same draws, bit for bit, through an f32 fast path with exact f64 fallback
 // (see kernels_sample.cu).  mu == nullptr: the kernel forms mu itself (period path).
 // mu_f_scratch: nnz floats (used when K > 256).
-// `deferred` holds up to nnz * ceil(K / 256) records of
-// deferred_record_bytes() each; n_deferred is one u64 of scratch; `aux` holds
-// deferred_aux_bytes(records, draw_cap) (per-record mu + a flat list of up to
-// draw_cap deferred draws; overflow is drawn inline, never dropped).
+// `deferred` holds deferred_buffer_bytes(nnz, K) (fixed record slots per work
+// item + a record count per item); n_deferred is one u64 (the records of the
+// sweep, for profiling); `aux` holds deferred_aux_bytes(deferred_max_records(
+// nnz, K), draw_cap) (per-record mu + a flat list of up to draw_cap deferred
+// draws; overflow is drawn inline, never dropped).
 int launch_sample_fast(const BatchView& bv, const double* theta_b64, const float* theta_b32,
                        const double* phi64, const float* phi32, const double* mu, int K,
                        double m_t, uint64_t seed, uint32_t t, uint32_t sweep,
@@ -90,7 +91,8 @@ int launch_sample_throughput(const BatchView& bv, const float* theta_b32, const 
                              double m_t, uint64_t seed, uint32_t t, uint32_t sweep,
                              unsigned long long* theta_counts, unsigned long long* phi_counts,
                              float* mu_f_scratch, cudaStream_t st);
-int64_t deferred_record_bytes();
+int64_t deferred_max_records(int64_t nnz, int K);
+int64_t deferred_buffer_bytes(int64_t nnz, int K);
 // fills the device's glibc lgamma table (call once per device, after cudaSetDevice)
 int init_lgamma_table();
 int64_t deferred_aux_bytes(int64_t max_records, int64_t draw_cap);

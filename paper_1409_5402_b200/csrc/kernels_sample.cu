@@ -488,7 +488,8 @@ __global__ void __launch_bounds__(kFastBlock, MINB) k_sample_v2(
     const double* __restrict__ mu_in, const float* __restrict__ mu_f_in, int K, double m_t,
     uint64_t seed, uint32_t t, uint32_t sweep, int64_t chunk,
     unsigned long long* __restrict__ theta_counts, unsigned long long* __restrict__ phi_counts,
-    Deferred* __restrict__ deferred, unsigned long long* __restrict__ n_deferred) {
+    Deferred* __restrict__ deferred, uint32_t* __restrict__ rec_count,
+    unsigned long long* __restrict__ n_deferred) {
   constexpr int KG = KPL < 4 ? KPL : 4;  // Philox chains in flight per group
   const int lane = threadIdx.x & 31;
   const int kbase = static_cast<int>(blockIdx.y) * kWarp * KPL;
@@ -512,7 +513,17 @@ __global__ void __launch_bounds__(kFastBlock, MINB) k_sample_v2(
   __syncthreads();
   const int64_t p0 = item * chunk;
   const int64_t p1 = min(p0 + chunk, bv.nnz);
-  if (p0 >= p1) return;
+  // this work item's deferred records live at fixed slots [item_g chunk,
+  // item_g chunk + rec_count[item_g]): no global counter per record (late in
+  // training nearly every nonzero carries a PTRS draw, and one contended
+  // atomic per record serialised the kernel); k_rec_prefix then numbers them
+  const int64_t item_g = static_cast<int64_t>(blockIdx.y) * gridDim.x * (kFastBlock / kWarp) + item;
+  if (p0 >= p1) {
+    if (lane == 0) rec_count[item_g] = 0;
+    return;
+  }
+  Deferred* const rec_out = deferred + item_g * chunk;
+  uint32_t n_rec = 0;
 
   int cur_b = -1;
   float th[KPL];
@@ -678,7 +689,7 @@ __global__ void __launch_bounds__(kFastBlock, MINB) k_sample_v2(
 #pragma unroll
         for (int j = 0; j < 8; ++j) masks[j] = j < KPL ? __ballot_sync(0xffffffffu, (defer_bits >> j) & 1u) : 0u;
         if (lane == 0) {
-          const unsigned long long slot = atomicAdd(n_deferred, 1ull);
+          const uint32_t slot = n_rec;
           Deferred rec;
           rec.p = g0 + i;
           rec.b = bi;
@@ -687,12 +698,47 @@ __global__ void __launch_bounds__(kFastBlock, MINB) k_sample_v2(
           rec.kbase = kbase;
 #pragma unroll
           for (int j = 0; j < 8; ++j) rec.mask[j] = masks[j];
-          deferred[slot] = rec;
+          rec_out[slot] = rec;
         }
+        ++n_rec;
       }
     }
   }
   if (cur_b >= 0) flush(cur_b);
+  if (lane == 0) rec_count[item_g] = n_rec;
+}
+
+// Exclusive prefix of the per-item record counts (one block): dense record r
+// is slot item chunk + (r - prefix[item]) for the item with prefix[item] <= r <
+// prefix[item + 1]; prefix[n_items] = the sweep's record count, also written
+// to *n_deferred (profiling).
+constexpr int kPrefixBlock = 1024;
+__global__ void __launch_bounds__(kPrefixBlock) k_rec_prefix(const uint32_t* __restrict__ count,
+                                                             int64_t n, uint32_t* __restrict__ prefix,
+                                                             unsigned long long* __restrict__ n_deferred) {
+  __shared__ uint32_t s_sum[kPrefixBlock];
+  const int tid = threadIdx.x;
+  const int64_t per = (n + kPrefixBlock - 1) / kPrefixBlock;
+  const int64_t a = min(n, tid * per), e = min(n, a + per);
+  uint32_t local = 0;
+  for (int64_t i = a; i < e; ++i) local += count[i];
+  s_sum[tid] = local;
+  __syncthreads();
+  for (int o = 1; o < kPrefixBlock; o <<= 1) {  // Hillis-Steele inclusive scan
+    const uint32_t v = tid >= o ? s_sum[tid - o] : 0u;
+    __syncthreads();
+    s_sum[tid] += v;
+    __syncthreads();
+  }
+  uint32_t run = s_sum[tid] - local;
+  for (int64_t i = a; i < e; ++i) {
+    prefix[i] = run;
+    run += count[i];
+  }
+  if (tid == kPrefixBlock - 1) {
+    prefix[n] = s_sum[tid];
+    *n_deferred = s_sum[tid];
+  }
 }
 
 // Deferred exact draws in two passes.
@@ -746,108 +792,98 @@ __device__ __forceinline__ void deferred_one(const BatchView& bv, const Deferred
   }
 }
 
-// Block tile = 32 records.  Product phase: the 8 warps load the records'
-// theta / phi row segments coalesced (lanes over topics, kExpKC topics per
-// chunk) and write the exact products to a shared [32][kExpKC + 1] tile.
-// Sum phase: warp 0, lane = record, extends each record's sequential f64 sum
-// over the chunk in the reference's k order (sampler.cpp:111-119) -- 32
-// independent chains, one DADD per topic per 32 records.  Then one atomic
-// reserves the tile's draw-list slots and warp v writes the entries of
-// records v, v + 8, ... (lane = topic bit, positions from popc prefixes).
-constexpr int kExpKC = 256;
-constexpr int kExpStride = kExpKC + 1;  // 2-way (optimal) f64 bank pattern
-constexpr size_t kExpSmem = sizeof(double) * 32 * kExpStride;
 
+// dense record r -> its slot: thread per (item, slot of the item)
+__global__ void __launch_bounds__(256) k_rec_map(const uint32_t* __restrict__ count,
+                                                  const uint32_t* __restrict__ prefix,
+                                                  int64_t n_items, int chunk,
+                                                  uint32_t* __restrict__ slot_of) {
+  const int64_t g = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+  const int64_t item = g / chunk;
+  const int i = static_cast<int>(g - item * chunk);
+  if (item >= n_items || i >= static_cast<int>(__ldg(count + item))) return;
+  slot_of[__ldg(prefix + item) + i] = static_cast<uint32_t>(item * chunk + i);
+}
+
+// Phase A, thread = record: the record's exact mu -- the reference's
+// sequential-k f64 dot (sampler.cpp:111-119: product then add, no FMA) over
+// the batch row's theta and the word's phi, both read as 16-byte pairs --
+// unless the caller supplied mu, then the record's flagged draws into the flat
+// list (one atomic per warp reserves the warp's slots).  No shared-memory
+// tiles and no block barriers: late in training nearly every nonzero carries a
+// PTRS draw and this pass is the exact SDDMM of the whole batch (staging the
+// phi rows through shared memory for coalesced loads measured slower: 7.7 and
+// 9.0 ms per sweep against 5.7).
 __global__ void __launch_bounds__(256) k_deferred_expand(
     BatchView bv, const double* __restrict__ theta_b64, const double* __restrict__ phi64,
     const double* __restrict__ mu_in, int K, double m_t, uint64_t seed, uint32_t t,
-    uint32_t sweep, const Deferred* __restrict__ deferred,
-    const unsigned long long* __restrict__ n_deferred, double* __restrict__ rec_mu,
+    uint32_t sweep, const Deferred* __restrict__ deferred, const uint32_t* __restrict__ slot_of,
+    const uint32_t* __restrict__ n_rec, double* __restrict__ rec_mu,
     DeferredDraw* __restrict__ draws, unsigned long long* __restrict__ n_draws,
     unsigned long long draw_cap, unsigned long long* __restrict__ theta_counts,
     unsigned long long* __restrict__ phi_counts, int* __restrict__ err) {
-  extern __shared__ double s_prod[];  // [32][kExpStride]
-  __shared__ double s_mu[32];
-  __shared__ unsigned long long s_pre[33];
   const int lane = threadIdx.x & 31;
-  const int wib = threadIdx.x >> 5;
-  const int nw = blockDim.x >> 5;
-  const int64_t n = static_cast<int64_t>(*n_deferred);
-  for (int64_t tile = blockIdx.x; tile * 32 < n; tile += gridDim.x) {
-    const int64_t r0 = tile * 32;
-    const int nh = static_cast<int>(min(static_cast<int64_t>(32), n - r0));
-    if (mu_in) {
-      if (threadIdx.x < nh) s_mu[threadIdx.x] = mu_in[deferred[r0 + threadIdx.x].p];
-    } else {
-      double mu = 0.0;  // warp 0: lane = record
-      for (int kc = 0; kc < K; kc += kExpKC) {
-        const int kn = min(kExpKC, K - kc);
-        for (int i = wib; i < nh; i += nw) {
-          const int32_t b = deferred[r0 + i].b, w = deferred[r0 + i].w;
-          const double* th = theta_b64 + static_cast<int64_t>(b) * K + kc;
-          const double* ph = phi64 + static_cast<int64_t>(w) * K + kc;
-          double* row = s_prod + i * kExpStride;
-#pragma unroll
-          for (int j = 0; j < kExpKC / 32; ++j) {
-            const int k = lane + 32 * j;
-            if (k < kn) row[k] = __dmul_rn(__ldg(th + k), __ldg(ph + k));
-          }
-        }
-        __syncthreads();
-        if (wib == 0 && lane < nh) {
-          const double* row = s_prod + lane * kExpStride;
+  const int64_t n = static_cast<int64_t>(__ldg(n_rec));
+  const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
+  for (int64_t r0 = blockIdx.x * static_cast<int64_t>(blockDim.x) + (threadIdx.x & ~31); r0 < n;
+       r0 += stride) {
+    const int64_t r = r0 + lane;
+    const bool live = r < n;
+    const uint32_t slot = live ? __ldg(slot_of + r) : 0u;
+    Deferred me{};
+    double mu = 0.0;
+    uint32_t cnt = 0;
+    if (live) {
+      me = deferred[slot];
+      if (mu_in) {
+        mu = __ldg(mu_in + me.p);
+      } else {
+        const double* th = theta_b64 + static_cast<int64_t>(me.b) * K;
+        const double* ph = phi64 + static_cast<int64_t>(me.w) * K;
+        if ((K & 1) == 0) {
+          const double2* th2 = reinterpret_cast<const double2*>(th);
+          const double2* ph2 = reinterpret_cast<const double2*>(ph);
 #pragma unroll 8
-          for (int k = 0; k < kn; ++k) mu = __dadd_rn(mu, row[k]);
+          for (int k2 = 0; k2 < (K >> 1); ++k2) {
+            const double2 a = __ldg(th2 + k2), b = __ldg(ph2 + k2);
+            mu = __dadd_rn(mu, __dmul_rn(a.x, b.x));
+            mu = __dadd_rn(mu, __dmul_rn(a.y, b.y));
+          }
+        } else {
+          for (int k = 0; k < K; ++k) mu = __dadd_rn(mu, __dmul_rn(__ldg(th + k), __ldg(ph + k)));
         }
-        __syncthreads();
       }
-      if (wib == 0 && lane < nh) s_mu[lane] = mu;
+      rec_mu[slot] = mu;
+#pragma unroll
+      for (int j = 0; j < 8; ++j) cnt += __popc(me.mask[j]);
     }
-    // one atomic reserves the tile's slots; every reserved slot below draw_cap
-    // is written (phase B reads exactly [0, min(n_draws, draw_cap))), the rest
-    // is drawn here
-    if (wib == 0) {
-      uint32_t cnt = 0;
-      if (lane < nh) {
-        const Deferred& me = deferred[r0 + lane];
+    // the warp's draw-list slots: inclusive scan + one atomic
+    uint32_t inc = cnt;
 #pragma unroll
-        for (int j = 0; j < 8; ++j) cnt += __popc(me.mask[j]);
-      }
-      uint32_t inc = cnt;  // inclusive warp scan
-#pragma unroll
-      for (int o = 1; o < 32; o <<= 1) {
-        const uint32_t v = __shfl_up_sync(0xffffffffu, inc, o);
-        if (lane >= o) inc += v;
-      }
-      unsigned long long b0 = 0;
-      if (lane == 31) b0 = atomicAdd(n_draws, static_cast<unsigned long long>(inc));
-      b0 = __shfl_sync(0xffffffffu, b0, 31);
-      s_pre[lane] = b0 + inc - cnt;
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t v = __shfl_up_sync(0xffffffffu, inc, o);
+      if (lane >= o) inc += v;
     }
-    __syncthreads();
-    const uint32_t below = (1u << lane) - 1u;
-    for (int i = wib; i < nh; i += nw) {
-      const int64_t r = r0 + i;
-      const Deferred me = deferred[r];
-      const double mu = s_mu[i];
-      if (lane == 0) rec_mu[r] = mu;
-      unsigned long long base = s_pre[i];
-#pragma unroll
-      for (int j = 0; j < 8; ++j) {
-        const uint32_t m = me.mask[j];
-        if ((m >> lane) & 1u) {
-          const unsigned long long slot = base + __popc(m & below);
-          const int k = me.kbase + lane + 32 * j;
-          if (slot < draw_cap)
-            draws[slot] = DeferredDraw{static_cast<uint32_t>(r), static_cast<uint32_t>(k)};
-          else
-            deferred_one(bv, me, mu, k, theta_b64, phi64, K, m_t, seed, t, sweep, theta_counts,
-                         phi_counts, err);
-        }
-        base += __popc(m);
+    unsigned long long b0 = 0;
+    if (lane == 31 && inc) b0 = atomicAdd(n_draws, static_cast<unsigned long long>(inc));
+    b0 = __shfl_sync(0xffffffffu, b0, 31);
+    unsigned long long base = b0 + inc - cnt;
+    if (!live) continue;
+#pragma unroll 1
+    for (int j = 0; j < 8; ++j) {
+      uint32_t m = me.mask[j];
+      while (m) {
+        const int bit = __ffs(m) - 1;
+        m &= m - 1;
+        const int k = me.kbase + bit + 32 * j;
+        // every reserved slot below draw_cap is written (phase B reads exactly
+        // [0, min(n_draws, draw_cap))), the rest is drawn here
+        if (base < draw_cap) draws[base] = DeferredDraw{slot, static_cast<uint32_t>(k)};
+        else deferred_one(bv, me, mu, k, theta_b64, phi64, K, m_t, seed, t, sweep, theta_counts,
+                          phi_counts, err);
+        ++base;
       }
     }
-    __syncthreads();  // s_prod / s_mu / s_pre are rewritten by the next tile
   }
 }
 
@@ -870,17 +906,19 @@ __global__ void __launch_bounds__(256) k_deferred_draw(
 // Both passes.  aux = [rec_mu: max_records f64][n_draws: u64][pad][draws: draw_cap]
 void launch_deferred(const BatchView& bv, const double* tb64, const double* phi64, const double* mu,
                      int K, double m_t, uint64_t seed, uint32_t t, uint32_t sweep, Deferred* rec,
-                     unsigned long long* n_deferred, void* aux, int64_t max_records,
-                     int64_t draw_cap, unsigned long long* tc, unsigned long long* pc, int* err,
-                     cudaStream_t st) {
+                     uint32_t* rec_count, int64_t n_items, int chunk, unsigned long long* n_deferred,
+                     void* aux, int64_t max_records, int64_t draw_cap, unsigned long long* tc,
+                     unsigned long long* pc, int* err, cudaStream_t st) {
+  uint32_t* prefix = rec_count + n_items;    // n_items + 1 entries (deferred_buffer_bytes)
+  uint32_t* slot_of = prefix + n_items + 1;   // dense record -> slot (max_records entries)
+  k_rec_prefix<<<1, kPrefixBlock, 0, st>>>(rec_count, n_items, prefix, n_deferred);
+  k_rec_map<<<grid_for(n_items * chunk, 256), 256, 0, st>>>(rec_count, prefix, n_items, chunk, slot_of);
   double* rec_mu = static_cast<double*>(aux);
   auto* n_draws = reinterpret_cast<unsigned long long*>(rec_mu + max_records);
   auto* draws = reinterpret_cast<DeferredDraw*>(n_draws + 2);
   cudaMemsetAsync(n_draws, 0, sizeof(unsigned long long), st);
-  static std::atomic<unsigned long long> attr_set{0};
-  smem_opt_in(k_deferred_expand, static_cast<int>(kExpSmem), attr_set);
-  k_deferred_expand<<<148 * 3, 256, kExpSmem, st>>>(bv, tb64, phi64, mu, K, m_t, seed, t, sweep, rec,
-                                             n_deferred, rec_mu, draws, n_draws,
+  k_deferred_expand<<<148 * 8, 256, 0, st>>>(bv, tb64, phi64, mu, K, m_t, seed, t, sweep, rec,
+                                             slot_of, prefix + n_items, rec_mu, draws, n_draws,
                                              static_cast<unsigned long long>(draw_cap), tc, pc, err);
   k_deferred_draw<<<148 * 16, 256, 0, st>>>(bv, tb64, phi64, K, m_t, seed, t, sweep, rec, rec_mu,
                                             draws, n_draws, static_cast<unsigned long long>(draw_cap),
@@ -1136,10 +1174,15 @@ int launch_fast_kpl(const BatchView& bv, const double* tb64, const float* tb32, 
     muf = mu_f;
     ++launched;
   }
-  auto* rec = static_cast<Deferred*>(deferred);
   // one chunk per warp (a persistent grid taking chunks from a counter was
   // measured 2% slower)
   const dim3 grid(static_cast<unsigned>((items + warps - 1) / warps), static_cast<unsigned>(n_slices));
+  // deferred records: chunk fixed slots per (slice, grid work item), then one
+  // record count per work item (deferred_buffer_bytes)
+  auto* rec = static_cast<Deferred*>(deferred);
+  const int64_t n_items = static_cast<int64_t>(grid.x) * warps * n_slices;
+  auto* rec_count = reinterpret_cast<uint32_t*>(rec + n_items * chunk);
+  const int64_t max_records = n_items * chunk;
   {
     const int musrc = mu ? 1 : (muf ? 2 : 0);
     const bool full = K % (kWarp * KPL) == 0;
@@ -1148,17 +1191,17 @@ int launch_fast_kpl(const BatchView& bv, const double* tb64, const float* tb32, 
       if constexpr (KPL == 8) {
         if (full && musrc == 0 && n_slices == 1) {
           k_sample_v2<8, true, 0, 4, kDecDefault, 0, false><<<grid, kFastBlock, 0, st>>>(
-              bv, tb32, phi32, mu, muf, K, m_t, seed, t, sweep, chunk, tc, pc, rec, n_deferred);
-          launch_deferred(bv, tb64, phi64, mu, K, m_t, seed, t, sweep, rec, n_deferred, aux,
-                          bv.nnz * ((K + 255) / 256), draw_cap, tc, pc, err, st);
-          return launched + 3;
+              bv, tb32, phi32, mu, muf, K, m_t, seed, t, sweep, chunk, tc, pc, rec, rec_count, n_deferred);
+          launch_deferred(bv, tb64, phi64, mu, K, m_t, seed, t, sweep, rec, rec_count, n_items,
+                          static_cast<int>(chunk), n_deferred, aux, max_records, draw_cap, tc, pc, err, st);
+          return launched + 4;
         }
       }
       return -1;  // caller passes phi counts for every other shape
     }
 #define SCU_V2_LAUNCH(FULLV, MS, MB, DC, ...)                                                   \
   k_sample_v2<KPL, FULLV, MS, MB, DC __VA_OPT__(,) __VA_ARGS__><<<grid, kFastBlock, 0, st>>>(    \
-      bv, tb32, phi32, mu, muf, K, m_t, seed, t, sweep, chunk, tc, pc, rec, n_deferred)
+      bv, tb32, phi32, mu, muf, K, m_t, seed, t, sweep, chunk, tc, pc, rec, rec_count, n_deferred)
     // production: DEC 1, 4 blocks/SM.  A library built with
     // -DSAMELDA_AB_VARIANTS also carries the measured alternatives (all
     // bit-identical, all slower at K = 256): SAMELDA_DEC=0|2, SAMELDA_MINB=3,
@@ -1186,9 +1229,9 @@ int launch_fast_kpl(const BatchView& bv, const double* tb64, const float* tb32, 
 #undef SCU_V2
 #undef SCU_V2_LAUNCH
   }
-  launch_deferred(bv, tb64, phi64, mu, K, m_t, seed, t, sweep, rec, n_deferred, aux,
-                  bv.nnz * ((K + 255) / 256), draw_cap, tc, pc, err, st);
-  return launched + 3;
+  launch_deferred(bv, tb64, phi64, mu, K, m_t, seed, t, sweep, rec, rec_count, n_items,
+                  static_cast<int>(chunk), n_deferred, aux, max_records, draw_cap, tc, pc, err, st);
+  return launched + 4;
 }
 
 // k_expected: the deterministic expected-count path (z := rate,
@@ -1363,7 +1406,21 @@ int launch_sample(const BatchView& bv, const double* theta_batch, const double* 
 
 
 // per (nonzero, 256-topic block): the record, its mu, and up to 256 flat draws
-int64_t deferred_record_bytes() { return static_cast<int64_t>(sizeof(Deferred)); }
+int64_t deferred_max_records(int64_t nnz, int K) {
+  // k_sample_v2's fixed slots: (work items rounded to whole blocks) x chunk
+  // per topic slice, chunk <= 128 and a block of 8 warps
+  const int n_slices = (K + 255) / 256;
+  return (nnz + 8 * 128) * n_slices;
+}
+
+int64_t deferred_buffer_bytes(int64_t nnz, int K) {
+  // records, then one u32 count per work item (chunk >= 32 nonzeros) and
+  // their exclusive prefix (+ the total), then the dense record -> slot map
+  const int n_slices = (K + 255) / 256;
+  const int64_t items = ((nnz + 8 * 128) / 32 + 1) * n_slices;
+  return deferred_max_records(nnz, K) * static_cast<int64_t>(sizeof(Deferred) + sizeof(uint32_t)) +
+         (2 * items + 1) * static_cast<int64_t>(sizeof(uint32_t));
+}
 
 int64_t deferred_aux_bytes(int64_t max_records, int64_t draw_cap) {
   return max_records * static_cast<int64_t>(sizeof(double)) + 16 +

@@ -16,6 +16,7 @@ ap = argparse.ArgumentParser()
 ap.add_argument("--config", default="nytimes")
 ap.add_argument("--periods", type=int, default=12)
 ap.add_argument("--mode", type=int, default=0)
+ap.add_argument("--every", type=int, default=1, help="print every n-th period")
 args = ap.parse_args()
 cfg = bench.CONFIGS[args.config]
 train, heldout = bench.single_gpu_corpus(args.config)
@@ -31,6 +32,8 @@ for t in range(args.periods):
     tr.ctx.synchronize()
     wall = (time.perf_counter() - t0) * 1e3
     p = tr.profile_read()
+    if t % args.every:
+        continue
     print(f"t={t:3d} wall={wall:8.2f}ms sample={p['sample_ms']:8.2f}ms mstep={p['mstep_ms']:6.2f}ms "
-          f"nnz={p['nnz']} deferred={p['deferred']} ({p['deferred'] / max(p['nnz'], 1) * 100:.2f}%)",
+          f"first={p['sample_first_ms']:7.2f} last={p['sample_last_ms']:7.2f} nnz={p['nnz']} deferred={p['deferred']} ({p['deferred'] / max(p['nnz'], 1) * 100:.2f}%)",
           flush=True)
