@@ -21,6 +21,8 @@
 #include <thread>
 #include <vector>
 
+#include <nvtx3/nvToolsExt.h>  // header-only NVTX v3: no-ops unless a profiler attaches
+
 #include "../../include/samelda_cu.h"
 #include "kernels.cuh"
 #include "philox.cuh"
@@ -341,7 +343,14 @@ struct samelda_cu_ctx {
   size_t events_used[kKinds] = {0, 0, 0, 0};
   int64_t prof_nnz = 0, prof_docs = 0, prof_deferred = 0;
 
+  // NVTX ranges around the sampling sweeps, the SDDMM and the M-step (every
+  // call; the profiler timeline shows where each period's launches come from),
+  // CUDA events only when profiling
   void tick(int kind, bool start) {
+    static const char* const kNames[kKinds] = {"samelda:sample_sweep", "samelda:sddmm",
+                                               "samelda:update_model", "samelda:sample_sweep_last"};
+    if (start) nvtxRangePushA(kNames[kind]);
+    else nvtxRangePop();
     if (!profile) return;
     auto& v = events[kind];
     size_t& used = events_used[kind];
@@ -690,6 +699,10 @@ struct samelda_cu_ctx {
   }
 
   double eval_ll(const double* phi_wk, int K_, double alpha) {
+    struct Range {
+      Range() { nvtxRangePushA("samelda:perword_loglik"); }
+      ~Range() { nvtxRangePop(); }
+    } range;
     const int64_t nd = heldout.n_docs;
     double* lp = ensure<double>(doc_logp, nd);
     int64_t* sc = ensure<int64_t>(doc_scored, nd + 1);  // + the eval kernel's work counter
@@ -1326,6 +1339,10 @@ int samelda_cu_heldout(samelda_cu_ctx* ctx, const samelda_cu_corpus* test, uint6
 int samelda_cu_period_sample(samelda_cu_ctx* ctx, const int32_t* doc_ids, int64_t B, int64_t t,
                              double m_t) {
   return guarded(ctx, [&] {
+    struct Range {
+      Range() { nvtxRangePushA("samelda:period"); }
+      ~Range() { nvtxRangePop(); }
+    } range;
     if (!ctx->model_ready) fail(SAMELDA_CU_CONFIG, "period: call samelda_cu_train_begin first");
     if (!(m_t > 0.0) || !std::isfinite(m_t)) fail(SAMELDA_CU_CONFIG, "sample_counts: m_t must be positive and finite");
     const samelda_cu_config& c = ctx->cfg;

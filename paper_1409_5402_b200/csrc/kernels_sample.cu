@@ -516,7 +516,7 @@ __global__ void __launch_bounds__(kFastBlock, MINB) k_sample_v2(
   // this work item's deferred records live at fixed slots [item_g chunk,
   // item_g chunk + rec_count[item_g]): no global counter per record (late in
   // training nearly every nonzero carries a PTRS draw, and one contended
-  // atomic per record serialised the kernel); k_rec_prefix then numbers them
+  // atomic per record serialised the kernel); k_deferred_expand walks them item by item
   const int64_t item_g = static_cast<int64_t>(blockIdx.y) * gridDim.x * (kFastBlock / kWarp) + item;
   if (p0 >= p1) {
     if (lane == 0) rec_count[item_g] = 0;
@@ -705,39 +705,9 @@ __global__ void __launch_bounds__(kFastBlock, MINB) k_sample_v2(
     }
   }
   if (cur_b >= 0) flush(cur_b);
-  if (lane == 0) rec_count[item_g] = n_rec;
-}
-
-// Exclusive prefix of the per-item record counts (one block): dense record r
-// is slot item chunk + (r - prefix[item]) for the item with prefix[item] <= r <
-// prefix[item + 1]; prefix[n_items] = the sweep's record count, also written
-// to *n_deferred (profiling).
-constexpr int kPrefixBlock = 1024;
-__global__ void __launch_bounds__(kPrefixBlock) k_rec_prefix(const uint32_t* __restrict__ count,
-                                                             int64_t n, uint32_t* __restrict__ prefix,
-                                                             unsigned long long* __restrict__ n_deferred) {
-  __shared__ uint32_t s_sum[kPrefixBlock];
-  const int tid = threadIdx.x;
-  const int64_t per = (n + kPrefixBlock - 1) / kPrefixBlock;
-  const int64_t a = min(n, tid * per), e = min(n, a + per);
-  uint32_t local = 0;
-  for (int64_t i = a; i < e; ++i) local += count[i];
-  s_sum[tid] = local;
-  __syncthreads();
-  for (int o = 1; o < kPrefixBlock; o <<= 1) {  // Hillis-Steele inclusive scan
-    const uint32_t v = tid >= o ? s_sum[tid - o] : 0u;
-    __syncthreads();
-    s_sum[tid] += v;
-    __syncthreads();
-  }
-  uint32_t run = s_sum[tid] - local;
-  for (int64_t i = a; i < e; ++i) {
-    prefix[i] = run;
-    run += count[i];
-  }
-  if (tid == kPrefixBlock - 1) {
-    prefix[n] = s_sum[tid];
-    *n_deferred = s_sum[tid];
+  if (lane == 0) {
+    rec_count[item_g] = n_rec;
+    if (n_rec) atomicAdd(n_deferred, static_cast<unsigned long long>(n_rec));
   }
 }
 
@@ -793,18 +763,6 @@ __device__ __forceinline__ void deferred_one(const BatchView& bv, const Deferred
 }
 
 
-// dense record r -> its slot: thread per (item, slot of the item)
-__global__ void __launch_bounds__(256) k_rec_map(const uint32_t* __restrict__ count,
-                                                  const uint32_t* __restrict__ prefix,
-                                                  int64_t n_items, int chunk,
-                                                  uint32_t* __restrict__ slot_of) {
-  const int64_t g = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
-  const int64_t item = g / chunk;
-  const int i = static_cast<int>(g - item * chunk);
-  if (item >= n_items || i >= static_cast<int>(__ldg(count + item))) return;
-  slot_of[__ldg(prefix + item) + i] = static_cast<uint32_t>(item * chunk + i);
-}
-
 // Phase A, thread = record: the record's exact mu -- the reference's
 // sequential-k f64 dot (sampler.cpp:111-119: product then add, no FMA) over
 // the batch row's theta and the word's phi, both read as 16-byte pairs --
@@ -817,19 +775,38 @@ __global__ void __launch_bounds__(256) k_rec_map(const uint32_t* __restrict__ co
 __global__ void __launch_bounds__(256) k_deferred_expand(
     BatchView bv, const double* __restrict__ theta_b64, const double* __restrict__ phi64,
     const double* __restrict__ mu_in, int K, double m_t, uint64_t seed, uint32_t t,
-    uint32_t sweep, const Deferred* __restrict__ deferred, const uint32_t* __restrict__ slot_of,
-    const uint32_t* __restrict__ n_rec, double* __restrict__ rec_mu,
+    uint32_t sweep, const Deferred* __restrict__ deferred, const uint32_t* __restrict__ rec_count,
+    int64_t n_items, int chunk, double* __restrict__ rec_mu,
     DeferredDraw* __restrict__ draws, unsigned long long* __restrict__ n_draws,
     unsigned long long draw_cap, unsigned long long* __restrict__ theta_counts,
     unsigned long long* __restrict__ phi_counts, int* __restrict__ err) {
   const int lane = threadIdx.x & 31;
-  const int64_t n = static_cast<int64_t>(__ldg(n_rec));
-  const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
-  for (int64_t r0 = blockIdx.x * static_cast<int64_t>(blockDim.x) + (threadIdx.x & ~31); r0 < n;
-       r0 += stride) {
-    const int64_t r = r0 + lane;
-    const bool live = r < n;
-    const uint32_t slot = live ? __ldg(slot_of + r) : 0u;
+  const int64_t warp_g = (blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x) >> 5;
+  const int64_t n_warps = (static_cast<int64_t>(gridDim.x) * blockDim.x) >> 5;
+  // a warp takes a window of kExpItems work items of k_sample_v2 (item i's
+  // records at slots i chunk + [0, rec_count[i])) and numbers their records
+  // densely (warp scan of the counts), lane = record, 32 at a time: early in
+  // training an item holds ~2 records, late ~chunk
+  constexpr int kExpItems = 8;
+  for (int64_t i0 = warp_g * kExpItems; i0 < n_items; i0 += n_warps * kExpItems) {
+   const uint32_t cnt_i = lane < kExpItems && i0 + lane < n_items ? __ldg(rec_count + i0 + lane) : 0u;
+   uint32_t inc_i = cnt_i;
+#pragma unroll
+   for (int o = 1; o < kExpItems; o <<= 1) {
+     const uint32_t v = __shfl_up_sync(0xffffffffu, inc_i, o);
+     if (lane >= o) inc_i += v;
+   }
+   const uint32_t excl_i = inc_i - cnt_i;
+   const uint32_t total = __shfl_sync(0xffffffffu, inc_i, kExpItems - 1);
+   for (uint32_t q0 = 0; q0 < total; q0 += 32) {
+    const uint32_t q = q0 + lane;
+    const bool live = q < total;
+    int j = 0;  // last window item with excl <= q
+#pragma unroll
+    for (int step = kExpItems / 2; step > 0; step >>= 1)
+      if (__shfl_sync(0xffffffffu, excl_i, j + step) <= q) j += step;
+    const uint32_t slot =
+        static_cast<uint32_t>((i0 + j) * chunk + (q - __shfl_sync(0xffffffffu, excl_i, j)));
     Deferred me{};
     double mu = 0.0;
     uint32_t cnt = 0;
@@ -884,6 +861,7 @@ __global__ void __launch_bounds__(256) k_deferred_expand(
         ++base;
       }
     }
+   }
   }
 }
 
@@ -909,16 +887,12 @@ void launch_deferred(const BatchView& bv, const double* tb64, const double* phi6
                      uint32_t* rec_count, int64_t n_items, int chunk, unsigned long long* n_deferred,
                      void* aux, int64_t max_records, int64_t draw_cap, unsigned long long* tc,
                      unsigned long long* pc, int* err, cudaStream_t st) {
-  uint32_t* prefix = rec_count + n_items;    // n_items + 1 entries (deferred_buffer_bytes)
-  uint32_t* slot_of = prefix + n_items + 1;   // dense record -> slot (max_records entries)
-  k_rec_prefix<<<1, kPrefixBlock, 0, st>>>(rec_count, n_items, prefix, n_deferred);
-  k_rec_map<<<grid_for(n_items * chunk, 256), 256, 0, st>>>(rec_count, prefix, n_items, chunk, slot_of);
   double* rec_mu = static_cast<double*>(aux);
   auto* n_draws = reinterpret_cast<unsigned long long*>(rec_mu + max_records);
   auto* draws = reinterpret_cast<DeferredDraw*>(n_draws + 2);
   cudaMemsetAsync(n_draws, 0, sizeof(unsigned long long), st);
   k_deferred_expand<<<148 * 8, 256, 0, st>>>(bv, tb64, phi64, mu, K, m_t, seed, t, sweep, rec,
-                                             slot_of, prefix + n_items, rec_mu, draws, n_draws,
+                                             rec_count, n_items, chunk, rec_mu, draws, n_draws,
                                              static_cast<unsigned long long>(draw_cap), tc, pc, err);
   k_deferred_draw<<<148 * 16, 256, 0, st>>>(bv, tb64, phi64, K, m_t, seed, t, sweep, rec, rec_mu,
                                             draws, n_draws, static_cast<unsigned long long>(draw_cap),
@@ -1194,7 +1168,7 @@ int launch_fast_kpl(const BatchView& bv, const double* tb64, const float* tb32, 
               bv, tb32, phi32, mu, muf, K, m_t, seed, t, sweep, chunk, tc, pc, rec, rec_count, n_deferred);
           launch_deferred(bv, tb64, phi64, mu, K, m_t, seed, t, sweep, rec, rec_count, n_items,
                           static_cast<int>(chunk), n_deferred, aux, max_records, draw_cap, tc, pc, err, st);
-          return launched + 4;
+          return launched + 3;
         }
       }
       return -1;  // caller passes phi counts for every other shape
@@ -1231,7 +1205,7 @@ int launch_fast_kpl(const BatchView& bv, const double* tb64, const float* tb32, 
   }
   launch_deferred(bv, tb64, phi64, mu, K, m_t, seed, t, sweep, rec, rec_count, n_items,
                   static_cast<int>(chunk), n_deferred, aux, max_records, draw_cap, tc, pc, err, st);
-  return launched + 4;
+  return launched + 3;
 }
 
 // k_expected: the deterministic expected-count path (z := rate,
@@ -1414,12 +1388,11 @@ int64_t deferred_max_records(int64_t nnz, int K) {
 }
 
 int64_t deferred_buffer_bytes(int64_t nnz, int K) {
-  // records, then one u32 count per work item (chunk >= 32 nonzeros) and
-  // their exclusive prefix (+ the total), then the dense record -> slot map
+  // records, then one u32 count per work item (chunk >= 32 nonzeros)
   const int n_slices = (K + 255) / 256;
   const int64_t items = ((nnz + 8 * 128) / 32 + 1) * n_slices;
-  return deferred_max_records(nnz, K) * static_cast<int64_t>(sizeof(Deferred) + sizeof(uint32_t)) +
-         (2 * items + 1) * static_cast<int64_t>(sizeof(uint32_t));
+  return deferred_max_records(nnz, K) * static_cast<int64_t>(sizeof(Deferred)) +
+         items * static_cast<int64_t>(sizeof(uint32_t));
 }
 
 int64_t deferred_aux_bytes(int64_t max_records, int64_t draw_cap) {
