@@ -517,26 +517,11 @@ def run_ours(args, cfg):
     samples_all = over_ranks(samples, "sum")
     value = samples_all / (dev_ms / 1000.0)
 
-    # ---- per-kernel CUDA-event timing on a separate profiled pass (the
-    # profiler synchronises after each sampling launch, so it stays out of
-    # the timed region above)
-    prof_steps = max(1, min(args.steps, 10))
-    trainer.profile(True)
-    prof_dev0 = torch.cuda.Event(enable_timing=True)
-    prof_dev1 = torch.cuda.Event(enable_timing=True)
-    prof_dev0.record(stream)
-    for _ in range(prof_steps):
-        period(t)
-        t += 1
-    prof_dev1.record(stream)
-    barrier()
-    prof = trainer.profile_read()
-    trainer.profile(False)
-    prof_ms = prof_dev0.elapsed_time(prof_dev1)
-
-    # ---- end to end through the public API with host buffers: per step the
-    # host batch ids go H2D inside Trainer.period and the batch theta rows
-    # (the step's result) come back D2H
+    # ---- end to end through the public API with host buffers, right after
+    # the timed region (the per-period cost drifts up as the model sharpens:
+    # more PTRS draws), on as many periods: per step the host batch ids go H2D
+    # inside Trainer.period and the batch theta rows (the step's result) come
+    # back D2H
     e2e_steps = max(1, args.steps)
     # a rank owns ~batch_fraction x D_global / N docs of each global batch
     # (the call fails loudly if a buffer is ever too small)
@@ -561,6 +546,23 @@ def run_ours(args, cfg):
            "d2h_bytes_per_step": d2h // e2e_steps,
            "how": "Trainer periods through the C ABI: host batch ids H2D, batch theta rows D2H"}
     gc.enable()
+    # ---- per-kernel CUDA-event timing on a separate profiled pass (the
+    # profiler synchronises after each sampling launch, so it stays out of
+    # the timed region above)
+    prof_steps = max(1, min(args.steps, 10))
+    trainer.profile(True)
+    prof_dev0 = torch.cuda.Event(enable_timing=True)
+    prof_dev1 = torch.cuda.Event(enable_timing=True)
+    prof_dev0.record(stream)
+    for _ in range(prof_steps):
+        period(t)
+        t += 1
+    prof_dev1.record(stream)
+    barrier()
+    prof = trainer.profile_read()
+    trainer.profile(False)
+    prof_ms = prof_dev0.elapsed_time(prof_dev1)
+
 
     # C1: the whole train() through the drop-in entry point (samelda_cu_train),
     # host buffers in and out, eval every 5 -- the call the reference's C++
@@ -570,11 +572,12 @@ def run_ours(args, cfg):
                                batch_fraction=cfg["batch_fraction"],
                                inner_sweeps=cfg["inner_sweeps"], t_max=cfg["t_max"], seed=1)
         runs = []
-        for _ in range(3):
+        for i in range(6):  # the first (untimed) loads the evaluation kernels
             c2 = S.Context(local)  # fresh context: corpus upload, init, everything
             t0 = time.perf_counter()
             _, trace = S.train(train, tcfg, wl.heldout, cfg["eval_every"], ctx=c2)
-            runs.append(time.perf_counter() - t0)
+            if i:
+                runs.append(time.perf_counter() - t0)
             c2.close()
         run_s = min(runs)
         s_run = cfg["inner_sweeps"] * cfg["m"] * train.n_tokens * cfg["t_max"]
@@ -587,7 +590,7 @@ def run_ours(args, cfg):
                "d2h_bytes_per_step": int(8 * (K * W + train.n_docs * K) / cfg["t_max"]),
                "how": f"samelda_cu_train (drop-in train(), sampler.cpp:269-353): fresh context, "
                       f"{cfg['t_max']} periods, eval every {cfg['eval_every']}, model download; "
-                      f"best of 3 runs {run_s:.3f}s", "final_ll": trace[-1]["ll"]}
+                      f"best of 5 runs after an untimed one, {run_s:.3f}s", "final_ll": trace[-1]["ll"]}
 
     heldout_ll = trainer.evaluate() if rank == 0 else None
 

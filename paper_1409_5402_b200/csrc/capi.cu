@@ -392,6 +392,16 @@ struct samelda_cu_ctx {
   // batch-theta read-back (samelda_cu_batch_theta_async): the D2H copy runs
   // on its own stream so it overlaps the next period's kernels; two row
   // buffers, each reused only after its previous copy has finished
+  // exact f64 mu on a side stream, concurrent with the fast sampler, once most
+  // nonzeros carry deferred draws (a converged model: PTRS at every dominant
+  // topic); the deferral rate is read back asynchronously, a sweep or more late
+  cudaStream_t mu_stream = nullptr;
+  cudaEvent_t mu_theta_ready = nullptr, mu_done = nullptr, defer_read = nullptr;
+  unsigned long long* h_deferred = nullptr;
+  int64_t defer_read_nnz = 0;
+  bool defer_read_pending = false;
+  double defer_frac = 0.0;
+  static constexpr double kConcurrentMu = 0.25;
   cudaStream_t copy_stream = nullptr;
   DevBuf rows2[2];
   cudaEvent_t rows_ready[2] = {nullptr, nullptr};
@@ -422,6 +432,17 @@ struct samelda_cu_ctx {
     if (copy_stream) {
       cudaStreamSynchronize(copy_stream);
       cudaStreamDestroy(copy_stream);
+    }
+    if (mu_stream) {
+      cudaStreamSynchronize(mu_stream);
+      cudaStreamDestroy(mu_stream);
+      cudaEventDestroy(mu_theta_ready);
+      cudaEventDestroy(mu_done);
+    }
+    if (h_deferred) {
+      cudaEventSynchronize(defer_read);
+      cudaEventDestroy(defer_read);
+      cudaFreeHost(h_deferred);
     }
     if (own_stream) cudaStreamDestroy(own_stream);
   }
@@ -639,12 +660,42 @@ struct samelda_cu_ctx {
       const int64_t draw_cap = draw_cap_for(records);
       void* rec = ensure<unsigned char>(deferred, scu::deferred_buffer_bytes(bv.nnz, K_));
       void* aux = ensure<unsigned char>(deferred_aux, scu::deferred_aux_bytes(records, draw_cap));
+      // the last readback of the deferral rate, if it has landed
+      if (defer_read_pending && cudaEventQuery(defer_read) == cudaSuccess) {
+        defer_frac = static_cast<double>(*h_deferred) / static_cast<double>(std::max<int64_t>(defer_read_nnz, 1));
+        defer_read_pending = false;
+      }
+      const double* mu_ex = nullptr;
+      if (mu_d == nullptr && defer_frac > kConcurrentMu) {
+        if (!mu_stream) {
+          ck(cudaStreamCreateWithFlags(&mu_stream, cudaStreamNonBlocking), "mu stream");
+          ck(cudaEventCreateWithFlags(&mu_theta_ready, cudaEventDisableTiming), "event");
+          ck(cudaEventCreateWithFlags(&mu_done, cudaEventDisableTiming), "event");
+        }
+        double* m = ensure<double>(mu, bv.nnz);
+        ck(cudaEventRecord(mu_theta_ready, stream), "event record");
+        ck(cudaStreamWaitEvent(mu_stream, mu_theta_ready, 0), "wait theta");
+        launches += scu::launch_sddmm(bv, theta_b, phi_wk, K_, m, mu_stream);
+        ck(cudaEventRecord(mu_done, mu_stream), "event record");
+        mu_ex = m;
+      }
+      unsigned long long* nd_ = ensure<unsigned long long>(n_deferred, 1);
       launches += scu::launch_sample_fast(bv, theta_b, theta_b32, phi_wk, phi_wk32, mu_d, K_,
                                           m_t_, seed, static_cast<uint32_t>(t),
-                                          static_cast<uint32_t>(sweep), tc_, pc_, rec,
-                                          ensure<unsigned long long>(n_deferred, 1), aux, draw_cap,
+                                          static_cast<uint32_t>(sweep), tc_, pc_, rec, nd_, aux, draw_cap,
                                           K_ > 256 ? ensure<float>(mu_f32, bv.nnz) : nullptr, d_err(),
-                                          stream);
+                                          stream, mu_ex, mu_ex ? mu_done : nullptr);
+      if (!defer_read_pending && mu_d == nullptr) {
+        if (!h_deferred) {
+          ck(cudaMallocHost(&h_deferred, sizeof(unsigned long long)), "pinned");
+          ck(cudaEventCreateWithFlags(&defer_read, cudaEventDisableTiming), "event");
+        }
+        ck(cudaMemcpyAsync(h_deferred, nd_, sizeof(unsigned long long), cudaMemcpyDeviceToHost, stream),
+           "defer readback");
+        ck(cudaEventRecord(defer_read, stream), "event record");
+        defer_read_nnz = bv.nnz;
+        defer_read_pending = true;
+      }
       tick(need_phi ? kSampleLast : kSample, false);
       if (profile) {
         unsigned long long nd = 0;

@@ -1135,8 +1135,15 @@ int launch_fast_kpl(const BatchView& bv, const double* tb64, const float* tb32, 
                     const float* phi32, const double* mu, int K, double m_t, uint64_t seed,
                     uint32_t t, uint32_t sweep, unsigned long long* tc, unsigned long long* pc,
                     void* deferred, unsigned long long* n_deferred, void* aux, int64_t draw_cap,
-                    float* mu_f, int* err, cudaStream_t st) {
+                    float* mu_f, int* err, cudaStream_t st, const double* mu_exact,
+                    cudaEvent_t mu_ready) {
   const int n_slices = (K + kWarp * KPL - 1) / (kWarp * KPL);
+  // the deferred passes take the caller's mu, else an exact mu computed
+  // concurrently on another stream (mu_exact, ready at mu_ready), else their own
+  const double* mu_defer = mu ? mu : mu_exact;
+  auto wait_mu = [&] {
+    if (!mu && mu_exact && mu_ready) cudaStreamWaitEvent(st, mu_ready, 0);
+  };
   const int64_t chunk = work_chunk(bv.nnz, n_slices);
   const int64_t items = (bv.nnz + chunk - 1) / chunk;
   const int warps = kFastBlock / kWarp;
@@ -1166,7 +1173,8 @@ int launch_fast_kpl(const BatchView& bv, const double* tb64, const float* tb32, 
         if (full && musrc == 0 && n_slices == 1) {
           k_sample_v2<8, true, 0, 4, kDecDefault, 0, false><<<grid, kFastBlock, 0, st>>>(
               bv, tb32, phi32, mu, muf, K, m_t, seed, t, sweep, chunk, tc, pc, rec, rec_count, n_deferred);
-          launch_deferred(bv, tb64, phi64, mu, K, m_t, seed, t, sweep, rec, rec_count, n_items,
+          wait_mu();
+          launch_deferred(bv, tb64, phi64, mu_defer, K, m_t, seed, t, sweep, rec, rec_count, n_items,
                           static_cast<int>(chunk), n_deferred, aux, max_records, draw_cap, tc, pc, err, st);
           return launched + 3;
         }
@@ -1203,7 +1211,8 @@ int launch_fast_kpl(const BatchView& bv, const double* tb64, const float* tb32, 
 #undef SCU_V2
 #undef SCU_V2_LAUNCH
   }
-  launch_deferred(bv, tb64, phi64, mu, K, m_t, seed, t, sweep, rec, rec_count, n_items,
+  wait_mu();
+  launch_deferred(bv, tb64, phi64, mu_defer, K, m_t, seed, t, sweep, rec, rec_count, n_items,
                   static_cast<int>(chunk), n_deferred, aux, max_records, draw_cap, tc, pc, err, st);
   return launched + 3;
 }
@@ -1453,7 +1462,7 @@ int launch_sample_fast(const BatchView& bv, const double* theta_b64, const float
                        double m_t, uint64_t seed, uint32_t t, uint32_t sweep,
                        unsigned long long* tc, unsigned long long* pc, void* deferred,
                        unsigned long long* n_deferred, void* aux, int64_t draw_cap, float* mu_f,
-                       int* err, cudaStream_t st) {
+                       int* err, cudaStream_t st, const double* mu_exact, cudaEvent_t mu_ready) {
   if (bv.nnz == 0) return 0;
   // lane = topic, 8 topics per lane (k_sample_v2); K > 256 in topic slices of
   // 256 with the full mu from a k_mu_f32 pre-pass.  SAMELDA_SAMPLER=x runs
@@ -1464,15 +1473,15 @@ int launch_sample_fast(const BatchView& bv, const double* theta_b64, const float
                          nullptr, nullptr, err, st);
   if (K <= 32)
     return launch_fast_kpl<1>(bv, theta_b64, theta_b32, phi64, phi32, mu, K, m_t, seed, t, sweep, tc, pc,
-                              deferred, n_deferred, aux, draw_cap, mu_f, err, st);
+                              deferred, n_deferred, aux, draw_cap, mu_f, err, st, mu_exact, mu_ready);
   if (K <= 64)
     return launch_fast_kpl<2>(bv, theta_b64, theta_b32, phi64, phi32, mu, K, m_t, seed, t, sweep, tc, pc,
-                              deferred, n_deferred, aux, draw_cap, mu_f, err, st);
+                              deferred, n_deferred, aux, draw_cap, mu_f, err, st, mu_exact, mu_ready);
   if (K <= 128)
     return launch_fast_kpl<4>(bv, theta_b64, theta_b32, phi64, phi32, mu, K, m_t, seed, t, sweep, tc, pc,
-                              deferred, n_deferred, aux, draw_cap, mu_f, err, st);
+                              deferred, n_deferred, aux, draw_cap, mu_f, err, st, mu_exact, mu_ready);
   return launch_fast_kpl<8>(bv, theta_b64, theta_b32, phi64, phi32, mu, K, m_t, seed, t, sweep, tc, pc,
-                            deferred, n_deferred, aux, draw_cap, mu_f, err, st);
+                            deferred, n_deferred, aux, draw_cap, mu_f, err, st, mu_exact, mu_ready);
 }
 
 // glibc lgamma(k + 1) for the PTRS acceptance test (poisson.cuh), per device
