@@ -654,33 +654,37 @@ __device__ __forceinline__ double fold_rcp(double x) {
   return __fma_rn(r, e, r);
 }
 
-// Kernel shape: NJ topic pairs per lane (K <= 64 NJ), G fold cells per group
-// (one transposed butterfly per group), NW warps, RES = the first group of
-// every warp keeps its rows in registers across sweeps.
-template <int NJ_, int G_, int NW_, bool RES_>
+// Kernel shape: NJ topic pairs per lane (K <= 64 NJ), NW warps; NRES
+// register-resident groups of G fold cells per warp (their rows stay in
+// registers across sweeps); the other cells in streaming groups of GS (rows
+// from shared memory or L2), one transposed butterfly per group.
+template <int NJ_, int G_, int NW_, int NRES_, int GS_>
 struct FoldCfg {
-  static constexpr int NJ = NJ_, G = G_, NW = NW_;
-  static constexpr bool RES = RES_;
+  static constexpr int NJ = NJ_, G = G_, NW = NW_, NRES = NRES_, GS = GS_;
   static constexpr int NT = 32 * NW;
-  static constexpr int LG = G == 1 ? 0 : G == 2 ? 1 : G == 4 ? 2 : G == 8 ? 3 : 4;
-  static constexpr int SH = 5 - LG;         // lane >> SH = the lane's cell in a group
-  static constexpr int KP = 64 * NJ;        // padded topics (row stride in shared memory)
-  static constexpr int GW = G * NW;         // cells per round of groups
-  static constexpr int S0 = RES ? GW : 0;   // first cell past the register-resident ones
+  static constexpr int KP = 64 * NJ;         // padded topics (row stride in shared memory)
+  static constexpr int S0 = NRES * G * NW;   // first cell past the register-resident ones
+  static constexpr int GW = GS * NW;         // streaming cells per round of groups
   static constexpr int TPT = (KP + NT - 1) / NT;  // topics per thread in the epilogue
+};
+
+template <int G>
+struct GroupShape {
+  static constexpr int LG = G == 1 ? 0 : G == 2 ? 1 : G == 4 ? 2 : G == 8 ? 3 : 4;
+  static constexpr int SH = 5 - LG;  // lane >> SH = the lane's cell in a group
 };
 
 // fold-list entries staged per document (longer lists are read from global)
 constexpr int kFoldList = 768;
 
-template <class C>
-__device__ __forceinline__ void fold_dots(const double2 (&th)[C::NJ],
-                                          const double2 (&r)[C::G][C::NJ], double (&v)[C::G]) {
+template <int NJ, int G>
+__device__ __forceinline__ void fold_dots(const double2 (&th)[NJ], const double2 (&r)[G][NJ],
+                                          double (&v)[G]) {
 #pragma unroll
-  for (int c = 0; c < C::G; ++c) {
+  for (int c = 0; c < G; ++c) {
     double a = 0.0, b = 0.0;
 #pragma unroll
-    for (int j = 0; j < C::NJ; ++j) {
+    for (int j = 0; j < NJ; ++j) {
       a = __fma_rn(th[j].x, r[c][j].x, a);
       b = __fma_rn(th[j].y, r[c][j].y, b);
     }
@@ -692,19 +696,18 @@ __device__ __forceinline__ void fold_dots(const double2 (&th)[C::NJ],
 // list) into the warp's g sums: partial dots, one transposed butterfly (the
 // lanes of cell c end with its mu), s = c / mu (eval.cpp:38-44; mu <= 0 or
 // NaN: 0), g_k += s_c phi[w_c][k] (eval.cpp:45-49)
-template <class C>
-__device__ __forceinline__ void fold_group(const double2 (&th)[C::NJ],
-                                           const double2 (&r)[C::G][C::NJ],
-                                           double2 (&acc)[C::NJ], int cnt, int lane) {
-  double v[C::G];
-  fold_dots<C>(th, r, v);
-  fold_tree<C::G / 2, 16>(v, lane);
+template <int NJ, int G>
+__device__ __forceinline__ void fold_group(const double2 (&th)[NJ], const double2 (&r)[G][NJ],
+                                           double2 (&acc)[NJ], int cnt, int lane) {
+  double v[G];
+  fold_dots<NJ, G>(th, r, v);
+  fold_tree<G / 2, 16>(v, lane);
   const double s = v[0] > 0.0 ? static_cast<double>(cnt) * fold_rcp(v[0]) : 0.0;
 #pragma unroll
-  for (int c = 0; c < C::G; ++c) {
-    const double sc = __shfl_sync(0xffffffffu, s, c << C::SH);
+  for (int c = 0; c < G; ++c) {
+    const double sc = __shfl_sync(0xffffffffu, s, c << GroupShape<G>::SH);
 #pragma unroll
-    for (int j = 0; j < C::NJ; ++j) {
+    for (int j = 0; j < NJ; ++j) {
       acc[j].x = __fma_rn(sc, r[c][j].x, acc[j].x);
       acc[j].y = __fma_rn(sc, r[c][j].y, acc[j].y);
     }
@@ -738,14 +741,15 @@ __global__ void __launch_bounds__(C::NT, 1) k_eval_fold(
     const double* __restrict__ phi_wk, int K, double alpha, int sweeps, int R,
     double* __restrict__ doc_logp, int64_t* __restrict__ doc_scored,
     double* __restrict__ theta_out, int* __restrict__ err) {
-  constexpr int NJ = C::NJ, G = C::G, NW = C::NW, NT = C::NT, SH = C::SH, KP = C::KP;
-  constexpr int GW = C::GW, S0 = C::S0, TPT = C::TPT;
+  constexpr int NJ = C::NJ, G = C::G, GS = C::GS, NW = C::NW, NT = C::NT, KP = C::KP;
+  constexpr int GW = C::GW, S0 = C::S0, TPT = C::TPT, NRES = C::NRES;
+  constexpr int SH = GroupShape<G>::SH, SHS = GroupShape<GS>::SH;
   extern __shared__ __align__(16) double smem[];
   double* red = smem;                                // [NW][KP] per-warp g
   double* ths = red + NW * KP;                       // [KP] theta (zero past K)
   int2* lst_s = reinterpret_cast<int2*>(ths + KP);   // [kFoldList] (word, count)
   double* rows = ths + KP + kFoldList;               // [R][KP] staged fold rows
-  __shared__ double s_part[NW], s_term[GW];
+  __shared__ double s_part[NW], s_term[G * NW];
   __shared__ long long s_cnt[NW];
   __shared__ int64_t s_doc;
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
@@ -779,17 +783,18 @@ __global__ void __launch_bounds__(C::NT, 1) k_eval_fold(
       *reinterpret_cast<double2*>(rows + f * KP + k) =
           load_pair_g(phi_wk + static_cast<int64_t>(__ldg(&gl[S0 + f].x)) * K, k, K, keven);
     }
-    double2 res[C::RES ? G : 1][NJ];
-    int res_cnt = 0;
-    if constexpr (C::RES) {
+    double2 res[NRES > 0 ? NRES : 1][G][NJ];
+    int res_cnt[NRES > 0 ? NRES : 1];
+#pragma unroll
+    for (int q = 0; q < NRES; ++q) {  // group q of warp w: cells q G NW + G w + [0, G)
 #pragma unroll
       for (int c = 0; c < G; ++c) {
-        const int f = G * wid + c;
-        if (f < F) fold_row_g<NJ>(res[c], phi_wk, __ldg(&gl[f].x), K, keven, lane);
-        else fold_row_zero<NJ>(res[c]);
+        const int f = q * G * NW + G * wid + c;
+        if (f < F) fold_row_g<NJ>(res[q][c], phi_wk, __ldg(&gl[f].x), K, keven, lane);
+        else fold_row_zero<NJ>(res[q][c]);
       }
-      const int my = G * wid + (lane >> SH);
-      res_cnt = my < F ? __ldg(&gl[my].y) : 0;
+      const int my = q * G * NW + G * wid + (lane >> SH);
+      res_cnt[q] = my < F ? __ldg(&gl[my].y) : 0;
     }
     double2 th[NJ];
 #pragma unroll
@@ -807,22 +812,22 @@ __global__ void __launch_bounds__(C::NT, 1) k_eval_fold(
       double2 acc[NJ];
 #pragma unroll
       for (int j = 0; j < NJ; ++j) acc[j] = make_double2(0.0, 0.0);
-      if constexpr (C::RES) {
-        if (G * wid < F) fold_group<C>(th, res, acc, res_cnt, lane);
-      }
-      for (int f0 = S0 + G * wid; f0 < F; f0 += GW) {
-        const int my = f0 + (lane >> SH);
-        const int cnt = my < F ? lst[my].y : 0;
-        double2 r[G][NJ];
-        if (f0 + G <= s_end) {  // whole group staged
 #pragma unroll
-          for (int c = 0; c < G; ++c)
+      for (int q = 0; q < NRES; ++q)
+        if (q * G * NW + G * wid < F) fold_group<NJ, G>(th, res[q], acc, res_cnt[q], lane);
+      for (int f0 = S0 + GS * wid; f0 < F; f0 += GW) {
+        const int my = f0 + (lane >> SHS);
+        const int cnt = my < F ? lst[my].y : 0;
+        double2 r[GS][NJ];
+        if (f0 + GS <= s_end) {  // whole group staged
+#pragma unroll
+          for (int c = 0; c < GS; ++c)
 #pragma unroll
             for (int j = 0; j < NJ; ++j)
               r[c][j] = *reinterpret_cast<const double2*>(rows + (f0 - S0 + c) * KP + 64 * j + 2 * lane);
         } else {  // L2 (and the staged / past-the-end edge)
 #pragma unroll
-          for (int c = 0; c < G; ++c) {
+          for (int c = 0; c < GS; ++c) {
             const int f = f0 + c;
             if (f < s_end) {
 #pragma unroll
@@ -835,7 +840,7 @@ __global__ void __launch_bounds__(C::NT, 1) k_eval_fold(
             }
           }
         }
-        fold_group<C>(th, r, acc, cnt, lane);
+        fold_group<NJ, GS>(th, r, acc, cnt, lane);
       }
       // ---- epilogue (eval.cpp:51-61).  total = K alpha + sum_k theta_k g_k
       // from per-warp partials, so theta = next / total and the stopping test
@@ -881,12 +886,13 @@ __global__ void __launch_bounds__(C::NT, 1) k_eval_fold(
 
     // scoring (eval.cpp:125-145): the document's log p is summed in cell
     // order with the reference's rounding (term = c * log p, then add), one
-    // round of GW cells at a time
+    // round of G NW cells at a time
     const int Sn = L.n_score[doc];
     const int2* sl = L.score + base;
+    constexpr int GWS = G * NW;
     double lp = 0.0;
     long long scored = 0;
-    for (int r0 = 0; r0 < Sn; r0 += GW) {
+    for (int r0 = 0; r0 < Sn; r0 += GWS) {
       const int f0 = r0 + G * wid;
       double2 r[G][NJ];
 #pragma unroll
@@ -895,7 +901,7 @@ __global__ void __launch_bounds__(C::NT, 1) k_eval_fold(
         else fold_row_zero<NJ>(r[c]);
       }
       double v[G];
-      fold_dots<C>(th, r, v);
+      fold_dots<NJ, G>(th, r, v);
       fold_tree<G / 2, 16>(v, lane);
       const int my = f0 + (lane >> SH);
       if ((lane & ((1 << SH) - 1)) == 0) {
@@ -910,7 +916,7 @@ __global__ void __launch_bounds__(C::NT, 1) k_eval_fold(
       }
       __syncthreads();
       if (tid == 0) {
-        const int n = min(GW, Sn - r0);
+        const int n = min(GWS, Sn - r0);
         for (int i = 0; i < n; ++i) lp = __dadd_rn(lp, s_term[i]);
       }
       __syncthreads();
@@ -1068,11 +1074,15 @@ int launch_eval_fold(const int64_t* doc_offsets, const EvalLists& lists, int64_t
   // K <= 256 measured at NYTimes shape (30K test docs, 127 fold cells on
   // average): G=4 / 8 warps / register-resident group 45.2 ms; 16 warps 46.9
   // (no resident group) and 50.3 (G=2); 8 warps without it 50.1
-  if (K <= 64) return SCU_FOLD(1, 16, 8, true);
-  if (K <= 128) return SCU_FOLD(2, 8, 8, true);
-  if (K <= 256) return SCU_FOLD(4, 4, 8, true);
-  if (K <= 512) return SCU_FOLD(8, 2, 8, false);
-  if (K <= 1024) return SCU_FOLD(16, 1, 8, false);
+  // K <= 256 measured at NYTimes shape (30K test docs, 127 fold cells on
+  // average): one resident group of 4 per warp, streaming groups of 4, 8
+  // warps 42.4 ms; two resident groups 43.5 (streaming groups of 2) / 49.0;
+  // 16 warps 46.9 (no resident group) and 50.3 (groups of 2)
+  if (K <= 64) return SCU_FOLD(1, 16, 8, 1, 16);
+  if (K <= 128) return SCU_FOLD(2, 8, 8, 1, 8);
+  if (K <= 256) return SCU_FOLD(4, 4, 8, 1, 4);
+  if (K <= 512) return SCU_FOLD(8, 2, 8, 0, 2);
+  if (K <= 1024) return SCU_FOLD(16, 1, 8, 0, 1);
 #undef SCU_FOLD
   return -1;  // K > 1024: the exact kernels
 }
