@@ -81,6 +81,11 @@ CONFIGS = {
                          inner_sweeps=2, schedule="constant", mode="throughput",
                          workload="NYTimes-shaped synthetic corpus, K=256, m=100, bf=0.05, "
                                   "2 inner sweeps, throughput mode (f32, own random streams)"),
+    "nytimes-multinomial": dict(baseline=1, corpus="nytimes", n_topics=256, m=100.0,
+                                batch_fraction=0.05, inner_sweeps=2, schedule="constant",
+                                mode="multinomial",
+                                workload="NYTimes-shaped synthetic corpus, K=256, m=100, bf=0.05, "
+                                         "2 inner sweeps, multinomial(c m) replicas (own streams)"),
     "nytimes-converged": dict(baseline=1, corpus="nytimes", n_topics=256, m=100.0,
                               batch_fraction=0.05, inner_sweeps=2, schedule="constant",
                               pre_periods=100,
@@ -345,9 +350,9 @@ def run_reference(args, cfg):
         return
     scaling = args.scaling
     record = config_record(cfg, world, scaling)
-    if cfg.get("mode") == "expected" or cfg.get("pre_periods"):
-        why = ("the reference has no expected-count mode (sampler.cpp draws Poisson replicas only)"
-               if cfg.get("mode") == "expected" else
+    if cfg.get("mode") in ("expected", "multinomial") or cfg.get("pre_periods"):
+        why = (f"the reference has no {cfg['mode']} mode (sampler.cpp draws Poisson replicas only)"
+               if cfg.get("mode") in ("expected", "multinomial") else
                "the converged-model state takes the reference ~100 full periods (~7 min) to reach")
         print(json.dumps({"impl": "reference", "unavailable": why, "config": record}), flush=True)
         return
@@ -406,10 +411,10 @@ def bytes_per_unit(cfg, final_sweep: bool) -> tuple[int, int]:
     per batch nonzero 8 (word id + count) + e_phi K (phi row) [+ e_cnt K (phi-count row),
     final sweep only: earlier sweeps scatter no phi counts]; per batch doc 8 + e_th K
     (theta row) + e_cnt K (theta counts).  Parity: f64 phi/theta, int32 counts;
-    expected: f64 rows and f64 counts; throughput: f32 rows, int32 counts."""
+    expected: f64 rows and f64 counts; throughput and multinomial: f32 rows, int32 counts."""
     K = cfg["n_topics"]
     mode = cfg.get("mode", "parity")
-    e_row, e_cnt = {"expected": (8, 8), "throughput": (4, 4)}.get(mode, (8, 4))
+    e_row, e_cnt = {"expected": (8, 8), "throughput": (4, 4), "multinomial": (4, 4)}.get(mode, (8, 4))
     # which sweeps scatter phi counts: the final one; every one in expected mode and in
     # the parity kernel's multi-slice shapes (K != 256)
     scatter = final_sweep or mode == "expected" or (mode == "parity" and K != 256)
@@ -455,7 +460,8 @@ def run_ours(args, cfg):
     scfg = S.SamplerConfig(n_topics=cfg["n_topics"], m=cfg["m"], schedule=cfg["schedule"],
                            batch_fraction=cfg["batch_fraction"], inner_sweeps=cfg["inner_sweeps"],
                            t_max=t_max, seed=1,
-                           mode={"expected": S.MODE_EXPECTED, "throughput": S.MODE_THROUGHPUT}.get(
+                           mode={"expected": S.MODE_EXPECTED, "throughput": S.MODE_THROUGHPUT,
+                                 "multinomial": S.MODE_MULTINOMIAL}.get(
                                cfg.get("mode"), S.MODE_PARITY))
     trainer = S.Trainer(train, scfg, ctx=ctx)
     if rank == 0:
@@ -670,7 +676,7 @@ def run_ours(args, cfg):
             "metric": METRIC, "value": value, "unit": "samples/s",
             "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": dev_ms / args.steps, "higher_is_better": True, "scaling": scaling,
-            "vs_baseline": None, "dtype": {"throughput": "f32"}.get(cfg.get("mode"), "f64"),
+            "vs_baseline": None, "dtype": {"throughput": "f32", "multinomial": "f32"}.get(cfg.get("mode"), "f64"),
             "data": "synthetic",
             "config": config_record(cfg, world, scaling),
             "corpus": corpus,
@@ -680,7 +686,8 @@ def run_ours(args, cfg):
                                   "8 + 8K (f64 phi row) + 4K (int32 phi-count row, final sweep "
                                   "only), per batch doc 8 + 12K; rows re-read from L2 count, so "
                                   "frac can exceed the DRAM fraction -- see dram",
-                         "kernel": {"expected": "k_expected", "throughput": "k_sample_thru"}.get(
+                         "kernel": {"expected": "k_expected", "throughput": "k_sample_thru",
+                                    "multinomial": "k_sample_multi"}.get(
                              cfg.get("mode"), "k_sample_v2 + deferred (parity)"),
                          "peak_kind": peaks_kind, "per_sweep": sweeps, "dram": dram,
                          "alg_bytes_per_launch": alg_bytes / max(prof["sample_launches"], 1),

@@ -36,6 +36,12 @@ extern "C" {
 #define SAMELDA_CU_MODE_THROUGHPUT 2 /* the same Poisson replicas on this library's own
                                         random streams in f32: statistically, not
                                         bit-for-bit, the reference's sampler */
+#define SAMELDA_CU_MODE_MULTINOMIAL 3 /* north_star's multinomial(c m) replicas: per
+                                         nonzero floor(c m_t) (+1 with the fractional
+                                         part's probability) categorical trials, so
+                                         E z = c m_t r as the Poisson replicas and
+                                         sum_k z_k = the trial count; own f32 streams,
+                                         K <= 1024; no reference implementation */
 
 /* AnnealSchedule (sampler.hpp:17) */
 #define SAMELDA_CU_SCHEDULE_CONSTANT 0
@@ -129,6 +135,18 @@ int samelda_cu_sample_counts_fast(samelda_cu_ctx* ctx, const samelda_cu_corpus* 
                                   int64_t mu_len, const int32_t* doc_ids, double m_t,
                                   uint64_t seed, int64_t t, int32_t sweep, int64_t* theta_counts,
                                   int64_t* phi_counts);
+
+/* Multinomial mode (SAMELDA_CU_MODE_MULTINOMIAL): sample_counts with the
+ * c m_t replicas of each nonzero drawn jointly as Multinomial(n, theta phi /
+ * mu), n = floor(c m_t) (+1 with probability frac(c m_t)); this library's own
+ * streams, deterministic for given inputs.  mu is validated for alignment and
+ * not read.  K <= 1024. */
+int samelda_cu_sample_counts_multinomial(samelda_cu_ctx* ctx, const samelda_cu_corpus* corpus,
+                                         const double* theta_batch, int64_t B, int64_t K_theta,
+                                         const double* phi, int64_t K, int64_t W, const double* mu,
+                                         int64_t mu_len, const int32_t* doc_ids, double m_t,
+                                         uint64_t seed, int64_t t, int32_t sweep,
+                                         int64_t* theta_counts, int64_t* phi_counts);
 
 /* Deterministic factored path: sample_counts with z := E[z] = rate, f64. */
 int samelda_cu_expected_counts(samelda_cu_ctx* ctx, const samelda_cu_corpus* corpus,

@@ -244,8 +244,10 @@ void validate_config(const samelda_cu_config* c) {
   if (!(c->init_noise >= 0.0) || !std::isfinite(c->init_noise))
     fail(SAMELDA_CU_CONFIG, "init_noise must be finite and >= 0");
   if (c->mode != SAMELDA_CU_MODE_PARITY && c->mode != SAMELDA_CU_MODE_EXPECTED &&
-      c->mode != SAMELDA_CU_MODE_THROUGHPUT)
+      c->mode != SAMELDA_CU_MODE_THROUGHPUT && c->mode != SAMELDA_CU_MODE_MULTINOMIAL)
     fail(SAMELDA_CU_CONFIG, "unknown sampling mode %d", c->mode);
+  if (c->mode == SAMELDA_CU_MODE_MULTINOMIAL && c->n_topics > 1024)
+    fail(SAMELDA_CU_CONFIG, "multinomial mode supports n_topics <= 1024");
   if (c->schedule < 0 || c->schedule > 3) fail(SAMELDA_CU_CONFIG, "unknown schedule %d", c->schedule);
 }
 
@@ -606,7 +608,7 @@ struct samelda_cu_ctx {
       ensure<unsigned long long>(tc, B_ * K_);
       ensure<unsigned long long>(pc, W_ * K_);
       if (K_ > 256) ensure<float>(mu_f32, nnz_);
-      if (mode == SAMELDA_CU_MODE_THROUGHPUT) {
+      if (mode == SAMELDA_CU_MODE_THROUGHPUT || mode == SAMELDA_CU_MODE_MULTINOMIAL) {
         for (int i = 0; i < 2; ++i) stage(B_);
         return;
       }
@@ -645,10 +647,20 @@ struct samelda_cu_ctx {
       // a non-final inner sweep of the K = 256 period kernel skips the phi-count
       // scatter (only the last sweep's phi counts feed update_model)
       const bool skip_phi =
-          !need_phi && mu_d == nullptr && (K_ == 256 || mode == SAMELDA_CU_MODE_THROUGHPUT);
+          !need_phi && mu_d == nullptr &&
+          (K_ == 256 || mode == SAMELDA_CU_MODE_THROUGHPUT || mode == SAMELDA_CU_MODE_MULTINOMIAL);
       if (skip_phi) pc_ = nullptr;
       else ck(cudaMemsetAsync(pc_, 0, sizeof(unsigned long long) * std::max<int64_t>(W_ * K_, 1), stream), "zero pc");
       tick(need_phi ? kSampleLast : kSample, true);
+      if (mode == SAMELDA_CU_MODE_MULTINOMIAL) {
+        const int r = scu::launch_sample_multinomial(bv, theta_b32, phi_wk32, K_, m_t_, seed,
+                                                     static_cast<uint32_t>(t), static_cast<uint32_t>(sweep),
+                                                     tc_, pc_, d_err(), stream);
+        if (r < 0) fail(SAMELDA_CU_CONFIG, "multinomial mode supports n_topics <= 1024");
+        launches += r;
+        tick(need_phi ? kSampleLast : kSample, false);
+        return;
+      }
       if (mode == SAMELDA_CU_MODE_THROUGHPUT) {
         launches += scu::launch_sample_throughput(
             bv, theta_b32, phi_wk32, K_, m_t_, seed, static_cast<uint32_t>(t), static_cast<uint32_t>(sweep),
@@ -972,6 +984,18 @@ int samelda_cu_sample_counts_fast(samelda_cu_ctx* ctx, const samelda_cu_corpus* 
   return guarded(ctx, [&] {
     sample_call(ctx, corpus, theta_batch, B, K_theta, phi, K, W, mu, mu_len, doc_ids, m_t, seed,
                 t, sweep, SAMELDA_CU_MODE_THROUGHPUT, theta_counts, phi_counts);
+  });
+}
+
+int samelda_cu_sample_counts_multinomial(samelda_cu_ctx* ctx, const samelda_cu_corpus* corpus,
+                                         const double* theta_batch, int64_t B, int64_t K_theta,
+                                         const double* phi, int64_t K, int64_t W, const double* mu,
+                                         int64_t mu_len, const int32_t* doc_ids, double m_t,
+                                         uint64_t seed, int64_t t, int32_t sweep,
+                                         int64_t* theta_counts, int64_t* phi_counts) {
+  return guarded(ctx, [&] {
+    sample_call(ctx, corpus, theta_batch, B, K_theta, phi, K, W, mu, mu_len, doc_ids, m_t, seed,
+                t, sweep, SAMELDA_CU_MODE_MULTINOMIAL, theta_counts, phi_counts);
   });
 }
 

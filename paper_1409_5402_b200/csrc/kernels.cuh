@@ -92,6 +92,13 @@ int launch_sample_throughput(const BatchView& bv, const float* theta_b32, const 
                              double m_t, uint64_t seed, uint32_t t, uint32_t sweep,
                              unsigned long long* theta_counts, unsigned long long* phi_counts,
                              float* mu_f_scratch, cudaStream_t st);
+// Multinomial mode: per nonzero, floor(c m_t) (+1 with the fractional
+// part's probability) categorical trials over the K topics (K <= 1024;
+// returns -1 above), on this library's own streams.
+int launch_sample_multinomial(const BatchView& bv, const float* theta_b32, const float* phi32, int K,
+                              double m_t, uint64_t seed, uint32_t t, uint32_t sweep,
+                              unsigned long long* theta_counts, unsigned long long* phi_counts,
+                              int* err, cudaStream_t st);
 int64_t deferred_max_records(int64_t nnz, int K);
 int64_t deferred_buffer_bytes(int64_t nnz, int K);
 // fills the device's glibc lgamma table (call once per device, after cudaSetDevice)

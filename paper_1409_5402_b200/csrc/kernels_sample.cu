@@ -1437,6 +1437,180 @@ static void launch_thru(const BatchView& bv, const float* theta_b32, const float
   }
 }
 
+// ----------------------------------------------- sample (multinomial mode)
+// k_sample_multi: north_star item 3's multinomial(c m) replicas (SURVEY 7
+// step 7, optional; no reference implementation).  Per batch nonzero (doc d,
+// word w, count c) the c m_t replicated tokens are drawn jointly:
+// n = floor(c m_t) + [u < frac(c m_t)] trials (unbiased rounding), each a
+// categorical draw over the K topics with probabilities theta_dk phi_kw / mu,
+// so z ~ Multinomial(n, r): E z_k = c m_t r_k as for the Poisson replicas,
+// and sum_k z_k = n exactly.  On this library's own streams in f32.
+//   * warp = work item of `chunk` consecutive nonzeros; lane l owns topics
+//     [l KPL, (l + 1) KPL) for the cdf: f32 products, a lane-local prefix,
+//     one warp scan, the cdf into the warp's shared-memory row;
+//   * trials 128 at a time (one Philox-4x32-10 block per lane gives 4
+//     uniforms, counter {round << 5 | lane, w, d, t}, key (seed,
+//     tag(multinomial, sweep))): u * total, binary search for the first k
+//     with cdf_k > u, a shared-memory histogram increment;
+//   * the histogram is flushed lane = topic mod 32 (k = lane + 32 j): theta
+//     counts per document in registers, phi counts with one coalesced u64
+//     RED per nonzero topic.
+// A row without mass (mu < 1e-30) draws uniformly over the K topics (the
+// reference's fallback weight 1 / K, sampler.cpp:160-166).
+template <int KPL, bool PHI>
+struct MultiShape {
+  static constexpr int WPB = KPL >= 16 ? 4 : 8;  // warps per block (shared rows of KP)
+};
+
+template <int KPL, bool PHI>
+__global__ void __launch_bounds__(MultiShape<KPL, PHI>::WPB * 32) k_sample_multi(
+    BatchView bv, const float* __restrict__ theta_b32, const float* __restrict__ phi32, int K,
+    double m_t, uint64_t seed, uint32_t t, uint32_t sweep, int64_t chunk,
+    unsigned long long* __restrict__ theta_counts, unsigned long long* __restrict__ phi_counts,
+    int* __restrict__ err) {
+  constexpr int KP = kWarp * KPL, WPB = MultiShape<KPL, PHI>::WPB;
+  __shared__ float s_cdf[WPB][KP];
+  __shared__ uint32_t s_hist[WPB][KP];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int64_t item = static_cast<int64_t>(blockIdx.x) * WPB + warp;
+  const int64_t p0 = item * chunk;
+  const int64_t p1 = min(p0 + chunk, bv.nnz);
+  if (p0 >= p1) return;
+  float* cdf = s_cdf[warp];
+  uint32_t* hist = s_hist[warp];
+#pragma unroll
+  for (int j = 0; j < KPL; ++j) hist[lane + kWarp * j] = 0u;
+  uint32_t k0, k1;
+  stream_key(seed, make_tag(kMultinomial, sweep, 0), k0, k1);
+  int cur_b = -1;
+  uint32_t acc[KPL];
+#pragma unroll
+  for (int j = 0; j < KPL; ++j) acc[j] = 0u;
+  auto flush = [&](int b) {
+#pragma unroll
+    for (int j = 0; j < KPL; ++j) {
+      const int k = lane + kWarp * j;
+      if (k < K && acc[j]) atomicAdd(theta_counts + static_cast<int64_t>(b) * K + k,
+                                     static_cast<unsigned long long>(acc[j]));
+      acc[j] = 0u;
+    }
+  };
+  for (int64_t g0 = p0; g0 < p1; g0 += kWarp) {
+    const int64_t p = g0 + lane;
+    int32_t b = 0, d = 0, w = 0, c = 0;
+    if (p < p1) {
+      b = static_cast<int32_t>(find_row(bv.batch_prefix, bv.B, p));
+      d = __ldg(bv.batch_docs + b);
+      const int64_t gi = __ldg(bv.doc_offsets + d) + (p - __ldg(bv.batch_prefix + b));
+      w = __ldg(bv.word_ids + gi);
+      c = __ldg(bv.counts + gi);
+    }
+    const int n_here = static_cast<int>(min(static_cast<int64_t>(kWarp), p1 - g0));
+    for (int i = 0; i < n_here; ++i) {
+      const int32_t bi = __shfl_sync(0xffffffffu, b, i);
+      const uint32_t di = static_cast<uint32_t>(__shfl_sync(0xffffffffu, d, i) + static_cast<int32_t>(bv.doc_base));
+      const int32_t wi = __shfl_sync(0xffffffffu, w, i);
+      const int32_t ci = __shfl_sync(0xffffffffu, c, i);
+      if (bi != cur_b) {
+        if (cur_b >= 0) flush(cur_b);
+        cur_b = bi;
+      }
+      // cdf over the lane's contiguous topics, then the warp scan
+      const float* trow = theta_b32 + static_cast<int64_t>(bi) * K;
+      const float* prow = phi32 + static_cast<int64_t>(wi) * K;
+      float pr[KPL];
+      float run = 0.0f;
+#pragma unroll
+      for (int j = 0; j < KPL; ++j) {
+        const int k = lane * KPL + j;
+        pr[j] = k < K ? __fmul_rn(__ldg(trow + k), __ldg(prow + k)) : 0.0f;
+        run = __fadd_rn(run, pr[j]);
+      }
+      float incl = run;
+#pragma unroll
+      for (int o = 1; o < kWarp; o <<= 1) {
+        const float v = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl = __fadd_rn(incl, v);
+      }
+      float total = __shfl_sync(0xffffffffu, incl, kWarp - 1);
+      if (!isfinite(total)) {
+        if (lane == 0) atomicOr(err, kErrNumerical);
+        continue;
+      }
+      const bool uniform = !(total >= 1e-30f);
+      float base = __fsub_rn(incl, run);
+#pragma unroll
+      for (int j = 0; j < KPL; ++j) {
+        const int k = lane * KPL + j;
+        base = uniform ? static_cast<float>(min(k + 1, K)) : __fadd_rn(base, pr[j]);
+        cdf[k] = base;
+      }
+      if (uniform) total = static_cast<float>(K);
+      __syncwarp();
+      // n = floor(c m_t) + [u < frac(c m_t)]
+      const double cm = m_t * static_cast<double>(ci);
+      const double fl = floor(cm);
+      const U4 fr = philox10(U4{0x80000000u, static_cast<uint32_t>(wi), di, t}, k0, k1);
+      const int64_t n = static_cast<int64_t>(fl) + (u64_to_uniform(join64(fr.x, fr.y)) < cm - fl ? 1 : 0);
+      for (int64_t r0 = 0; r0 < n; r0 += 4 * kWarp) {
+        const U4 y = philox10(U4{static_cast<uint32_t>(r0 >> 7) << 5 | static_cast<uint32_t>(lane),
+                                 static_cast<uint32_t>(wi), di, t}, k0, k1);
+        const uint32_t ys[4] = {y.x, y.y, y.z, y.w};
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          if (r0 + q * kWarp + lane >= n) continue;
+          float u = __fmul_rn(__fmul_rn(static_cast<float>(ys[q] >> 8), 0x1p-24f), total);
+          if (!(u < total)) u = 0.0f;  // f32 rounding at the top end
+          int lo = 0;  // first k with cdf_k > u (the last cdf entry >= total > u)
+#pragma unroll
+          for (int step = KP >> 1; step > 0; step >>= 1)
+            if (cdf[lo + step - 1] <= u) lo += step;
+          atomicAdd(hist + min(lo, K - 1), 1u);
+        }
+      }
+      __syncwarp();
+#pragma unroll
+      for (int j = 0; j < KPL; ++j) {
+        const int k = lane + kWarp * j;
+        const uint32_t z = hist[k];
+        hist[k] = 0u;
+        acc[j] += z;
+        if (PHI && z && k < K)
+          red_add_u64(phi_counts + static_cast<int64_t>(wi) * K + k, static_cast<unsigned long long>(z));
+      }
+      __syncwarp();
+    }
+  }
+  if (cur_b >= 0) flush(cur_b);
+}
+
+template <int KPL>
+void launch_multi_kpl(const BatchView& bv, const float* tb32, const float* phi32, int K, double m_t,
+                      uint64_t seed, uint32_t t, uint32_t sweep, unsigned long long* tc,
+                      unsigned long long* pc, int* err, cudaStream_t st) {
+  constexpr int WPB = MultiShape<KPL, true>::WPB;
+  const int64_t chunk = work_chunk(bv.nnz, 1);
+  const int64_t items = (bv.nnz + chunk - 1) / chunk;
+  const unsigned grid = static_cast<unsigned>((items + WPB - 1) / WPB);
+  if (pc) k_sample_multi<KPL, true><<<grid, WPB * 32, 0, st>>>(bv, tb32, phi32, K, m_t, seed, t, sweep, chunk, tc, pc, err);
+  else k_sample_multi<KPL, false><<<grid, WPB * 32, 0, st>>>(bv, tb32, phi32, K, m_t, seed, t, sweep, chunk, tc, pc, err);
+}
+
+int launch_sample_multinomial(const BatchView& bv, const float* theta_b32, const float* phi32, int K,
+                              double m_t, uint64_t seed, uint32_t t, uint32_t sweep,
+                              unsigned long long* tc, unsigned long long* pc, int* err,
+                              cudaStream_t st) {
+  if (bv.nnz == 0) return 0;
+  if (K <= 32) launch_multi_kpl<1>(bv, theta_b32, phi32, K, m_t, seed, t, sweep, tc, pc, err, st);
+  else if (K <= 64) launch_multi_kpl<2>(bv, theta_b32, phi32, K, m_t, seed, t, sweep, tc, pc, err, st);
+  else if (K <= 128) launch_multi_kpl<4>(bv, theta_b32, phi32, K, m_t, seed, t, sweep, tc, pc, err, st);
+  else if (K <= 256) launch_multi_kpl<8>(bv, theta_b32, phi32, K, m_t, seed, t, sweep, tc, pc, err, st);
+  else if (K <= 512) launch_multi_kpl<16>(bv, theta_b32, phi32, K, m_t, seed, t, sweep, tc, pc, err, st);
+  else if (K <= 1024) launch_multi_kpl<32>(bv, theta_b32, phi32, K, m_t, seed, t, sweep, tc, pc, err, st);
+  else return -1;
+  return 1;
+}
+
 int launch_sample_throughput(const BatchView& bv, const float* theta_b32, const float* phi32, int K,
                              double m_t, uint64_t seed, uint32_t t, uint32_t sweep,
                              unsigned long long* tc, unsigned long long* pc, float* mu_f,

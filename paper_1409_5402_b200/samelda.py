@@ -30,6 +30,7 @@ _LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "libsamelda
 MODE_PARITY = 0
 MODE_EXPECTED = 1
 MODE_THROUGHPUT = 2  # own f32 random streams: statistical (not bit) parity
+MODE_MULTINOMIAL = 3  # multinomial(c m) replicas on own streams (no reference counterpart)
 SCHEDULES = {"constant": 0, "linear": 1, "log": 2, "invlinear": 3}
 
 
@@ -92,6 +93,8 @@ SIGNATURES = [
     ("samelda_cu_sample_counts", C.c_int, [_P, _CP, _P, _I64, _I64, _P, _I64, _I64, _P, _I64,
                                            _P, _D, _U64, _I64, _I32, _P, _P]),
     ("samelda_cu_sample_counts_fast", C.c_int, [_P, _CP, _P, _I64, _I64, _P, _I64, _I64, _P, _I64,
+                                           _P, _D, _U64, _I64, _I32, _P, _P]),
+    ("samelda_cu_sample_counts_multinomial", C.c_int, [_P, _CP, _P, _I64, _I64, _P, _I64, _I64, _P, _I64,
                                            _P, _D, _U64, _I64, _I32, _P, _P]),
     ("samelda_cu_expected_counts", C.c_int, [_P, _CP, _P, _I64, _I64, _P, _I64, _I64, _P, _I64,
                                              _P, _D, _P, _P]),
@@ -410,9 +413,10 @@ def sample_counts(theta_batch, phi, mu, corpus, doc_ids, m_t, seed, t, sweep=0, 
                   ctx: Context | None = None, mode: int = MODE_PARITY) -> SampledCounts:
     """sampler.cpp:125-195 on the device: reference-identical Poisson replicas
     (MODE_PARITY), or the same law on this library's own f32 streams
-    (MODE_THROUGHPUT; mu is then only checked for alignment)."""
-    if mode not in (MODE_PARITY, MODE_THROUGHPUT):
-        raise ConfigError("sample_counts: mode must be MODE_PARITY or MODE_THROUGHPUT")
+    (MODE_THROUGHPUT), or the c m_t replicas of each nonzero drawn jointly as
+    a multinomial (MODE_MULTINOMIAL); mu is then only checked for alignment."""
+    if mode not in (MODE_PARITY, MODE_THROUGHPUT, MODE_MULTINOMIAL):
+        raise ConfigError("sample_counts: mode must be MODE_PARITY, MODE_THROUGHPUT or MODE_MULTINOMIAL")
     ctx = ctx or default_context()
     ctx._train_token = None  # per-call use replaces a Trainer's device state
     corpus = Corpus.of(corpus)
@@ -425,7 +429,9 @@ def sample_counts(theta_batch, phi, mu, corpus, doc_ids, m_t, seed, t, sweep=0, 
     tc = np.zeros(max(B * K, 1), np.int64)
     pc = np.zeros(max(W * K, 1), np.int64)
     cs = corpus._struct()
-    fn = ctx.lib.samelda_cu_sample_counts if mode == MODE_PARITY else ctx.lib.samelda_cu_sample_counts_fast
+    fn = {MODE_PARITY: ctx.lib.samelda_cu_sample_counts,
+          MODE_THROUGHPUT: ctx.lib.samelda_cu_sample_counts_fast,
+          MODE_MULTINOMIAL: ctx.lib.samelda_cu_sample_counts_multinomial}[mode]
     ctx.check(fn(
         ctx.h, C.byref(cs), _ptr(theta_batch if theta_batch.size else np.zeros(1)), B, Kt,
         _ptr(phi), K, W, _ptr(mu if len(mu) else np.zeros(1)), len(mu), _ptr(ids), float(m_t),

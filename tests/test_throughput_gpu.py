@@ -108,7 +108,7 @@ def test_train_ll_trajectory_matches_parity_mode(S, port, K):
 def test_unknown_mode_rejected(S, port):
     g = port.make_corpus(10, 20, 2, 10.0, 1)
     with pytest.raises(S.ConfigError):
-        S.Trainer(g, S.SamplerConfig(n_topics=4, mode=3))
+        S.Trainer(g, S.SamplerConfig(n_topics=4, mode=4))
 
 
 @pytest.mark.parametrize("K", [64, 256, 300])
