@@ -582,7 +582,9 @@ __global__ void __launch_bounds__(kOrderedBlock) k_ordered_ll(
 // (1e-12 relative on ll) instead of the reference's summation order: the
 // exact kernels above are latency-bound on sequential f64 chains (a K-term
 // chain per fold cell and sweep) and re-read every fold row from L2 twice per
-// sweep.  Here one CTA (8 warps) owns a document at a time:
+// sweep.  Here one CTA owns a document at a time (K <= 256: two CTAs of 4
+// warps per SM, so one document's barriers and staging overlap the other's
+// cells):
 //   * lane l owns topics k = 64 j + 2 l + {0, 1} (j < NJ), theta in registers;
 //   * a warp takes groups of G consecutive fold cells (G x 2 NJ = 32 row
 //     values per lane); per group: the lane's partial dots (FMA), one
@@ -658,9 +660,10 @@ __device__ __forceinline__ double fold_rcp(double x) {
 // register-resident groups of G fold cells per warp (their rows stay in
 // registers across sweeps); the other cells in streaming groups of GS (rows
 // from shared memory or L2), one transposed butterfly per group.
-template <int NJ_, int G_, int NW_, int NRES_, int GS_>
+template <int NJ_, int G_, int NW_, int NRES_, int GS_, int CPS_ = 1>
 struct FoldCfg {
   static constexpr int NJ = NJ_, G = G_, NW = NW_, NRES = NRES_, GS = GS_;
+  static constexpr int CPS = CPS_;  // CTAs (documents) per SM
   static constexpr int NT = 32 * NW;
   static constexpr int KP = 64 * NJ;         // padded topics (row stride in shared memory)
   static constexpr int S0 = NRES * G * NW;   // first cell past the register-resident ones
@@ -736,7 +739,7 @@ __device__ unsigned long long g_fold_prof[8];  // cycles of thread 0: stage, cel
 #endif
 
 template <class C>
-__global__ void __launch_bounds__(C::NT, 1) k_eval_fold(
+__global__ void __launch_bounds__(C::NT, C::CPS) k_eval_fold(
     const int64_t* __restrict__ doc_offsets, EvalLists L, int64_t n_docs,
     const double* __restrict__ phi_wk, int K, double alpha, int sweeps, int R,
     double* __restrict__ doc_logp, int64_t* __restrict__ doc_scored,
@@ -945,16 +948,22 @@ int launch_fold(const int64_t* doc_offsets, const EvalLists& L, int64_t n_docs,
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+  int per_sm = 0;
+  cudaDeviceGetAttribute(&per_sm, cudaDevAttrMaxSharedMemoryPerMultiprocessor, dev);
   cudaFuncAttributes fa{};
   cudaFuncGetAttributes(&fa, k_eval_fold<C>);
   const size_t fixed = (static_cast<size_t>(C::NW + 1) * C::KP + kFoldList) * sizeof(double);
-  const size_t budget = static_cast<size_t>(optin) - fa.sharedSizeBytes;
+  // per CTA: the SM's shared memory split CPS ways, less each CTA's static
+  // part and the 1 KB the runtime reserves per block
+  const size_t cap = C::CPS == 1 ? static_cast<size_t>(optin)
+                                 : static_cast<size_t>(per_sm) / C::CPS - 1024;
+  const size_t budget = std::min(static_cast<size_t>(optin), cap) - fa.sharedSizeBytes;
   const size_t row = static_cast<size_t>(C::KP) * sizeof(double);
   const int R = budget > fixed ? static_cast<int>((budget - fixed) / row) : 0;
   const size_t bytes = fixed + static_cast<size_t>(R) * row;
   static std::atomic<unsigned long long> configured{0};
   smem_opt_in(k_eval_fold<C>, static_cast<int>(bytes), configured);
-  const int64_t blocks = min(n_docs, static_cast<int64_t>(sms));
+  const int64_t blocks = min(n_docs, static_cast<int64_t>(sms) * C::CPS);
 #ifdef SAMELDA_FOLD_PROF
   unsigned long long z[8] = {};
   cudaMemcpyToSymbolAsync(g_fold_prof, z, sizeof(z), 0, cudaMemcpyHostToDevice, st);
@@ -1075,12 +1084,13 @@ int launch_eval_fold(const int64_t* doc_offsets, const EvalLists& lists, int64_t
   // average): G=4 / 8 warps / register-resident group 45.2 ms; 16 warps 46.9
   // (no resident group) and 50.3 (G=2); 8 warps without it 50.1
   // K <= 256 measured at NYTimes shape (30K test docs, 127 fold cells on
-  // average): one resident group of 4 per warp, streaming groups of 4, 8
-  // warps 42.4 ms; two resident groups 43.5 (streaming groups of 2) / 49.0;
-  // 16 warps 46.9 (no resident group) and 50.3 (groups of 2)
+  // average): two documents per SM (CTAs of 4 warps, two resident groups of
+  // 4 per warp, streaming groups of 4) 40.6 ms; one document per SM with 8
+  // warps and one resident group 42.4 (two: 43.5 / 49.0); 16 warps 46.9 /
+  // 50.3
   if (K <= 64) return SCU_FOLD(1, 16, 8, 1, 16);
   if (K <= 128) return SCU_FOLD(2, 8, 8, 1, 8);
-  if (K <= 256) return SCU_FOLD(4, 4, 8, 1, 4);
+  if (K <= 256) return SCU_FOLD(4, 4, 4, 2, 4, 2);
   if (K <= 512) return SCU_FOLD(8, 2, 8, 0, 2);
   if (K <= 1024) return SCU_FOLD(16, 1, 8, 0, 1);
 #undef SCU_FOLD
