@@ -7,7 +7,8 @@ train, heldout = bench.single_gpu_corpus("nytimes")
 ctx = S.Context(0)
 stream = torch.cuda.Stream(device=0); torch.cuda.set_stream(stream); ctx.set_stream(stream.cuda_stream)
 T = 100
-tr = S.Trainer(train, S.SamplerConfig(n_topics=256, m=100.0, batch_fraction=0.05, t_max=T, seed=1), ctx=ctx)
+MODE = int(os.environ.get("MODE", "0"))
+tr = S.Trainer(train, S.SamplerConfig(n_topics=256, m=100.0, batch_fraction=0.05, t_max=T, seed=1, mode=MODE), ctx=ctx)
 tr.set_heldout(heldout, seed=1)
 eng = DIST.CudaEngine(tr, 0)
 st = DIST.ShardedTrainer(eng, train.n_docs, 0, train.n_docs, train.doc_tokens(), 0.05, 1, 100.0, "constant", T)
