@@ -468,6 +468,30 @@ def test_train_k256_production_kernel_bit_exact(port, m, schedule):
     np.testing.assert_allclose([r["ll"] for r in trace], [r["ll"] for r in otrace], rtol=1e-12)
 
 
+def test_converged_regime_concurrent_exact_mu_bit_exact(port):
+    """The converged-model path: once most nonzeros carry deferred (PTRS)
+    draws the exact f64 mu comes from k_sddmm_staged on a side stream
+    instead of the expand pass ("Two regimes").  m = 3000 puts a
+    PTRS draw on nearly every nonzero from the first period; phi, theta and
+    the ll trace must still equal the reference's bit for bit."""
+    g = port.make_corpus(120, 400, 12, 150.0, 41)
+    tr, te = port.split_holdout(g, 0.1, 3)
+    cfg = dict(n_topics=256, m=3000.0, t_max=8, batch_fraction=0.5, seed=12)
+    # the regime is really the converged one: the deferral rate per sweep
+    t = S.Trainer(tr, S.SamplerConfig(**cfg))
+    stream = S.MinibatchStream(tr.n_docs, 0.5, 12)
+    t.profile(True)
+    t.period(stream.next(), 0, 3000.0, S.rho_schedule(0, 1.0, 0.5))
+    prof = t.profile_read()
+    t.profile(False)
+    assert prof["deferred"] > 0.5 * prof["nnz"], prof
+    model, trace = S.train(tr, S.SamplerConfig(**cfg), te, 2)
+    ophi, otheta, otrace = port.train(tr, TrainConfig(**cfg), te, 2)
+    np.testing.assert_array_equal(model.phi, ophi)
+    np.testing.assert_array_equal(model.theta, otheta)
+    np.testing.assert_allclose([r["ll"] for r in trace], [r["ll"] for r in otrace], rtol=1e-12)
+
+
 @pytest.mark.parametrize("K", [300, 520])
 def test_train_sliced_k_bit_exact(port, K):
     """K > 256 on the period path: topic slices with the k_mu_f32 pre-pass."""
