@@ -78,3 +78,42 @@ def test_heldout_eval_at_the_timed_config(setup):
     tr.set_heldout(sub, seed=SEED)
     assert tr.evaluate() == pytest.approx(want, rel=1e-12, abs=0)
     assert S.perword_loglik(phi, sub, ALPHA, SEED, ctx=tr.ctx) == pytest.approx(want, rel=1e-12, abs=0)
+
+
+def test_converged_period_bit_exact_at_the_timed_config():
+    """The converged-model regime at the timed shape: after 80 untimed periods
+    nearly every nonzero carries a deferred PTRS draw, the exact mu comes from
+    the concurrent staged SDDMM ("Two regimes"); one more period
+    must equal the compiled reference's period on the downloaded model bit
+    for bit."""
+    import bench
+    from oracle import Ref
+    from paper_1409_5402_b200 import samelda as S
+    ref = Ref()
+    train, _ = bench.single_gpu_corpus("nytimes")
+    cfg = S.SamplerConfig(n_topics=256, m=100.0, batch_fraction=0.05, t_max=100, seed=SEED)
+    tr = S.Trainer(train, cfg)
+    stream = S.MinibatchStream(train.n_docs, 0.05, SEED)
+    for t in range(80):
+        tr.period(stream.next(), t, 100.0, S.rho_schedule(t, 1.0, 0.5))
+    m0 = tr.model()
+    phi, theta = m0.phi.copy(), m0.theta.copy()
+    t, m_t = 80, 100.0
+    batch = stream.next()
+    rho = S.rho_schedule(t, 1.0, 0.5)
+    tr.profile(True)
+    tr.period(batch, t, m_t, rho)
+    prof = tr.profile_read()
+    tr.profile(False)
+    assert prof["deferred"] > 0.9 * prof["nnz"], prof  # the converged regime
+    nt = os.cpu_count() or 1
+    tb = np.ascontiguousarray(theta[batch])
+    for sweep in range(2):
+        mu = ref.sddmm(tb, phi, train, batch, nt)
+        tc, pc = ref.sample_counts(tb, phi, mu, train, batch, m_t, SEED, t, sweep, nt)
+        if sweep == 0:
+            tb = tc / m_t + ALPHA
+    theta, phi = ref.update_model(theta, phi, batch, tc, pc, m_t, rho, ALPHA, BETA)
+    dev = tr.model()
+    np.testing.assert_array_equal(dev.phi, phi)
+    np.testing.assert_array_equal(dev.theta[batch], theta[batch])
