@@ -606,6 +606,29 @@ def run_ours(args, cfg):
 
     heldout_ll = trainer.evaluate() if rank == 0 else None
 
+    # the drop-in entry point at this shape: samelda_cu_train (what the
+    # reference's C++ train() shim calls) from host buffers on a fresh context
+    # -- corpus upload, init, 20 periods, one held-out evaluation, model
+    # download -- beside the reference arm's period rate
+    dropin = None
+    if world == 1 and cfg["corpus"] != "c1" and cfg.get("mode", "parity") == "parity":
+        T = 20
+        tcfg = S.SamplerConfig(n_topics=cfg["n_topics"], m=cfg["m"], schedule=cfg["schedule"],
+                               batch_fraction=cfg["batch_fraction"],
+                               inner_sweeps=cfg["inner_sweeps"], t_max=T, seed=1)
+        c3 = S.Context(local)
+        t0 = time.perf_counter()
+        _, dtrace = S.train(train, tcfg, wl.heldout, T, ctx=c3)
+        d_s = time.perf_counter() - t0
+        c3.close()
+        tokens_run = float(dtrace[-1]["passes"]) * train.n_tokens
+        dropin = {"value": cfg["inner_sweeps"] * cfg["m"] * tokens_run / d_s, "unit": "samples/s",
+                  "seconds": d_s, "periods": T,
+                  "how": "samelda_cu_train (drop-in train(), sampler.cpp:269-353) on a fresh "
+                         "context: corpus upload, init, 20 periods, one held-out evaluation, "
+                         "model download (phi W x K + theta D x K, f64)",
+                  "final_ll": dtrace[-1]["ll"]}
+
     # ---- roofline of the dominant kernel (sampling), algorithmic bytes per sweep kind
     peaks, peaks_kind = load_peaks()
     peak = float(peaks.get("hbm_gbs", PEAKS_FALLBACK["hbm_gbs"]))
@@ -698,6 +721,7 @@ def run_ours(args, cfg):
                          "profiled_steps": prof_steps},
             "cpu_baseline": cpu,
             "e2e": e2e,
+            "dropin_train": dropin,
             "gpu_launches": launches,
             "clocks": clk,
             "heldout_ll": heldout_ll,
