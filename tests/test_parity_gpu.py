@@ -468,6 +468,40 @@ def test_train_k256_production_kernel_bit_exact(port, m, schedule):
     np.testing.assert_allclose([r["ll"] for r in trace], [r["ll"] for r in otrace], rtol=1e-12)
 
 
+def test_long_run_bit_exact_through_the_regime_change():
+    """40 periods (10 passes) at K = 256, m = 100 on a 1,500-document corpus:
+    the run crosses from the early regime (~1% of nonzeros defer) past the
+    25% deferral rate at which the exact mu moves to the concurrent side-stream
+    SDDMM (measured ~29% by period 39) and must stay bit-identical to the
+    compiled reference's train() the whole way (phi, theta, the ll trace every
+    10 periods)."""
+    from oracle import Ref
+    ref = Ref()
+    g = ref.make_corpus(1500, 1000, 16, 120.0, 5)
+    tr, te = ref.split_holdout(g, 0.1, 4)
+    cfg = dict(n_topics=256, m=100.0, t_max=40, batch_fraction=0.25, seed=8)
+    model, trace = S.train(tr, S.SamplerConfig(**cfg), te, 10)
+    rphi, rtheta, rtrace = ref.train(tr, TrainConfig(**cfg), te, 10)
+    np.testing.assert_array_equal(model.phi, rphi)
+    np.testing.assert_array_equal(model.theta, rtheta)
+    np.testing.assert_allclose([r["ll"] for r in trace], [r["ll"] for r in rtrace], rtol=1e-12)
+    # the same 40 periods through a Trainer: the deferral rate at the start and the end
+    t = S.Trainer(tr, S.SamplerConfig(**cfg))
+    stream = S.MinibatchStream(tr.n_docs, 0.25, 8)
+    rates = []
+    for p in range(40):
+        probe = p in (0, 39)
+        if probe:
+            t.profile(True)
+        t.period(stream.next(), p, 100.0, S.rho_schedule(p, 1.0, 0.5))
+        if probe:
+            prof = t.profile_read()
+            t.profile(False)
+            rates.append(prof["deferred"] / prof["nnz"])
+    assert rates[0] < 0.05 and rates[1] > 0.25, rates
+    np.testing.assert_array_equal(t.model().phi, rphi)
+
+
 def test_converged_regime_concurrent_exact_mu_bit_exact(port):
     """The converged-model path: once most nonzeros carry deferred (PTRS)
     draws the exact f64 mu comes from k_sddmm_staged on a side stream
