@@ -313,7 +313,7 @@ __device__ __forceinline__ float ex2_approx(float x) {
   return y;
 }
 
-// Fast-path Poisson decision (fast_poisson3 + fast_poisson_tail below; the
+// Fast-path Poisson decision (fast_poisson3 + fast_poisson_tail_z below; the
 // error bound above).  z is the first k with u <= cdf_k; a draw is left
 // undecided when u falls inside a threshold's band, or the search passes
 // z = 40.  The first three thresholds (z in {0, 1, 2}, ~99% of draws at
@@ -517,7 +517,8 @@ __device__ __forceinline__ uint32_t fast_poisson3(float lam, float M, float Mb, 
 // read from constant tables (the step index is the same for every lane still
 // searching: one broadcast load) instead of rcp.approx and running sums; the
 // correctly rounded 1/k is within the 1-ulp rcp.approx the budget assumed.
-// Returns z, or sets *und (also at z = 40).
+// Returns z, or kUndZ when undecided (also past z = 40): the outcome as a
+// value, so no flag state lives across the loop.
 __constant__ float c_tail_inv[41] = {
     0.0f,        1.0f,         0.5f,         1.0f / 3,  0.25f,     0.2f,      1.0f / 6,
     1.0f / 7,    0.125f,       1.0f / 9,     0.1f,      1.0f / 11, 1.0f / 12, 1.0f / 13,
@@ -532,8 +533,8 @@ __constant__ float c_tail_rk[41] = {
     1.62e-5f, 1.68e-5f, 1.74e-5f, 1.8e-5f,  1.86e-5f, 1.92e-5f, 1.98e-5f, 2.04e-5f, 2.1e-5f,
     2.16e-5f, 2.22e-5f, 2.28e-5f, 2.34e-5f, 2.4e-5f};
 
-__device__ __forceinline__ uint32_t fast_poisson_tail(float lam, float u, float t1, float c2,
-                                                      bool* und) {
+constexpr uint32_t kUndZ = 64;
+__device__ __forceinline__ uint32_t fast_poisson_tail_z(float lam, float u, float t1, float c2) {
   const float r0 = __fmaf_rn(2.4e-7f, lam, 4.8e-7f);
   const float pl = __fmul_rn(3e-6f, lam);
   float pmf = __fmul_rn(t1, __fmul_rn(lam, 0.5f)), cdf = c2;
@@ -544,10 +545,9 @@ __device__ __forceinline__ uint32_t fast_poisson_tail(float lam, float u, float 
     const float mk = __fmaf_rn(cdf, __fadd_rn(r0, c_tail_rk[k]), __fmaf_rn(pmf, pl, 2.5e-7f));
     const float dk = __fsub_rn(u, cdf);
     if (dk < -mk) return k;
-    if (!(dk > mk)) break;
+    if (!(dk > mk)) return kUndZ;
   }
-  *und = true;
-  return 0;
+  return kUndZ;
 }
 
 // PHI = false: a non-final inner sweep -- only the last sweep's phi counts feed
@@ -730,24 +730,31 @@ __global__ void __launch_bounds__(kFastBlock, MINB) k_sample_v2(
           float t1, c2;
           const float M = __fmaf_rn(prod[j], mslope, 2e-6f);
           uint32_t z = fast_poisson3<DEC>(lam, M, __fmul_rn(M, 0x1p100f), u, und, t1, c2);
-          bool park = false;
-          if (TAIL == 0) {
-            if (z == 3 && !und) z = fast_poisson_tail(lam, u, t1, c2, &und);
-          } else {
-            park = z == 3 && !und;
+          if constexpr (TAIL == 0) {
+            // z carries the band flag (kUndZ: undecided): no flag state lives
+            // across the search (first sweep 3.18 -> 3.14 ms)
+            z = und ? kUndZ : z;
+            if (z == 3) z = fast_poisson_tail_z(lam, u, t1, c2);
+            if (!FULL && kbase + lane + kWarp * j >= K) z = 0;
+#ifdef SAMELDA_DEFER_STATS
+            if (FULL || kbase + lane + kWarp * j < K) defer_stats(nz_exact, prod[j], lam, z == kUndZ);
+#endif
+            defer_bits += (z & kUndZ) << j;  // bit 6 + j
+            z &= kUndZ - 1;
+            acc[j >> 1] += (j & 1) ? (z << 16) : z;
+            if (PHI && (FULL || kbase + lane + kWarp * j < K)) red_add_u64(pc + kWarp * j, z);
+            continue;
           }
+          bool park = z == 3 && !und;  // TAIL 1
           if (!FULL && kbase + lane + kWarp * j >= K) {
             und = false;
             z = 0;
             park = false;
           }
-          if (TAIL && park) {
+          if (park) {
             s_park[warp][j][lane] = make_float2(lam, u);
             parked |= 1u << j;
           }
-#ifdef SAMELDA_DEFER_STATS
-          if (FULL || kbase + lane + kWarp * j < K) defer_stats(nz_exact, prod[j], lam, und);
-#endif
           if (und) {
             defer_bits |= 1u << j;
             z = 0;
@@ -756,6 +763,7 @@ __global__ void __launch_bounds__(kFastBlock, MINB) k_sample_v2(
           if (PHI && (FULL || kbase + lane + kWarp * j < K)) red_add_u64(pc + kWarp * j, z);
         }
       }
+      if (TAIL == 0) defer_bits >>= 6;
       if (TAIL && __any_sync(0xffffffffu, parked != 0)) {
         // finish parked draws: z = 3 was counted; add z - 3, or undo the 3
         // (u64 wrap-around) and defer the draw when the search is undecided
@@ -769,8 +777,8 @@ __global__ void __launch_bounds__(kFastBlock, MINB) k_sample_v2(
             const float e0 = ex2_approx(__fmul_rn(st.x, -1.4426950408889634f));
             const float t1 = __fmul_rn(e0, st.x);
             const float c2 = __fmaf_rn(t1, __fmul_rn(st.x, 0.5f), __fadd_rn(e0, t1));
-            bool und = false;
-            const uint32_t z = fast_poisson_tail(st.x, st.y, t1, c2, &und);
+            const uint32_t z = fast_poisson_tail_z(st.x, st.y, t1, c2);
+            const bool und = z == kUndZ;
             const unsigned long long delta =
                 und ? ~2ull : static_cast<unsigned long long>(z - 3u);
             if (und) defer_bits |= 1u << j;
