@@ -828,7 +828,16 @@ __global__ void __launch_bounds__(C::NT, C::CPS) k_eval_fold(
 #pragma unroll
             for (int j = 0; j < NJ; ++j)
               r[c][j] = *reinterpret_cast<const double2*>(rows + (f0 - S0 + c) * KP + 64 * j + 2 * lane);
-        } else {  // L2 (and the staged / past-the-end edge)
+        } else if (f0 >= s_end && f0 + GS <= F && K == KP) {
+          // whole group from L2, full-width rows: unconditional 16-byte loads
+          // (the generic path below costs ~160 extra instructions per group)
+#pragma unroll
+          for (int c = 0; c < GS; ++c) {
+            const double2* row = reinterpret_cast<const double2*>(phi_wk + static_cast<int64_t>(lst[f0 + c].x) * KP);
+#pragma unroll
+            for (int j = 0; j < NJ; ++j) r[c][j] = __ldg(row + 32 * j + lane);
+          }
+        } else {  // the staged / L2 boundary and the past-the-end edge
 #pragma unroll
           for (int c = 0; c < GS; ++c) {
             const int f = f0 + c;
@@ -836,6 +845,12 @@ __global__ void __launch_bounds__(C::NT, C::CPS) k_eval_fold(
 #pragma unroll
               for (int j = 0; j < NJ; ++j)
                 r[c][j] = *reinterpret_cast<const double2*>(rows + (f - S0) * KP + 64 * j + 2 * lane);
+            } else if (K == KP) {
+              // past the end: the last cell's row with count 0 (adds exactly 0)
+              const double2* row = reinterpret_cast<const double2*>(
+                  phi_wk + static_cast<int64_t>(lst[min(f, F - 1)].x) * KP);
+#pragma unroll
+              for (int j = 0; j < NJ; ++j) r[c][j] = __ldg(row + 32 * j + lane);
             } else if (f < F) {
               fold_row_g<NJ>(r[c], phi_wk, lst[f].x, K, keven, lane);
             } else {
@@ -1081,16 +1096,14 @@ int launch_eval_fold(const int64_t* doc_offsets, const EvalLists& lists, int64_t
   launch_fold<FoldCfg<__VA_ARGS__>>(doc_offsets, lists, n_docs, phi_wk, K, alpha, sweeps,      \
                                     doc_logp, doc_scored, theta_out, err, st)
   // K <= 256 measured at NYTimes shape (30K test docs, 127 fold cells on
-  // average): G=4 / 8 warps / register-resident group 45.2 ms; 16 warps 46.9
-  // (no resident group) and 50.3 (G=2); 8 warps without it 50.1
-  // K <= 256 measured at NYTimes shape (30K test docs, 127 fold cells on
-  // average): two documents per SM (CTAs of 4 warps, two resident groups of
-  // 4 per warp, streaming groups of 4) 40.6 ms; one document per SM with 8
-  // warps and one resident group 42.4 (two: 43.5 / 49.0); 16 warps 46.9 /
-  // 50.3
+  // average), after the lean L2 path (unconditional 16-byte row loads): four
+  // documents per SM, CTAs of 4 warps, no register-resident group, streaming
+  // groups of 4 -- 29.5 ms; two documents per SM with two resident groups per
+  // warp 34.6 (40.6 before the lean path); 3 CTAs / one resident group 31.1;
+  // 8-warp CTAs x 2 30.4; 5-6 CTAs per SM spill (34-57)
   if (K <= 64) return SCU_FOLD(1, 16, 8, 1, 16);
   if (K <= 128) return SCU_FOLD(2, 8, 8, 1, 8);
-  if (K <= 256) return SCU_FOLD(4, 4, 4, 2, 4, 2);
+  if (K <= 256) return SCU_FOLD(4, 4, 4, 0, 4, 4);
   if (K <= 512) return SCU_FOLD(8, 2, 8, 0, 2);
   if (K <= 1024) return SCU_FOLD(16, 1, 8, 0, 1);
 #undef SCU_FOLD
