@@ -294,6 +294,7 @@ const Tuning& tuning() {
     if (const char* e = env("SAMELDA_MINB")) v.minb = std::atoi(e);
     if (const char* e = env("SAMELDA_DEC")) v.dec = std::atoi(e);
     if (const char* e = env("SAMELDA_TAIL")) v.tail = std::atoi(e);
+    if (const char* e = env("SAMELDA_FAST_PTRS")) v.fast_ptrs = e[0] != '0';
     return v;
   }();
   return t;
@@ -678,7 +679,7 @@ struct samelda_cu_ctx {
         defer_read_pending = false;
       }
       const double* mu_ex = nullptr;
-      if (mu_d == nullptr && defer_frac > kConcurrentMu) {
+      if (mu_d == nullptr && defer_frac > kConcurrentMu && !scu::tuning().fast_ptrs) {
         if (!mu_stream) {
           ck(cudaStreamCreateWithFlags(&mu_stream, cudaStreamNonBlocking), "mu stream");
           ck(cudaEventCreateWithFlags(&mu_theta_ready, cudaEventDisableTiming), "event");

@@ -39,6 +39,7 @@ struct Tuning {
   char eval_variant = 0;    // 0 default, 'c' cta, 'w' warp
   int eval_ctas_per_sm = 0;
   int minb = 4, dec = 1, tail = 0;
+  bool fast_ptrs = true;  // deferred PTRS draws decided from the fast path's rate
 };
 const Tuning& tuning();
 

@@ -356,6 +356,8 @@ struct Deferred {
   int32_t b, w, c;    // batch row, word id, token count
   int32_t kbase;      // first topic of the slice
   uint32_t mask[8];   // bit lane of mask[j]: topic kbase + lane + 32 j
+  float scale;        // the fast path's m c / mu_f (its lambda_f = (theta32 phi32) scale)
+  uint32_t spare;     // written (0): the 64-byte record has no uninitialised bytes
 };
 
 // Round keys a draw of topic k needs (philox_y_sched), precomputed once per topic:
@@ -801,6 +803,8 @@ __global__ void __launch_bounds__(kFastBlock, MINB) k_sample_v2(
           rec.w = wi;
           rec.c = ci;
           rec.kbase = kbase;
+          rec.scale = scale;
+          rec.spare = 0;
 #pragma unroll
           for (int j = 0; j < 8; ++j) rec.mask[j] = masks[j];
           rec_out[slot] = rec;
@@ -867,6 +871,122 @@ __device__ __forceinline__ void deferred_one(const BatchView& bv, const Deferred
   }
 }
 
+// The reference's sequential-k exact mu of a record (sampler.cpp:111-119).
+__device__ __forceinline__ double record_mu(const Deferred& rec, const double* __restrict__ theta_b64,
+                                            const double* __restrict__ phi64, int K) {
+  const double* th = theta_b64 + static_cast<int64_t>(rec.b) * K;
+  const double* ph = phi64 + static_cast<int64_t>(rec.w) * K;
+  double mu = 0.0;
+  if ((K & 1) == 0) {
+    const double2* th2 = reinterpret_cast<const double2*>(th);
+    const double2* ph2 = reinterpret_cast<const double2*>(ph);
+#pragma unroll 8
+    for (int k2 = 0; k2 < (K >> 1); ++k2) {
+      const double2 a = __ldg(th2 + k2), b = __ldg(ph2 + k2);
+      mu = __dadd_rn(mu, __dmul_rn(a.x, b.x));
+      mu = __dadd_rn(mu, __dmul_rn(a.y, b.y));
+    }
+  } else {
+    for (int k = 0; k < K; ++k) mu = __dadd_rn(mu, __dmul_rn(__ldg(th + k), __ldg(ph + k)));
+  }
+  return mu;
+}
+
+// PTRS (rng.cpp:57-86) for a rate known only to lie in [L (1 - e), L (1 + e)],
+// e = kLamRel (the fast path's f32 lambda: 1.5e-6 relative, 2x): every
+// decision the reference takes is evaluated at L and accepted only when no
+// rate in the interval could change it, with bounds on its derivative in
+// lambda >= 10 (b' = 1.265 / sqrt(lambda) <= 0.4, a' = 0.02483 b'):
+//   v_r:  |dv_r/dlambda| lambda <= 1.46 / sqrt(lambda) <= 0.46      -> band e
+//   g:    |dg/dlambda| <= 1 + |u| (2 a' / us + b') <= 1.2 + 0.00993 / us
+//   lhs:  lambda |dlhs/dlambda| <= 0.111 (inv_alpha) + 0.61 (a / us^2 + b)
+//   rhs:  |drhs/dlambda| = |k / lambda - 1|
+// plus slack for the reference's f64 rounding and the libdevice / glibc ulp
+// differences of log, sqrt and lgamma.  The uniforms, us and the rejection
+// tests that do not involve lambda are the reference's exactly.  Returns
+// false when any decision is inside its band (the caller then forms the
+// exact rate), true with the draw in *z otherwise.
+constexpr double kLamRel = 3e-6;
+constexpr float kPtrsMinF = 10.0001f;  // lambda_f (1 - kLamRel) >= 10: PTRS for every rate
+__device__ __noinline__ bool ptrs_banded(double L, U4 blk, uint32_t k0, uint32_t k1, uint32_t w,
+                                            uint32_t d, uint32_t t, long long* z) {
+  constexpr double e = kLamRel;
+  const double log_lambda = log(L);
+  const double b = __dadd_rn(0.931, __dmul_rn(2.53, sqrt(L)));
+  const double a = __dadd_rn(-0.059, __dmul_rn(0.02483, b));
+  const double v_r = __dadd_rn(0.9277, -__ddiv_rn(3.6224, __dadd_rn(b, -2.0)));
+  const double e_vr = e + 1e-12;
+  const double a2 = __dmul_rn(2.0, a);
+  // each iteration consumes one Philox block (two uniforms, rng.cpp:70-71)
+  for (uint32_t it = 0; it < 16; ++it) {
+    if (it) blk = philox10(U4{it, w, d, t}, k0, k1);
+    const double u = __dadd_rn(u64_to_uniform_oo(join64(blk.x, blk.y)), -0.5);
+    const double v = u64_to_uniform_oo(join64(blk.z, blk.w));
+    const double us = __dadd_rn(0.5, -fabs(u));
+    const double g = __dadd_rn(__dadd_rn(__dmul_rn(__dadd_rn(__ddiv_rn(a2, us), b), u), L), 0.43);
+    const double slack = 1e-12 * (fabs(g) + 2.0 * L + 1.0);
+    if (us >= 0.07) {
+      if (v <= v_r - e_vr) {  // quick acceptance for every rate in the interval
+        const double e_g = 1.35 * e * L * 1.01 + slack;  // 1.2 + 0.00993 / 0.07 < 1.35
+        const double lo = g - e_g, hi = g + e_g;
+        if (!(lo >= 0.0) || !(hi < 9.0e18) || floor(lo) != floor(hi)) return false;
+        *z = static_cast<long long>(g);
+        return true;
+      }
+      if (!(v > v_r + e_vr)) return false;
+    }
+    const double e_g = (1.2 + 0.01 / us) * e * L * 1.01 + slack;
+    if (g + e_g < 0.0 || (us < 0.013 && v > us)) continue;  // rejected for every rate
+    if (!(g - e_g >= 0.0) || !(g + e_g <= 9.0e18) || floor(g - e_g) != floor(g + e_g)) return false;
+    const long long k = static_cast<long long>(g);
+    const double inv_alpha = __dadd_rn(1.1239, __ddiv_rn(1.1328, __dadd_rn(b, -3.4)));
+    const double lhs =
+        log(__ddiv_rn(__dmul_rn(v, inv_alpha), __dadd_rn(__ddiv_rn(a, __dmul_rn(us, us)), b)));
+    const double lg = k < kLgammaTab && g_lgamma_ready ? g_lgamma_int[k]
+                                                       : lgamma(__dadd_rn(static_cast<double>(k), 1.0));
+    const double kl = __dmul_rn(static_cast<double>(k), log_lambda);
+    const double rhs = __dadd_rn(__dadd_rn(-L, kl), -lg);
+    const double mag = fabs(lhs) + L + fabs(kl) + fabs(lg);
+    const double e_log = 0.74 * e + (fabs(static_cast<double>(k) - L) + e * L) * e * 1.01 + 1e-13 * mag;
+    if (lhs <= rhs - e_log) {
+      *z = k;
+      return true;
+    }
+    if (!(lhs > rhs + e_log)) return false;
+  }
+  return false;
+}
+
+// A deferred draw without a precomputed mu: a PTRS draw is decided from the
+// fast path's lambda_f when its interval allows (ptrs_banded).  Returns false
+// when the draw needs the exact rate (the record's mu, deferred_one).
+__device__ __forceinline__ bool deferred_try_fast(const BatchView& bv, const Deferred& rec, int k,
+                                                  const float* __restrict__ theta_b32,
+                                                  const float* __restrict__ phi32, int K,
+                                                  uint64_t seed, uint32_t t, uint32_t sweep,
+                                                  unsigned long long* __restrict__ theta_counts,
+                                                  unsigned long long* __restrict__ phi_counts) {
+  // lambda_f exactly as k_sample_v2 formed it
+  const float prod = __fmul_rn(__ldg(theta_b32 + static_cast<int64_t>(rec.b) * K + k),
+                               __ldg(phi32 + static_cast<int64_t>(rec.w) * K + k));
+  const float lam = __fmul_rn(prod, rec.scale);
+  if (!(prod >= 1e-30f && lam >= kPtrsMinF && lam <= 1e30f)) return false;
+  const uint32_t d = static_cast<uint32_t>(__ldg(bv.batch_docs + rec.b) + bv.doc_base);
+  const uint32_t tag = make_tag(kPoissonCounts, sweep, static_cast<uint32_t>(k));
+  uint32_t k0, k1;
+  stream_key(seed, tag, k0, k1);
+  const U4 blk = philox10(U4{0u, static_cast<uint32_t>(rec.w), d, t}, k0, k1);
+  long long z = 0;
+  if (!ptrs_banded(static_cast<double>(lam), blk, k0, k1, static_cast<uint32_t>(rec.w), d, t, &z))
+    return false;
+  if (z != 0) {
+    atomicAdd(theta_counts + static_cast<int64_t>(rec.b) * K + k, static_cast<unsigned long long>(z));
+    if (phi_counts)
+      atomicAdd(phi_counts + static_cast<int64_t>(rec.w) * K + k, static_cast<unsigned long long>(z));
+  }
+  return true;
+}
+
 
 // Phase A, thread = record: the record's exact mu -- the reference's
 // sequential-k f64 dot (sampler.cpp:111-119: product then add, no FMA) over
@@ -914,28 +1034,16 @@ __global__ void __launch_bounds__(256) k_deferred_expand(
         static_cast<uint32_t>((i0 + j) * chunk + (q - __shfl_sync(0xffffffffu, excl_i, j)));
     Deferred me{};
     double mu = 0.0;
+    bool mu_ok = false;
     uint32_t cnt = 0;
     if (live) {
       me = deferred[slot];
-      if (mu_in) {
-        mu = __ldg(mu_in + me.p);
-      } else {
-        const double* th = theta_b64 + static_cast<int64_t>(me.b) * K;
-        const double* ph = phi64 + static_cast<int64_t>(me.w) * K;
-        if ((K & 1) == 0) {
-          const double2* th2 = reinterpret_cast<const double2*>(th);
-          const double2* ph2 = reinterpret_cast<const double2*>(ph);
-#pragma unroll 8
-          for (int k2 = 0; k2 < (K >> 1); ++k2) {
-            const double2 a = __ldg(th2 + k2), b = __ldg(ph2 + k2);
-            mu = __dadd_rn(mu, __dmul_rn(a.x, b.x));
-            mu = __dadd_rn(mu, __dmul_rn(a.y, b.y));
-          }
-        } else {
-          for (int k = 0; k < K; ++k) mu = __dadd_rn(mu, __dmul_rn(__ldg(th + k), __ldg(ph + k)));
-        }
-      }
-      rec_mu[slot] = mu;
+      // rec_mu == nullptr: the draw pass forms mu itself where it needs it
+      // (after deferred_try_fast); only draws past the list's capacity need it here
+      if (mu_in) mu = __ldg(mu_in + me.p);
+      else if (rec_mu) mu = record_mu(me, theta_b64, phi64, K);
+      if (rec_mu) rec_mu[slot] = mu;
+      mu_ok = mu_in != nullptr || rec_mu != nullptr;
 #pragma unroll
       for (int j = 0; j < 8; ++j) cnt += __popc(me.mask[j]);
     }
@@ -960,9 +1068,16 @@ __global__ void __launch_bounds__(256) k_deferred_expand(
         const int k = me.kbase + bit + 32 * j;
         // every reserved slot below draw_cap is written (phase B reads exactly
         // [0, min(n_draws, draw_cap))), the rest is drawn here
-        if (base < draw_cap) draws[base] = DeferredDraw{slot, static_cast<uint32_t>(k)};
-        else deferred_one(bv, me, mu, k, theta_b64, phi64, K, m_t, seed, t, sweep, theta_counts,
-                          phi_counts, err);
+        if (base < draw_cap) {
+          draws[base] = DeferredDraw{slot, static_cast<uint32_t>(k)};
+        } else {
+          if (!mu_ok) {
+            mu = record_mu(me, theta_b64, phi64, K);
+            mu_ok = true;
+          }
+          deferred_one(bv, me, mu, k, theta_b64, phi64, K, m_t, seed, t, sweep, theta_counts,
+                       phi_counts, err);
+        }
         ++base;
       }
     }
@@ -971,7 +1086,8 @@ __global__ void __launch_bounds__(256) k_deferred_expand(
 }
 
 __global__ void __launch_bounds__(256) k_deferred_draw(
-    BatchView bv, const double* __restrict__ theta_b64, const double* __restrict__ phi64, int K,
+    BatchView bv, const double* __restrict__ theta_b64, const double* __restrict__ phi64,
+    const float* __restrict__ theta_b32, const float* __restrict__ phi32, int K,
     double m_t, uint64_t seed, uint32_t t, uint32_t sweep, const Deferred* __restrict__ deferred,
     const double* __restrict__ rec_mu, const DeferredDraw* __restrict__ draws,
     const unsigned long long* __restrict__ n_draws, unsigned long long draw_cap,
@@ -981,25 +1097,43 @@ __global__ void __launch_bounds__(256) k_deferred_draw(
   for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
        i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
     const DeferredDraw dd = draws[i];
-    deferred_one(bv, deferred[dd.rec], rec_mu[dd.rec], static_cast<int>(dd.k), theta_b64, phi64, K,
-                 m_t, seed, t, sweep, theta_counts, phi_counts, err);
+    if (rec_mu) {
+      deferred_one(bv, deferred[dd.rec], rec_mu[dd.rec], static_cast<int>(dd.k), theta_b64, phi64, K,
+                   m_t, seed, t, sweep, theta_counts, phi_counts, err);
+      continue;
+    }
+    // fast mode: PTRS from lambda_f where its interval decides, else the
+    // record's exact mu and the reference's draw
+    if (deferred_try_fast(bv, deferred[dd.rec], static_cast<int>(dd.k), theta_b32, phi32, K, seed, t,
+                          sweep, theta_counts, phi_counts))
+      continue;
+    const Deferred rec = deferred[dd.rec];
+    deferred_one(bv, rec, record_mu(rec, theta_b64, phi64, K), static_cast<int>(dd.k), theta_b64,
+                 phi64, K, m_t, seed, t, sweep, theta_counts, phi_counts, err);
   }
 }
 
 // Both passes.  aux = [rec_mu: max_records f64][n_draws: u64][pad][draws: draw_cap]
-void launch_deferred(const BatchView& bv, const double* tb64, const double* phi64, const double* mu,
-                     int K, double m_t, uint64_t seed, uint32_t t, uint32_t sweep, Deferred* rec,
-                     uint32_t* rec_count, int64_t n_items, int chunk, unsigned long long* n_deferred,
-                     void* aux, int64_t max_records, int64_t draw_cap, unsigned long long* tc,
-                     unsigned long long* pc, int* err, cudaStream_t st) {
+// tb32 / phi32 given and no caller mu (fast mode): the expand pass lists the
+// draws without forming mu; the draw pass decides PTRS draws from the fast
+// path's lambda_f (deferred_try_fast, thread per draw) and forms the record's
+// exact mu only for the rest.
+void launch_deferred(const BatchView& bv, const double* tb64, const double* phi64, const float* tb32,
+                     const float* phi32, const double* mu, int K, double m_t, uint64_t seed,
+                     uint32_t t, uint32_t sweep, Deferred* rec, uint32_t* rec_count, int64_t n_items,
+                     int chunk, unsigned long long* n_deferred, void* aux, int64_t max_records,
+                     int64_t draw_cap, unsigned long long* tc, unsigned long long* pc, int* err,
+                     cudaStream_t st) {
+  const bool fast = mu == nullptr && tb32 != nullptr && phi32 != nullptr && tuning().fast_ptrs;
   double* rec_mu = static_cast<double*>(aux);
   auto* n_draws = reinterpret_cast<unsigned long long*>(rec_mu + max_records);
   auto* draws = reinterpret_cast<DeferredDraw*>(n_draws + 2);
+  if (fast) rec_mu = nullptr;
   cudaMemsetAsync(n_draws, 0, sizeof(unsigned long long), st);
   k_deferred_expand<<<148 * 8, 256, 0, st>>>(bv, tb64, phi64, mu, K, m_t, seed, t, sweep, rec,
                                              rec_count, n_items, chunk, rec_mu, draws, n_draws,
                                              static_cast<unsigned long long>(draw_cap), tc, pc, err);
-  k_deferred_draw<<<148 * 16, 256, 0, st>>>(bv, tb64, phi64, K, m_t, seed, t, sweep, rec, rec_mu,
+  k_deferred_draw<<<148 * 16, 256, 0, st>>>(bv, tb64, phi64, tb32, phi32, K, m_t, seed, t, sweep, rec, rec_mu,
                                             draws, n_draws, static_cast<unsigned long long>(draw_cap),
                                             tc, pc, err);
 }
@@ -1279,7 +1413,7 @@ int launch_fast_kpl(const BatchView& bv, const double* tb64, const float* tb32, 
           k_sample_v2<8, true, 0, 4, kDecDefault, 0, false><<<grid, kFastBlock, 0, st>>>(
               bv, tb32, phi32, mu, muf, K, m_t, seed, t, sweep, chunk, tc, pc, rec, rec_count, n_deferred);
           wait_mu();
-          launch_deferred(bv, tb64, phi64, mu_defer, K, m_t, seed, t, sweep, rec, rec_count, n_items,
+          launch_deferred(bv, tb64, phi64, tb32, phi32, mu_defer, K, m_t, seed, t, sweep, rec, rec_count, n_items,
                           static_cast<int>(chunk), n_deferred, aux, max_records, draw_cap, tc, pc, err, st);
           return launched + 3;
         }
@@ -1317,7 +1451,7 @@ int launch_fast_kpl(const BatchView& bv, const double* tb64, const float* tb32, 
 #undef SCU_V2_LAUNCH
   }
   wait_mu();
-  launch_deferred(bv, tb64, phi64, mu_defer, K, m_t, seed, t, sweep, rec, rec_count, n_items,
+  launch_deferred(bv, tb64, phi64, tb32, phi32, mu_defer, K, m_t, seed, t, sweep, rec, rec_count, n_items,
                   static_cast<int>(chunk), n_deferred, aux, max_records, draw_cap, tc, pc, err, st);
   return launched + 3;
 }

@@ -470,11 +470,11 @@ def test_train_k256_production_kernel_bit_exact(port, m, schedule):
 
 def test_long_run_bit_exact_through_the_regime_change():
     """40 periods (10 passes) at K = 256, m = 100 on a 1,500-document corpus:
-    the run crosses from the early regime (~1% of nonzeros defer) past the
-    25% deferral rate at which the exact mu moves to the concurrent side-stream
-    SDDMM (measured ~29% by period 39) and must stay bit-identical to the
-    compiled reference's train() the whole way (phi, theta, the ll trace every
-    10 periods)."""
+    the run crosses from the early regime (~1% of nonzeros defer, mostly
+    inversion draws inside their band) to ~29% by period 39 (mostly PTRS
+    draws, decided from the fast path's lambda_f by ptrs_banded) and must stay
+    bit-identical to the compiled reference's train() the whole way (phi,
+    theta, the ll trace every 10 periods)."""
     from oracle import Ref
     ref = Ref()
     g = ref.make_corpus(1500, 1000, 16, 120.0, 5)
@@ -502,12 +502,13 @@ def test_long_run_bit_exact_through_the_regime_change():
     np.testing.assert_array_equal(t.model().phi, rphi)
 
 
-def test_converged_regime_concurrent_exact_mu_bit_exact(port):
+def test_converged_regime_banded_ptrs_bit_exact(port):
     """The converged-model path: once most nonzeros carry deferred (PTRS)
-    draws the exact f64 mu comes from k_sddmm_staged on a side stream
-    instead of the expand pass ("Two regimes").  m = 3000 puts a
-    PTRS draw on nearly every nonzero from the first period; phi, theta and
-    the ll trace must still equal the reference's bit for bit."""
+    draws, they are decided from the fast path's f32 rate with error bands
+    (ptrs_banded) and only the undecided ones form the exact f64 mu (DESIGN.md
+    4, "Two regimes").  m = 3000 puts a PTRS draw on nearly every nonzero from
+    the first period; phi, theta and the ll trace must still equal the
+    reference's bit for bit."""
     g = port.make_corpus(120, 400, 12, 150.0, 41)
     tr, te = port.split_holdout(g, 0.1, 3)
     cfg = dict(n_topics=256, m=3000.0, t_max=8, batch_fraction=0.5, seed=12)
@@ -519,6 +520,21 @@ def test_converged_regime_concurrent_exact_mu_bit_exact(port):
     prof = t.profile_read()
     t.profile(False)
     assert prof["deferred"] > 0.5 * prof["nnz"], prof
+    model, trace = S.train(tr, S.SamplerConfig(**cfg), te, 2)
+    ophi, otheta, otrace = port.train(tr, TrainConfig(**cfg), te, 2)
+    np.testing.assert_array_equal(model.phi, ophi)
+    np.testing.assert_array_equal(model.theta, otheta)
+    np.testing.assert_allclose([r["ll"] for r in trace], [r["ll"] for r in otrace], rtol=1e-12)
+
+
+@pytest.mark.parametrize("m,K", [(2e4, 64), (2e5, 16), (5e3, 300)])
+def test_large_rate_ptrs_bit_exact(port, m, K):
+    """Rates of 1e3 .. 1e6 (m up to 2e5, counts up to ~40): the banded PTRS
+    decisions (whose bands grow with lambda) and their exact fallbacks,
+    including topic slices (K = 300), against the reference's train()."""
+    g = port.make_corpus(60, 150, 6, 60.0, 23)
+    tr, te = port.split_holdout(g, 0.2, 5)
+    cfg = dict(n_topics=K, m=m, t_max=4, batch_fraction=0.5, seed=19)
     model, trace = S.train(tr, S.SamplerConfig(**cfg), te, 2)
     ophi, otheta, otrace = port.train(tr, TrainConfig(**cfg), te, 2)
     np.testing.assert_array_equal(model.phi, ophi)

@@ -82,10 +82,10 @@ def test_heldout_eval_at_the_timed_config(setup):
 
 def test_converged_period_bit_exact_at_the_timed_config():
     """The converged-model regime at the timed shape: after 80 untimed periods
-    nearly every nonzero carries a deferred PTRS draw, the exact mu comes from
-    the concurrent staged SDDMM ("Two regimes"); one more period
-    must equal the compiled reference's period on the downloaded model bit
-    for bit."""
+    nearly every nonzero carries a deferred PTRS draw, decided from the fast
+    path's lambda_f with error bands (ptrs_banded, "Two
+    regimes"); one more period must equal the compiled reference's period on
+    the downloaded model bit for bit."""
     import bench
     from oracle import Ref
     from paper_1409_5402_b200 import samelda as S
