@@ -404,7 +404,7 @@ struct samelda_cu_ctx {
   int64_t defer_read_nnz = 0;
   bool defer_read_pending = false;
   double defer_frac = 0.0;
-  static constexpr double kConcurrentMu = 0.25;
+  static constexpr double kManyDeferred = 0.25;
   cudaStream_t copy_stream = nullptr;
   DevBuf rows2[2];
   cudaEvent_t rows_ready[2] = {nullptr, nullptr};
@@ -678,8 +678,12 @@ struct samelda_cu_ctx {
         defer_frac = static_cast<double>(*h_deferred) / static_cast<double>(std::max<int64_t>(defer_read_nnz, 1));
         defer_read_pending = false;
       }
+      // once most nonzeros defer (a PTRS draw each, late in training) the
+      // deferred draws are decided from the fast path's rate (ptrs_banded);
+      // SAMELDA_FAST_PTRS=0 keeps the exact mu from a concurrent SDDMM instead
+      const bool fast_ptrs_now = defer_frac > kManyDeferred && scu::tuning().fast_ptrs;
       const double* mu_ex = nullptr;
-      if (mu_d == nullptr && defer_frac > kConcurrentMu && !scu::tuning().fast_ptrs) {
+      if (mu_d == nullptr && defer_frac > kManyDeferred && !scu::tuning().fast_ptrs) {
         if (!mu_stream) {
           ck(cudaStreamCreateWithFlags(&mu_stream, cudaStreamNonBlocking), "mu stream");
           ck(cudaEventCreateWithFlags(&mu_theta_ready, cudaEventDisableTiming), "event");
@@ -697,7 +701,8 @@ struct samelda_cu_ctx {
                                           m_t_, seed, static_cast<uint32_t>(t),
                                           static_cast<uint32_t>(sweep), tc_, pc_, rec, nd_, aux, draw_cap,
                                           K_ > 256 ? ensure<float>(mu_f32, bv.nnz) : nullptr, d_err(),
-                                          stream, mu_ex, mu_ex ? mu_done : nullptr);
+                                          stream, mu_ex, mu_ex ? mu_done : nullptr,
+                                          mu_d == nullptr && fast_ptrs_now);
       if (!defer_read_pending && mu_d == nullptr) {
         if (!h_deferred) {
           ck(cudaMallocHost(&h_deferred, sizeof(unsigned long long)), "pinned");

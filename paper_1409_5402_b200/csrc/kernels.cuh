@@ -85,7 +85,8 @@ int launch_sample_fast(const BatchView& bv, const double* theta_b64, const float
                        unsigned long long* theta_counts, unsigned long long* phi_counts,
                        void* deferred, unsigned long long* n_deferred, void* aux,
                        int64_t draw_cap, float* mu_f_scratch, int* err, cudaStream_t st,
-                       const double* mu_exact = nullptr, cudaEvent_t mu_ready = nullptr);
+                       const double* mu_exact = nullptr, cudaEvent_t mu_ready = nullptr,
+                       bool fast_ptrs = false);
 // Throughput mode: the same sampler on its own random
 // streams in f32, four draws per Philox block, no deferral -- statistically,
 // not bit-for-bit, the reference's.  mu_f_scratch: nnz floats when K > 256.

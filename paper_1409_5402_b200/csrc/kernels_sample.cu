@@ -957,6 +957,15 @@ __device__ __noinline__ bool ptrs_banded(double L, U4 blk, uint32_t k0, uint32_t
   return false;
 }
 
+// The fast path's lambda_f of a deferred draw, exactly as k_sample_v2 formed it
+__device__ __forceinline__ float draw_lambda_f(const Deferred& rec, int k,
+                                               const float* __restrict__ theta_b32,
+                                               const float* __restrict__ phi32, int K) {
+  const float prod = __fmul_rn(__ldg(theta_b32 + static_cast<int64_t>(rec.b) * K + k),
+                               __ldg(phi32 + static_cast<int64_t>(rec.w) * K + k));
+  return prod >= 1e-30f ? __fmul_rn(prod, rec.scale) : 0.0f;
+}
+
 // A deferred draw without a precomputed mu: a PTRS draw is decided from the
 // fast path's lambda_f when its interval allows (ptrs_banded).  Returns false
 // when the draw needs the exact rate (the record's mu, deferred_one).
@@ -966,11 +975,8 @@ __device__ __forceinline__ bool deferred_try_fast(const BatchView& bv, const Def
                                                   uint64_t seed, uint32_t t, uint32_t sweep,
                                                   unsigned long long* __restrict__ theta_counts,
                                                   unsigned long long* __restrict__ phi_counts) {
-  // lambda_f exactly as k_sample_v2 formed it
-  const float prod = __fmul_rn(__ldg(theta_b32 + static_cast<int64_t>(rec.b) * K + k),
-                               __ldg(phi32 + static_cast<int64_t>(rec.w) * K + k));
-  const float lam = __fmul_rn(prod, rec.scale);
-  if (!(prod >= 1e-30f && lam >= kPtrsMinF && lam <= 1e30f)) return false;
+  const float lam = draw_lambda_f(rec, k, theta_b32, phi32, K);
+  if (!(lam >= kPtrsMinF && lam <= 1e30f)) return false;
   const uint32_t d = static_cast<uint32_t>(__ldg(bv.batch_docs + rec.b) + bv.doc_base);
   const uint32_t tag = make_tag(kPoissonCounts, sweep, static_cast<uint32_t>(k));
   uint32_t k0, k1;
@@ -999,6 +1005,7 @@ __device__ __forceinline__ bool deferred_try_fast(const BatchView& bv, const Def
 // 9.0 ms per sweep against 5.7).
 __global__ void __launch_bounds__(256) k_deferred_expand(
     BatchView bv, const double* __restrict__ theta_b64, const double* __restrict__ phi64,
+    const float* __restrict__ theta_b32, const float* __restrict__ phi32, bool fast,
     const double* __restrict__ mu_in, int K, double m_t, uint64_t seed, uint32_t t,
     uint32_t sweep, const Deferred* __restrict__ deferred, const uint32_t* __restrict__ rec_count,
     int64_t n_items, int chunk, double* __restrict__ rec_mu,
@@ -1038,12 +1045,15 @@ __global__ void __launch_bounds__(256) k_deferred_expand(
     uint32_t cnt = 0;
     if (live) {
       me = deferred[slot];
-      // rec_mu == nullptr: the draw pass forms mu itself where it needs it
-      // (after deferred_try_fast); only draws past the list's capacity need it here
+      // fast mode (late in training: nearly every record is one PTRS draw):
+      // no mu here (NaN); the draw pass decides PTRS draws from lambda_f and
+      // forms the record's mu itself for the others
+      const bool need_mu = !fast;
       if (mu_in) mu = __ldg(mu_in + me.p);
-      else if (rec_mu) mu = record_mu(me, theta_b64, phi64, K);
-      if (rec_mu) rec_mu[slot] = mu;
-      mu_ok = mu_in != nullptr || rec_mu != nullptr;
+      else if (need_mu) mu = record_mu(me, theta_b64, phi64, K);
+      else mu = __longlong_as_double(0x7ff8000000000000ll);
+      rec_mu[slot] = mu;
+      mu_ok = mu_in != nullptr || need_mu;
 #pragma unroll
       for (int j = 0; j < 8; ++j) cnt += __popc(me.mask[j]);
     }
@@ -1087,7 +1097,7 @@ __global__ void __launch_bounds__(256) k_deferred_expand(
 
 __global__ void __launch_bounds__(256) k_deferred_draw(
     BatchView bv, const double* __restrict__ theta_b64, const double* __restrict__ phi64,
-    const float* __restrict__ theta_b32, const float* __restrict__ phi32, int K,
+    const float* __restrict__ theta_b32, const float* __restrict__ phi32, bool fast, int K,
     double m_t, uint64_t seed, uint32_t t, uint32_t sweep, const Deferred* __restrict__ deferred,
     const double* __restrict__ rec_mu, const DeferredDraw* __restrict__ draws,
     const unsigned long long* __restrict__ n_draws, unsigned long long draw_cap,
@@ -1097,43 +1107,41 @@ __global__ void __launch_bounds__(256) k_deferred_draw(
   for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
        i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
     const DeferredDraw dd = draws[i];
-    if (rec_mu) {
-      deferred_one(bv, deferred[dd.rec], rec_mu[dd.rec], static_cast<int>(dd.k), theta_b64, phi64, K,
-                   m_t, seed, t, sweep, theta_counts, phi_counts, err);
-      continue;
-    }
     // fast mode: PTRS from lambda_f where its interval decides, else the
-    // record's exact mu and the reference's draw
-    if (deferred_try_fast(bv, deferred[dd.rec], static_cast<int>(dd.k), theta_b32, phi32, K, seed, t,
-                          sweep, theta_counts, phi_counts))
+    // record's exact mu (from the expand pass, or formed here: NaN) and the
+    // reference's draw
+    if (fast && deferred_try_fast(bv, deferred[dd.rec], static_cast<int>(dd.k), theta_b32, phi32, K,
+                                  seed, t, sweep, theta_counts, phi_counts))
       continue;
     const Deferred rec = deferred[dd.rec];
-    deferred_one(bv, rec, record_mu(rec, theta_b64, phi64, K), static_cast<int>(dd.k), theta_b64,
-                 phi64, K, m_t, seed, t, sweep, theta_counts, phi_counts, err);
+    double mu = rec_mu[dd.rec];
+    if (isnan(mu)) mu = record_mu(rec, theta_b64, phi64, K);
+    deferred_one(bv, rec, mu, static_cast<int>(dd.k), theta_b64, phi64, K, m_t, seed, t, sweep,
+                 theta_counts, phi_counts, err);
   }
 }
 
 // Both passes.  aux = [rec_mu: max_records f64][n_draws: u64][pad][draws: draw_cap]
-// tb32 / phi32 given and no caller mu (fast mode): the expand pass lists the
-// draws without forming mu; the draw pass decides PTRS draws from the fast
-// path's lambda_f (deferred_try_fast, thread per draw) and forms the record's
-// exact mu only for the rest.
+// fast (the caller's choice: late in training, when most nonzeros defer a
+// PTRS draw), tb32 / phi32 given and no caller mu: the expand pass forms no
+// mu; the draw pass decides PTRS draws from the fast path's lambda_f
+// (deferred_try_fast, thread per draw) and forms the record's exact mu only
+// for the rest.
 void launch_deferred(const BatchView& bv, const double* tb64, const double* phi64, const float* tb32,
-                     const float* phi32, const double* mu, int K, double m_t, uint64_t seed,
+                     const float* phi32, bool fast, const double* mu, int K, double m_t, uint64_t seed,
                      uint32_t t, uint32_t sweep, Deferred* rec, uint32_t* rec_count, int64_t n_items,
                      int chunk, unsigned long long* n_deferred, void* aux, int64_t max_records,
                      int64_t draw_cap, unsigned long long* tc, unsigned long long* pc, int* err,
                      cudaStream_t st) {
-  const bool fast = mu == nullptr && tb32 != nullptr && phi32 != nullptr && tuning().fast_ptrs;
+  fast = fast && mu == nullptr && tb32 != nullptr && phi32 != nullptr;
   double* rec_mu = static_cast<double*>(aux);
   auto* n_draws = reinterpret_cast<unsigned long long*>(rec_mu + max_records);
   auto* draws = reinterpret_cast<DeferredDraw*>(n_draws + 2);
-  if (fast) rec_mu = nullptr;
   cudaMemsetAsync(n_draws, 0, sizeof(unsigned long long), st);
-  k_deferred_expand<<<148 * 8, 256, 0, st>>>(bv, tb64, phi64, mu, K, m_t, seed, t, sweep, rec,
+  k_deferred_expand<<<148 * 8, 256, 0, st>>>(bv, tb64, phi64, tb32, phi32, fast, mu, K, m_t, seed, t, sweep, rec,
                                              rec_count, n_items, chunk, rec_mu, draws, n_draws,
                                              static_cast<unsigned long long>(draw_cap), tc, pc, err);
-  k_deferred_draw<<<148 * 16, 256, 0, st>>>(bv, tb64, phi64, tb32, phi32, K, m_t, seed, t, sweep, rec, rec_mu,
+  k_deferred_draw<<<148 * 16, 256, 0, st>>>(bv, tb64, phi64, tb32, phi32, fast, K, m_t, seed, t, sweep, rec, rec_mu,
                                             draws, n_draws, static_cast<unsigned long long>(draw_cap),
                                             tc, pc, err);
 }
@@ -1375,7 +1383,7 @@ int launch_fast_kpl(const BatchView& bv, const double* tb64, const float* tb32, 
                     uint32_t t, uint32_t sweep, unsigned long long* tc, unsigned long long* pc,
                     void* deferred, unsigned long long* n_deferred, void* aux, int64_t draw_cap,
                     float* mu_f, int* err, cudaStream_t st, const double* mu_exact,
-                    cudaEvent_t mu_ready) {
+                    cudaEvent_t mu_ready, bool fast_ptrs) {
   const int n_slices = (K + kWarp * KPL - 1) / (kWarp * KPL);
   // the deferred passes take the caller's mu, else an exact mu computed
   // concurrently on another stream (mu_exact, ready at mu_ready), else their own
@@ -1413,7 +1421,7 @@ int launch_fast_kpl(const BatchView& bv, const double* tb64, const float* tb32, 
           k_sample_v2<8, true, 0, 4, kDecDefault, 0, false><<<grid, kFastBlock, 0, st>>>(
               bv, tb32, phi32, mu, muf, K, m_t, seed, t, sweep, chunk, tc, pc, rec, rec_count, n_deferred);
           wait_mu();
-          launch_deferred(bv, tb64, phi64, tb32, phi32, mu_defer, K, m_t, seed, t, sweep, rec, rec_count, n_items,
+          launch_deferred(bv, tb64, phi64, tb32, phi32, fast_ptrs, mu_defer, K, m_t, seed, t, sweep, rec, rec_count, n_items,
                           static_cast<int>(chunk), n_deferred, aux, max_records, draw_cap, tc, pc, err, st);
           return launched + 3;
         }
@@ -1451,7 +1459,7 @@ int launch_fast_kpl(const BatchView& bv, const double* tb64, const float* tb32, 
 #undef SCU_V2_LAUNCH
   }
   wait_mu();
-  launch_deferred(bv, tb64, phi64, tb32, phi32, mu_defer, K, m_t, seed, t, sweep, rec, rec_count, n_items,
+  launch_deferred(bv, tb64, phi64, tb32, phi32, fast_ptrs, mu_defer, K, m_t, seed, t, sweep, rec, rec_count, n_items,
                   static_cast<int>(chunk), n_deferred, aux, max_records, draw_cap, tc, pc, err, st);
   return launched + 3;
 }
@@ -1879,7 +1887,8 @@ int launch_sample_fast(const BatchView& bv, const double* theta_b64, const float
                        double m_t, uint64_t seed, uint32_t t, uint32_t sweep,
                        unsigned long long* tc, unsigned long long* pc, void* deferred,
                        unsigned long long* n_deferred, void* aux, int64_t draw_cap, float* mu_f,
-                       int* err, cudaStream_t st, const double* mu_exact, cudaEvent_t mu_ready) {
+                       int* err, cudaStream_t st, const double* mu_exact, cudaEvent_t mu_ready,
+                       bool fast_ptrs) {
   if (bv.nnz == 0) return 0;
   // lane = topic, 8 topics per lane (k_sample_v2); K > 256 in topic slices of
   // 256 with the full mu from a k_mu_f32 pre-pass.  SAMELDA_SAMPLER=x runs
@@ -1890,15 +1899,15 @@ int launch_sample_fast(const BatchView& bv, const double* theta_b64, const float
                          nullptr, nullptr, err, st);
   if (K <= 32)
     return launch_fast_kpl<1>(bv, theta_b64, theta_b32, phi64, phi32, mu, K, m_t, seed, t, sweep, tc, pc,
-                              deferred, n_deferred, aux, draw_cap, mu_f, err, st, mu_exact, mu_ready);
+                              deferred, n_deferred, aux, draw_cap, mu_f, err, st, mu_exact, mu_ready, fast_ptrs);
   if (K <= 64)
     return launch_fast_kpl<2>(bv, theta_b64, theta_b32, phi64, phi32, mu, K, m_t, seed, t, sweep, tc, pc,
-                              deferred, n_deferred, aux, draw_cap, mu_f, err, st, mu_exact, mu_ready);
+                              deferred, n_deferred, aux, draw_cap, mu_f, err, st, mu_exact, mu_ready, fast_ptrs);
   if (K <= 128)
     return launch_fast_kpl<4>(bv, theta_b64, theta_b32, phi64, phi32, mu, K, m_t, seed, t, sweep, tc, pc,
-                              deferred, n_deferred, aux, draw_cap, mu_f, err, st, mu_exact, mu_ready);
+                              deferred, n_deferred, aux, draw_cap, mu_f, err, st, mu_exact, mu_ready, fast_ptrs);
   return launch_fast_kpl<8>(bv, theta_b64, theta_b32, phi64, phi32, mu, K, m_t, seed, t, sweep, tc, pc,
-                            deferred, n_deferred, aux, draw_cap, mu_f, err, st, mu_exact, mu_ready);
+                            deferred, n_deferred, aux, draw_cap, mu_f, err, st, mu_exact, mu_ready, fast_ptrs);
 }
 
 // glibc lgamma(k + 1) for the PTRS acceptance test (poisson.cuh), per device
