@@ -157,13 +157,126 @@ void validate_corpus(const samelda_cu_corpus* c) {
   if (c->doc_offsets[0] != 0) fail(SAMELDA_CU_CONFIG, "corpus doc_offsets[0] != 0");
 }
 
-void upload_corpus(CorpusSlot& s, const samelda_cu_corpus* c, cudaStream_t st) {
-  validate_corpus(c);
-  const uint64_t fp = fingerprint(c);
-  const int64_t nnz = c->doc_offsets[c->n_docs];
-  if (s.valid && s.fp == fp && s.n_docs == c->n_docs && s.nnz == nnz &&
-      s.n_words == c->n_words)
+// Large copies between device memory and caller-owned (pageable) host
+// buffers -- the corpus upload, the model download -- staged through two
+// pinned 32 MB chunks: the DMA of one chunk overlaps the multi-threaded host
+// memcpy of the other.  A pageable cudaMemcpy runs at ~5 GB/s on the B200
+// boxes (the drop-in train()'s 824 MB model download took 160 ms).
+struct PinnedStage {
+  static constexpr size_t kChunk = size_t{32} << 20;
+  unsigned char* buf[2] = {nullptr, nullptr};
+  cudaEvent_t ev[2] = {nullptr, nullptr};
+  bool pending[2] = {false, false};
+  void init() {
+    if (buf[0]) return;
+    for (int i = 0; i < 2; ++i) {
+      ck(cudaHostAlloc(reinterpret_cast<void**>(&buf[i]), kChunk, cudaHostAllocDefault), "pinned stage");
+      ck(cudaEventCreateWithFlags(&ev[i], cudaEventDisableTiming), "stage event");
+    }
+  }
+  ~PinnedStage() {
+    for (int i = 0; i < 2; ++i) {
+      if (ev[i]) {
+        cudaEventSynchronize(ev[i]);
+        cudaEventDestroy(ev[i]);
+      }
+      if (buf[i]) cudaFreeHost(buf[i]);
+    }
+  }
+};
+
+void par_memcpy(void* dst, const void* src, size_t n) {
+  const unsigned hw = std::max(1u, std::min(8u, std::thread::hardware_concurrency()));
+  if (n < (size_t{4} << 20) || hw == 1) {
+    std::memcpy(dst, src, n);
     return;
+  }
+  const size_t per = (n + hw - 1) / hw;
+  std::vector<std::thread> pool;
+  for (unsigned t = 1; t < hw; ++t) {
+    const size_t off = per * t;
+    if (off >= n) break;
+    pool.emplace_back([=] {
+      std::memcpy(static_cast<unsigned char*>(dst) + off, static_cast<const unsigned char*>(src) + off,
+                  std::min(per, n - off));
+    });
+  }
+  std::memcpy(dst, src, std::min(per, n));
+  for (auto& th : pool) th.join();
+}
+
+constexpr size_t kStageMin = size_t{16} << 20;  // smaller copies go direct
+
+// device -> pageable host; returns with the data in dst
+void copy_d2h(PinnedStage* ps, void* dst, const void* src, size_t bytes, cudaStream_t st) {
+  if (!ps || bytes < kStageMin) {
+    ck(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToHost, st), "download");
+    ck(cudaStreamSynchronize(st), "download");
+    return;
+  }
+  ps->init();
+  auto* d = static_cast<unsigned char*>(dst);
+  const auto* sp = static_cast<const unsigned char*>(src);
+  int prev = -1;
+  size_t prev_off = 0, prev_n = 0;
+  for (size_t off = 0, i = 0; off < bytes; off += PinnedStage::kChunk, ++i) {
+    const int slot = static_cast<int>(i & 1);
+    const size_t n = std::min(PinnedStage::kChunk, bytes - off);
+    ck(cudaMemcpyAsync(ps->buf[slot], sp + off, n, cudaMemcpyDeviceToHost, st), "download");
+    ck(cudaEventRecord(ps->ev[slot], st), "stage event");
+    ps->pending[slot] = true;
+    if (prev >= 0) {
+      ck(cudaEventSynchronize(ps->ev[prev]), "download");
+      par_memcpy(d + prev_off, ps->buf[prev], prev_n);
+    }
+    prev = slot;
+    prev_off = off;
+    prev_n = n;
+  }
+  ck(cudaEventSynchronize(ps->ev[prev]), "download");
+  par_memcpy(d + prev_off, ps->buf[prev], prev_n);
+}
+
+// pageable host -> device, enqueued on st (the source may be reused on return)
+void copy_h2d(PinnedStage* ps, void* dst, const void* src, size_t bytes, cudaStream_t st) {
+  if (!ps || bytes < kStageMin) {
+    ck(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, st), "upload");
+    return;
+  }
+  ps->init();
+  auto* d = static_cast<unsigned char*>(dst);
+  const auto* sp = static_cast<const unsigned char*>(src);
+  for (size_t off = 0, i = 0; off < bytes; off += PinnedStage::kChunk, ++i) {
+    const int slot = static_cast<int>(i & 1);
+    const size_t n = std::min(PinnedStage::kChunk, bytes - off);
+    if (ps->pending[slot]) ck(cudaEventSynchronize(ps->ev[slot]), "upload");
+    par_memcpy(ps->buf[slot], sp + off, n);
+    ck(cudaMemcpyAsync(d + off, ps->buf[slot], n, cudaMemcpyHostToDevice, st), "upload");
+    ck(cudaEventRecord(ps->ev[slot], st), "stage event");
+    ps->pending[slot] = true;
+  }
+}
+
+void upload_corpus(CorpusSlot& s, const samelda_cu_corpus* c, cudaStream_t st,
+                   PinnedStage* ps = nullptr) {
+  validate_corpus(c);
+  const int64_t nnz = c->doc_offsets[c->n_docs];
+  const bool same_shape = s.valid && s.n_docs == c->n_docs && s.nnz == nnz && s.n_words == c->n_words;
+  uint64_t fp = 0;
+  std::thread fp_thread;
+  if (same_shape) {
+    fp = fingerprint(c);
+    if (s.fp == fp) return;
+  } else {
+    // a new corpus: its identity hash runs beside the upload
+    fp_thread = std::thread([&] { fp = fingerprint(c); });
+  }
+  struct Join {
+    std::thread& t;
+    ~Join() {
+      if (t.joinable()) t.join();
+    }
+  } join{fp_thread};
   s.valid = false;
   s.n_docs = c->n_docs;
   s.n_words = c->n_words;
@@ -171,27 +284,39 @@ void upload_corpus(CorpusSlot& s, const samelda_cu_corpus* c, cudaStream_t st) {
   s.offsets.assign(c->doc_offsets, c->doc_offsets + c->n_docs + 1);
   s.doc_tokens.assign(static_cast<size_t>(c->n_docs), 0);
   s.n_tokens = 0;
-  for (int64_t d = 0; d < c->n_docs; ++d) {
-    int64_t tok = 0;
-    for (int64_t i = c->doc_offsets[d]; i < c->doc_offsets[d + 1]; ++i) tok += c->counts[i];
-    s.doc_tokens[static_cast<size_t>(d)] = tok;
-    s.n_tokens += tok;
+  {
+    // per-document token totals, documents split over host threads
+    const unsigned hw = std::max(1u, std::min(8u, std::thread::hardware_concurrency()));
+    const int64_t nt = nnz > (int64_t{1} << 22) ? hw : 1;
+    std::vector<int64_t> part(static_cast<size_t>(nt), 0);
+    auto run = [&](int64_t t) {
+      const int64_t d0 = c->n_docs * t / nt, d1 = c->n_docs * (t + 1) / nt;
+      int64_t sum = 0;
+      for (int64_t d = d0; d < d1; ++d) {
+        int64_t tok = 0;
+        for (int64_t i = c->doc_offsets[d]; i < c->doc_offsets[d + 1]; ++i) tok += c->counts[i];
+        s.doc_tokens[static_cast<size_t>(d)] = tok;
+        sum += tok;
+      }
+      part[static_cast<size_t>(t)] = sum;
+    };
+    std::vector<std::thread> pool;
+    for (int64_t t = 1; t < nt; ++t) pool.emplace_back(run, t);
+    run(0);
+    for (auto& th : pool) th.join();
+    for (int64_t v : part) s.n_tokens += v;
   }
-  ck(cudaMemcpyAsync(ensure<int64_t>(s.offs, c->n_docs + 1), c->doc_offsets,
-                     sizeof(int64_t) * (c->n_docs + 1), cudaMemcpyHostToDevice, st),
-     "upload offsets");
+  copy_h2d(ps, ensure<int64_t>(s.offs, c->n_docs + 1), c->doc_offsets,
+           sizeof(int64_t) * (c->n_docs + 1), st);
   if (nnz > 0) {
-    ck(cudaMemcpyAsync(ensure<int32_t>(s.words, nnz), c->word_ids, sizeof(int32_t) * nnz,
-                       cudaMemcpyHostToDevice, st),
-       "upload word ids");
-    ck(cudaMemcpyAsync(ensure<int32_t>(s.counts, nnz), c->counts, sizeof(int32_t) * nnz,
-                       cudaMemcpyHostToDevice, st),
-       "upload counts");
+    copy_h2d(ps, ensure<int32_t>(s.words, nnz), c->word_ids, sizeof(int32_t) * nnz, st);
+    copy_h2d(ps, ensure<int32_t>(s.counts, nnz), c->counts, sizeof(int32_t) * nnz, st);
   } else {
     ensure<int32_t>(s.words, 1);
     ensure<int32_t>(s.counts, 1);
   }
   ck(cudaStreamSynchronize(st), "corpus upload");
+  if (fp_thread.joinable()) fp_thread.join();
   s.fp = fp;
   s.valid = true;
 }
@@ -303,6 +428,7 @@ const Tuning& tuning() {
 
 struct samelda_cu_ctx {
   int device = 0;
+  PinnedStage pstage;  // staged copies of large caller buffers (destroyed last)
   cudaStream_t own_stream = nullptr;
   cudaStream_t stream = nullptr;
   std::string error;
@@ -913,7 +1039,7 @@ int samelda_cu_sddmm(samelda_cu_ctx* ctx, const samelda_cu_corpus* corpus,
     if (K < 1 || K >= (1 << 20)) fail(SAMELDA_CU_CONFIG, "sddmm: K out of range");
     *mu_len = 0;
     if (B == 0) return;
-    upload_corpus(ctx->train, corpus, ctx->stream);
+    upload_corpus(ctx->train, corpus, ctx->stream, &ctx->pstage);
     const scu::BatchView bv = ctx->upload_batch(ctx->train, doc_ids, B);
     if (bv.nnz > mu_cap) fail(SAMELDA_CU_CONFIG, "sddmm: mu buffer too small");
     double* th = ensure<double>(ctx->theta_call, B * K);
@@ -941,7 +1067,7 @@ static void sample_call(samelda_cu_ctx* ctx, const samelda_cu_corpus* corpus,
   validate_corpus(corpus);
   if (W != corpus->n_words) fail(SAMELDA_CU_CONFIG, "sample_counts: phi columns must match the vocabulary size");
   if (sweep < 0 || sweep > 255) fail(SAMELDA_CU_CONFIG, "sample_counts: sweep out of range");
-  upload_corpus(ctx->train, corpus, ctx->stream);
+  upload_corpus(ctx->train, corpus, ctx->stream, &ctx->pstage);
   const int64_t nnz = batch_nnz_host(ctx->train, doc_ids, B);
   if (mu_len != nnz) fail(SAMELDA_CU_CONFIG, "sample_counts: mu is not aligned with the batch nonzeros");
   const size_t elem = 8;
@@ -1164,7 +1290,7 @@ int samelda_cu_perword_loglik(samelda_cu_ctx* ctx, const double* phi, int64_t K,
     if (K < 1) fail(SAMELDA_CU_CONFIG, "perword_loglik: K must be >= 1");
     const uint64_t before = ctx->heldout.fp;
     const bool was_valid = ctx->heldout.valid;
-    upload_corpus(ctx->heldout, test, ctx->stream);
+    upload_corpus(ctx->heldout, test, ctx->stream, &ctx->pstage);
     if (!was_valid || before != ctx->heldout.fp) ctx->split_ready = false;
     ctx->prepare_split(seed);
     const double* phi_wk = ctx->upload_phi(phi, K, W);
@@ -1186,7 +1312,7 @@ int samelda_cu_cgs_init(samelda_cu_ctx* ctx, const samelda_cu_corpus* corpus, in
     if (!(alpha > 0.0) || !(beta > 0.0)) fail(SAMELDA_CU_CONFIG, "cgs_init: alpha and beta must be positive");
     if (n_topics > 1024) fail(SAMELDA_CU_CONFIG, "cgs_init: the device sampler supports n_topics <= 1024");
     validate_corpus(corpus);
-    upload_corpus(ctx->train, corpus, ctx->stream);
+    upload_corpus(ctx->train, corpus, ctx->stream, &ctx->pstage);
     const CorpusSlot& s = ctx->train;
     const int K = static_cast<int>(n_topics);
     std::vector<int64_t> tok(static_cast<size_t>(s.nnz) + 1, 0);
@@ -1369,7 +1495,7 @@ int samelda_cu_train_begin(samelda_cu_ctx* ctx, const samelda_cu_corpus* corpus,
     validate_config(config);
     validate_corpus(corpus);
     if (corpus->n_docs < 1) fail(SAMELDA_CU_CONFIG, "train: corpus is empty");
-    upload_corpus(ctx->train, corpus, ctx->stream);
+    upload_corpus(ctx->train, corpus, ctx->stream, &ctx->pstage);
     ctx->cfg = *config;
     ctx->K = static_cast<int>(config->n_topics);
     ctx->W = corpus->n_words;
@@ -1411,7 +1537,7 @@ int samelda_cu_heldout(samelda_cu_ctx* ctx, const samelda_cu_corpus* test, uint6
     if (test->n_docs < 1) fail(SAMELDA_CU_CONFIG, "perword_loglik: test corpus is empty");
     const uint64_t before = ctx->heldout.fp;
     const bool was_valid = ctx->heldout.valid;
-    upload_corpus(ctx->heldout, test, ctx->stream);
+    upload_corpus(ctx->heldout, test, ctx->stream, &ctx->pstage);
     if (!was_valid || before != ctx->heldout.fp) ctx->split_ready = false;
     ctx->prepare_split(seed);
   });
@@ -1629,11 +1755,9 @@ int samelda_cu_model_download(samelda_cu_ctx* ctx, double* phi, double* theta) {
     if (phi) {
       double* tmp = ensure<double>(ctx->phi_call, K * ctx->W);
       ctx->launches += scu::launch_transpose(ctx->phi.as<double>(), ctx->W, K, tmp, ctx->stream);
-      ck(cudaMemcpyAsync(phi, tmp, sizeof(double) * K * ctx->W, cudaMemcpyDeviceToHost, ctx->stream), "download phi");
+      copy_d2h(&ctx->pstage, phi, tmp, sizeof(double) * K * ctx->W, ctx->stream);
     }
-    if (theta)
-      ck(cudaMemcpyAsync(theta, ctx->theta.p, sizeof(double) * ctx->D * K, cudaMemcpyDeviceToHost, ctx->stream),
-         "download theta");
+    if (theta) copy_d2h(&ctx->pstage, theta, ctx->theta.p, sizeof(double) * ctx->D * K, ctx->stream);
     ck(cudaStreamSynchronize(ctx->stream), "model_download");
   });
 }
