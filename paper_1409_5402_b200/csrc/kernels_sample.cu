@@ -290,6 +290,10 @@ constexpr int kFastBlock = 256;
 // threshold was measured equal -- its extra instructions cost what the rarer
 // search saves -- with 9% more deferrals from the wider band)
 constexpr int kDecDefault = 1;
+#ifndef SAMELDA_V2_MINB
+#define SAMELDA_V2_MINB 4
+#endif
+constexpr int kV2Minb = SAMELDA_V2_MINB;  // blocks per SM of the period kernel
 
 // Nonzeros per warp work item: 128 (the packed u16 theta-count pairs hold
 // <= 128 nonzeros x z <= 40), fewer on small batches so the grid keeps ~4
@@ -1421,7 +1425,7 @@ int launch_fast_kpl(const BatchView& bv, const double* tb64, const float* tb32, 
       // non-final inner sweep (theta counts only): the K = 256 period kernel
       if constexpr (KPL == 8) {
         if (full && musrc == 0 && n_slices == 1) {
-          k_sample_v2<8, true, 0, 4, kDecDefault, 0, false><<<grid, kFastBlock, 0, st>>>(
+          k_sample_v2<8, true, 0, kV2Minb, kDecDefault, 0, false><<<grid, kFastBlock, 0, st>>>(
               bv, tb32, phi32, mu, muf, K, m_t, seed, t, sweep, chunk, tc, pc, rec, rec_count, n_deferred);
           wait_mu();
           launch_deferred(bv, tb64, phi64, tb32, phi32, fast_ptrs, mu_defer, K, m_t, seed, t, sweep, rec, rec_count, n_items,
@@ -1448,10 +1452,10 @@ int launch_fast_kpl(const BatchView& bv, const double* tb64, const float* tb32, 
       if (tu.dec == 2) { SCU_V2_LAUNCH(FULLV, MS, 4, 2); break; }                                \
       if (tu.tail == 1) { SCU_V2_LAUNCH(FULLV, MS, 4, 1, 1); break; }                            \
     }                                                                                            \
-    SCU_V2_LAUNCH(FULLV, MS, 4, kDecDefault);                                                    \
+    SCU_V2_LAUNCH(FULLV, MS, kV2Minb, kDecDefault);                                                    \
   } while (0)
 #else
-#define SCU_V2(FULLV, MS) SCU_V2_LAUNCH(FULLV, MS, 4, kDecDefault)
+#define SCU_V2(FULLV, MS) SCU_V2_LAUNCH(FULLV, MS, kV2Minb, kDecDefault)
 #endif
     if (full) {
       if (musrc == 0) SCU_V2(true, 0); else if (musrc == 1) SCU_V2(true, 1); else SCU_V2(true, 2);

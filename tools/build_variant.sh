@@ -8,12 +8,12 @@ set -e
 ROOT=$(cd "$(dirname "$0")/.." && pwd)
 PKG=$ROOT/paper_1409_5402_b200
 python -m paper_1409_5402_b200.build >/dev/null
-mkdir -p "$ROOT/_variants"
+VDIR=${VDIR:-$ROOT/_variants}; mkdir -p "$VDIR"
 UNIT=${3:-kernels_sample.cu}
-OBJ=$ROOT/_variants/${UNIT%.cu}_$1.o
+OBJ=$VDIR/${UNIT%.cu}_$1.o
 nvcc -gencode arch=compute_100a,code=sm_100a -O3 -lineinfo -std=c++20 -Xcompiler -fPIC \
   -I "$PKG/csrc" -I "$ROOT/include" -fmad=false $2 -c "$PKG/csrc/$UNIT" -o "$OBJ"
 OTHERS=$(ls "$PKG"/_build/*.o | grep -v "/${UNIT%.cu}.o")
-nvcc -gencode arch=compute_100a,code=sm_100a -shared -o "$ROOT/_variants/libsamelda_cuda_$1.so" \
+nvcc -gencode arch=compute_100a,code=sm_100a -shared -o "$VDIR/libsamelda_cuda_$1.so" \
   "$OBJ" $OTHERS -lpthread -ldl
-echo "$ROOT/_variants/libsamelda_cuda_$1.so"
+echo "$VDIR/libsamelda_cuda_$1.so"
