@@ -136,6 +136,19 @@ int samelda_cu_sample_counts_fast(samelda_cu_ctx* ctx, const samelda_cu_corpus* 
                                   uint64_t seed, int64_t t, int32_t sweep, int64_t* theta_counts,
                                   int64_t* phi_counts);
 
+/* Throughput mode, non-final inner sweep (sampler.cpp:318-319: only the
+ * theta counts of a sweep before the last are used): theta_counts[b,k] drawn
+ * ONCE per (document, topic) as Poisson(theta_bk sum_w (m_t c_w / mu_w)
+ * phi_wk) -- the law of the per-(nonzero, topic) draws' sum (a sum of
+ * independent Poissons), with mu the f32 dot the kernel forms.  This is what
+ * the device-resident period runs for its inner sweeps in
+ * SAMELDA_CU_MODE_THROUGHPUT; deterministic for given inputs. */
+int samelda_cu_sample_theta_counts_fast(samelda_cu_ctx* ctx, const samelda_cu_corpus* corpus,
+                                        const double* theta_batch, int64_t B, int64_t K_theta,
+                                        const double* phi, int64_t K, int64_t W, const int32_t* doc_ids,
+                                        double m_t, uint64_t seed, int64_t t, int32_t sweep,
+                                        int64_t* theta_counts);
+
 /* Multinomial mode (SAMELDA_CU_MODE_MULTINOMIAL): sample_counts with the
  * c m_t replicas of each nonzero drawn jointly as Multinomial(n, theta phi /
  * mu), n = floor(c m_t) (+1 with probability frac(c m_t)); this library's own

@@ -506,7 +506,7 @@ struct samelda_cu_ctx {
   // scratch
   DevBuf batch, prefix, theta_batch, theta_batch32, mu, tc, pc, tf, pf, totals, err, ll,
       phi_call, phi_call_wk, phi_call32, theta_call, theta_call32, eval_scratch, theta_rows,
-      deferred, n_deferred, cand, deferred_aux, mu_f32;
+      deferred, n_deferred, cand, deferred_aux, mu_f32, rates32;
   // double-buffered pinned staging of batch ids / prefixes: the host may run
   // periods ahead of the device; a buffer is reused only after the copies of
   // two periods ago have executed (event)
@@ -736,6 +736,7 @@ struct samelda_cu_ctx {
       ensure<unsigned long long>(pc, W_ * K_);
       if (K_ > 256) ensure<float>(mu_f32, nnz_);
       if (mode == SAMELDA_CU_MODE_THROUGHPUT || mode == SAMELDA_CU_MODE_MULTINOMIAL) {
+        if (mode == SAMELDA_CU_MODE_THROUGHPUT) ensure<float>(rates32, B_ * K_);
         for (int i = 0; i < 2; ++i) stage(B_);
         return;
       }
@@ -791,7 +792,8 @@ struct samelda_cu_ctx {
       if (mode == SAMELDA_CU_MODE_THROUGHPUT) {
         launches += scu::launch_sample_throughput(
             bv, theta_b32, phi_wk32, K_, m_t_, seed, static_cast<uint32_t>(t), static_cast<uint32_t>(sweep),
-            tc_, pc_, K_ > 256 ? ensure<float>(mu_f32, bv.nnz) : nullptr, stream);
+            tc_, pc_, K_ > 256 ? ensure<float>(mu_f32, bv.nnz) : nullptr,
+            pc_ ? nullptr : ensure<float>(rates32, bv.B * K_), stream);
         tick(need_phi ? kSampleLast : kSample, false);
         return;
       }
@@ -1059,7 +1061,8 @@ static void sample_call(samelda_cu_ctx* ctx, const samelda_cu_corpus* corpus,
                         const double* theta_batch, int64_t B, int64_t K_theta,
                         const double* phi, int64_t K, int64_t W, const double* mu,
                         int64_t mu_len, const int32_t* doc_ids, double m_t, uint64_t seed,
-                        int64_t t, int32_t sweep, int mode, void* theta_out, void* phi_out) {
+                        int64_t t, int32_t sweep, int mode, void* theta_out, void* phi_out,
+                        bool theta_only = false) {
   // sampler.cpp:130-140
   if (!(m_t > 0.0) || !std::isfinite(m_t)) fail(SAMELDA_CU_CONFIG, "sample_counts: m_t must be positive and finite");
   if (K_theta != K) fail(SAMELDA_CU_CONFIG, "sample_counts: theta columns must match phi rows");
@@ -1069,10 +1072,10 @@ static void sample_call(samelda_cu_ctx* ctx, const samelda_cu_corpus* corpus,
   if (sweep < 0 || sweep > 255) fail(SAMELDA_CU_CONFIG, "sample_counts: sweep out of range");
   upload_corpus(ctx->train, corpus, ctx->stream, &ctx->pstage);
   const int64_t nnz = batch_nnz_host(ctx->train, doc_ids, B);
-  if (mu_len != nnz) fail(SAMELDA_CU_CONFIG, "sample_counts: mu is not aligned with the batch nonzeros");
+  if (!theta_only && mu_len != nnz) fail(SAMELDA_CU_CONFIG, "sample_counts: mu is not aligned with the batch nonzeros");
   const size_t elem = 8;
   if (B == 0) {
-    std::memset(phi_out, 0, elem * W * K);
+    if (!theta_only) std::memset(phi_out, 0, elem * W * K);
     return;
   }
   const scu::BatchView bv = ctx->upload_batch(ctx->train, doc_ids, B);
@@ -1082,12 +1085,18 @@ static void sample_call(samelda_cu_ctx* ctx, const samelda_cu_corpus* corpus,
   ctx->launches += scu::launch_to_f32(th, B * K, th32, ctx->stream);
   float* phi32 = nullptr;
   const double* phi_wk = ctx->upload_phi(phi, K, W, &phi32);
-  double* mu_d = ensure<double>(ctx->mu, nnz);
-  if (nnz > 0)
+  double* mu_d = theta_only ? nullptr : ensure<double>(ctx->mu, nnz);
+  if (nnz > 0 && !theta_only)
     ck(cudaMemcpyAsync(mu_d, mu, sizeof(double) * nnz, cudaMemcpyHostToDevice, ctx->stream), "upload mu");
   ctx->reset_err();
-  ctx->sample_sweep(bv, th, th32, phi_wk, phi32, mu_d, static_cast<int>(K), W, m_t, seed, t, sweep, mode);
+  ctx->sample_sweep(bv, th, th32, phi_wk, phi32, mu_d, static_cast<int>(K), W, m_t, seed, t, sweep, mode,
+                    !theta_only);
   ctx->check_err("sample_counts");
+  if (theta_only) {
+    ck(cudaMemcpyAsync(theta_out, ctx->tc.p, elem * B * K, cudaMemcpyDeviceToHost, ctx->stream), "download theta counts");
+    ck(cudaStreamSynchronize(ctx->stream), "sample_counts");
+    return;
+  }
   const void* tsrc = mode == SAMELDA_CU_MODE_EXPECTED ? ctx->tf.p : ctx->tc.p;
   const void* psrc = mode == SAMELDA_CU_MODE_EXPECTED ? ctx->pf.p : ctx->pc.p;
   ck(cudaMemcpyAsync(theta_out, tsrc, elem * B * K, cudaMemcpyDeviceToHost, ctx->stream), "download theta counts");
@@ -1116,6 +1125,17 @@ int samelda_cu_sample_counts_fast(samelda_cu_ctx* ctx, const samelda_cu_corpus* 
   return guarded(ctx, [&] {
     sample_call(ctx, corpus, theta_batch, B, K_theta, phi, K, W, mu, mu_len, doc_ids, m_t, seed,
                 t, sweep, SAMELDA_CU_MODE_THROUGHPUT, theta_counts, phi_counts);
+  });
+}
+
+int samelda_cu_sample_theta_counts_fast(samelda_cu_ctx* ctx, const samelda_cu_corpus* corpus,
+                                        const double* theta_batch, int64_t B, int64_t K_theta,
+                                        const double* phi, int64_t K, int64_t W, const int32_t* doc_ids,
+                                        double m_t, uint64_t seed, int64_t t, int32_t sweep,
+                                        int64_t* theta_counts) {
+  return guarded(ctx, [&] {
+    sample_call(ctx, corpus, theta_batch, B, K_theta, phi, K, W, nullptr, 0, doc_ids, m_t, seed, t,
+                sweep, SAMELDA_CU_MODE_THROUGHPUT, theta_counts, nullptr, true);
   });
 }
 

@@ -90,10 +90,13 @@ int launch_sample_fast(const BatchView& bv, const double* theta_b64, const float
 // Throughput mode: the same sampler on its own random
 // streams in f32, four draws per Philox block, no deferral -- statistically,
 // not bit-for-bit, the reference's.  mu_f_scratch: nnz floats when K > 256.
+// phi_counts == nullptr (a non-final inner sweep): theta counts only, drawn
+// once per (document, topic) from the summed rate (k_theta_rates /
+// k_theta_draws); rate_scratch: B x K floats.
 int launch_sample_throughput(const BatchView& bv, const float* theta_b32, const float* phi32, int K,
                              double m_t, uint64_t seed, uint32_t t, uint32_t sweep,
                              unsigned long long* theta_counts, unsigned long long* phi_counts,
-                             float* mu_f_scratch, cudaStream_t st);
+                             float* mu_f_scratch, float* rate_scratch, cudaStream_t st);
 // Multinomial mode: per nonzero, floor(c m_t) (+1 with the fractional
 // part's probability) categorical trials over the K topics (K <= 1024;
 // returns -1 above), on this library's own streams.

@@ -1384,6 +1384,103 @@ __global__ void __launch_bounds__(BLK, MINB) k_sample_thru(
   if (cur_b >= 0) flush(cur_b);
 }
 
+// The throughput mode's non-final inner sweep.  Only its theta counts are
+// used (update_model reads the last sweep's phi counts, sampler.cpp:320-332),
+// and a sum of independent Poisson draws is a Poisson draw of the summed rate:
+// theta_counts[b,k] = sum_w Poisson(m c_w theta_bk phi_wk / mu_w) has exactly
+// the law Poisson(Lambda_bk), Lambda_bk = theta_bk sum_w (m c_w / mu_w) phi_wk,
+// independent over (b, k) (mu_w < 1e-30: weight 1/K, sampler.cpp:164, i.e.
+// m c_w / K for every topic).  So no per-(nonzero, topic) draw:
+//   k_theta_rates: one warp per batch document, lane = topic (KPL per lane),
+//     the phi row gather and the f32 mu of k_sample_thru, rates accumulated
+//     in registers and written (not added) to a B x K f32 buffer;
+//   k_theta_draws: one thread per (b, k), ONE draw -- f64 inversion / PTRS
+//     (poisson_from_block0) on the mode's own streams (purpose
+//     kThroughputDoc, counter {0, 2^31 | k, doc, t}) -- written to
+//     theta_counts.
+// Deterministic (no atomics); K draws per document instead of K per nonzero.
+template <int KPL, bool FULL, int MUSRC>
+__global__ void __launch_bounds__(256) k_theta_rates(
+    BatchView bv, const float* __restrict__ theta_b32, const float* __restrict__ phi32,
+    const float* __restrict__ mu_f_in, int K, float m_t, float* __restrict__ rates) {
+  const int lane = threadIdx.x & 31;
+  const int64_t b = static_cast<int64_t>(blockIdx.x) * (256 / kWarp) + (threadIdx.x >> 5);
+  if (b >= bv.B) return;
+  const int kbase = static_cast<int>(blockIdx.y) * kWarp * KPL;
+  const int64_t p0 = __ldg(bv.batch_prefix + b), p1 = __ldg(bv.batch_prefix + b + 1);
+  const int64_t off = __ldg(bv.doc_offsets + __ldg(bv.batch_docs + b)) - p0;
+  float th[KPL], acc[KPL];
+  {
+    const float* trow = theta_b32 + b * K + kbase + lane;
+#pragma unroll
+    for (int j = 0; j < KPL; ++j) {
+      th[j] = (FULL || kbase + lane + kWarp * j < K) ? __ldg(trow + kWarp * j) : 0.0f;
+      acc[j] = 0.0f;
+    }
+  }
+  float acc_u = 0.0f;  // the uniform-weight nonzeros' m c / K (the same for every topic)
+  const float inv_k = 1.0f / static_cast<float>(K);
+  for (int64_t g0 = p0; g0 < p1; g0 += kWarp) {
+    const int64_t p = g0 + lane;
+    int32_t w = 0, c = 0;
+    float muv = 0.0f;
+    if (p < p1) {
+      w = __ldg(bv.word_ids + off + p);
+      c = __ldg(bv.counts + off + p);
+      if (MUSRC == 2) muv = __ldg(mu_f_in + p);
+    }
+    const int n_here = static_cast<int>(min(static_cast<int64_t>(kWarp), p1 - g0));
+    for (int i = 0; i < n_here; ++i) {
+      const int32_t wi = __shfl_sync(0xffffffffu, w, i);
+      const float cs = m_t * static_cast<float>(__shfl_sync(0xffffffffu, c, i));
+      const float* prow = phi32 + static_cast<int64_t>(wi) * K + kbase + lane;
+      float ph[KPL];
+#pragma unroll
+      for (int j = 0; j < KPL; ++j) ph[j] = (FULL || kbase + lane + kWarp * j < K) ? __ldg(prow + kWarp * j) : 0.0f;
+      float mu;
+      if (MUSRC == 2) {
+        mu = __shfl_sync(0xffffffffu, muv, i);
+      } else {
+        mu = 0.0f;
+#pragma unroll
+        for (int j = 0; j < KPL; ++j) mu = __fmaf_rn(th[j], ph[j], mu);
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) mu += __shfl_xor_sync(0xffffffffu, mu, o);
+      }
+      if (mu >= 1e-30f) {  // warp-uniform
+        const float s = __fdividef(cs, mu);
+#pragma unroll
+        for (int j = 0; j < KPL; ++j) acc[j] = __fmaf_rn(ph[j], s, acc[j]);
+      } else {
+        acc_u += cs * inv_k;
+      }
+    }
+  }
+  float* const out = rates + b * K + kbase + lane;
+#pragma unroll
+  for (int j = 0; j < KPL; ++j)
+    if (FULL || kbase + lane + kWarp * j < K) out[kWarp * j] = __fmaf_rn(th[j], acc[j], acc_u);
+}
+
+__global__ void __launch_bounds__(256) k_theta_draws(BatchView bv, const float* __restrict__ rates, int K,
+                                                     uint64_t seed, uint32_t t, uint32_t sweep,
+                                                     unsigned long long* __restrict__ theta_counts) {
+  const int64_t n = bv.B * K;
+  const uint32_t tag = make_tag(kThroughputDoc, sweep, 0);
+  uint32_t k0, k1;
+  stream_key(seed, tag, k0, k1);
+  for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int64_t b = i / K;
+    const uint32_t k = static_cast<uint32_t>(i - b * K);
+    const uint32_t dg = static_cast<uint32_t>(__ldg(bv.batch_docs + b) + static_cast<int32_t>(bv.doc_base));
+    const uint32_t word = 0x80000000u | k;
+    const double lam = static_cast<double>(__ldg(rates + i));
+    const U4 b0 = philox10(U4{0u, word, dg, t}, k0, k1);
+    theta_counts[i] = static_cast<unsigned long long>(poisson_from_block0(lam, b0, seed, t, dg, word, tag));
+  }
+}
+
 template <int KPL>
 int launch_fast_kpl(const BatchView& bv, const double* tb64, const float* tb32, const double* phi64,
                     const float* phi32, const double* mu, int K, double m_t, uint64_t seed,
@@ -1872,7 +1969,7 @@ int launch_sample_multinomial(const BatchView& bv, const float* theta_b32, const
 int launch_sample_throughput(const BatchView& bv, const float* theta_b32, const float* phi32, int K,
                              double m_t, uint64_t seed, uint32_t t, uint32_t sweep,
                              unsigned long long* tc, unsigned long long* pc, float* mu_f,
-                             cudaStream_t st) {
+                             float* rate_scratch, cudaStream_t st) {
   if (bv.nnz == 0) return 0;
   int launched = 0;
   const float* mu = nullptr;
@@ -1884,8 +1981,24 @@ int launch_sample_throughput(const BatchView& bv, const float* theta_b32, const 
   const float mf = static_cast<float>(m_t);
   // 128-thread blocks at <= 72 registers: 28 resident warps per SM (measured
   // 3% faster than 256 x 80 registers; 64 registers spills)
-  if (pc != nullptr) launch_thru<true, 128, 7>(bv, theta_b32, phi32, K, mf, seed, t, sweep, tc, pc, mu, st);
-  else launch_thru<false, 128, 7>(bv, theta_b32, phi32, K, mf, seed, t, sweep, tc, pc, mu, st);
+  if (pc != nullptr) {
+    launch_thru<true, 128, 7>(bv, theta_b32, phi32, K, mf, seed, t, sweep, tc, pc, mu, st);
+    return launched + 1;
+  }
+  // a non-final inner sweep: theta counts only, one draw per (document, topic)
+  constexpr int KPL = 8;
+  const dim3 grid(static_cast<unsigned>((bv.B + 7) / 8), static_cast<unsigned>((K + kWarp * KPL - 1) / (kWarp * KPL)));
+  const bool full = K % (kWarp * KPL) == 0;
+  if (mu != nullptr) {
+    if (full) k_theta_rates<KPL, true, 2><<<grid, 256, 0, st>>>(bv, theta_b32, phi32, mu, K, mf, rate_scratch);
+    else k_theta_rates<KPL, false, 2><<<grid, 256, 0, st>>>(bv, theta_b32, phi32, mu, K, mf, rate_scratch);
+  } else if (full) {
+    k_theta_rates<KPL, true, 0><<<grid, 256, 0, st>>>(bv, theta_b32, phi32, nullptr, K, mf, rate_scratch);
+  } else {
+    k_theta_rates<KPL, false, 0><<<grid, 256, 0, st>>>(bv, theta_b32, phi32, nullptr, K, mf, rate_scratch);
+  }
+  k_theta_draws<<<grid_for(bv.B * K, 256), 256, 0, st>>>(bv, rate_scratch, K, seed, t, sweep, tc);
+  launched += 2;
   return launched + 1;
 }
 

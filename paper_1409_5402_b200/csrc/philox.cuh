@@ -34,6 +34,7 @@ enum Purpose : uint32_t {
   kPhiInit = 8,
   kThroughput = 9,  // throughput mode's own streams (not in the reference)
   kMultinomial = 10,  // multinomial mode's own streams (not in the reference)
+  kThroughputDoc = 11,  // throughput mode's per-(document, topic) draws (not in the reference)
 };
 
 SCU_HD uint32_t make_tag(uint32_t purpose, uint32_t sub, uint32_t index) {

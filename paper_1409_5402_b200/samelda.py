@@ -94,6 +94,8 @@ SIGNATURES = [
                                            _P, _D, _U64, _I64, _I32, _P, _P]),
     ("samelda_cu_sample_counts_fast", C.c_int, [_P, _CP, _P, _I64, _I64, _P, _I64, _I64, _P, _I64,
                                            _P, _D, _U64, _I64, _I32, _P, _P]),
+    ("samelda_cu_sample_theta_counts_fast", C.c_int, [_P, _CP, _P, _I64, _I64, _P, _I64, _I64, _P,
+                                                      _D, _U64, _I64, _I32, _P]),
     ("samelda_cu_sample_counts_multinomial", C.c_int, [_P, _CP, _P, _I64, _I64, _P, _I64, _I64, _P, _I64,
                                            _P, _D, _U64, _I64, _I32, _P, _P]),
     ("samelda_cu_expected_counts", C.c_int, [_P, _CP, _P, _I64, _I64, _P, _I64, _I64, _P, _I64,
@@ -438,6 +440,29 @@ def sample_counts(theta_batch, phi, mu, corpus, doc_ids, m_t, seed, t, sweep=0, 
         int(seed) & (2**64 - 1), int(t), int(sweep), _ptr(tc), _ptr(pc)))
     return SampledCounts(ids[:B].copy(), K, W, float(m_t), tc[:B * K].reshape(B, K),
                          pc[:W * K].reshape(W, K))
+
+
+def sample_theta_counts_fast(theta_batch, phi, corpus, doc_ids, m_t, seed, t, sweep,
+                             ctx: Context | None = None):
+    """The throughput mode's non-final inner sweep (theta counts only, B x K
+    int64): one Poisson draw per (document, topic) of the summed rate
+    theta_bk sum_w (m_t c_w / mu_w) phi_wk -- the law of the sum of the
+    per-(nonzero, topic) draws (samelda_cu_sample_theta_counts_fast)."""
+    ctx = ctx or default_context()
+    ctx._train_token = None  # per-call use replaces a Trainer's device state
+    corpus = Corpus.of(corpus)
+    theta_batch = _f64(theta_batch)
+    phi = _f64(phi)
+    ids, B = _ids(doc_ids)
+    K, W = phi.shape
+    Kt = theta_batch.shape[1] if theta_batch.ndim == 2 and theta_batch.size else K
+    tc = np.zeros(max(B * K, 1), np.int64)
+    cs = corpus._struct()
+    ctx.check(ctx.lib.samelda_cu_sample_theta_counts_fast(
+        ctx.h, C.byref(cs), _ptr(theta_batch if theta_batch.size else np.zeros(1)), B, Kt,
+        _ptr(phi), K, W, _ptr(ids), float(m_t), int(seed) & (2**64 - 1), int(t), int(sweep),
+        _ptr(tc)))
+    return tc[:B * K].reshape(B, K)
 
 
 def expected_counts(theta_batch, phi, mu, corpus, doc_ids, m_t, ctx: Context | None = None):

@@ -144,3 +144,39 @@ def test_per_call_fast_empty_batch(S, port):
     sc = S.sample_counts(np.zeros((0, K)), phi, np.zeros(0), g, np.zeros(0, np.int32), 3.0, 1, 1,
                          mode=S.MODE_THROUGHPUT)
     assert sc.theta_total() == 0 and sc.phi_total() == 0
+
+
+@pytest.mark.parametrize("K,m_t", [(16, 3.0), (256, 3.0), (256, 400.0), (300, 40.0), (512, 5.0)])
+def test_theta_superposed_counts_poisson_around_expected(S, port, K, m_t):
+    """The throughput mode's non-final inner sweep draws theta_counts[b,k]
+    once per (document, topic) from the summed rate (k_theta_rates /
+    k_theta_draws): the sum of independent per-(nonzero, topic) Poisson draws
+    IS Poisson with that rate.  The mean over T draws matches the oracle's
+    expected theta counts (sampler.cpp:150-185's model, incl. a word whose mu
+    is 0 -> uniform weights 1/K) with Poisson dispersion; deterministic for
+    given inputs, different for another period t; m_t = 400 puts the summed
+    rates on PTRS."""
+    g = port.make_corpus(60, 120, 5, 40.0, 17)
+    rng = np.random.default_rng(K)
+    batch = rng.permutation(g.n_docs)[:40].astype(np.int32)
+    tb = rng.uniform(0.05, 1.0, size=(len(batch), K))
+    phi = rng.uniform(0.0, 1.0, size=(K, g.n_words))
+    phi[:, 3] = 0.0  # mu = 0 for word 3's nonzeros: uniform weights
+    phi /= phi.sum(1, keepdims=True)
+    mu = port.sddmm(tb, phi, g, batch)
+    tf, _ = port.expected_counts(tb, phi, mu, g, batch, m_t)
+    a = S.sample_theta_counts_fast(tb, phi, g, batch, m_t, 7, 1, 0)
+    b = S.sample_theta_counts_fast(tb, phi, g, batch, m_t, 7, 1, 0)
+    np.testing.assert_array_equal(a, b)
+    assert not np.array_equal(a, S.sample_theta_counts_fast(tb, phi, g, batch, m_t, 7, 2, 0))
+    T = 48
+    acc = np.zeros_like(tf)
+    for t in range(1, T + 1):
+        acc += S.sample_theta_counts_fast(tb, phi, g, batch, m_t, 7, t, 0)
+    mean = acc / T
+    live = tf > 1e-3
+    disp = float(np.sum((mean[live] - tf[live]) ** 2 / (tf[live] / T)) / live.sum())
+    assert abs(disp - 1.0) < 6 * np.sqrt(2.0 / live.sum()) + 0.03, disp
+    assert np.all(acc[tf == 0.0] == 0.0)
+    tot_obs, tot_exp = acc.sum(), tf.sum() * T
+    assert abs(tot_obs - tot_exp) < 6 * np.sqrt(tot_exp), (tot_obs, tot_exp)
