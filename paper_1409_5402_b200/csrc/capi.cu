@@ -761,6 +761,13 @@ struct samelda_cu_ctx {
     if (mode == SAMELDA_CU_MODE_EXPECTED) {
       double* tf_ = ensure<double>(tf, bv.B * K_);
       double* pf_ = ensure<double>(pf, W_ * K_);
+      if (!need_phi && mu_d == nullptr && K_ <= 256) {
+        // a non-final inner sweep: the expected theta counts only (k_theta_rates)
+        tick(kSample, true);
+        launches += scu::launch_expected_theta(bv, theta_b, phi_wk, K_, m_t_, tf_, stream);
+        tick(kSample, false);
+        return;
+      }
       ck(cudaMemsetAsync(tf_, 0, sizeof(double) * std::max<int64_t>(bv.B * K_, 1), stream), "zero tf");
       ck(cudaMemsetAsync(pf_, 0, sizeof(double) * std::max<int64_t>(W_ * K_, 1), stream), "zero pf");
       tick(need_phi ? kSampleLast : kSample, true);

@@ -71,6 +71,12 @@ int launch_sample(const BatchView& bv, const double* theta_batch, const double* 
                    unsigned long long* phi_counts, double* theta_exp, double* phi_exp,
                    int* err, cudaStream_t st);
 
+// The expected-count mode's non-final inner sweep: theta_exp[b,k] only
+// (= theta_bk sum_w (m_t c_w / mu_w) phi_wk, written, f64; k_theta_rates).
+// Returns -1 for K > 256 (the caller runs launch_sample).
+int launch_expected_theta(const BatchView& bv, const double* theta_batch, const double* phi_wk, int K,
+                          double m_t, double* theta_exp, cudaStream_t st);
+
 // Same draws, bit for bit, through an f32 fast path with exact f64 fallback
 // (see kernels_sample.cu).  mu == nullptr: the kernel forms mu itself (period path).
 // mu_f_scratch: nnz floats (used when K > 256).

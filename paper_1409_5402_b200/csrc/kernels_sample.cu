@@ -1399,27 +1399,30 @@ __global__ void __launch_bounds__(BLK, MINB) k_sample_thru(
 //     kThroughputDoc, counter {0, 2^31 | k, doc, t}) -- written to
 //     theta_counts.
 // Deterministic (no atomics); K draws per document instead of K per nonzero.
-template <int KPL, bool FULL, int MUSRC>
-__global__ void __launch_bounds__(256) k_theta_rates(
-    BatchView bv, const float* __restrict__ theta_b32, const float* __restrict__ phi32,
-    const float* __restrict__ mu_f_in, int K, float m_t, float* __restrict__ rates) {
+// T = double: the expected-count mode's non-final inner sweep (the expected
+// theta counts ARE these rates; f64 rows, f64 mu, K <= 256).
+template <typename T, int KPL, bool FULL, int MUSRC, int NU = (sizeof(T) == 4 ? 2 : 1)>
+__global__ void __launch_bounds__(256, sizeof(T) == 4 ? 4 : 3) k_theta_rates(
+    BatchView bv, const T* __restrict__ theta_b32, const T* __restrict__ phi32,
+    const float* __restrict__ mu_f_in, int K, T m_t, T* __restrict__ rates) {
+  static_assert(MUSRC == 0 || sizeof(T) == 4, "a supplied mu is f32");
   const int lane = threadIdx.x & 31;
   const int64_t b = static_cast<int64_t>(blockIdx.x) * (256 / kWarp) + (threadIdx.x >> 5);
   if (b >= bv.B) return;
   const int kbase = static_cast<int>(blockIdx.y) * kWarp * KPL;
   const int64_t p0 = __ldg(bv.batch_prefix + b), p1 = __ldg(bv.batch_prefix + b + 1);
   const int64_t off = __ldg(bv.doc_offsets + __ldg(bv.batch_docs + b)) - p0;
-  float th[KPL], acc[KPL];
+  T th[KPL], acc[KPL];
   {
-    const float* trow = theta_b32 + b * K + kbase + lane;
+    const T* trow = theta_b32 + b * K + kbase + lane;
 #pragma unroll
     for (int j = 0; j < KPL; ++j) {
-      th[j] = (FULL || kbase + lane + kWarp * j < K) ? __ldg(trow + kWarp * j) : 0.0f;
-      acc[j] = 0.0f;
+      th[j] = (FULL || kbase + lane + kWarp * j < K) ? __ldg(trow + kWarp * j) : T(0);
+      acc[j] = T(0);
     }
   }
-  float acc_u = 0.0f;  // the uniform-weight nonzeros' m c / K (the same for every topic)
-  const float inv_k = 1.0f / static_cast<float>(K);
+  T acc_u = T(0);  // the uniform-weight nonzeros' m c / K (the same for every topic)
+  const T inv_k = T(1) / static_cast<T>(K);
   for (int64_t g0 = p0; g0 < p1; g0 += kWarp) {
     const int64_t p = g0 + lane;
     int32_t w = 0, c = 0;
@@ -1430,36 +1433,51 @@ __global__ void __launch_bounds__(256) k_theta_rates(
       if (MUSRC == 2) muv = __ldg(mu_f_in + p);
     }
     const int n_here = static_cast<int>(min(static_cast<int64_t>(kWarp), p1 - g0));
-    for (int i = 0; i < n_here; ++i) {
-      const int32_t wi = __shfl_sync(0xffffffffu, w, i);
-      const float cs = m_t * static_cast<float>(__shfl_sync(0xffffffffu, c, i));
-      const float* prow = phi32 + static_cast<int64_t>(wi) * K + kbase + lane;
-      float ph[KPL];
+    // NU nonzeros per step: their row loads and mu butterflies interleave (the
+    // loop is latency-bound); a slot past the group re-reads slot 0's row with
+    // a zero count
+    for (int i = 0; i < n_here; i += NU) {
+      T ph[NU][KPL], mu[NU], cs[NU];
 #pragma unroll
-      for (int j = 0; j < KPL; ++j) ph[j] = (FULL || kbase + lane + kWarp * j < K) ? __ldg(prow + kWarp * j) : 0.0f;
-      float mu;
-      if (MUSRC == 2) {
-        mu = __shfl_sync(0xffffffffu, muv, i);
-      } else {
-        mu = 0.0f;
+      for (int u = 0; u < NU; ++u) {
+        const bool ok = i + u < n_here;
+        const int src = ok ? i + u : i;
+        const int32_t wi = __shfl_sync(0xffffffffu, w, src);
+        const int32_t ci = __shfl_sync(0xffffffffu, c, src);
+        cs[u] = ok ? m_t * static_cast<T>(ci) : T(0);
+        if (MUSRC == 2) mu[u] = __shfl_sync(0xffffffffu, muv, src);
+        const T* prow = phi32 + static_cast<int64_t>(wi) * K + kbase + lane;
 #pragma unroll
-        for (int j = 0; j < KPL; ++j) mu = __fmaf_rn(th[j], ph[j], mu);
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) mu += __shfl_xor_sync(0xffffffffu, mu, o);
+        for (int j = 0; j < KPL; ++j) ph[u][j] = (FULL || kbase + lane + kWarp * j < K) ? __ldg(prow + kWarp * j) : T(0);
       }
-      if (mu >= 1e-30f) {  // warp-uniform
-        const float s = __fdividef(cs, mu);
+      if (MUSRC != 2) {
 #pragma unroll
-        for (int j = 0; j < KPL; ++j) acc[j] = __fmaf_rn(ph[j], s, acc[j]);
-      } else {
-        acc_u += cs * inv_k;
+        for (int u = 0; u < NU; ++u) {
+          mu[u] = T(0);
+#pragma unroll
+          for (int j = 0; j < KPL; ++j) mu[u] = fma(th[j], ph[u][j], mu[u]);
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1)
+#pragma unroll
+          for (int u = 0; u < NU; ++u) mu[u] += __shfl_xor_sync(0xffffffffu, mu[u], o);
+      }
+#pragma unroll
+      for (int u = 0; u < NU; ++u) {
+        const bool use = mu[u] >= T(1e-30);  // else uniform weights (sampler.cpp:164)
+        const T sv = sizeof(T) == 4 ? static_cast<T>(__fdividef(static_cast<float>(cs[u]), static_cast<float>(mu[u])))
+                                    : cs[u] / mu[u];
+        const T s = use ? sv : T(0);
+        acc_u += use ? T(0) : cs[u] * inv_k;
+#pragma unroll
+        for (int j = 0; j < KPL; ++j) acc[j] = fma(ph[u][j], s, acc[j]);
       }
     }
   }
-  float* const out = rates + b * K + kbase + lane;
+  T* const out = rates + b * K + kbase + lane;
 #pragma unroll
   for (int j = 0; j < KPL; ++j)
-    if (FULL || kbase + lane + kWarp * j < K) out[kWarp * j] = __fmaf_rn(th[j], acc[j], acc_u);
+    if (FULL || kbase + lane + kWarp * j < K) out[kWarp * j] = fma(th[j], acc[j], acc_u);
 }
 
 __global__ void __launch_bounds__(256) k_theta_draws(BatchView bv, const float* __restrict__ rates, int K,
@@ -1966,6 +1984,16 @@ int launch_sample_multinomial(const BatchView& bv, const float* theta_b32, const
   return 1;
 }
 
+int launch_expected_theta(const BatchView& bv, const double* theta_b, const double* phi_wk, int K,
+                          double m_t, double* tf, cudaStream_t st) {
+  if (K > kWarp * 8) return -1;
+  if (bv.B == 0) return 0;
+  const dim3 grid(static_cast<unsigned>((bv.B + 7) / 8), 1u);
+  if (K == kWarp * 8) k_theta_rates<double, 8, true, 0><<<grid, 256, 0, st>>>(bv, theta_b, phi_wk, nullptr, K, m_t, tf);
+  else k_theta_rates<double, 8, false, 0><<<grid, 256, 0, st>>>(bv, theta_b, phi_wk, nullptr, K, m_t, tf);
+  return 1;
+}
+
 int launch_sample_throughput(const BatchView& bv, const float* theta_b32, const float* phi32, int K,
                              double m_t, uint64_t seed, uint32_t t, uint32_t sweep,
                              unsigned long long* tc, unsigned long long* pc, float* mu_f,
@@ -1990,12 +2018,12 @@ int launch_sample_throughput(const BatchView& bv, const float* theta_b32, const 
   const dim3 grid(static_cast<unsigned>((bv.B + 7) / 8), static_cast<unsigned>((K + kWarp * KPL - 1) / (kWarp * KPL)));
   const bool full = K % (kWarp * KPL) == 0;
   if (mu != nullptr) {
-    if (full) k_theta_rates<KPL, true, 2><<<grid, 256, 0, st>>>(bv, theta_b32, phi32, mu, K, mf, rate_scratch);
-    else k_theta_rates<KPL, false, 2><<<grid, 256, 0, st>>>(bv, theta_b32, phi32, mu, K, mf, rate_scratch);
+    if (full) k_theta_rates<float, KPL, true, 2><<<grid, 256, 0, st>>>(bv, theta_b32, phi32, mu, K, mf, rate_scratch);
+    else k_theta_rates<float, KPL, false, 2><<<grid, 256, 0, st>>>(bv, theta_b32, phi32, mu, K, mf, rate_scratch);
   } else if (full) {
-    k_theta_rates<KPL, true, 0><<<grid, 256, 0, st>>>(bv, theta_b32, phi32, nullptr, K, mf, rate_scratch);
+    k_theta_rates<float, KPL, true, 0><<<grid, 256, 0, st>>>(bv, theta_b32, phi32, nullptr, K, mf, rate_scratch);
   } else {
-    k_theta_rates<KPL, false, 0><<<grid, 256, 0, st>>>(bv, theta_b32, phi32, nullptr, K, mf, rate_scratch);
+    k_theta_rates<float, KPL, false, 0><<<grid, 256, 0, st>>>(bv, theta_b32, phi32, nullptr, K, mf, rate_scratch);
   }
   k_theta_draws<<<grid_for(bv.B * K, 256), 256, 0, st>>>(bv, rate_scratch, K, seed, t, sweep, tc);
   launched += 2;
