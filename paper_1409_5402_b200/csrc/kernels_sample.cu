@@ -1401,13 +1401,17 @@ __global__ void __launch_bounds__(BLK, MINB) k_sample_thru(
 // Deterministic (no atomics); K draws per document instead of K per nonzero.
 // T = double: the expected-count mode's non-final inner sweep (the expected
 // theta counts ARE these rates; f64 rows, f64 mu, K <= 256).
+#ifndef SAMELDA_RATES_BLK
+#define SAMELDA_RATES_BLK 64  // 128: equal; 256: 5-12% slower (doc-length tail per block)
+#endif
+constexpr int kRatesBlk = SAMELDA_RATES_BLK;  // documents per block = kRatesBlk / 32
 template <typename T, int KPL, bool FULL, int MUSRC, int NU = (sizeof(T) == 4 ? 2 : 1)>
-__global__ void __launch_bounds__(256, sizeof(T) == 4 ? 4 : 3) k_theta_rates(
+__global__ void __launch_bounds__(kRatesBlk, (sizeof(T) == 4 ? 4 : 3) * 256 / kRatesBlk) k_theta_rates(
     BatchView bv, const T* __restrict__ theta_b32, const T* __restrict__ phi32,
     const float* __restrict__ mu_f_in, int K, T m_t, T* __restrict__ rates) {
   static_assert(MUSRC == 0 || sizeof(T) == 4, "a supplied mu is f32");
   const int lane = threadIdx.x & 31;
-  const int64_t b = static_cast<int64_t>(blockIdx.x) * (256 / kWarp) + (threadIdx.x >> 5);
+  const int64_t b = static_cast<int64_t>(blockIdx.x) * (kRatesBlk / kWarp) + (threadIdx.x >> 5);
   if (b >= bv.B) return;
   const int kbase = static_cast<int>(blockIdx.y) * kWarp * KPL;
   const int64_t p0 = __ldg(bv.batch_prefix + b), p1 = __ldg(bv.batch_prefix + b + 1);
@@ -1988,9 +1992,9 @@ int launch_expected_theta(const BatchView& bv, const double* theta_b, const doub
                           double m_t, double* tf, cudaStream_t st) {
   if (K > kWarp * 8) return -1;
   if (bv.B == 0) return 0;
-  const dim3 grid(static_cast<unsigned>((bv.B + 7) / 8), 1u);
-  if (K == kWarp * 8) k_theta_rates<double, 8, true, 0><<<grid, 256, 0, st>>>(bv, theta_b, phi_wk, nullptr, K, m_t, tf);
-  else k_theta_rates<double, 8, false, 0><<<grid, 256, 0, st>>>(bv, theta_b, phi_wk, nullptr, K, m_t, tf);
+  const dim3 grid(static_cast<unsigned>((bv.B + kRatesBlk / kWarp - 1) / (kRatesBlk / kWarp)), 1u);
+  if (K == kWarp * 8) k_theta_rates<double, 8, true, 0><<<grid, kRatesBlk, 0, st>>>(bv, theta_b, phi_wk, nullptr, K, m_t, tf);
+  else k_theta_rates<double, 8, false, 0><<<grid, kRatesBlk, 0, st>>>(bv, theta_b, phi_wk, nullptr, K, m_t, tf);
   return 1;
 }
 
@@ -2015,15 +2019,16 @@ int launch_sample_throughput(const BatchView& bv, const float* theta_b32, const 
   }
   // a non-final inner sweep: theta counts only, one draw per (document, topic)
   constexpr int KPL = 8;
-  const dim3 grid(static_cast<unsigned>((bv.B + 7) / 8), static_cast<unsigned>((K + kWarp * KPL - 1) / (kWarp * KPL)));
+  const dim3 grid(static_cast<unsigned>((bv.B + kRatesBlk / kWarp - 1) / (kRatesBlk / kWarp)),
+                  static_cast<unsigned>((K + kWarp * KPL - 1) / (kWarp * KPL)));
   const bool full = K % (kWarp * KPL) == 0;
   if (mu != nullptr) {
-    if (full) k_theta_rates<float, KPL, true, 2><<<grid, 256, 0, st>>>(bv, theta_b32, phi32, mu, K, mf, rate_scratch);
-    else k_theta_rates<float, KPL, false, 2><<<grid, 256, 0, st>>>(bv, theta_b32, phi32, mu, K, mf, rate_scratch);
+    if (full) k_theta_rates<float, KPL, true, 2><<<grid, kRatesBlk, 0, st>>>(bv, theta_b32, phi32, mu, K, mf, rate_scratch);
+    else k_theta_rates<float, KPL, false, 2><<<grid, kRatesBlk, 0, st>>>(bv, theta_b32, phi32, mu, K, mf, rate_scratch);
   } else if (full) {
-    k_theta_rates<float, KPL, true, 0><<<grid, 256, 0, st>>>(bv, theta_b32, phi32, nullptr, K, mf, rate_scratch);
+    k_theta_rates<float, KPL, true, 0><<<grid, kRatesBlk, 0, st>>>(bv, theta_b32, phi32, nullptr, K, mf, rate_scratch);
   } else {
-    k_theta_rates<float, KPL, false, 0><<<grid, 256, 0, st>>>(bv, theta_b32, phi32, nullptr, K, mf, rate_scratch);
+    k_theta_rates<float, KPL, false, 0><<<grid, kRatesBlk, 0, st>>>(bv, theta_b32, phi32, nullptr, K, mf, rate_scratch);
   }
   k_theta_draws<<<grid_for(bv.B * K, 256), 256, 0, st>>>(bv, rate_scratch, K, seed, t, sweep, tc);
   launched += 2;
