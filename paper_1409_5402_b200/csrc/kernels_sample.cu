@@ -1405,8 +1405,14 @@ __global__ void __launch_bounds__(BLK, MINB) k_sample_thru(
 #define SAMELDA_RATES_BLK 64  // 128: equal; 256: 5-12% slower (doc-length tail per block)
 #endif
 constexpr int kRatesBlk = SAMELDA_RATES_BLK;  // documents per block = kRatesBlk / 32
-template <typename T, int KPL, bool FULL, int MUSRC, int NU = (sizeof(T) == 4 ? 2 : 1)>
-__global__ void __launch_bounds__(kRatesBlk, (sizeof(T) == 4 ? 4 : 3) * 256 / kRatesBlk) k_theta_rates(
+#ifndef SAMELDA_RATES_NU
+#define SAMELDA_RATES_NU 2
+#endif
+#ifndef SAMELDA_RATES_MINB
+#define SAMELDA_RATES_MINB 4
+#endif
+template <typename T, int KPL, bool FULL, int MUSRC, int NU = (sizeof(T) == 4 ? SAMELDA_RATES_NU : 1)>
+__global__ void __launch_bounds__(kRatesBlk, (sizeof(T) == 4 ? SAMELDA_RATES_MINB : 3) * 256 / kRatesBlk) k_theta_rates(
     BatchView bv, const T* __restrict__ theta_b32, const T* __restrict__ phi32,
     const float* __restrict__ mu_f_in, int K, T m_t, T* __restrict__ rates) {
   static_assert(MUSRC == 0 || sizeof(T) == 4, "a supplied mu is f32");
