@@ -1406,10 +1406,10 @@ __global__ void __launch_bounds__(BLK, MINB) k_sample_thru(
 #endif
 constexpr int kRatesBlk = SAMELDA_RATES_BLK;  // documents per block = kRatesBlk / 32
 #ifndef SAMELDA_RATES_NU
-#define SAMELDA_RATES_NU 2
+#define SAMELDA_RATES_NU 4  // nonzeros per step (f32): 4 -> 0.56 ms, 3 -> 0.58, 2 -> 0.60 (NYTimes shape)
 #endif
 #ifndef SAMELDA_RATES_MINB
-#define SAMELDA_RATES_MINB 4
+#define SAMELDA_RATES_MINB 3  // x 256 threads per SM (85 registers at NU = 4)
 #endif
 template <typename T, int KPL, bool FULL, int MUSRC, int NU = (sizeof(T) == 4 ? SAMELDA_RATES_NU : 1)>
 __global__ void __launch_bounds__(kRatesBlk, (sizeof(T) == 4 ? SAMELDA_RATES_MINB : 3) * 256 / kRatesBlk) k_theta_rates(
