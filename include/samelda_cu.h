@@ -240,6 +240,17 @@ int samelda_cu_period_update(samelda_cu_ctx* ctx, double rho_t);
  * elem_bytes is 8 (u64 parity counts or f64 expected counts); is_float 1 for f64. */
 int samelda_cu_phi_counts_device(samelda_cu_ctx* ctx, void** ptr, int64_t* n_elems,
                                  int32_t* elem_bytes, int32_t* is_float);
+/* The count exchange in 32-bit words (half the bytes of the u64
+ * all-reduce), integer-count modes: pack32 writes lo[i] = count[i] as int32
+ * into the caller's device buffer and the number of cells >= (2^31 - 1) /
+ * world_size into the caller's device u64 *n_over (zeroed first), on the
+ * context's stream.  When the all-reduced n_over is 0, the int32 all-reduce
+ * of lo is exact (its sums stay below 2^31) and unpack32 writes the summed
+ * counts back into the W x K buffer; otherwise the caller all-reduces the
+ * untouched u64 buffer instead. */
+int samelda_cu_phi_counts_pack32(samelda_cu_ctx* ctx, void* lo, int64_t n_elems, int32_t world_size,
+                                 void* n_over);
+int samelda_cu_phi_counts_unpack32(samelda_cu_ctx* ctx, const void* lo, int64_t n_elems);
 /* Doc-sharded runs: this context holds documents [doc_base, doc_base + D)
  * of the global corpus under local ids 0..D-1; Philox stream keys use the
  * global id, so every shard draws exactly what a single GPU would. */

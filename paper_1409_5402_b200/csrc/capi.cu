@@ -1703,6 +1703,30 @@ int samelda_cu_phi_counts_device(samelda_cu_ctx* ctx, void** ptr, int64_t* n_ele
   });
 }
 
+int samelda_cu_phi_counts_pack32(samelda_cu_ctx* ctx, void* lo, int64_t n_elems, int32_t world_size,
+                                 void* n_over) {
+  return guarded(ctx, [&] {
+    if (!ctx->counts_ready) fail(SAMELDA_CU_CONFIG, "no sampled counts yet");
+    if (ctx->counts_float) fail(SAMELDA_CU_CONFIG, "pack32: the expected-count mode exchanges f64 counts");
+    if (n_elems != ctx->W * ctx->K) fail(SAMELDA_CU_CONFIG, "pack32: n_elems must be W x K");
+    if (world_size < 1) fail(SAMELDA_CU_CONFIG, "pack32: world_size must be >= 1");
+    // world_size x (bound - 1) < 2^31: the int32 sum of packed cells never wraps
+    const unsigned long long bound = (0x7fffffffull / static_cast<unsigned long long>(world_size));
+    ctx->launches += scu::launch_pack_counts(ctx->pc.as<unsigned long long>(), n_elems, bound,
+                                             static_cast<int32_t*>(lo), static_cast<unsigned long long*>(n_over),
+                                             ctx->stream);
+  });
+}
+
+int samelda_cu_phi_counts_unpack32(samelda_cu_ctx* ctx, const void* lo, int64_t n_elems) {
+  return guarded(ctx, [&] {
+    if (!ctx->counts_ready || ctx->counts_float) fail(SAMELDA_CU_CONFIG, "unpack32: no integer counts");
+    if (n_elems != ctx->W * ctx->K) fail(SAMELDA_CU_CONFIG, "unpack32: n_elems must be W x K");
+    ctx->launches += scu::launch_unpack_counts(static_cast<const int32_t*>(lo), n_elems,
+                                               ctx->pc.as<unsigned long long>(), ctx->stream);
+  });
+}
+
 int samelda_cu_batch_theta(samelda_cu_ctx* ctx, double* out, int64_t cap) {
   return guarded(ctx, [&] {
     ctx->poll_err(true, "period");

@@ -141,6 +141,11 @@ int launch_col_sums(const double* x, int64_t W, int K, double* totals, void* col
                     int* err, cudaStream_t st);
 
 // f32 shadow copy (the sampler's fast path reads f32 theta / phi)
+// the count exchange in 32-bit words: lo[i] = c[i] (exact below bound),
+// *n_over = number of cells >= bound (zeroed first)
+int launch_pack_counts(const unsigned long long* c, int64_t n, unsigned long long bound, int32_t* lo,
+                       unsigned long long* n_over, cudaStream_t st);
+int launch_unpack_counts(const int32_t* lo, int64_t n, unsigned long long* c, cudaStream_t st);
 int launch_to_f32(const double* x, int64_t n, float* y, cudaStream_t st);
 
 // phi init with seeded perturbation (model.cpp:41-52, sampler.cpp:285-298)

@@ -20,6 +20,8 @@ from __future__ import annotations
 
 from dataclasses import dataclass
 
+import os
+
 import numpy as np
 
 
@@ -58,6 +60,7 @@ class CudaEngine:
         self.trainer = trainer
         self.device = device
         self._counts = None
+        self._lo = self._over = None
         # the count all-reduce is enqueued on torch's current stream: run the
         # trainer on that stream so the collective is ordered after sampling
         trainer.ctx.set_stream(torch.cuda.current_stream(device).cuda_stream)
@@ -75,6 +78,32 @@ class CudaEngine:
             self._counts = torch.as_tensor(_CAI(ptr, n, "<f8" if is_f else "<i8"),
                                            device=f"cuda:{self.device}")
         return self._counts
+
+    def exchange(self, group=None):
+        """The per-period all-reduce of the W x K counts.  Integer counts go
+        as int32 words (half the bytes): packed on the device, the number of
+        cells too large for an exact int32 sum over the ranks all-reduced
+        first (8 bytes), then either the packed words (unpacked in place) or,
+        if any rank had such a cell, the untouched u64 counts.  Expected-mode
+        f64 counts are all-reduced as they are."""
+        import torch
+        import torch.distributed as dist
+        counts = self.counts()
+        if counts.dtype != torch.int64 or os.environ.get("SAMELDA_EXCHANGE") == "u64":
+            dist.all_reduce(counts, group=group)
+            return
+        n = counts.numel()
+        if self._lo is None or self._lo.numel() != n:
+            self._lo = torch.empty(n, dtype=torch.int32, device=counts.device)
+            self._over = torch.zeros(1, dtype=torch.int64, device=counts.device)
+        self.trainer.phi_counts_pack32(self._lo.data_ptr(), n, dist.get_world_size(group),
+                                       self._over.data_ptr())
+        dist.all_reduce(self._over, group=group)
+        if int(self._over.item()) == 0:  # the one host wait of the exchange
+            dist.all_reduce(self._lo, group=group)
+            self.trainer.phi_counts_unpack32(self._lo.data_ptr(), n)
+        else:
+            dist.all_reduce(counts, group=group)
 
     def update(self, rho_t):
         self.trainer.period_update(rho_t)
@@ -122,7 +151,11 @@ class ShardedTrainer:
         rho = self.S.rho_schedule(t, self.tau0, self.gamma)
         self.engine.sample(own, t, m_t)
         if dist.is_available() and dist.is_initialized() and dist.get_world_size(self.group) > 1:
-            dist.all_reduce(self.engine.counts(), group=self.group)
+            exchange = getattr(self.engine, "exchange", None)
+            if exchange is not None:
+                exchange(self.group)
+            else:
+                dist.all_reduce(self.engine.counts(), group=self.group)
         self.engine.update(rho)
         self.t += 1
         return PeriodStats(t, m_t, rho, len(batch), len(own), float(self.doc_tokens[own].sum()))

@@ -119,6 +119,8 @@ SIGNATURES = [
     ("samelda_cu_period", C.c_int, [_P, _P, _I64, _I64, _D, _D]),
     ("samelda_cu_period_sample", C.c_int, [_P, _P, _I64, _I64, _D]),
     ("samelda_cu_period_update", C.c_int, [_P, _D]),
+    ("samelda_cu_phi_counts_pack32", C.c_int, [_P, C.c_void_p, _I64, _I32, C.c_void_p]),
+    ("samelda_cu_phi_counts_unpack32", C.c_int, [_P, C.c_void_p, _I64]),
     ("samelda_cu_phi_counts_device", C.c_int, [_P, C.POINTER(C.c_void_p), C.POINTER(_I64),
                                                C.POINTER(_I32), C.POINTER(_I32)]),
     ("samelda_cu_batch_theta", C.c_int, [_P, _P, _I64]),
@@ -644,6 +646,19 @@ class Trainer:
         c.check(c.lib.samelda_cu_phi_counts_device(
             c.h, C.byref(p), C.byref(n), C.byref(eb), C.byref(fl)))
         return p.value, n.value, eb.value, bool(fl.value)
+
+    def phi_counts_pack32(self, lo_ptr: int, n: int, world_size: int, n_over_ptr: int):
+        """Pack the u64 phi counts into the int32 device buffer at lo_ptr (exact
+        below (2^31 - 1) / world_size; the count of cells at or above it goes to
+        the u64 device word at n_over_ptr), on the context's stream."""
+        c = self._live()
+        c.check(c.lib.samelda_cu_phi_counts_pack32(c.h, C.c_void_p(lo_ptr), int(n), int(world_size),
+                                                   C.c_void_p(n_over_ptr)))
+
+    def phi_counts_unpack32(self, lo_ptr: int, n: int):
+        """Write the (all-reduced) int32 counts at lo_ptr back into the u64 phi counts."""
+        c = self._live()
+        c.check(c.lib.samelda_cu_phi_counts_unpack32(c.h, C.c_void_p(lo_ptr), int(n)))
 
     def set_doc_base(self, base: int):
         c = self._live()

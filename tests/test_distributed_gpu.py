@@ -27,7 +27,7 @@ def _corpus():
     return port.make_corpus(120, 60, 4, 30.0, 3)
 
 
-def _worker(rank, world, port_no, out_path, mode=0, backend="gloo"):
+def _worker(rank, world, port_no, out_path, mode=0, backend="gloo", engine_kind="host"):
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port_no))
     dev = rank if backend == "nccl" else 0
     torch.cuda.set_device(dev)
@@ -52,7 +52,10 @@ def _worker(rank, world, port_no, out_path, mode=0, backend="gloo"):
     tr = S.Trainer(local, cfg, ctx=ctx)
 
     class GlooEngine(D.CudaEngine):
-        """gloo reduces host tensors: stage the device counts through the host."""
+        """gloo reduces host tensors: stage the device counts through the host
+        (the plain u64 all-reduce, no int32 packing)."""
+
+        exchange = None
 
         def counts(self):
             self._host = super().counts().cpu()
@@ -62,7 +65,9 @@ def _worker(rank, world, port_no, out_path, mode=0, backend="gloo"):
             super().counts().copy_(self._host)
             super().update(rho)
 
-    engine = GlooEngine(tr, 0) if backend == "gloo" else D.CudaEngine(tr, dev)
+    # engine_kind "device": the production engine (int32 count exchange of
+    # device tensors), here over gloo's CUDA all-reduce
+    engine = GlooEngine(tr, 0) if backend == "gloo" and engine_kind == "host" else D.CudaEngine(tr, dev)
     # ShardedTrainer sets the engine's doc base (global Philox doc ids)
     st = D.ShardedTrainer(engine, g.n_docs, lo, hi, local.doc_tokens(), BF, SEED, M,
                           "invlinear", T_MAX)
@@ -97,6 +102,54 @@ def test_two_rank_sharded_training_equals_single_gpu(tmp_path, mode):
     model, _ = S.train(g, S.SamplerConfig(n_topics=K, m=M, schedule="invlinear", t_max=T_MAX,
                                           batch_fraction=BF, seed=SEED, mode=mode))
     np.testing.assert_array_equal(got["phi"], model.phi)
+
+
+@pytest.mark.timeout(600)
+def test_two_rank_int32_exchange_equals_single_gpu(tmp_path):
+    """The production engine's count exchange in int32 words (pack32 on the
+    device, the 8-byte over-bound count all-reduced first, the packed words
+    all-reduced and unpacked in place) leaves phi bit-equal to one GPU."""
+    from paper_1409_5402_b200 import samelda as S
+    out = str(tmp_path / "rank0.npz")
+    mp.start_processes(_worker, args=(2, _free_port(), out, 0, "gloo", "device"), nprocs=2,
+                       start_method="spawn")
+    got = np.load(out)
+    model, _ = S.train(_corpus(), S.SamplerConfig(n_topics=K, m=M, schedule="invlinear",
+                                                  t_max=T_MAX, batch_fraction=BF, seed=SEED))
+    np.testing.assert_array_equal(got["phi"], model.phi)
+
+
+def test_pack32_unpack32_roundtrip_and_bound():
+    """pack32 copies every count below (2^31 - 1) / world_size exactly and counts
+    the cells at or above it; unpack32 writes int32 words back as u64 counts."""
+    from paper_1409_5402_b200 import distributed as D
+    from paper_1409_5402_b200 import samelda as S
+    g = _corpus()
+    ctx = S.Context(0)
+    stream = torch.cuda.Stream(device=0)
+    torch.cuda.set_stream(stream)
+    ctx.set_stream(stream.cuda_stream)
+    tr = S.Trainer(g, S.SamplerConfig(n_topics=K, m=M, t_max=2, batch_fraction=1.0, seed=SEED), ctx=ctx)
+    eng = D.CudaEngine(tr, 0)
+    tr.period_sample(np.arange(g.n_docs, dtype=np.int32), 1, M)
+    c = eng.counts()
+    ref = c.clone()
+    n = c.numel()
+    lo = torch.empty(n, dtype=torch.int32, device="cuda:0")
+    over = torch.zeros(1, dtype=torch.int64, device="cuda:0")
+    tr.phi_counts_pack32(lo.data_ptr(), n, 8, over.data_ptr())
+    torch.cuda.synchronize()
+    assert int(over.item()) == 0 and int(ref.sum()) > 0
+    assert torch.equal(lo.to(torch.int64), ref)
+    # a bound of (2^31 - 1) // 2^30 = 1: every nonzero cell is over it
+    tr.phi_counts_pack32(lo.data_ptr(), n, 2**30, over.data_ptr())
+    torch.cuda.synchronize()
+    assert int(over.item()) == int((ref >= 1).sum())
+    lo2 = (lo * 3).contiguous()
+    torch.cuda.synchronize()
+    tr.phi_counts_unpack32(lo2.data_ptr(), n)
+    torch.cuda.synchronize()
+    assert torch.equal(eng.counts(), ref * 3)
 
 
 def test_bench_two_rank_path_runs(tmp_path):
