@@ -23,6 +23,7 @@
 // communicator; its exchange sums the count buffers with a device kernel
 // instead -- the same integer sum.
 #include <cuda_runtime.h>
+#include <cstdlib>
 #include <dlfcn.h>
 #include <nccl.h>
 
@@ -106,6 +107,10 @@ struct samelda_cu_group {
   std::vector<cudaEvent_t> sampled;  // per member: its sampling is enqueued
   cudaEvent_t reduced = nullptr;     // same-device exchange finished (member 0's stream)
   std::vector<ncclComm_t> comms;     // empty when devices repeat
+  // the int32 count exchange: per member a packed W x K buffer and its
+  // over-bound cell count (device), and the counts read back (pinned)
+  std::vector<void*> lo32, over_dev;
+  unsigned long long* over_host = nullptr;
   bool local_exchange = false;
   std::string error;
   int64_t launches_nccl = 0;
@@ -138,8 +143,63 @@ struct samelda_cu_group {
       cudaSetDevice(devices[0]);
       cudaEventDestroy(reduced);
     }
+    for (size_t i = 0; i < lo32.size(); ++i) {
+      cudaSetDevice(devices[i]);
+      if (lo32[i]) cudaFree(lo32[i]);
+      if (over_dev[i]) cudaFree(over_dev[i]);
+    }
+    if (over_host) cudaFreeHost(over_host);
     if (!comms.empty() && nccl().ok)
       for (auto c : comms) nccl().destroy(c);
+  }
+
+  // integer counts over NCCL in int32 words (half the bytes): every member
+  // packs its cells below (2^31 - 1) / n and counts the others; when no
+  // member has such a cell the int32 sum is exact and is unpacked in place.
+  // Returns false (nothing exchanged) when the u64 all-reduce is needed.
+  bool exchange32(int64_t elems) {
+    const size_t n = ctx.size();
+    if (lo32.size() != n) {
+      lo32.assign(n, nullptr);
+      over_dev.assign(n, nullptr);
+      gck(cudaMallocHost(reinterpret_cast<void**>(&over_host), sizeof(unsigned long long) * n), "pinned");
+    }
+    for (size_t i = 0; i < n; ++i) {
+      gck(cudaSetDevice(devices[i]), "cudaSetDevice");
+      if (!lo32[i]) {
+        gck(cudaMalloc(&lo32[i], sizeof(int32_t) * static_cast<size_t>(elems)), "cudaMalloc");
+        gck(cudaMalloc(&over_dev[i], sizeof(unsigned long long)), "cudaMalloc");
+      }
+      check(static_cast<int>(i),
+            samelda_cu_phi_counts_pack32(ctx[i], lo32[i], elems, static_cast<int32_t>(n), over_dev[i]), "pack32");
+      gck(cudaMemcpyAsync(over_host + i, over_dev[i], sizeof(unsigned long long), cudaMemcpyDeviceToHost,
+                          streams[i]), "over count");
+    }
+    unsigned long long over = 0;
+    for (size_t i = 0; i < n; ++i) {
+      gck(cudaStreamSynchronize(streams[i]), "over count");  // the exchange's one host wait
+      over += over_host[i];
+    }
+    if (over) return false;
+    const Nccl& N = nccl();
+    N.group_start();
+    for (size_t i = 0; i < n; ++i) {
+      gck(cudaSetDevice(devices[i]), "cudaSetDevice");
+      const ncclResult_t r = N.all_reduce(lo32[i], lo32[i], static_cast<size_t>(elems), ncclInt32, ncclSum,
+                                          comms[i], streams[i]);
+      if (r != ncclSuccess) {
+        N.group_end();
+        gfail(SAMELDA_CU_CUDA, std::string("ncclAllReduce: ") + N.error_string(r));
+      }
+    }
+    const ncclResult_t r = N.group_end();
+    if (r != ncclSuccess) gfail(SAMELDA_CU_CUDA, std::string("ncclGroupEnd: ") + N.error_string(r));
+    ++launches_nccl;
+    for (size_t i = 0; i < n; ++i) {
+      gck(cudaSetDevice(devices[i]), "cudaSetDevice");
+      check(static_cast<int>(i), samelda_cu_phi_counts_unpack32(ctx[i], lo32[i], elems), "unpack32");
+    }
+    return true;
   }
 
   // the W x K phi-count exchange of one period (after every member's sample)
@@ -153,6 +213,8 @@ struct samelda_cu_group {
       check(static_cast<int>(i), samelda_cu_phi_counts_device(ctx[i], &buf[i], &elems, &eb, &is_f),
             "phi counts");
     if (!local_exchange) {
+      const char* ex = std::getenv("SAMELDA_EXCHANGE");  // "u64": keep the u64 all-reduce
+      if (!is_f && !(ex && std::strcmp(ex, "u64") == 0) && exchange32(elems)) return;
       const Nccl& N = nccl();
       N.group_start();
       for (size_t i = 0; i < n; ++i) {
